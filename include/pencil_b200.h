@@ -1,0 +1,241 @@
+/*
+ * pencil_b200.h — C ABI of the B200-native Pencil HE linear-layer engine.
+ *
+ * Drop-in boundary for the hot path named in BASELINE.json.north_star:
+ * encrypt -> ciphertext x plaintext multiply-accumulate in the NTT domain ->
+ * masking -> decrypt-to-additive-share, plus share arithmetic mod 2^ell.
+ *
+ * Conventions
+ *  - Every pointer argument is a DEVICE pointer (cudaMalloc'd or a torch CUDA
+ *    tensor's data_ptr()) unless the name says `host`.  `stream` is a
+ *    cudaStream_t (NULL = legacy default stream).  Calls are asynchronous on
+ *    `stream`; no call synchronises except pb_ctx_create/destroy.
+ *  - RNS residues are uint32 (moduli q_i < 2^30), polynomials are rows of N
+ *    residues, a polynomial over all limbs is [L][N], a ciphertext [2][L][N]
+ *    (c0 then c1), always in NTT form unless a function says "coefficient".
+ *  - Z_{2^ell} elements (shares, plaintext coefficients) are uint64 holding a
+ *    canonical value < 2^ell.
+ *  - Every function returns an int status (PB_OK = 0); nothing throws across
+ *    the ABI.  pb_last_error() returns a thread-local message.  Status codes
+ *    map 1:1 to the reference exception taxonomy
+ *    (/root/reference/pkg/src/pencil/errors.py:4-41).
+ *
+ * Each entry point cites the reference interface it replaces.  "K" is
+ * /root/reference/pkg/src/pencil/_kernels.py, "R" is .../pencil/ring.py,
+ * "SPEC" is /root/reference/SPEC.md (the SPEC-only modules the reference
+ * specifies but does not ship).
+ */
+#ifndef PENCIL_B200_H_
+#define PENCIL_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PB_ABI_VERSION 1
+#define PB_MAX_LIMBS 8
+
+/* status codes -> errors.py classes (E:4-41) */
+enum {
+  PB_OK = 0,
+  PB_ERR_PARAMS = 1,   /* ParamsError    E:8   */
+  PB_ERR_RANGE = 2,    /* EncodeRangeError E:12 */
+  PB_ERR_SCALE = 3,    /* ScaleError     E:16  */
+  PB_ERR_SHAPE = 4,    /* ShapeError     E:20  */
+  PB_ERR_FORM = 5,     /* FormError      E:24  */
+  PB_ERR_GEOMETRY = 6, /* GeometryError  E:28  */
+  PB_ERR_CUDA = 7,     /* PencilError (device failure) */
+  PB_ERR_ARG = 8       /* PencilError (bad argument)   */
+};
+
+/* Parameter descriptor (SPEC:103-106 BfvParams).  All big-integer constants
+ * are precomputed by the host (Python ints) and passed as words. */
+typedef struct pb_params {
+  int32_t N;   /* power of two, 16..32768 */
+  int32_t L;   /* number of RNS limbs, 1..PB_MAX_LIMBS */
+  int32_t ell; /* plaintext modulus t = 2^ell, 2..62 */
+  int32_t reserved;
+  uint32_t q[PB_MAX_LIMBS];                 /* primes, q = 1 mod 2N, q < 2^30 */
+  uint32_t psi[PB_MAX_LIMBS];               /* primitive 2N-th roots of unity */
+  uint32_t delta_mod_q[PB_MAX_LIMBS];       /* floor(Q/t) mod q_i            */
+  uint32_t garner_prefix_inv[PB_MAX_LIMBS]; /* (q_0..q_{i-1})^-1 mod q_i  K:158 */
+  uint64_t scale_int[PB_MAX_LIMBS];         /* floor(t*P_{i-1}/Q) mod 2^64 K:182 */
+  double scale_frac[PB_MAX_LIMBS];          /* frac(t*P_{i-1}/Q)          K:182 */
+} pb_params;
+
+typedef struct pb_ctx pb_ctx; /* immutable, shareable across streams */
+
+int pb_abi_version(void);
+const char* pb_last_error(void);
+int pb_device_sm_count(int* out_host);
+
+/* Builds twiddle tables (Shoup form) on the device.  Replaces the host-side
+ * table construction the K callers perform (K:22-29). */
+int pb_ctx_create(const pb_params* params_host, pb_ctx** out_host);
+int pb_ctx_destroy(pb_ctx* ctx);
+
+/* ------------------------------------------------ polynomial engine (K) --- */
+/* Row r of `rows` uses limb row_limb[r] (or r % L when row_limb == NULL). */
+
+/* K:31-50 ntt_forward: in place, natural -> bit-reversed order. */
+int pb_ntt_forward(const pb_ctx* ctx, uint32_t* rows, int64_t n_rows, const int32_t* row_limb,
+                   void* stream);
+/* K:53-77 ntt_inverse: in place, bit-reversed -> natural, includes x N^-1. */
+int pb_ntt_inverse(const pb_ctx* ctx, uint32_t* rows, int64_t n_rows, const int32_t* row_limb,
+                   void* stream);
+
+/* K:80-113 pointwise ops.  op: 0 pw_mul, 1 pw_mul_acc (out += a*b), 2 pw_add,
+ * 3 pw_sub.  Row r of b is b[r % b_rows] (b_rows == n_rows: plain). */
+enum { PB_PW_MUL = 0, PB_PW_MAC = 1, PB_PW_ADD = 2, PB_PW_SUB = 3 };
+int pb_pw(const pb_ctx* ctx, int op, uint32_t* out, const uint32_t* a, const uint32_t* b,
+          int64_t n_rows, int64_t b_rows, const int32_t* row_limb, void* stream);
+
+/* K:158-179 garner_digits over n_polys polynomials [L][N] (coefficient form). */
+int pb_garner_digits(const pb_ctx* ctx, const uint32_t* rows, int64_t n_polys, uint32_t* digits,
+                     void* stream);
+/* K:182-199 scale_round_digits: digits [P][L][N] -> m [P][N] = round(t x/Q) mod t. */
+int pb_scale_round_digits(const pb_ctx* ctx, const uint32_t* digits, int64_t n_polys,
+                          uint64_t* out, void* stream);
+/* Fused K:158-199 (garner + scale-round) for coefficient-form rows. */
+int pb_decode(const pb_ctx* ctx, const uint32_t* rows, int64_t n_polys, uint64_t* out,
+              void* stream);
+
+/* K:135-147 negacyclic_mul_wrap (mod 2^64 schoolbook), batch of n pairs. */
+int pb_negacyclic_mul_wrap(const uint64_t* a, const uint64_t* b, int64_t n_pairs, int32_t N,
+                           uint64_t* out, void* stream);
+
+/* ------------------------------------------------------- BFV (SPEC bfv) --- */
+/* Plaintext sources: `vals` is a flat Z_t tensor; src_map [P][N] gives, per
+ * output coefficient, the index into vals or -1 for a zero coefficient
+ * (the packing maps pi_v / pi_W of SPEC:231-266).  src_map == NULL means
+ * vals is already a dense [P][N] polynomial array. */
+
+/* Centered lift (fact 4) + forward NTT + Shoup companions:
+ * plaintext multiplier for he_plain_mul.  pt/pt_shoup [P][L][N]. */
+int pb_encode_plain(const pb_ctx* ctx, const uint64_t* vals, const int64_t* src_map, int64_t P,
+                    uint32_t* pt, uint32_t* pt_shoup, void* stream);
+
+/* Unsigned lift of Z_t polys, coefficient form: out [P][L][N] = m mod q_i.
+ * centered != 0 selects the centered lift. */
+int pb_lift(const pb_ctx* ctx, const uint64_t* vals, const int64_t* src_map, int64_t P,
+            int centered, uint32_t* out, void* stream);
+
+/* SPEC:139-147 encrypt under the public key pk [2][L][N] (NTT form):
+ * c0 = pk0*NTT(u) + NTT(e1 + Delta m), c1 = pk1*NTT(u) + NTT(e2).
+ * u ternary, e1/e2 centred binomial (eta=20) drawn on the device from
+ * Philox4x32(seed, nonce + poly index). ct [P][2][L][N]. */
+int pb_encrypt_pk(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* vals,
+                  const int64_t* src_map, int64_t P, uint64_t seed, uint64_t nonce, uint32_t* ct,
+                  void* stream);
+/* Same with caller-supplied noise (int8 [P][N] each): bit-exact with the
+ * oracle's encrypt when fed the oracle's draws. */
+int pb_encrypt_pk_noise(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* vals,
+                        const int64_t* src_map, int64_t P, const int8_t* u, const int8_t* e1,
+                        const int8_t* e2, uint32_t* ct, void* stream);
+/* Symmetric-key encryption by the key owner: c1 = a (uniform, NTT domain),
+ * c0 = NTT(e + Delta m) - a*s.  sk_ntt [L][N]. */
+int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint64_t* vals,
+                  const int64_t* src_map, int64_t P, uint64_t seed, uint64_t nonce, uint32_t* ct,
+                  void* stream);
+/* Caller-supplied a ([P][L][N], NTT domain) and e (int8 [P][N]). */
+int pb_encrypt_sk_noise(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint64_t* vals,
+                        const int64_t* src_map, int64_t P, const uint32_t* a, const int8_t* e,
+                        uint32_t* ct, void* stream);
+
+/* x = INTT(c0 + c1*s) in coefficient form, x [P][L][N]. */
+int pb_decrypt_coeffs(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint32_t* ct, int64_t P,
+                      uint32_t* x, void* stream);
+/* SPEC:148-156 decrypt: m [P][N]; scratch [P][L][N] uint32. */
+int pb_decrypt(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint32_t* ct, int64_t P,
+               uint64_t* m, uint32_t* scratch, void* stream);
+/* Alg.1 step 4 / SPEC:240-266 decrypt + pi_y^-1 gather into a share tensor:
+ * for each ct p and slot u < U: if out_pos[p][u] >= 0, share_out[out_dst[p][u]]
+ * = decrypted coefficient out_pos[p][u].  scratch [P][L][U] uint32. */
+int pb_decrypt_to_share(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint32_t* ct, int64_t P,
+                        const int32_t* out_pos, const int64_t* out_dst, int32_t U,
+                        uint64_t* share_out, uint32_t* scratch, void* stream);
+
+/* Alg.1 steps 2-3 / Alg.2 step 2, MO side, fused:
+ *   ct_out[p] = sum_k ct_in[terms[p][k][0]] (*) pt[terms[p][k][1]]  -  Delta*mask_p
+ * where mask_p has mask_vals[out_dst[p][u]] at coefficient out_pos[p][u] and,
+ * when filler != 0, uniform Z_q filler (Philox4x32(filler_seed, p)) at every
+ * other coefficient so the DO learns nothing beyond the useful slots.
+ * terms[p][k] with ct index < 0 is skipped.  ct_in [n][2][L][N],
+ * pt/pt_shoup [n_pt][L][N], ct_out [P][2][L][N]. */
+int pb_ctpt_mac_mask(const pb_ctx* ctx, const uint32_t* ct_in, const uint32_t* pt,
+                     const uint32_t* pt_shoup, const int32_t* terms, int32_t K, int64_t P,
+                     const int32_t* out_pos, const int64_t* out_dst, int32_t U,
+                     const uint64_t* mask_vals, int filler, uint64_t filler_seed, uint32_t* ct_out,
+                     void* stream);
+
+/* ------------------------------------------- ring Z_{2^ell} (R:93-233) --- */
+enum {
+  PB_RING_ADD = 0, /* R:132-134 */
+  PB_RING_SUB = 1, /* R:136-138 */
+  PB_RING_MUL = 2, /* elementwise product (dealer / local terms) */
+  PB_RING_NEG = 3, /* R:140-141 */
+  PB_RING_SCALAR_MUL = 4, /* R:143-145, k = scalar */
+  PB_RING_MASK = 5,       /* R:99-102 canonicalise */
+  PB_RING_ARITH_SHIFT = 6 /* R:206-211, k = bits */
+};
+/* out = a (op) b elementwise mod 2^ell; b broadcast cyclically over b_n. */
+int pb_ring_binary(int op, uint64_t* out, const uint64_t* a, const uint64_t* b, int64_t n,
+                   int64_t b_n, int32_t ell, void* stream);
+int pb_ring_unary(int op, uint64_t* out, const uint64_t* a, uint64_t k, int64_t n, int32_t ell,
+                  void* stream);
+/* R:174-182 encode_fixed; *range_flag (device int32) set to 1 on |x| >= limit. */
+int pb_encode_fixed(const double* x, int64_t n, int32_t ell, int32_t scale, uint64_t* out,
+                    int32_t* range_flag, void* stream);
+/* R:185-191 decode_fixed. */
+int pb_decode_fixed(const uint64_t* v, int64_t n, int32_t ell, int32_t scale, double* out,
+                    void* stream);
+/* R:60-61 SeededRng.uniform_ring: out[i] = raw(seed, stream_id, raw_offset+i) >> (64-ell),
+ * bit-identical to numpy Generator(Philox(key=[seed, stream])).integers(0, 2^ell). */
+int pb_uniform_ring(uint64_t* out, int64_t n, uint64_t seed, uint64_t stream_id,
+                    uint64_t raw_offset, int32_t ell, void* stream);
+/* R:214-219 share_tensor fused: r = uniform_ring(...); mo = r; do = x - r. */
+int pb_share(const uint64_t* x, int64_t n, uint64_t seed, uint64_t stream_id, uint64_t raw_offset,
+             int32_t ell, uint64_t* mo_out, uint64_t* do_out, void* stream);
+/* K:206-218 matmul_wrap (+ mask to ell bits when ell < 64): (n,k)@(k,m).
+ * trans_a / trans_b read a as (k,n) / b as (m,k) row-major. */
+int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m,
+                   int trans_a, int trans_b, int32_t ell, uint64_t* out, void* stream);
+/* Row reduction: out[i] = sum_j a[i][j] mod 2^ell  (reveal_grad_bias). */
+int pb_ring_rowsum(const uint64_t* a, int64_t rows, int64_t cols, int32_t ell, uint64_t* out,
+                   void* stream);
+/* K:221-238 im2col_wrap, K:241-257 col2im_wrap, K:260-278 conv2d_wrap. */
+int pb_im2col(const uint64_t* x, int32_t B, int32_t C, int32_t H, int32_t W, int32_t s,
+              int32_t stride, uint64_t* out, void* stream);
+int pb_col2im(const uint64_t* cols, int32_t B, int32_t C, int32_t H, int32_t W, int32_t s,
+              int32_t stride, uint64_t* out, void* stream);
+int pb_conv2d(const uint64_t* x, const uint64_t* w, int32_t B, int32_t Ci, int32_t H, int32_t W,
+              int32_t Co, int32_t s, int32_t ell, uint64_t* out, void* stream);
+
+/* ------------------------------- dealer-assisted non-linear --- */
+/* The SPEC's dealer OT backend ("fast, insecure, default for benchmarks of
+ * non-OT costs"): reconstruct x = mo + do, apply f, reshare with
+ * r = uniform_ring(seed, stream_id, raw_offset + i).
+ *   PB_DEALER_RELU     y = (x >= 0) ? x : 0, d_out[i] = (x >= 0)
+ *   PB_DEALER_TRUNC    y = arith_shift(x, k)                       (faithful)
+ *   PB_DEALER_SELECT   y = d_in[i] ? x : 0                         (ReLU backward, cached d)
+ *   PB_DEALER_RESHARE  y = x
+ * Outputs overwrite mo/do in place. */
+enum { PB_DEALER_RELU = 0, PB_DEALER_TRUNC = 1, PB_DEALER_SELECT = 2, PB_DEALER_RESHARE = 3 };
+int pb_dealer_op(int op, uint64_t* mo, uint64_t* do_, int64_t n, int32_t k, const uint8_t* d_in,
+                 uint8_t* d_out, uint64_t seed, uint64_t stream_id, uint64_t raw_offset,
+                 int32_t ell, void* stream);
+
+/* SGD with momentum in float64 + re-quantisation:
+ * v = mu*v + g; w = w - lr*v; w_ring = encode_fixed(w, scale). */
+int pb_sgd_momentum(double* w, double* v, const uint64_t* grad_ring, int64_t n, int32_t grad_scale,
+                    double lr, double momentum, int32_t ell, int32_t w_scale, uint64_t* w_ring,
+                    int32_t* range_flag, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PENCIL_B200_H_ */

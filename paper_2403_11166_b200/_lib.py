@@ -1,0 +1,124 @@
+"""ctypes binding of the C ABI in include/pencil_b200.h.
+
+The shared library is built in-tree (``_build.py``) and loaded from the
+package directory.  There is no CPU fallback: if the library or a CUDA
+device is missing, every entry point raises ``DeviceError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import STATUS_TO_ERROR, DeviceError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpencil_b200.so")
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int32
+I64 = ctypes.c_int64
+U64 = ctypes.c_uint64
+INT = ctypes.c_int
+F64 = ctypes.c_double
+
+MAX_LIMBS = 8
+
+
+class PbParams(ctypes.Structure):
+    _fields_ = [
+        ("N", I32),
+        ("L", I32),
+        ("ell", I32),
+        ("reserved", I32),
+        ("q", ctypes.c_uint32 * MAX_LIMBS),
+        ("psi", ctypes.c_uint32 * MAX_LIMBS),
+        ("delta_mod_q", ctypes.c_uint32 * MAX_LIMBS),
+        ("garner_prefix_inv", ctypes.c_uint32 * MAX_LIMBS),
+        ("scale_int", ctypes.c_uint64 * MAX_LIMBS),
+        ("scale_frac", ctypes.c_double * MAX_LIMBS),
+    ]
+
+
+# name -> argtypes (every function returns int status unless listed in _RET)
+SIGNATURES = {
+    "pb_abi_version": [],
+    "pb_last_error": [],
+    "pb_device_sm_count": [P],
+    "pb_ctx_create": [P, P],
+    "pb_ctx_destroy": [P],
+    "pb_ntt_forward": [P, P, I64, P, P],
+    "pb_ntt_inverse": [P, P, I64, P, P],
+    "pb_pw": [P, INT, P, P, P, I64, I64, P, P],
+    "pb_garner_digits": [P, P, I64, P, P],
+    "pb_scale_round_digits": [P, P, I64, P, P],
+    "pb_decode": [P, P, I64, P, P],
+    "pb_negacyclic_mul_wrap": [P, P, I64, I32, P, P],
+    "pb_encode_plain": [P, P, P, I64, P, P, P],
+    "pb_lift": [P, P, P, I64, INT, P, P],
+    "pb_encrypt_pk": [P, P, P, P, I64, U64, U64, P, P],
+    "pb_encrypt_pk_noise": [P, P, P, P, I64, P, P, P, P, P],
+    "pb_encrypt_sk": [P, P, P, P, I64, U64, U64, P, P],
+    "pb_encrypt_sk_noise": [P, P, P, P, I64, P, P, P, P],
+    "pb_decrypt_coeffs": [P, P, P, I64, P, P],
+    "pb_decrypt": [P, P, P, I64, P, P, P],
+    "pb_decrypt_to_share": [P, P, P, I64, P, P, I32, P, P, P],
+    "pb_ctpt_mac_mask": [P, P, P, P, P, I32, I64, P, P, I32, P, INT, U64, P, P],
+    "pb_ring_binary": [INT, P, P, P, I64, I64, I32, P],
+    "pb_ring_unary": [INT, P, P, U64, I64, I32, P],
+    "pb_encode_fixed": [P, I64, I32, I32, P, P, P],
+    "pb_decode_fixed": [P, I64, I32, I32, P, P],
+    "pb_uniform_ring": [P, I64, U64, U64, U64, I32, P],
+    "pb_share": [P, I64, U64, U64, U64, I32, P, P, P],
+    "pb_ring_matmul": [P, P, I64, I64, I64, INT, INT, I32, P, P],
+    "pb_ring_rowsum": [P, I64, I64, I32, P, P],
+    "pb_im2col": [P, I32, I32, I32, I32, I32, I32, P, P],
+    "pb_col2im": [P, I32, I32, I32, I32, I32, I32, P, P],
+    "pb_conv2d": [P, P, I32, I32, I32, I32, I32, I32, I32, P, P],
+    "pb_dealer_op": [INT, P, P, I64, I32, P, P, U64, U64, U64, I32, P],
+    "pb_sgd_momentum": [P, P, P, I64, I32, F64, F64, I32, I32, P, P, P],
+}
+_RET = {"pb_last_error": ctypes.c_char_p}
+
+# ring / pointwise / dealer op codes (mirror the enums in pencil_b200.h)
+PW_MUL, PW_MAC, PW_ADD, PW_SUB = 0, 1, 2, 3
+RING_ADD, RING_SUB, RING_MUL, RING_NEG, RING_SCALAR_MUL, RING_MASK, RING_ARITH_SHIFT = range(7)
+DEALER_RELU, DEALER_TRUNC, DEALER_SELECT, DEALER_RESHARE = range(4)
+
+_lib = None
+
+
+def load(build_if_missing: bool = True):
+    """Load (building first if needed) the in-tree CUDA library."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH) and build_if_missing:
+        from . import _build
+
+        _build.build()
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(f"CUDA engine library missing: {LIB_PATH} (run __graft_entry__.build())")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RET.get(name, ctypes.c_int)
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    msg = load().pb_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int, what: str = "") -> None:
+    if status != 0:
+        cls = STATUS_TO_ERROR.get(int(status), DeviceError)
+        raise cls(f"{what}: {last_error()}" if what else last_error())
+
+
+def call(name: str, *args) -> None:
+    """Invoke a C ABI entry point and raise the mapped exception on failure."""
+    check(getattr(load(), name)(*args), name)

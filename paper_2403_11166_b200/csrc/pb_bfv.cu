@@ -1,0 +1,573 @@
+// pb_bfv.cu — fused RNS-BFV kernels for the Pencil linear-layer protocol.
+//
+//   encode_plain     centered lift + NTT + Shoup companions   (he_plain_mul operand)
+//   encrypt_pk/_sk   lift/pack + Delta*m + NTT + key MAC
+//   decrypt*         c0 + c1*s + INTT (+ Garner/scale-round, + pi_y^-1 gather)
+//   ctpt_mac_mask    sum_k ct (*) pt - Delta*NTT(mask)        (Alg.1 steps 2-3, Alg.2 step 2)
+//
+// One CTA per (polynomial, limb); the NTT lives in registers/shared memory
+// (pb_ntt.cuh) so every kernel reads its operands once from HBM and writes
+// its result once.
+#include "pb_ntt.cuh"
+
+namespace {
+
+// Z_t coefficient j of polynomial p (packing map or dense).
+__device__ __forceinline__ uint64_t coeff_val(const uint64_t* vals, const int64_t* src_map, int64_t p, int N,
+                                              int j) {
+  if (src_map) {
+    const int64_t idx = __ldg(src_map + p * N + j);
+    return idx >= 0 ? __ldg(vals + idx) : 0ull;
+  }
+  return __ldg(vals + p * N + j);
+}
+
+__device__ __forceinline__ uint32_t lift_small(int v, uint32_t q) { return v < 0 ? q - (uint32_t)(-v) : (uint32_t)v; }
+
+// Delta * m mod q for a Z_t value m.
+__device__ __forceinline__ uint32_t delta_m(const PbDev& P, int l, uint64_t m) {
+  const uint32_t q = P.q[l];
+  return mul_shoup(reduce64(m, q, P.mu[l]), P.delta[l], P.delta_sh[l], q);
+}
+
+// --------------------------------------------------------------- encode ---
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5))
+    k_encode_plain(PbDev P, const uint64_t* vals, const int64_t* src_map, int64_t nP, uint32_t* pt,
+                   uint32_t* pt_sh) {
+  using Nt = pb::Ntt<LOGN>;
+  extern __shared__ uint32_t sm[];
+  const int tid = threadIdx.x;
+  const int L = P.L;
+  const int64_t p = blockIdx.x / L;
+  const int l = blockIdx.x % L;
+  const uint32_t q = P.q[l];
+  uint32_t a[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c)
+    a[c] = lift_centered(coeff_val(vals, src_map, p, Nt::N, Nt::j1(tid, c)), P.ell, q, P.mu[l], P.tmod[l]);
+  Nt::forward(a, sm, P.tw_fwd + (size_t)l * Nt::N, tid, q);
+  uint32_t* row = pt + (p * L + l) * Nt::N;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = pb::canon4(a[c], q);
+  Nt::gst3(row, a, tid);
+  if (pt_sh) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a[c] = shoup_of(a[c], q, P.inv_q32[l]);
+    Nt::gst3(pt_sh + (p * L + l) * Nt::N, a, tid);
+  }
+}
+
+__global__ void k_lift(PbDev P, const uint64_t* vals, const int64_t* src_map, int64_t nP, int centered, uint32_t* out) {
+  const int N = P.N, L = P.L;
+  const int64_t total = nP * L * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e % N);
+    const int64_t pl = e / N;
+    const int l = (int)(pl % L);
+    const int64_t p = pl / L;
+    const uint64_t v = coeff_val(vals, src_map, p, N, j);
+    out[e] = centered ? lift_centered(v, P.ell, P.q[l], P.mu[l], P.tmod[l]) : reduce64(v, P.q[l], P.mu[l]);
+  }
+}
+
+// ----------------------------------------------------------------- noise ---
+// Device-only encryption randomness (fact 5: decrypted values do not depend
+// on it): ternary u and centred-binomial(eta=20) e from Philox4x32-10 keyed by
+// (seed, domain) with counter (coefficient, poly).
+__device__ __forceinline__ int cbd20(uint32_t x, uint32_t y) {
+  return __popc(x & 0xFFFFFu) - __popc(y & 0xFFFFFu);
+}
+
+__global__ void k_sample_noise(int N, int64_t nP, uint64_t seed, uint64_t nonce, int with_u, int8_t* u, int8_t* e1,
+                               int8_t* e2) {
+  const int64_t total = nP * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / N;
+    const uint32_t j = (uint32_t)(e - p * N);
+    const uint64_t pp = (uint64_t)p + nonce;
+    const u32x4 r = philox4x32_10(j, (uint32_t)pp, (uint32_t)(pp >> 32), 0x454e4331u /* "ENC1" */, (uint32_t)seed,
+                                  (uint32_t)(seed >> 32));
+    if (with_u) {
+      const u32x4 r2 = philox4x32_10(j, (uint32_t)pp, (uint32_t)(pp >> 32), 0x454e4332u, (uint32_t)seed,
+                                     (uint32_t)(seed >> 32));
+      u[e] = (int8_t)((int)(((uint64_t)r2.v[0] * 3ull) >> 32) - 1);
+      e2[e] = (int8_t)cbd20(r2.v[1], r2.v[2]);
+    }
+    e1[e] = (int8_t)cbd20(r.v[0], r.v[1]);
+  }
+}
+
+// --------------------------------------------------------------- encrypt ---
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5))
+    k_encrypt_pk(PbDev P, const uint32_t* pk, const uint64_t* vals, const int64_t* src_map, int64_t nP,
+                 const int8_t* u, const int8_t* e1, const int8_t* e2, uint32_t* ct) {
+  using Nt = pb::Ntt<LOGN>;
+  constexpr int N = Nt::N;
+  extern __shared__ uint32_t sm[];
+  const int tid = threadIdx.x;
+  const int L = P.L;
+  const int64_t p = blockIdx.x / L;
+  const int l = blockIdx.x % L;
+  const uint32_t q = P.q[l];
+  const uint64_t mu = P.mu[l];
+  const uint2* tw = P.tw_fwd + (size_t)l * N;
+  const int8_t* up = u + p * N;
+  const int8_t* e1p = e1 + p * N;
+  const int8_t* e2p = e2 + p * N;
+
+  uint32_t U[32], b[32], k[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) U[c] = lift_small(up[Nt::j1(tid, c)], q);
+  Nt::forward(U, sm, tw, tid, q);
+  __syncthreads();
+  // c1 = pk1 * U + NTT(e2)
+#pragma unroll
+  for (int c = 0; c < 32; ++c) b[c] = lift_small(e2p[Nt::j1(tid, c)], q);
+  Nt::forward(b, sm, tw, tid, q);
+  Nt::gld3(pk + ((size_t)1 * L + l) * N, k, tid);
+#pragma unroll
+  for (int c = 0; c < 32; ++c) b[c] = addmod(mulmod(k[c], U[c], q, mu), pb::canon4(b[c], q), q);
+  Nt::gst3(ct + ((p * 2 + 1) * L + l) * N, b, tid);
+  __syncthreads();
+  // c0 = pk0 * U + NTT(e1 + Delta m)
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const int j = Nt::j1(tid, c);
+    b[c] = addmod(lift_small(e1p[j], q), delta_m(P, l, coeff_val(vals, src_map, p, N, j)), q);
+  }
+  Nt::forward(b, sm, tw, tid, q);
+  Nt::gld3(pk + (size_t)l * N, k, tid);
+#pragma unroll
+  for (int c = 0; c < 32; ++c) b[c] = addmod(mulmod(k[c], U[c], q, mu), pb::canon4(b[c], q), q);
+  Nt::gst3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
+}
+
+// Uniform residue mod q for (poly, limb, coefficient-pair) from Philox4x32.
+__device__ __forceinline__ void uniform_pair(uint64_t seed, uint64_t nonce, int64_t p, int l, int jpair, uint32_t q,
+                                             uint32_t domain, uint32_t& x0, uint32_t& x1) {
+  const uint64_t pp = (uint64_t)p + nonce;
+  const u32x4 r = philox4x32_10((uint32_t)jpair | ((uint32_t)l << 24), (uint32_t)pp, (uint32_t)(pp >> 32), domain,
+                                (uint32_t)seed, (uint32_t)(seed >> 32));
+  const uint64_t a = ((uint64_t)r.v[1] << 32) | r.v[0];
+  const uint64_t b = ((uint64_t)r.v[3] << 32) | r.v[2];
+  x0 = (uint32_t)__umul64hi(a, q);
+  x1 = (uint32_t)__umul64hi(b, q);
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5))
+    k_encrypt_sk(PbDev P, const uint32_t* sk, const uint64_t* vals, const int64_t* src_map, int64_t nP,
+                 const uint32_t* a_in, const int8_t* e, uint64_t seed, uint64_t nonce, uint32_t* ct) {
+  using Nt = pb::Ntt<LOGN>;
+  constexpr int N = Nt::N;
+  extern __shared__ uint32_t sm[];
+  const int tid = threadIdx.x;
+  const int L = P.L;
+  const int64_t p = blockIdx.x / L;
+  const int l = blockIdx.x % L;
+  const uint32_t q = P.q[l];
+  const uint64_t mu = P.mu[l];
+  const int8_t* ep = e + p * N;
+  uint32_t b[32], a[32], s[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const int j = Nt::j1(tid, c);
+    b[c] = addmod(lift_small(ep[j], q), delta_m(P, l, coeff_val(vals, src_map, p, N, j)), q);
+  }
+  Nt::forward(b, sm, P.tw_fwd + (size_t)l * N, tid, q);
+  if (a_in) {
+    Nt::gld3(a_in + (p * L + l) * N, a, tid);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 32; c += 2) uniform_pair(seed, nonce, p, l, (tid << 4) + (c >> 1), q, 0x53454e43u, a[c], a[c + 1]);
+  }
+  Nt::gld3(sk + (size_t)l * N, s, tid);
+#pragma unroll
+  for (int c = 0; c < 32; ++c) b[c] = submod(pb::canon4(b[c], q), mulmod(a[c], s[c], q, mu), q);
+  Nt::gst3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
+  Nt::gst3(ct + ((p * 2 + 1) * L + l) * N, a, tid);
+}
+
+// --------------------------------------------------------------- decrypt ---
+// mode 0: write x = INTT(c0 + c1 s) for all coefficients to out32 [P][L][N].
+// mode 1: write only the useful slots out_pos[p][u] to out32 [P][L][U].
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5))
+    k_decrypt_inv(PbDev P, const uint32_t* sk, const uint32_t* ct, int64_t nP, int mode, const int32_t* out_pos,
+                  int U, uint32_t* out32) {
+  using Nt = pb::Ntt<LOGN>;
+  constexpr int N = Nt::N;
+  extern __shared__ uint32_t sm[];
+  const int tid = threadIdx.x;
+  const int L = P.L;
+  const int64_t p = blockIdx.x / L;
+  const int l = blockIdx.x % L;
+  const uint32_t q = P.q[l];
+  const uint64_t mu = P.mu[l];
+  uint32_t a[32], b[32];
+  Nt::gld3(ct + ((p * 2 + 1) * L + l) * N, a, tid);
+  Nt::gld3(sk + (size_t)l * N, b, tid);
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = mulmod(a[c], b[c], q, mu);
+  Nt::gld3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = addmod(a[c], b[c], q);
+  Nt::inverse(a, sm, P.tw_inv + (size_t)l * N, tid, q);
+  const uint32_t ni = P.ninv[l], nis = P.ninv_sh[l];
+  if (mode == 0) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a[c] = mul_shoup(a[c], ni, nis, q);
+    Nt::gst1(out32 + (p * L + l) * N, a, tid);
+  } else {
+    __syncthreads();
+    Nt::st1(sm, a, tid);
+    __syncthreads();
+    const int32_t* pos = out_pos + p * U;
+    uint32_t* dst = out32 + (p * L + l) * U;
+    for (int u = tid; u < U; u += Nt::T) {
+      const int j = pos[u];
+      if (j >= 0) dst[u] = mul_shoup(sm[Nt::pad(j)], ni, nis, q);
+    }
+  }
+}
+
+__device__ __forceinline__ void garner_dev(const PbDev& P, const uint32_t* x, int64_t xs, uint32_t (&d)[PB_MAXL]) {
+#pragma unroll
+  for (int i = 0; i < PB_MAXL; ++i) {
+    if (i < P.L) {
+      const uint32_t qi = P.q[i];
+      const uint64_t mu = P.mu[i];
+      uint32_t acc = 0;
+#pragma unroll
+      for (int k = 0; k < PB_MAXL; ++k)
+        if (k < i) acc = addmod(acc, mulmod(d[k], P.pmod[i][k], qi, mu), qi);
+      const uint32_t xv = reduce64(x[i * xs], qi, mu);
+      d[i] = mul_shoup(submod(xv, acc, qi), P.pinv[i], P.pinv_sh[i], qi);
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t scale_round_dev(const PbDev& P, const uint32_t (&d)[PB_MAXL]) {
+  uint64_t acc_i = 0;
+  double acc_f = 0.0;
+#pragma unroll
+  for (int i = 0; i < PB_MAXL; ++i) {
+    if (i < P.L) {
+      acc_i += (uint64_t)d[i] * P.sc_int[i];
+      acc_f = __dadd_rn(acc_f, __dmul_rn((double)d[i], P.sc_frac[i]));
+    }
+  }
+  return (acc_i + (uint64_t)floor(__dadd_rn(acc_f, 0.5))) & P.t_mask;
+}
+
+// Garner + scale-round on the gathered slots, scattered into the share tensor.
+__global__ void k_decode_gather(PbDev P, const uint32_t* x, int64_t nP, int U, const int32_t* out_pos,
+                                const int64_t* out_dst, uint64_t* share) {
+  const int L = P.L;
+  const int64_t total = nP * U;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    if (out_pos[e] < 0) continue;
+    const int64_t p = e / U;
+    const int u = (int)(e - p * U);
+    uint32_t d[PB_MAXL];
+    garner_dev(P, x + p * L * U + u, U, d);
+    share[out_dst[e]] = scale_round_dev(P, d);
+  }
+}
+
+__global__ void k_decode_dense(PbDev P, const uint32_t* x, int64_t nP, uint64_t* out) {
+  const int N = P.N, L = P.L;
+  const int64_t total = nP * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / N;
+    const int j = (int)(e - p * N);
+    uint32_t d[PB_MAXL];
+    garner_dev(P, x + p * L * N + j, N, d);
+    out[e] = scale_round_dev(P, d);
+  }
+}
+
+// ------------------------------------------------------------- MO: MAC ---
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5))
+    k_ctpt_mac_mask(PbDev P, const uint32_t* ct_in, const uint32_t* pt, const uint32_t* pt_sh, const int32_t* terms,
+                    int K, int64_t nP, const int32_t* out_pos, const int64_t* out_dst, int U, const uint64_t* mask_vals,
+                    int filler, uint64_t filler_seed, uint32_t* ct_out) {
+  using Nt = pb::Ntt<LOGN>;
+  constexpr int N = Nt::N;
+  extern __shared__ uint32_t sm[];
+  const int tid = threadIdx.x;
+  const int L = P.L;
+  const int64_t p = blockIdx.x / L;
+  const int l = blockIdx.x % L;
+  const uint32_t q = P.q[l];
+
+  // 1. Delta * mask polynomial (coefficient form) in shared memory.
+  if (filler) {
+    for (int jp = tid; jp < N / 2; jp += Nt::T) {
+      uint32_t x0, x1;
+      uniform_pair(filler_seed, 0, p, l, jp, q, 0x4d41534bu /* "MASK" */, x0, x1);
+      sm[Nt::pad(2 * jp)] = x0;
+      sm[Nt::pad(2 * jp + 1)] = x1;
+    }
+  } else {
+    for (int j = tid; j < N; j += Nt::T) sm[Nt::pad(j)] = 0u;
+  }
+  __syncthreads();
+  if (mask_vals) {
+    const int32_t* pos = out_pos + p * U;
+    const int64_t* dst = out_dst + p * U;
+    for (int u = tid; u < U; u += Nt::T) {
+      const int j = pos[u];
+      if (j >= 0) sm[Nt::pad(j)] = delta_m(P, l, __ldg(mask_vals + dst[u]));
+    }
+  }
+  __syncthreads();
+  uint32_t m[32];
+  Nt::ld1(sm, m, tid);
+  __syncthreads();
+  Nt::forward(m, sm, P.tw_fwd + (size_t)l * N, tid, q);
+
+  // 2. MAC over the K (ct, pt) terms in P3 layout.
+  uint32_t acc0[32], acc1[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) { acc0[c] = 0u; acc1[c] = 0u; }
+  for (int kk = 0; kk < K; ++kk) {
+    const int ci = terms[(p * K + kk) * 2 + 0];
+    const int pi = terms[(p * K + kk) * 2 + 1];
+    if (ci < 0) continue;
+    const uint4* w4 = reinterpret_cast<const uint4*>(pt + ((size_t)pi * L + l) * N + (tid << 5));
+    const uint4* ws4 = reinterpret_cast<const uint4*>(pt_sh + ((size_t)pi * L + l) * N + (tid << 5));
+    const uint4* c04 = reinterpret_cast<const uint4*>(ct_in + (((size_t)ci * 2 + 0) * L + l) * N + (tid << 5));
+    const uint4* c14 = reinterpret_cast<const uint4*>(ct_in + (((size_t)ci * 2 + 1) * L + l) * N + (tid << 5));
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const uint4 w = __ldg(w4 + v), ws = __ldg(ws4 + v), x0 = __ldg(c04 + v), x1 = __ldg(c14 + v);
+      acc0[4 * v + 0] = addmod(acc0[4 * v + 0], mul_shoup(x0.x, w.x, ws.x, q), q);
+      acc0[4 * v + 1] = addmod(acc0[4 * v + 1], mul_shoup(x0.y, w.y, ws.y, q), q);
+      acc0[4 * v + 2] = addmod(acc0[4 * v + 2], mul_shoup(x0.z, w.z, ws.z, q), q);
+      acc0[4 * v + 3] = addmod(acc0[4 * v + 3], mul_shoup(x0.w, w.w, ws.w, q), q);
+      acc1[4 * v + 0] = addmod(acc1[4 * v + 0], mul_shoup(x1.x, w.x, ws.x, q), q);
+      acc1[4 * v + 1] = addmod(acc1[4 * v + 1], mul_shoup(x1.y, w.y, ws.y, q), q);
+      acc1[4 * v + 2] = addmod(acc1[4 * v + 2], mul_shoup(x1.z, w.z, ws.z, q), q);
+      acc1[4 * v + 3] = addmod(acc1[4 * v + 3], mul_shoup(x1.w, w.w, ws.w, q), q);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 32; ++c) acc0[c] = submod(acc0[c], pb::canon4(m[c], q), q);
+  Nt::gst3(ct_out + ((p * 2 + 0) * L + l) * N, acc0, tid);
+  Nt::gst3(ct_out + ((p * 2 + 1) * L + l) * N, acc1, tid);
+}
+
+// ------------------------------------------------------------- launchers ---
+template <typename KernelT>
+static void set_smem(KernelT k, size_t smem) {
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <int LOGN>
+void launch_encode_plain(const PbDev& P, const uint64_t* vals, const int64_t* src_map, int64_t nP, uint32_t* pt,
+                         uint32_t* pt_sh, cudaStream_t st) {
+  using Nt = pb::Ntt<LOGN>;
+  const size_t smem = Nt::SMEM_WORDS * 4;
+  set_smem(k_encode_plain<LOGN>, smem);
+  k_encode_plain<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, vals, src_map, nP, pt, pt_sh);
+}
+
+template <int LOGN>
+void launch_encrypt_pk(const PbDev& P, const uint32_t* pk, const uint64_t* vals, const int64_t* src_map, int64_t nP,
+                       const int8_t* u, const int8_t* e1, const int8_t* e2, uint32_t* ct, cudaStream_t st) {
+  using Nt = pb::Ntt<LOGN>;
+  const size_t smem = Nt::SMEM_WORDS * 4;
+  set_smem(k_encrypt_pk<LOGN>, smem);
+  k_encrypt_pk<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, pk, vals, src_map, nP, u, e1, e2, ct);
+}
+
+template <int LOGN>
+void launch_encrypt_sk(const PbDev& P, const uint32_t* sk, const uint64_t* vals, const int64_t* src_map, int64_t nP,
+                       const uint32_t* a_in, const int8_t* e, uint64_t seed, uint64_t nonce, uint32_t* ct,
+                       cudaStream_t st) {
+  using Nt = pb::Ntt<LOGN>;
+  const size_t smem = Nt::SMEM_WORDS * 4;
+  set_smem(k_encrypt_sk<LOGN>, smem);
+  k_encrypt_sk<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, sk, vals, src_map, nP, a_in, e, seed, nonce, ct);
+}
+
+template <int LOGN>
+void launch_decrypt_inv(const PbDev& P, const uint32_t* sk, const uint32_t* ct, int64_t nP, int mode,
+                        const int32_t* out_pos, int U, uint32_t* out32, cudaStream_t st) {
+  using Nt = pb::Ntt<LOGN>;
+  const size_t smem = Nt::SMEM_WORDS * 4;
+  set_smem(k_decrypt_inv<LOGN>, smem);
+  k_decrypt_inv<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, sk, ct, nP, mode, out_pos, U, out32);
+}
+
+template <int LOGN>
+void launch_mac(const PbDev& P, const uint32_t* ct_in, const uint32_t* pt, const uint32_t* pt_sh, const int32_t* terms,
+                int K, int64_t nP, const int32_t* out_pos, const int64_t* out_dst, int U, const uint64_t* mask_vals,
+                int filler, uint64_t filler_seed, uint32_t* ct_out, cudaStream_t st) {
+  using Nt = pb::Ntt<LOGN>;
+  const size_t smem = Nt::SMEM_WORDS * 4;
+  set_smem(k_ctpt_mac_mask<LOGN>, smem);
+  k_ctpt_mac_mask<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, ct_in, pt, pt_sh, terms, K, nP, out_pos, out_dst,
+                                                                   U, mask_vals, filler, filler_seed, ct_out);
+}
+
+int need_big_n(const pb_ctx* ctx) {
+  if (!ctx) return pb_set_error(PB_ERR_ARG, "null context");
+  if (ctx->dev.logN < 11) return pb_set_error(PB_ERR_PARAMS, "fused BFV kernels need N >= 2048");
+  return PB_OK;
+}
+
+int64_t max_grid_polys(const pb_ctx* ctx) { return (int64_t)0x7fffffff / ctx->dev.L; }
+
+}  // namespace
+
+// ================================================================ C ABI ===
+extern "C" int pb_encode_plain(const pb_ctx* ctx, const uint64_t* vals, const int64_t* src_map, int64_t nP,
+                               uint32_t* pt, uint32_t* pt_shoup, void* stream) {
+  if (int s = need_big_n(ctx)) return s;
+  if (!vals || !pt) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (nP <= 0) return PB_OK;
+  if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encode_plain, ctx->dev, vals, src_map, nP, pt, pt_shoup, pb_stream_of(stream));
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_lift(const pb_ctx* ctx, const uint64_t* vals, const int64_t* src_map, int64_t nP, int centered,
+                       uint32_t* out, void* stream) {
+  if (!ctx || !vals || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (nP <= 0) return PB_OK;
+  k_lift<<<pb_grid_1d(nP * ctx->dev.L * ctx->dev.N, 256), 256, 0, pb_stream_of(stream)>>>(ctx->dev, vals, src_map, nP,
+                                                                                          centered, out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_encrypt_pk_noise(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* vals, const int64_t* src_map,
+                                   int64_t nP, const int8_t* u, const int8_t* e1, const int8_t* e2, uint32_t* ct,
+                                   void* stream) {
+  if (int s = need_big_n(ctx)) return s;
+  if (!pk || !vals || !u || !e1 || !e2 || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (nP <= 0) return PB_OK;
+  if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_pk, ctx->dev, pk, vals, src_map, nP, u, e1, e2, ct,
+                   pb_stream_of(stream));
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+// Scratch for device-sampled noise: a per-thread cached buffer reused
+// across calls (stream-ordered use only).
+static thread_local int8_t* g_noise = nullptr;
+static thread_local size_t g_noise_bytes = 0;
+static int8_t* noise_buffer(size_t bytes) {
+  if (bytes > g_noise_bytes) {
+    if (g_noise) cudaFree(g_noise);
+    g_noise = nullptr;
+    g_noise_bytes = 0;
+    if (cudaMalloc(&g_noise, bytes) != cudaSuccess) return nullptr;
+    g_noise_bytes = bytes;
+  }
+  return g_noise;
+}
+
+extern "C" int pb_encrypt_pk(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* vals, const int64_t* src_map,
+                             int64_t nP, uint64_t seed, uint64_t nonce, uint32_t* ct, void* stream) {
+  if (int s = need_big_n(ctx)) return s;
+  if (nP <= 0) return PB_OK;
+  const int N = ctx->dev.N;
+  int8_t* buf = noise_buffer((size_t)nP * N * 3);
+  if (!buf) return pb_set_error(PB_ERR_CUDA, "noise scratch allocation failed");
+  int8_t *u = buf, *e1 = buf + nP * N, *e2 = buf + 2 * nP * N;
+  cudaStream_t st = pb_stream_of(stream);
+  k_sample_noise<<<pb_grid_1d(nP * N, 256), 256, 0, st>>>(N, nP, seed, nonce, 1, u, e1, e2);
+  PB_CHECK_LAUNCH();
+  return pb_encrypt_pk_noise(ctx, pk, vals, src_map, nP, u, e1, e2, ct, stream);
+}
+
+extern "C" int pb_encrypt_sk_noise(const pb_ctx* ctx, const uint32_t* sk, const uint64_t* vals, const int64_t* src_map,
+                                   int64_t nP, const uint32_t* a, const int8_t* e, uint32_t* ct, void* stream) {
+  if (int s = need_big_n(ctx)) return s;
+  if (!sk || !vals || !e || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (nP <= 0) return PB_OK;
+  if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, vals, src_map, nP, a, e, 0ull, 0ull, ct,
+                   pb_stream_of(stream));
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk, const uint64_t* vals, const int64_t* src_map,
+                             int64_t nP, uint64_t seed, uint64_t nonce, uint32_t* ct, void* stream) {
+  if (int s = need_big_n(ctx)) return s;
+  if (!sk || !vals || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (nP <= 0) return PB_OK;
+  if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  const int N = ctx->dev.N;
+  int8_t* e = noise_buffer((size_t)nP * N);
+  if (!e) return pb_set_error(PB_ERR_CUDA, "noise scratch allocation failed");
+  cudaStream_t st = pb_stream_of(stream);
+  k_sample_noise<<<pb_grid_1d(nP * N, 256), 256, 0, st>>>(N, nP, seed, nonce, 0, nullptr, e, nullptr);
+  PB_CHECK_LAUNCH();
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, vals, src_map, nP, (const uint32_t*)nullptr, e,
+                   seed, nonce, ct, st);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_decrypt_coeffs(const pb_ctx* ctx, const uint32_t* sk, const uint32_t* ct, int64_t nP, uint32_t* x,
+                                 void* stream) {
+  if (int s = need_big_n(ctx)) return s;
+  if (!sk || !ct || !x) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (nP <= 0) return PB_OK;
+  if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_decrypt_inv, ctx->dev, sk, ct, nP, 0, (const int32_t*)nullptr, 0, x,
+                   pb_stream_of(stream));
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_decrypt(const pb_ctx* ctx, const uint32_t* sk, const uint32_t* ct, int64_t nP, uint64_t* m,
+                          uint32_t* scratch, void* stream) {
+  if (int s = pb_decrypt_coeffs(ctx, sk, ct, nP, scratch, stream)) return s;
+  if (nP <= 0) return PB_OK;
+  if (!m) return pb_set_error(PB_ERR_ARG, "null argument");
+  k_decode_dense<<<pb_grid_1d(nP * ctx->dev.N, 256), 256, 0, pb_stream_of(stream)>>>(ctx->dev, scratch, nP, m);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_decrypt_to_share(const pb_ctx* ctx, const uint32_t* sk, const uint32_t* ct, int64_t nP,
+                                   const int32_t* out_pos, const int64_t* out_dst, int32_t U, uint64_t* share_out,
+                                   uint32_t* scratch, void* stream) {
+  if (int s = need_big_n(ctx)) return s;
+  if (!sk || !ct || !out_pos || !out_dst || !share_out || !scratch) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (nP <= 0 || U <= 0) return PB_OK;
+  if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  cudaStream_t st = pb_stream_of(stream);
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_decrypt_inv, ctx->dev, sk, ct, nP, 1, out_pos, U, scratch, st);
+  PB_CHECK_LAUNCH();
+  k_decode_gather<<<pb_grid_1d(nP * U, 128), 128, 0, st>>>(ctx->dev, scratch, nP, U, out_pos, out_dst, share_out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_ctpt_mac_mask(const pb_ctx* ctx, const uint32_t* ct_in, const uint32_t* pt, const uint32_t* pt_shoup,
+                                const int32_t* terms, int32_t K, int64_t nP, const int32_t* out_pos,
+                                const int64_t* out_dst, int32_t U, const uint64_t* mask_vals, int filler,
+                                uint64_t filler_seed, uint32_t* ct_out, void* stream) {
+  if (int s = need_big_n(ctx)) return s;
+  if (!ct_in || !pt || !pt_shoup || !terms || !ct_out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (mask_vals && (!out_pos || !out_dst)) return pb_set_error(PB_ERR_ARG, "mask needs out_pos/out_dst");
+  if (K < 1) return pb_set_error(PB_ERR_SHAPE, "K must be >= 1");
+  if (nP <= 0) return PB_OK;
+  if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_mac, ctx->dev, ct_in, pt, pt_shoup, terms, K, nP, out_pos, out_dst, U,
+                   mask_vals, filler, filler_seed, ct_out, pb_stream_of(stream));
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}

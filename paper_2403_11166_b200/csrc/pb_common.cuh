@@ -1,0 +1,170 @@
+// pb_common.cuh — device-side parameter block, modular arithmetic and RNG
+// shared by every sm_100a kernel of the Pencil HE linear-layer engine.
+//
+// Residues are u32 (moduli q < 2^30, so lazy values in [0, 4q) fit u32;
+// SURVEY §0 fact 3 set A).  Z_{2^ell} share elements are u64 bit patterns.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pencil_b200.h"
+
+#define PB_MAXL PB_MAX_LIMBS
+
+// Everything a kernel needs about the parameter set, passed by value
+// (kernel parameter space) so it is served from the constant bank.
+struct PbDev {
+  int N, logN, L, ell;
+  uint64_t t_mask;
+  uint32_t q[PB_MAXL];
+  uint32_t ninv[PB_MAXL], ninv_sh[PB_MAXL];    // N^-1 mod q and its Shoup quotient
+  uint32_t delta[PB_MAXL], delta_sh[PB_MAXL];  // floor(Q/t) mod q_i
+  uint64_t mu[PB_MAXL];                        // floor(2^64 / q) (Barrett)
+  double inv_q32[PB_MAXL];                     // 2^32 / q (Shoup quotient estimate)
+  uint32_t tmod[PB_MAXL];                      // t mod q_i (centered lift)
+  uint32_t pinv[PB_MAXL], pinv_sh[PB_MAXL];    // Garner (q_0..q_{i-1})^-1 mod q_i
+  uint32_t pmod[PB_MAXL][PB_MAXL];             // pmod[i][k] = (q_0..q_{k-1}) mod q_i
+  uint64_t sc_int[PB_MAXL];                    // floor(t P_{i-1} / Q) mod 2^64
+  double sc_frac[PB_MAXL];                     // frac(t P_{i-1} / Q)
+  const uint2* tw_fwd;                         // [L][N] {psi^brv(i), shoup}
+  const uint2* tw_inv;                         // [L][N] {psi^-brv(i), shoup}
+};
+
+struct pb_ctx {
+  PbDev dev;        // device pointers inside point at the buffers below
+  uint2* d_tw_fwd;
+  uint2* d_tw_inv;
+  pb_params host;   // the descriptor the context was created from
+};
+
+// ------------------------------------------------------------ mod arith ---
+
+// Shoup multiplication: a * w mod q given ws = floor(w * 2^32 / q).
+// Valid for any a < 2^32; result in [0, 2q).
+__device__ __forceinline__ uint32_t mul_shoup_lazy(uint32_t a, uint32_t w, uint32_t ws, uint32_t q) {
+  const uint32_t hi = __umulhi(a, ws);
+  return a * w - hi * q;
+}
+
+__device__ __forceinline__ uint32_t csub(uint32_t x, uint32_t m) {  // x in [0, 2m) -> [0, m)
+  return min(x, x - m);
+}
+
+__device__ __forceinline__ uint32_t mul_shoup(uint32_t a, uint32_t w, uint32_t ws, uint32_t q) {
+  return csub(mul_shoup_lazy(a, w, ws, q), q);
+}
+
+// Exact Shoup quotient floor(w * 2^32 / q) for w < q, from a float64 estimate.
+__device__ __forceinline__ uint32_t shoup_of(uint32_t w, uint32_t q, double inv_q32) {
+  const uint64_t num = (uint64_t)w << 32;
+  uint32_t est = (uint32_t)__double2uint_rz(__dmul_rn((double)w, inv_q32));
+  int64_t r = (int64_t)(num - (uint64_t)est * q);
+  while (r < 0) { --est; r += q; }
+  while (r >= (int64_t)q) { ++est; r -= q; }
+  return est;
+}
+
+// Barrett reduction of a 64-bit value: x mod q, mu = floor(2^64/q).
+__device__ __forceinline__ uint32_t reduce64(uint64_t x, uint32_t q, uint64_t mu) {
+  const uint64_t qh = __umul64hi(x, mu);
+  uint64_t r = x - qh * (uint64_t)q;  // r < 3q
+  uint32_t rr = (uint32_t)r;
+  rr = min(rr, rr - q);
+  rr = min(rr, rr - q);
+  return rr;
+}
+
+// Generic a*b mod q for a, b < 2^32.
+__device__ __forceinline__ uint32_t mulmod(uint32_t a, uint32_t b, uint32_t q, uint64_t mu) {
+  return reduce64((uint64_t)a * b, q, mu);
+}
+
+__device__ __forceinline__ uint32_t addmod(uint32_t a, uint32_t b, uint32_t q) {  // a,b < q
+  return csub(a + b, q);
+}
+__device__ __forceinline__ uint32_t submod(uint32_t a, uint32_t b, uint32_t q) {  // a,b < q
+  return csub(a + q - b, q);
+}
+
+// Centered lift of a Z_t value (t = 2^ell) into Z_q: v >= t/2 -> v - t.
+__device__ __forceinline__ uint32_t lift_centered(uint64_t v, int ell, uint32_t q, uint64_t mu,
+                                                  uint32_t tmod) {
+  const uint32_t r = reduce64(v, q, mu);
+  const bool neg = (v >> (ell - 1)) & 1ull;
+  return neg ? submod(r, tmod, q) : r;
+}
+
+// ---------------------------------------------------------------- Philox ---
+// Philox4x64-10 exactly as numpy's PhiloxGenerator (R:52-55 uses
+// np.random.Philox(key=[seed, stream])): counter words pre-incremented, so
+// raw output r of a fresh stream comes from block ctr=(r/4 + 1, 0, 0, 0),
+// lane r % 4 (pinned by tests/test_gpu_rng.py).
+struct u64x4 {
+  uint64_t v[4];
+};
+
+__device__ __forceinline__ u64x4 philox4x64_10(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3,
+                                               uint64_t k0, uint64_t k1) {
+  const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+  const uint64_t W0 = 0x9E3779B97F4A7C15ull, W1 = 0xBB67AE8584CAA73Bull;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t hi0 = __umul64hi(c0, M0), lo0 = c0 * M0;
+    const uint64_t hi1 = __umul64hi(c2, M1), lo1 = c2 * M1;
+    const uint64_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    k0 += W0; k1 += W1;
+  }
+  u64x4 o;
+  o.v[0] = c0; o.v[1] = c1; o.v[2] = c2; o.v[3] = c3;
+  return o;
+}
+
+// Raw 64-bit output #idx (0-based) of numpy Philox(key=[seed, stream]).
+__device__ __forceinline__ uint64_t philox_np_raw(uint64_t seed, uint64_t stream, uint64_t idx) {
+  const uint64_t blk = (idx >> 2) + 1;
+  const u64x4 o = philox4x64_10(blk, 0, 0, 0, seed, stream);
+  return o.v[idx & 3];
+}
+
+// Philox4x32-10 for device-only randomness (encryption noise, mask filler):
+// independent of numpy, domain-separated by the key words.
+struct u32x4 {
+  uint32_t v[4];
+};
+__device__ __forceinline__ u32x4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                               uint32_t k0, uint32_t k1) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(c0, M0), lo0 = c0 * M0;
+    const uint32_t hi1 = __umulhi(c2, M1), lo1 = c2 * M1;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    k0 += W0; k1 += W1;
+  }
+  u32x4 o;
+  o.v[0] = c0; o.v[1] = c1; o.v[2] = c2; o.v[3] = c3;
+  return o;
+}
+
+// ---------------------------------------------------------- launch glue ---
+
+#define PB_CHECK_LAUNCH()                                      \
+  do {                                                         \
+    cudaError_t _e = cudaGetLastError();                       \
+    if (_e != cudaSuccess) return pb_set_cuda_error(_e);       \
+  } while (0)
+
+int pb_set_cuda_error(cudaError_t e);
+int pb_set_error(int code, const char* msg);
+
+static inline cudaStream_t pb_stream_of(void* s) { return (cudaStream_t)s; }
+
+static inline int pb_grid_1d(int64_t n, int threads, int64_t cap = 148 * 32) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}

@@ -1,0 +1,275 @@
+// pb_ntt.cuh — register-blocked negacyclic NTT building blocks for sm_100a.
+//
+// Same transform as the reference ntt_forward / ntt_inverse (K:31-77):
+// Cooley-Tukey with psi^bitrev twiddles, natural -> bit-reversed order, and
+// the Gentleman-Sande inverse back to natural order.  The arithmetic is
+// Harvey's lazy butterfly with Shoup twiddles over u32 residues (q < 2^30,
+// values kept in [0,4q) forward / [0,2q) inverse, canonicalised once at the
+// end), so results are bit-identical to K's fully reduced `%` version.
+//
+// Layout: one CTA of T = N/32 threads owns a row; every thread holds 32
+// residues in registers.  The log2(N) stages are done in three register
+// passes separated by two shared-memory exchanges:
+//   P1  stages 0..4        (index bits N-1..N-5)   j = tid + T*c
+//   P2  stages 5..logN-6   (middle bits)           j = lane | mid(c)<<5 | top(c,warp)
+//   P3  stages logN-5..    (bits 4..0)             j = tid*32 + c
+// Shared memory is padded (word j lives at j + j/32), which makes all three
+// access patterns bank-conflict free with compile-time immediate offsets.
+#pragma once
+
+#include "pb_common.cuh"
+
+namespace pb {
+
+__device__ __forceinline__ void ct_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t q, uint32_t q2) {
+  const uint32_t xx = min(x, x - q2);          // [0, 2q)
+  const uint32_t tt = mul_shoup_lazy(y, w.x, w.y, q);  // [0, 2q)
+  x = xx + tt;                                 // [0, 4q)
+  y = xx - tt + q2;                            // (0, 4q)
+}
+
+__device__ __forceinline__ void gs_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t q, uint32_t q2) {
+  uint32_t s = x + y;                          // inputs in [0, 2q)
+  s = min(s, s - q2);                          // [0, 2q)
+  const uint32_t d = x - y + q2;               // (0, 4q)
+  y = mul_shoup_lazy(d, w.x, w.y, q);          // [0, 2q)
+  x = s;
+}
+
+template <int LOGN>
+struct Ntt {
+  static_assert(LOGN >= 11 && LOGN <= 15, "register NTT covers N = 2^11 .. 2^15");
+  static constexpr int N = 1 << LOGN;
+  static constexpr int T = N >> 5;
+  static constexpr int M = LOGN - 10;
+  static constexpr int SMEM_WORDS = N + (N >> 5);
+
+  __device__ __forceinline__ static int pad(int j) { return j + (j >> 5); }
+
+  // ---- index maps ----
+  __device__ __forceinline__ static int fc2(int c) {  // compile-time part of the P2 index
+    return ((c & ((1 << M) - 1)) << 5) | ((c >> M) << (LOGN - 5));
+  }
+  __device__ __forceinline__ static int j1(int tid, int c) { return tid + T * c; }
+  __device__ __forceinline__ static int j2(int tid, int c) {
+    return (tid & 31) + ((tid >> 5) << 10) + fc2(c);
+  }
+  __device__ __forceinline__ static int j3(int tid, int c) { return (tid << 5) + c; }
+
+  // ---- shared memory exchanges (padded layout) ----
+  __device__ __forceinline__ static void st1(uint32_t* sm, const uint32_t (&a)[32], int tid) {
+    uint32_t* b = sm + pad(tid);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) b[c * (T + T / 32)] = a[c];
+  }
+  __device__ __forceinline__ static void ld1(const uint32_t* sm, uint32_t (&a)[32], int tid) {
+    const uint32_t* b = sm + pad(tid);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a[c] = b[c * (T + T / 32)];
+  }
+  __device__ __forceinline__ static void st2(uint32_t* sm, const uint32_t (&a)[32], int tid) {
+    uint32_t* b = sm + pad(j2(tid, 0));
+#pragma unroll
+    for (int c = 0; c < 32; ++c) b[pad(fc2(c))] = a[c];
+  }
+  __device__ __forceinline__ static void ld2(const uint32_t* sm, uint32_t (&a)[32], int tid) {
+    const uint32_t* b = sm + pad(j2(tid, 0));
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a[c] = b[pad(fc2(c))];
+  }
+  __device__ __forceinline__ static void st3(uint32_t* sm, const uint32_t (&a)[32], int tid) {
+    uint32_t* b = sm + tid * 33;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) b[c] = a[c];
+  }
+  __device__ __forceinline__ static void ld3(const uint32_t* sm, uint32_t (&a)[32], int tid) {
+    const uint32_t* b = sm + tid * 33;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a[c] = b[c];
+  }
+
+  // ---- P3 twiddles for stage s = LOGN-5+d: 2^d contiguous entries per thread ----
+  template <int D>
+  __device__ __forceinline__ static void tw3(const uint2* tw, int tid, uint2 (&w)[16]) {
+    const uint2* base = tw + (1 << (LOGN - 5 + D)) + (tid << D);
+    if constexpr (D == 0) {
+      w[0] = __ldg(base);
+    } else {
+      const uint4* b4 = reinterpret_cast<const uint4*>(base);
+#pragma unroll
+      for (int v = 0; v < (1 << (D - 1)); ++v) {
+        const uint4 x = __ldg(b4 + v);
+        w[2 * v] = make_uint2(x.x, x.y);
+        w[2 * v + 1] = make_uint2(x.z, x.w);
+      }
+    }
+  }
+
+  // =========================== forward ===========================
+  __device__ __forceinline__ static void fwd_p1(uint32_t (&a)[32], const uint2* tw, uint32_t q) {
+    const uint32_t q2 = 2 * q;
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const int tc = 16 >> s;
+      uint2 w[16];
+#pragma unroll
+      for (int g = 0; g < (1 << s); ++g) w[g] = __ldg(tw + (1 << s) + g);
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (!(c & tc)) ct_bfly(a[c], a[c + tc], w[c >> (5 - s)], q, q2);
+    }
+  }
+  __device__ __forceinline__ static void fwd_p2(uint32_t (&a)[32], const uint2* tw, int tid, uint32_t q) {
+    const uint32_t q2 = 2 * q;
+    const int warp = tid >> 5;
+#pragma unroll
+    for (int s = 5; s < 5 + M; ++s) {
+      const int tc = 1 << (LOGN - 6 - s);
+      const uint2* wb = tw + (1 << s) + (warp << (s + 10 - LOGN));
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (!(c & tc)) ct_bfly(a[c], a[c + tc], __ldg(wb + (fc2(c) >> (LOGN - s))), q, q2);
+    }
+  }
+  template <int D>
+  __device__ __forceinline__ static void fwd_p3_stage(uint32_t (&a)[32], const uint2* tw, int tid,
+                                                      uint32_t q, uint32_t q2) {
+    uint2 w[16];
+    tw3<D>(tw, tid, w);
+    const int tc = 16 >> D;
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (!(c & tc)) ct_bfly(a[c], a[c + tc], w[c >> (5 - D)], q, q2);
+  }
+  __device__ __forceinline__ static void fwd_p3(uint32_t (&a)[32], const uint2* tw, int tid, uint32_t q) {
+    const uint32_t q2 = 2 * q;
+    fwd_p3_stage<0>(a, tw, tid, q, q2);
+    fwd_p3_stage<1>(a, tw, tid, q, q2);
+    fwd_p3_stage<2>(a, tw, tid, q, q2);
+    fwd_p3_stage<3>(a, tw, tid, q, q2);
+    fwd_p3_stage<4>(a, tw, tid, q, q2);
+  }
+
+  // Full forward transform: a[] holds the row in P1 layout on entry and the
+  // lazily reduced ([0,4q)) result in P3 layout on exit.  `sm` needs
+  // SMEM_WORDS words; the caller syncs before reusing it.
+  __device__ __forceinline__ static void forward(uint32_t (&a)[32], uint32_t* sm, const uint2* tw,
+                                                 int tid, uint32_t q) {
+    fwd_p1(a, tw, q);
+    st1(sm, a, tid);
+    __syncthreads();
+    ld2(sm, a, tid);
+    fwd_p2(a, tw, tid, q);
+    __syncthreads();
+    st2(sm, a, tid);
+    __syncthreads();
+    ld3(sm, a, tid);
+    fwd_p3(a, tw, tid, q);
+  }
+
+  // =========================== inverse ===========================
+  template <int D>
+  __device__ __forceinline__ static void inv_p3_stage(uint32_t (&a)[32], const uint2* tw, int tid,
+                                                      uint32_t q, uint32_t q2) {
+    uint2 w[16];
+    tw3<D>(tw, tid, w);
+    const int tc = 16 >> D;
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (!(c & tc)) gs_bfly(a[c], a[c + tc], w[c >> (5 - D)], q, q2);
+  }
+  __device__ __forceinline__ static void inv_p3(uint32_t (&a)[32], const uint2* tw, int tid, uint32_t q) {
+    const uint32_t q2 = 2 * q;
+    inv_p3_stage<4>(a, tw, tid, q, q2);
+    inv_p3_stage<3>(a, tw, tid, q, q2);
+    inv_p3_stage<2>(a, tw, tid, q, q2);
+    inv_p3_stage<1>(a, tw, tid, q, q2);
+    inv_p3_stage<0>(a, tw, tid, q, q2);
+  }
+  __device__ __forceinline__ static void inv_p2(uint32_t (&a)[32], const uint2* tw, int tid, uint32_t q) {
+    const uint32_t q2 = 2 * q;
+    const int warp = tid >> 5;
+#pragma unroll
+    for (int ss = 0; ss < M; ++ss) {
+      const int s = 4 + M - ss;
+      const int tc = 1 << (LOGN - 6 - s);
+      const uint2* wb = tw + (1 << s) + (warp << (s + 10 - LOGN));
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (!(c & tc)) gs_bfly(a[c], a[c + tc], __ldg(wb + (fc2(c) >> (LOGN - s))), q, q2);
+    }
+  }
+  __device__ __forceinline__ static void inv_p1(uint32_t (&a)[32], const uint2* tw, uint32_t q) {
+    const uint32_t q2 = 2 * q;
+#pragma unroll
+    for (int ss = 0; ss < 5; ++ss) {
+      const int s = 4 - ss;
+      const int tc = 16 >> s;
+      uint2 w[16];
+#pragma unroll
+      for (int g = 0; g < (1 << s); ++g) w[g] = __ldg(tw + (1 << s) + g);
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (!(c & tc)) gs_bfly(a[c], a[c + tc], w[c >> (5 - s)], q, q2);
+    }
+  }
+
+  // Full inverse (without the N^-1 scaling): a[] in P3 layout with values in
+  // [0, 2q) on entry, P1 layout with values in [0, 2q) on exit.
+  __device__ __forceinline__ static void inverse(uint32_t (&a)[32], uint32_t* sm, const uint2* tw,
+                                                 int tid, uint32_t q) {
+    inv_p3(a, tw, tid, q);
+    st3(sm, a, tid);
+    __syncthreads();
+    ld2(sm, a, tid);
+    inv_p2(a, tw, tid, q);
+    __syncthreads();
+    st2(sm, a, tid);
+    __syncthreads();
+    ld1(sm, a, tid);
+    inv_p1(a, tw, q);
+  }
+
+  // ---- vectorised P3 global load/store (32 contiguous words per thread) ----
+  __device__ __forceinline__ static void gld3(const uint32_t* row, uint32_t (&a)[32], int tid) {
+    const uint4* p = reinterpret_cast<const uint4*>(row + (tid << 5));
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const uint4 x = __ldg(p + v);
+      a[4 * v] = x.x; a[4 * v + 1] = x.y; a[4 * v + 2] = x.z; a[4 * v + 3] = x.w;
+    }
+  }
+  __device__ __forceinline__ static void gst3(uint32_t* row, const uint32_t (&a)[32], int tid) {
+    uint4* p = reinterpret_cast<uint4*>(row + (tid << 5));
+#pragma unroll
+    for (int v = 0; v < 8; ++v) p[v] = make_uint4(a[4 * v], a[4 * v + 1], a[4 * v + 2], a[4 * v + 3]);
+  }
+  __device__ __forceinline__ static void gld1(const uint32_t* row, uint32_t (&a)[32], int tid) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a[c] = __ldg(row + tid + T * c);
+  }
+  __device__ __forceinline__ static void gst1(uint32_t* row, const uint32_t (&a)[32], int tid) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) row[tid + T * c] = a[c];
+  }
+};
+
+__device__ __forceinline__ uint32_t canon4(uint32_t x, uint32_t q) {  // [0,4q) -> [0,q)
+  x = min(x, x - 2 * q);
+  return min(x, x - q);
+}
+
+}  // namespace pb
+
+// Dispatch a templated launcher over LOGN in [11, 15].
+#define PB_DISPATCH_LOGN(logn, FN, ...)             \
+  do {                                              \
+    switch (logn) {                                 \
+      case 11: FN<11>(__VA_ARGS__); break;          \
+      case 12: FN<12>(__VA_ARGS__); break;          \
+      case 13: FN<13>(__VA_ARGS__); break;          \
+      case 14: FN<14>(__VA_ARGS__); break;          \
+      case 15: FN<15>(__VA_ARGS__); break;          \
+      default: break;                               \
+    }                                               \
+  } while (0)

@@ -1,0 +1,427 @@
+// pb_poly.cu — context, polynomial engine entry points (the sm_100a
+// replacements of the reference kernel tier K:31-199) and error plumbing.
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "pb_ntt.cuh"
+
+// ------------------------------------------------------------------ errors --
+static thread_local char g_err[512] = "";
+
+int pb_set_error(int code, const char* msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return code;
+}
+int pb_set_cuda_error(cudaError_t e) {
+  snprintf(g_err, sizeof(g_err), "CUDA error: %s", cudaGetErrorString(e));
+  return PB_ERR_CUDA;
+}
+
+extern "C" const char* pb_last_error(void) { return g_err; }
+extern "C" int pb_abi_version(void) { return PB_ABI_VERSION; }
+extern "C" int pb_device_sm_count(int* out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return pb_set_cuda_error(e);
+  e = cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return pb_set_cuda_error(e);
+  return PB_OK;
+}
+
+// --------------------------------------------------------- host mod arith --
+static uint64_t h_mulmod(uint64_t a, uint64_t b, uint64_t q) {
+  return (uint64_t)((unsigned __int128)a * b % q);
+}
+static uint64_t h_powmod(uint64_t a, uint64_t e, uint64_t q) {
+  uint64_t r = 1 % q;
+  a %= q;
+  while (e) {
+    if (e & 1) r = h_mulmod(r, a, q);
+    a = h_mulmod(a, a, q);
+    e >>= 1;
+  }
+  return r;
+}
+static uint32_t h_shoup(uint32_t w, uint32_t q) { return (uint32_t)(((uint64_t)w << 32) / q); }
+static uint32_t h_bitrev(uint32_t x, int bits) {
+  uint32_t r = 0;
+  for (int i = 0; i < bits; ++i) r |= ((x >> i) & 1u) << (bits - 1 - i);
+  return r;
+}
+
+// ------------------------------------------------------------------ context --
+extern "C" int pb_ctx_create(const pb_params* p, pb_ctx** out) {
+  if (!p || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  const int N = p->N, L = p->L;
+  int logN = 0;
+  while ((1 << logN) < N) ++logN;
+  if (N < 4 || N > 32768 || (1 << logN) != N) return pb_set_error(PB_ERR_PARAMS, "N must be a power of two in [4, 32768]");
+  if (L < 1 || L > PB_MAX_LIMBS) return pb_set_error(PB_ERR_PARAMS, "L must be in [1, 8]");
+  if (p->ell < 2 || p->ell > 62) return pb_set_error(PB_ERR_PARAMS, "ell must be in [2, 62]");
+  for (int i = 0; i < L; ++i) {
+    const uint64_t q = p->q[i];
+    if (q < 3 || q >= (1u << 30)) return pb_set_error(PB_ERR_PARAMS, "moduli must be < 2^30");
+    if ((q - 1) % (2ull * N) != 0) return pb_set_error(PB_ERR_PARAMS, "moduli must be 1 mod 2N");
+    if (h_powmod(p->psi[i], N, q) != q - 1) return pb_set_error(PB_ERR_PARAMS, "psi is not a primitive 2N-th root");
+  }
+  pb_ctx* c = new (std::nothrow) pb_ctx();
+  if (!c) return pb_set_error(PB_ERR_ARG, "out of host memory");
+  c->host = *p;
+  PbDev& d = c->dev;
+  memset(&d, 0, sizeof(d));
+  d.N = N; d.logN = logN; d.L = L; d.ell = p->ell;
+  d.t_mask = (p->ell >= 64) ? ~0ull : ((1ull << p->ell) - 1);
+  const uint64_t t = 1ull << p->ell;
+  for (int i = 0; i < L; ++i) {
+    const uint32_t q = p->q[i];
+    d.q[i] = q;
+    d.ninv[i] = (uint32_t)h_powmod(N, q - 2, q);
+    d.ninv_sh[i] = h_shoup(d.ninv[i], q);
+    d.delta[i] = p->delta_mod_q[i] % q;
+    d.delta_sh[i] = h_shoup(d.delta[i], q);
+    d.mu[i] = (uint64_t)(((unsigned __int128)1 << 64) / q);
+    d.inv_q32[i] = 4294967296.0 / (double)q;
+    d.tmod[i] = (uint32_t)(t % q);
+    d.pinv[i] = p->garner_prefix_inv[i] % q;
+    d.pinv_sh[i] = h_shoup(d.pinv[i], q);
+    uint64_t prod = 1;
+    for (int k = 0; k < PB_MAX_LIMBS; ++k) {
+      d.pmod[i][k] = (uint32_t)prod;
+      if (k < L) prod = h_mulmod(prod, p->q[k] % q, q);
+    }
+    d.sc_int[i] = p->scale_int[i];
+    d.sc_frac[i] = p->scale_frac[i];
+  }
+  // twiddle tables {w, shoup(w)}: psi^bitrev(i) and psi^-bitrev(i)  (K:22-29)
+  const size_t n_tw = (size_t)L * N;
+  uint2* h_f = (uint2*)malloc(n_tw * sizeof(uint2));
+  uint2* h_i = (uint2*)malloc(n_tw * sizeof(uint2));
+  uint64_t* pw = (uint64_t*)malloc((size_t)N * sizeof(uint64_t));
+  uint64_t* ipw = (uint64_t*)malloc((size_t)N * sizeof(uint64_t));
+  if (!h_f || !h_i || !pw || !ipw) {
+    free(h_f); free(h_i); free(pw); free(ipw); delete c;
+    return pb_set_error(PB_ERR_ARG, "out of host memory");
+  }
+  for (int l = 0; l < L; ++l) {
+    const uint64_t q = p->q[l], psi = p->psi[l] % q, ipsi = h_powmod(psi, q - 2, q);
+    uint64_t a = 1, b = 1;
+    for (int k = 0; k < N; ++k) {
+      pw[k] = a; ipw[k] = b;
+      a = h_mulmod(a, psi, q);
+      b = h_mulmod(b, ipsi, q);
+    }
+    for (int k = 0; k < N; ++k) {
+      const uint32_t br = h_bitrev((uint32_t)k, logN);
+      const uint32_t wf = (uint32_t)pw[br], wi = (uint32_t)ipw[br];
+      h_f[(size_t)l * N + k] = make_uint2(wf, h_shoup(wf, (uint32_t)q));
+      h_i[(size_t)l * N + k] = make_uint2(wi, h_shoup(wi, (uint32_t)q));
+    }
+  }
+  free(pw); free(ipw);
+  cudaError_t e = cudaMalloc(&c->d_tw_fwd, n_tw * sizeof(uint2));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_tw_inv, n_tw * sizeof(uint2));
+  if (e == cudaSuccess) e = cudaMemcpy(c->d_tw_fwd, h_f, n_tw * sizeof(uint2), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(c->d_tw_inv, h_i, n_tw * sizeof(uint2), cudaMemcpyHostToDevice);
+  free(h_f); free(h_i);
+  if (e != cudaSuccess) {
+    cudaFree(c->d_tw_fwd); cudaFree(c->d_tw_inv); delete c;
+    return pb_set_cuda_error(e);
+  }
+  d.tw_fwd = c->d_tw_fwd;
+  d.tw_inv = c->d_tw_inv;
+  *out = c;
+  return PB_OK;
+}
+
+extern "C" int pb_ctx_destroy(pb_ctx* c) {
+  if (!c) return PB_OK;
+  cudaFree(c->d_tw_fwd);
+  cudaFree(c->d_tw_inv);
+  delete c;
+  return PB_OK;
+}
+
+// ------------------------------------------------------------ NTT kernels --
+__device__ __forceinline__ int row_limb_of(const PbDev& P, const int32_t* row_limb, int64_t r) {
+  return row_limb ? row_limb[r] : (int)(r % P.L);
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5)) k_ntt_fwd(PbDev P, uint32_t* rows, int64_t n_rows,
+                                                           const int32_t* row_limb) {
+  using Nt = pb::Ntt<LOGN>;
+  extern __shared__ uint32_t sm[];
+  const int tid = threadIdx.x;
+  for (int64_t r = blockIdx.x; r < n_rows; r += gridDim.x) {
+    const int limb = row_limb_of(P, row_limb, r);
+    const uint32_t q = P.q[limb];
+    const uint2* tw = P.tw_fwd + (size_t)limb * Nt::N;
+    uint32_t* row = rows + r * Nt::N;
+    uint32_t a[32];
+    Nt::gld1(row, a, tid);
+    Nt::forward(a, sm, tw, tid, q);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a[c] = pb::canon4(a[c], q);
+    Nt::gst3(row, a, tid);
+    __syncthreads();
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5)) k_ntt_inv(PbDev P, uint32_t* rows, int64_t n_rows,
+                                                           const int32_t* row_limb) {
+  using Nt = pb::Ntt<LOGN>;
+  extern __shared__ uint32_t sm[];
+  const int tid = threadIdx.x;
+  for (int64_t r = blockIdx.x; r < n_rows; r += gridDim.x) {
+    const int limb = row_limb_of(P, row_limb, r);
+    const uint32_t q = P.q[limb];
+    const uint2* tw = P.tw_inv + (size_t)limb * Nt::N;
+    uint32_t* row = rows + r * Nt::N;
+    uint32_t a[32];
+    Nt::gld3(row, a, tid);
+    Nt::inverse(a, sm, tw, tid, q);
+    const uint32_t ni = P.ninv[limb], nis = P.ninv_sh[limb];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a[c] = mul_shoup(a[c], ni, nis, q);
+    Nt::gst1(row, a, tid);
+    __syncthreads();
+  }
+}
+
+// Small-N path (N <= 1024): one CTA per row, one radix-2 stage per barrier,
+// fully reduced arithmetic.  Used for tests / tiny parameter sets.
+__global__ void k_ntt_small(PbDev P, uint32_t* rows, int64_t n_rows, const int32_t* row_limb, int inverse) {
+  extern __shared__ uint32_t sm[];
+  const int N = P.N, logN = P.logN;
+  for (int64_t r = blockIdx.x; r < n_rows; r += gridDim.x) {
+    const int limb = row_limb_of(P, row_limb, r);
+    const uint32_t q = P.q[limb];
+    const uint2* tw = (inverse ? P.tw_inv : P.tw_fwd) + (size_t)limb * N;
+    uint32_t* row = rows + r * N;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) sm[j] = row[j];
+    __syncthreads();
+    for (int st = 0; st < logN; ++st) {
+      const int s = inverse ? (logN - 1 - st) : st;
+      const int t = N >> (s + 1);
+      for (int b = threadIdx.x; b < N / 2; b += blockDim.x) {
+        const int g = b / t, j = 2 * g * t + (b % t);
+        const uint2 w = tw[(1 << s) + g];
+        const uint32_t x = sm[j], y = sm[j + t];
+        if (!inverse) {
+          const uint32_t v = mul_shoup(y, w.x, w.y, q);
+          sm[j] = addmod(x, v, q);
+          sm[j + t] = submod(x, v, q);
+        } else {
+          sm[j] = addmod(x, y, q);
+          sm[j + t] = mul_shoup(submod(x, y, q), w.x, w.y, q);
+        }
+      }
+      __syncthreads();
+    }
+    for (int j = threadIdx.x; j < N; j += blockDim.x)
+      row[j] = inverse ? mul_shoup(sm[j], P.ninv[limb], P.ninv_sh[limb], q) : sm[j];
+    __syncthreads();
+  }
+}
+
+template <int LOGN>
+static void launch_ntt(const PbDev& P, uint32_t* rows, int64_t n_rows, const int32_t* row_limb,
+                       cudaStream_t st, bool inverse) {
+  using Nt = pb::Ntt<LOGN>;
+  const size_t smem = Nt::SMEM_WORDS * sizeof(uint32_t);
+  const int grid = (int)(n_rows < (1 << 30) ? n_rows : (1 << 30));
+  if (inverse) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_ntt_inv<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_ntt_inv<LOGN><<<grid, Nt::T, smem, st>>>(P, rows, n_rows, row_limb);
+  } else {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_ntt_fwd<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_ntt_fwd<LOGN><<<grid, Nt::T, smem, st>>>(P, rows, n_rows, row_limb);
+  }
+}
+
+static int ntt_entry(const pb_ctx* ctx, uint32_t* rows, int64_t n_rows, const int32_t* row_limb,
+                     void* stream, bool inverse) {
+  if (!ctx || (!rows && n_rows)) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n_rows <= 0) return PB_OK;
+  const PbDev& P = ctx->dev;
+  cudaStream_t st = pb_stream_of(stream);
+  if (P.logN >= 11) {
+    PB_DISPATCH_LOGN(P.logN, launch_ntt, P, rows, n_rows, row_limb, st, inverse);
+  } else {
+    const int grid = (int)(n_rows < (1 << 30) ? n_rows : (1 << 30));
+    const int thr = P.N / 2 < 32 ? 32 : (P.N / 2 > 512 ? 512 : P.N / 2);
+    k_ntt_small<<<grid, thr, P.N * sizeof(uint32_t), st>>>(P, rows, n_rows, row_limb, inverse ? 1 : 0);
+  }
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_ntt_forward(const pb_ctx* ctx, uint32_t* rows, int64_t n_rows, const int32_t* row_limb,
+                              void* stream) {
+  return ntt_entry(ctx, rows, n_rows, row_limb, stream, false);
+}
+extern "C" int pb_ntt_inverse(const pb_ctx* ctx, uint32_t* rows, int64_t n_rows, const int32_t* row_limb,
+                              void* stream) {
+  return ntt_entry(ctx, rows, n_rows, row_limb, stream, true);
+}
+
+// -------------------------------------------------------------- pointwise --
+// Semantics follow K:80-113 exactly, including uint64 wraparound of
+// (a + q - b) in pw_sub for non-canonical inputs.
+__global__ void k_pw(PbDev P, int op, uint32_t* out, const uint32_t* a, const uint32_t* b, int64_t n_rows,
+                     int64_t b_rows, const int32_t* row_limb) {
+  const int N = P.N;
+  const int64_t total = n_rows * (int64_t)N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / N;
+    const int j = (int)(e - r * N);
+    const int limb = row_limb_of(P, row_limb, r);
+    const uint32_t q = P.q[limb];
+    const uint64_t mu = P.mu[limb];
+    const uint64_t av = a[e];
+    const uint64_t bv = b[(r % b_rows) * N + j];
+    uint32_t res;
+    switch (op) {
+      case PB_PW_MUL: res = reduce64(av * bv, q, mu); break;
+      case PB_PW_MAC: {
+        const uint64_t prod = reduce64(av * bv, q, mu);
+        res = reduce64((uint64_t)out[e] + prod, q, mu);
+        break;
+      }
+      case PB_PW_ADD: res = reduce64(av + bv, q, mu); break;
+      default: res = reduce64(av + q - bv, q, mu); break;
+    }
+    out[e] = res;
+  }
+}
+
+extern "C" int pb_pw(const pb_ctx* ctx, int op, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                     int64_t n_rows, int64_t b_rows, const int32_t* row_limb, void* stream) {
+  if (!ctx || !out || !a || !b) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (op < 0 || op > 3) return pb_set_error(PB_ERR_ARG, "bad pointwise op");
+  if (n_rows <= 0) return PB_OK;
+  if (b_rows <= 0) return pb_set_error(PB_ERR_SHAPE, "b_rows must be positive");
+  const int64_t total = n_rows * (int64_t)ctx->dev.N;
+  k_pw<<<pb_grid_1d(total, 256), 256, 0, pb_stream_of(stream)>>>(ctx->dev, op, out, a, b, n_rows, b_rows, row_limb);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+// ----------------------------------------------------------------- decode --
+// K:158-179 garner_digits for one coefficient: x[i] at stride `xs`.
+__device__ __forceinline__ void garner(const PbDev& P, const uint32_t* x, int64_t xs, uint32_t (&d)[PB_MAXL]) {
+#pragma unroll
+  for (int i = 0; i < PB_MAXL; ++i) {
+    if (i < P.L) {
+      const uint32_t qi = P.q[i];
+      const uint64_t mu = P.mu[i];
+      uint32_t acc = 0;
+#pragma unroll
+      for (int k = 0; k < PB_MAXL; ++k)
+        if (k < i) acc = addmod(acc, mulmod(d[k], P.pmod[i][k], qi, mu), qi);
+      const uint32_t xv = reduce64(x[i * xs], qi, mu);
+      d[i] = mul_shoup(submod(xv, acc, qi), P.pinv[i], P.pinv_sh[i], qi);
+    }
+  }
+}
+
+// K:182-199 scale_round_digits for one coefficient (float64, same order, no FMA).
+__device__ __forceinline__ uint64_t scale_round(const PbDev& P, const uint32_t (&d)[PB_MAXL]) {
+  uint64_t acc_i = 0;
+  double acc_f = 0.0;
+#pragma unroll
+  for (int i = 0; i < PB_MAXL; ++i) {
+    if (i < P.L) {
+      acc_i += (uint64_t)d[i] * P.sc_int[i];
+      acc_f = __dadd_rn(acc_f, __dmul_rn((double)d[i], P.sc_frac[i]));
+    }
+  }
+  return (acc_i + (uint64_t)floor(__dadd_rn(acc_f, 0.5))) & P.t_mask;
+}
+
+__global__ void k_garner(PbDev P, const uint32_t* rows, int64_t n_polys, uint32_t* digits) {
+  const int N = P.N, L = P.L;
+  const int64_t total = n_polys * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / N;
+    const int j = (int)(e - p * N);
+    uint32_t d[PB_MAXL];
+    garner(P, rows + p * L * N + j, N, d);
+    for (int i = 0; i < L; ++i) digits[p * L * N + (int64_t)i * N + j] = d[i];
+  }
+}
+
+__global__ void k_scale_round(PbDev P, const uint32_t* digits, int64_t n_polys, uint64_t* out) {
+  const int N = P.N, L = P.L;
+  const int64_t total = n_polys * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / N;
+    const int j = (int)(e - p * N);
+    uint32_t d[PB_MAXL];
+#pragma unroll
+    for (int i = 0; i < PB_MAXL; ++i) d[i] = (i < L) ? digits[p * L * N + (int64_t)i * N + j] : 0u;
+    out[e] = scale_round(P, d);
+  }
+}
+
+__global__ void k_decode(PbDev P, const uint32_t* rows, int64_t n_polys, uint64_t* out) {
+  const int N = P.N, L = P.L;
+  const int64_t total = n_polys * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / N;
+    const int j = (int)(e - p * N);
+    uint32_t d[PB_MAXL];
+    garner(P, rows + p * L * N + j, N, d);
+    out[e] = scale_round(P, d);
+  }
+}
+
+extern "C" int pb_garner_digits(const pb_ctx* ctx, const uint32_t* rows, int64_t n_polys, uint32_t* digits,
+                                void* stream) {
+  if (!ctx || !rows || !digits) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n_polys <= 0) return PB_OK;
+  k_garner<<<pb_grid_1d(n_polys * ctx->dev.N, 256), 256, 0, pb_stream_of(stream)>>>(ctx->dev, rows, n_polys, digits);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+extern "C" int pb_scale_round_digits(const pb_ctx* ctx, const uint32_t* digits, int64_t n_polys, uint64_t* out,
+                                     void* stream) {
+  if (!ctx || !digits || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n_polys <= 0) return PB_OK;
+  k_scale_round<<<pb_grid_1d(n_polys * ctx->dev.N, 256), 256, 0, pb_stream_of(stream)>>>(ctx->dev, digits, n_polys, out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+extern "C" int pb_decode(const pb_ctx* ctx, const uint32_t* rows, int64_t n_polys, uint64_t* out, void* stream) {
+  if (!ctx || !rows || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n_polys <= 0) return PB_OK;
+  k_decode<<<pb_grid_1d(n_polys * ctx->dev.N, 256), 256, 0, pb_stream_of(stream)>>>(ctx->dev, rows, n_polys, out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+// ------------------------------------------------ negacyclic mod 2^64 (K:135)
+__global__ void k_negacyclic_wrap(const uint64_t* a, const uint64_t* b, int64_t n_pairs, int N, uint64_t* out) {
+  const int64_t total = n_pairs * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / N;
+    const int k = (int)(e - p * N);
+    const uint64_t* ap = a + p * N;
+    const uint64_t* bp = b + p * N;
+    uint64_t acc = 0;
+    for (int i = 0; i <= k; ++i) acc += ap[i] * bp[k - i];
+    for (int i = k + 1; i < N; ++i) acc -= ap[i] * bp[k + N - i];
+    out[e] = acc;
+  }
+}
+
+extern "C" int pb_negacyclic_mul_wrap(const uint64_t* a, const uint64_t* b, int64_t n_pairs, int32_t N,
+                                      uint64_t* out, void* stream) {
+  if (!a || !b || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n_pairs <= 0 || N <= 0) return PB_OK;
+  k_negacyclic_wrap<<<pb_grid_1d(n_pairs * N, 128), 128, 0, pb_stream_of(stream)>>>(a, b, n_pairs, N, out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}

@@ -1,0 +1,384 @@
+// pb_ring.cu — share arithmetic over Z_{2^ell} (R:93-233), the ring GEMM /
+// convolution kernels (K:206-278), the numpy-identical Philox share RNG
+// (R:48-61) and the dealer-assisted non-linear steps.
+//
+// Elementwise kernels move 128-bit vectors (two u64 per lane access) and
+// use grid-stride loops sized to a multiple of the SM count.
+#include <math.h>
+
+#include "pb_common.cuh"
+
+namespace {
+
+__device__ __forceinline__ uint64_t ring_mask(int ell) { return ell >= 64 ? ~0ull : ((1ull << ell) - 1); }
+
+__device__ __forceinline__ int64_t to_signed(uint64_t v, int ell) {  // R:194-198
+  const uint64_t m = ring_mask(ell);
+  v &= m;
+  const uint64_t half = 1ull << (ell - 1);
+  return (v >= half) ? (int64_t)(v - m - 1) : (int64_t)v;
+}
+
+__global__ void k_ring_binary(int op, uint64_t* out, const uint64_t* a, const uint64_t* b, int64_t n, int64_t bn,
+                              int ell) {
+  const uint64_t m = ring_mask(ell);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = a[i], y = b[bn == n ? i : i % bn];
+    uint64_t r;
+    switch (op) {
+      case PB_RING_ADD: r = x + y; break;
+      case PB_RING_SUB: r = x - y; break;
+      default: r = x * y; break;
+    }
+    out[i] = r & m;
+  }
+}
+
+__global__ void k_ring_unary(int op, uint64_t* out, const uint64_t* a, uint64_t k, int64_t n, int ell) {
+  const uint64_t m = ring_mask(ell);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = a[i];
+    uint64_t r;
+    switch (op) {
+      case PB_RING_NEG: r = 0ull - x; break;
+      case PB_RING_SCALAR_MUL: r = x * (k & m); break;
+      case PB_RING_MASK: r = x; break;
+      default: r = (uint64_t)(to_signed(x, ell) >> (int)k); break;  // arith shift
+    }
+    out[i] = r & m;
+  }
+}
+
+// R:174-182: floor(x * 2^scale) as two's complement mod 2^ell.
+__global__ void k_encode_fixed(const double* x, int64_t n, int ell, int scale, uint64_t* out, int32_t* flag) {
+  const double limit = ldexp(1.0, ell - 1) / ldexp(1.0, scale);
+  const double s = ldexp(1.0, scale);
+  const uint64_t m = ring_mask(ell);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    if (!(fabs(v) < limit)) {
+      if (flag) atomicExch(flag, 1);
+      out[i] = 0;
+      continue;
+    }
+    const int64_t f = (int64_t)floor(__dmul_rn(v, s));
+    out[i] = (uint64_t)f & m;
+  }
+}
+
+// R:185-191
+__global__ void k_decode_fixed(const uint64_t* v, int64_t n, int ell, int scale, double* out) {
+  const double s = ldexp(1.0, scale);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __ddiv_rn((double)to_signed(v[i], ell), s);
+}
+
+// R:60-61 uniform_ring == raw >> (64 - ell) (Lemire with a power-of-two
+// range never rejects).  Each thread produces one Philox block (4 raw words).
+__global__ void k_uniform_ring(uint64_t* out, const uint64_t* x, uint64_t* do_out, int64_t n, uint64_t seed,
+                               uint64_t stream_id, uint64_t off, int ell) {
+  const int shift = 64 - ell;
+  const uint64_t m = ring_mask(ell);
+  const uint64_t first_blk = off >> 2;
+  const int64_t nblk = (int64_t)(((off + n + 3) >> 2) - first_blk);
+  for (int64_t bi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; bi < nblk; bi += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t blk = first_blk + bi;
+    const u64x4 r = philox4x64_10(blk + 1, 0, 0, 0, seed, stream_id);
+#pragma unroll
+    for (int lane = 0; lane < 4; ++lane) {
+      const uint64_t raw_idx = blk * 4 + lane;
+      if (raw_idx < off || raw_idx >= off + (uint64_t)n) continue;
+      const int64_t i = (int64_t)(raw_idx - off);
+      const uint64_t v = r.v[lane] >> shift;
+      out[i] = v;
+      if (do_out) do_out[i] = (x[i] - v) & m;
+    }
+  }
+}
+
+// K:206-218 ring GEMM with uint64 wraparound, 16x16 smem tiles.
+template <int TS>
+__global__ void k_ring_matmul(const uint64_t* __restrict__ A, const uint64_t* __restrict__ B, int64_t n, int64_t k,
+                              int64_t m, int ta, int tb, uint64_t mask, uint64_t* __restrict__ C) {
+  __shared__ uint64_t sa[TS][TS + 1];
+  __shared__ uint64_t sb[TS][TS + 1];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t row = (int64_t)blockIdx.y * TS + ty;
+  const int64_t col = (int64_t)blockIdx.x * TS + tx;
+  uint64_t acc = 0;
+  for (int64_t k0 = 0; k0 < k; k0 += TS) {
+    const int64_t ak = k0 + tx, bk = k0 + ty;
+    sa[ty][tx] = (row < n && ak < k) ? (ta ? A[ak * n + row] : A[row * k + ak]) : 0ull;
+    sb[ty][tx] = (bk < k && col < m) ? (tb ? B[col * k + bk] : B[bk * m + col]) : 0ull;
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TS; ++kk) acc += sa[ty][kk] * sb[kk][tx];
+    __syncthreads();
+  }
+  if (row < n && col < m) C[row * m + col] = acc & mask;
+}
+
+__global__ void k_rowsum(const uint64_t* a, int64_t rows, int64_t cols, uint64_t mask, uint64_t* out) {
+  const int64_t r = blockIdx.x;
+  uint64_t acc = 0;
+  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) acc += a[r * cols + j];
+  __shared__ uint64_t red[256];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[r] = red[0] & mask;
+}
+
+// K:221-238 im2col (gather form: one thread per output element).
+__global__ void k_im2col(const uint64_t* x, int B, int C, int H, int W, int s, int stride, uint64_t* out) {
+  const int oh = (H - s) / stride + 1, ow = (W - s) / stride + 1;
+  const int64_t ncol = (int64_t)B * oh * ow;
+  const int64_t total = ncol * C * s * s;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / ncol, col = e - row * ncol;
+    const int dj = (int)(row % s), di = (int)((row / s) % s), c = (int)(row / (s * s));
+    const int j = (int)(col % ow), i = (int)((col / ow) % oh), b = (int)(col / ((int64_t)oh * ow));
+    out[e] = x[(((int64_t)b * C + c) * H + i * stride + di) * W + j * stride + dj];
+  }
+}
+
+// K:241-257 col2im (gather form of the scatter-add: each output pixel sums
+// the patch entries that map onto it, so no atomics are needed).
+__global__ void k_col2im(const uint64_t* cols, int B, int C, int H, int W, int s, int stride, uint64_t* out) {
+  const int oh = (H - s) / stride + 1, ow = (W - s) / stride + 1;
+  const int64_t ncol = (int64_t)B * oh * ow;
+  const int64_t total = (int64_t)B * C * H * W;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int xw = (int)(e % W), xh = (int)((e / W) % H), c = (int)((e / ((int64_t)W * H)) % C);
+    const int b = (int)(e / ((int64_t)W * H * C));
+    uint64_t acc = 0;
+    for (int di = 0; di < s; ++di) {
+      const int ii = xh - di;
+      if (ii < 0 || ii % stride) continue;
+      const int i = ii / stride;
+      if (i >= oh) continue;
+      for (int dj = 0; dj < s; ++dj) {
+        const int jj = xw - dj;
+        if (jj < 0 || jj % stride) continue;
+        const int j = jj / stride;
+        if (j >= ow) continue;
+        const int64_t row = ((int64_t)c * s + di) * s + dj;
+        const int64_t col = ((int64_t)b * oh + i) * ow + j;
+        acc += cols[row * ncol + col];
+      }
+    }
+    out[e] = acc;
+  }
+}
+
+// K:260-278 conv2d_wrap (valid, stride 1).
+__global__ void k_conv2d(const uint64_t* x, const uint64_t* w, int B, int Ci, int H, int W, int Co, int s, uint64_t mask,
+                         uint64_t* out) {
+  const int oh = H - s + 1, ow = W - s + 1;
+  const int64_t total = (int64_t)B * Co * oh * ow;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e % ow), i = (int)((e / ow) % oh), co = (int)((e / ((int64_t)ow * oh)) % Co);
+    const int b = (int)(e / ((int64_t)ow * oh * Co));
+    uint64_t acc = 0;
+    for (int ci = 0; ci < Ci; ++ci)
+      for (int di = 0; di < s; ++di)
+        for (int dj = 0; dj < s; ++dj)
+          acc += x[(((int64_t)b * Ci + ci) * H + i + di) * W + j + dj] * w[(((int64_t)co * Ci + ci) * s + di) * s + dj];
+    out[e] = acc & mask;
+  }
+}
+
+// Dealer-assisted non-linear step: reconstruct, apply, reshare with the
+// numpy-identical uniform_ring stream (so oracle and device shares agree).
+__global__ void k_dealer(int op, uint64_t* mo, uint64_t* dov, int64_t n, int k, const uint8_t* d_in, uint8_t* d_out,
+                         uint64_t seed, uint64_t stream_id, uint64_t off, int ell) {
+  const uint64_t m = ring_mask(ell);
+  const int shift = 64 - ell;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = (mo[i] + dov[i]) & m;
+    uint64_t y;
+    switch (op) {
+      case PB_DEALER_RELU: {
+        const bool pos = to_signed(x, ell) >= 0;
+        if (d_out) d_out[i] = pos ? 1 : 0;
+        y = pos ? x : 0ull;
+        break;
+      }
+      case PB_DEALER_TRUNC: y = (uint64_t)(to_signed(x, ell) >> k) & m; break;
+      case PB_DEALER_SELECT: y = d_in[i] ? x : 0ull; break;
+      default: y = x; break;
+    }
+    const uint64_t r = philox_np_raw(seed, stream_id, off + (uint64_t)i) >> shift;
+    mo[i] = r;
+    dov[i] = (y - r) & m;
+  }
+}
+
+__global__ void k_sgd(double* w, double* v, const uint64_t* g, int64_t n, int gscale, double lr, double mom, int ell,
+                      int wscale, uint64_t* w_ring, int32_t* flag) {
+  const double gs = ldexp(1.0, gscale), ws = ldexp(1.0, wscale);
+  const double limit = ldexp(1.0, ell - 1) / ws;
+  const uint64_t m = ring_mask(ell);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double gi = __ddiv_rn((double)to_signed(g[i], ell), gs);
+    const double vi = __dadd_rn(__dmul_rn(mom, v[i]), gi);
+    const double wi = __dsub_rn(w[i], __dmul_rn(lr, vi));
+    v[i] = vi;
+    w[i] = wi;
+    if (!(fabs(wi) < limit)) {
+      if (flag) atomicExch(flag, 1);
+      w_ring[i] = 0;
+    } else {
+      w_ring[i] = (uint64_t)(int64_t)floor(__dmul_rn(wi, ws)) & m;
+    }
+  }
+}
+
+bool bad_ell(int ell) { return ell < 2 || ell > 64; }
+
+}  // namespace
+
+// ================================================================ C ABI ===
+#define RING_GRID(n) pb_grid_1d((n), 256), 256, 0, pb_stream_of(stream)
+
+extern "C" int pb_ring_binary(int op, uint64_t* out, const uint64_t* a, const uint64_t* b, int64_t n, int64_t b_n,
+                              int32_t ell, void* stream) {
+  if (!out || !a || !b) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (op < PB_RING_ADD || op > PB_RING_MUL || bad_ell(ell)) return pb_set_error(PB_ERR_ARG, "bad ring op / ell");
+  if (n <= 0) return PB_OK;
+  if (b_n <= 0 || n % b_n) return pb_set_error(PB_ERR_SHAPE, "broadcast size must divide n");
+  k_ring_binary<<<RING_GRID(n)>>>(op, out, a, b, n, b_n, ell);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_ring_unary(int op, uint64_t* out, const uint64_t* a, uint64_t k, int64_t n, int32_t ell, void* stream) {
+  if (!out || !a) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (op < PB_RING_NEG || op > PB_RING_ARITH_SHIFT || bad_ell(ell)) return pb_set_error(PB_ERR_ARG, "bad ring op / ell");
+  if (op == PB_RING_ARITH_SHIFT && k >= 64) return pb_set_error(PB_ERR_ARG, "shift too large");
+  if (n <= 0) return PB_OK;
+  k_ring_unary<<<RING_GRID(n)>>>(op, out, a, k, n, ell);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_encode_fixed(const double* x, int64_t n, int32_t ell, int32_t scale, uint64_t* out, int32_t* flag,
+                               void* stream) {
+  if (!x || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (bad_ell(ell) || scale < 0 || scale >= ell) return pb_set_error(PB_ERR_SCALE, "bad scale");
+  if (n <= 0) return PB_OK;
+  k_encode_fixed<<<RING_GRID(n)>>>(x, n, ell, scale, out, flag);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_decode_fixed(const uint64_t* v, int64_t n, int32_t ell, int32_t scale, double* out, void* stream) {
+  if (!v || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (bad_ell(ell) || scale < 0 || scale >= ell) return pb_set_error(PB_ERR_SCALE, "bad scale");
+  if (n <= 0) return PB_OK;
+  k_decode_fixed<<<RING_GRID(n)>>>(v, n, ell, scale, out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_uniform_ring(uint64_t* out, int64_t n, uint64_t seed, uint64_t stream_id, uint64_t raw_offset,
+                               int32_t ell, void* stream) {
+  if (!out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (ell < 1 || ell > 63) return pb_set_error(PB_ERR_ARG, "bad ell");
+  if (n <= 0) return PB_OK;
+  k_uniform_ring<<<RING_GRID((n + 3) / 4 + 1)>>>(out, nullptr, nullptr, n, seed, stream_id, raw_offset, ell);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_share(const uint64_t* x, int64_t n, uint64_t seed, uint64_t stream_id, uint64_t raw_offset,
+                        int32_t ell, uint64_t* mo_out, uint64_t* do_out, void* stream) {
+  if (!x || !mo_out || !do_out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (ell < 1 || ell > 63) return pb_set_error(PB_ERR_ARG, "bad ell");
+  if (n <= 0) return PB_OK;
+  k_uniform_ring<<<RING_GRID((n + 3) / 4 + 1)>>>(mo_out, x, do_out, n, seed, stream_id, raw_offset, ell);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m, int trans_a,
+                              int trans_b, int32_t ell, uint64_t* out, void* stream) {
+  if (!a || !b || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n <= 0 || m <= 0) return PB_OK;
+  if (k < 0 || n > (1ll << 31) || m > (1ll << 31)) return pb_set_error(PB_ERR_SHAPE, "bad matmul shape");
+  const uint64_t mask = (ell >= 64 || ell <= 0) ? ~0ull : ((1ull << ell) - 1);
+  dim3 blk(16, 16), grd((unsigned)((m + 15) / 16), (unsigned)((n + 15) / 16));
+  k_ring_matmul<16><<<grd, blk, 0, pb_stream_of(stream)>>>(a, b, n, k, m, trans_a, trans_b, mask, out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_ring_rowsum(const uint64_t* a, int64_t rows, int64_t cols, int32_t ell, uint64_t* out, void* stream) {
+  if (!a || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (rows <= 0) return PB_OK;
+  const uint64_t mask = (ell >= 64 || ell <= 0) ? ~0ull : ((1ull << ell) - 1);
+  k_rowsum<<<(unsigned)rows, 256, 0, pb_stream_of(stream)>>>(a, rows, cols, mask, out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_im2col(const uint64_t* x, int32_t B, int32_t C, int32_t H, int32_t W, int32_t s, int32_t stride,
+                         uint64_t* out, void* stream) {
+  if (!x || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (s < 1 || stride < 1 || s > H || s > W) return pb_set_error(PB_ERR_GEOMETRY, "bad im2col geometry");
+  const int64_t total = (int64_t)B * ((H - s) / stride + 1) * ((W - s) / stride + 1) * C * s * s;
+  if (total <= 0) return PB_OK;
+  k_im2col<<<RING_GRID(total)>>>(x, B, C, H, W, s, stride, out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_col2im(const uint64_t* cols, int32_t B, int32_t C, int32_t H, int32_t W, int32_t s, int32_t stride,
+                         uint64_t* out, void* stream) {
+  if (!cols || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (s < 1 || stride < 1 || s > H || s > W) return pb_set_error(PB_ERR_GEOMETRY, "bad col2im geometry");
+  const int64_t total = (int64_t)B * C * H * W;
+  if (total <= 0) return PB_OK;
+  k_col2im<<<RING_GRID(total)>>>(cols, B, C, H, W, s, stride, out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_conv2d(const uint64_t* x, const uint64_t* w, int32_t B, int32_t Ci, int32_t H, int32_t W, int32_t Co,
+                         int32_t s, int32_t ell, uint64_t* out, void* stream) {
+  if (!x || !w || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (s < 1 || s > H || s > W) return pb_set_error(PB_ERR_GEOMETRY, "bad conv geometry");
+  const int64_t total = (int64_t)B * Co * (H - s + 1) * (W - s + 1);
+  if (total <= 0) return PB_OK;
+  const uint64_t mask = (ell >= 64 || ell <= 0) ? ~0ull : ((1ull << ell) - 1);
+  k_conv2d<<<RING_GRID(total)>>>(x, w, B, Ci, H, W, Co, s, mask, out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_dealer_op(int op, uint64_t* mo, uint64_t* do_, int64_t n, int32_t k, const uint8_t* d_in,
+                            uint8_t* d_out, uint64_t seed, uint64_t stream_id, uint64_t raw_offset, int32_t ell,
+                            void* stream) {
+  if (!mo || !do_) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (op < PB_DEALER_RELU || op > PB_DEALER_RESHARE) return pb_set_error(PB_ERR_ARG, "bad dealer op");
+  if (op == PB_DEALER_SELECT && !d_in) return pb_set_error(PB_ERR_ARG, "select needs d_in");
+  if (ell < 2 || ell > 63 || k < 0 || k >= ell) return pb_set_error(PB_ERR_ARG, "bad ell / shift");
+  if (n <= 0) return PB_OK;
+  k_dealer<<<RING_GRID(n)>>>(op, mo, do_, n, k, d_in, d_out, seed, stream_id, raw_offset, ell);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_sgd_momentum(double* w, double* v, const uint64_t* grad_ring, int64_t n, int32_t grad_scale, double lr,
+                               double momentum, int32_t ell, int32_t w_scale, uint64_t* w_ring, int32_t* range_flag,
+                               void* stream) {
+  if (!w || !v || !grad_ring || !w_ring) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (bad_ell(ell)) return pb_set_error(PB_ERR_ARG, "bad ell");
+  if (n <= 0) return PB_OK;
+  k_sgd<<<RING_GRID(n)>>>(w, v, grad_ring, n, grad_scale, lr, momentum, ell, w_scale, w_ring, range_flag);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}

@@ -1,0 +1,126 @@
+"""Kernel-level parity: the sm_100a engine vs the CPU oracle (K restated),
+bit-exact on identical inputs and tables (SURVEY §8c parity definition i)."""
+
+import numpy as np
+import pytest
+
+from oracle import kernels as OK
+from oracle.params import make_params
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def kc():
+    from paper_2403_11166_b200 import kernels_compat
+
+    return kernels_compat
+
+
+def _rows(p, P, seed):
+    rng = np.random.default_rng(seed)
+    return np.ascontiguousarray(
+        np.stack([np.stack([rng.integers(0, q, size=p.N, dtype=np.uint64) for q in p.moduli]) for _ in range(P)])
+        .reshape(P * p.L, p.N)
+    )
+
+
+@pytest.mark.parametrize("N,L", [(16, 2), (64, 3), (1024, 2), (2048, 2), (4096, 3), (8192, 7), (16384, 4), (32768, 8)])
+def test_ntt_forward_inverse_bit_exact(kc, N, L):
+    p = make_params(N, L)
+    tb = p.tables
+    P = 3
+    rows = _rows(p, P, N + L)
+    q = np.tile(tb["q"], P)
+    psi = np.ascontiguousarray(np.tile(tb["psi_brv"], (P, 1)))
+    ipsi = np.ascontiguousarray(np.tile(tb["ipsi_brv"], (P, 1)))
+    ninv = np.tile(tb["n_inv"], P)
+    want = rows.copy()
+    OK.ntt_forward_cyc(want, tb["psi_brv"], tb["q"])
+    got = rows.copy()
+    kc.ntt_forward(got, psi, q)
+    assert np.array_equal(got, want)
+    want_i = rows.copy()
+    OK.ntt_inverse_cyc(want_i, tb["ipsi_brv"], tb["n_inv"], tb["q"])
+    got_i = rows.copy()
+    kc.ntt_inverse(got_i, ipsi, ninv, q)
+    assert np.array_equal(got_i, want_i)
+    # round trip
+    kc.ntt_inverse(got, ipsi, ninv, q)
+    assert np.array_equal(got, rows)
+
+
+def test_ntt_edge_values(kc):
+    """All-zero, all-(q-1) and delta rows (maximal lazy-reduction pressure)."""
+    p = make_params(8192, 2)
+    tb = p.tables
+    rows = np.zeros((6, p.N), dtype=np.uint64)
+    rows[2] = tb["q"][0] - 1
+    rows[3] = tb["q"][1] - 1
+    rows[4, 0] = 1
+    rows[5, -1] = tb["q"][1] - 1
+    q = np.tile(tb["q"], 3)
+    want = rows.copy()
+    OK.ntt_forward_cyc(want, tb["psi_brv"], tb["q"])
+    got = rows.copy()
+    kc.ntt_forward(got, np.ascontiguousarray(np.tile(tb["psi_brv"], (3, 1))), q)
+    assert np.array_equal(got, want)
+
+
+def test_spec_ntt_example_small_n(kc, golden):
+    g = golden["kernels"]
+    for N, L in ((16, 2), (256, 3), (2048, 2), (8192, 1)):
+        tb = make_params(N, L).tables
+        rows = g[f"ntt_{N}_{L}_in"].copy()
+        P = rows.shape[0] // L
+        kc.ntt_forward(rows, np.ascontiguousarray(np.tile(tb["psi_brv"], (P, 1))), np.tile(tb["q"], P))
+        assert np.array_equal(rows, g[f"ntt_{N}_{L}_fwd"])
+
+
+@pytest.mark.parametrize("N,L", [(2048, 2), (8192, 7)])
+def test_pointwise_bit_exact(kc, N, L):
+    p = make_params(N, L)
+    tb = p.tables
+    P = 2
+    a = _rows(p, P, 1)
+    b = _rows(p, P, 2)
+    o0 = _rows(p, P, 3)
+    q = np.tile(tb["q"], P)
+    for fn_o, fn_g in ((OK.pw_mul, kc.pw_mul), (OK.pw_mul_acc, kc.pw_mul_acc), (OK.pw_add, kc.pw_add),
+                       (OK.pw_sub, kc.pw_sub)):
+        w = o0.copy()
+        fn_o(w, a, b, q)
+        g = o0.copy()
+        fn_g(g, a, b, q)
+        assert np.array_equal(g, w), fn_o.__name__
+
+
+@pytest.mark.parametrize("N,L", [(256, 3), (1024, 7)])
+def test_decode_bit_exact(kc, golden, N, L):
+    g = golden["kernels"]
+    tb = make_params(N, L).tables
+    d = kc.garner_digits(g[f"dec_{N}_{L}_in"], tb["q"], tb["prefix_inv"])
+    assert np.array_equal(d, g[f"dec_{N}_{L}_digits"])
+    m = kc.scale_round_digits(d, tb["int_part"], tb["frac_part"], np.uint64((1 << 59) - 1), q=tb["q"])
+    assert np.array_equal(m, g[f"dec_{N}_{L}_m"])
+
+
+def test_ring_kernels_bit_exact(kc, golden):
+    g = golden["kernels"]
+    assert np.array_equal(kc.negacyclic_mul_wrap(g["negwrap_a"], g["negwrap_b"]), g["negwrap"])
+    assert np.array_equal(kc.matmul_wrap(g["mm_a"], g["mm_b"]), g["mm"])
+    assert np.array_equal(kc.conv2d_wrap(g["conv_x"], g["conv_w"]), g["conv"])
+    assert np.array_equal(kc.im2col_wrap(g["conv_x"], 3, 2), g["im2col_s3_st2"])
+    cols = OK.im2col_wrap(g["conv_x"], 3, 1)
+    assert np.array_equal(kc.col2im_wrap(cols, 2, 3, 7, 6, 3, 1), g["col2im_s3_st1"])
+    qm = np.uint64(1073692673)
+    # NTT-based negacyclic product mod q equals the schoolbook oracle
+    a, b = g["negwrap_a"] % qm, g["negwrap_b"] % qm
+    assert np.array_equal(kc.negacyclic_mul_mod(a, b, int(qm)), g["negmod"])
+
+
+def test_large_matmul(kc):
+    rng = np.random.default_rng(5)
+    a = rng.integers(0, 1 << 63, size=(128, 784), dtype=np.uint64)
+    b = rng.integers(0, 1 << 63, size=(784, 64), dtype=np.uint64)
+    assert np.array_equal(kc.matmul_wrap(a, b), OK.matmul_wrap(a, b))
