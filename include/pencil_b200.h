@@ -80,12 +80,23 @@ int pb_ctx_destroy(pb_ctx* ctx);
 /* ------------------------------------------------ polynomial engine (K) --- */
 /* Row r of `rows` uses limb row_limb[r] (or r % L when row_limb == NULL). */
 
-/* K:31-50 ntt_forward: in place, natural -> bit-reversed order. */
+/* NTT-domain rows are kept in DEVICE ORDER: bit-reversed index j = 32*t + 4*v + k
+ * (t < N/32, v < 8, k < 4) lives at address v*(N/8) + 4*t + k, which lets the
+ * register-blocked NTT move whole rows with coalesced 128-bit accesses.  All
+ * NTT-domain operands (ciphertexts, plaintexts, keys) share this order, so
+ * pointwise products are unaffected.  N < 2048 uses the reference order. */
+
+/* K:31-50 ntt_forward: in place, natural -> bit-reversed (device order). */
 int pb_ntt_forward(const pb_ctx* ctx, uint32_t* rows, int64_t n_rows, const int32_t* row_limb,
                    void* stream);
 /* K:53-77 ntt_inverse: in place, bit-reversed -> natural, includes x N^-1. */
 int pb_ntt_inverse(const pb_ctx* ctx, uint32_t* rows, int64_t n_rows, const int32_t* row_limb,
                    void* stream);
+
+/* Convert NTT-domain rows between device order (to_device=1 from reference
+ * bit-reversed order, to_device=0 back).  K-compat callers use this to see
+ * exactly K's output order. */
+int pb_ntt_reorder(const pb_ctx* ctx, uint32_t* rows, int64_t n_rows, int to_device, void* stream);
 
 /* K:80-113 pointwise ops.  op: 0 pw_mul, 1 pw_mul_acc (out += a*b), 2 pw_add,
  * 3 pw_sub.  Row r of b is b[r % b_rows] (b_rows == n_rows: plain). */

@@ -49,6 +49,7 @@ SIGNATURES = {
     "pb_ctx_destroy": [P],
     "pb_ntt_forward": [P, P, I64, P, P],
     "pb_ntt_inverse": [P, P, I64, P, P],
+    "pb_ntt_reorder": [P, P, I64, INT, P],
     "pb_pw": [P, INT, P, P, P, I64, I64, P, P],
     "pb_garner_digits": [P, P, I64, P, P],
     "pb_scale_round_digits": [P, P, I64, P, P],

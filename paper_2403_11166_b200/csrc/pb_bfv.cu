@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
 #pragma unroll
   for (int c = 0; c < 32; ++c)
     a[c] = lift_centered(coeff_val(vals, src_map, p, Nt::N, Nt::j1(tid, c)), P.ell, q, P.mu[l], P.tmod[l]);
-  Nt::forward(a, sm, P.tw_fwd + (size_t)l * Nt::N, tid, q);
+  Nt::forward(a, sm, P.tw_fwd + (size_t)l * Nt::N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
   uint32_t* row = pt + (p * L + l) * Nt::N;
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = pb::canon4(a[c], q);
@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   const uint32_t q = P.q[l];
   const uint64_t mu = P.mu[l];
   const uint2* tw = P.tw_fwd + (size_t)l * N;
+  const uint2* t3 = P.tw3_fwd + (size_t)l * P.tw3_stride;
   const int8_t* up = u + p * N;
   const int8_t* e1p = e1 + p * N;
   const int8_t* e2p = e2 + p * N;
@@ -120,12 +121,12 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   uint32_t U[32], b[32], k[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) U[c] = lift_small(up[Nt::j1(tid, c)], q);
-  Nt::forward(U, sm, tw, tid, q);
+  Nt::forward(U, sm, tw, t3, tid, q);
   __syncthreads();
   // c1 = pk1 * U + NTT(e2)
 #pragma unroll
   for (int c = 0; c < 32; ++c) b[c] = lift_small(e2p[Nt::j1(tid, c)], q);
-  Nt::forward(b, sm, tw, tid, q);
+  Nt::forward(b, sm, tw, t3, tid, q);
   Nt::gld3(pk + ((size_t)1 * L + l) * N, k, tid);
 #pragma unroll
   for (int c = 0; c < 32; ++c) b[c] = addmod(mulmod(k[c], U[c], q, mu), pb::canon4(b[c], q), q);
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
     const int j = Nt::j1(tid, c);
     b[c] = addmod(lift_small(e1p[j], q), delta_m(P, l, coeff_val(vals, src_map, p, N, j)), q);
   }
-  Nt::forward(b, sm, tw, tid, q);
+  Nt::forward(b, sm, tw, t3, tid, q);
   Nt::gld3(pk + (size_t)l * N, k, tid);
 #pragma unroll
   for (int c = 0; c < 32; ++c) b[c] = addmod(mulmod(k[c], U[c], q, mu), pb::canon4(b[c], q), q);
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
     const int j = Nt::j1(tid, c);
     b[c] = addmod(lift_small(ep[j], q), delta_m(P, l, coeff_val(vals, src_map, p, N, j)), q);
   }
-  Nt::forward(b, sm, P.tw_fwd + (size_t)l * N, tid, q);
+  Nt::forward(b, sm, P.tw_fwd + (size_t)l * N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
   if (a_in) {
     Nt::gld3(a_in + (p * L + l) * N, a, tid);
   } else {
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   Nt::gld3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = addmod(a[c], b[c], q);
-  Nt::inverse(a, sm, P.tw_inv + (size_t)l * N, tid, q);
+  Nt::inverse(a, sm, P.tw_inv + (size_t)l * N, P.tw3_inv + (size_t)l * P.tw3_stride, tid, q);
   const uint32_t ni = P.ninv[l], nis = P.ninv_sh[l];
   if (mode == 0) {
 #pragma unroll
@@ -328,37 +329,39 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   uint32_t m[32];
   Nt::ld1(sm, m, tid);
   __syncthreads();
-  Nt::forward(m, sm, P.tw_fwd + (size_t)l * N, tid, q);
+  Nt::forward(m, sm, P.tw_fwd + (size_t)l * N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
 
-  // 2. MAC over the K (ct, pt) terms in P3 layout.
-  uint32_t acc0[32], acc1[32];
+  // 2. MAC over the K (ct, pt) terms, one 128-bit device-order vector at a
+  //    time (P3 register v <-> uint4 #(v*T + tid) of the row), then
+  //    subtract the mask and store.
+  const size_t rowoff = (size_t)l * N;
+  uint4* o0 = reinterpret_cast<uint4*>(ct_out + ((size_t)p * 2 + 0) * L * N + rowoff) + tid;
+  uint4* o1 = reinterpret_cast<uint4*>(ct_out + ((size_t)p * 2 + 1) * L * N + rowoff) + tid;
+  const int32_t* tp = terms + p * K * 2;
 #pragma unroll
-  for (int c = 0; c < 32; ++c) { acc0[c] = 0u; acc1[c] = 0u; }
-  for (int kk = 0; kk < K; ++kk) {
-    const int ci = terms[(p * K + kk) * 2 + 0];
-    const int pi = terms[(p * K + kk) * 2 + 1];
-    if (ci < 0) continue;
-    const uint4* w4 = reinterpret_cast<const uint4*>(pt + ((size_t)pi * L + l) * N + (tid << 5));
-    const uint4* ws4 = reinterpret_cast<const uint4*>(pt_sh + ((size_t)pi * L + l) * N + (tid << 5));
-    const uint4* c04 = reinterpret_cast<const uint4*>(ct_in + (((size_t)ci * 2 + 0) * L + l) * N + (tid << 5));
-    const uint4* c14 = reinterpret_cast<const uint4*>(ct_in + (((size_t)ci * 2 + 1) * L + l) * N + (tid << 5));
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const uint4 w = __ldg(w4 + v), ws = __ldg(ws4 + v), x0 = __ldg(c04 + v), x1 = __ldg(c14 + v);
-      acc0[4 * v + 0] = addmod(acc0[4 * v + 0], mul_shoup(x0.x, w.x, ws.x, q), q);
-      acc0[4 * v + 1] = addmod(acc0[4 * v + 1], mul_shoup(x0.y, w.y, ws.y, q), q);
-      acc0[4 * v + 2] = addmod(acc0[4 * v + 2], mul_shoup(x0.z, w.z, ws.z, q), q);
-      acc0[4 * v + 3] = addmod(acc0[4 * v + 3], mul_shoup(x0.w, w.w, ws.w, q), q);
-      acc1[4 * v + 0] = addmod(acc1[4 * v + 0], mul_shoup(x1.x, w.x, ws.x, q), q);
-      acc1[4 * v + 1] = addmod(acc1[4 * v + 1], mul_shoup(x1.y, w.y, ws.y, q), q);
-      acc1[4 * v + 2] = addmod(acc1[4 * v + 2], mul_shoup(x1.z, w.z, ws.z, q), q);
-      acc1[4 * v + 3] = addmod(acc1[4 * v + 3], mul_shoup(x1.w, w.w, ws.w, q), q);
+  for (int v = 0; v < 8; ++v) {
+    uint32_t a0[4] = {0u, 0u, 0u, 0u}, a1[4] = {0u, 0u, 0u, 0u};
+    for (int kk = 0; kk < K; ++kk) {
+      const int ci = __ldg(tp + 2 * kk), pi = __ldg(tp + 2 * kk + 1);
+      if (ci < 0) continue;
+      const size_t vo = (size_t)v * Nt::T + tid;
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(pt + (size_t)pi * L * N + rowoff) + vo);
+      const uint4 ws = __ldg(reinterpret_cast<const uint4*>(pt_sh + (size_t)pi * L * N + rowoff) + vo);
+      const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(ct_in + ((size_t)ci * 2 + 0) * L * N + rowoff) + vo);
+      const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(ct_in + ((size_t)ci * 2 + 1) * L * N + rowoff) + vo);
+      a0[0] = addmod(a0[0], mul_shoup(x0.x, w.x, ws.x, q), q);
+      a0[1] = addmod(a0[1], mul_shoup(x0.y, w.y, ws.y, q), q);
+      a0[2] = addmod(a0[2], mul_shoup(x0.z, w.z, ws.z, q), q);
+      a0[3] = addmod(a0[3], mul_shoup(x0.w, w.w, ws.w, q), q);
+      a1[0] = addmod(a1[0], mul_shoup(x1.x, w.x, ws.x, q), q);
+      a1[1] = addmod(a1[1], mul_shoup(x1.y, w.y, ws.y, q), q);
+      a1[2] = addmod(a1[2], mul_shoup(x1.z, w.z, ws.z, q), q);
+      a1[3] = addmod(a1[3], mul_shoup(x1.w, w.w, ws.w, q), q);
     }
+    o0[v * Nt::T] = make_uint4(submod(a0[0], pb::canon4(m[4 * v + 0], q), q), submod(a0[1], pb::canon4(m[4 * v + 1], q), q),
+                               submod(a0[2], pb::canon4(m[4 * v + 2], q), q), submod(a0[3], pb::canon4(m[4 * v + 3], q), q));
+    o1[v * Nt::T] = make_uint4(a1[0], a1[1], a1[2], a1[3]);
   }
-#pragma unroll
-  for (int c = 0; c < 32; ++c) acc0[c] = submod(acc0[c], pb::canon4(m[c], q), q);
-  Nt::gst3(ct_out + ((p * 2 + 0) * L + l) * N, acc0, tid);
-  Nt::gst3(ct_out + ((p * 2 + 1) * L + l) * N, acc1, tid);
 }
 
 // ------------------------------------------------------------- launchers ---

@@ -29,12 +29,17 @@ struct PbDev {
   double sc_frac[PB_MAXL];                     // frac(t P_{i-1} / Q)
   const uint2* tw_fwd;                         // [L][N] {psi^brv(i), shoup}
   const uint2* tw_inv;                         // [L][N] {psi^-brv(i), shoup}
+  const uint2* tw3_fwd;                        // [L][31*N/32] P3-stage twiddles, interleaved
+  const uint2* tw3_inv;
+  int tw3_stride;                              // uint2 per limb in tw3_* (0 when N < 2048)
 };
 
 struct pb_ctx {
   PbDev dev;        // device pointers inside point at the buffers below
   uint2* d_tw_fwd;
   uint2* d_tw_inv;
+  uint2* d_tw3_fwd;
+  uint2* d_tw3_inv;
   pb_params host;   // the descriptor the context was created from
 };
 

@@ -88,17 +88,19 @@ struct Ntt {
     for (int c = 0; c < 32; ++c) a[c] = b[c];
   }
 
-  // ---- P3 twiddles for stage s = LOGN-5+d: 2^d contiguous entries per thread ----
+  // ---- P3 twiddles: interleaved table, stage D at offset (2^D - 1)*T uint2,
+  // entry [v][tid] = {w(2v), w(2v+1)} as one uint4, so every warp load is a
+  // contiguous 512-byte line set (built by pb_ctx_create). ----
   template <int D>
-  __device__ __forceinline__ static void tw3(const uint2* tw, int tid, uint2 (&w)[16]) {
-    const uint2* base = tw + (1 << (LOGN - 5 + D)) + (tid << D);
+  __device__ __forceinline__ static void tw3(const uint2* t3, int tid, uint2 (&w)[16]) {
+    const uint2* base = t3 + ((1 << D) - 1) * T;
     if constexpr (D == 0) {
-      w[0] = __ldg(base);
+      w[0] = __ldg(base + tid);
     } else {
       const uint4* b4 = reinterpret_cast<const uint4*>(base);
 #pragma unroll
       for (int v = 0; v < (1 << (D - 1)); ++v) {
-        const uint4 x = __ldg(b4 + v);
+        const uint4 x = __ldg(b4 + v * T + tid);
         w[2 * v] = make_uint2(x.x, x.y);
         w[2 * v + 1] = make_uint2(x.z, x.w);
       }
@@ -154,7 +156,7 @@ struct Ntt {
   // lazily reduced ([0,4q)) result in P3 layout on exit.  `sm` needs
   // SMEM_WORDS words; the caller syncs before reusing it.
   __device__ __forceinline__ static void forward(uint32_t (&a)[32], uint32_t* sm, const uint2* tw,
-                                                 int tid, uint32_t q) {
+                                                 const uint2* t3, int tid, uint32_t q) {
     fwd_p1(a, tw, q);
     st1(sm, a, tid);
     __syncthreads();
@@ -164,7 +166,7 @@ struct Ntt {
     st2(sm, a, tid);
     __syncthreads();
     ld3(sm, a, tid);
-    fwd_p3(a, tw, tid, q);
+    fwd_p3(a, t3, tid, q);
   }
 
   // =========================== inverse ===========================
@@ -217,8 +219,8 @@ struct Ntt {
   // Full inverse (without the N^-1 scaling): a[] in P3 layout with values in
   // [0, 2q) on entry, P1 layout with values in [0, 2q) on exit.
   __device__ __forceinline__ static void inverse(uint32_t (&a)[32], uint32_t* sm, const uint2* tw,
-                                                 int tid, uint32_t q) {
-    inv_p3(a, tw, tid, q);
+                                                 const uint2* t3, int tid, uint32_t q) {
+    inv_p3(a, t3, tid, q);
     st3(sm, a, tid);
     __syncthreads();
     ld2(sm, a, tid);
@@ -230,19 +232,23 @@ struct Ntt {
     inv_p1(a, tw, q);
   }
 
-  // ---- vectorised P3 global load/store (32 contiguous words per thread) ----
+  // ---- NTT-domain rows in DEVICE ORDER: bit-reversed index j = tid*32 + 4v + k
+  // (the P3 layout) is stored at address v*4T + tid*4 + k, so a P3-layout
+  // register file moves to/from HBM with fully coalesced 128-bit accesses.
+  // (pb_ntt_reorder converts to/from the reference's bit-reversed order.) ----
+  __device__ __forceinline__ static int dev_addr(int j) { return ((j & 31) >> 2) * 4 * T + (j >> 5) * 4 + (j & 3); }
   __device__ __forceinline__ static void gld3(const uint32_t* row, uint32_t (&a)[32], int tid) {
-    const uint4* p = reinterpret_cast<const uint4*>(row + (tid << 5));
+    const uint4* p = reinterpret_cast<const uint4*>(row) + tid;
 #pragma unroll
     for (int v = 0; v < 8; ++v) {
-      const uint4 x = __ldg(p + v);
+      const uint4 x = __ldg(p + v * T);
       a[4 * v] = x.x; a[4 * v + 1] = x.y; a[4 * v + 2] = x.z; a[4 * v + 3] = x.w;
     }
   }
   __device__ __forceinline__ static void gst3(uint32_t* row, const uint32_t (&a)[32], int tid) {
-    uint4* p = reinterpret_cast<uint4*>(row + (tid << 5));
+    uint4* p = reinterpret_cast<uint4*>(row) + tid;
 #pragma unroll
-    for (int v = 0; v < 8; ++v) p[v] = make_uint4(a[4 * v], a[4 * v + 1], a[4 * v + 2], a[4 * v + 3]);
+    for (int v = 0; v < 8; ++v) p[v * T] = make_uint4(a[4 * v], a[4 * v + 1], a[4 * v + 2], a[4 * v + 3]);
   }
   __device__ __forceinline__ static void gld1(const uint32_t* row, uint32_t (&a)[32], int tid) {
 #pragma unroll

@@ -119,17 +119,51 @@ extern "C" int pb_ctx_create(const pb_params* p, pb_ctx** out) {
     }
   }
   free(pw); free(ipw);
+  // P3-stage tables (register NTT, N >= 2048): stage D (s = logN-5+D) at
+  // uint2 offset (2^D-1)*T; for D >= 1 the pair (2v, 2v+1) of thread tid is
+  // uint4 #(v*T + tid), so each warp load is contiguous (pb_ntt.cuh tw3).
+  const int T = N / 32;
+  const size_t n3 = (logN >= 11) ? (size_t)31 * T : 0;
+  uint2* h3f = n3 ? (uint2*)malloc((size_t)L * n3 * sizeof(uint2)) : nullptr;
+  uint2* h3i = n3 ? (uint2*)malloc((size_t)L * n3 * sizeof(uint2)) : nullptr;
+  if (n3 && (!h3f || !h3i)) {
+    free(h_f); free(h_i); free(h3f); free(h3i); delete c;
+    return pb_set_error(PB_ERR_ARG, "out of host memory");
+  }
+  for (int l = 0; n3 && l < L; ++l) {
+    for (int D = 0; D < 5; ++D) {
+      const int s = logN - 5 + D;
+      const size_t off = (size_t)l * n3 + (size_t)((1 << D) - 1) * T;
+      for (int tid = 0; tid < T; ++tid) {
+        for (int r = 0; r < (1 << D); ++r) {
+          const size_t src = (size_t)l * N + (1u << s) + ((size_t)tid << D) + r;
+          const size_t dst = (D == 0) ? off + tid : off + 2 * ((size_t)(r >> 1) * T + tid) + (r & 1);
+          h3f[dst] = h_f[src];
+          h3i[dst] = h_i[src];
+        }
+      }
+    }
+  }
   cudaError_t e = cudaMalloc(&c->d_tw_fwd, n_tw * sizeof(uint2));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_tw_inv, n_tw * sizeof(uint2));
   if (e == cudaSuccess) e = cudaMemcpy(c->d_tw_fwd, h_f, n_tw * sizeof(uint2), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_tw_inv, h_i, n_tw * sizeof(uint2), cudaMemcpyHostToDevice);
-  free(h_f); free(h_i);
+  if (n3) {
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_tw3_fwd, (size_t)L * n3 * sizeof(uint2));
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_tw3_inv, (size_t)L * n3 * sizeof(uint2));
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_tw3_fwd, h3f, (size_t)L * n3 * sizeof(uint2), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_tw3_inv, h3i, (size_t)L * n3 * sizeof(uint2), cudaMemcpyHostToDevice);
+  }
+  free(h_f); free(h_i); free(h3f); free(h3i);
   if (e != cudaSuccess) {
-    cudaFree(c->d_tw_fwd); cudaFree(c->d_tw_inv); delete c;
+    cudaFree(c->d_tw_fwd); cudaFree(c->d_tw_inv); cudaFree(c->d_tw3_fwd); cudaFree(c->d_tw3_inv); delete c;
     return pb_set_cuda_error(e);
   }
   d.tw_fwd = c->d_tw_fwd;
   d.tw_inv = c->d_tw_inv;
+  d.tw3_fwd = c->d_tw3_fwd;
+  d.tw3_inv = c->d_tw3_inv;
+  d.tw3_stride = (int)n3;
   *out = c;
   return PB_OK;
 }
@@ -138,6 +172,8 @@ extern "C" int pb_ctx_destroy(pb_ctx* c) {
   if (!c) return PB_OK;
   cudaFree(c->d_tw_fwd);
   cudaFree(c->d_tw_inv);
+  cudaFree(c->d_tw3_fwd);
+  cudaFree(c->d_tw3_inv);
   delete c;
   return PB_OK;
 }
@@ -157,10 +193,11 @@ __global__ void __launch_bounds__(1 << (LOGN - 5)) k_ntt_fwd(PbDev P, uint32_t* 
     const int limb = row_limb_of(P, row_limb, r);
     const uint32_t q = P.q[limb];
     const uint2* tw = P.tw_fwd + (size_t)limb * Nt::N;
+    const uint2* t3 = P.tw3_fwd + (size_t)limb * P.tw3_stride;
     uint32_t* row = rows + r * Nt::N;
     uint32_t a[32];
     Nt::gld1(row, a, tid);
-    Nt::forward(a, sm, tw, tid, q);
+    Nt::forward(a, sm, tw, t3, tid, q);
 #pragma unroll
     for (int c = 0; c < 32; ++c) a[c] = pb::canon4(a[c], q);
     Nt::gst3(row, a, tid);
@@ -178,10 +215,11 @@ __global__ void __launch_bounds__(1 << (LOGN - 5)) k_ntt_inv(PbDev P, uint32_t* 
     const int limb = row_limb_of(P, row_limb, r);
     const uint32_t q = P.q[limb];
     const uint2* tw = P.tw_inv + (size_t)limb * Nt::N;
+    const uint2* t3 = P.tw3_inv + (size_t)limb * P.tw3_stride;
     uint32_t* row = rows + r * Nt::N;
     uint32_t a[32];
     Nt::gld3(row, a, tid);
-    Nt::inverse(a, sm, tw, tid, q);
+    Nt::inverse(a, sm, tw, t3, tid, q);
     const uint32_t ni = P.ninv[limb], nis = P.ninv_sh[limb];
 #pragma unroll
     for (int c = 0; c < 32; ++c) a[c] = mul_shoup(a[c], ni, nis, q);
@@ -265,6 +303,39 @@ extern "C" int pb_ntt_forward(const pb_ctx* ctx, uint32_t* rows, int64_t n_rows,
 extern "C" int pb_ntt_inverse(const pb_ctx* ctx, uint32_t* rows, int64_t n_rows, const int32_t* row_limb,
                               void* stream) {
   return ntt_entry(ctx, rows, n_rows, row_limb, stream, true);
+}
+
+// ----------------------------------------------- NTT-domain order convert --
+// Device order (pb_ntt.cuh dev_addr) <-> the reference's bit-reversed order.
+__global__ void k_reorder(int N, int logN, uint32_t* rows, int64_t n_rows, int to_device) {
+  extern __shared__ uint32_t sm[];
+  const int T = N >> 5;
+  for (int64_t r = blockIdx.x; r < n_rows; r += gridDim.x) {
+    uint32_t* row = rows + r * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sm[i] = row[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      if (to_device) {  // address i holds K index j
+        const int v = i / (4 * T), rem = i - v * 4 * T;
+        row[i] = sm[(rem >> 2) * 32 + 4 * v + (rem & 3)];
+      } else {  // K index i lives at device address dev_addr(i)
+        row[i] = sm[((i & 31) >> 2) * 4 * T + (i >> 5) * 4 + (i & 3)];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+extern "C" int pb_ntt_reorder(const pb_ctx* ctx, uint32_t* rows, int64_t n_rows, int to_device, void* stream) {
+  if (!ctx || (!rows && n_rows)) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n_rows <= 0 || ctx->dev.logN < 11) return PB_OK;  // small N: device order == reference order
+  const int N = ctx->dev.N;
+  const size_t smem = (size_t)N * 4;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_reorder, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = (int)(n_rows < (1 << 30) ? n_rows : (1 << 30));
+  k_reorder<<<grid, 512, smem, pb_stream_of(stream)>>>(N, ctx->dev.logN, rows, n_rows, to_device ? 1 : 0);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
 }
 
 // -------------------------------------------------------------- pointwise --

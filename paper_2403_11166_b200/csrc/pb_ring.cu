@@ -246,7 +246,7 @@ bool bad_ell(int ell) { return ell < 2 || ell > 64; }
 
 extern "C" int pb_ring_binary(int op, uint64_t* out, const uint64_t* a, const uint64_t* b, int64_t n, int64_t b_n,
                               int32_t ell, void* stream) {
-  if (!out || !a || !b) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n > 0 && (!out || !a || !b)) return pb_set_error(PB_ERR_ARG, "null argument");
   if (op < PB_RING_ADD || op > PB_RING_MUL || bad_ell(ell)) return pb_set_error(PB_ERR_ARG, "bad ring op / ell");
   if (n <= 0) return PB_OK;
   if (b_n <= 0 || n % b_n) return pb_set_error(PB_ERR_SHAPE, "broadcast size must divide n");
@@ -256,7 +256,7 @@ extern "C" int pb_ring_binary(int op, uint64_t* out, const uint64_t* a, const ui
 }
 
 extern "C" int pb_ring_unary(int op, uint64_t* out, const uint64_t* a, uint64_t k, int64_t n, int32_t ell, void* stream) {
-  if (!out || !a) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n > 0 && (!out || !a)) return pb_set_error(PB_ERR_ARG, "null argument");
   if (op < PB_RING_NEG || op > PB_RING_ARITH_SHIFT || bad_ell(ell)) return pb_set_error(PB_ERR_ARG, "bad ring op / ell");
   if (op == PB_RING_ARITH_SHIFT && k >= 64) return pb_set_error(PB_ERR_ARG, "shift too large");
   if (n <= 0) return PB_OK;
@@ -267,7 +267,7 @@ extern "C" int pb_ring_unary(int op, uint64_t* out, const uint64_t* a, uint64_t 
 
 extern "C" int pb_encode_fixed(const double* x, int64_t n, int32_t ell, int32_t scale, uint64_t* out, int32_t* flag,
                                void* stream) {
-  if (!x || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n > 0 && (!x || !out)) return pb_set_error(PB_ERR_ARG, "null argument");
   if (bad_ell(ell) || scale < 0 || scale >= ell) return pb_set_error(PB_ERR_SCALE, "bad scale");
   if (n <= 0) return PB_OK;
   k_encode_fixed<<<RING_GRID(n)>>>(x, n, ell, scale, out, flag);
@@ -276,7 +276,7 @@ extern "C" int pb_encode_fixed(const double* x, int64_t n, int32_t ell, int32_t 
 }
 
 extern "C" int pb_decode_fixed(const uint64_t* v, int64_t n, int32_t ell, int32_t scale, double* out, void* stream) {
-  if (!v || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n > 0 && (!v || !out)) return pb_set_error(PB_ERR_ARG, "null argument");
   if (bad_ell(ell) || scale < 0 || scale >= ell) return pb_set_error(PB_ERR_SCALE, "bad scale");
   if (n <= 0) return PB_OK;
   k_decode_fixed<<<RING_GRID(n)>>>(v, n, ell, scale, out);
@@ -286,7 +286,7 @@ extern "C" int pb_decode_fixed(const uint64_t* v, int64_t n, int32_t ell, int32_
 
 extern "C" int pb_uniform_ring(uint64_t* out, int64_t n, uint64_t seed, uint64_t stream_id, uint64_t raw_offset,
                                int32_t ell, void* stream) {
-  if (!out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n > 0 && !out) return pb_set_error(PB_ERR_ARG, "null argument");
   if (ell < 1 || ell > 63) return pb_set_error(PB_ERR_ARG, "bad ell");
   if (n <= 0) return PB_OK;
   k_uniform_ring<<<RING_GRID((n + 3) / 4 + 1)>>>(out, nullptr, nullptr, n, seed, stream_id, raw_offset, ell);
@@ -296,7 +296,7 @@ extern "C" int pb_uniform_ring(uint64_t* out, int64_t n, uint64_t seed, uint64_t
 
 extern "C" int pb_share(const uint64_t* x, int64_t n, uint64_t seed, uint64_t stream_id, uint64_t raw_offset,
                         int32_t ell, uint64_t* mo_out, uint64_t* do_out, void* stream) {
-  if (!x || !mo_out || !do_out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n > 0 && (!x || !mo_out || !do_out)) return pb_set_error(PB_ERR_ARG, "null argument");
   if (ell < 1 || ell > 63) return pb_set_error(PB_ERR_ARG, "bad ell");
   if (n <= 0) return PB_OK;
   k_uniform_ring<<<RING_GRID((n + 3) / 4 + 1)>>>(mo_out, x, do_out, n, seed, stream_id, raw_offset, ell);
@@ -306,7 +306,7 @@ extern "C" int pb_share(const uint64_t* x, int64_t n, uint64_t seed, uint64_t st
 
 extern "C" int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m, int trans_a,
                               int trans_b, int32_t ell, uint64_t* out, void* stream) {
-  if (!a || !b || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n > 0 && m > 0 && k > 0 && (!a || !b || !out)) return pb_set_error(PB_ERR_ARG, "null argument");
   if (n <= 0 || m <= 0) return PB_OK;
   if (k < 0 || n > (1ll << 31) || m > (1ll << 31)) return pb_set_error(PB_ERR_SHAPE, "bad matmul shape");
   const uint64_t mask = (ell >= 64 || ell <= 0) ? ~0ull : ((1ull << ell) - 1);
@@ -317,7 +317,7 @@ extern "C" int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, i
 }
 
 extern "C" int pb_ring_rowsum(const uint64_t* a, int64_t rows, int64_t cols, int32_t ell, uint64_t* out, void* stream) {
-  if (!a || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (rows > 0 && (!a || !out)) return pb_set_error(PB_ERR_ARG, "null argument");
   if (rows <= 0) return PB_OK;
   const uint64_t mask = (ell >= 64 || ell <= 0) ? ~0ull : ((1ull << ell) - 1);
   k_rowsum<<<(unsigned)rows, 256, 0, pb_stream_of(stream)>>>(a, rows, cols, mask, out);
@@ -362,7 +362,7 @@ extern "C" int pb_conv2d(const uint64_t* x, const uint64_t* w, int32_t B, int32_
 extern "C" int pb_dealer_op(int op, uint64_t* mo, uint64_t* do_, int64_t n, int32_t k, const uint8_t* d_in,
                             uint8_t* d_out, uint64_t seed, uint64_t stream_id, uint64_t raw_offset, int32_t ell,
                             void* stream) {
-  if (!mo || !do_) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n > 0 && (!mo || !do_)) return pb_set_error(PB_ERR_ARG, "null argument");
   if (op < PB_DEALER_RELU || op > PB_DEALER_RESHARE) return pb_set_error(PB_ERR_ARG, "bad dealer op");
   if (op == PB_DEALER_SELECT && !d_in) return pb_set_error(PB_ERR_ARG, "select needs d_in");
   if (ell < 2 || ell > 63 || k < 0 || k >= ell) return pb_set_error(PB_ERR_ARG, "bad ell / shift");
@@ -375,7 +375,7 @@ extern "C" int pb_dealer_op(int op, uint64_t* mo, uint64_t* do_, int64_t n, int3
 extern "C" int pb_sgd_momentum(double* w, double* v, const uint64_t* grad_ring, int64_t n, int32_t grad_scale, double lr,
                                double momentum, int32_t ell, int32_t w_scale, uint64_t* w_ring, int32_t* range_flag,
                                void* stream) {
-  if (!w || !v || !grad_ring || !w_ring) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n > 0 && (!w || !v || !grad_ring || !w_ring)) return pb_set_error(PB_ERR_ARG, "null argument");
   if (bad_ell(ell)) return pb_set_error(PB_ERR_ARG, "bad ell");
   if (n <= 0) return PB_OK;
   k_sgd<<<RING_GRID(n)>>>(w, v, grad_ring, n, grad_scale, lr, momentum, ell, w_scale, w_ring, range_flag);

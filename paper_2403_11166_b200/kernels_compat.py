@@ -86,8 +86,14 @@ def _run_ntt(rows, tab, q, inverse):
     ctx, limb = _tables_ctx(np.asarray(tab), np.asarray(q), inverse)
     d = _dev.u32_to_device(rows.astype(np.uint32))
     rl = _dev.i32_to_device(limb)
-    fn = "pb_ntt_inverse" if inverse else "pb_ntt_forward"
-    _lib.call(fn, ctx.handle, _dev.ptr(d), rows.shape[0], _dev.ptr(rl), _dev.stream())
+    R = rows.shape[0]
+    st = _dev.stream()
+    if inverse:  # K's bit-reversed order -> device order -> INTT
+        _lib.call("pb_ntt_reorder", ctx.handle, _dev.ptr(d), R, 1, st)
+        _lib.call("pb_ntt_inverse", ctx.handle, _dev.ptr(d), R, _dev.ptr(rl), st)
+    else:  # NTT -> device order -> K's bit-reversed order
+        _lib.call("pb_ntt_forward", ctx.handle, _dev.ptr(d), R, _dev.ptr(rl), st)
+        _lib.call("pb_ntt_reorder", ctx.handle, _dev.ptr(d), R, 0, st)
     rows[...] = _dev.to_numpy_u32(d).astype(np.uint64)
 
 
@@ -198,8 +204,8 @@ def matmul_wrap(a, b):  # K:206-218
     n, k = a.shape
     m = b.shape[1]
     out = _dev.empty_u64(n, m)
-    _lib.call("pb_ring_matmul", _dev.ptr(_dev.u64_to_device(a)), _dev.ptr(_dev.u64_to_device(b)), n, k, m, 0, 0, 64,
-              _dev.ptr(out), _dev.stream())
+    da, db = _dev.u64_to_device(a), _dev.u64_to_device(b)  # keep alive until the kernel is enqueued
+    _lib.call("pb_ring_matmul", _dev.ptr(da), _dev.ptr(db), n, k, m, 0, 0, 64, _dev.ptr(out), _dev.stream())
     return _dev.to_numpy_u64(out).copy()
 
 
@@ -208,14 +214,16 @@ def im2col_wrap(x, s, stride):  # K:221-238
     B, C, H, W = x.shape
     oh, ow = (H - s) // stride + 1, (W - s) // stride + 1
     out = _dev.empty_u64(C * s * s, B * oh * ow)
-    _lib.call("pb_im2col", _dev.ptr(_dev.u64_to_device(x)), B, C, H, W, s, stride, _dev.ptr(out), _dev.stream())
+    dx = _dev.u64_to_device(x)
+    _lib.call("pb_im2col", _dev.ptr(dx), B, C, H, W, s, stride, _dev.ptr(out), _dev.stream())
     return _dev.to_numpy_u64(out).copy()
 
 
 def col2im_wrap(cols, B, C, H, W, s, stride):  # K:241-257
     cols = np.ascontiguousarray(cols, dtype=np.uint64)
     out = _dev.empty_u64(B, C, H, W)
-    _lib.call("pb_col2im", _dev.ptr(_dev.u64_to_device(cols)), B, C, H, W, s, stride, _dev.ptr(out), _dev.stream())
+    dc = _dev.u64_to_device(cols)
+    _lib.call("pb_col2im", _dev.ptr(dc), B, C, H, W, s, stride, _dev.ptr(out), _dev.stream())
     return _dev.to_numpy_u64(out).copy()
 
 
@@ -225,6 +233,6 @@ def conv2d_wrap(x, w):  # K:260-278
     B, Ci, H, W = x.shape
     Co, _, s, _ = w.shape
     out = _dev.empty_u64(B, Co, H - s + 1, W - s + 1)
-    _lib.call("pb_conv2d", _dev.ptr(_dev.u64_to_device(x)), _dev.ptr(_dev.u64_to_device(w)), B, Ci, H, W, Co, s, 64,
-              _dev.ptr(out), _dev.stream())
+    dx, dw = _dev.u64_to_device(x), _dev.u64_to_device(w)
+    _lib.call("pb_conv2d", _dev.ptr(dx), _dev.ptr(dw), B, Ci, H, W, Co, s, 64, _dev.ptr(out), _dev.stream())
     return _dev.to_numpy_u64(out).copy()

@@ -1,0 +1,307 @@
+"""The four share-level linear-layer procedures of Pencil on the B200
+(the SPEC-only ``linear_protocols`` module; PAPER.md
+Alg. 1, Alg. 2).
+
+    linear_forward          Alg.1
+    linear_backward_input   Alg.1 with W^T
+    reveal_grad_bias        local sums + DP
+    grad_weight             Alg.2 (cross terms)
+    sample_dp_noise         N(0, sigma^2 C^2 / B)
+
+Per protocol message the work is three fused device kernels:
+    DO   pb_encrypt_sk        pack (pi_v / pi_W gather) + Delta m + NTT + key mul
+    MO   pb_ctpt_mac_mask     sum_k ct (*) pt  -  Delta NTT(pi_y(mask) + filler)
+    DO   pb_decrypt_to_share  c0 + c1 s + INTT + Garner/scale-round + pi_y^-1
+plus the MO's plaintext encoding (pb_encode_plain) and ring GEMMs for the
+local terms.  Both parties run in this process (as in the paper's artifact,
+PAPER:1525); every MO<->DO message still goes through ``Channel`` so the
+census and transcript are the protocol's.
+
+Conventions are the oracle's (oracle/protocols.py) so that, under the same
+seed, the DO's decrypted shares are bit-identical to the CPU oracle's:
+activations (n, B), W (n_o, n_i), bias at scale 2f, MO mask streams
+stream_id(layer, op, purpose); s_eff = s - W o <X>_0 replaces the
+homomorphic addition of <X>_0 (same DO output W o X - s).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .bfv import Ciphertext, KeyPair
+from .errors import DesyncError, ScaleError, ShapeError
+from .params import BfvParams, context
+from .poly_encoding import MatmulGeometry, plan_matmul
+from .ring import DO, MO, RingParams, RingTensor, SeededRng, ShareTensor
+
+OP_FWD, OP_BWD_X, OP_GRAD_W, OP_GRAD_B, OP_RELU, OP_TRUNC_F, OP_TRUNC_B, OP_RELU_B = range(8)
+P_MASK, P_ENC, P_DEALER, P_DP = range(4)
+
+# SPEC:372 message codes
+MSG_FWD_INPUT_CT = 0x10
+MSG_FWD_MASKED_CT = 0x11
+MSG_BWD_X = 0x20
+MSG_GRADW = 0x30
+MSG_GRADB = 0x31
+FRAME_HEADER = 12  # {u16 type, u16 flags, u64 len}
+
+
+def stream_id(layer: int, op: int, purpose: int) -> int:
+    return 1_000_000 + 1000 * layer + 10 * op + purpose
+
+
+@dataclass
+class Channel:
+    """In-process duplex MO<->DO channel with a byte census.
+    Payloads are handed over by reference (device tensors stay in HBM)."""
+
+    census: dict = field(default_factory=dict)
+    transcript: list = field(default_factory=list)
+    record: bool = False
+
+    def send(self, sender: str, msg_type: int, payload, nbytes: int):
+        c = self.census.setdefault(msg_type, [0, 0])
+        c[0] += 1
+        c[1] += FRAME_HEADER + int(nbytes)
+        if self.record:
+            self.transcript.append((sender, msg_type, int(nbytes)))
+        return payload
+
+    def total_bytes(self) -> int:
+        return sum(v[1] for v in self.census.values())
+
+
+@dataclass
+class DpConfig:
+    sigma: float = 0.0
+    C: float = 1.0
+    B: int = 1
+    enabled: bool = False
+
+
+class Session:
+    """Both parties' protocol state: BFV keys (DO), ring params, seeds, channel."""
+
+    def __init__(self, params: BfvParams, ring: RingParams, kp: KeyPair, seed: int, filler: bool = True,
+                 channel: Channel | None = None):
+        if ring.ell != params.ell:
+            raise ScaleError("ring ell must equal the BFV plaintext modulus bits")
+        self.p = params
+        self.ring = ring
+        self.kp = kp
+        self.seed = int(seed)
+        self.filler = filler
+        self.channel = channel or Channel()
+        self.ctx = context(params)
+        self._enc_nonce = 0
+        self.layer_phase = {}
+
+    def rng(self, layer: int, op: int, purpose: int) -> SeededRng:
+        return SeededRng(self.seed, stream_id(layer, op, purpose))
+
+    def reseed(self, seed: int):
+        self.seed = int(seed)
+
+    # --------------------------------------------------------- HE matmul ---
+    def he_matmul(self, layer: int, op: int, g: MatmulGeometry, out: torch.Tensor, mask: torch.Tensor,
+                  v_ct=None, v_strides=None, w_pt=None, w_strides=None, w_ct=None, v_pt=None,
+                  y_strides=None, msg_in=MSG_FWD_INPUT_CT, msg_out=MSG_FWD_MASKED_CT):
+        """DO-decrypted share of  [Enc(pi_v(v_ct)) (x) pi_W(w_pt)] + [Enc(pi_W(w_ct)) (x) pi_v(v_pt)] - mask,
+        written into ``out`` (flat, addressed through y_strides).  Operands are flat
+        device tensors addressed through the given strides; absent terms are None."""
+        p, h, st = self.p, self.ctx.handle, _dev.stream()
+        plan = plan_matmul(g, p.N, v_strides, w_strides, y_strides)
+        dm = plan.device()
+        N, L = p.N, p.L
+        cts, pts, pairs = [], [], []
+        enc_rng = self.rng(layer, op, P_ENC)
+        if v_ct is not None:  # term A: Enc(pi_v(v)) (x) pi_W(W)
+            ct = _dev.empty_u32(plan.n_in, 2, L, N)
+            _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(v_ct), _dev.ptr(dm["in_src"]),
+                      plan.n_in, enc_rng.device_key, enc_rng.reserve(plan.n_in), _dev.ptr(ct), st)
+            pt = _dev.empty_u32(plan.n_pt, L, N)
+            sh = _dev.empty_u32(plan.n_pt, L, N)
+            _lib.call("pb_encode_plain", h, _dev.ptr(w_pt), _dev.ptr(dm["pt_src"]), plan.n_pt, _dev.ptr(pt),
+                      _dev.ptr(sh), st)
+            cts.append(ct)
+            pts.append((pt, sh))
+            pairs.append(plan.terms)
+            self.channel.send(DO, msg_in, ct, Ciphertext(ct, p).nbytes_wire())
+        if w_ct is not None:  # term B: Enc(pi_W(W)) (x) pi_v(v)
+            ct = _dev.empty_u32(plan.n_pt, 2, L, N)
+            _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(w_ct), _dev.ptr(dm["pt_src"]),
+                      plan.n_pt, enc_rng.device_key, enc_rng.reserve(plan.n_pt), _dev.ptr(ct), st)
+            pt = _dev.empty_u32(plan.n_in, L, N)
+            sh = _dev.empty_u32(plan.n_in, L, N)
+            _lib.call("pb_encode_plain", h, _dev.ptr(v_pt), _dev.ptr(dm["in_src"]), plan.n_in, _dev.ptr(pt),
+                      _dev.ptr(sh), st)
+            cts.append(ct)
+            pts.append((pt, sh))
+            pairs.append(plan.terms[:, :, ::-1])
+        # concatenate operands of both terms and build the MAC term list
+        if len(cts) == 2:
+            ct_all = torch.cat([cts[0], cts[1]])
+            pt_all = torch.cat([pts[0][0], pts[1][0]])
+            sh_all = torch.cat([pts[0][1], pts[1][1]])
+            t2 = pairs[1].copy()
+            t2[:, :, 0] += cts[0].shape[0]
+            t2[:, :, 1] += pts[0][0].shape[0]
+            terms = np.concatenate([pairs[0], t2], axis=1)
+        elif len(cts) == 1:
+            ct_all, (pt_all, sh_all), terms = cts[0], pts[0], pairs[0]
+        else:  # no cross term at all: the DO decrypts an encryption of -mask
+            ct_all = torch.zeros(1, 2, L, N, dtype=torch.int32, device=_dev.device())
+            pt_all = torch.zeros(1, L, N, dtype=torch.int32, device=_dev.device())
+            sh_all = pt_all
+            terms = np.full((plan.n_out, 1, 2), -1, dtype=np.int64)
+            terms[:, 0, 1] = 0
+        K = terms.shape[1]
+        terms_d = _dev.i32_to_device(np.ascontiguousarray(terms, dtype=np.int32))
+        out_ct = _dev.empty_u32(plan.n_out, 2, L, N)
+        fseed = self.rng(layer, op, P_MASK).device_key ^ 0x5A5A5A5A5A5A5A5A
+        _lib.call("pb_ctpt_mac_mask", h, _dev.ptr(ct_all), _dev.ptr(pt_all), _dev.ptr(sh_all), _dev.ptr(terms_d), K,
+                  plan.n_out, _dev.ptr(dm["out_pos"]), _dev.ptr(dm["out_dst"]), plan.U, _dev.ptr(mask),
+                  1 if self.filler else 0, fseed, _dev.ptr(out_ct), st)
+        self.channel.send(MO, msg_out, out_ct, Ciphertext(out_ct, p).nbytes_wire())
+        scratch = _dev.empty_u32(plan.n_out, L, plan.U)
+        _lib.call("pb_decrypt_to_share", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(out_ct), plan.n_out,
+                  _dev.ptr(dm["out_pos"]), _dev.ptr(dm["out_dst"]), plan.U, _dev.ptr(out), _dev.ptr(scratch), st)
+        # keep every operand alive until the kernels above are enqueued
+        del cts, pts, ct_all, pt_all, sh_all, terms_d
+        return out
+
+
+# ----------------------------------------------------------------- helpers ---
+
+def _ring_matmul(a: torch.Tensor, b: torch.Tensor, n, k, m, ell, ta=False, tb=False) -> torch.Tensor:
+    out = _dev.empty_u64(n, m)
+    _lib.call("pb_ring_matmul", _dev.ptr(a), _dev.ptr(b), n, k, m, 1 if ta else 0, 1 if tb else 0, ell,
+              _dev.ptr(out), _dev.stream())
+    return out
+
+
+def _ring_bin(op, a, b, ell, bn=None) -> torch.Tensor:
+    out = torch.empty_like(a)
+    n = a.numel()
+    _lib.call("pb_ring_binary", op, _dev.ptr(out), _dev.ptr(a), _dev.ptr(b), n, n if bn is None else bn, ell,
+              _dev.stream())
+    return out
+
+
+def _check_share_pair(a: ShareTensor, b: ShareTensor):
+    if {a.owner_role, b.owner_role} != {MO, DO}:
+        raise DesyncError("need one MO share and one DO share")
+    if a.scale != b.scale:
+        raise ScaleError("share scales differ")
+    if a.shape != b.shape:
+        raise ShapeError("share shapes differ")
+
+
+def _split(a: ShareTensor, b: ShareTensor):
+    _check_share_pair(a, b)
+    return (a, b) if a.owner_role == MO else (b, a)
+
+
+# ------------------------------------------------------------- protocols ---
+
+def linear_forward(sess: Session, layer: int, W: RingTensor, b: RingTensor, x_a: ShareTensor, x_b: ShareTensor,
+                   mo_x_zero: bool = False):  # Alg.1
+    """Shares of Y = W X + b at scale 2f.  X shares (n_i, B) at f, W (n_o, n_i) at f, b (n_o,) at 2f."""
+    x_mo, x_do = _split(x_a, x_b)
+    ring = sess.ring
+    if x_mo.scale != ring.f or W.scale != ring.f or b.scale != 2 * ring.f:
+        raise ScaleError("linear_forward needs X, W at f and b at 2f")
+    n_o, n_i = W.shape
+    if x_do.shape[0] != n_i:
+        raise ShapeError(f"X has {x_do.shape[0]} features, W expects {n_i}")
+    B = x_do.shape[1]
+    s = sess.rng(layer, OP_FWD, P_MASK).uniform_ring((n_o, B), ring)
+    if mo_x_zero:
+        s_eff = s
+    else:
+        s_eff = _ring_bin(_lib.RING_SUB, s, _ring_matmul(W.values, x_mo.value.values, n_o, n_i, B, ring.ell), ring.ell)
+    y_do = _dev.empty_u64(n_o, B)
+    sess.he_matmul(layer, OP_FWD, MatmulGeometry(n_i, n_o, B), y_do, s_eff, v_ct=x_do.value.values, w_pt=W.values)
+    bb = b.values.reshape(n_o, 1).expand(n_o, B).contiguous()
+    y_mo = _ring_bin(_lib.RING_ADD, s, bb, ring.ell)
+    return (ShareTensor(MO, RingTensor(y_mo, 2 * ring.f, ring, _canonical=True)),
+            ShareTensor(DO, RingTensor(y_do, 2 * ring.f, ring, _canonical=True)))
+
+
+def linear_backward_input(sess: Session, layer: int, W: RingTensor, gy_a: ShareTensor, gy_b: ShareTensor,
+                          mo_gy_zero: bool = False):
+    """Shares of grad X = W^T gY at scale 2f (Alg.1 message pattern with W^T)."""
+    gy_mo, gy_do = _split(gy_a, gy_b)
+    ring = sess.ring
+    n_o, n_i = W.shape
+    B = gy_do.shape[1]
+    s = sess.rng(layer, OP_BWD_X, P_MASK).uniform_ring((n_i, B), ring)
+    if mo_gy_zero:
+        s_eff = s
+    else:
+        s_eff = _ring_bin(_lib.RING_SUB, s,
+                          _ring_matmul(W.values, gy_mo.value.values, n_i, n_o, B, ring.ell, ta=True), ring.ell)
+    g_do = _dev.empty_u64(n_i, B)
+    # W^T (n_i, n_o) addressed in W's storage through strides (1, n_i)
+    sess.he_matmul(layer, OP_BWD_X, MatmulGeometry(n_o, n_i, B), g_do, s_eff, v_ct=gy_do.value.values,
+                   w_pt=W.values, w_strides=(1, n_i), msg_in=MSG_BWD_X, msg_out=MSG_BWD_X + 1)
+    return (ShareTensor(MO, RingTensor(s, 2 * ring.f, ring, _canonical=True)),
+            ShareTensor(DO, RingTensor(g_do, 2 * ring.f, ring, _canonical=True)))
+
+
+def reveal_grad_bias(sess: Session, layer: int, gy_a: ShareTensor, gy_b: ShareTensor,
+                     e: torch.Tensor | None = None) -> RingTensor:
+    gy_mo, gy_do = _split(gy_a, gy_b)
+    ring = sess.ring
+    n, B = gy_do.shape
+    sd = _dev.empty_u64(n)
+    _lib.call("pb_ring_rowsum", _dev.ptr(gy_do.value.values), n, B, ring.ell, _dev.ptr(sd), _dev.stream())
+    if e is not None:
+        sd = _ring_bin(_lib.RING_ADD, sd, e, ring.ell)
+    sess.channel.send(DO, MSG_GRADB, sd, n * 8)
+    sm = _dev.empty_u64(n)
+    _lib.call("pb_ring_rowsum", _dev.ptr(gy_mo.value.values), n, B, ring.ell, _dev.ptr(sm), _dev.stream())
+    return RingTensor(_ring_bin(_lib.RING_ADD, sm, sd, ring.ell), gy_do.scale, ring, _canonical=True)
+
+
+def grad_weight(sess: Session, layer: int, x_a: ShareTensor, x_b: ShareTensor, gy_a: ShareTensor,
+                gy_b: ShareTensor, e: torch.Tensor | None = None, mo_x_zero: bool = False,
+                mo_gy_zero: bool = False) -> RingTensor:  # Alg.2
+    """grad W = gY X^T revealed to the MO at scale 2f (n_o, n_i)."""
+    x_mo, x_do = _split(x_a, x_b)
+    gy_mo, gy_do = _split(gy_a, gy_b)
+    ring = sess.ring
+    n_i, B = x_do.shape
+    n_o = gy_do.shape[0]
+    g = MatmulGeometry(B, n_o, n_i)  # v = X^T (B x n_i) via strides (1, B); W = gY (n_o x B)
+    s = sess.rng(layer, OP_GRAD_W, P_MASK).uniform_ring((n_o, n_i), ring)
+    cross_do = _dev.empty_u64(n_o, n_i)
+    sess.he_matmul(layer, OP_GRAD_W, g, cross_do, s,
+                   v_ct=None if mo_gy_zero else x_do.value.values, v_strides=(1, B),
+                   w_pt=None if mo_gy_zero else gy_mo.value.values,
+                   w_ct=None if mo_x_zero else gy_do.value.values,
+                   v_pt=None if mo_x_zero else x_mo.value.values,
+                   msg_in=MSG_GRADW, msg_out=MSG_GRADW)
+    # DO: + local term gY_1 X_1^T (+ e), sends the masked sum
+    msg = _ring_bin(_lib.RING_ADD, cross_do,
+                    _ring_matmul(gy_do.value.values, x_do.value.values, n_o, B, n_i, ring.ell, tb=True), ring.ell)
+    if e is not None:
+        msg = _ring_bin(_lib.RING_ADD, msg, e, ring.ell)
+    sess.channel.send(DO, MSG_GRADW, msg, msg.numel() * 8)
+    # MO: + s + local term gY_0 X_0^T
+    out = _ring_bin(_lib.RING_ADD, msg, s, ring.ell)
+    if not (mo_x_zero or mo_gy_zero):
+        out = _ring_bin(_lib.RING_ADD, out,
+                        _ring_matmul(gy_mo.value.values, x_mo.value.values, n_o, B, n_i, ring.ell, tb=True), ring.ell)
+    return RingTensor(out, 2 * ring.f, ring, _canonical=True)
+
+
+def sample_dp_noise(shape, dp: DpConfig, rng: SeededRng) -> np.ndarray:
+    """e ~ N(0, (sigma C)^2 / B) per element (host float64, encoded by the caller)."""
+    if not dp.enabled or dp.sigma == 0.0:
+        return np.zeros(shape)
+    return rng.normal(shape, dp.sigma * dp.C / np.sqrt(dp.B))

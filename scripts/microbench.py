@@ -1,6 +1,9 @@
 """Kernel microbenchmarks (CUDA events): NTT fwd/inv over >= 1 GiB of residues."""
 import json
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch
 
