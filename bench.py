@@ -1,0 +1,327 @@
+"""Benchmark: Pencil private training step on the B200 (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload: one private training step of the MNIST MLP
+784-128-128-10, batch 64, synthetic MNIST-shaped data, BFV N=8192, t=2^59,
+7 x 30-bit RNS limbs, f=25: per FC layer Alg.1 forward, Alg.2 weight
+gradient, bias reveal and (layers 2-3) the input gradient, all through the
+B200 engine; ReLU/truncation via the SPEC's dealer backend; softmax-CE and
+SGD-momentum exactly as the reference engine.  A "step" therefore performs
+~2000 ciphertext x plaintext products, ~2000 decryptions and ~900
+encryptions (see DESIGN.md for the block plan).
+
+Prints ONE JSON line on rank 0.  ``value`` is samples/s with the batch
+resident in HBM; ``e2e`` is the same metric through the public API with the
+batch copied from pinned host memory every step and the loss read back;
+``roofline`` is the dominant kernel's algorithmic HBM bytes / its CUDA-event
+time; ``cpu_baseline`` is the oracle (the reference's CPU algorithm restated
+in C + numpy) timed on this host's cores on one step of the same workload.
+``--impl reference`` times that CPU path alone on the same config.
+
+Multi-GPU (torchrun, N>1): every he-matmul's output ciphertext blocks are
+sharded round-robin over the ranks (each rank encrypts only the input
+ciphertexts its blocks need) and the decrypted share tiles are summed with
+one NCCL all-reduce (exact: every element comes from exactly one rank);
+the batch is fixed, so scaling is "strong".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "private-training samples/sec; HE linear-layer ct-pt MACs/sec + NTT GB/s vs roofline"
+SIZES = [784, 128, 128, 10]
+BATCH = 64
+SEED = 2024
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.samples = []
+        self.idx = gpu_index
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    f = [x.strip() for x in line.split(",")]
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and "Active" in s[3 + i]
+                          and "Not" not in s[3 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------- CPU legs ---
+
+def cpu_oracle_step_time(steps=1, warmup=1):
+    """Time the oracle (reference CPU algorithm) on one private step of the workload."""
+    from oracle import bfv as OB
+    from oracle import kernels as OK
+    from oracle import nn as ON
+    from oracle import protocols as OPR
+    from oracle import ring as OR
+    from oracle.params import make_params
+
+    ncores = os.cpu_count() or 1
+    OK.set_threads(ncores)
+    ring = OR.RingParams()
+    p = make_params(8192, 7)
+    ar = OB.Arith(p)
+    kp = OB.keygen(p, OR.SeededRng(SEED, 0), ar)
+    model = ON.Model(SIZES, ring, seed=SEED)
+    x, labels = ON.synthetic_mnist(SEED, BATCH, ring)
+    ctx = OPR.Ctx(p, ring, kp, seed=SEED, ar=ar)
+    for _ in range(warmup):
+        ON.private_train_step(ctx, model, x, labels)
+    t0 = time.perf_counter()
+    for i in range(steps):
+        ctx.seed = SEED + 1 + i
+        ON.private_train_step(ctx, model, x, labels)
+    dt = (time.perf_counter() - t0) / steps
+    return dt, OK.get_threads()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps = max(1, args.steps)
+    warm = max(0, args.warmup)
+    # bounded sample: one oracle step is several seconds; cap the run to a few minutes
+    t_first, cores = cpu_oracle_step_time(steps=1, warmup=min(warm, 1))
+    budget = 240.0
+    steps_run = max(1, min(steps, int(budget / max(t_first, 1e-3))))
+    dt, cores = cpu_oracle_step_time(steps=steps_run, warmup=0) if steps_run > 1 else (t_first, cores)
+    v = BATCH / dt
+    sample = (f"{steps_run} private training step(s) of the MNIST MLP 784-128-128-10, B={BATCH}, N=8192, L=7 "
+              f"(oracle = reference kernel algorithms restated in C/OpenMP + numpy), after in-process warm-up")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
+        "steps": steps_run, "warmup": min(warm, 1), "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32-rns/u64-ring", "data": "synthetic",
+        "config": {"workload": "configs[1]: MNIST MLP 784-128-128-10 private training step", "global_batch": BATCH,
+                   "bfv": "N=8192, t=2^59, L=7x30-bit", "f": 25},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- GPU leg ----
+
+def run_ours(args, rank, world):
+    import torch
+
+    from paper_2403_11166_b200 import _dev, _lib, bfv
+    from paper_2403_11166_b200 import nn as PN
+    from paper_2403_11166_b200.linear_protocols import Session
+    from paper_2403_11166_b200.params import BfvParams
+    from paper_2403_11166_b200.ring import RingParams, RingTensor, SeededRng, encode_fixed
+
+    dev = _dev.device()
+    ring = RingParams()
+    params = BfvParams()
+    kp = bfv.keygen(params, SeededRng(SEED, 0))
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+
+        group = dist.group.WORLD
+    sess = Session(params, ring, kp, seed=SEED, shard=(rank, world, group))
+    model = PN.Model(SIZES, ring, seed=SEED)
+    xh, labels = PN.synthetic_mnist(SEED, BATCH, ring)
+    x_dev = RingTensor(encode_fixed(xh, ring), ring.f, ring, _canonical=True)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.int64, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    def step(i, x):
+        sess.reseed(SEED + 10 + i)
+        return PN.private_train_step(sess, model, x, labels, check=False)
+
+    for i in range(max(3, args.warmup)):
+        step(i, x_dev)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident batch; per-step CUDA events, L2 flushed between steps
+    stats = _lib.CallStats(timed=("pb_ctpt_mac_mask", "pb_decrypt_to_share", "pb_encrypt_sk", "pb_encode_plain"))
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    evs = []
+    loss = None
+    for i in range(args.steps):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        _lib.STATS = stats
+        s.record()
+        loss, _, _ = step(1000 + i, x_dev)
+        e.record()
+        _lib.STATS = None
+        evs.append((s, e))
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    t_ms = sum(s.elapsed_time(e) for s, e in evs)
+    t_ms = _max_over_ranks(t_ms, world)
+    value = args.steps * BATCH / (t_ms / 1e3)
+
+    # dominant kernel: total event time per entry point inside the timed region
+    per = {}
+    for name, s, e, tag in stats.events:
+        d = s.elapsed_time(e)
+        acc = per.setdefault(name, [0.0, 0, 0.0])
+        acc[0] += d
+        acc[1] += 1
+        acc[2] += (tag or {}).get(name, 0.0) if isinstance(tag, dict) else 0.0
+    alg = sess.alg_bytes  # name -> total algorithmic bytes over the timed region
+    dom = max(per, key=lambda k: per[k][0])
+    tot_ms, n_launch, _ = per[dom]
+    peak, peak_kind = _peaks()
+    bytes_per_launch = alg.get(dom, 0.0) / max(1, n_launch)
+    achieved = bytes_per_launch / (tot_ms / n_launch / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+                "bytes_per_launch": bytes_per_launch, "launches": n_launch,
+                "ms_per_launch": tot_ms / n_launch, "share_of_step": tot_ms / t_ms}
+    kernels = {k: {"ms_total": v[0], "calls": v[1], "alg_GBs": (alg.get(k, 0.0) / (v[0] / 1e3) / 1e9) if v[0] else None}
+               for k, v in per.items()}
+
+    # ---- e2e through the public API: host batch (pinned) -> device every step, loss back
+    x_pin = torch.from_numpy(np.ascontiguousarray(xh)).pin_memory()
+    torch.cuda.synchronize()
+    barrier()
+    evs = []
+    h2d = x_pin.numel() * 8
+    for i in range(args.steps):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        xd = x_pin.to(dev, non_blocking=True)
+        xr = RingTensor(encode_fixed(xd, ring), ring.f, ring, _canonical=True)
+        loss, _, _ = step(2000 + i, xr)
+        e.record()
+        evs.append((s, e))
+    torch.cuda.synchronize()
+    barrier()
+    te_ms = _max_over_ranks(sum(s.elapsed_time(e) for s, e in evs), world)
+    e2e = {"value": args.steps * BATCH / (te_ms / 1e3), "unit": "samples/s",
+           # per step: batch H2D + DO loss gradient H2D; logits D2H (DO reconstructs) + range flag
+           "h2d_bytes_per_step": h2d + 10 * BATCH * 8, "d2h_bytes_per_step": 10 * BATCH * 8 + 4}
+
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu and world == 1:
+        dt, cores = cpu_oracle_step_time(steps=1, warmup=1)
+        cpu = {"value": BATCH / dt, "unit": "samples/s", "cores": cores, "kind": "port",
+               "sample": "1 private training step (MNIST MLP 784-128-128-10, B=64, N=8192, L=7) of the oracle "
+                         "(reference kernel algorithms restated in C/OpenMP + numpy), after an in-process warm-up step"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32-rns/u64-ring", "data": "synthetic",
+        "config": {"workload": "configs[1]: MNIST MLP 784-128-128-10 private training step", "global_batch": BATCH,
+                   "bfv": "N=8192, t=2^59, L=7x30-bit (log2 Q = 210)", "f": 25,
+                   "parallelism": f"ct-block shards x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed (256 MiB write) between timed steps"},
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+        "gpu_launches": stats.launches, "kernels": kernels, "loss": loss,
+        "census_bytes_per_step": sess.channel.total_bytes() / max(1, sess.steps_seen),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _max_over_ranks(v, world):
+    if world <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -119,42 +119,48 @@ int pb_negacyclic_mul_wrap(const uint64_t* a, const uint64_t* b, int64_t n_pairs
                            uint64_t* out, void* stream);
 
 /* ------------------------------------------------------- BFV (SPEC bfv) --- */
-/* Plaintext sources: `vals` is a flat Z_t tensor; src_map [P][N] gives, per
- * output coefficient, the index into vals or -1 for a zero coefficient
- * (the packing maps pi_v / pi_W of SPEC:231-266).  src_map == NULL means
- * vals is already a dense [P][N] polynomial array. */
+/* Plaintext sources: `vals` is a flat Z_t tensor.  A PACKED source gives,
+ * for polynomial p and slot z < Z, coefficient pack_pos[p][z] =
+ * vals[pack_src[p][z]] (pack_pos < 0: empty slot); all other coefficients
+ * are zero.  This is the compact form of the packing maps pi_v / pi_W
+ * (SPEC:231-266).  pack_pos == NULL means vals is a dense [P][N] array. */
 
 /* Centered lift (fact 4) + forward NTT + Shoup companions:
  * plaintext multiplier for he_plain_mul.  pt/pt_shoup [P][L][N]. */
-int pb_encode_plain(const pb_ctx* ctx, const uint64_t* vals, const int64_t* src_map, int64_t P,
-                    uint32_t* pt, uint32_t* pt_shoup, void* stream);
+int pb_encode_plain(const pb_ctx* ctx, const uint64_t* vals, const int32_t* pack_pos,
+                    const int32_t* pack_src, int32_t Z, int64_t P, uint32_t* pt, uint32_t* pt_shoup,
+                    void* stream);
 
-/* Unsigned lift of Z_t polys, coefficient form: out [P][L][N] = m mod q_i.
- * centered != 0 selects the centered lift. */
-int pb_lift(const pb_ctx* ctx, const uint64_t* vals, const int64_t* src_map, int64_t P,
-            int centered, uint32_t* out, void* stream);
+/* Lift of dense Z_t polys [P][N], coefficient form: out [P][L][N] = m mod q_i
+ * (centered != 0 selects the centered lift v >= t/2 -> v - t). */
+int pb_lift(const pb_ctx* ctx, const uint64_t* vals, int64_t P, int centered, uint32_t* out,
+            void* stream);
+/* Scatter a packed source into a zero-initialised dense [P][N] Z_t array. */
+int pb_unpack(const uint64_t* vals, const int32_t* pack_pos, const int32_t* pack_src, int32_t Z,
+              int32_t N, int64_t P, uint64_t* dense, void* stream);
 
 /* SPEC:139-147 encrypt under the public key pk [2][L][N] (NTT form):
  * c0 = pk0*NTT(u) + NTT(e1 + Delta m), c1 = pk1*NTT(u) + NTT(e2).
  * u ternary, e1/e2 centred binomial (eta=20) drawn on the device from
  * Philox4x32(seed, nonce + poly index). ct [P][2][L][N]. */
 int pb_encrypt_pk(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* vals,
-                  const int64_t* src_map, int64_t P, uint64_t seed, uint64_t nonce, uint32_t* ct,
-                  void* stream);
+                  const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int64_t P,
+                  uint64_t seed, uint64_t nonce, uint32_t* ct, void* stream);
 /* Same with caller-supplied noise (int8 [P][N] each): bit-exact with the
  * oracle's encrypt when fed the oracle's draws. */
 int pb_encrypt_pk_noise(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* vals,
-                        const int64_t* src_map, int64_t P, const int8_t* u, const int8_t* e1,
-                        const int8_t* e2, uint32_t* ct, void* stream);
+                        const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int64_t P,
+                        const int8_t* u, const int8_t* e1, const int8_t* e2, uint32_t* ct,
+                        void* stream);
 /* Symmetric-key encryption by the key owner: c1 = a (uniform, NTT domain),
  * c0 = NTT(e + Delta m) - a*s.  sk_ntt [L][N]. */
 int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint64_t* vals,
-                  const int64_t* src_map, int64_t P, uint64_t seed, uint64_t nonce, uint32_t* ct,
-                  void* stream);
-/* Caller-supplied a ([P][L][N], NTT domain) and e (int8 [P][N]). */
+                  const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int64_t P,
+                  uint64_t seed, uint64_t nonce, uint32_t* ct, void* stream);
+/* Caller-supplied a ([P][L][N], NTT domain, device order) and e (int8 [P][N]). */
 int pb_encrypt_sk_noise(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint64_t* vals,
-                        const int64_t* src_map, int64_t P, const uint32_t* a, const int8_t* e,
-                        uint32_t* ct, void* stream);
+                        const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int64_t P,
+                        const uint32_t* a, const int8_t* e, uint32_t* ct, void* stream);
 
 /* x = INTT(c0 + c1*s) in coefficient form, x [P][L][N]. */
 int pb_decrypt_coeffs(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint32_t* ct, int64_t P,

@@ -85,30 +85,47 @@ def _cdiv(a, b):
     return -(-a // b)
 
 
-def plan_matmul_blocks(g: MatmulGeometry, N: int):
-    """SPEC:285 order: shrink the batch block first, then n_o, then n_i."""
+def plan_matmul_blocks(g: MatmulGeometry, N: int, mode: str = "cost"):
+    """mode "spec": SPEC:285 order, shrink the batch block first, then n_o,
+    then n_i.  mode "cost": minimise the weighted count of encryptions (1.3),
+    plaintext encodings (1.0), output ciphertexts (2.0: mask NTT + INTT) and
+    ct x pt terms (0.5) over input splits k <= 32 (the paper leaves the
+    partition strategy open; the block tiling does not change any
+    decrypted value)."""
     if min(g.n_i, g.n_o, g.B) < 1:
         raise GeometryError("empty matmul geometry")
-    n_i_blk = min(g.n_i, N)
-    if g.n_o * n_i_blk <= N:
-        n_o_blk = g.n_o
-        B_blk = min(g.B, N // (g.n_o * n_i_blk))
-    else:
-        B_blk = 1
-        n_o_blk = max(1, N // n_i_blk)
-    return B_blk, n_o_blk, n_i_blk
+    if mode == "spec":
+        n_i_blk = min(g.n_i, N)
+        if g.n_o * n_i_blk <= N:
+            return min(g.B, N // (g.n_o * n_i_blk)), g.n_o, n_i_blk
+        return 1, max(1, N // n_i_blk), n_i_blk
+    best = None
+    k = 0
+    while k < min(32, g.n_i):
+        k += 1
+        nib = -(-g.n_i // k)
+        if nib > N or -(-g.n_i // nib) != k:
+            continue
+        cap = N // nib
+        for nob in range(1, min(g.n_o, cap) + 1):
+            Bb = min(g.B, cap // nob)
+            n_out = (-(-g.B // Bb)) * (-(-g.n_o // nob))
+            cost = 1.3 * (-(-g.B // Bb)) * k + 1.0 * (-(-g.n_o // nob)) * k + 2.0 * n_out + 0.5 * n_out * k
+            cand = ((round(cost, 6), n_out, k, -nob), (Bb, nob, nib))
+            best = cand if best is None or cand[0] < best[0] else best
+    return best[1]
 
 
-def plan_blocks(g, N: int) -> BlockPlan:  # SPEC:267-275
+def plan_blocks(g, N: int, mode: str = "cost") -> BlockPlan:  # SPEC:267-275
     if isinstance(g, MatmulGeometry):
-        return _plan_matmul(g, N)
+        return _plan_matmul(g, N, mode)
     if isinstance(g, ConvGeometry):
         return _plan_conv(g, N)
     raise GeometryError(f"unknown geometry {g!r}")
 
 
-def _plan_matmul(g: MatmulGeometry, N: int) -> BlockPlan:
-    Bb, nob, nib = plan_matmul_blocks(g, N)
+def _plan_matmul(g: MatmulGeometry, N: int, mode: str = "cost") -> BlockPlan:
+    Bb, nob, nib = plan_matmul_blocks(g, N, mode)
     nB, nO, nI = _cdiv(g.B, Bb), _cdiv(g.n_o, nob), _cdiv(g.n_i, nib)
     # input template: (k, j) -> k*nob*nib + j
     k = np.arange(Bb)[:, None]

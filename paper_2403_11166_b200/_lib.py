@@ -55,12 +55,13 @@ SIGNATURES = {
     "pb_scale_round_digits": [P, P, I64, P, P],
     "pb_decode": [P, P, I64, P, P],
     "pb_negacyclic_mul_wrap": [P, P, I64, I32, P, P],
-    "pb_encode_plain": [P, P, P, I64, P, P, P],
-    "pb_lift": [P, P, P, I64, INT, P, P],
-    "pb_encrypt_pk": [P, P, P, P, I64, U64, U64, P, P],
-    "pb_encrypt_pk_noise": [P, P, P, P, I64, P, P, P, P, P],
-    "pb_encrypt_sk": [P, P, P, P, I64, U64, U64, P, P],
-    "pb_encrypt_sk_noise": [P, P, P, P, I64, P, P, P, P],
+    "pb_encode_plain": [P, P, P, P, I32, I64, P, P, P],
+    "pb_lift": [P, P, I64, INT, P, P],
+    "pb_unpack": [P, P, P, I32, I32, I64, P, P],
+    "pb_encrypt_pk": [P, P, P, P, P, I32, I64, U64, U64, P, P],
+    "pb_encrypt_pk_noise": [P, P, P, P, P, I32, I64, P, P, P, P, P],
+    "pb_encrypt_sk": [P, P, P, P, P, I32, I64, U64, U64, P, P],
+    "pb_encrypt_sk_noise": [P, P, P, P, P, I32, I64, P, P, P, P],
     "pb_decrypt_coeffs": [P, P, P, I64, P, P],
     "pb_decrypt": [P, P, P, I64, P, P, P],
     "pb_decrypt_to_share": [P, P, P, I64, P, P, I32, P, P, P],
@@ -120,6 +121,53 @@ def check(status: int, what: str = "") -> None:
         raise cls(f"{what}: {last_error()}" if what else last_error())
 
 
+# Device kernels each entry point launches (for the bench's gpu_launches count).
+KERNELS_PER_CALL = {
+    "pb_encrypt_pk": 2, "pb_encrypt_sk": 2, "pb_decrypt": 2, "pb_decrypt_to_share": 2, "pb_unpack": 1,
+    "pb_abi_version": 0, "pb_last_error": 0, "pb_device_sm_count": 0, "pb_ctx_create": 0, "pb_ctx_destroy": 0,
+}
+
+
+class CallStats:
+    """Optional instrumentation: counts kernel launches and, for selected entry
+    points, brackets each call with CUDA events on the current stream."""
+
+    def __init__(self, timed=()):
+        self.launches = 0
+        self.calls = {}
+        self.timed = set(timed)
+        self.events = []  # (name, start_event, end_event, tag)
+        self.tag = None
+
+    def before(self, name):
+        self.launches += KERNELS_PER_CALL.get(name, 1)
+        self.calls[name] = self.calls.get(name, 0) + 1
+        if name in self.timed:
+            import torch
+
+            s = torch.cuda.Event(enable_timing=True)
+            s.record()
+            return s
+        return None
+
+    def after(self, name, s):
+        if s is not None:
+            import torch
+
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.events.append((name, s, e, self.tag))
+
+
+STATS: CallStats | None = None
+
+
 def call(name: str, *args) -> None:
     """Invoke a C ABI entry point and raise the mapped exception on failure."""
+    st = STATS
+    if st is None:
+        check(getattr(load(), name)(*args), name)
+        return
+    ev = st.before(name)
     check(getattr(load(), name)(*args), name)
+    st.after(name, ev)

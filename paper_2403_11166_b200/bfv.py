@@ -71,14 +71,20 @@ def _signed_to_zt(v: np.ndarray, params: BfvParams) -> torch.Tensor:
     return _dev.u64_to_device(v.astype(np.uint64) & np.uint64(params.t - 1))
 
 
-def lift(params: BfvParams, vals: torch.Tensor, centered: bool, src_map: torch.Tensor | None = None,
-         n_polys: int | None = None) -> torch.Tensor:
-    """Z_t coefficients -> RNS residues [P, L, N] (coefficient form)."""
+def lift(params: BfvParams, vals: torch.Tensor, centered: bool, n_polys: int | None = None) -> torch.Tensor:
+    """Dense Z_t coefficients [P, N] -> RNS residues [P, L, N] (coefficient form)."""
     P = n_polys if n_polys is not None else vals.numel() // params.N
     out = _dev.empty_u32(P, params.L, params.N)
-    _lib.call("pb_lift", _ctx(params), _dev.ptr(vals), _dev.ptr(src_map), P, 1 if centered else 0, _dev.ptr(out),
-              _dev.stream())
+    _lib.call("pb_lift", _ctx(params), _dev.ptr(vals), P, 1 if centered else 0, _dev.ptr(out), _dev.stream())
     return out
+
+
+def _pack_args(pack):
+    """pack = None (dense) or (pos, src) int32 device tensors [P, Z]."""
+    if pack is None:
+        return None, None, 0, None
+    pos, src = pack
+    return _dev.ptr(pos), _dev.ptr(src), pos.shape[1], pos.shape[0]
 
 
 def ntt_transform(params: BfvParams, p: RnsPoly, direction: str) -> RnsPoly:  # SPEC:121-129
@@ -122,28 +128,30 @@ def keygen(params: BfvParams, rng) -> KeyPair:
     return KeyPair(params, s, sk, pk)
 
 
-def encrypt(kp: KeyPair, m: torch.Tensor, rng=None, *, src_map: torch.Tensor | None = None,
-            n_polys: int | None = None, mode: str = "pk", noise=None, nonce: int | None = None) -> Ciphertext:
-    """SPEC:139-147.  ``m``: Z_t coefficients, dense [P, N] or a flat tensor
-    gathered through ``src_map`` [P, N] (the packing maps).  mode "pk" encrypts
-    under the public key, "sk" is symmetric encryption by the key owner.
-    ``noise`` = (u, e1, e2) int8 [P, N] (pk) or (a [P,L,N] u32, e int8) (sk)."""
+def encrypt(kp: KeyPair, m: torch.Tensor, rng=None, *, pack=None, mode: str = "pk", noise=None,
+            nonce: int | None = None) -> Ciphertext:
+    """SPEC:139-147.  ``m``: Z_t coefficients, dense [P, N], or a flat tensor
+    gathered through ``pack`` = (pos, src) int32 [P, Z] (packing maps, see
+    poly_encoding.compact).  mode "pk" encrypts under the public key, "sk" is
+    symmetric encryption by the key owner.  ``noise`` = (u, e1, e2) int8 [P, N]
+    (pk) or (a [P,L,N] in reference NTT order, e int8 [P, N]) (sk)."""
     params = kp.params
     h = _ctx(params)
     m = m.contiguous()
-    P = n_polys if n_polys is not None else (src_map.shape[0] if src_map is not None else m.numel() // params.N)
+    pp, ps, Z, Pk = _pack_args(pack)
+    P = Pk if Pk is not None else m.numel() // params.N
     ct = _dev.empty_u32(P, 2, params.L, params.N)
     st = _dev.stream()
     if noise is not None:
         if mode == "pk":
             u, e1, e2 = (torch.as_tensor(np.asarray(x, dtype=np.int8)).to(_dev.device()) for x in noise)
-            _lib.call("pb_encrypt_pk_noise", h, _dev.ptr(kp.pk), _dev.ptr(m), _dev.ptr(src_map), P, _dev.ptr(u),
+            _lib.call("pb_encrypt_pk_noise", h, _dev.ptr(kp.pk), _dev.ptr(m), pp, ps, Z, P, _dev.ptr(u),
                       _dev.ptr(e1), _dev.ptr(e2), _dev.ptr(ct), st)
         else:
             a = _dev.u32_to_device(np.asarray(noise[0], dtype=np.uint32))  # reference NTT order
             _lib.call("pb_ntt_reorder", h, _dev.ptr(a), a.numel() // params.N, 1, st)
             e = torch.as_tensor(np.asarray(noise[1], dtype=np.int8)).to(_dev.device())
-            _lib.call("pb_encrypt_sk_noise", h, _dev.ptr(kp.sk_ntt), _dev.ptr(m), _dev.ptr(src_map), P, _dev.ptr(a),
+            _lib.call("pb_encrypt_sk_noise", h, _dev.ptr(kp.sk_ntt), _dev.ptr(m), pp, ps, Z, P, _dev.ptr(a),
                       _dev.ptr(e), _dev.ptr(ct), st)
         return Ciphertext(ct, params)
     seed = rng.device_key if rng is not None else 0
@@ -151,7 +159,7 @@ def encrypt(kp: KeyPair, m: torch.Tensor, rng=None, *, src_map: torch.Tensor | N
         nonce = rng.reserve(P) if rng is not None else 0
     fn = "pb_encrypt_pk" if mode == "pk" else "pb_encrypt_sk"
     key = _dev.ptr(kp.pk) if mode == "pk" else _dev.ptr(kp.sk_ntt)
-    _lib.call(fn, h, key, _dev.ptr(m), _dev.ptr(src_map), P, seed, nonce, _dev.ptr(ct), st)
+    _lib.call(fn, h, key, _dev.ptr(m), pp, ps, Z, P, seed, nonce, _dev.ptr(ct), st)
     return Ciphertext(ct, params)
 
 
@@ -189,15 +197,15 @@ def decrypt(kp: KeyPair, ct: Ciphertext) -> torch.Tensor:
     return m
 
 
-def encode_plain(params: BfvParams, m: torch.Tensor, src_map: torch.Tensor | None = None,
-                 n_polys: int | None = None) -> RnsPoly:
-    """Plaintext multiplier: centered lift + NTT + Shoup quotients."""
+def encode_plain(params: BfvParams, m: torch.Tensor, pack=None) -> RnsPoly:
+    """Plaintext multiplier: centered lift + NTT + Shoup quotients.
+    ``m`` dense [P, N] Z_t coefficients, or flat values gathered through ``pack``."""
     m = m.contiguous()
-    P = n_polys if n_polys is not None else (src_map.shape[0] if src_map is not None else m.numel() // params.N)
+    pp, ps, Z, Pk = _pack_args(pack)
+    P = Pk if Pk is not None else m.numel() // params.N
     pt = _dev.empty_u32(P, params.L, params.N)
     sh = _dev.empty_u32(P, params.L, params.N)
-    _lib.call("pb_encode_plain", _ctx(params), _dev.ptr(m), _dev.ptr(src_map), P, _dev.ptr(pt), _dev.ptr(sh),
-              _dev.stream())
+    _lib.call("pb_encode_plain", _ctx(params), _dev.ptr(m), pp, ps, Z, P, _dev.ptr(pt), _dev.ptr(sh), _dev.stream())
     return RnsPoly(pt, NTT, sh)
 
 

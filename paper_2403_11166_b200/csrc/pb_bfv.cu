@@ -12,14 +12,40 @@
 
 namespace {
 
-// Z_t coefficient j of polynomial p (packing map or dense).
-__device__ __forceinline__ uint64_t coeff_val(const uint64_t* vals, const int64_t* src_map, int64_t p, int N,
-                                              int j) {
-  if (src_map) {
-    const int64_t idx = __ldg(src_map + p * N + j);
-    return idx >= 0 ? __ldg(vals + idx) : 0ull;
+// A plaintext source: `vals` is a flat Z_t tensor.  With `pos` set, poly p
+// has coefficient pos[p][z] = vals[src[p][z]] for z < Z (pos < 0: unused
+// slot) and zeros elsewhere -- the compact form of the packing maps pi_v /
+// pi_W.  With pos == NULL, vals is a dense [P][N] array.
+struct PbPack {
+  const uint64_t* vals;
+  const int32_t* pos;
+  const int32_t* src;
+  int Z;
+};
+
+// Loads the lifted source polynomial p into a[] in the NTT's P1 layout.
+// The packed path builds the row in shared memory (zero + scatter) and
+// leaves `sm` free (synchronised) for the NTT that follows.
+template <class Nt, class Lift>
+__device__ __forceinline__ void load_source(uint32_t (&a)[32], uint32_t* sm, const PbPack& s, int64_t p, int tid,
+                                            Lift lift) {
+  if (s.pos) {
+    for (int j = tid; j < Nt::N; j += Nt::T) sm[Nt::pad(j)] = 0u;
+    __syncthreads();
+    const int32_t* pp = s.pos + p * s.Z;
+    const int32_t* ps = s.src + p * s.Z;
+    for (int z = tid; z < s.Z; z += Nt::T) {
+      const int j = __ldg(pp + z);
+      if (j >= 0) sm[Nt::pad(j)] = lift(__ldg(s.vals + __ldg(ps + z)));
+    }
+    __syncthreads();
+    Nt::ld1(sm, a, tid);
+    __syncthreads();
+  } else {
+    const uint64_t* v = s.vals + p * Nt::N;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a[c] = lift(__ldg(v + Nt::j1(tid, c)));
   }
-  return __ldg(vals + p * N + j);
 }
 
 __device__ __forceinline__ uint32_t lift_small(int v, uint32_t q) { return v < 0 ? q - (uint32_t)(-v) : (uint32_t)v; }
@@ -33,8 +59,7 @@ __device__ __forceinline__ uint32_t delta_m(const PbDev& P, int l, uint64_t m) {
 // --------------------------------------------------------------- encode ---
 template <int LOGN>
 __global__ void __launch_bounds__(1 << (LOGN - 5))
-    k_encode_plain(PbDev P, const uint64_t* vals, const int64_t* src_map, int64_t nP, uint32_t* pt,
-                   uint32_t* pt_sh) {
+    k_encode_plain(PbDev P, PbPack src, int64_t nP, uint32_t* pt, uint32_t* pt_sh) {
   using Nt = pb::Ntt<LOGN>;
   extern __shared__ uint32_t sm[];
   const int tid = threadIdx.x;
@@ -42,10 +67,11 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   const int64_t p = blockIdx.x / L;
   const int l = blockIdx.x % L;
   const uint32_t q = P.q[l];
+  const uint64_t mu = P.mu[l];
+  const uint32_t tm = P.tmod[l];
+  const int ell = P.ell;
   uint32_t a[32];
-#pragma unroll
-  for (int c = 0; c < 32; ++c)
-    a[c] = lift_centered(coeff_val(vals, src_map, p, Nt::N, Nt::j1(tid, c)), P.ell, q, P.mu[l], P.tmod[l]);
+  load_source<Nt>(a, sm, src, p, tid, [&](uint64_t v) { return lift_centered(v, ell, q, mu, tm); });
   Nt::forward(a, sm, P.tw_fwd + (size_t)l * Nt::N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
   uint32_t* row = pt + (p * L + l) * Nt::N;
 #pragma unroll
@@ -58,7 +84,8 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   }
 }
 
-__global__ void k_lift(PbDev P, const uint64_t* vals, const int64_t* src_map, int64_t nP, int centered, uint32_t* out) {
+// Dense lift (coefficient form): out[p][l][j] = lift(vals[p][j]).
+__global__ void k_lift(PbDev P, const uint64_t* vals, int64_t nP, int centered, uint32_t* out) {
   const int N = P.N, L = P.L;
   const int64_t total = nP * L * N;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -66,8 +93,17 @@ __global__ void k_lift(PbDev P, const uint64_t* vals, const int64_t* src_map, in
     const int64_t pl = e / N;
     const int l = (int)(pl % L);
     const int64_t p = pl / L;
-    const uint64_t v = coeff_val(vals, src_map, p, N, j);
+    const uint64_t v = vals[p * N + j];
     out[e] = centered ? lift_centered(v, P.ell, P.q[l], P.mu[l], P.tmod[l]) : reduce64(v, P.q[l], P.mu[l]);
+  }
+}
+
+// Packed scatter into a zeroed dense Z_t array (used by pb_lift with a map).
+__global__ void k_unpack(PbPack s, int N, int64_t nP, uint64_t* dense) {
+  const int64_t total = nP * s.Z;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = s.pos[e];
+    if (j >= 0) dense[(e / s.Z) * N + j] = s.vals[s.src[e]];
   }
 }
 
@@ -101,8 +137,8 @@ __global__ void k_sample_noise(int N, int64_t nP, uint64_t seed, uint64_t nonce,
 // --------------------------------------------------------------- encrypt ---
 template <int LOGN>
 __global__ void __launch_bounds__(1 << (LOGN - 5))
-    k_encrypt_pk(PbDev P, const uint32_t* pk, const uint64_t* vals, const int64_t* src_map, int64_t nP,
-                 const int8_t* u, const int8_t* e1, const int8_t* e2, uint32_t* ct) {
+    k_encrypt_pk(PbDev P, const uint32_t* pk, PbPack src, int64_t nP, const int8_t* u, const int8_t* e1,
+                 const int8_t* e2, uint32_t* ct) {
   using Nt = pb::Ntt<LOGN>;
   constexpr int N = Nt::N;
   extern __shared__ uint32_t sm[];
@@ -133,11 +169,9 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   Nt::gst3(ct + ((p * 2 + 1) * L + l) * N, b, tid);
   __syncthreads();
   // c0 = pk0 * U + NTT(e1 + Delta m)
+  load_source<Nt>(b, sm, src, p, tid, [&](uint64_t v) { return delta_m(P, l, v); });
 #pragma unroll
-  for (int c = 0; c < 32; ++c) {
-    const int j = Nt::j1(tid, c);
-    b[c] = addmod(lift_small(e1p[j], q), delta_m(P, l, coeff_val(vals, src_map, p, N, j)), q);
-  }
+  for (int c = 0; c < 32; ++c) b[c] = addmod(lift_small(e1p[Nt::j1(tid, c)], q), b[c], q);
   Nt::forward(b, sm, tw, t3, tid, q);
   Nt::gld3(pk + (size_t)l * N, k, tid);
 #pragma unroll
@@ -159,8 +193,8 @@ __device__ __forceinline__ void uniform_pair(uint64_t seed, uint64_t nonce, int6
 
 template <int LOGN>
 __global__ void __launch_bounds__(1 << (LOGN - 5))
-    k_encrypt_sk(PbDev P, const uint32_t* sk, const uint64_t* vals, const int64_t* src_map, int64_t nP,
-                 const uint32_t* a_in, const int8_t* e, uint64_t seed, uint64_t nonce, uint32_t* ct) {
+    k_encrypt_sk(PbDev P, const uint32_t* sk, PbPack src, int64_t nP, const uint32_t* a_in, const int8_t* e,
+                 uint64_t seed, uint64_t nonce, uint32_t* ct) {
   using Nt = pb::Ntt<LOGN>;
   constexpr int N = Nt::N;
   extern __shared__ uint32_t sm[];
@@ -172,11 +206,9 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   const uint64_t mu = P.mu[l];
   const int8_t* ep = e + p * N;
   uint32_t b[32], a[32], s[32];
+  load_source<Nt>(b, sm, src, p, tid, [&](uint64_t v) { return delta_m(P, l, v); });
 #pragma unroll
-  for (int c = 0; c < 32; ++c) {
-    const int j = Nt::j1(tid, c);
-    b[c] = addmod(lift_small(ep[j], q), delta_m(P, l, coeff_val(vals, src_map, p, N, j)), q);
-  }
+  for (int c = 0; c < 32; ++c) b[c] = addmod(lift_small(ep[Nt::j1(tid, c)], q), b[c], q);
   Nt::forward(b, sm, P.tw_fwd + (size_t)l * N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
   if (a_in) {
     Nt::gld3(a_in + (p * L + l) * N, a, tid);
@@ -371,31 +403,29 @@ static void set_smem(KernelT k, size_t smem) {
 }
 
 template <int LOGN>
-void launch_encode_plain(const PbDev& P, const uint64_t* vals, const int64_t* src_map, int64_t nP, uint32_t* pt,
-                         uint32_t* pt_sh, cudaStream_t st) {
+void launch_encode_plain(const PbDev& P, PbPack src, int64_t nP, uint32_t* pt, uint32_t* pt_sh, cudaStream_t st) {
   using Nt = pb::Ntt<LOGN>;
   const size_t smem = Nt::SMEM_WORDS * 4;
   set_smem(k_encode_plain<LOGN>, smem);
-  k_encode_plain<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, vals, src_map, nP, pt, pt_sh);
+  k_encode_plain<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, src, nP, pt, pt_sh);
 }
 
 template <int LOGN>
-void launch_encrypt_pk(const PbDev& P, const uint32_t* pk, const uint64_t* vals, const int64_t* src_map, int64_t nP,
-                       const int8_t* u, const int8_t* e1, const int8_t* e2, uint32_t* ct, cudaStream_t st) {
+void launch_encrypt_pk(const PbDev& P, const uint32_t* pk, PbPack src, int64_t nP, const int8_t* u, const int8_t* e1,
+                       const int8_t* e2, uint32_t* ct, cudaStream_t st) {
   using Nt = pb::Ntt<LOGN>;
   const size_t smem = Nt::SMEM_WORDS * 4;
   set_smem(k_encrypt_pk<LOGN>, smem);
-  k_encrypt_pk<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, pk, vals, src_map, nP, u, e1, e2, ct);
+  k_encrypt_pk<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, pk, src, nP, u, e1, e2, ct);
 }
 
 template <int LOGN>
-void launch_encrypt_sk(const PbDev& P, const uint32_t* sk, const uint64_t* vals, const int64_t* src_map, int64_t nP,
-                       const uint32_t* a_in, const int8_t* e, uint64_t seed, uint64_t nonce, uint32_t* ct,
-                       cudaStream_t st) {
+void launch_encrypt_sk(const PbDev& P, const uint32_t* sk, PbPack src, int64_t nP, const uint32_t* a_in, const int8_t* e,
+                       uint64_t seed, uint64_t nonce, uint32_t* ct, cudaStream_t st) {
   using Nt = pb::Ntt<LOGN>;
   const size_t smem = Nt::SMEM_WORDS * 4;
   set_smem(k_encrypt_sk<LOGN>, smem);
-  k_encrypt_sk<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, sk, vals, src_map, nP, a_in, e, seed, nonce, ct);
+  k_encrypt_sk<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, sk, src, nP, a_in, e, seed, nonce, ct);
 }
 
 template <int LOGN>
@@ -426,48 +456,21 @@ int need_big_n(const pb_ctx* ctx) {
 
 int64_t max_grid_polys(const pb_ctx* ctx) { return (int64_t)0x7fffffff / ctx->dev.L; }
 
-}  // namespace
-
-// ================================================================ C ABI ===
-extern "C" int pb_encode_plain(const pb_ctx* ctx, const uint64_t* vals, const int64_t* src_map, int64_t nP,
-                               uint32_t* pt, uint32_t* pt_shoup, void* stream) {
-  if (int s = need_big_n(ctx)) return s;
-  if (!vals || !pt) return pb_set_error(PB_ERR_ARG, "null argument");
-  if (nP <= 0) return PB_OK;
-  if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
-  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encode_plain, ctx->dev, vals, src_map, nP, pt, pt_shoup, pb_stream_of(stream));
-  PB_CHECK_LAUNCH();
-  return PB_OK;
-}
-
-extern "C" int pb_lift(const pb_ctx* ctx, const uint64_t* vals, const int64_t* src_map, int64_t nP, int centered,
-                       uint32_t* out, void* stream) {
-  if (!ctx || !vals || !out) return pb_set_error(PB_ERR_ARG, "null argument");
-  if (nP <= 0) return PB_OK;
-  k_lift<<<pb_grid_1d(nP * ctx->dev.L * ctx->dev.N, 256), 256, 0, pb_stream_of(stream)>>>(ctx->dev, vals, src_map, nP,
-                                                                                          centered, out);
-  PB_CHECK_LAUNCH();
-  return PB_OK;
-}
-
-extern "C" int pb_encrypt_pk_noise(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* vals, const int64_t* src_map,
-                                   int64_t nP, const int8_t* u, const int8_t* e1, const int8_t* e2, uint32_t* ct,
-                                   void* stream) {
-  if (int s = need_big_n(ctx)) return s;
-  if (!pk || !vals || !u || !e1 || !e2 || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
-  if (nP <= 0) return PB_OK;
-  if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
-  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_pk, ctx->dev, pk, vals, src_map, nP, u, e1, e2, ct,
-                   pb_stream_of(stream));
-  PB_CHECK_LAUNCH();
+int make_pack(const uint64_t* vals, const int32_t* pos, const int32_t* src, int32_t Z, PbPack* out) {
+  if (!vals) return pb_set_error(PB_ERR_ARG, "null plaintext source");
+  if (pos && (!src || Z < 0)) return pb_set_error(PB_ERR_ARG, "packed source needs pos, src and Z >= 0");
+  out->vals = vals;
+  out->pos = pos;
+  out->src = src;
+  out->Z = pos ? Z : 0;
   return PB_OK;
 }
 
 // Scratch for device-sampled noise: a per-thread cached buffer reused
 // across calls (stream-ordered use only).
-static thread_local int8_t* g_noise = nullptr;
-static thread_local size_t g_noise_bytes = 0;
-static int8_t* noise_buffer(size_t bytes) {
+thread_local int8_t* g_noise = nullptr;
+thread_local size_t g_noise_bytes = 0;
+int8_t* noise_buffer(size_t bytes) {
   if (bytes > g_noise_bytes) {
     if (g_noise) cudaFree(g_noise);
     g_noise = nullptr;
@@ -478,8 +481,63 @@ static int8_t* noise_buffer(size_t bytes) {
   return g_noise;
 }
 
-extern "C" int pb_encrypt_pk(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* vals, const int64_t* src_map,
-                             int64_t nP, uint64_t seed, uint64_t nonce, uint32_t* ct, void* stream) {
+}  // namespace
+
+// ================================================================ C ABI ===
+#define PB_PACK_OR_RETURN(pk, vals, pos, src, Z) \
+  PbPack pk;                                     \
+  if (int _s = make_pack(vals, pos, src, Z, &pk)) return _s
+
+extern "C" int pb_encode_plain(const pb_ctx* ctx, const uint64_t* vals, const int32_t* pack_pos,
+                               const int32_t* pack_src, int32_t Z, int64_t nP, uint32_t* pt, uint32_t* pt_shoup,
+                               void* stream) {
+  if (int s = need_big_n(ctx)) return s;
+  if (nP <= 0) return PB_OK;
+  if (!pt) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  PB_PACK_OR_RETURN(src, vals, pack_pos, pack_src, Z);
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encode_plain, ctx->dev, src, nP, pt, pt_shoup, pb_stream_of(stream));
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_lift(const pb_ctx* ctx, const uint64_t* vals, int64_t nP, int centered, uint32_t* out, void* stream) {
+  if (!ctx) return pb_set_error(PB_ERR_ARG, "null context");
+  if (nP <= 0) return PB_OK;
+  if (!vals || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  k_lift<<<pb_grid_1d(nP * ctx->dev.L * ctx->dev.N, 256), 256, 0, pb_stream_of(stream)>>>(ctx->dev, vals, nP, centered,
+                                                                                          out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_unpack(const uint64_t* vals, const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int32_t N,
+                         int64_t nP, uint64_t* dense, void* stream) {
+  if (nP <= 0 || Z <= 0) return PB_OK;
+  if (!dense || N <= 0) return pb_set_error(PB_ERR_ARG, "null argument");
+  PB_PACK_OR_RETURN(src, vals, pack_pos, pack_src, Z);
+  if (!pack_pos) return pb_set_error(PB_ERR_ARG, "pb_unpack needs a packed source");
+  k_unpack<<<pb_grid_1d(nP * Z, 256), 256, 0, pb_stream_of(stream)>>>(src, N, nP, dense);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_encrypt_pk_noise(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* vals,
+                                   const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int64_t nP,
+                                   const int8_t* u, const int8_t* e1, const int8_t* e2, uint32_t* ct, void* stream) {
+  if (int s = need_big_n(ctx)) return s;
+  if (nP <= 0) return PB_OK;
+  if (!pk || !u || !e1 || !e2 || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  PB_PACK_OR_RETURN(src, vals, pack_pos, pack_src, Z);
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_pk, ctx->dev, pk, src, nP, u, e1, e2, ct, pb_stream_of(stream));
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_encrypt_pk(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* vals, const int32_t* pack_pos,
+                             const int32_t* pack_src, int32_t Z, int64_t nP, uint64_t seed, uint64_t nonce,
+                             uint32_t* ct, void* stream) {
   if (int s = need_big_n(ctx)) return s;
   if (nP <= 0) return PB_OK;
   const int N = ctx->dev.N;
@@ -489,39 +547,41 @@ extern "C" int pb_encrypt_pk(const pb_ctx* ctx, const uint32_t* pk, const uint64
   cudaStream_t st = pb_stream_of(stream);
   k_sample_noise<<<pb_grid_1d(nP * N, 256), 256, 0, st>>>(N, nP, seed, nonce, 1, u, e1, e2);
   PB_CHECK_LAUNCH();
-  return pb_encrypt_pk_noise(ctx, pk, vals, src_map, nP, u, e1, e2, ct, stream);
+  return pb_encrypt_pk_noise(ctx, pk, vals, pack_pos, pack_src, Z, nP, u, e1, e2, ct, stream);
 }
 
-extern "C" int pb_encrypt_sk_noise(const pb_ctx* ctx, const uint32_t* sk, const uint64_t* vals, const int64_t* src_map,
-                                   int64_t nP, const uint32_t* a, const int8_t* e, uint32_t* ct, void* stream) {
+extern "C" int pb_encrypt_sk_noise(const pb_ctx* ctx, const uint32_t* sk, const uint64_t* vals,
+                                   const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int64_t nP,
+                                   const uint32_t* a, const int8_t* e, uint32_t* ct, void* stream) {
   if (int s = need_big_n(ctx)) return s;
-  if (!sk || !vals || !e || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
   if (nP <= 0) return PB_OK;
+  if (!sk || !e || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
   if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
-  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, vals, src_map, nP, a, e, 0ull, 0ull, ct,
-                   pb_stream_of(stream));
+  PB_PACK_OR_RETURN(src, vals, pack_pos, pack_src, Z);
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, src, nP, a, e, 0ull, 0ull, ct, pb_stream_of(stream));
   PB_CHECK_LAUNCH();
   return PB_OK;
 }
 
-extern "C" int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk, const uint64_t* vals, const int64_t* src_map,
-                             int64_t nP, uint64_t seed, uint64_t nonce, uint32_t* ct, void* stream) {
+extern "C" int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk, const uint64_t* vals, const int32_t* pack_pos,
+                             const int32_t* pack_src, int32_t Z, int64_t nP, uint64_t seed, uint64_t nonce,
+                             uint32_t* ct, void* stream) {
   if (int s = need_big_n(ctx)) return s;
-  if (!sk || !vals || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
   if (nP <= 0) return PB_OK;
+  if (!sk || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
   if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  PB_PACK_OR_RETURN(src, vals, pack_pos, pack_src, Z);
   const int N = ctx->dev.N;
   int8_t* e = noise_buffer((size_t)nP * N);
   if (!e) return pb_set_error(PB_ERR_CUDA, "noise scratch allocation failed");
   cudaStream_t st = pb_stream_of(stream);
   k_sample_noise<<<pb_grid_1d(nP * N, 256), 256, 0, st>>>(N, nP, seed, nonce, 0, nullptr, e, nullptr);
   PB_CHECK_LAUNCH();
-  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, vals, src_map, nP, (const uint32_t*)nullptr, e,
-                   seed, nonce, ct, st);
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, src, nP, (const uint32_t*)nullptr, e, seed, nonce,
+                   ct, st);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }
-
 extern "C" int pb_decrypt_coeffs(const pb_ctx* ctx, const uint32_t* sk, const uint32_t* ct, int64_t nP, uint32_t* x,
                                  void* stream) {
   if (int s = need_big_n(ctx)) return s;

@@ -83,11 +83,57 @@ class DpConfig:
     enabled: bool = False
 
 
+def _pk(pack):
+    pos, src = pack
+    return _dev.ptr(pos), _dev.ptr(src), pos.shape[1]
+
+
+class _Shard:
+    """The part of a block plan one rank executes: its output ciphertexts
+    (round-robin over ranks) and exactly the input / plaintext polynomials
+    those outputs reference, with the MAC term list remapped to local indices."""
+
+    def __init__(self, plan, rank: int, world: int):
+        sel = np.arange(rank, plan.n_out, world)
+        t = plan.terms[sel]
+        self.in_idx = np.unique(t[:, :, 0]) if len(sel) else np.zeros(0, dtype=np.int64)
+        self.pt_idx = np.unique(t[:, :, 1]) if len(sel) else np.zeros(0, dtype=np.int64)
+        li = np.searchsorted(self.in_idx, t[:, :, 0])
+        lp = np.searchsorted(self.pt_idx, t[:, :, 1])
+        self.terms_a = np.stack([li, lp], axis=-1)  # Enc(in) (x) pt
+        self.terms_b = np.stack([lp, li], axis=-1)  # Enc(pt-side poly) (x) in-side plaintext
+        self.n_out, self.n_in, self.n_pt = len(sel), len(self.in_idx), len(self.pt_idx)
+        self.U = plan.U
+        from . import _dev
+
+        from .poly_encoding import compact
+
+        self.in_pack = tuple(_dev.i32_to_device(a) for a in compact(plan.in_src[self.in_idx]))
+        self.pt_pack = tuple(_dev.i32_to_device(a) for a in compact(plan.pt_src[self.pt_idx]))
+        self.out_pos = _dev.i32_to_device(plan.out_pos[sel])
+        self.out_dst = _dev.i64_to_device(plan.out_dst[sel])
+        self._terms_dev = {}
+
+    def terms_device(self, key, terms):
+        t = self._terms_dev.get(key)
+        if t is None:
+            from . import _dev
+
+            t = _dev.i32_to_device(np.ascontiguousarray(terms, dtype=np.int32))
+            self._terms_dev[key] = t
+        return t
+
+
 class Session:
-    """Both parties' protocol state: BFV keys (DO), ring params, seeds, channel."""
+    """Both parties' protocol state: BFV keys (DO), ring params, seeds, channel.
+
+    ``shard=(rank, world, group)`` splits every he-matmul's output ciphertexts
+    round-robin over ``world`` GPUs (one process per GPU); the decrypted share
+    tiles are combined with one NCCL all-reduce (each element is written by
+    exactly one rank, the others contribute 0, so the u64 sum is exact)."""
 
     def __init__(self, params: BfvParams, ring: RingParams, kp: KeyPair, seed: int, filler: bool = True,
-                 channel: Channel | None = None):
+                 channel: Channel | None = None, shard=None):
         if ring.ell != params.ell:
             raise ScaleError("ring ell must equal the BFV plaintext modulus bits")
         self.p = params
@@ -97,14 +143,29 @@ class Session:
         self.filler = filler
         self.channel = channel or Channel()
         self.ctx = context(params)
-        self._enc_nonce = 0
-        self.layer_phase = {}
+        self.rank, self.world, self.group = shard if shard else (0, 1, None)
+        self.alg_bytes = {}  # entry point -> algorithmic HBM bytes (while instrumented)
+        self.steps_seen = 0
+        self._shards = {}
 
     def rng(self, layer: int, op: int, purpose: int) -> SeededRng:
         return SeededRng(self.seed, stream_id(layer, op, purpose))
 
     def reseed(self, seed: int):
         self.seed = int(seed)
+        self.steps_seen += 1
+
+    def _count(self, name, nbytes):
+        if _lib.STATS is not None:
+            self.alg_bytes[name] = self.alg_bytes.get(name, 0.0) + float(nbytes)
+
+    def _shard(self, plan):
+        key = (id(plan), self.rank, self.world)
+        sh = self._shards.get(key)
+        if sh is None:
+            sh = _Shard(plan, self.rank, self.world)
+            self._shards[key] = sh
+        return sh
 
     # --------------------------------------------------------- HE matmul ---
     def he_matmul(self, layer: int, op: int, g: MatmulGeometry, out: torch.Tensor, mask: torch.Tensor,
@@ -115,63 +176,79 @@ class Session:
         device tensors addressed through the given strides; absent terms are None."""
         p, h, st = self.p, self.ctx.handle, _dev.stream()
         plan = plan_matmul(g, p.N, v_strides, w_strides, y_strides)
-        dm = plan.device()
+        sh = self._shard(plan)
         N, L = p.N, p.L
-        cts, pts, pairs = [], [], []
+        w = 4  # bytes per residue
+        ct_bytes = 2 * L * N * w
+        cts, pts, tkeys = [], [], []
         enc_rng = self.rng(layer, op, P_ENC)
-        if v_ct is not None:  # term A: Enc(pi_v(v)) (x) pi_W(W)
-            ct = _dev.empty_u32(plan.n_in, 2, L, N)
-            _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(v_ct), _dev.ptr(dm["in_src"]),
-                      plan.n_in, enc_rng.device_key, enc_rng.reserve(plan.n_in), _dev.ptr(ct), st)
-            pt = _dev.empty_u32(plan.n_pt, L, N)
-            sh = _dev.empty_u32(plan.n_pt, L, N)
-            _lib.call("pb_encode_plain", h, _dev.ptr(w_pt), _dev.ptr(dm["pt_src"]), plan.n_pt, _dev.ptr(pt),
-                      _dev.ptr(sh), st)
+        base = enc_rng.reserve((plan.n_in + plan.n_pt) * self.world)
+        if v_ct is not None and sh.n_out:  # term A: Enc(pi_v(v)) (x) pi_W(W)
+            ct = _dev.empty_u32(sh.n_in, 2, L, N)
+            _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(v_ct), *_pk(sh.in_pack), sh.n_in,
+                      enc_rng.device_key, base + self.rank * sh.n_in, _dev.ptr(ct), st)
+            self._count("pb_encrypt_sk", sh.n_in * (ct_bytes + 8 * N))
+            pt = _dev.empty_u32(sh.n_pt, L, N)
+            sq = _dev.empty_u32(sh.n_pt, L, N)
+            _lib.call("pb_encode_plain", h, _dev.ptr(w_pt), *_pk(sh.pt_pack), sh.n_pt, _dev.ptr(pt), _dev.ptr(sq), st)
+            self._count("pb_encode_plain", sh.n_pt * (L * N * w + 8 * N))
             cts.append(ct)
-            pts.append((pt, sh))
-            pairs.append(plan.terms)
+            pts.append((pt, sq))
+            tkeys.append(("a", sh.terms_a))
             self.channel.send(DO, msg_in, ct, Ciphertext(ct, p).nbytes_wire())
-        if w_ct is not None:  # term B: Enc(pi_W(W)) (x) pi_v(v)
-            ct = _dev.empty_u32(plan.n_pt, 2, L, N)
-            _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(w_ct), _dev.ptr(dm["pt_src"]),
-                      plan.n_pt, enc_rng.device_key, enc_rng.reserve(plan.n_pt), _dev.ptr(ct), st)
-            pt = _dev.empty_u32(plan.n_in, L, N)
-            sh = _dev.empty_u32(plan.n_in, L, N)
-            _lib.call("pb_encode_plain", h, _dev.ptr(v_pt), _dev.ptr(dm["in_src"]), plan.n_in, _dev.ptr(pt),
-                      _dev.ptr(sh), st)
+        if w_ct is not None and sh.n_out:  # term B: Enc(pi_W(W)) (x) pi_v(v)
+            ct = _dev.empty_u32(sh.n_pt, 2, L, N)
+            _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(w_ct), *_pk(sh.pt_pack), sh.n_pt,
+                      enc_rng.device_key, base + self.world * plan.n_in + self.rank * sh.n_pt, _dev.ptr(ct), st)
+            self._count("pb_encrypt_sk", sh.n_pt * (ct_bytes + 8 * N))
+            pt = _dev.empty_u32(sh.n_in, L, N)
+            sq = _dev.empty_u32(sh.n_in, L, N)
+            _lib.call("pb_encode_plain", h, _dev.ptr(v_pt), *_pk(sh.in_pack), sh.n_in, _dev.ptr(pt), _dev.ptr(sq), st)
+            self._count("pb_encode_plain", sh.n_in * (L * N * w + 8 * N))
             cts.append(ct)
-            pts.append((pt, sh))
-            pairs.append(plan.terms[:, :, ::-1])
-        # concatenate operands of both terms and build the MAC term list
-        if len(cts) == 2:
-            ct_all = torch.cat([cts[0], cts[1]])
-            pt_all = torch.cat([pts[0][0], pts[1][0]])
-            sh_all = torch.cat([pts[0][1], pts[1][1]])
-            t2 = pairs[1].copy()
-            t2[:, :, 0] += cts[0].shape[0]
-            t2[:, :, 1] += pts[0][0].shape[0]
-            terms = np.concatenate([pairs[0], t2], axis=1)
-        elif len(cts) == 1:
-            ct_all, (pt_all, sh_all), terms = cts[0], pts[0], pairs[0]
-        else:  # no cross term at all: the DO decrypts an encryption of -mask
-            ct_all = torch.zeros(1, 2, L, N, dtype=torch.int32, device=_dev.device())
-            pt_all = torch.zeros(1, L, N, dtype=torch.int32, device=_dev.device())
-            sh_all = pt_all
-            terms = np.full((plan.n_out, 1, 2), -1, dtype=np.int64)
-            terms[:, 0, 1] = 0
-        K = terms.shape[1]
-        terms_d = _dev.i32_to_device(np.ascontiguousarray(terms, dtype=np.int32))
-        out_ct = _dev.empty_u32(plan.n_out, 2, L, N)
-        fseed = self.rng(layer, op, P_MASK).device_key ^ 0x5A5A5A5A5A5A5A5A
-        _lib.call("pb_ctpt_mac_mask", h, _dev.ptr(ct_all), _dev.ptr(pt_all), _dev.ptr(sh_all), _dev.ptr(terms_d), K,
-                  plan.n_out, _dev.ptr(dm["out_pos"]), _dev.ptr(dm["out_dst"]), plan.U, _dev.ptr(mask),
-                  1 if self.filler else 0, fseed, _dev.ptr(out_ct), st)
-        self.channel.send(MO, msg_out, out_ct, Ciphertext(out_ct, p).nbytes_wire())
-        scratch = _dev.empty_u32(plan.n_out, L, plan.U)
-        _lib.call("pb_decrypt_to_share", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(out_ct), plan.n_out,
-                  _dev.ptr(dm["out_pos"]), _dev.ptr(dm["out_dst"]), plan.U, _dev.ptr(out), _dev.ptr(scratch), st)
-        # keep every operand alive until the kernels above are enqueued
-        del cts, pts, ct_all, pt_all, sh_all, terms_d
+            pts.append((pt, sq))
+            tkeys.append(("b", sh.terms_b))
+        if self.world > 1:
+            out.zero_()
+        if sh.n_out:
+            # operands of both terms side by side, MAC term list remapped to them
+            if len(cts) == 2:
+                ct_all = torch.cat([cts[0], cts[1]])
+                pt_all = torch.cat([pts[0][0], pts[1][0]])
+                sq_all = torch.cat([pts[0][1], pts[1][1]])
+                t2 = tkeys[1][1].copy()
+                t2[:, :, 0] += cts[0].shape[0]
+                t2[:, :, 1] += pts[0][0].shape[0]
+                terms_d = sh.terms_device("ab", np.concatenate([tkeys[0][1], t2], axis=1))
+            elif len(cts) == 1:
+                ct_all, (pt_all, sq_all) = cts[0], pts[0]
+                terms_d = sh.terms_device(tkeys[0][0], tkeys[0][1])
+            else:  # no cross term at all: the DO decrypts an encryption of -mask
+                ct_all = torch.zeros(1, 2, L, N, dtype=torch.int32, device=_dev.device())
+                pt_all = sq_all = torch.zeros(1, L, N, dtype=torch.int32, device=_dev.device())
+                none = np.full((sh.n_out, 1, 2), -1, dtype=np.int64)
+                none[:, 0, 1] = 0
+                terms_d = sh.terms_device("none", none)
+            K = terms_d.shape[1]
+            out_ct = _dev.empty_u32(sh.n_out, 2, L, N)
+            fseed = self.rng(layer, op, P_MASK).device_key ^ 0x5A5A5A5A5A5A5A5A
+            _lib.call("pb_ctpt_mac_mask", h, _dev.ptr(ct_all), _dev.ptr(pt_all), _dev.ptr(sq_all), _dev.ptr(terms_d),
+                      K, sh.n_out, _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U, _dev.ptr(mask),
+                      1 if self.filler else 0, fseed, _dev.ptr(out_ct), st)
+            n_ct_in = sum(c.shape[0] for c in cts)
+            n_pt_in = sum(q[0].shape[0] for q in pts)
+            self._count("pb_ctpt_mac_mask", n_ct_in * ct_bytes + n_pt_in * L * N * w + sh.n_out * ct_bytes)
+            self.channel.send(MO, msg_out, out_ct, Ciphertext(out_ct, p).nbytes_wire())
+            scratch = _dev.empty_u32(sh.n_out, L, sh.U)
+            _lib.call("pb_decrypt_to_share", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(out_ct), sh.n_out,
+                      _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U, _dev.ptr(out), _dev.ptr(scratch), st)
+            self._count("pb_decrypt_to_share", sh.n_out * (ct_bytes + 8 * sh.U))
+            # keep every operand alive until the kernels above are enqueued
+            del cts, pts, ct_all, pt_all, sq_all
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(out, op=dist.ReduceOp.SUM, group=self.group)
         return out
 
 

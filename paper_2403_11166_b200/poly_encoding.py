@@ -97,13 +97,63 @@ def _cdiv(a, b):
     return -(-a // b)
 
 
-def matmul_blocks(g: MatmulGeometry, N: int):
+def compact(dense_map: np.ndarray):
+    """Dense [P, N] source map (-1 = zero) -> packed (pos, src) int32 [P, Z]:
+    the form the device kernels consume (pencil_b200.h "packed source")."""
+    dense_map = np.asarray(dense_map)
+    P = dense_map.shape[0]
+    nz = dense_map >= 0
+    cnt = nz.sum(axis=1)
+    Z = int(cnt.max()) if P else 0
+    pos = np.full((P, max(Z, 1)), -1, dtype=np.int32)
+    src = np.zeros((P, max(Z, 1)), dtype=np.int32)
+    rows, cols = np.nonzero(nz)
+    slot = np.arange(len(rows)) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    pos[rows, slot] = cols
+    src[rows, slot] = dense_map[rows, cols]
+    return pos, src
+
+
+# Relative device cost of one polynomial-row unit of each plan component
+# (an NTT-row of work or its HBM equivalent): encrypting an input poly, encoding
+# a plaintext, producing + decrypting an output ciphertext (mask NTT + INTT),
+# and one ct x pt product term (streaming reads).
+COST_ENC, COST_PT, COST_OUT, COST_PROD = 1.3, 1.0, 2.0, 0.5
+MAX_INPUT_BLOCKS = 32  # bounds the homomorphic accumulation depth (noise)
+
+
+def matmul_blocks(g: MatmulGeometry, N: int, mode: str = "cost"):
+    """(B_blk, n_o_blk, n_i_blk) with n_o_blk * n_i_blk * B_blk <= N.
+
+    mode "spec": SPEC:285 order -- shrink the batch block first, then the
+    output dimension, then the input dimension.
+    mode "cost": the tiling minimising the engine's cost model above (the
+    partition strategy is not fixed by the paper); ties broken
+    deterministically.  Decrypted outputs do not depend on the tiling."""
     if min(g.n_i, g.n_o, g.B) < 1:
         raise GeometryError("empty matmul geometry")
-    nib = min(g.n_i, N)
-    if g.n_o * nib <= N:
-        return min(g.B, N // (g.n_o * nib)), g.n_o, nib
-    return 1, max(1, N // nib), nib
+    if mode == "spec":
+        nib = min(g.n_i, N)
+        if g.n_o * nib <= N:
+            return min(g.B, N // (g.n_o * nib)), g.n_o, nib
+        return 1, max(1, N // nib), nib
+    best = None
+    for k in range(1, MAX_INPUT_BLOCKS + 1):
+        nib = _cdiv(g.n_i, k)
+        if nib > N or _cdiv(g.n_i, nib) != k:
+            continue
+        cap = N // nib
+        for nob in range(1, min(g.n_o, cap) + 1):
+            Bb = min(g.B, cap // nob)
+            nO, nB = _cdiv(g.n_o, nob), _cdiv(g.B, Bb)
+            n_out = nB * nO
+            cost = COST_ENC * nB * k + COST_PT * nO * k + COST_OUT * n_out + COST_PROD * n_out * k
+            key = (round(cost, 6), n_out, k, -nob)
+            if best is None or key < best[0]:
+                best = (key, (Bb, nob, nib))
+        if k >= g.n_i:
+            break
+    return best[1]
 
 
 def conv_blocks(g: ConvGeometry, N: int):
@@ -131,12 +181,13 @@ def _terms(nB, nO, nI):
 
 
 @lru_cache(maxsize=256)
-def plan_matmul(g: MatmulGeometry, N: int, v_strides=None, w_strides=None, y_strides=None) -> BlockPlan:
+def plan_matmul(g: MatmulGeometry, N: int, v_strides=None, w_strides=None, y_strides=None,
+                mode: str = "cost") -> BlockPlan:
     """v is (n_i, B), W is (n_o, n_i), Y is (n_o, B); strides default to row-major."""
     vs = v_strides or (g.B, 1)
     ws = w_strides or (g.n_i, 1)
     ys = y_strides or (g.B, 1)
-    Bb, nob, nib = matmul_blocks(g, N)
+    Bb, nob, nib = matmul_blocks(g, N, mode)
     nB, nO, nI = _cdiv(g.B, Bb), _cdiv(g.n_o, nob), _cdiv(g.n_i, nib)
     # inputs: axes (bb, ii, k, j)
     bb = np.arange(nB)[:, None, None, None]
@@ -225,9 +276,9 @@ def plan_conv(g: ConvGeometry, N: int) -> BlockPlan:
                      _terms(nB, nO, nI))
 
 
-def plan_blocks(g, N: int) -> BlockPlan:
+def plan_blocks(g, N: int, mode: str = "cost") -> BlockPlan:
     if isinstance(g, MatmulGeometry):
-        return plan_matmul(g, N)
+        return plan_matmul(g, N, mode=mode)
     if isinstance(g, ConvGeometry):
         return plan_conv(g, N)
     raise GeometryError(f"unknown geometry {g!r}")
@@ -239,7 +290,7 @@ def matmul_poly_encode(which: str, tensor, g: MatmulGeometry, N: int):
     """Single-block encode (the SPEC operation); raises GeometryError on overflow."""
     if g.n_o * g.n_i * g.B > N:
         raise GeometryError("n_o * n_i * B must not exceed N")
-    plan = plan_matmul(g, N)
+    plan = plan_matmul(g, N, mode="spec")
     src = plan.in_src if which == "input" else plan.pt_src
     vals = np.asarray(tensor, dtype=np.uint64).ravel()
     out = np.zeros(N, dtype=np.uint64)
@@ -249,7 +300,7 @@ def matmul_poly_encode(which: str, tensor, g: MatmulGeometry, N: int):
 
 
 def matmul_poly_decode(y, g: MatmulGeometry, N: int):
-    plan = plan_matmul(g, N)
+    plan = plan_matmul(g, N, mode="spec")
     y = np.asarray(y, dtype=np.uint64)
     out = np.zeros(g.n_o * g.B, dtype=np.uint64)
     ok = plan.out_pos[0] >= 0

@@ -15,10 +15,11 @@ CONV = [(1, 1, 1, 2, 2, 1, 16), (2, 3, 4, 5, 6, 3, 256), (3, 2, 5, 4, 4, 2, 64),
         (4, 64, 64, 16, 16, 5, 8192), (64, 1, 5, 32, 32, 5, 8192)]
 
 
+@pytest.mark.parametrize("mode", ["cost", "spec"])
 @pytest.mark.parametrize("ni,no,B,N", MATMUL)
-def test_matmul_maps_match_oracle(ni, no, B, N):
+def test_matmul_maps_match_oracle(ni, no, B, N, mode):
     g = PE.MatmulGeometry(ni, no, B)
-    a, b = PE.plan_blocks(g, N), OP.plan_blocks(OP.MatmulGeometry(ni, no, B), N)
+    a, b = PE.plan_blocks(g, N, mode), OP.plan_blocks(OP.MatmulGeometry(ni, no, B), N, mode)
     for f in ("in_src", "pt_src", "out_pos", "out_dst", "terms"):
         assert np.array_equal(getattr(a, f), getattr(b, f)), f
     assert a.blk == b.blk and a.nblk == b.nblk
@@ -42,13 +43,14 @@ def _plain_eval(plan, v, W, N):
     return outs
 
 
+@pytest.mark.parametrize("mode", ["cost", "spec"])
 @pytest.mark.parametrize("ni,no,B,N", MATMUL[:6])
-def test_matmul_identity(ni, no, B, N):
+def test_matmul_identity(ni, no, B, N, mode):
     """decode(pi_W(W) pi_v(v)) == W v, incl. input-dimension blocks."""
     rng = np.random.default_rng(ni * 7 + no)
     v = rng.integers(0, 1 << 63, size=(ni, B), dtype=np.uint64)
     W = rng.integers(0, 1 << 63, size=(no, ni), dtype=np.uint64)
-    plan = PE.plan_blocks(PE.MatmulGeometry(ni, no, B), N)
+    plan = PE.plan_blocks(PE.MatmulGeometry(ni, no, B), N, mode)
     y = OP.unpack(_plain_eval(plan, v, W, N), plan, no * B).reshape(no, B)
     assert np.array_equal(y, OK.matmul_wrap(W, v))
 
@@ -86,9 +88,20 @@ def test_spec_examples():
         PE.matmul_poly_encode("input", np.zeros((100, 1)), PE.MatmulGeometry(100, 1, 1), 64)
 
 
-def test_plan_examples():
-    assert PE.plan_blocks(PE.MatmulGeometry(3, 2, 1), 8192).n_out == 1
-    p = PE.plan_blocks(PE.MatmulGeometry(2048, 1001, 1), 8192)  # SPEC:274 tiling
+def test_compact_maps():
+    plan = PE.plan_blocks(PE.MatmulGeometry(100, 7, 3), 64)
+    pos, src = PE.compact(plan.in_src)
+    dense = np.full_like(plan.in_src, -1)
+    for p in range(pos.shape[0]):
+        ok = pos[p] >= 0
+        dense[p, pos[p][ok]] = src[p][ok]
+    assert np.array_equal(dense, plan.in_src)
+
+
+@pytest.mark.parametrize("mode", ["cost", "spec"])
+def test_plan_examples(mode):
+    assert PE.plan_blocks(PE.MatmulGeometry(3, 2, 1), 8192, mode).n_out == 1
+    p = PE.plan_blocks(PE.MatmulGeometry(2048, 1001, 1), 8192, mode)  # SPEC:274 tiling
     covered = np.zeros(1001, dtype=int)
     ok = p.out_pos >= 0
     np.add.at(covered, p.out_dst[ok], 1)
