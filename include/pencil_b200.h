@@ -145,7 +145,7 @@ int pb_unpack(const uint64_t* vals, const int32_t* pack_pos, const int32_t* pack
  * Philox4x32(seed, nonce + poly index). ct [P][2][L][N]. */
 int pb_encrypt_pk(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* vals,
                   const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int64_t P,
-                  uint64_t seed, uint64_t nonce, uint32_t* ct, void* stream);
+                  uint64_t seed, const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct, void* stream);
 /* Same with caller-supplied noise (int8 [P][N] each): bit-exact with the
  * oracle's encrypt when fed the oracle's draws. */
 int pb_encrypt_pk_noise(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* vals,
@@ -156,7 +156,7 @@ int pb_encrypt_pk_noise(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* v
  * c0 = NTT(e + Delta m) - a*s.  sk_ntt [L][N]. */
 int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint64_t* vals,
                   const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int64_t P,
-                  uint64_t seed, uint64_t nonce, uint32_t* ct, void* stream);
+                  uint64_t seed, const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct, void* stream);
 /* Caller-supplied a ([P][L][N], NTT domain, device order) and e (int8 [P][N]). */
 int pb_encrypt_sk_noise(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint64_t* vals,
                         const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int64_t P,
@@ -180,13 +180,16 @@ int pb_decrypt_to_share(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint32_
  * where mask_p has mask_vals[out_dst[p][u]] at coefficient out_pos[p][u] and,
  * when filler != 0, uniform Z_q filler (Philox4x32(filler_seed, p)) at every
  * other coefficient so the DO learns nothing beyond the useful slots.
+ * Every RNG-consuming entry point takes `seed_dev` (nullable): when set, the
+ * per-step seed is read from device memory so a CUDA graph can replay the
+ * call with fresh randomness (see pb_common.cuh "seed indirection").
  * terms[p][k] with ct index < 0 is skipped.  ct_in [n][2][L][N],
  * pt/pt_shoup [n_pt][L][N], ct_out [P][2][L][N]. */
 int pb_ctpt_mac_mask(const pb_ctx* ctx, const uint32_t* ct_in, const uint32_t* pt,
                      const uint32_t* pt_shoup, const int32_t* terms, int32_t K, int64_t P,
                      const int32_t* out_pos, const int64_t* out_dst, int32_t U,
-                     const uint64_t* mask_vals, int filler, uint64_t filler_seed, uint32_t* ct_out,
-                     void* stream);
+                     const uint64_t* mask_vals, int filler, uint64_t filler_seed, const uint64_t* seed_dev,
+                     uint32_t* ct_out, void* stream);
 
 /* ------------------------------------------- ring Z_{2^ell} (R:93-233) --- */
 enum {
@@ -211,11 +214,11 @@ int pb_decode_fixed(const uint64_t* v, int64_t n, int32_t ell, int32_t scale, do
                     void* stream);
 /* R:60-61 SeededRng.uniform_ring: out[i] = raw(seed, stream_id, raw_offset+i) >> (64-ell),
  * bit-identical to numpy Generator(Philox(key=[seed, stream])).integers(0, 2^ell). */
-int pb_uniform_ring(uint64_t* out, int64_t n, uint64_t seed, uint64_t stream_id,
+int pb_uniform_ring(uint64_t* out, int64_t n, uint64_t seed, const uint64_t* seed_dev, uint64_t stream_id,
                     uint64_t raw_offset, int32_t ell, void* stream);
 /* R:214-219 share_tensor fused: r = uniform_ring(...); mo = r; do = x - r. */
-int pb_share(const uint64_t* x, int64_t n, uint64_t seed, uint64_t stream_id, uint64_t raw_offset,
-             int32_t ell, uint64_t* mo_out, uint64_t* do_out, void* stream);
+int pb_share(const uint64_t* x, int64_t n, uint64_t seed, const uint64_t* seed_dev, uint64_t stream_id,
+             uint64_t raw_offset, int32_t ell, uint64_t* mo_out, uint64_t* do_out, void* stream);
 /* K:206-218 matmul_wrap (+ mask to ell bits when ell < 64): (n,k)@(k,m).
  * trans_a / trans_b read a as (k,n) / b as (m,k) row-major. */
 int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m,
@@ -242,8 +245,8 @@ int pb_conv2d(const uint64_t* x, const uint64_t* w, int32_t B, int32_t Ci, int32
  * Outputs overwrite mo/do in place. */
 enum { PB_DEALER_RELU = 0, PB_DEALER_TRUNC = 1, PB_DEALER_SELECT = 2, PB_DEALER_RESHARE = 3 };
 int pb_dealer_op(int op, uint64_t* mo, uint64_t* do_, int64_t n, int32_t k, const uint8_t* d_in,
-                 uint8_t* d_out, uint64_t seed, uint64_t stream_id, uint64_t raw_offset,
-                 int32_t ell, void* stream);
+                 uint8_t* d_out, uint64_t seed, const uint64_t* seed_dev, uint64_t stream_id,
+                 uint64_t raw_offset, int32_t ell, void* stream);
 
 /* SGD with momentum in float64 + re-quantisation:
  * v = mu*v + g; w = w - lr*v; w_ring = encode_fixed(w, scale). */

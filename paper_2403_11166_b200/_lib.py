@@ -58,26 +58,26 @@ SIGNATURES = {
     "pb_encode_plain": [P, P, P, P, I32, I64, P, P, P],
     "pb_lift": [P, P, I64, INT, P, P],
     "pb_unpack": [P, P, P, I32, I32, I64, P, P],
-    "pb_encrypt_pk": [P, P, P, P, P, I32, I64, U64, U64, P, P],
+    "pb_encrypt_pk": [P, P, P, P, P, I32, I64, U64, P, U64, P, P],
     "pb_encrypt_pk_noise": [P, P, P, P, P, I32, I64, P, P, P, P, P],
-    "pb_encrypt_sk": [P, P, P, P, P, I32, I64, U64, U64, P, P],
+    "pb_encrypt_sk": [P, P, P, P, P, I32, I64, U64, P, U64, P, P],
     "pb_encrypt_sk_noise": [P, P, P, P, P, I32, I64, P, P, P, P],
     "pb_decrypt_coeffs": [P, P, P, I64, P, P],
     "pb_decrypt": [P, P, P, I64, P, P, P],
     "pb_decrypt_to_share": [P, P, P, I64, P, P, I32, P, P, P],
-    "pb_ctpt_mac_mask": [P, P, P, P, P, I32, I64, P, P, I32, P, INT, U64, P, P],
+    "pb_ctpt_mac_mask": [P, P, P, P, P, I32, I64, P, P, I32, P, INT, U64, P, P, P],
     "pb_ring_binary": [INT, P, P, P, I64, I64, I32, P],
     "pb_ring_unary": [INT, P, P, U64, I64, I32, P],
     "pb_encode_fixed": [P, I64, I32, I32, P, P, P],
     "pb_decode_fixed": [P, I64, I32, I32, P, P],
-    "pb_uniform_ring": [P, I64, U64, U64, U64, I32, P],
-    "pb_share": [P, I64, U64, U64, U64, I32, P, P, P],
+    "pb_uniform_ring": [P, I64, U64, P, U64, U64, I32, P],
+    "pb_share": [P, I64, U64, P, U64, U64, I32, P, P, P],
     "pb_ring_matmul": [P, P, I64, I64, I64, INT, INT, I32, P, P],
     "pb_ring_rowsum": [P, I64, I64, I32, P, P],
     "pb_im2col": [P, I32, I32, I32, I32, I32, I32, P, P],
     "pb_col2im": [P, I32, I32, I32, I32, I32, I32, P, P],
     "pb_conv2d": [P, P, I32, I32, I32, I32, I32, I32, I32, P, P],
-    "pb_dealer_op": [INT, P, P, I64, I32, P, P, U64, U64, U64, I32, P],
+    "pb_dealer_op": [INT, P, P, I64, I32, P, P, U64, P, U64, U64, I32, P],
     "pb_sgd_momentum": [P, P, P, I64, I32, F64, F64, I32, I32, P, P, P],
 }
 _RET = {"pb_last_error": ctypes.c_char_p}

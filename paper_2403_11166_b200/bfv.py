@@ -154,12 +154,12 @@ def encrypt(kp: KeyPair, m: torch.Tensor, rng=None, *, pack=None, mode: str = "p
             _lib.call("pb_encrypt_sk_noise", h, _dev.ptr(kp.sk_ntt), _dev.ptr(m), pp, ps, Z, P, _dev.ptr(a),
                       _dev.ptr(e), _dev.ptr(ct), st)
         return Ciphertext(ct, params)
-    seed = rng.device_key if rng is not None else 0
+    seed, sptr = rng.dev_args() if rng is not None else (0, None)
     if nonce is None:
         nonce = rng.reserve(P) if rng is not None else 0
     fn = "pb_encrypt_pk" if mode == "pk" else "pb_encrypt_sk"
     key = _dev.ptr(kp.pk) if mode == "pk" else _dev.ptr(kp.sk_ntt)
-    _lib.call(fn, h, key, _dev.ptr(m), pp, ps, Z, P, seed, nonce, _dev.ptr(ct), st)
+    _lib.call(fn, h, key, _dev.ptr(m), pp, ps, Z, P, seed, sptr, nonce, _dev.ptr(ct), st)
     return Ciphertext(ct, params)
 
 
@@ -262,7 +262,7 @@ def he_plain_mul(ct: Ciphertext, w) -> Ciphertext:
     terms_d = _dev.i32_to_device(terms)
     out = _dev.empty_u32(P, 2, p.L, p.N)
     _lib.call("pb_ctpt_mac_mask", _ctx(p), _dev.ptr(ct.data), _dev.ptr(w.data), _dev.ptr(w.shoup), _dev.ptr(terms_d), 1,
-              P, None, None, 0, None, 0, 0, _dev.ptr(out), _dev.stream())
+              P, None, None, 0, None, 0, 0, None, _dev.ptr(out), _dev.stream())
     return Ciphertext(out, p)
 
 

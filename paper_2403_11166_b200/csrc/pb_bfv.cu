@@ -115,8 +115,9 @@ __device__ __forceinline__ int cbd20(uint32_t x, uint32_t y) {
   return __popc(x & 0xFFFFFu) - __popc(y & 0xFFFFFu);
 }
 
-__global__ void k_sample_noise(int N, int64_t nP, uint64_t seed, uint64_t nonce, int with_u, int8_t* u, int8_t* e1,
-                               int8_t* e2) {
+__global__ void k_sample_noise(int N, int64_t nP, uint64_t seed_arg, const uint64_t* seed_dev, uint64_t nonce,
+                               int with_u, int8_t* u, int8_t* e1, int8_t* e2) {
+  const uint64_t seed = dev_key(seed_arg, seed_dev);
   const int64_t total = nP * N;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = e / N;
@@ -194,8 +195,9 @@ __device__ __forceinline__ void uniform_pair(uint64_t seed, uint64_t nonce, int6
 template <int LOGN>
 __global__ void __launch_bounds__(1 << (LOGN - 5))
     k_encrypt_sk(PbDev P, const uint32_t* sk, PbPack src, int64_t nP, const uint32_t* a_in, const int8_t* e,
-                 uint64_t seed, uint64_t nonce, uint32_t* ct) {
+                 uint64_t seed_arg, const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct) {
   using Nt = pb::Ntt<LOGN>;
+  const uint64_t seed = dev_key(seed_arg, seed_dev);
   constexpr int N = Nt::N;
   extern __shared__ uint32_t sm[];
   const int tid = threadIdx.x;
@@ -327,8 +329,9 @@ template <int LOGN>
 __global__ void __launch_bounds__(1 << (LOGN - 5))
     k_ctpt_mac_mask(PbDev P, const uint32_t* ct_in, const uint32_t* pt, const uint32_t* pt_sh, const int32_t* terms,
                     int K, int64_t nP, const int32_t* out_pos, const int64_t* out_dst, int U, const uint64_t* mask_vals,
-                    int filler, uint64_t filler_seed, uint32_t* ct_out) {
+                    int filler, uint64_t filler_arg, const uint64_t* seed_dev, uint32_t* ct_out) {
   using Nt = pb::Ntt<LOGN>;
+  const uint64_t filler_seed = dev_key(filler_arg, seed_dev);
   constexpr int N = Nt::N;
   extern __shared__ uint32_t sm[];
   const int tid = threadIdx.x;
@@ -421,11 +424,11 @@ void launch_encrypt_pk(const PbDev& P, const uint32_t* pk, PbPack src, int64_t n
 
 template <int LOGN>
 void launch_encrypt_sk(const PbDev& P, const uint32_t* sk, PbPack src, int64_t nP, const uint32_t* a_in, const int8_t* e,
-                       uint64_t seed, uint64_t nonce, uint32_t* ct, cudaStream_t st) {
+                       uint64_t seed, const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct, cudaStream_t st) {
   using Nt = pb::Ntt<LOGN>;
   const size_t smem = Nt::SMEM_WORDS * 4;
   set_smem(k_encrypt_sk<LOGN>, smem);
-  k_encrypt_sk<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, sk, src, nP, a_in, e, seed, nonce, ct);
+  k_encrypt_sk<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, sk, src, nP, a_in, e, seed, seed_dev, nonce, ct);
 }
 
 template <int LOGN>
@@ -440,12 +443,12 @@ void launch_decrypt_inv(const PbDev& P, const uint32_t* sk, const uint32_t* ct, 
 template <int LOGN>
 void launch_mac(const PbDev& P, const uint32_t* ct_in, const uint32_t* pt, const uint32_t* pt_sh, const int32_t* terms,
                 int K, int64_t nP, const int32_t* out_pos, const int64_t* out_dst, int U, const uint64_t* mask_vals,
-                int filler, uint64_t filler_seed, uint32_t* ct_out, cudaStream_t st) {
+                int filler, uint64_t filler_seed, const uint64_t* seed_dev, uint32_t* ct_out, cudaStream_t st) {
   using Nt = pb::Ntt<LOGN>;
   const size_t smem = Nt::SMEM_WORDS * 4;
   set_smem(k_ctpt_mac_mask<LOGN>, smem);
   k_ctpt_mac_mask<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, ct_in, pt, pt_sh, terms, K, nP, out_pos, out_dst,
-                                                                   U, mask_vals, filler, filler_seed, ct_out);
+                                                                   U, mask_vals, filler, filler_seed, seed_dev, ct_out);
 }
 
 int need_big_n(const pb_ctx* ctx) {
@@ -536,8 +539,8 @@ extern "C" int pb_encrypt_pk_noise(const pb_ctx* ctx, const uint32_t* pk, const 
 }
 
 extern "C" int pb_encrypt_pk(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* vals, const int32_t* pack_pos,
-                             const int32_t* pack_src, int32_t Z, int64_t nP, uint64_t seed, uint64_t nonce,
-                             uint32_t* ct, void* stream) {
+                             const int32_t* pack_src, int32_t Z, int64_t nP, uint64_t seed, const uint64_t* seed_dev,
+                             uint64_t nonce, uint32_t* ct, void* stream) {
   if (int s = need_big_n(ctx)) return s;
   if (nP <= 0) return PB_OK;
   const int N = ctx->dev.N;
@@ -545,7 +548,7 @@ extern "C" int pb_encrypt_pk(const pb_ctx* ctx, const uint32_t* pk, const uint64
   if (!buf) return pb_set_error(PB_ERR_CUDA, "noise scratch allocation failed");
   int8_t *u = buf, *e1 = buf + nP * N, *e2 = buf + 2 * nP * N;
   cudaStream_t st = pb_stream_of(stream);
-  k_sample_noise<<<pb_grid_1d(nP * N, 256), 256, 0, st>>>(N, nP, seed, nonce, 1, u, e1, e2);
+  k_sample_noise<<<pb_grid_1d(nP * N, 256), 256, 0, st>>>(N, nP, seed, seed_dev, nonce, 1, u, e1, e2);
   PB_CHECK_LAUNCH();
   return pb_encrypt_pk_noise(ctx, pk, vals, pack_pos, pack_src, Z, nP, u, e1, e2, ct, stream);
 }
@@ -558,14 +561,15 @@ extern "C" int pb_encrypt_sk_noise(const pb_ctx* ctx, const uint32_t* sk, const 
   if (!sk || !e || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
   if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
   PB_PACK_OR_RETURN(src, vals, pack_pos, pack_src, Z);
-  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, src, nP, a, e, 0ull, 0ull, ct, pb_stream_of(stream));
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, src, nP, a, e, 0ull, (const uint64_t*)nullptr, 0ull, ct,
+                   pb_stream_of(stream));
   PB_CHECK_LAUNCH();
   return PB_OK;
 }
 
 extern "C" int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk, const uint64_t* vals, const int32_t* pack_pos,
-                             const int32_t* pack_src, int32_t Z, int64_t nP, uint64_t seed, uint64_t nonce,
-                             uint32_t* ct, void* stream) {
+                             const int32_t* pack_src, int32_t Z, int64_t nP, uint64_t seed, const uint64_t* seed_dev,
+                             uint64_t nonce, uint32_t* ct, void* stream) {
   if (int s = need_big_n(ctx)) return s;
   if (nP <= 0) return PB_OK;
   if (!sk || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
@@ -575,10 +579,10 @@ extern "C" int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk, const uint64
   int8_t* e = noise_buffer((size_t)nP * N);
   if (!e) return pb_set_error(PB_ERR_CUDA, "noise scratch allocation failed");
   cudaStream_t st = pb_stream_of(stream);
-  k_sample_noise<<<pb_grid_1d(nP * N, 256), 256, 0, st>>>(N, nP, seed, nonce, 0, nullptr, e, nullptr);
+  k_sample_noise<<<pb_grid_1d(nP * N, 256), 256, 0, st>>>(N, nP, seed, seed_dev, nonce, 0, nullptr, e, nullptr);
   PB_CHECK_LAUNCH();
-  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, src, nP, (const uint32_t*)nullptr, e, seed, nonce,
-                   ct, st);
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, src, nP, (const uint32_t*)nullptr, e, seed, seed_dev,
+                   nonce, ct, st);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }
@@ -622,7 +626,7 @@ extern "C" int pb_decrypt_to_share(const pb_ctx* ctx, const uint32_t* sk, const 
 extern "C" int pb_ctpt_mac_mask(const pb_ctx* ctx, const uint32_t* ct_in, const uint32_t* pt, const uint32_t* pt_shoup,
                                 const int32_t* terms, int32_t K, int64_t nP, const int32_t* out_pos,
                                 const int64_t* out_dst, int32_t U, const uint64_t* mask_vals, int filler,
-                                uint64_t filler_seed, uint32_t* ct_out, void* stream) {
+                                uint64_t filler_seed, const uint64_t* seed_dev, uint32_t* ct_out, void* stream) {
   if (int s = need_big_n(ctx)) return s;
   if (!ct_in || !pt || !pt_shoup || !terms || !ct_out) return pb_set_error(PB_ERR_ARG, "null argument");
   if (mask_vals && (!out_pos || !out_dst)) return pb_set_error(PB_ERR_ARG, "mask needs out_pos/out_dst");
@@ -630,7 +634,7 @@ extern "C" int pb_ctpt_mac_mask(const pb_ctx* ctx, const uint32_t* ct_in, const 
   if (nP <= 0) return PB_OK;
   if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
   PB_DISPATCH_LOGN(ctx->dev.logN, launch_mac, ctx->dev, ct_in, pt, pt_shoup, terms, K, nP, out_pos, out_dst, U,
-                   mask_vals, filler, filler_seed, ct_out, pb_stream_of(stream));
+                   mask_vals, filler, filler_seed, seed_dev, ct_out, pb_stream_of(stream));
   PB_CHECK_LAUNCH();
   return PB_OK;
 }

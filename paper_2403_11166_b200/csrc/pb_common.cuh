@@ -154,6 +154,26 @@ __device__ __forceinline__ u32x4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_
   return o;
 }
 
+// ------------------------------------------------------- seed indirection ---
+// A CUDA graph replays kernels with frozen arguments, so every RNG-consuming
+// entry point also accepts `seed_dev`: when non-NULL the per-step seed S is
+// read from device memory at run time.
+//   numpy-identical streams:  key word 0 = S + seed            (np_seed)
+//   device-only streams:      key = fmix64(S * G + seed)       (dev_key)
+// With seed_dev == NULL the host passes the final value (eager mode); the
+// host-side SeededRng.device_key uses the same mixing, so both modes agree.
+__device__ __forceinline__ uint64_t fmix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t np_seed(uint64_t seed, const uint64_t* seed_dev) {
+  return seed_dev ? *seed_dev + seed : seed;
+}
+__device__ __forceinline__ uint64_t dev_key(uint64_t seed, const uint64_t* seed_dev) {
+  return seed_dev ? fmix64(*seed_dev * 0x9E3779B97F4A7C15ull + seed) : seed;
+}
+
 // ---------------------------------------------------------- launch glue ---
 
 #define PB_CHECK_LAUNCH()                                      \

@@ -75,8 +75,9 @@ __global__ void k_decode_fixed(const uint64_t* v, int64_t n, int ell, int scale,
 
 // R:60-61 uniform_ring == raw >> (64 - ell) (Lemire with a power-of-two
 // range never rejects).  Each thread produces one Philox block (4 raw words).
-__global__ void k_uniform_ring(uint64_t* out, const uint64_t* x, uint64_t* do_out, int64_t n, uint64_t seed,
-                               uint64_t stream_id, uint64_t off, int ell) {
+__global__ void k_uniform_ring(uint64_t* out, const uint64_t* x, uint64_t* do_out, int64_t n, uint64_t seed_arg,
+                               const uint64_t* seed_dev, uint64_t stream_id, uint64_t off, int ell) {
+  const uint64_t seed = np_seed(seed_arg, seed_dev);
   const int shift = 64 - ell;
   const uint64_t m = ring_mask(ell);
   const uint64_t first_blk = off >> 2;
@@ -194,7 +195,8 @@ __global__ void k_conv2d(const uint64_t* x, const uint64_t* w, int B, int Ci, in
 // Dealer-assisted non-linear step: reconstruct, apply, reshare with the
 // numpy-identical uniform_ring stream (so oracle and device shares agree).
 __global__ void k_dealer(int op, uint64_t* mo, uint64_t* dov, int64_t n, int k, const uint8_t* d_in, uint8_t* d_out,
-                         uint64_t seed, uint64_t stream_id, uint64_t off, int ell) {
+                         uint64_t seed_arg, const uint64_t* seed_dev, uint64_t stream_id, uint64_t off, int ell) {
+  const uint64_t seed = np_seed(seed_arg, seed_dev);
   const uint64_t m = ring_mask(ell);
   const int shift = 64 - ell;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -284,22 +286,24 @@ extern "C" int pb_decode_fixed(const uint64_t* v, int64_t n, int32_t ell, int32_
   return PB_OK;
 }
 
-extern "C" int pb_uniform_ring(uint64_t* out, int64_t n, uint64_t seed, uint64_t stream_id, uint64_t raw_offset,
+extern "C" int pb_uniform_ring(uint64_t* out, int64_t n, uint64_t seed, const uint64_t* seed_dev, uint64_t stream_id,
+                               uint64_t raw_offset,
                                int32_t ell, void* stream) {
   if (n > 0 && !out) return pb_set_error(PB_ERR_ARG, "null argument");
   if (ell < 1 || ell > 63) return pb_set_error(PB_ERR_ARG, "bad ell");
   if (n <= 0) return PB_OK;
-  k_uniform_ring<<<RING_GRID((n + 3) / 4 + 1)>>>(out, nullptr, nullptr, n, seed, stream_id, raw_offset, ell);
+  k_uniform_ring<<<RING_GRID((n + 3) / 4 + 1)>>>(out, nullptr, nullptr, n, seed, seed_dev, stream_id, raw_offset, ell);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }
 
-extern "C" int pb_share(const uint64_t* x, int64_t n, uint64_t seed, uint64_t stream_id, uint64_t raw_offset,
+extern "C" int pb_share(const uint64_t* x, int64_t n, uint64_t seed, const uint64_t* seed_dev, uint64_t stream_id,
+                        uint64_t raw_offset,
                         int32_t ell, uint64_t* mo_out, uint64_t* do_out, void* stream) {
   if (n > 0 && (!x || !mo_out || !do_out)) return pb_set_error(PB_ERR_ARG, "null argument");
   if (ell < 1 || ell > 63) return pb_set_error(PB_ERR_ARG, "bad ell");
   if (n <= 0) return PB_OK;
-  k_uniform_ring<<<RING_GRID((n + 3) / 4 + 1)>>>(mo_out, x, do_out, n, seed, stream_id, raw_offset, ell);
+  k_uniform_ring<<<RING_GRID((n + 3) / 4 + 1)>>>(mo_out, x, do_out, n, seed, seed_dev, stream_id, raw_offset, ell);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }
@@ -360,14 +364,15 @@ extern "C" int pb_conv2d(const uint64_t* x, const uint64_t* w, int32_t B, int32_
 }
 
 extern "C" int pb_dealer_op(int op, uint64_t* mo, uint64_t* do_, int64_t n, int32_t k, const uint8_t* d_in,
-                            uint8_t* d_out, uint64_t seed, uint64_t stream_id, uint64_t raw_offset, int32_t ell,
+                            uint8_t* d_out, uint64_t seed, const uint64_t* seed_dev, uint64_t stream_id,
+                            uint64_t raw_offset, int32_t ell,
                             void* stream) {
   if (n > 0 && (!mo || !do_)) return pb_set_error(PB_ERR_ARG, "null argument");
   if (op < PB_DEALER_RELU || op > PB_DEALER_RESHARE) return pb_set_error(PB_ERR_ARG, "bad dealer op");
   if (op == PB_DEALER_SELECT && !d_in) return pb_set_error(PB_ERR_ARG, "select needs d_in");
   if (ell < 2 || ell > 63 || k < 0 || k >= ell) return pb_set_error(PB_ERR_ARG, "bad ell / shift");
   if (n <= 0) return PB_OK;
-  k_dealer<<<RING_GRID(n)>>>(op, mo, do_, n, k, d_in, d_out, seed, stream_id, raw_offset, ell);
+  k_dealer<<<RING_GRID(n)>>>(op, mo, do_, n, k, d_in, d_out, seed, seed_dev, stream_id, raw_offset, ell);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }

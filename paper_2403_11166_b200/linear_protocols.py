@@ -147,13 +147,30 @@ class Session:
         self.alg_bytes = {}  # entry point -> algorithmic HBM bytes (while instrumented)
         self.steps_seen = 0
         self._shards = {}
+        self.graph_mode = False
+        self._seed_dev = None
 
     def rng(self, layer: int, op: int, purpose: int) -> SeededRng:
-        return SeededRng(self.seed, stream_id(layer, op, purpose))
+        g = SeededRng(self.seed, stream_id(layer, op, purpose))
+        return g.bind(self._seed_dev.data_ptr()) if self.graph_mode else g
 
     def reseed(self, seed: int):
+        """Start a new step: every mask / share / noise stream is re-keyed.
+        In graph mode the seed is also written to the device word the
+        captured kernels read (seed indirection, pb_common.cuh)."""
         self.seed = int(seed)
         self.steps_seen += 1
+        if self._seed_dev is not None:
+            self._seed_host[0] = self.seed
+            self._seed_dev.copy_(self._seed_host, non_blocking=True)
+
+    def enable_graph_mode(self):
+        """Route the step seed through device memory so CUDA graphs can replay steps."""
+        if self.seed >= 1 << 63:
+            raise ValueError("graph mode needs seeds < 2^63 (numpy key derivation)")
+        self._seed_host = torch.tensor([self.seed], dtype=torch.int64).pin_memory()
+        self._seed_dev = torch.tensor([self.seed], dtype=torch.int64, device=_dev.device())
+        self.graph_mode = True
 
     def _count(self, name, nbytes):
         if _lib.STATS is not None:
@@ -186,7 +203,7 @@ class Session:
         if v_ct is not None and sh.n_out:  # term A: Enc(pi_v(v)) (x) pi_W(W)
             ct = _dev.empty_u32(sh.n_in, 2, L, N)
             _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(v_ct), *_pk(sh.in_pack), sh.n_in,
-                      enc_rng.device_key, base + self.rank * sh.n_in, _dev.ptr(ct), st)
+                      *enc_rng.dev_args(), base + self.rank * sh.n_in, _dev.ptr(ct), st)
             self._count("pb_encrypt_sk", sh.n_in * (ct_bytes + 8 * N))
             pt = _dev.empty_u32(sh.n_pt, L, N)
             sq = _dev.empty_u32(sh.n_pt, L, N)
@@ -199,7 +216,7 @@ class Session:
         if w_ct is not None and sh.n_out:  # term B: Enc(pi_W(W)) (x) pi_v(v)
             ct = _dev.empty_u32(sh.n_pt, 2, L, N)
             _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(w_ct), *_pk(sh.pt_pack), sh.n_pt,
-                      enc_rng.device_key, base + self.world * plan.n_in + self.rank * sh.n_pt, _dev.ptr(ct), st)
+                      *enc_rng.dev_args(), base + self.world * plan.n_in + self.rank * sh.n_pt, _dev.ptr(ct), st)
             self._count("pb_encrypt_sk", sh.n_pt * (ct_bytes + 8 * N))
             pt = _dev.empty_u32(sh.n_in, L, N)
             sq = _dev.empty_u32(sh.n_in, L, N)
@@ -231,10 +248,10 @@ class Session:
                 terms_d = sh.terms_device("none", none)
             K = terms_d.shape[1]
             out_ct = _dev.empty_u32(sh.n_out, 2, L, N)
-            fseed = self.rng(layer, op, P_MASK).device_key ^ 0x5A5A5A5A5A5A5A5A
+            fseed, fptr = self.rng(layer, op, P_MASK).dev_args()
             _lib.call("pb_ctpt_mac_mask", h, _dev.ptr(ct_all), _dev.ptr(pt_all), _dev.ptr(sq_all), _dev.ptr(terms_d),
                       K, sh.n_out, _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U, _dev.ptr(mask),
-                      1 if self.filler else 0, fseed, _dev.ptr(out_ct), st)
+                      1 if self.filler else 0, fseed ^ 0x5A5A5A5A5A5A5A5A, fptr, _dev.ptr(out_ct), st)
             n_ct_in = sum(c.shape[0] for c in cts)
             n_pt_in = sum(q[0].shape[0] for q in pts)
             self._count("pb_ctpt_mac_mask", n_ct_in * ct_bytes + n_pt_in * L * N * w + sh.n_out * ct_bytes)

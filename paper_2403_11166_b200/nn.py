@@ -92,9 +92,8 @@ def softmax_ce_grad(logits_2f: np.ndarray, labels: np.ndarray, ring: RingParams)
     return loss, np.floor(g * float(1 << ring.f)).astype(np.int64).astype(np.uint64) & ring.mask
 
 
-def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e-2, momentum=0.8,
-                       trace=None, check=True):
-    """One private step (SPEC:629-637); x (784, B) at scale f, held by the DO."""
+def forward_phase(sess: Session, model: Model, x: RingTensor):
+    """Private forward pass; returns (state for the backward pass, logits = MO share + DO share)."""
     ring, f = model.ring, model.ring.f
     L = model.n_layers
     acts = [(ShareTensor(MO, RingTensor(torch.zeros_like(x.values), f, ring, _canonical=True)), ShareTensor(DO, x))]
@@ -106,12 +105,20 @@ def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e
             z_mo, z_do, d = relu_forward(sess, l, *y)
             acts.append(truncate(sess, l, z_mo, z_do, f))
             ds.append(d)
-    # DO reconstructs the logits (MO sends its share) and computes the loss
+    # the MO sends its share of the logits; the DO reconstructs them
     y_mo, y_do = ys[-1]
-    logits = (y_mo.value + y_do.value).numpy()
-    loss, g = softmax_ce_grad(logits, np.asarray(labels), ring)
-    gy_do = ShareTensor(DO, RingTensor(_dev.u64_to_device(g), f, ring, _canonical=True))
-    gy_mo = ShareTensor(MO, RingTensor(torch.zeros_like(gy_do.value.values), f, ring, _canonical=True))
+    logits = y_mo.value + y_do.value
+    return (acts, ds, ys), logits
+
+
+def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e-2, momentum=0.8, trace=None,
+                   check=True):
+    """Private backward pass from the DO's loss gradient share (MO share 0) + SGD at the MO."""
+    ring, f = model.ring, model.ring.f
+    L = model.n_layers
+    acts, ds, ys = state
+    gy_do = ShareTensor(DO, RingTensor(g_do, f, ring, _canonical=True))
+    gy_mo = ShareTensor(MO, RingTensor(torch.zeros_like(g_do), f, ring, _canonical=True))
     gws, gbs = [None] * L, [None] * L
     for l in reversed(range(L)):
         last = l == L - 1
@@ -124,7 +131,56 @@ def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e
             t_mo, t_do = truncate(sess, l, *ga, f, backward=True)
             gy_mo, gy_do = relu_backward(sess, l - 1, ds[l - 1], t_mo, t_do)
     model.sgd(gws, gbs, lr, momentum, check=check)
+    return gws, gbs
+
+
+def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e-2, momentum=0.8,
+                       trace=None, check=True):
+    """One private step (SPEC:629-637); x (784, B) at scale f, held by the DO."""
+    state, logits = forward_phase(sess, model, x)
+    loss, g = softmax_ce_grad(logits.numpy(), np.asarray(labels), model.ring)  # DO, float64 (host)
+    gws, gbs = backward_phase(sess, model, state, _dev.u64_to_device(g), lr, momentum, trace, check)
     return loss, gws, gbs
+
+
+class GraphStep:
+    """A private training step replayed from two CUDA graphs (forward up to
+    the logits, backward + SGD from the DO's loss gradient), with the DO's
+    float64 softmax-CE on the host in between.  All randomness is re-keyed
+    per step through the device seed word (Session.enable_graph_mode), and
+    every kernel of the step is the same sm_100a kernel the eager path runs:
+    the graphs only remove per-launch host overhead."""
+
+    def __init__(self, sess: Session, model: Model, x: RingTensor, lr=1e-2, momentum=0.8):
+        self.sess, self.model, self.lr, self.momentum = sess, model, lr, momentum
+        sess.enable_graph_mode()
+        self.x = x  # device input buffer; callers copy new batches into x.values
+        n_cls, B = model.sizes[-1], x.shape[1]
+        self.g_do = torch.zeros(n_cls, B, dtype=torch.int64, device=x.values.device)
+        self.logits_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
+        self.g_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
+        # warm-up (eager, graph-mode keys): builds plans/maps, sizes scratch buffers
+        st, lg = forward_phase(sess, model, x)
+        backward_phase(sess, model, st, self.g_do, lr, momentum, check=False)
+        torch.cuda.synchronize()
+        self.g_fwd = torch.cuda.CUDAGraph()
+        self.g_bwd = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g_fwd):
+            self.state, self.logits = forward_phase(sess, model, x)
+        with torch.cuda.graph(self.g_bwd, pool=self.g_fwd.pool()):
+            self.grads = backward_phase(sess, model, self.state, self.g_do, lr, momentum, check=False)
+        torch.cuda.synchronize()
+
+    def step(self, seed: int, labels):
+        self.sess.reseed(seed)
+        self.g_fwd.replay()
+        self.logits_host.copy_(self.logits.values, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        loss, g = softmax_ce_grad(self.logits_host.numpy().view(np.uint64), np.asarray(labels), self.model.ring)
+        self.g_host.numpy().view(np.uint64)[...] = g
+        self.g_do.copy_(self.g_host, non_blocking=True)
+        self.g_bwd.replay()
+        return loss
 
 
 def synthetic_mnist(seed: int, B: int, ring: RingParams):

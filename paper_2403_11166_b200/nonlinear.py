@@ -33,7 +33,8 @@ def _dealer(sess: Session, layer: int, op_code: int, kind: int, a: ShareTensor, 
     d_out = torch.empty(x_mo.shape, dtype=torch.uint8, device=x_mo.device) if want_d else None
     rng = sess.rng(layer, op_code, P_DEALER)
     off = rng.reserve(n)
-    _lib.call("pb_dealer_op", kind, _dev.ptr(x_mo), _dev.ptr(x_do), n, k, _dev.ptr(d_in), _dev.ptr(d_out), rng.seed,
+    sd, sp = rng.np_args()
+    _lib.call("pb_dealer_op", kind, _dev.ptr(x_mo), _dev.ptr(x_do), n, k, _dev.ptr(d_in), _dev.ptr(d_out), sd, sp,
               rng.stream, off, ring.ell, _dev.stream())
     return x_mo, x_do, d_out
 

@@ -71,15 +71,36 @@ class SeededRng:  # R:48-90
     def child(self, stream: int) -> "SeededRng":
         return SeededRng(self.seed_arg, stream)
 
+    seed_ptr = None  # device address of the step seed (CUDA-graph mode), see bind()
+
+    def bind(self, seed_ptr: int) -> "SeededRng":
+        """Read key word 0 from device memory at kernel run time (graph replay);
+        the device value must equal this generator's seed whenever it runs."""
+        self.seed_ptr = seed_ptr
+        return self
+
+    @property
+    def _stream_const(self) -> int:
+        return (self.stream * 0xD1B54A32D192ED03 + 0x632BE59BD9B4E019) & ((1 << 64) - 1)
+
     @property
     def device_key(self) -> int:
         """64-bit key for the device-only Philox4x32 streams (encryption noise,
-        mask filler): a splitmix64 mix of (seed, stream), distinct per stream."""
+        mask filler): fmix64(seed * G + C(stream)), distinct per stream
+        (the same mixing as dev_key() in pb_common.cuh)."""
         M = (1 << 64) - 1
-        z = (self.seed * 0x9E3779B97F4A7C15 + self.stream * 0xD1B54A32D192ED03 + 0x632BE59BD9B4E019) & M
+        z = (self.seed * 0x9E3779B97F4A7C15 + self._stream_const) & M
         z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
         z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
         return z ^ (z >> 31)
+
+    def np_args(self):
+        """(seed, seed_dev) for numpy-identical device streams."""
+        return (0, self.seed_ptr) if self.seed_ptr else (self.seed, None)
+
+    def dev_args(self):
+        """(seed, seed_dev) for device-only streams."""
+        return (self._stream_const, self.seed_ptr) if self.seed_ptr else (self.device_key, None)
 
     # -- position bookkeeping -------------------------------------------------
     def reserve(self, n: int) -> int:
@@ -123,7 +144,8 @@ class SeededRng:  # R:48-90
         n = int(np.prod(shape)) if shape else 1
         out = _dev.empty_u64(n)
         off = self.reserve(n)
-        _lib.call("pb_uniform_ring", _dev.ptr(out), n, self.seed, self.stream, off, params.ell, _dev.stream())
+        sd, sp = self.np_args()
+        _lib.call("pb_uniform_ring", _dev.ptr(out), n, sd, sp, self.stream, off, params.ell, _dev.stream())
         return out.view(shape)
 
     def _host_draw(self, fn):
@@ -324,7 +346,8 @@ def share_tensor(x: RingTensor, rng: SeededRng) -> tuple[ShareTensor, ShareTenso
     do = torch.empty_like(x.values)
     off = rng.reserve(n)
     if n:
-        _lib.call("pb_share", _dev.ptr(x.values), n, rng.seed, rng.stream, off, x.params.ell, _dev.ptr(mo),
+        sd, sp = rng.np_args()
+        _lib.call("pb_share", _dev.ptr(x.values), n, sd, sp, rng.stream, off, x.params.ell, _dev.ptr(mo),
                   _dev.ptr(do), _dev.stream())
     return (ShareTensor(MO, RingTensor(mo, x.scale, x.params, _canonical=True)),
             ShareTensor(DO, RingTensor(do, x.scale, x.params, _canonical=True)))

@@ -21,7 +21,7 @@ def test_uniform_ring_matches_numpy(seed, stream, n, off):
 
     key = np.random.Philox(key=[seed, stream]).state["state"]["key"]  # numpy's own key derivation
     out = _dev.empty_u64(n)
-    _lib.call("pb_uniform_ring", _dev.ptr(out), n, int(key[0]), int(key[1]), off, 59, _dev.stream())
+    _lib.call("pb_uniform_ring", _dev.ptr(out), n, int(key[0]), None, int(key[1]), off, 59, _dev.stream())
     assert np.array_equal(_dev.to_numpy_u64(out), _np_ring(seed, stream, n, off))
     # through the SeededRng mirror, interleaving device and host draws
     g = SeededRng(seed, stream)
@@ -41,7 +41,7 @@ def test_share_matches_numpy():
     x = rng.integers(0, 1 << 59, size=333, dtype=np.uint64)
     mo, do = _dev.empty_u64(333), _dev.empty_u64(333)
     dx = _dev.u64_to_device(x)
-    _lib.call("pb_share", _dev.ptr(dx), 333, 99, 3, 0, 59, _dev.ptr(mo), _dev.ptr(do), _dev.stream())
+    _lib.call("pb_share", _dev.ptr(dx), 333, 99, None, 3, 0, 59, _dev.ptr(mo), _dev.ptr(do), _dev.stream())
     r = _np_ring(99, 3, 333)
     assert np.array_equal(_dev.to_numpy_u64(mo), r)
     assert np.array_equal(_dev.to_numpy_u64(do), (x - r) & np.uint64((1 << 59) - 1))
