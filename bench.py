@@ -198,7 +198,8 @@ def run_ours(args, rank, world):
     # ---- kernel profile pass (eager, CUDA events around every fused entry point):
     #      per-kernel durations + algorithmic bytes, kernel launches per step
     prof_steps = 3
-    stats = _lib.CallStats(timed=("pb_ctpt_mac_mask", "pb_decrypt_to_share", "pb_encrypt_sk", "pb_encode_plain"))
+    stats = _lib.CallStats(timed=("pb_ctpt_mac_tiled", "pb_mask_ntt", "pb_decrypt_to_share", "pb_encrypt_sk",
+                                  "pb_encode_plain_mont"))
     sess.alg_bytes.clear()
     _lib.STATS = stats
     for i in range(prof_steps):

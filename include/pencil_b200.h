@@ -191,6 +191,23 @@ int pb_ctpt_mac_mask(const pb_ctx* ctx, const uint32_t* ct_in, const uint32_t* p
                      const uint64_t* mask_vals, int filler, uint64_t filler_seed, const uint64_t* seed_dev,
                      uint32_t* ct_out, void* stream);
 
+/* Tiled MO evaluation (the production path of Alg.1/Alg.2), in two steps:
+ *  pb_mask_ntt:  ct_out[p].c0 = -Delta*NTT(mask_p)  (mask_p as in pb_ctpt_mac_mask:
+ *                mask_vals at out_pos / filler elsewhere); c1 untouched.
+ *  pb_ctpt_mac_tiled: for the nB x nO grid of outputs r = b*nO + o,
+ *                ct_out[r].c0 += sum_k ctA[b*nI+k].c0 (*) ptA[o*nI+k] (+ ctB[o*nI+k].c0 (*) ptB[b*nI+k]),
+ *                ct_out[r].c1  = the same sums over c1.
+ *                Plaintexts in Montgomery form (pb_encode_plain_mont); either
+ *                term may be absent (NULL ct). */
+int pb_encode_plain_mont(const pb_ctx* ctx, const uint64_t* vals, const int32_t* pack_pos,
+                         const int32_t* pack_src, int32_t Z, int64_t P, uint32_t* pt_mont, void* stream);
+int pb_mask_ntt(const pb_ctx* ctx, int64_t P, const int32_t* out_pos, const int64_t* out_dst, int32_t U,
+                const uint64_t* mask_vals, int filler, uint64_t filler_seed, const uint64_t* seed_dev,
+                uint32_t* ct_out, void* stream);
+int pb_ctpt_mac_tiled(const pb_ctx* ctx, const uint32_t* ctA, const uint32_t* ptA_mont, const uint32_t* ctB,
+                      const uint32_t* ptB_mont, int32_t nB, int32_t nO, int32_t nI, uint32_t* ct_out,
+                      void* stream);
+
 /* ------------------------------------------- ring Z_{2^ell} (R:93-233) --- */
 enum {
   PB_RING_ADD = 0, /* R:132-134 */

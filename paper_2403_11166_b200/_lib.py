@@ -66,6 +66,9 @@ SIGNATURES = {
     "pb_decrypt": [P, P, P, I64, P, P, P],
     "pb_decrypt_to_share": [P, P, P, I64, P, P, I32, P, P, P],
     "pb_ctpt_mac_mask": [P, P, P, P, P, I32, I64, P, P, I32, P, INT, U64, P, P, P],
+    "pb_encode_plain_mont": [P, P, P, P, I32, I64, P, P],
+    "pb_mask_ntt": [P, I64, P, P, I32, P, INT, U64, P, P, P],
+    "pb_ctpt_mac_tiled": [P, P, P, P, P, I32, I32, I32, P, P],
     "pb_ring_binary": [INT, P, P, P, I64, I64, I32, P],
     "pb_ring_unary": [INT, P, P, U64, I64, I32, P],
     "pb_encode_fixed": [P, I64, I32, I32, P, P, P],

@@ -22,6 +22,8 @@ struct PbDev {
   uint32_t delta[PB_MAXL], delta_sh[PB_MAXL];  // floor(Q/t) mod q_i
   uint64_t mu[PB_MAXL];                        // floor(2^64 / q) (Barrett)
   double inv_q32[PB_MAXL];                     // 2^32 / q (Shoup quotient estimate)
+  uint32_t qn[PB_MAXL];                        // -q^-1 mod 2^32 (Montgomery)
+  uint32_t r2[PB_MAXL], r2_sh[PB_MAXL];        // 2^32 mod q (to Montgomery form) + Shoup
   uint32_t tmod[PB_MAXL];                      // t mod q_i (centered lift)
   uint32_t pinv[PB_MAXL], pinv_sh[PB_MAXL];    // Garner (q_0..q_{i-1})^-1 mod q_i
   uint32_t pmod[PB_MAXL][PB_MAXL];             // pmod[i][k] = (q_0..q_{k-1}) mod q_i

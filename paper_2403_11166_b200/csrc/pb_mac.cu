@@ -1,0 +1,277 @@
+// pb_mac.cu — MO-side evaluation of the packed matmul/conv products, tiled.
+//
+// The MO's work for one protocol message (Alg.1 step 2-3, Alg.2 step 2) is
+//   out[b,o] = sum_k ctA[b,k] (*) ptA[o,k]  (+ sum_k ctB[o,k] (*) ptB[b,k])  -  Delta*NTT(mask[b,o])
+// over an (nB x nO) grid of output ciphertexts with nI input blocks.  It is
+// split into two kernels:
+//   k_mask_ntt    one CTA per (output, limb): builds Delta*(mask + filler) in
+//                 shared memory, forward NTT in registers, writes -mask into
+//                 the output's c0 row (device order);
+//   k_mac_tiled   a TB x TO tile of outputs per CTA and a 512-coefficient
+//                 slice of one limb: every ciphertext / plaintext vector is
+//                 loaded once per tile (TB*TO/(TB+TO)-fold reuse instead of
+//                 one reload per output), multiplied in Montgomery form (the
+//                 plaintexts are stored as pt*2^32 mod q, so no Shoup
+//                 companion row is streamed), accumulated in registers and
+//                 written once.
+#include "pb_pack.cuh"
+
+namespace {
+
+using pbk::mont_lazy;
+
+__device__ __forceinline__ uint32_t delta_m(const PbDev& P, int l, uint64_t m) {
+  const uint32_t q = P.q[l];
+  return mul_shoup(reduce64(m, q, P.mu[l]), P.delta[l], P.delta_sh[l], q);
+}
+
+__device__ __forceinline__ void uniform_pair(uint64_t seed, int64_t p, int l, int jpair, uint32_t q, uint32_t domain,
+                                             uint32_t& x0, uint32_t& x1) {
+  const uint64_t pp = (uint64_t)p;
+  const u32x4 r = philox4x32_10((uint32_t)jpair | ((uint32_t)l << 24), (uint32_t)pp, (uint32_t)(pp >> 32), domain,
+                                (uint32_t)seed, (uint32_t)(seed >> 32));
+  const uint64_t a = ((uint64_t)r.v[1] << 32) | r.v[0];
+  const uint64_t b = ((uint64_t)r.v[3] << 32) | r.v[2];
+  x0 = (uint32_t)__umul64hi(a, q);
+  x1 = (uint32_t)__umul64hi(b, q);
+}
+
+// ------------------------------------------------ plaintexts, Montgomery ---
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5))
+    k_encode_plain_mont(PbDev P, pbk::Pack src, int64_t nP, uint32_t* pt) {
+  using Nt = pb::Ntt<LOGN>;
+  extern __shared__ uint32_t sm[];
+  const int tid = threadIdx.x;
+  const int L = P.L;
+  const int64_t p = blockIdx.x / L;
+  const int l = blockIdx.x % L;
+  const uint32_t q = P.q[l];
+  const uint64_t mu = P.mu[l];
+  const uint32_t tm = P.tmod[l];
+  const int ell = P.ell;
+  uint32_t a[32];
+  pbk::load_source<Nt>(a, sm, src, p, tid, [&](uint64_t v) { return lift_centered(v, ell, q, mu, tm); });
+  Nt::forward(a, sm, P.tw_fwd + (size_t)l * Nt::N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
+  const uint32_t r2 = P.r2[l], r2s = P.r2_sh[l];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = mul_shoup(pb::canon4(a[c], q), r2, r2s, q);
+  Nt::gst3(pt + (p * L + l) * Nt::N, a, tid);
+}
+
+// ----------------------------------------------------------- mask NTT ----
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5))
+    k_mask_ntt(PbDev P, int64_t nP, const int32_t* out_pos, const int64_t* out_dst, int U, const uint64_t* mask_vals,
+               int filler, uint64_t filler_arg, const uint64_t* seed_dev, uint32_t* ct_out) {
+  using Nt = pb::Ntt<LOGN>;
+  constexpr int N = Nt::N;
+  extern __shared__ uint32_t sm[];
+  const int tid = threadIdx.x;
+  const int L = P.L;
+  const int64_t p = blockIdx.x / L;
+  const int l = blockIdx.x % L;
+  const uint32_t q = P.q[l];
+  if (filler) {
+    const uint64_t fseed = dev_key(filler_arg, seed_dev);
+    for (int jp = tid; jp < N / 2; jp += Nt::T) {
+      uint32_t x0, x1;
+      uniform_pair(fseed, p, l, jp, q, 0x4d41534bu /* "MASK" */, x0, x1);
+      sm[Nt::pad(2 * jp)] = x0;
+      sm[Nt::pad(2 * jp + 1)] = x1;
+    }
+  } else {
+    for (int j = tid; j < N; j += Nt::T) sm[Nt::pad(j)] = 0u;
+  }
+  __syncthreads();
+  if (mask_vals) {
+    const int32_t* pos = out_pos + p * U;
+    const int64_t* dst = out_dst + p * U;
+    for (int u = tid; u < U; u += Nt::T) {
+      const int j = pos[u];
+      if (j >= 0) sm[Nt::pad(j)] = delta_m(P, l, __ldg(mask_vals + dst[u]));
+    }
+  }
+  __syncthreads();
+  uint32_t m[32];
+  Nt::ld1(sm, m, tid);
+  __syncthreads();
+  Nt::forward(m, sm, P.tw_fwd + (size_t)l * N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const uint32_t v = pb::canon4(m[c], q);
+    m[c] = v ? q - v : 0u;  // -mask, added by the MAC
+  }
+  Nt::gst3(ct_out + ((size_t)p * 2 * L + l) * N, m, tid);
+}
+
+// ------------------------------------------------------------ tiled MAC ---
+constexpr int MAC_THREADS = 128;  // one uint4 (4 coefficients) per thread per row slice
+
+template <int TB, int TO>
+__global__ void __launch_bounds__(MAC_THREADS)
+    k_mac_tiled(PbDev P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB, int nB,
+                int nO, int nI, uint32_t* ct_out) {
+  const int N = P.N, L = P.L;
+  const int slices = N / (4 * MAC_THREADS);
+  const int tilesO = (nO + TO - 1) / TO;
+  const int tb = blockIdx.x / tilesO, to = blockIdx.x % tilesO;
+  const int l = blockIdx.y / slices, sl = blockIdx.y % slices;
+  const uint32_t q = P.q[l], qn = P.qn[l];
+  const size_t row = (size_t)N / 4;  // uint4 per row
+  const size_t v = (size_t)sl * MAC_THREADS + threadIdx.x;
+  const uint4* cA = reinterpret_cast<const uint4*>(ctA);
+  const uint4* pA = reinterpret_cast<const uint4*>(ptA);
+  const uint4* cB = reinterpret_cast<const uint4*>(ctB);
+  const uint4* pB = reinterpret_cast<const uint4*>(ptB);
+  uint32_t acc[TB][TO][2][4];
+#pragma unroll
+  for (int i = 0; i < TB; ++i)
+#pragma unroll
+    for (int o = 0; o < TO; ++o)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[i][o][c][e] = 0u;
+  bool okb[TB], oko[TO];
+#pragma unroll
+  for (int i = 0; i < TB; ++i) okb[i] = tb * TB + i < nB;
+#pragma unroll
+  for (int o = 0; o < TO; ++o) oko[o] = to * TO + o < nO;
+
+  auto mac4 = [&](uint32_t (&a)[4], const uint4& x, const uint4& w) {
+    a[0] = addmod(a[0], csub(mont_lazy(x.x, w.x, q, qn), q), q);
+    a[1] = addmod(a[1], csub(mont_lazy(x.y, w.y, q, qn), q), q);
+    a[2] = addmod(a[2], csub(mont_lazy(x.z, w.z, q, qn), q), q);
+    a[3] = addmod(a[3], csub(mont_lazy(x.w, w.w, q, qn), q), q);
+  };
+  const uint4 z4 = make_uint4(0, 0, 0, 0);
+  for (int k = 0; k < nI; ++k) {
+    if (cA) {  // term A: ctA[b-block] (*) ptA[o-block]
+      uint4 x0[TB], x1[TB], w[TO];
+#pragma unroll
+      for (int i = 0; i < TB; ++i) {
+        const size_t base = ((size_t)((tb * TB + i) * nI + k) * 2 * L + l) * row + v;
+        x0[i] = okb[i] ? __ldg(cA + base) : z4;
+        x1[i] = okb[i] ? __ldg(cA + base + (size_t)L * row) : z4;
+      }
+#pragma unroll
+      for (int o = 0; o < TO; ++o) w[o] = oko[o] ? __ldg(pA + ((size_t)((to * TO + o) * nI + k) * L + l) * row + v) : z4;
+#pragma unroll
+      for (int i = 0; i < TB; ++i)
+#pragma unroll
+        for (int o = 0; o < TO; ++o) {
+          mac4(acc[i][o][0], x0[i], w[o]);
+          mac4(acc[i][o][1], x1[i], w[o]);
+        }
+    }
+    if (cB) {  // term B: ctB[o-block] (*) ptB[b-block]
+      uint4 y0[TO], y1[TO], u[TB];
+#pragma unroll
+      for (int o = 0; o < TO; ++o) {
+        const size_t base = ((size_t)((to * TO + o) * nI + k) * 2 * L + l) * row + v;
+        y0[o] = oko[o] ? __ldg(cB + base) : z4;
+        y1[o] = oko[o] ? __ldg(cB + base + (size_t)L * row) : z4;
+      }
+#pragma unroll
+      for (int i = 0; i < TB; ++i) u[i] = okb[i] ? __ldg(pB + ((size_t)((tb * TB + i) * nI + k) * L + l) * row + v) : z4;
+#pragma unroll
+      for (int i = 0; i < TB; ++i)
+#pragma unroll
+        for (int o = 0; o < TO; ++o) {
+          mac4(acc[i][o][0], y0[o], u[i]);
+          mac4(acc[i][o][1], y1[o], u[i]);
+        }
+    }
+  }
+  uint4* out = reinterpret_cast<uint4*>(ct_out);
+#pragma unroll
+  for (int i = 0; i < TB; ++i)
+#pragma unroll
+    for (int o = 0; o < TO; ++o) {
+      if (!(okb[i] && oko[o])) continue;
+      const size_t r = (size_t)(tb * TB + i) * nO + (to * TO + o);
+      const size_t b0 = (r * 2 * L + l) * row + v;
+      const uint4 m = out[b0];  // -mask written by k_mask_ntt
+      out[b0] = make_uint4(addmod(acc[i][o][0][0], m.x, q), addmod(acc[i][o][0][1], m.y, q),
+                           addmod(acc[i][o][0][2], m.z, q), addmod(acc[i][o][0][3], m.w, q));
+      out[b0 + (size_t)L * row] = make_uint4(acc[i][o][1][0], acc[i][o][1][1], acc[i][o][1][2], acc[i][o][1][3]);
+    }
+}
+
+template <typename KernelT>
+void set_smem(KernelT k, size_t smem) {
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <int LOGN>
+void launch_encode_mont(const PbDev& P, pbk::Pack src, int64_t nP, uint32_t* pt, cudaStream_t st) {
+  using Nt = pb::Ntt<LOGN>;
+  const size_t smem = Nt::SMEM_WORDS * 4;
+  set_smem(k_encode_plain_mont<LOGN>, smem);
+  k_encode_plain_mont<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, src, nP, pt);
+}
+
+template <int LOGN>
+void launch_mask(const PbDev& P, int64_t nP, const int32_t* out_pos, const int64_t* out_dst, int U,
+                 const uint64_t* mask_vals, int filler, uint64_t fseed, const uint64_t* seed_dev, uint32_t* ct_out,
+                 cudaStream_t st) {
+  using Nt = pb::Ntt<LOGN>;
+  const size_t smem = Nt::SMEM_WORDS * 4;
+  set_smem(k_mask_ntt<LOGN>, smem);
+  k_mask_ntt<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, nP, out_pos, out_dst, U, mask_vals, filler, fseed,
+                                                              seed_dev, ct_out);
+}
+
+int check_ctx(const pb_ctx* ctx) {
+  if (!ctx) return pb_set_error(PB_ERR_ARG, "null context");
+  if (ctx->dev.logN < 11) return pb_set_error(PB_ERR_PARAMS, "fused BFV kernels need N >= 2048");
+  return PB_OK;
+}
+
+}  // namespace
+
+extern "C" int pb_encode_plain_mont(const pb_ctx* ctx, const uint64_t* vals, const int32_t* pack_pos,
+                                    const int32_t* pack_src, int32_t Z, int64_t P, uint32_t* pt_mont, void* stream) {
+  if (int s = check_ctx(ctx)) return s;
+  if (P <= 0) return PB_OK;
+  if (!vals || !pt_mont) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (pack_pos && (!pack_src || Z < 0)) return pb_set_error(PB_ERR_ARG, "packed source needs pos, src and Z");
+  if (P > (int64_t)0x7fffffff / ctx->dev.L) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  pbk::Pack src{vals, pack_pos, pack_src, pack_pos ? Z : 0};
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encode_mont, ctx->dev, src, P, pt_mont, pb_stream_of(stream));
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_mask_ntt(const pb_ctx* ctx, int64_t P, const int32_t* out_pos, const int64_t* out_dst, int32_t U,
+                           const uint64_t* mask_vals, int filler, uint64_t filler_seed, const uint64_t* seed_dev,
+                           uint32_t* ct_out, void* stream) {
+  if (int s = check_ctx(ctx)) return s;
+  if (P <= 0) return PB_OK;
+  if (!ct_out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (mask_vals && (!out_pos || !out_dst)) return pb_set_error(PB_ERR_ARG, "mask needs out_pos/out_dst");
+  if (P > (int64_t)0x7fffffff / ctx->dev.L) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_mask, ctx->dev, P, out_pos, out_dst, U, mask_vals, filler, filler_seed,
+                   seed_dev, ct_out, pb_stream_of(stream));
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_ctpt_mac_tiled(const pb_ctx* ctx, const uint32_t* ctA, const uint32_t* ptA_mont, const uint32_t* ctB,
+                                 const uint32_t* ptB_mont, int32_t nB, int32_t nO, int32_t nI, uint32_t* ct_out,
+                                 void* stream) {
+  if (int s = check_ctx(ctx)) return s;
+  if (nB <= 0 || nO <= 0) return PB_OK;
+  if (!ct_out || (!ctA && !ctB)) return pb_set_error(PB_ERR_ARG, "null argument");
+  if ((ctA && !ptA_mont) || (ctB && !ptB_mont)) return pb_set_error(PB_ERR_ARG, "each term needs ct and pt");
+  if (nI < 1) return pb_set_error(PB_ERR_SHAPE, "nI must be >= 1");
+  const int N = ctx->dev.N, L = ctx->dev.L;
+  const int slices = N / (4 * MAC_THREADS);
+  const unsigned tiles = (unsigned)(((nB + 1) / 2) * ((nO + 1) / 2));
+  dim3 grid(tiles, (unsigned)(L * slices));
+  k_mac_tiled<2, 2><<<grid, MAC_THREADS, 0, pb_stream_of(stream)>>>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI,
+                                                                   ct_out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}

@@ -1,0 +1,54 @@
+// pb_pack.cuh — packed plaintext sources (compact pi_v / pi_W maps) and
+// Montgomery arithmetic shared by the MO-side kernels.
+#pragma once
+
+#include "pb_ntt.cuh"
+
+namespace pbk {
+
+// A plaintext source: `vals` is a flat Z_t tensor.  With `pos` set, poly p
+// has coefficient pos[p][z] = vals[src[p][z]] for z < Z (pos < 0: unused
+// slot) and zeros elsewhere -- the compact form of the packing maps pi_v /
+// pi_W.  With pos == NULL, vals is a dense [P][N] array.
+struct Pack {
+  const uint64_t* vals;
+  const int32_t* pos;
+  const int32_t* src;
+  int Z;
+};
+
+// Loads the lifted source polynomial p into a[] in the NTT's P1 layout; the
+// packed path builds the row in shared memory and leaves `sm` free.
+template <class Nt, class Lift>
+__device__ __forceinline__ void load_source(uint32_t (&a)[32], uint32_t* sm, const Pack& s, int64_t p, int tid,
+                                            Lift lift) {
+  if (s.pos) {
+    for (int j = tid; j < Nt::N; j += Nt::T) sm[Nt::pad(j)] = 0u;
+    __syncthreads();
+    const int32_t* pp = s.pos + p * s.Z;
+    const int32_t* ps = s.src + p * s.Z;
+    for (int z = tid; z < s.Z; z += Nt::T) {
+      const int j = __ldg(pp + z);
+      if (j >= 0) sm[Nt::pad(j)] = lift(__ldg(s.vals + __ldg(ps + z)));
+    }
+    __syncthreads();
+    Nt::ld1(sm, a, tid);
+    __syncthreads();
+  } else {
+    const uint64_t* v = s.vals + p * Nt::N;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a[c] = lift(__ldg(v + Nt::j1(tid, c)));
+  }
+}
+
+// Montgomery multiplication with R = 2^32: returns a*b*R^-1 mod q in [0, 2q)
+// for a, b < q.  qn = -q^-1 mod 2^32.  Plaintext multipliers are stored in
+// Montgomery form (pt*R mod q) so mont(ct, ptR) = ct*pt mod q and no Shoup
+// companion row has to be streamed.
+__device__ __forceinline__ uint32_t mont_lazy(uint32_t a, uint32_t b, uint32_t q, uint32_t qn) {
+  const uint64_t t = (uint64_t)a * b;
+  const uint32_t m = (uint32_t)t * qn;
+  return (uint32_t)((t + (uint64_t)m * q) >> 32);
+}
+
+}  // namespace pbk

@@ -82,6 +82,13 @@ extern "C" int pb_ctx_create(const pb_params* p, pb_ctx** out) {
     d.delta_sh[i] = h_shoup(d.delta[i], q);
     d.mu[i] = (uint64_t)(((unsigned __int128)1 << 64) / q);
     d.inv_q32[i] = 4294967296.0 / (double)q;
+    {
+      uint32_t inv = 1;  // Newton iteration for q^-1 mod 2^32 (q odd)
+      for (int it = 0; it < 5; ++it) inv *= 2u - q * inv;
+      d.qn[i] = 0u - inv;
+      d.r2[i] = (uint32_t)((1ull << 32) % q);
+      d.r2_sh[i] = h_shoup(d.r2[i], q);
+    }
     d.tmod[i] = (uint32_t)(t % q);
     d.pinv[i] = p->garner_prefix_inv[i] % q;
     d.pinv_sh[i] = h_shoup(d.pinv[i], q);

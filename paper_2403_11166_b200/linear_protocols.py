@@ -88,40 +88,36 @@ def _pk(pack):
     return _dev.ptr(pos), _dev.ptr(src), pos.shape[1]
 
 
+def shard_grid(nB: int, nO: int, rank: int, world: int):
+    """The rectangle [b0, b1) x [o0, o1) of the (nB x nO) output-ciphertext grid
+    that ``rank`` evaluates: split the batch blocks when there are enough of
+    them, else the output blocks (ranks beyond the available blocks idle)."""
+    if world <= 1:
+        return 0, nB, 0, nO
+    if nB >= world or nB >= nO:
+        return rank * nB // world, (rank + 1) * nB // world, 0, nO
+    return 0, nB, rank * nO // world, (rank + 1) * nO // world
+
+
 class _Shard:
-    """The part of a block plan one rank executes: its output ciphertexts
-    (round-robin over ranks) and exactly the input / plaintext polynomials
-    those outputs reference, with the MAC term list remapped to local indices."""
+    """One rank's part of a block plan: a rectangle of the (b-block x o-block)
+    output grid plus exactly the input-side polynomials (indices b*nI + k) and
+    weight-side polynomials (o*nI + k) it needs -- both contiguous ranges."""
 
     def __init__(self, plan, rank: int, world: int):
-        sel = np.arange(rank, plan.n_out, world)
-        t = plan.terms[sel]
-        self.in_idx = np.unique(t[:, :, 0]) if len(sel) else np.zeros(0, dtype=np.int64)
-        self.pt_idx = np.unique(t[:, :, 1]) if len(sel) else np.zeros(0, dtype=np.int64)
-        li = np.searchsorted(self.in_idx, t[:, :, 0])
-        lp = np.searchsorted(self.pt_idx, t[:, :, 1])
-        self.terms_a = np.stack([li, lp], axis=-1)  # Enc(in) (x) pt
-        self.terms_b = np.stack([lp, li], axis=-1)  # Enc(pt-side poly) (x) in-side plaintext
-        self.n_out, self.n_in, self.n_pt = len(sel), len(self.in_idx), len(self.pt_idx)
-        self.U = plan.U
-        from . import _dev
-
         from .poly_encoding import compact
 
-        self.in_pack = tuple(_dev.i32_to_device(a) for a in compact(plan.in_src[self.in_idx]))
-        self.pt_pack = tuple(_dev.i32_to_device(a) for a in compact(plan.pt_src[self.pt_idx]))
-        self.out_pos = _dev.i32_to_device(plan.out_pos[sel])
-        self.out_dst = _dev.i64_to_device(plan.out_dst[sel])
-        self._terms_dev = {}
-
-    def terms_device(self, key, terms):
-        t = self._terms_dev.get(key)
-        if t is None:
-            from . import _dev
-
-            t = _dev.i32_to_device(np.ascontiguousarray(terms, dtype=np.int32))
-            self._terms_dev[key] = t
-        return t
+        nB, nO, nI = plan.nblk
+        b0, b1, o0, o1 = shard_grid(nB, nO, rank, world)
+        self.nb, self.no, self.nI = max(0, b1 - b0), max(0, o1 - o0), nI
+        rows = (np.arange(b0, b1)[:, None] * nO + np.arange(o0, o1)[None, :]).reshape(-1)
+        self.n_out = len(rows)
+        self.n_in, self.n_pt = self.nb * nI, self.no * nI
+        self.U = plan.U
+        self.in_pack = tuple(_dev.i32_to_device(a) for a in compact(plan.in_src[b0 * nI:b1 * nI]))
+        self.pt_pack = tuple(_dev.i32_to_device(a) for a in compact(plan.pt_src[o0 * nI:o1 * nI]))
+        self.out_pos = _dev.i32_to_device(plan.out_pos[rows])
+        self.out_dst = _dev.i64_to_device(plan.out_dst[rows])
 
 
 class Session:
@@ -149,6 +145,7 @@ class Session:
         self._shards = {}
         self.graph_mode = False
         self._seed_dev = None
+        self._streams = None
 
     def rng(self, layer: int, op: int, purpose: int) -> SeededRng:
         g = SeededRng(self.seed, stream_id(layer, op, purpose))
@@ -171,6 +168,11 @@ class Session:
         self._seed_host = torch.tensor([self.seed], dtype=torch.int64).pin_memory()
         self._seed_dev = torch.tensor([self.seed], dtype=torch.int64, device=_dev.device())
         self.graph_mode = True
+
+    def _side_streams(self):
+        if self._streams is None:
+            self._streams = (torch.cuda.Stream(), torch.cuda.Stream())
+        return self._streams
 
     def _count(self, name, nbytes):
         if _lib.STATS is not None:
@@ -197,71 +199,73 @@ class Session:
         N, L = p.N, p.L
         w = 4  # bytes per residue
         ct_bytes = 2 * L * N * w
-        cts, pts, tkeys = [], [], []
         enc_rng = self.rng(layer, op, P_ENC)
         base = enc_rng.reserve((plan.n_in + plan.n_pt) * self.world)
-        if v_ct is not None and sh.n_out:  # term A: Enc(pi_v(v)) (x) pi_W(W)
-            ct = _dev.empty_u32(sh.n_in, 2, L, N)
-            _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(v_ct), *_pk(sh.in_pack), sh.n_in,
-                      *enc_rng.dev_args(), base + self.rank * sh.n_in, _dev.ptr(ct), st)
-            self._count("pb_encrypt_sk", sh.n_in * (ct_bytes + 8 * N))
-            pt = _dev.empty_u32(sh.n_pt, L, N)
-            sq = _dev.empty_u32(sh.n_pt, L, N)
-            _lib.call("pb_encode_plain", h, _dev.ptr(w_pt), *_pk(sh.pt_pack), sh.n_pt, _dev.ptr(pt), _dev.ptr(sq), st)
-            self._count("pb_encode_plain", sh.n_pt * (L * N * w + 8 * N))
-            cts.append(ct)
-            pts.append((pt, sq))
-            tkeys.append(("a", sh.terms_a))
-            self.channel.send(DO, msg_in, ct, Ciphertext(ct, p).nbytes_wire())
-        if w_ct is not None and sh.n_out:  # term B: Enc(pi_W(W)) (x) pi_v(v)
-            ct = _dev.empty_u32(sh.n_pt, 2, L, N)
-            _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(w_ct), *_pk(sh.pt_pack), sh.n_pt,
-                      *enc_rng.dev_args(), base + self.world * plan.n_in + self.rank * sh.n_pt, _dev.ptr(ct), st)
-            self._count("pb_encrypt_sk", sh.n_pt * (ct_bytes + 8 * N))
-            pt = _dev.empty_u32(sh.n_in, L, N)
-            sq = _dev.empty_u32(sh.n_in, L, N)
-            _lib.call("pb_encode_plain", h, _dev.ptr(v_pt), *_pk(sh.in_pack), sh.n_in, _dev.ptr(pt), _dev.ptr(sq), st)
-            self._count("pb_encode_plain", sh.n_in * (L * N * w + 8 * N))
-            cts.append(ct)
-            pts.append((pt, sq))
-            tkeys.append(("b", sh.terms_b))
+        ctA = ptA = ctB = ptB = None
         if self.world > 1:
             out.zero_()
+        # Buffers are allocated on the main stream; the DO's encryptions and the
+        # MO's plaintext encodings run on two side streams concurrently with the
+        # MO's mask NTT, and the MAC joins all three (the graph keeps the fork).
+        has_a = sh.n_out and v_ct is not None
+        has_b = sh.n_out and w_ct is not None
+        if has_a:
+            ctA = _dev.empty_u32(sh.n_in, 2, L, N)
+            ptA = _dev.empty_u32(sh.n_pt, L, N)
+        if has_b:
+            ctB = _dev.empty_u32(sh.n_pt, 2, L, N)
+            ptB = _dev.empty_u32(sh.n_in, L, N)
+        out_ct = _dev.empty_u32(sh.n_out, 2, L, N) if sh.n_out else None
+        main = torch.cuda.current_stream()
+        if has_a or has_b:
+            s_enc, s_pt = self._side_streams()
+            s_enc.wait_stream(main)
+            s_pt.wait_stream(main)
+            with torch.cuda.stream(s_enc):  # DO
+                se = _dev.stream()
+                if has_a:  # term A: Enc_DO(pi_v(v)) (x) pi_W(W)
+                    _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(v_ct), *_pk(sh.in_pack),
+                              sh.n_in, *enc_rng.dev_args(), base + self.rank * plan.n_in, _dev.ptr(ctA), se)
+                    self._count("pb_encrypt_sk", sh.n_in * (ct_bytes + 8 * N))
+                    self.channel.send(DO, msg_in, ctA, Ciphertext(ctA, p).nbytes_wire())
+                if has_b:  # term B: Enc_DO(pi_W(W)) (x) pi_v(v)
+                    _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(w_ct), *_pk(sh.pt_pack),
+                              sh.n_pt, *enc_rng.dev_args(), base + self.world * plan.n_in + self.rank * plan.n_pt,
+                              _dev.ptr(ctB), se)
+                    self._count("pb_encrypt_sk", sh.n_pt * (ct_bytes + 8 * N))
+                    self.channel.send(DO, msg_in, ctB, Ciphertext(ctB, p).nbytes_wire())
+            with torch.cuda.stream(s_pt):  # MO
+                sp = _dev.stream()
+                if has_a:
+                    _lib.call("pb_encode_plain_mont", h, _dev.ptr(w_pt), *_pk(sh.pt_pack), sh.n_pt, _dev.ptr(ptA), sp)
+                    self._count("pb_encode_plain_mont", sh.n_pt * (L * N * w + 8 * N))
+                if has_b:
+                    _lib.call("pb_encode_plain_mont", h, _dev.ptr(v_pt), *_pk(sh.in_pack), sh.n_in, _dev.ptr(ptB), sp)
+                    self._count("pb_encode_plain_mont", sh.n_in * (L * N * w + 8 * N))
         if sh.n_out:
-            # operands of both terms side by side, MAC term list remapped to them
-            if len(cts) == 2:
-                ct_all = torch.cat([cts[0], cts[1]])
-                pt_all = torch.cat([pts[0][0], pts[1][0]])
-                sq_all = torch.cat([pts[0][1], pts[1][1]])
-                t2 = tkeys[1][1].copy()
-                t2[:, :, 0] += cts[0].shape[0]
-                t2[:, :, 1] += pts[0][0].shape[0]
-                terms_d = sh.terms_device("ab", np.concatenate([tkeys[0][1], t2], axis=1))
-            elif len(cts) == 1:
-                ct_all, (pt_all, sq_all) = cts[0], pts[0]
-                terms_d = sh.terms_device(tkeys[0][0], tkeys[0][1])
-            else:  # no cross term at all: the DO decrypts an encryption of -mask
-                ct_all = torch.zeros(1, 2, L, N, dtype=torch.int32, device=_dev.device())
-                pt_all = sq_all = torch.zeros(1, L, N, dtype=torch.int32, device=_dev.device())
-                none = np.full((sh.n_out, 1, 2), -1, dtype=np.int64)
-                none[:, 0, 1] = 0
-                terms_d = sh.terms_device("none", none)
-            K = terms_d.shape[1]
-            out_ct = _dev.empty_u32(sh.n_out, 2, L, N)
+            # MO: out.c0 = -Delta NTT(mask + filler), then the tiled MAC accumulates onto it
             fseed, fptr = self.rng(layer, op, P_MASK).dev_args()
-            _lib.call("pb_ctpt_mac_mask", h, _dev.ptr(ct_all), _dev.ptr(pt_all), _dev.ptr(sq_all), _dev.ptr(terms_d),
-                      K, sh.n_out, _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U, _dev.ptr(mask),
+            _lib.call("pb_mask_ntt", h, sh.n_out, _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U, _dev.ptr(mask),
                       1 if self.filler else 0, fseed ^ 0x5A5A5A5A5A5A5A5A, fptr, _dev.ptr(out_ct), st)
-            n_ct_in = sum(c.shape[0] for c in cts)
-            n_pt_in = sum(q[0].shape[0] for q in pts)
-            self._count("pb_ctpt_mac_mask", n_ct_in * ct_bytes + n_pt_in * L * N * w + sh.n_out * ct_bytes)
+            self._count("pb_mask_ntt", sh.n_out * (L * N * w + 8 * sh.U))
+            if has_a or has_b:
+                main.wait_stream(s_enc)
+                main.wait_stream(s_pt)
+            if ctA is None and ctB is None:  # no cross term: the DO decrypts an encryption of -mask
+                out_ct[:, 1].zero_()
+            else:
+                _lib.call("pb_ctpt_mac_tiled", h, _dev.ptr(ctA), _dev.ptr(ptA), _dev.ptr(ctB), _dev.ptr(ptB), sh.nb,
+                          sh.no, sh.nI, _dev.ptr(out_ct), st)
+                n_ct = (sh.n_in if ctA is not None else 0) + (sh.n_pt if ctB is not None else 0)
+                n_pt = (sh.n_pt if ctA is not None else 0) + (sh.n_in if ctB is not None else 0)
+                self._count("pb_ctpt_mac_tiled", n_ct * ct_bytes + n_pt * L * N * w + sh.n_out * (ct_bytes + L * N * w))
             self.channel.send(MO, msg_out, out_ct, Ciphertext(out_ct, p).nbytes_wire())
             scratch = _dev.empty_u32(sh.n_out, L, sh.U)
             _lib.call("pb_decrypt_to_share", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(out_ct), sh.n_out,
                       _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U, _dev.ptr(out), _dev.ptr(scratch), st)
             self._count("pb_decrypt_to_share", sh.n_out * (ct_bytes + 8 * sh.U))
-            # keep every operand alive until the kernels above are enqueued
-            del cts, pts, ct_all, pt_all, sq_all
+            # operands stay referenced until here, i.e. until every kernel is enqueued
+            del ctA, ptA, ctB, ptB, out_ct, scratch
         if self.world > 1:
             import torch.distributed as dist
 
