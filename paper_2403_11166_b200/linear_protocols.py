@@ -99,25 +99,36 @@ def shard_grid(nB: int, nO: int, rank: int, world: int):
     return 0, nB, rank * nO // world, (rank + 1) * nO // world
 
 
+def shard_maps(plan, rank: int, world: int) -> dict:
+    """Host-side (numpy) index maps of one rank's part of a block plan: a
+    rectangle of the (b-block x o-block) output grid plus exactly the
+    input-side polynomials (indices b*nI + k) and weight-side polynomials
+    (o*nI + k) it needs -- both contiguous ranges.  Output row r of the shard
+    is grid cell (b0 + r // no, o0 + r % no); its MAC terms are
+    (b*nI + k, o*nI + k) relative to the shard's own input / plaintext lists."""
+    from .poly_encoding import compact
+
+    nB, nO, nI = plan.nblk
+    b0, b1, o0, o1 = shard_grid(nB, nO, rank, world)
+    nb, no = max(0, b1 - b0), max(0, o1 - o0)
+    rows = (np.arange(b0, b1)[:, None] * nO + np.arange(o0, o1)[None, :]).reshape(-1)
+    return dict(rect=(b0, b1, o0, o1), nb=nb, no=no, nI=nI, n_out=len(rows), n_in=nb * nI, n_pt=no * nI,
+                U=plan.U, in_src=plan.in_src[b0 * nI:b1 * nI], pt_src=plan.pt_src[o0 * nI:o1 * nI],
+                in_pack=compact(plan.in_src[b0 * nI:b1 * nI]), pt_pack=compact(plan.pt_src[o0 * nI:o1 * nI]),
+                out_pos=plan.out_pos[rows], out_dst=plan.out_dst[rows])
+
+
 class _Shard:
-    """One rank's part of a block plan: a rectangle of the (b-block x o-block)
-    output grid plus exactly the input-side polynomials (indices b*nI + k) and
-    weight-side polynomials (o*nI + k) it needs -- both contiguous ranges."""
+    """Device copies of ``shard_maps`` (uploaded once per plan and rank)."""
 
     def __init__(self, plan, rank: int, world: int):
-        from .poly_encoding import compact
-
-        nB, nO, nI = plan.nblk
-        b0, b1, o0, o1 = shard_grid(nB, nO, rank, world)
-        self.nb, self.no, self.nI = max(0, b1 - b0), max(0, o1 - o0), nI
-        rows = (np.arange(b0, b1)[:, None] * nO + np.arange(o0, o1)[None, :]).reshape(-1)
-        self.n_out = len(rows)
-        self.n_in, self.n_pt = self.nb * nI, self.no * nI
-        self.U = plan.U
-        self.in_pack = tuple(_dev.i32_to_device(a) for a in compact(plan.in_src[b0 * nI:b1 * nI]))
-        self.pt_pack = tuple(_dev.i32_to_device(a) for a in compact(plan.pt_src[o0 * nI:o1 * nI]))
-        self.out_pos = _dev.i32_to_device(plan.out_pos[rows])
-        self.out_dst = _dev.i64_to_device(plan.out_dst[rows])
+        m = shard_maps(plan, rank, world)
+        self.nb, self.no, self.nI = m["nb"], m["no"], m["nI"]
+        self.n_out, self.n_in, self.n_pt, self.U = m["n_out"], m["n_in"], m["n_pt"], m["U"]
+        self.in_pack = tuple(_dev.i32_to_device(a) for a in m["in_pack"])
+        self.pt_pack = tuple(_dev.i32_to_device(a) for a in m["pt_pack"])
+        self.out_pos = _dev.i32_to_device(m["out_pos"])
+        self.out_dst = _dev.i64_to_device(m["out_dst"])
 
 
 class Session:
