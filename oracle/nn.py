@@ -5,12 +5,21 @@ models, the private training step composed from oracle/protocols.py, and
 ``reference_train_step`` -- the fixed-point Z_t pipeline without any
 cryptography that SPEC:620-628 defines as THE oracle for training parity.
 
+Model graphs (PAPER Appendix D) are lists of layer specs:
+  ("fc", n_i, n_o)                       feature-major activations (n, B)
+  ("conv", c_i, c_o, s, pad, stride)     activations (B, C, H, W)
+  ("pool",)                              AvgPool2 (SPEC:566-573)
+  ("flatten",)                           (B, C, H, W) -> (C*H*W, B)
+Every linear layer except the last is followed by ReLU + truncation by f.
+
 Step semantics (shared with paper_2403_11166_b200/nn.py):
-  forward  Y_l = W_l X_{l-1} + b_l (2f); A_l = trunc_f(relu(Y_l)) (f) for l < last
+  forward  Y_l = lin_l(X_{l-1}) + b_l (2f); A_l = trunc_f(relu(Y_l)) (f) for l < last;
+           pool: trunc_2(window sums); flatten: local transpose
   loss     DO reconstructs logits (2f), softmax-CE in float64, g = encode_f((p - y)/B)
            with the MO's share of g set to 0
-  backward gb_l = rowsum(gY_l) (f); gW_l = arith_shift(gY_l A_{l-1}^T, f) (2f -> f)
-           gA_{l-1} = trunc_f(W_l^T gY_l); gY_{l-1} = relu'(Y_{l-1}) * gA_{l-1}
+  backward gb_l = sums of gY_l (f); gW_l = arith_shift(grad_w(X_{l-1}, gY_l), f) (2f -> f)
+           gA_{l-1} = trunc_f(lin_l^T gY_l); pool: trunc_2(replicate); flatten^-1;
+           gY_{l-1} = relu'(Y_{l-1}) * gA_{l-1}
   update   SGD momentum in float64 on master weights:
            v = mu v + g;  w = w - lr v;  W = encode_f(w), b = encode_2f(b)
 """
@@ -19,27 +28,91 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import convops as CO
 from . import kernels as OK
 from . import protocols as PR
+from .packing import conv_out_hw
 from .ring import RingParams, SeededRng, decode_fixed, encode_fixed, to_signed
+
+MODELS = {
+    # PAPER Fig. 5 / SPEC:608
+    "mnist_mlp": ((784,), [("fc", 784, 128), ("fc", 128, 128), ("fc", 128, 10)]),
+    # PAPER Fig. 6 / SPEC:609: Conv 1->5 5x5 s2 p2, FC 980->100, FC 100->10
+    "mnist_cnn": ((1, 28, 28), [("conv", 1, 5, 5, 2, 2), ("flatten",), ("fc", 980, 100), ("fc", 100, 10)]),
+    # BASELINE configs[2] "2 x conv5x5 + FC": the paper's CNN plus a documented second conv
+    "mnist_cnn2": ((1, 28, 28), [("conv", 1, 5, 5, 2, 2), ("conv", 5, 5, 5, 2, 1), ("flatten",),
+                                 ("fc", 980, 100), ("fc", 100, 10)]),
+    # PAPER Fig. 7: the private-conv CIFAR-10 CNN
+    "cifar_cnn": ((3, 32, 32), [("conv", 3, 64, 5, 2, 1), ("pool",), ("conv", 64, 64, 5, 2, 1), ("pool",),
+                                ("conv", 64, 64, 3, 1, 1), ("conv", 64, 64, 1, 0, 1), ("conv", 64, 16, 1, 0, 1),
+                                ("flatten",), ("fc", 1024, 10)]),
+}
+
+
+def mlp_spec(sizes):
+    return (sizes[0],), [("fc", a, b) for a, b in zip(sizes[:-1], sizes[1:])]
+
+
+def shapes(in_shape, layers):
+    """Per-entry (input shape, output shape) of one sample, validating composition."""
+    cur = tuple(in_shape)
+    out = []
+    for e in layers:
+        if e[0] == "fc":
+            if cur != (e[1],):
+                raise ValueError(f"fc expects ({e[1]},), got {cur}")
+            nxt = (e[2],)
+        elif e[0] == "conv":
+            _, ci, co, s, p, st = e
+            if len(cur) != 3 or cur[0] != ci:
+                raise ValueError(f"conv expects {ci} channels, got {cur}")
+            nxt = (co, *conv_out_hw(cur[1], cur[2], s, p, st))
+        elif e[0] == "pool":
+            if len(cur) != 3 or cur[1] % 2 or cur[2] % 2:
+                raise ValueError("avgpool2 needs even spatial dims")
+            nxt = (cur[0], cur[1] // 2, cur[2] // 2)
+        elif e[0] == "flatten":
+            nxt = (int(np.prod(cur)),)
+        else:
+            raise ValueError(f"unknown layer {e!r}")
+        out.append((cur, nxt))
+        cur = nxt
+    return out
 
 
 class Model:
-    def __init__(self, sizes, ring: RingParams, seed: int = 0):
-        self.sizes = list(sizes)
+    """``Model(sizes)`` = FC stack (MLP); ``Model(name)`` / ``Model((in_shape, layers))`` = graph."""
+
+    def __init__(self, arch, ring: RingParams, seed: int = 0):
+        if isinstance(arch, str):
+            arch = MODELS[arch]
+        if isinstance(arch, (list, tuple)) and all(isinstance(v, (int, np.integer)) for v in arch):
+            arch = mlp_spec(list(arch))
+        self.in_shape, self.layers = tuple(arch[0]), list(arch[1])
+        self.io = shapes(self.in_shape, self.layers)
+        self.lin = [i for i, e in enumerate(self.layers) if e[0] in ("fc", "conv")]
         self.ring = ring
         self.w, self.b, self.vw, self.vb = [], [], [], []
-        for l, (ni, no) in enumerate(zip(sizes[:-1], sizes[1:])):
-            g = SeededRng(seed, 500 + l)
-            a = np.sqrt(1.0 / ni)
-            self.w.append(g.uniform_real((no, ni), -a, a))
-            self.b.append(g.uniform_real((no,), -a, a))
-            self.vw.append(np.zeros((no, ni)))
-            self.vb.append(np.zeros(no))
+        for l, i in enumerate(self.lin):
+            e = self.layers[i]
+            if e[0] == "fc":
+                wshape, fan_in, nb = (e[2], e[1]), e[1], e[2]
+            else:
+                wshape, fan_in, nb = (e[2], e[1], e[3], e[3]), e[1] * e[3] * e[3], e[2]
+            g = SeededRng(seed, 500 + l)  # SPEC:646 init
+            a = np.sqrt(1.0 / fan_in)
+            self.w.append(g.uniform_real(wshape, -a, a))
+            self.b.append(g.uniform_real((nb,), -a, a))
+            self.vw.append(np.zeros(wshape))
+            self.vb.append(np.zeros(nb))
+
+    @property
+    def sizes(self):  # MLP compatibility
+        return [self.layers[self.lin[0]][1]] + [self.layers[i][2] for i in self.lin]
 
     @property
     def n_layers(self):
-        return len(self.w)
+        return len(self.lin)
 
     def W(self, l):
         return encode_fixed(self.w[l], self.ring)
@@ -66,23 +139,66 @@ def _shift(v, bits, ring):
     return _m((to_signed(v, ring) >> np.int64(bits)).astype(np.uint64), ring)
 
 
+def _flatten(x):  # (B, C, H, W) -> (C*H*W, B)
+    return np.ascontiguousarray(x.reshape(x.shape[0], -1).T)
+
+
+def _unflatten(g, shape):  # (C*H*W, B) -> (B, C, H, W)
+    return np.ascontiguousarray(g.T).reshape(-1, *shape)
+
+
+def _segments(model):
+    """For each linear l: the entries between linear l and linear l+1."""
+    seg = []
+    for l, i in enumerate(model.lin):
+        j = model.lin[l + 1] if l + 1 < model.n_layers else len(model.layers)
+        seg.append(list(range(i + 1, j)))
+    return seg
+
+
 def reference_train_step(model: Model, x_enc, labels, lr=1e-2, momentum=0.8):
     """the exact Z_t fixed-point pipeline, no cryptography."""
     ring, f = model.ring, model.ring.f
-    acts, pre = [x_enc], []
-    for l in range(model.n_layers):
-        y = _m(OK.matmul_wrap(model.W(l), acts[-1]) + model.Bias(l)[:, None], ring)
+    L = model.n_layers
+    seg = _segments(model)
+    cur, acts, pre = x_enc, [], []
+    for l, i in enumerate(model.lin):
+        e = model.layers[i]
+        acts.append(cur)
+        if e[0] == "fc":
+            y = _m(OK.matmul_wrap(model.W(l), cur) + model.Bias(l)[:, None], ring)
+        else:
+            y = _m(CO.conv_fwd(cur, model.W(l), e[4], e[5]) + model.Bias(l)[None, :, None, None], ring)
         pre.append(y)
-        if l < model.n_layers - 1:
-            r = np.where(to_signed(y, ring) >= 0, y, np.uint64(0))
-            acts.append(_shift(r, f, ring))
+        if l < L - 1:
+            cur = _shift(np.where(to_signed(y, ring) >= 0, y, np.uint64(0)), f, ring)
+            for k in seg[l]:
+                if model.layers[k][0] == "pool":
+                    cur = _shift(_m(CO.pool_sum(cur), ring), 2, ring)
+                elif model.layers[k][0] == "flatten":
+                    cur = _flatten(cur)
     loss, gy = PR.softmax_ce_grad(pre[-1], labels, ring)
-    gws, gbs = [None] * model.n_layers, [None] * model.n_layers
-    for l in reversed(range(model.n_layers)):
-        gbs[l] = _m(gy.sum(axis=1, dtype=np.uint64), ring)
-        gws[l] = _shift(_m(OK.matmul_wrap(gy, np.ascontiguousarray(acts[l].T)), ring), f, ring)
+    gws, gbs = [None] * L, [None] * L
+    for l in reversed(range(L)):
+        e = model.layers[model.lin[l]]
+        if e[0] == "fc":
+            gbs[l] = _m(gy.sum(axis=1, dtype=np.uint64), ring)
+            gws[l] = _shift(_m(OK.matmul_wrap(gy, np.ascontiguousarray(acts[l].T)), ring), f, ring)
+        else:
+            gbs[l] = _m(gy.sum(axis=(0, 2, 3), dtype=np.uint64), ring)
+            gws[l] = _shift(_m(CO.conv_gradw(acts[l], gy, e[3], e[4], e[5]), ring), f, ring)
         if l > 0:
-            ga = _shift(_m(OK.matmul_wrap(np.ascontiguousarray(model.W(l).T), gy), ring), f, ring)
+            if e[0] == "fc":
+                ga = _m(OK.matmul_wrap(np.ascontiguousarray(model.W(l).T), gy), ring)
+            else:
+                H, Wd = acts[l].shape[2:]
+                ga = _m(CO.conv_bwdx(gy, model.W(l), H, Wd, e[4], e[5]), ring)
+            ga = _shift(ga, f, ring)
+            for k in reversed(seg[l - 1]):
+                if model.layers[k][0] == "pool":
+                    ga = _shift(_m(CO.pool_replicate(ga), ring), 2, ring)
+                elif model.layers[k][0] == "flatten":
+                    ga = _unflatten(ga, model.io[k][0])
             gy = np.where(to_signed(pre[l - 1], ring) >= 0, ga, np.uint64(0))
     model.sgd(gws, gbs, lr, momentum)
     return loss, gws, gbs
@@ -93,34 +209,56 @@ def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, moment
     dealer non-linear backend; <X_0>_0 = 0 at MO, <X_0>_1 = X at DO."""
     ring, f = model.ring, model.ring.f
     L = model.n_layers
-    x_mo = np.zeros_like(x_enc)
-    x_do = x_enc.copy()
-    acts = [(x_mo, x_do)]
-    ds = []
-    ys = []
-    for l in range(L):
-        W = model.W(l)
-        y_mo, y_do = PR.linear_forward(ctx, l, W, model.Bias(l), *acts[-1], mo_x_zero=(l == 0))
-        ys.append((y_mo, y_do))
+    seg = _segments(model)
+    cur = (np.zeros_like(x_enc), x_enc.copy())
+    acts, ds, ys = [], [], []
+    for l, i in enumerate(model.lin):
+        e = model.layers[i]
+        acts.append(cur)
+        if e[0] == "fc":
+            y = PR.linear_forward(ctx, l, model.W(l), model.Bias(l), *cur, mo_x_zero=(l == 0))
+        else:
+            y = PR.conv_forward(ctx, l, model.W(l), model.Bias(l), *cur, e[4], e[5], mo_x_zero=(l == 0))
+        ys.append(y)
         if l < L - 1:
-            z_mo, z_do, d = PR.dealer_op(ctx, l, PR.OP_RELU, y_mo, y_do)
+            z_mo, z_do, d = PR.dealer_op(ctx, l, PR.OP_RELU, *y)
             a_mo, a_do, _ = PR.dealer_op(ctx, l, PR.OP_TRUNC_F, z_mo, z_do, k=f)
             ds.append(d)
-            acts.append((a_mo, a_do))
+            cur = (a_mo, a_do)
+            for k in seg[l]:
+                if model.layers[k][0] == "pool":
+                    cur = PR.avgpool_forward(ctx, l, *cur)
+                elif model.layers[k][0] == "flatten":
+                    cur = (_flatten(cur[0]), _flatten(cur[1]))
     logits = _m(ys[-1][0] + ys[-1][1], ring)  # MO sends its share; DO reconstructs
     loss, g = PR.softmax_ce_grad(logits, labels, ring)
     gy_mo, gy_do = np.zeros_like(g), g
     gws, gbs = [None] * L, [None] * L
     for l in reversed(range(L)):
+        e = model.layers[model.lin[l]]
         last = l == L - 1
-        gbs[l] = PR.reveal_grad_bias(ctx, l, gy_mo, gy_do)
-        gw2f = PR.grad_weight(ctx, l, *acts[l], gy_mo, gy_do, mo_x_zero=(l == 0), mo_gy_zero=last)
+        if e[0] == "fc":
+            gbs[l] = PR.reveal_grad_bias(ctx, l, gy_mo, gy_do)
+            gw2f = PR.grad_weight(ctx, l, *acts[l], gy_mo, gy_do, mo_x_zero=(l == 0), mo_gy_zero=last)
+        else:
+            gbs[l] = PR.reveal_grad_bias_conv(ctx, l, gy_mo, gy_do)
+            gw2f = PR.conv_grad_weight(ctx, l, *acts[l], gy_mo, gy_do, e[3], e[4], e[5], mo_x_zero=(l == 0),
+                                       mo_gy_zero=last)
         gws[l] = _shift(gw2f, f, ring)  # MO: plaintext shift (SPEC:366)
         if trace is not None:
             trace.append((l, ys[l], gbs[l], gws[l]))
         if l > 0:
-            ga_mo, ga_do = PR.linear_backward_input(ctx, l, model.W(l), gy_mo, gy_do, mo_gy_zero=last)
-            t_mo, t_do, _ = PR.dealer_op(ctx, l, PR.OP_TRUNC_B, ga_mo, ga_do, k=f)
+            if e[0] == "fc":
+                ga = PR.linear_backward_input(ctx, l, model.W(l), gy_mo, gy_do, mo_gy_zero=last)
+            else:
+                H, Wd = acts[l][1].shape[2:]
+                ga = PR.conv_backward_input(ctx, l, model.W(l), gy_mo, gy_do, H, Wd, e[4], e[5], mo_gy_zero=last)
+            t_mo, t_do, _ = PR.dealer_op(ctx, l, PR.OP_TRUNC_B, *ga, k=f)
+            for k in reversed(seg[l - 1]):
+                if model.layers[k][0] == "pool":
+                    t_mo, t_do = PR.avgpool_backward(ctx, l - 1, t_mo, t_do)
+                elif model.layers[k][0] == "flatten":
+                    t_mo, t_do = _unflatten(t_mo, model.io[k][0]), _unflatten(t_do, model.io[k][0])
             gy_mo, gy_do, _ = PR.dealer_op(ctx, l - 1, PR.OP_RELU_B, t_mo, t_do, d=ds[l - 1])
     model.sgd(gws, gbs, lr, momentum)
     return loss, gws, gbs
@@ -131,5 +269,18 @@ def synthetic_mnist(seed: int, B: int, ring: RingParams):
     g = SeededRng(seed, 900)
     x = g.uniform_real((784, B), 0.0, 1.0)
     x = (x - 0.1307) / 0.3081
+    labels = g._gen.integers(0, 10, size=B)
+    return encode_fixed(x, ring), labels
+
+
+def synthetic_images(seed: int, B: int, in_shape, ring: RingParams):
+    """Image-shaped batch (B, C, H, W) for the CNNs: MNIST shapes reuse
+    synthetic_mnist's pixels; CIFAR shapes draw U[0,1] per channel,
+    standardised with (0.5, 0.25)."""
+    if tuple(in_shape) == (1, 28, 28):
+        x, labels = synthetic_mnist(seed, B, ring)
+        return np.ascontiguousarray(x.T).reshape(B, 1, 28, 28), labels
+    g = SeededRng(seed, 901)
+    x = (g.uniform_real((B, *in_shape), 0.0, 1.0) - 0.5) / 0.25
     labels = g._gen.integers(0, 10, size=B)
     return encode_fixed(x, ring), labels

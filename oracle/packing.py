@@ -260,3 +260,99 @@ def unpack(polys, plan: BlockPlan, out_size: int):
     rows = np.nonzero(ok)[0]
     out[plan.out_dst[ok]] = polys[rows, plan.out_pos[ok]]
     return out
+
+
+# ------------------------------------------- conv layers (pad / stride) ---
+#
+# SPEC:284 keeps the codec at valid-mode stride-1 cross-correlation and puts
+# padding / stride "outside the codec"; SPEC:286 lowers the backward
+# operators by local share reshaping.  Here every such reshaping (zero
+# padding, stride subsampling, zero-stuffing dilation, kernel flip,
+# channel/batch transposition) is a data-movement-only linear map, folded
+# into the plan's index maps: a logical-geometry plan is built with the
+# verified codec and its source / destination indices are re-pointed into
+# the physical tensors (-1 = structural zero / dropped output).  The three
+# layer operators (forward, input gradient, weight gradient) all use the
+# paper's native conv packing.
+
+def remap(plan: BlockPlan, in_map, pt_map, out_map) -> BlockPlan:
+    def re(src, m):
+        out = np.full(src.shape, -1, dtype=np.int64)
+        ok = src >= 0
+        out[ok] = m[src[ok]]
+        return out
+
+    dst = re(plan.out_dst, out_map)
+    pos = np.where(dst >= 0, plan.out_pos, -1)
+    return BlockPlan(plan.kind, plan.geometry, plan.N, plan.blk, plan.nblk, re(plan.in_src, in_map),
+                     re(plan.pt_src, pt_map), pos, dst, plan.terms)
+
+
+def conv_out_hw(H, W, s, pad, stride):
+    return (H + 2 * pad - s) // stride + 1, (W + 2 * pad - s) // stride + 1
+
+
+def conv_index_maps(kind: str, B, c_i, c_o, H, W, s, pad, stride):
+    """(logical ConvGeometry, in_map, pt_map, out_map) of one conv-layer operator.
+
+    fwd   Y[b,o,y,x]   = sum W[o,c,i,j] Xpad[b,c,y*st+i,x*st+j]      v=X,  W=W,  y=Y
+    bwdx  dX[b,c,y,x]  = sum W[o,c,i,j] dY[b,o,(y+p-i)/st,(x+p-j)/st]  v=dY, W=W,  y=dX
+    gradw dW[o,c,i,j]  = sum dY[b,o,y,x] Xpad[b,c,y*st+i,x*st+j]       v=X,  W=dY, y=dW
+    """
+    oh, ow = conv_out_hw(H, W, s, pad, stride)
+    hp, wp = H + 2 * pad, W + 2 * pad
+
+    def pad_map(C, Bn, transpose=False):  # logical (Bn, C, hp, wp) of Xpad -> X (B, c_i, H, W) index
+        b, c, y, x = np.meshgrid(np.arange(Bn), np.arange(C), np.arange(hp), np.arange(wp), indexing="ij")
+        yy, xx = y - pad, x - pad
+        ok = (yy >= 0) & (yy < H) & (xx >= 0) & (xx < W)
+        bb, cc = (c, b) if transpose else (b, c)  # transpose: logical batch = channel
+        src = ((bb * c_i + cc) * H + yy) * W + xx
+        return np.where(ok, src, -1).ravel()
+
+    if kind == "fwd":
+        g = ConvGeometry(B, c_i, c_o, hp, wp, s)
+        in_map = pad_map(c_i, B)
+        pt_map = np.arange(c_o * c_i * s * s)
+        b, o, y, x = np.meshgrid(np.arange(B), np.arange(c_o), np.arange(hp - s + 1), np.arange(wp - s + 1),
+                                 indexing="ij")
+        ok = (y % stride == 0) & (x % stride == 0) & (y // stride < oh) & (x // stride < ow)
+        out_map = np.where(ok, ((b * c_o + o) * oh + y // stride) * ow + x // stride, -1).ravel()
+        return g, in_map, pt_map, out_map
+    if kind == "bwdx":
+        hd, wd = (oh - 1) * stride + 1 + 2 * (s - 1), (ow - 1) * stride + 1 + 2 * (s - 1)
+        if hd - s + 1 < H + pad or wd - s + 1 < W + pad:
+            raise GeometryError("conv stride/padding leave input rows without gradient coverage")
+        g = ConvGeometry(B, c_o, c_i, hd, wd, s)
+        b, o, y, x = np.meshgrid(np.arange(B), np.arange(c_o), np.arange(hd), np.arange(wd), indexing="ij")
+        u, v = y - (s - 1), x - (s - 1)
+        ok = (u >= 0) & (v >= 0) & (u % stride == 0) & (v % stride == 0) & (u // stride < oh) & (v // stride < ow)
+        in_map = np.where(ok, ((b * c_o + o) * oh + u // stride) * ow + v // stride, -1).ravel()
+        c, o2, i, j = np.meshgrid(np.arange(c_i), np.arange(c_o), np.arange(s), np.arange(s), indexing="ij")
+        pt_map = (((o2 * c_i + c) * s + (s - 1 - i)) * s + (s - 1 - j)).ravel()  # logical K[c,o,i,j]
+        b, c, y, x = np.meshgrid(np.arange(B), np.arange(c_i), np.arange(hd - s + 1), np.arange(wd - s + 1),
+                                 indexing="ij")
+        yy, xx = y - pad, x - pad
+        ok = (yy >= 0) & (yy < H) & (xx >= 0) & (xx < W)
+        out_map = np.where(ok, ((b * c_i + c) * H + yy) * W + xx, -1).ravel()
+        return g, in_map, pt_map, out_map
+    if kind == "gradw":
+        sd_h, sd_w = (oh - 1) * stride + 1, (ow - 1) * stride + 1
+        if sd_h != sd_w:
+            raise GeometryError("gradw lowering needs a square output")
+        g = ConvGeometry(c_i, B, c_o, hp, wp, sd_h)
+        in_map = pad_map(B, c_i, transpose=True)
+        o, b, i, j = np.meshgrid(np.arange(c_o), np.arange(B), np.arange(sd_h), np.arange(sd_w), indexing="ij")
+        ok = (i % stride == 0) & (j % stride == 0)
+        pt_map = np.where(ok, ((b * c_o + o) * oh + i // stride) * ow + j // stride, -1).ravel()
+        c, o, y, x = np.meshgrid(np.arange(c_i), np.arange(c_o), np.arange(hp - sd_h + 1), np.arange(wp - sd_w + 1),
+                                 indexing="ij")
+        ok = (y < s) & (x < s)
+        out_map = np.where(ok, ((o * c_i + c) * s + y) * s + x, -1).ravel()
+        return g, in_map, pt_map, out_map
+    raise GeometryError(f"unknown conv operator {kind!r}")
+
+
+def plan_conv_layer(kind: str, B, c_i, c_o, H, W, s, pad, stride, N) -> BlockPlan:
+    g, in_map, pt_map, out_map = conv_index_maps(kind, B, c_i, c_o, H, W, s, pad, stride)
+    return remap(_plan_conv(g, N), in_map, pt_map, out_map)

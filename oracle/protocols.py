@@ -28,11 +28,12 @@ from __future__ import annotations
 import numpy as np
 
 from . import bfv as OB
+from . import convops as CO
 from . import kernels as OK
 from . import packing as PK
 from .ring import DO, MO, RingParams, SeededRng, to_signed
 
-OP_FWD, OP_BWD_X, OP_GRAD_W, OP_GRAD_B, OP_RELU, OP_TRUNC_F, OP_TRUNC_B, OP_RELU_B = range(8)
+OP_FWD, OP_BWD_X, OP_GRAD_W, OP_GRAD_B, OP_RELU, OP_TRUNC_F, OP_TRUNC_B, OP_RELU_B, OP_POOL_F, OP_POOL_B = range(10)
 P_MASK, P_ENC, P_DEALER, P_DP = range(4)
 
 
@@ -63,8 +64,15 @@ def he_matmul(ctx: Ctx, v_ct_vals, v_pt_vals, W_pt_vals, W_ct_vals, g: PK.Matmul
     sum over present terms of  Enc(pi_v(v_ct)) (x) pi_W(W_pt)  and
     Enc(pi_W(W_ct)) (x) pi_v(v_pt), minus Delta*pi_y(s_eff); returns the DO's
     decrypted share (n_o, B).  Any *_vals may be None (term absent)."""
+    plan = PK.plan_blocks(g, ctx.p.N)
+    return he_eval(ctx, plan, v_ct_vals, v_pt_vals, W_pt_vals, W_ct_vals, s_eff, g.n_o * g.B,
+                   enc_rng).reshape(g.n_o, g.B)
+
+
+def he_eval(ctx: Ctx, plan, v_ct_vals, v_pt_vals, W_pt_vals, W_ct_vals, s_eff, out_size, enc_rng):
+    """he_matmul over an arbitrary block plan (matmul or conv-layer packing):
+    returns the DO's decrypted flat share of size ``out_size``."""
     p, ar = ctx.p, ctx.ar
-    plan = PK.plan_blocks(g, p.N)
     outs = np.zeros((plan.n_out, 2, p.L, p.N), dtype=np.uint64)
 
     def mac(cts, pts, ct_col, pt_col):  # outs[r] += sum_k cts[terms[r,k,ct_col]] (x) pts[terms[r,k,pt_col]]
@@ -92,7 +100,7 @@ def he_matmul(ctx: Ctx, v_ct_vals, v_pt_vals, W_pt_vals, W_ct_vals, g: PK.Matmul
     outs = OB.he_add_plain(p, outs, mpoly, ar, subtract=True)
     # DO decrypts and gathers pi_y^-1
     dec = OB.decrypt(p, ctx.kp, outs, ar)
-    return PK.unpack(dec, plan, g.n_o * g.B).reshape(g.n_o, g.B)
+    return PK.unpack(dec, plan, out_size)
 
 
 def linear_forward(ctx: Ctx, layer: int, W, b, x_mo, x_do, mo_x_zero=False):  # Alg.1
@@ -151,6 +159,83 @@ def grad_weight(ctx: Ctx, layer: int, x_mo, x_do, gy_mo, gy_do, e=None, mo_x_zer
     return _mask(msg + s + OK.matmul_wrap(gy_mo, xmT), ring)  # MO: + s + local term
 
 
+# ------------------------------------------------------- conv layers ---
+# Conv2d layers (SPEC:249-266 packing, SPEC:284-286 transforms): activations
+# (B, C, H, W), weights (c_o, c_i, s, s) at f, bias (c_o,) at 2f.  Every
+# operator uses the native conv packing with padding / stride / flips folded
+# into the plan's index maps (packing.plan_conv_layer); the MO's local terms
+# use the matching plaintext operators (convops).
+
+
+def conv_forward(ctx: Ctx, layer: int, W, b, x_mo, x_do, pad: int, stride: int, mo_x_zero=False):
+    """Alg.1 with conv packing: shares of Y = conv(X; W) + b at 2f, (B, c_o, oh, ow)."""
+    ring = ctx.ring
+    B, c_i, H, Wd = x_do.shape
+    c_o, _, s, _ = W.shape
+    oh, ow = PK.conv_out_hw(H, Wd, s, pad, stride)
+    msk = ctx.rng(layer, OP_FWD, P_MASK).uniform_ring((B, c_o, oh, ow), ring)
+    s_eff = msk if mo_x_zero else _mask(msk - CO.conv_fwd(x_mo, W, pad, stride), ring)
+    plan = PK.plan_conv_layer("fwd", B, c_i, c_o, H, Wd, s, pad, stride, ctx.p.N)
+    y_do = he_eval(ctx, plan, x_do, None, W, None, s_eff, B * c_o * oh * ow,
+                   ctx.rng(layer, OP_FWD, P_ENC)).reshape(B, c_o, oh, ow)
+    y_mo = _mask(msk + b[None, :, None, None], ring)
+    return y_mo, y_do
+
+
+def conv_backward_input(ctx: Ctx, layer: int, W, gy_mo, gy_do, H: int, Wd: int, pad: int, stride: int,
+                        mo_gy_zero=False):
+    """SPEC:321-329 for Conv2d: shares of dX = conv_fwd^T(dY) at 2f, (B, c_i, H, W)."""
+    ring = ctx.ring
+    B, c_o = gy_do.shape[:2]
+    c_i, s = W.shape[1], W.shape[2]
+    msk = ctx.rng(layer, OP_BWD_X, P_MASK).uniform_ring((B, c_i, H, Wd), ring)
+    s_eff = msk if mo_gy_zero else _mask(msk - CO.conv_bwdx(gy_mo, W, H, Wd, pad, stride), ring)
+    plan = PK.plan_conv_layer("bwdx", B, c_i, c_o, H, Wd, s, pad, stride, ctx.p.N)
+    g_do = he_eval(ctx, plan, gy_do, None, W, None, s_eff, B * c_i * H * Wd,
+                   ctx.rng(layer, OP_BWD_X, P_ENC)).reshape(B, c_i, H, Wd)
+    return msk, g_do
+
+
+def conv_grad_weight(ctx: Ctx, layer: int, x_mo, x_do, gy_mo, gy_do, s: int, pad: int, stride: int, e=None,
+                     mo_x_zero=False, mo_gy_zero=False):
+    """Alg.2 for Conv2d: dW = sum_b,y,x dY Xpad revealed at MO, scale 2f, (c_o, c_i, s, s)."""
+    ring = ctx.ring
+    B, c_i, H, Wd = x_do.shape
+    c_o = gy_do.shape[1]
+    msk = ctx.rng(layer, OP_GRAD_W, P_MASK).uniform_ring((c_o, c_i, s, s), ring)
+    plan = PK.plan_conv_layer("gradw", B, c_i, c_o, H, Wd, s, pad, stride, ctx.p.N)
+    cross_do = he_eval(ctx, plan,
+                       None if mo_gy_zero else x_do, None if mo_x_zero else x_mo,
+                       None if mo_gy_zero else gy_mo, None if mo_x_zero else gy_do,
+                       msk, c_o * c_i * s * s, ctx.rng(layer, OP_GRAD_W, P_ENC)).reshape(c_o, c_i, s, s)
+    msg = _mask(cross_do + CO.conv_gradw(x_do, gy_do, s, pad, stride), ring)  # DO: + local term
+    if e is not None:
+        msg = _mask(msg + e, ring)
+    return _mask(msg + msk + CO.conv_gradw(x_mo, gy_mo, s, pad, stride), ring)  # MO: + s + local term
+
+
+def reveal_grad_bias_conv(ctx: Ctx, layer: int, gy_mo, gy_do, e=None):
+    """SPEC:330-338 for Conv2d: local sums over batch and spatial positions per channel."""
+    ring = ctx.ring
+    do_sum = _mask(gy_do.sum(axis=(0, 2, 3), dtype=np.uint64), ring)
+    if e is not None:
+        do_sum = _mask(do_sum + e, ring)
+    return _mask(gy_mo.sum(axis=(0, 2, 3), dtype=np.uint64) + do_sum, ring)
+
+
+def avgpool_forward(ctx: Ctx, layer: int, a_mo, a_do):
+    """local 2x2 window sums, then a 2-bit truncation (dealer)."""
+    s_mo, s_do = CO.pool_sum(a_mo), CO.pool_sum(a_do)
+    r, y, _ = dealer_op(ctx, layer, OP_POOL_F, s_mo, s_do, k=2)
+    return r, y
+
+
+def avgpool_backward(ctx: Ctx, layer: int, g_mo, g_do):
+    """Replicate each gradient to its 2x2 window, then a 2-bit truncation (dealer)."""
+    r, y, _ = dealer_op(ctx, layer, OP_POOL_B, CO.pool_replicate(g_mo), CO.pool_replicate(g_do), k=2)
+    return r, y
+
+
 # ----------------------------------------------------- dealer non-linear ---
 
 def dealer_op(ctx: Ctx, layer: int, op: int, y_mo, y_do, k: int = 0, d=None):
@@ -162,7 +247,7 @@ def dealer_op(ctx: Ctx, layer: int, op: int, y_mo, y_do, k: int = 0, d=None):
     if op == OP_RELU:
         d_out = (sx >= 0).astype(np.uint8)
         y = np.where(sx >= 0, x, np.uint64(0))
-    elif op in (OP_TRUNC_F, OP_TRUNC_B):
+    elif op in (OP_TRUNC_F, OP_TRUNC_B, OP_POOL_F, OP_POOL_B):
         y = _mask((sx >> np.int64(k)).astype(np.uint64), ring)
     elif op == OP_RELU_B:
         y = np.where(d.astype(bool), x, np.uint64(0))
