@@ -251,6 +251,23 @@ int pb_col2im(const uint64_t* cols, int32_t B, int32_t C, int32_t H, int32_t W, 
 int pb_conv2d(const uint64_t* x, const uint64_t* w, int32_t B, int32_t Ci, int32_t H, int32_t W,
               int32_t Co, int32_t s, int32_t ell, uint64_t* out, void* stream);
 
+/* Conv-layer operators with padding / stride, computed directly (no padded
+ * or dilated copies): the parties' local terms of the conv protocols.  They
+ * equal the oracle's compositions of K:260-278 conv2d_wrap with the SPEC:284
+ * pad / stride transforms (oracle/convops.py), mod 2^ell:
+ *   PB_CONV_FWD   a = X  (B,c_i,H,W),   b = W (c_o,c_i,s,s), out = Y  (B,c_o,oh,ow)
+ *   PB_CONV_BWDX  a = dY (B,c_o,oh,ow), b = W,               out = dX (B,c_i,H,W)
+ *   PB_CONV_GRADW a = X,                b = dY,              out = dW (c_o,c_i,s,s)
+ * with oh = (H + 2 pad - s) / stride + 1 (same for ow). */
+enum { PB_CONV_FWD = 0, PB_CONV_BWDX = 1, PB_CONV_GRADW = 2 };
+int pb_ring_conv(int kind, const uint64_t* a, const uint64_t* b, int32_t B, int32_t c_i, int32_t c_o, int32_t H,
+                 int32_t W, int32_t s, int32_t pad, int32_t stride, int32_t ell, uint64_t* out, void* stream);
+/* AvgPool2 local steps: PB_POOL_SUM in (bc,H,W) -> out (bc,H/2,W/2)
+ * 2x2 window sums; PB_POOL_REPLICATE in (bc,H/2,W/2) -> out (bc,H,W). */
+enum { PB_POOL_SUM = 0, PB_POOL_REPLICATE = 1 };
+int pb_pool2(int op, const uint64_t* in, int64_t bc, int32_t H, int32_t W, int32_t ell, uint64_t* out,
+             void* stream);
+
 /* ------------------------------- dealer-assisted non-linear --- */
 /* The SPEC's dealer OT backend ("fast, insecure, default for benchmarks of
  * non-OT costs"): reconstruct x = mo + do, apply f, reshare with

@@ -321,8 +321,6 @@ def conv_index_maps(kind: str, B, c_i, c_o, H, W, s, pad, stride):
         return g, in_map, pt_map, out_map
     if kind == "bwdx":
         hd, wd = (oh - 1) * stride + 1 + 2 * (s - 1), (ow - 1) * stride + 1 + 2 * (s - 1)
-        if hd - s + 1 < H + pad or wd - s + 1 < W + pad:
-            raise GeometryError("conv stride/padding leave input rows without gradient coverage")
         g = ConvGeometry(B, c_o, c_i, hd, wd, s)
         b, o, y, x = np.meshgrid(np.arange(B), np.arange(c_o), np.arange(hd), np.arange(wd), indexing="ij")
         u, v = y - (s - 1), x - (s - 1)

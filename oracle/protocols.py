@@ -189,8 +189,13 @@ def conv_backward_input(ctx: Ctx, layer: int, W, gy_mo, gy_do, H: int, Wd: int, 
     B, c_o = gy_do.shape[:2]
     c_i, s = W.shape[1], W.shape[2]
     msk = ctx.rng(layer, OP_BWD_X, P_MASK).uniform_ring((B, c_i, H, Wd), ring)
-    s_eff = msk if mo_gy_zero else _mask(msk - CO.conv_bwdx(gy_mo, W, H, Wd, pad, stride), ring)
     plan = PK.plan_conv_layer("bwdx", B, c_i, c_o, H, Wd, s, pad, stride, ctx.p.N)
+    # input positions no output reads (stride > 1 tails) have gradient exactly 0:
+    # no ciphertext slot carries them, so the MO's share there is 0 as well
+    covered = np.zeros(B * c_i * H * Wd, dtype=bool)
+    covered[plan.out_dst[plan.out_dst >= 0]] = True
+    msk = np.where(covered.reshape(msk.shape), msk, np.uint64(0))
+    s_eff = msk if mo_gy_zero else _mask(msk - CO.conv_bwdx(gy_mo, W, H, Wd, pad, stride), ring)
     g_do = he_eval(ctx, plan, gy_do, None, W, None, s_eff, B * c_i * H * Wd,
                    ctx.rng(layer, OP_BWD_X, P_ENC)).reshape(B, c_i, H, Wd)
     return msk, g_do

@@ -80,6 +80,8 @@ SIGNATURES = {
     "pb_im2col": [P, I32, I32, I32, I32, I32, I32, P, P],
     "pb_col2im": [P, I32, I32, I32, I32, I32, I32, P, P],
     "pb_conv2d": [P, P, I32, I32, I32, I32, I32, I32, I32, P, P],
+    "pb_ring_conv": [INT, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P],
+    "pb_pool2": [INT, P, I64, I32, I32, I32, P, P],
     "pb_dealer_op": [INT, P, P, I64, I32, P, P, U64, P, U64, U64, I32, P],
     "pb_sgd_momentum": [P, P, P, I64, I32, F64, F64, I32, I32, P, P, P],
 }
@@ -89,6 +91,8 @@ _RET = {"pb_last_error": ctypes.c_char_p}
 PW_MUL, PW_MAC, PW_ADD, PW_SUB = 0, 1, 2, 3
 RING_ADD, RING_SUB, RING_MUL, RING_NEG, RING_SCALAR_MUL, RING_MASK, RING_ARITH_SHIFT = range(7)
 DEALER_RELU, DEALER_TRUNC, DEALER_SELECT, DEALER_RESHARE = range(4)
+CONV_FWD, CONV_BWDX, CONV_GRADW = range(3)
+POOL_SUM, POOL_REPLICATE = range(2)
 
 _lib = None
 

@@ -35,10 +35,10 @@ from . import _dev, _lib
 from .bfv import Ciphertext, KeyPair
 from .errors import DesyncError, ScaleError, ShapeError
 from .params import BfvParams, context
-from .poly_encoding import MatmulGeometry, plan_matmul
+from .poly_encoding import MatmulGeometry, conv_out_hw, plan_conv_layer, plan_matmul
 from .ring import DO, MO, RingParams, RingTensor, SeededRng, ShareTensor
 
-OP_FWD, OP_BWD_X, OP_GRAD_W, OP_GRAD_B, OP_RELU, OP_TRUNC_F, OP_TRUNC_B, OP_RELU_B = range(8)
+OP_FWD, OP_BWD_X, OP_GRAD_W, OP_GRAD_B, OP_RELU, OP_TRUNC_F, OP_TRUNC_B, OP_RELU_B, OP_POOL_F, OP_POOL_B = range(10)
 P_MASK, P_ENC, P_DEALER, P_DP = range(4)
 
 # SPEC:372 message codes
@@ -204,8 +204,15 @@ class Session:
         """DO-decrypted share of  [Enc(pi_v(v_ct)) (x) pi_W(w_pt)] + [Enc(pi_W(w_ct)) (x) pi_v(v_pt)] - mask,
         written into ``out`` (flat, addressed through y_strides).  Operands are flat
         device tensors addressed through the given strides; absent terms are None."""
+        plan = plan_matmul(g, self.p.N, v_strides, w_strides, y_strides)
+        return self.he_eval(layer, op, plan, out, mask, v_ct=v_ct, w_pt=w_pt, w_ct=w_ct, v_pt=v_pt,
+                            msg_in=msg_in, msg_out=msg_out)
+
+    def he_eval(self, layer: int, op: int, plan, out: torch.Tensor, mask: torch.Tensor, v_ct=None, w_pt=None,
+                w_ct=None, v_pt=None, msg_in=MSG_FWD_INPUT_CT, msg_out=MSG_FWD_MASKED_CT):
+        """he_matmul over any block plan (matmul or conv-layer packing); the
+        plan's maps address the flat operand / output tensors directly."""
         p, h, st = self.p, self.ctx.handle, _dev.stream()
-        plan = plan_matmul(g, p.N, v_strides, w_strides, y_strides)
         sh = self._shard(plan)
         N, L = p.N, p.L
         w = 4  # bytes per residue
@@ -213,8 +220,8 @@ class Session:
         enc_rng = self.rng(layer, op, P_ENC)
         base = enc_rng.reserve((plan.n_in + plan.n_pt) * self.world)
         ctA = ptA = ctB = ptB = None
-        if self.world > 1:
-            out.zero_()
+        if self.world > 1 or plan.kind == "conv":
+            out.zero_()  # conv plans may leave structural-zero outputs without a slot
         # Buffers are allocated on the main stream; the DO's encryptions and the
         # MO's plaintext encodings run on two side streams concurrently with the
         # MO's mask NTT, and the MAC joins all three (the graph keeps the fork).
@@ -407,6 +414,139 @@ def grad_weight(sess: Session, layer: int, x_a: ShareTensor, x_b: ShareTensor, g
         out = _ring_bin(_lib.RING_ADD, out,
                         _ring_matmul(gy_mo.value.values, x_mo.value.values, n_o, B, n_i, ring.ell, tb=True), ring.ell)
     return RingTensor(out, 2 * ring.f, ring, _canonical=True)
+
+
+# ------------------------------------------------------- conv layers ---
+# Conv2d layers (SPEC:249-266 packing; SPEC:284-286 transforms): activations
+# (B, C, H, W), W (c_o, c_i, s, s) at f, bias (c_o,) at 2f.  The three
+# operators run on the native conv packing with padding / stride / flips
+# folded into the plan maps (poly_encoding.plan_conv_layer), through the same
+# fused kernels as the FC protocols; local terms use pb_ring_conv.
+
+def _ring_conv(kind: int, a: torch.Tensor, b: torch.Tensor, B, c_i, c_o, H, W, s, pad, stride, ell, out_shape):
+    out = _dev.empty_u64(*out_shape)
+    _lib.call("pb_ring_conv", kind, _dev.ptr(a), _dev.ptr(b), B, c_i, c_o, H, W, s, pad, stride, ell, _dev.ptr(out),
+              _dev.stream())
+    return out
+
+
+_UNCOVERED = {}
+
+
+def _covered(plan, n: int):
+    """0/1 device mask of the output elements some ciphertext slot carries, or
+    None when all are (the rest are structural zeros of a strided input gradient)."""
+    key = id(plan)
+    if key not in _UNCOVERED:
+        cov = np.zeros(n, dtype=bool)
+        cov[plan.out_dst[plan.out_dst >= 0]] = True
+        _UNCOVERED[key] = (plan, None if cov.all() else _dev.u64_to_device(cov.astype(np.uint64)))
+    return _UNCOVERED[key][1]
+
+
+def conv_forward(sess: Session, layer: int, W: RingTensor, b: RingTensor, x_a: ShareTensor, x_b: ShareTensor,
+                 pad: int, stride: int, mo_x_zero: bool = False):
+    """Alg.1 with conv packing: shares of Y = conv(X; W) + b at 2f, (B, c_o, oh, ow)."""
+    x_mo, x_do = _split(x_a, x_b)
+    ring = sess.ring
+    if x_mo.scale != ring.f or W.scale != ring.f or b.scale != 2 * ring.f:
+        raise ScaleError("conv_forward needs X, W at f and b at 2f")
+    B, c_i, H, Wd = x_do.shape
+    c_o, ci2, s, _ = W.shape
+    if ci2 != c_i:
+        raise ShapeError(f"X has {c_i} channels, W expects {ci2}")
+    oh, ow = conv_out_hw(H, Wd, s, pad, stride)
+    msk = sess.rng(layer, OP_FWD, P_MASK).uniform_ring((B, c_o, oh, ow), ring)
+    if mo_x_zero:
+        s_eff = msk
+    else:
+        loc = _ring_conv(_lib.CONV_FWD, x_mo.value.values, W.values, B, c_i, c_o, H, Wd, s, pad, stride, ring.ell,
+                         (B, c_o, oh, ow))
+        s_eff = _ring_bin(_lib.RING_SUB, msk, loc, ring.ell)
+    plan = plan_conv_layer("fwd", B, c_i, c_o, H, Wd, s, pad, stride, sess.p.N)
+    y_do = _dev.empty_u64(B, c_o, oh, ow)
+    sess.he_eval(layer, OP_FWD, plan, y_do, s_eff, v_ct=x_do.value.values, w_pt=W.values)
+    bb = b.values.reshape(1, c_o, 1, 1).expand(B, c_o, oh, ow).contiguous()
+    y_mo = _ring_bin(_lib.RING_ADD, msk, bb, ring.ell)
+    return (ShareTensor(MO, RingTensor(y_mo, 2 * ring.f, ring, _canonical=True)),
+            ShareTensor(DO, RingTensor(y_do, 2 * ring.f, ring, _canonical=True)))
+
+
+def conv_backward_input(sess: Session, layer: int, W: RingTensor, gy_a: ShareTensor, gy_b: ShareTensor, H: int,
+                        Wd: int, pad: int, stride: int, mo_gy_zero: bool = False):
+    """SPEC:321-329 for Conv2d: shares of dX = conv^T(dY) at 2f, (B, c_i, H, W)."""
+    gy_mo, gy_do = _split(gy_a, gy_b)
+    ring = sess.ring
+    B, c_o = gy_do.shape[:2]
+    c_i, s = W.shape[1], W.shape[2]
+    msk = sess.rng(layer, OP_BWD_X, P_MASK).uniform_ring((B, c_i, H, Wd), ring)
+    plan = plan_conv_layer("bwdx", B, c_i, c_o, H, Wd, s, pad, stride, sess.p.N)
+    cov = _covered(plan, B * c_i * H * Wd)
+    if cov is not None:  # input positions no output reads: gradient exactly 0, MO share 0 too
+        msk = _ring_bin(_lib.RING_MUL, msk, cov.reshape(msk.shape), ring.ell)
+    if mo_gy_zero:
+        s_eff = msk
+    else:
+        loc = _ring_conv(_lib.CONV_BWDX, gy_mo.value.values, W.values, B, c_i, c_o, H, Wd, s, pad, stride, ring.ell,
+                         (B, c_i, H, Wd))
+        s_eff = _ring_bin(_lib.RING_SUB, msk, loc, ring.ell)
+    g_do = _dev.empty_u64(B, c_i, H, Wd)
+    sess.he_eval(layer, OP_BWD_X, plan, g_do, s_eff, v_ct=gy_do.value.values, w_pt=W.values, msg_in=MSG_BWD_X,
+                 msg_out=MSG_BWD_X + 1)
+    return (ShareTensor(MO, RingTensor(msk, 2 * ring.f, ring, _canonical=True)),
+            ShareTensor(DO, RingTensor(g_do, 2 * ring.f, ring, _canonical=True)))
+
+
+def conv_grad_weight(sess: Session, layer: int, x_a: ShareTensor, x_b: ShareTensor, gy_a: ShareTensor,
+                     gy_b: ShareTensor, s: int, pad: int, stride: int, e: torch.Tensor | None = None,
+                     mo_x_zero: bool = False, mo_gy_zero: bool = False) -> RingTensor:
+    """Alg.2 for Conv2d: dW = sum_{b,y,x} dY Xpad revealed to the MO at 2f, (c_o, c_i, s, s)."""
+    x_mo, x_do = _split(x_a, x_b)
+    gy_mo, gy_do = _split(gy_a, gy_b)
+    ring = sess.ring
+    B, c_i, H, Wd = x_do.shape
+    c_o = gy_do.shape[1]
+    msk = sess.rng(layer, OP_GRAD_W, P_MASK).uniform_ring((c_o, c_i, s, s), ring)
+    plan = plan_conv_layer("gradw", B, c_i, c_o, H, Wd, s, pad, stride, sess.p.N)
+    cross_do = _dev.empty_u64(c_o, c_i, s, s)
+    sess.he_eval(layer, OP_GRAD_W, plan, cross_do, msk,
+                 v_ct=None if mo_gy_zero else x_do.value.values, w_pt=None if mo_gy_zero else gy_mo.value.values,
+                 w_ct=None if mo_x_zero else gy_do.value.values, v_pt=None if mo_x_zero else x_mo.value.values,
+                 msg_in=MSG_GRADW, msg_out=MSG_GRADW)
+    shp = (c_o, c_i, s, s)
+    loc_do = _ring_conv(_lib.CONV_GRADW, x_do.value.values, gy_do.value.values, B, c_i, c_o, H, Wd, s, pad, stride,
+                        ring.ell, shp)
+    msg = _ring_bin(_lib.RING_ADD, cross_do, loc_do, ring.ell)  # DO: + local term (+ e)
+    if e is not None:
+        msg = _ring_bin(_lib.RING_ADD, msg, e, ring.ell)
+    sess.channel.send(DO, MSG_GRADW, msg, msg.numel() * 8)
+    out = _ring_bin(_lib.RING_ADD, msg, msk, ring.ell)  # MO: + s + local term
+    if not (mo_x_zero or mo_gy_zero):
+        loc_mo = _ring_conv(_lib.CONV_GRADW, x_mo.value.values, gy_mo.value.values, B, c_i, c_o, H, Wd, s, pad,
+                            stride, ring.ell, shp)
+        out = _ring_bin(_lib.RING_ADD, out, loc_mo, ring.ell)
+    return RingTensor(out, 2 * ring.f, ring, _canonical=True)
+
+
+def reveal_grad_bias_conv(sess: Session, layer: int, gy_a: ShareTensor, gy_b: ShareTensor,
+                          e: torch.Tensor | None = None) -> RingTensor:
+    """SPEC:330-338 for Conv2d: per-channel local sums over batch and positions."""
+    gy_mo, gy_do = _split(gy_a, gy_b)
+    ring = sess.ring
+    B, c, h, w = gy_do.shape
+
+    def chan_sum(v):
+        t = v.reshape(B, c, h * w).permute(1, 0, 2).contiguous()  # local data movement
+        out = _dev.empty_u64(c)
+        _lib.call("pb_ring_rowsum", _dev.ptr(t), c, B * h * w, ring.ell, _dev.ptr(out), _dev.stream())
+        return out
+
+    sd = chan_sum(gy_do.value.values)
+    if e is not None:
+        sd = _ring_bin(_lib.RING_ADD, sd, e, ring.ell)
+    sess.channel.send(DO, MSG_GRADB, sd, c * 8)
+    return RingTensor(_ring_bin(_lib.RING_ADD, chan_sum(gy_mo.value.values), sd, ring.ell), gy_do.scale, ring,
+                      _canonical=True)
 
 
 def sample_dp_noise(shape, dp: DpConfig, rng: SeededRng) -> np.ndarray:  # SPEC:348-356

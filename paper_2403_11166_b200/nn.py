@@ -22,37 +22,115 @@ import torch
 
 from . import _dev, _lib
 from .errors import EncodeRangeError, ShapeError
-from .linear_protocols import Session, grad_weight, linear_backward_input, linear_forward, reveal_grad_bias
-from .nonlinear import relu_backward, relu_forward, truncate
+from .linear_protocols import (Session, conv_backward_input, conv_forward, conv_grad_weight, grad_weight,
+                               linear_backward_input, linear_forward, reveal_grad_bias, reveal_grad_bias_conv)
+from .nonlinear import avgpool_backward, avgpool_forward, relu_backward, relu_forward, truncate
+from .poly_encoding import conv_out_hw
 from .ring import DO, MO, RingParams, RingTensor, SeededRng, ShareTensor, arith_shift, encode_fixed
 
 MODELS = {
-    "mnist_mlp": [784, 128, 128, 10],  # SPEC:608, PAPER Fig. 5
+    # PAPER Fig. 5 / SPEC:608
+    "mnist_mlp": ((784,), [("fc", 784, 128), ("fc", 128, 128), ("fc", 128, 10)]),
+    # PAPER Fig. 6 / SPEC:609: Conv 1->5 5x5 s2 p2, FC 980->100, FC 100->10
+    "mnist_cnn": ((1, 28, 28), [("conv", 1, 5, 5, 2, 2), ("flatten",), ("fc", 980, 100), ("fc", 100, 10)]),
+    # BASELINE configs[2] "2 x conv5x5 + FC": the paper's CNN plus a second conv
+    "mnist_cnn2": ((1, 28, 28), [("conv", 1, 5, 5, 2, 2), ("conv", 5, 5, 5, 2, 1), ("flatten",),
+                                 ("fc", 980, 100), ("fc", 100, 10)]),
+    # PAPER Fig. 7: the private-conv CIFAR-10 CNN (BASELINE configs[3])
+    "cifar_cnn": ((3, 32, 32), [("conv", 3, 64, 5, 2, 1), ("pool",), ("conv", 64, 64, 5, 2, 1), ("pool",),
+                                ("conv", 64, 64, 3, 1, 1), ("conv", 64, 64, 1, 0, 1), ("conv", 64, 16, 1, 0, 1),
+                                ("flatten",), ("fc", 1024, 10)]),
 }
 
 
-class Model:
-    """FC stack with MO-held float64 master weights on the device."""
+def mlp_spec(sizes):
+    return (sizes[0],), [("fc", a, b) for a, b in zip(sizes[:-1], sizes[1:])]
 
-    def __init__(self, sizes, ring: RingParams, seed: int = 0):
-        self.sizes = list(sizes)
+
+def shapes(in_shape, layers):
+    """Per-entry (input shape, output shape) of one sample; raises ShapeError
+    when adjacent layers do not compose."""
+    cur = tuple(in_shape)
+    out = []
+    for e in layers:
+        if e[0] == "fc":
+            if cur != (e[1],):
+                raise ShapeError(f"fc expects ({e[1]},), got {cur}")
+            nxt = (e[2],)
+        elif e[0] == "conv":
+            _, ci, co, s, p, st = e
+            if len(cur) != 3 or cur[0] != ci:
+                raise ShapeError(f"conv expects {ci} channels, got {cur}")
+            nxt = (co, *conv_out_hw(cur[1], cur[2], s, p, st))
+        elif e[0] == "pool":
+            if len(cur) != 3 or cur[1] % 2 or cur[2] % 2:
+                raise ShapeError("avgpool2 needs even spatial dims")
+            nxt = (cur[0], cur[1] // 2, cur[2] // 2)
+        elif e[0] == "flatten":
+            nxt = (int(np.prod(cur)),)
+        else:
+            raise ShapeError(f"unknown layer {e!r}")
+        out.append((cur, nxt))
+        cur = nxt
+    return out
+
+
+class Model:
+    """Layer graph with MO-held float64 master weights on the device.
+
+    ``Model(sizes)`` builds the FC stack (MLP); ``Model(name)`` one of MODELS;
+    ``Model((in_shape, layers))`` any graph of ("fc", n_i, n_o),
+    ("conv", c_i, c_o, s, pad, stride), ("pool",), ("flatten",).  Every linear
+    layer except the last is followed by ReLU + truncation by f."""
+
+    def __init__(self, arch, ring: RingParams, seed: int = 0):
+        if isinstance(arch, str):
+            if arch not in MODELS:
+                raise ShapeError(f"unknown model {arch!r}")
+            arch = MODELS[arch]
+        if isinstance(arch, (list, tuple)) and all(isinstance(v, (int, np.integer)) for v in arch):
+            arch = mlp_spec(list(arch))
+        self.in_shape, self.layers = tuple(arch[0]), list(arch[1])
+        self.io = shapes(self.in_shape, self.layers)
+        self.lin = [i for i, e in enumerate(self.layers) if e[0] in ("fc", "conv")]
         self.ring = ring
         dev = _dev.device()
         self.w, self.b, self.vw, self.vb = [], [], [], []
-        for l, (ni, no) in enumerate(zip(sizes[:-1], sizes[1:])):
+        for l, i in enumerate(self.lin):
+            e = self.layers[i]
+            if e[0] == "fc":
+                wshape, fan_in, nb = (e[2], e[1]), e[1], e[2]
+            else:
+                wshape, fan_in, nb = (e[2], e[1], e[3], e[3]), e[1] * e[3] * e[3], e[2]
             g = SeededRng(seed, 500 + l)  # SPEC:646 init, same draws as the oracle
-            a = np.sqrt(1.0 / ni)
-            self.w.append(torch.from_numpy(g.uniform_real((no, ni), -a, a)).to(dev))
-            self.b.append(torch.from_numpy(g.uniform_real((no,), -a, a)).to(dev))
-            self.vw.append(torch.zeros(no, ni, dtype=torch.float64, device=dev))
-            self.vb.append(torch.zeros(no, dtype=torch.float64, device=dev))
+            a = np.sqrt(1.0 / fan_in)
+            self.w.append(torch.from_numpy(g.uniform_real(wshape, -a, a)).to(dev))
+            self.b.append(torch.from_numpy(g.uniform_real((nb,), -a, a)).to(dev))
+            self.vw.append(torch.zeros(wshape, dtype=torch.float64, device=dev))
+            self.vb.append(torch.zeros(nb, dtype=torch.float64, device=dev))
         self.W = [RingTensor(encode_fixed(w, ring), ring.f, ring, _canonical=True) for w in self.w]
         self.B = [RingTensor(encode_fixed(b, ring, 2 * ring.f), 2 * ring.f, ring, _canonical=True) for b in self.b]
         self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
 
     @property
+    def sizes(self):  # MLP compatibility
+        return [self.layers[self.lin[0]][1]] + [self.layers[i][2] for i in self.lin]
+
+    @property
     def n_layers(self):
-        return len(self.w)
+        return len(self.lin)
+
+    @property
+    def n_classes(self):
+        return self.io[-1][1][0]
+
+    def segments(self):
+        """For each linear l: the (pool / flatten) entries up to linear l+1."""
+        seg = []
+        for l, i in enumerate(self.lin):
+            j = self.lin[l + 1] if l + 1 < self.n_layers else len(self.layers)
+            seg.append(list(range(i + 1, j)))
+        return seg
 
     def sgd(self, gws, gbs, lr=1e-2, momentum=0.8, check=True):
         ring = self.ring
@@ -68,10 +146,6 @@ class Model:
 
 
 def build_model(name, ring: RingParams, seed: int = 0) -> Model:
-    if isinstance(name, str):
-        if name not in MODELS:
-            raise ShapeError(f"unknown model {name!r}")
-        return Model(MODELS[name], ring, seed)
     return Model(name, ring, seed)
 
 
@@ -92,19 +166,42 @@ def softmax_ce_grad(logits_2f: np.ndarray, labels: np.ndarray, ring: RingParams)
     return loss, np.floor(g * float(1 << ring.f)).astype(np.int64).astype(np.uint64) & ring.mask
 
 
+def _flatten(sh: ShareTensor) -> ShareTensor:  # (B, C, H, W) -> (C*H*W, B), local data movement
+    v = sh.value
+    return ShareTensor(sh.owner_role, RingTensor(v.values.reshape(v.shape[0], -1).t().contiguous(), v.scale,
+                                                 v.params, _canonical=True))
+
+
+def _unflatten(sh: ShareTensor, chw) -> ShareTensor:  # (C*H*W, B) -> (B, C, H, W)
+    v = sh.value
+    return ShareTensor(sh.owner_role, RingTensor(v.values.t().contiguous().reshape(-1, *chw), v.scale, v.params,
+                                                 _canonical=True))
+
+
 def forward_phase(sess: Session, model: Model, x: RingTensor):
     """Private forward pass; returns (state for the backward pass, logits = MO share + DO share)."""
     ring, f = model.ring, model.ring.f
     L = model.n_layers
-    acts = [(ShareTensor(MO, RingTensor(torch.zeros_like(x.values), f, ring, _canonical=True)), ShareTensor(DO, x))]
-    ds, ys = [], []
-    for l in range(L):
-        y = linear_forward(sess, l, model.W[l], model.B[l], *acts[-1], mo_x_zero=(l == 0))
+    seg = model.segments()
+    cur = (ShareTensor(MO, RingTensor(torch.zeros_like(x.values), f, ring, _canonical=True)), ShareTensor(DO, x))
+    acts, ds, ys = [], [], []
+    for l, i in enumerate(model.lin):
+        e = model.layers[i]
+        acts.append(cur)
+        if e[0] == "fc":
+            y = linear_forward(sess, l, model.W[l], model.B[l], *cur, mo_x_zero=(l == 0))
+        else:
+            y = conv_forward(sess, l, model.W[l], model.B[l], *cur, e[4], e[5], mo_x_zero=(l == 0))
         ys.append(y)
         if l < L - 1:
             z_mo, z_do, d = relu_forward(sess, l, *y)
-            acts.append(truncate(sess, l, z_mo, z_do, f))
+            cur = truncate(sess, l, z_mo, z_do, f)
             ds.append(d)
+            for k in seg[l]:
+                if model.layers[k][0] == "pool":
+                    cur = avgpool_forward(sess, l, *cur)
+                elif model.layers[k][0] == "flatten":
+                    cur = (_flatten(cur[0]), _flatten(cur[1]))
     # the MO sends its share of the logits; the DO reconstructs them (SPEC:614)
     y_mo, y_do = ys[-1]
     logits = y_mo.value + y_do.value
@@ -116,19 +213,37 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
     """Private backward pass from the DO's loss gradient share (MO share 0) + SGD at the MO."""
     ring, f = model.ring, model.ring.f
     L = model.n_layers
+    seg = model.segments()
     acts, ds, ys = state
     gy_do = ShareTensor(DO, RingTensor(g_do, f, ring, _canonical=True))
     gy_mo = ShareTensor(MO, RingTensor(torch.zeros_like(g_do), f, ring, _canonical=True))
     gws, gbs = [None] * L, [None] * L
     for l in reversed(range(L)):
+        e = model.layers[model.lin[l]]
         last = l == L - 1
-        gbs[l] = reveal_grad_bias(sess, l, gy_mo, gy_do)
-        gws[l] = arith_shift(grad_weight(sess, l, *acts[l], gy_mo, gy_do, mo_x_zero=(l == 0), mo_gy_zero=last), f)
+        if e[0] == "fc":
+            gbs[l] = reveal_grad_bias(sess, l, gy_mo, gy_do)
+            gw = grad_weight(sess, l, *acts[l], gy_mo, gy_do, mo_x_zero=(l == 0), mo_gy_zero=last)
+        else:
+            gbs[l] = reveal_grad_bias_conv(sess, l, gy_mo, gy_do)
+            gw = conv_grad_weight(sess, l, *acts[l], gy_mo, gy_do, e[3], e[4], e[5], mo_x_zero=(l == 0),
+                                  mo_gy_zero=last)
+        gws[l] = arith_shift(gw, f)
         if trace is not None:
             trace.append((l, ys[l], gbs[l], gws[l]))
         if l > 0:
-            ga = linear_backward_input(sess, l, model.W[l], gy_mo, gy_do, mo_gy_zero=last)
+            if e[0] == "fc":
+                ga = linear_backward_input(sess, l, model.W[l], gy_mo, gy_do, mo_gy_zero=last)
+            else:
+                H, Wd = acts[l][1].shape[2:]
+                ga = conv_backward_input(sess, l, model.W[l], gy_mo, gy_do, H, Wd, e[4], e[5], mo_gy_zero=last)
             t_mo, t_do = truncate(sess, l, *ga, f, backward=True)
+            for k in reversed(seg[l - 1]):
+                if model.layers[k][0] == "pool":
+                    t_mo, t_do = avgpool_backward(sess, l - 1, t_mo, t_do)
+                elif model.layers[k][0] == "flatten":
+                    chw = model.io[k][0]
+                    t_mo, t_do = _unflatten(t_mo, chw), _unflatten(t_do, chw)
             gy_mo, gy_do = relu_backward(sess, l - 1, ds[l - 1], t_mo, t_do)
     model.sgd(gws, gbs, lr, momentum, check=check)
     return gws, gbs
@@ -136,7 +251,8 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
 
 def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e-2, momentum=0.8,
                        trace=None, check=True):
-    """One private step; x (784, B) at scale f, held by the DO."""
+    """One private step; x held by the DO at scale f: (784, B)
+    feature-major for FC-first models, (B, C, H, W) for CNNs."""
     state, logits = forward_phase(sess, model, x)
     loss, g = softmax_ce_grad(logits.numpy(), np.asarray(labels), model.ring)  # DO, float64 (host)
     gws, gbs = backward_phase(sess, model, state, _dev.u64_to_device(g), lr, momentum, trace, check)
@@ -155,7 +271,8 @@ class GraphStep:
         self.sess, self.model, self.lr, self.momentum = sess, model, lr, momentum
         sess.enable_graph_mode()
         self.x = x  # device input buffer; callers copy new batches into x.values
-        n_cls, B = model.sizes[-1], x.shape[1]
+        n_cls = model.n_classes
+        B = x.shape[1] if len(model.in_shape) == 1 else x.shape[0]
         self.g_do = torch.zeros(n_cls, B, dtype=torch.int64, device=x.values.device)
         self.logits_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
         self.g_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
@@ -189,5 +306,18 @@ def synthetic_mnist(seed: int, B: int, ring: RingParams):
     g = SeededRng(seed, 900)
     x = g.uniform_real((784, B), 0.0, 1.0)
     x = (x - 0.1307) / 0.3081
+    labels = g._host_draw(lambda gen: gen.integers(0, 10, size=B))
+    return x, labels
+
+
+def synthetic_images(seed: int, B: int, in_shape, ring: RingParams):
+    """Host float64 image batch (B, C, H, W) + labels, the oracle's draws
+    (oracle/nn.synthetic_images): MNIST shapes reuse synthetic_mnist's pixels,
+    CIFAR shapes draw U[0,1] standardised with (0.5, 0.25)."""
+    if tuple(in_shape) == (1, 28, 28):
+        x, labels = synthetic_mnist(seed, B, ring)
+        return np.ascontiguousarray(x.T).reshape(B, 1, 28, 28), labels
+    g = SeededRng(seed, 901)
+    x = (g.uniform_real((B, *in_shape), 0.0, 1.0) - 0.5) / 0.25
     labels = g._host_draw(lambda gen: gen.integers(0, 10, size=B))
     return x, labels

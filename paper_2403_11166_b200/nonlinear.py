@@ -12,6 +12,8 @@ so every output share matches the CPU oracle bit-for-bit.
     relu_forward     y = DReLU(x) * x, d cached        (SPEC:533-541, 1{x >= 0})
     truncate         faithful: arith_shift(x, bits)
     relu_backward    grad x = d * grad y (no new compare)
+    avgpool_forward  local 2x2 window sums, then a 2-bit truncation
+    avgpool_backward replicate to the 2x2 window, then a 2-bit truncation
 """
 
 from __future__ import annotations
@@ -19,7 +21,8 @@ from __future__ import annotations
 import torch
 
 from . import _dev, _lib
-from .linear_protocols import OP_RELU, OP_RELU_B, OP_TRUNC_B, OP_TRUNC_F, P_DEALER, Session, _split
+from .linear_protocols import (OP_POOL_B, OP_POOL_F, OP_RELU, OP_RELU_B, OP_TRUNC_B, OP_TRUNC_F, P_DEALER, Session,
+                               _split)
 from .ring import DO, MO, RingTensor, ShareTensor
 
 
@@ -59,3 +62,42 @@ def relu_backward(sess: Session, layer: int, d: torch.Tensor, a: ShareTensor, b:
     s = a.scale
     return (ShareTensor(MO, RingTensor(x_mo, s, sess.ring, _canonical=True)),
             ShareTensor(DO, RingTensor(x_do, s, sess.ring, _canonical=True)))
+
+
+def _pool_local(op: int, v: torch.Tensor, out_hw, ell: int) -> torch.Tensor:
+    B, C, H, W = v.shape
+    oh, ow = out_hw
+    out = _dev.empty_u64(B, C, oh, ow)
+    hh, ww = (H, W) if op == _lib.POOL_SUM else (oh, ow)
+    _lib.call("pb_pool2", op, _dev.ptr(v), B * C, hh, ww, ell, _dev.ptr(out), _dev.stream())
+    return out
+
+
+def avgpool_forward(sess: Session, layer: int, a: ShareTensor, b: ShareTensor):
+    """AvgPool2 forward: each party sums its 2x2 windows, then
+    the sum is truncated by 2 bits (dealer, stream (layer, OP_POOL_F))."""
+    mo, do = _split(a, b)
+    ring = sess.ring
+    B, C, H, W = do.shape
+    sm = _pool_local(_lib.POOL_SUM, mo.value.values, (H // 2, W // 2), ring.ell)
+    sd = _pool_local(_lib.POOL_SUM, do.value.values, (H // 2, W // 2), ring.ell)
+    s = a.scale
+    x_mo, x_do, _ = _dealer(sess, layer, OP_POOL_F, _lib.DEALER_TRUNC, ShareTensor(MO, RingTensor(sm, s, ring, _canonical=True)),
+                            ShareTensor(DO, RingTensor(sd, s, ring, _canonical=True)), k=2)
+    return (ShareTensor(MO, RingTensor(x_mo, s, ring, _canonical=True)),
+            ShareTensor(DO, RingTensor(x_do, s, ring, _canonical=True)))
+
+
+def avgpool_backward(sess: Session, layer: int, a: ShareTensor, b: ShareTensor):
+    """AvgPool2 backward: replicate each gradient to its 2x2 window, then a
+    2-bit truncation (dealer, stream (layer, OP_POOL_B))."""
+    mo, do = _split(a, b)
+    ring = sess.ring
+    B, C, h, w = do.shape
+    rm = _pool_local(_lib.POOL_REPLICATE, mo.value.values, (2 * h, 2 * w), ring.ell)
+    rd = _pool_local(_lib.POOL_REPLICATE, do.value.values, (2 * h, 2 * w), ring.ell)
+    s = a.scale
+    x_mo, x_do, _ = _dealer(sess, layer, OP_POOL_B, _lib.DEALER_TRUNC, ShareTensor(MO, RingTensor(rm, s, ring, _canonical=True)),
+                            ShareTensor(DO, RingTensor(rd, s, ring, _canonical=True)), k=2)
+    return (ShareTensor(MO, RingTensor(x_mo, s, ring, _canonical=True)),
+            ShareTensor(DO, RingTensor(x_do, s, ring, _canonical=True)))

@@ -156,16 +156,34 @@ def matmul_blocks(g: MatmulGeometry, N: int, mode: str = "cost"):
     return best[1]
 
 
-def conv_blocks(g: ConvGeometry, N: int):
+def conv_blocks(g: ConvGeometry, N: int, mode: str = "cost"):
+    """(B_blk, c_o_blk, c_i_blk) with B_blk * c_o_blk * c_i_blk * h * w <= N.
+    mode "spec": SPEC:285 order; mode "cost": minimise the cost model above."""
     hw = g.h * g.w
     if g.s < 1 or g.s > min(g.h, g.w):
         raise GeometryError("kernel must fit the image")
     if hw > N:
         raise GeometryError(f"h*w = {hw} exceeds N = {N}")
-    cib = min(g.c_i, N // hw)
-    if g.c_o * cib * hw <= N:
-        return min(g.B, N // (g.c_o * cib * hw)), g.c_o, cib
-    return 1, max(1, N // (cib * hw)), cib
+    if mode == "spec":
+        cib = min(g.c_i, N // hw)
+        if g.c_o * cib * hw <= N:
+            return min(g.B, N // (g.c_o * cib * hw)), g.c_o, cib
+        return 1, max(1, N // (cib * hw)), cib
+    cap = N // hw
+    best = None
+    for cib in range(1, min(g.c_i, cap) + 1):
+        nI = _cdiv(g.c_i, cib)
+        if _cdiv(g.c_i, _cdiv(g.c_i, nI)) != nI or _cdiv(g.c_i, nI) != cib:
+            continue  # only balanced splits
+        for cob in range(1, min(g.c_o, cap // cib) + 1):
+            Bb = min(g.B, cap // (cib * cob))
+            nB, nO = _cdiv(g.B, Bb), _cdiv(g.c_o, cob)
+            n_out = nB * nO
+            cost = COST_ENC * nB * nI + COST_PT * nO * nI + COST_OUT * n_out + COST_PROD * n_out * nI
+            key = (round(cost, 6), n_out, nI, -cob)
+            if best is None or key < best[0]:
+                best = (key, (Bb, cob, cib))
+    return best[1]
 
 
 def _scatter(n_poly, N, poly_idx, pos, src, ok):
@@ -227,9 +245,9 @@ def plan_matmul(g: MatmulGeometry, N: int, v_strides=None, w_strides=None, y_str
 
 
 @lru_cache(maxsize=256)
-def plan_conv(g: ConvGeometry, N: int) -> BlockPlan:
+def plan_conv(g: ConvGeometry, N: int, mode: str = "spec") -> BlockPlan:
     """v is (B, c_i, h, w), W is (c_o, c_i, s, s), y is (B, c_o, h-s+1, w-s+1)."""
-    Bb, cob, cib = conv_blocks(g, N)
+    Bb, cob, cib = conv_blocks(g, N, mode)
     nB, nO, nI = _cdiv(g.B, Bb), _cdiv(g.c_o, cob), _cdiv(g.c_i, cib)
     h, w, s = g.h, g.w, g.s
     hw = h * w
@@ -282,6 +300,114 @@ def plan_blocks(g, N: int, mode: str = "cost") -> BlockPlan:
     if isinstance(g, ConvGeometry):
         return plan_conv(g, N)
     raise GeometryError(f"unknown geometry {g!r}")
+
+
+# ------------------------------------------- conv layers (pad / stride) ---
+# SPEC:284 keeps the codec at valid-mode stride-1 cross-correlation with
+# padding / stride "outside the codec", and SPEC:286 lowers the backward
+# operators by local share reshaping.  Each such reshaping (zero padding,
+# stride subsampling, zero-stuffing dilation, kernel flip, channel / batch
+# transposition) is a data-movement-only linear map, so it is folded into the
+# plan's index maps: a plan of the logical geometry (the verified codec) has
+# its source / destination indices re-pointed into the physical tensors
+# (-1 = structural zero / dropped output).  Forward, input-gradient and
+# weight-gradient operators all use the paper's native conv packing
+# (PAPER:1226-1247); nothing is materialised.
+
+
+def conv_out_hw(H, W, s, pad, stride):
+    return (H + 2 * pad - s) // stride + 1, (W + 2 * pad - s) // stride + 1
+
+
+def _compact_out(pos, dst):
+    """Move each row's useful (pos, dst) pairs to the front; U = max count."""
+    ok = dst >= 0
+    cnt = ok.sum(axis=1)
+    U = max(1, int(cnt.max()) if len(cnt) else 1)
+    P = pos.shape[0]
+    npos = np.full((P, U), -1, dtype=np.int64)
+    ndst = np.full((P, U), -1, dtype=np.int64)
+    rows, cols = np.nonzero(ok)
+    slot = np.arange(len(rows)) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    npos[rows, slot] = pos[rows, cols]
+    ndst[rows, slot] = dst[rows, cols]
+    return npos, ndst
+
+
+def remap(plan: BlockPlan, in_map, pt_map, out_map) -> BlockPlan:
+    def re(src, m):
+        out = np.full(src.shape, -1, dtype=np.int64)
+        ok = src >= 0
+        out[ok] = m[src[ok]]
+        return out
+
+    dst = re(plan.out_dst, out_map)
+    pos, dst = _compact_out(np.where(dst >= 0, plan.out_pos, -1), dst)
+    return BlockPlan(plan.kind, plan.geometry, plan.N, plan.blk, plan.nblk, re(plan.in_src, in_map),
+                     re(plan.pt_src, pt_map), pos, dst, plan.terms)
+
+
+def conv_index_maps(kind: str, B, c_i, c_o, H, W, s, pad, stride):
+    """(logical ConvGeometry, in_map, pt_map, out_map) of one conv-layer operator:
+
+    fwd   Y[b,o,y,x]  = sum W[o,c,i,j] Xpad[b,c,y*st+i,x*st+j]          v=X,  W=W,  y=Y
+    bwdx  dX[b,c,y,x] = sum W[o,c,i,j] dY[b,o,(y+p-i)/st,(x+p-j)/st]    v=dY, W=W,  y=dX
+          (correlation of the dilated, (s-1)-padded dY with the flipped, transposed W)
+    gradw dW[o,c,i,j] = sum dY[b,o,y,x] Xpad[b,c,y*st+i,x*st+j]         v=X,  W=dY, y=dW
+          (correlation of Xpad^T (channels as batch) with the dilated dY^T as kernel)
+    """
+    oh, ow = conv_out_hw(H, W, s, pad, stride)
+    hp, wp = H + 2 * pad, W + 2 * pad
+
+    def pad_map(C, Bn, transpose=False):  # logical (Bn, C, hp, wp) -> X (B, c_i, H, W) index
+        b, c, y, x = np.meshgrid(np.arange(Bn), np.arange(C), np.arange(hp), np.arange(wp), indexing="ij")
+        yy, xx = y - pad, x - pad
+        ok = (yy >= 0) & (yy < H) & (xx >= 0) & (xx < W)
+        bb, cc = (c, b) if transpose else (b, c)
+        return np.where(ok, ((bb * c_i + cc) * H + yy) * W + xx, -1).ravel()
+
+    if kind == "fwd":
+        g = ConvGeometry(B, c_i, c_o, hp, wp, s)
+        b, o, y, x = np.meshgrid(np.arange(B), np.arange(c_o), np.arange(hp - s + 1), np.arange(wp - s + 1),
+                                 indexing="ij")
+        ok = (y % stride == 0) & (x % stride == 0) & (y // stride < oh) & (x // stride < ow)
+        out_map = np.where(ok, ((b * c_o + o) * oh + y // stride) * ow + x // stride, -1).ravel()
+        return g, pad_map(c_i, B), np.arange(c_o * c_i * s * s), out_map
+    if kind == "bwdx":
+        hd, wd = (oh - 1) * stride + 1 + 2 * (s - 1), (ow - 1) * stride + 1 + 2 * (s - 1)
+        g = ConvGeometry(B, c_o, c_i, hd, wd, s)
+        b, o, y, x = np.meshgrid(np.arange(B), np.arange(c_o), np.arange(hd), np.arange(wd), indexing="ij")
+        u, v = y - (s - 1), x - (s - 1)
+        ok = (u >= 0) & (v >= 0) & (u % stride == 0) & (v % stride == 0) & (u // stride < oh) & (v // stride < ow)
+        in_map = np.where(ok, ((b * c_o + o) * oh + u // stride) * ow + v // stride, -1).ravel()
+        c, o2, i, j = np.meshgrid(np.arange(c_i), np.arange(c_o), np.arange(s), np.arange(s), indexing="ij")
+        pt_map = (((o2 * c_i + c) * s + (s - 1 - i)) * s + (s - 1 - j)).ravel()
+        b, c, y, x = np.meshgrid(np.arange(B), np.arange(c_i), np.arange(hd - s + 1), np.arange(wd - s + 1),
+                                 indexing="ij")
+        yy, xx = y - pad, x - pad
+        ok = (yy >= 0) & (yy < H) & (xx >= 0) & (xx < W)
+        return g, in_map, pt_map, np.where(ok, ((b * c_i + c) * H + yy) * W + xx, -1).ravel()
+    if kind == "gradw":
+        sd_h, sd_w = (oh - 1) * stride + 1, (ow - 1) * stride + 1
+        if sd_h != sd_w:
+            raise GeometryError("gradw lowering needs a square output")
+        g = ConvGeometry(c_i, B, c_o, hp, wp, sd_h)
+        o, b, i, j = np.meshgrid(np.arange(c_o), np.arange(B), np.arange(sd_h), np.arange(sd_w), indexing="ij")
+        ok = (i % stride == 0) & (j % stride == 0)
+        pt_map = np.where(ok, ((b * c_o + o) * oh + i // stride) * ow + j // stride, -1).ravel()
+        c, o, y, x = np.meshgrid(np.arange(c_i), np.arange(c_o), np.arange(hp - sd_h + 1), np.arange(wp - sd_w + 1),
+                                 indexing="ij")
+        ok = (y < s) & (x < s)
+        return g, pad_map(B, c_i, transpose=True), pt_map, np.where(ok, ((o * c_i + c) * s + y) * s + x, -1).ravel()
+    raise GeometryError(f"unknown conv operator {kind!r}")
+
+
+@lru_cache(maxsize=128)
+def plan_conv_layer(kind: str, B, c_i, c_o, H, W, s, pad, stride, N, mode: str = "cost") -> BlockPlan:
+    """Block plan of one conv-layer operator (kind fwd / bwdx / gradw) over the
+    physical tensors; its maps feed the same fused kernels as matmul plans."""
+    g, in_map, pt_map, out_map = conv_index_maps(kind, B, c_i, c_o, H, W, s, pad, stride)
+    return remap(plan_conv(g, N, mode), in_map, pt_map, out_map)
 
 
 # --------------------------------------------- plaintext codecs (host) ---
