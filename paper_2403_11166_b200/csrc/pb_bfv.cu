@@ -64,8 +64,8 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   extern __shared__ uint32_t sm[];
   const int tid = threadIdx.x;
   const int L = P.L;
-  const int64_t p = blockIdx.x / L;
-  const int l = blockIdx.x % L;
+  const int l = (int)(blockIdx.x / nP);  // limb-major: co-resident CTAs share one limb's twiddles
+  const int64_t p = blockIdx.x % nP;
   const uint32_t q = P.q[l];
   const uint64_t mu = P.mu[l];
   const uint32_t tm = P.tmod[l];
@@ -145,8 +145,8 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   extern __shared__ uint32_t sm[];
   const int tid = threadIdx.x;
   const int L = P.L;
-  const int64_t p = blockIdx.x / L;
-  const int l = blockIdx.x % L;
+  const int l = (int)(blockIdx.x / nP);  // limb-major: co-resident CTAs share one limb's twiddles
+  const int64_t p = blockIdx.x % nP;
   const uint32_t q = P.q[l];
   const uint64_t mu = P.mu[l];
   const uint2* tw = P.tw_fwd + (size_t)l * N;
@@ -193,7 +193,7 @@ __device__ __forceinline__ void uniform_pair(uint64_t seed, uint64_t nonce, int6
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(1 << (LOGN - 5))
+__global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
     k_encrypt_sk(PbDev P, const uint32_t* sk, PbPack src, int64_t nP, const uint32_t* a_in, const int8_t* e,
                  uint64_t seed_arg, const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct) {
   using Nt = pb::Ntt<LOGN>;
@@ -202,27 +202,40 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   extern __shared__ uint32_t sm[];
   const int tid = threadIdx.x;
   const int L = P.L;
-  const int64_t p = blockIdx.x / L;
-  const int l = blockIdx.x % L;
+  const int l = (int)(blockIdx.x / nP);  // limb-major: co-resident CTAs share one limb's twiddles
+  const int64_t p = blockIdx.x % nP;
   const uint32_t q = P.q[l];
   const uint64_t mu = P.mu[l];
   const int8_t* ep = e + p * N;
-  uint32_t b[32], a[32], s[32];
+  uint32_t b[32];
   load_source<Nt>(b, sm, src, p, tid, [&](uint64_t v) { return delta_m(P, l, v); });
 #pragma unroll
   for (int c = 0; c < 32; ++c) b[c] = addmod(lift_small(ep[Nt::j1(tid, c)], q), b[c], q);
   Nt::forward(b, sm, P.tw_fwd + (size_t)l * N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
-  if (a_in) {
-    Nt::gld3(a_in + (p * L + l) * N, a, tid);
-  } else {
+  // c1 = a, c0 = NTT(e + Delta m) - a*s, one 128-bit device-order vector at a
+  // time (keeps a and s out of the register file: 32 live residues, not 96)
+  const uint4* s4 = reinterpret_cast<const uint4*>(sk + (size_t)l * N) + tid;
+  const uint4* a4 = a_in ? reinterpret_cast<const uint4*>(a_in + (p * L + l) * N) + tid : nullptr;
+  uint4* c0 = reinterpret_cast<uint4*>(ct + ((p * 2 + 0) * L + l) * N) + tid;
+  uint4* c1 = reinterpret_cast<uint4*>(ct + ((p * 2 + 1) * L + l) * N) + tid;
 #pragma unroll
-    for (int c = 0; c < 32; c += 2) uniform_pair(seed, nonce, p, l, (tid << 4) + (c >> 1), q, 0x53454e43u, a[c], a[c + 1]);
+  for (int v = 0; v < 8; ++v) {
+    uint32_t a[4];
+    if (a4) {
+      const uint4 x = __ldg(a4 + v * Nt::T);
+      a[0] = x.x; a[1] = x.y; a[2] = x.z; a[3] = x.w;
+    } else {
+      uniform_pair(seed, nonce, p, l, (tid << 4) + 2 * v, q, 0x53454e43u, a[0], a[1]);
+      uniform_pair(seed, nonce, p, l, (tid << 4) + 2 * v + 1, q, 0x53454e43u, a[2], a[3]);
+    }
+    const uint4 sv = __ldg(s4 + v * Nt::T);
+    const uint32_t sk_[4] = {sv.x, sv.y, sv.z, sv.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = submod(pb::canon4(b[4 * v + k], q), mulmod(a[k], sk_[k], q, mu), q);
+    c0[v * Nt::T] = make_uint4(o[0], o[1], o[2], o[3]);
+    c1[v * Nt::T] = make_uint4(a[0], a[1], a[2], a[3]);
   }
-  Nt::gld3(sk + (size_t)l * N, s, tid);
-#pragma unroll
-  for (int c = 0; c < 32; ++c) b[c] = submod(pb::canon4(b[c], q), mulmod(a[c], s[c], q, mu), q);
-  Nt::gst3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
-  Nt::gst3(ct + ((p * 2 + 1) * L + l) * N, a, tid);
 }
 
 // --------------------------------------------------------------- decrypt ---
@@ -237,8 +250,8 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   extern __shared__ uint32_t sm[];
   const int tid = threadIdx.x;
   const int L = P.L;
-  const int64_t p = blockIdx.x / L;
-  const int l = blockIdx.x % L;
+  const int l = (int)(blockIdx.x / nP);  // limb-major: co-resident CTAs share one limb's twiddles
+  const int64_t p = blockIdx.x % nP;
   const uint32_t q = P.q[l];
   const uint64_t mu = P.mu[l];
   uint32_t a[32], b[32];
@@ -336,8 +349,8 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   extern __shared__ uint32_t sm[];
   const int tid = threadIdx.x;
   const int L = P.L;
-  const int64_t p = blockIdx.x / L;
-  const int l = blockIdx.x % L;
+  const int l = (int)(blockIdx.x / nP);  // limb-major: co-resident CTAs share one limb's twiddles
+  const int64_t p = blockIdx.x % nP;
   const uint32_t q = P.q[l];
 
   // 1. Delta * mask polynomial (coefficient form) in shared memory.

@@ -158,6 +158,161 @@ __global__ void k_pool2(int op, const uint64_t* __restrict__ in, int64_t bc, int
   }
 }
 
+// ---------------------------------------------------------- implicit GEMM ---
+// The three operators as one tiled u64 GEMM  out[m][n] = sum_k A[m][k] B[k][n]
+// with A / B gathered on the fly (no im2col buffer):
+//   FWD    m = o,  n = (b,y,x) of Y,  k = (c,i,j):  A = W[o,c,i,j],  B = X[b,c,y*st+i-p,x*st+j-p]
+//   BWDX   m = c,  n = (b,y,x) of dX, k = (o,i,j):  A = W[o,c,i,j],  B = dY[b,o,(y+p-i)/st,(x+p-j)/st]
+//   GRADW  m = o,  n = (c,i,j),       k = (b,y,x):  A = dY[b,o,y,x], B = X[b,c,y*st+i-p,x*st+j-p]
+// CTA tile 64 x 64 x 16 through shared memory, 256 threads x (4 x 4) register
+// accumulators; a u64 multiply-add is 3 IMAD-class instructions.  GRADW
+// (K = B*oh*ow, small M*N) splits K over gridDim.z and accumulates with u64
+// atomics (exact mod 2^64), then masks in a second pass.
+struct ConvDims {
+  int B, ci, co, H, W, p, st, oh, ow;
+};
+
+template <int S, int KIND>
+struct ConvGemm {  // 32-bit index arithmetic (the launcher checks every tensor has < 2^31 elements)
+  static constexpr int SS = S * S;
+  __device__ __forceinline__ static void mnk(const ConvDims& d, int& M, int& N, int& K) {
+    if (KIND == PB_CONV_FWD) { M = d.co; N = d.B * d.oh * d.ow; K = d.ci * SS; }
+    else if (KIND == PB_CONV_BWDX) { M = d.ci; N = d.B * d.H * d.W; K = d.co * SS; }
+    else { M = d.co; N = d.ci * SS; K = d.B * d.oh * d.ow; }
+  }
+  __device__ __forceinline__ static uint64_t a_at(const ConvDims& d, const uint64_t* A, int m, int k) {
+    if (KIND == PB_CONV_FWD) return __ldg(A + (size_t)m * (d.ci * SS) + k);
+    if (KIND == PB_CONV_BWDX) {  // k = (o, i, j)
+      const int o = k / SS, r = k - o * SS;
+      return __ldg(A + (size_t)(o * d.ci + m) * SS + r);
+    }
+    const unsigned hw = (unsigned)(d.oh * d.ow);  // GRADW: k = (b, y, x) of dY, m = o
+    const unsigned b = (unsigned)k / hw, r = (unsigned)k - b * hw;
+    return __ldg(A + (size_t)(b * d.co + m) * hw + r);
+  }
+  __device__ __forceinline__ static uint64_t b_at(const ConvDims& d, const uint64_t* Bm, int k, int n) {
+    if (KIND == PB_CONV_FWD || KIND == PB_CONV_GRADW) {
+      const int kc = KIND == PB_CONV_FWD ? k : n;  // (c,i,j)
+      const unsigned kp = (unsigned)(KIND == PB_CONV_FWD ? n : k);  // (b,y,x)
+      const int c = kc / SS, r = kc - c * SS, i = r / S, j = r - i * S;
+      const unsigned hw = (unsigned)(d.oh * d.ow), ow = (unsigned)d.ow;
+      const unsigned b = kp / hw, q = kp - b * hw, y = q / ow, x = q - y * ow;
+      const int yy = (int)y * d.st + i - d.p, xx = (int)x * d.st + j - d.p;
+      if (yy < 0 || yy >= d.H || xx < 0 || xx >= d.W) return 0ull;
+      return __ldg(Bm + ((size_t)(b * d.ci + c) * d.H + yy) * d.W + xx);
+    }
+    const int o = k / SS, r = k - o * SS, i = r / S, j = r - i * S;  // BWDX: k = (o,i,j), n = (b,y,x) of dX
+    const unsigned hw = (unsigned)(d.H * d.W), Wd = (unsigned)d.W;
+    const unsigned b = (unsigned)n / hw, q = (unsigned)n - b * hw, y = q / Wd, x = q - y * Wd;
+    const int u = (int)y + d.p - i, v = (int)x + d.p - j;
+    if (u < 0 || v < 0) return 0ull;
+    const unsigned yy = (unsigned)u / (unsigned)d.st, xx = (unsigned)v / (unsigned)d.st;
+    if (yy * d.st != (unsigned)u || xx * d.st != (unsigned)v || yy >= (unsigned)d.oh || xx >= (unsigned)d.ow)
+      return 0ull;
+    return __ldg(Bm + ((size_t)(b * d.co + o) * d.oh + yy) * d.ow + xx);
+  }
+  __device__ __forceinline__ static size_t out_at(const ConvDims& d, int m, int n) {
+    if (KIND == PB_CONV_FWD) {
+      const unsigned hw = (unsigned)(d.oh * d.ow), b = (unsigned)n / hw, q = (unsigned)n - b * hw;
+      return (size_t)(b * d.co + m) * hw + q;
+    }
+    if (KIND == PB_CONV_BWDX) {
+      const unsigned hw = (unsigned)(d.H * d.W), b = (unsigned)n / hw, q = (unsigned)n - b * hw;
+      return (size_t)(b * d.ci + m) * hw + q;
+    }
+    return (size_t)m * (d.ci * SS) + n;
+  }
+};
+
+template <int S, int KIND>
+__global__ void __launch_bounds__(256) k_conv_gemm(ConvDims d, const uint64_t* __restrict__ A,
+                                                   const uint64_t* __restrict__ Bm, int64_t k_per_split, uint64_t m,
+                                                   uint64_t* __restrict__ out) {
+  using G = ConvGemm<S, KIND>;
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ uint64_t As[BK][BM];
+  __shared__ uint64_t Bs[BK][BN + 1];
+  int M, N, K;
+  G::mnk(d, M, N, K);
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int kb = (int)(blockIdx.z * k_per_split), ke = min(K, kb + (int)k_per_split);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  uint64_t acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0;
+  // load assignment: A tile element (k = tid & 15, m = (tid >> 4) + 16 r); B tile (k = tid >> 6 + 4 r, n = tid & 63)
+  const int la_k = tid & 15, la_m = tid >> 4;
+  const int lb_n = tid & 63, lb_k = tid >> 6;
+  for (int k0 = kb; k0 < ke; k0 += BK) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int mm = m0 + la_m + 16 * r, kk = k0 + la_k;
+      As[la_k][la_m + 16 * r] = (mm < M && kk < ke) ? G::a_at(d, A, mm, kk) : 0ull;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int kk = k0 + lb_k + 4 * r, nn = n0 + lb_n;
+      Bs[lb_k + 4 * r][lb_n] = (nn < N && kk < ke) ? G::b_at(d, Bm, kk, nn) : 0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      uint64_t a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[k][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[k][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int mm = m0 + ty + 16 * i;
+    if (mm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int nn = n0 + tx + 16 * j;
+      if (nn >= N) continue;
+      const size_t o = G::out_at(d, mm, nn);
+      if (gridDim.z == 1) out[o] = acc[i][j] & m;
+      else atomicAdd(reinterpret_cast<unsigned long long*>(out + o), (unsigned long long)acc[i][j]);
+    }
+  }
+}
+
+__global__ void k_mask_inplace(uint64_t* v, int64_t n, uint64_t m) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] &= m;
+}
+
+template <int S>
+int conv_gemm_launch(int kind, const ConvDims& d, const uint64_t* a, const uint64_t* b, uint64_t m, uint64_t* out,
+                     cudaStream_t st) {
+  int64_t M, N, K;
+  if (kind == PB_CONV_FWD) { M = d.co; N = (int64_t)d.B * d.oh * d.ow; K = (int64_t)d.ci * S * S; }
+  else if (kind == PB_CONV_BWDX) { M = d.ci; N = (int64_t)d.B * d.H * d.W; K = (int64_t)d.co * S * S; }
+  else { M = d.co; N = (int64_t)d.ci * S * S; K = (int64_t)d.B * d.oh * d.ow; }
+  const int64_t tiles = ((M + 63) / 64) * ((N + 63) / 64);
+  int splits = 1;
+  if (kind == PB_CONV_GRADW) {  // fill ~2 waves of 148 SMs, >= 256 K per split
+    while (tiles * splits < 2 * 148 * 2 && K / (splits * 2) >= 256) splits *= 2;
+  }
+  const int64_t kps = ((K + splits - 1) / splits + 15) / 16 * 16;
+  dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)splits);
+  if (splits > 1) cudaMemsetAsync(out, 0, (size_t)(M * N) * sizeof(uint64_t), st);
+  if (kind == PB_CONV_FWD) k_conv_gemm<S, PB_CONV_FWD><<<grid, 256, 0, st>>>(d, b, a, kps, m, out);  // A = W, B = X
+  else if (kind == PB_CONV_BWDX) k_conv_gemm<S, PB_CONV_BWDX><<<grid, 256, 0, st>>>(d, b, a, kps, m, out);  // A = W, B = dY
+  else k_conv_gemm<S, PB_CONV_GRADW><<<grid, 256, 0, st>>>(d, b, a, kps, m, out);  // A = dY, B = X
+  if (splits > 1) k_mask_inplace<<<pb_grid_1d(M * N, 256), 256, 0, st>>>(out, M * N, m);
+  return 0;
+}
+
 }  // namespace
 
 extern "C" int pb_ring_conv(int kind, const uint64_t* a, const uint64_t* b, int32_t B, int32_t c_i, int32_t c_o,
@@ -170,6 +325,17 @@ extern "C" int pb_ring_conv(int kind, const uint64_t* a, const uint64_t* b, int3
   const int oh = (H + 2 * pad - s) / stride + 1, ow = (W + 2 * pad - s) / stride + 1;
   const uint64_t m = cmask(ell);
   cudaStream_t st = pb_stream_of(stream);
+  if (kind < PB_CONV_FWD || kind > PB_CONV_GRADW) return pb_set_error(PB_ERR_ARG, "bad conv kind");
+  const ConvDims d{B, c_i, c_o, H, W, pad, stride, oh, ow};
+  const int64_t big = (int64_t)B * (c_i > c_o ? c_i : c_o) * (H > oh ? H : oh) * (W > ow ? W : ow);
+  if (big >= (1ll << 31) || (int64_t)c_o * c_i * s * s >= (1ll << 31))
+    return pb_set_error(PB_ERR_GEOMETRY, "conv tensor too large for 32-bit indexing");
+  switch (s) {  // tiled implicit GEMM for the kernel sizes the models use
+    case 1: conv_gemm_launch<1>(kind, d, a, b, m, out, st); PB_CHECK_LAUNCH(); return PB_OK;
+    case 3: conv_gemm_launch<3>(kind, d, a, b, m, out, st); PB_CHECK_LAUNCH(); return PB_OK;
+    case 5: conv_gemm_launch<5>(kind, d, a, b, m, out, st); PB_CHECK_LAUNCH(); return PB_OK;
+    default: break;
+  }
   switch (kind) {
     case PB_CONV_FWD: {
       const int64_t n = (int64_t)B * c_o * oh * ow;

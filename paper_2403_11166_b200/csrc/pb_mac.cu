@@ -44,8 +44,8 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   extern __shared__ uint32_t sm[];
   const int tid = threadIdx.x;
   const int L = P.L;
-  const int64_t p = blockIdx.x / L;
-  const int l = blockIdx.x % L;
+  const int l = (int)(blockIdx.x / nP);  // limb-major: co-resident CTAs share one limb's twiddles
+  const int64_t p = blockIdx.x % nP;
   const uint32_t q = P.q[l];
   const uint64_t mu = P.mu[l];
   const uint32_t tm = P.tmod[l];
@@ -69,8 +69,8 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   extern __shared__ uint32_t sm[];
   const int tid = threadIdx.x;
   const int L = P.L;
-  const int64_t p = blockIdx.x / L;
-  const int l = blockIdx.x % L;
+  const int l = (int)(blockIdx.x / nP);  // limb-major: co-resident CTAs share one limb's twiddles
+  const int64_t p = blockIdx.x % nP;
   const uint32_t q = P.q[l];
   if (filler) {
     const uint64_t fseed = dev_key(filler_arg, seed_dev);

@@ -19,6 +19,11 @@
 
 #include "pb_common.cuh"
 
+// Min CTAs per SM for a row-per-CTA NTT kernel so that its register budget is
+// 64 (32 residues + 16 twiddle pairs per thread fit; more registers cost
+// occupancy -- measured slower on B200).
+#define NTT_MINB(LOGN) ((1 << ((LOGN) - 5)) >= 1024 ? 1 : 1024 / (1 << ((LOGN) - 5)))
+
 namespace pb {
 
 __device__ __forceinline__ void ct_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t q, uint32_t q2) {

@@ -156,7 +156,8 @@ class Session:
         self._shards = {}
         self.graph_mode = False
         self._seed_dev = None
-        self._streams = None
+        self._streams = {}
+        self._grad_stream = None
 
     def rng(self, layer: int, op: int, purpose: int) -> SeededRng:
         g = SeededRng(self.seed, stream_id(layer, op, purpose))
@@ -181,9 +182,19 @@ class Session:
         self.graph_mode = True
 
     def _side_streams(self):
-        if self._streams is None:
-            self._streams = (torch.cuda.Stream(), torch.cuda.Stream())
-        return self._streams
+        """The (DO encrypt, MO encode) side streams forked by he_eval, one pair
+        per calling stream so concurrent protocol calls do not serialise."""
+        key = torch.cuda.current_stream().cuda_stream
+        if key not in self._streams:
+            self._streams[key] = (torch.cuda.Stream(), torch.cuda.Stream())
+        return self._streams[key]
+
+    def grad_stream(self) -> torch.cuda.Stream:
+        """Stream the training step runs weight-gradient protocols on, concurrently
+        with the input-gradient chain (they are independent given grad Y)."""
+        if self._grad_stream is None:
+            self._grad_stream = torch.cuda.Stream()
+        return self._grad_stream
 
     def _count(self, name, nbytes):
         if _lib.STATS is not None:

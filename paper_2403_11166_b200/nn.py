@@ -218,17 +218,25 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
     gy_do = ShareTensor(DO, RingTensor(g_do, f, ring, _canonical=True))
     gy_mo = ShareTensor(MO, RingTensor(torch.zeros_like(g_do), f, ring, _canonical=True))
     gws, gbs = [None] * L, [None] * L
+    # The weight-gradient protocols (bias reveal + Alg.2) of layer l and the
+    # input-gradient chain to layer l-1 are independent given grad Y_l: Alg.2
+    # runs on the session's grad stream, overlapping the chain on this stream.
+    main, gstream = torch.cuda.current_stream(), sess.grad_stream()
+    keep = []  # grad Y shares read on the grad stream stay referenced until the join
     for l in reversed(range(L)):
         e = model.layers[model.lin[l]]
         last = l == L - 1
-        if e[0] == "fc":
-            gbs[l] = reveal_grad_bias(sess, l, gy_mo, gy_do)
-            gw = grad_weight(sess, l, *acts[l], gy_mo, gy_do, mo_x_zero=(l == 0), mo_gy_zero=last)
-        else:
-            gbs[l] = reveal_grad_bias_conv(sess, l, gy_mo, gy_do)
-            gw = conv_grad_weight(sess, l, *acts[l], gy_mo, gy_do, e[3], e[4], e[5], mo_x_zero=(l == 0),
-                                  mo_gy_zero=last)
-        gws[l] = arith_shift(gw, f)
+        gstream.wait_stream(main)
+        with torch.cuda.stream(gstream):
+            if e[0] == "fc":
+                gbs[l] = reveal_grad_bias(sess, l, gy_mo, gy_do)
+                gw = grad_weight(sess, l, *acts[l], gy_mo, gy_do, mo_x_zero=(l == 0), mo_gy_zero=last)
+            else:
+                gbs[l] = reveal_grad_bias_conv(sess, l, gy_mo, gy_do)
+                gw = conv_grad_weight(sess, l, *acts[l], gy_mo, gy_do, e[3], e[4], e[5], mo_x_zero=(l == 0),
+                                      mo_gy_zero=last)
+            gws[l] = arith_shift(gw, f)
+        keep.append((gy_mo, gy_do))
         if trace is not None:
             trace.append((l, ys[l], gbs[l], gws[l]))
         if l > 0:
@@ -245,6 +253,8 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
                     chw = model.io[k][0]
                     t_mo, t_do = _unflatten(t_mo, chw), _unflatten(t_do, chw)
             gy_mo, gy_do = relu_backward(sess, l - 1, ds[l - 1], t_mo, t_do)
+    main.wait_stream(gstream)
+    del keep
     model.sgd(gws, gbs, lr, momentum, check=check)
     return gws, gbs
 
