@@ -130,7 +130,7 @@ def check(status: int, what: str = "") -> None:
 
 # Device kernels each entry point launches (for the bench's gpu_launches count).
 KERNELS_PER_CALL = {
-    "pb_encrypt_pk": 2, "pb_encrypt_sk": 2, "pb_decrypt": 2, "pb_decrypt_to_share": 2, "pb_unpack": 1,
+    "pb_encrypt_pk": 2, "pb_encrypt_sk": 1, "pb_decrypt": 2, "pb_decrypt_to_share": 2, "pb_unpack": 1,
     "pb_abi_version": 0, "pb_last_error": 0, "pb_device_sm_count": 0, "pb_ctx_create": 0, "pb_ctx_destroy": 0,
 }
 

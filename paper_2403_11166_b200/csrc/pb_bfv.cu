@@ -34,9 +34,23 @@ __device__ __forceinline__ void load_source(uint32_t (&a)[32], uint32_t* sm, con
     __syncthreads();
     const int32_t* pp = s.pos + p * s.Z;
     const int32_t* ps = s.src + p * s.Z;
-    for (int z = tid; z < s.Z; z += Nt::T) {
-      const int j = __ldg(pp + z);
-      if (j >= 0) sm[Nt::pad(j)] = lift(__ldg(s.vals + __ldg(ps + z)));
+    // batches of 8 slots per thread: all position / source loads are issued
+    // before the dependent value loads (a per-slot pos -> src -> value chain
+    // serialises three L2 round trips per slot)
+    for (int z0 = tid; z0 < s.Z; z0 += 8 * Nt::T) {
+      int j[8], si[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int z = z0 + u * Nt::T;
+        j[u] = z < s.Z ? __ldg(pp + z) : -1;
+        si[u] = z < s.Z ? __ldg(ps + z) : 0;
+      }
+      uint64_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = j[u] >= 0 ? __ldg(s.vals + si[u]) : 0ull;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j[u] >= 0) sm[Nt::pad(j[u])] = lift(v[u]);
     }
     __syncthreads();
     Nt::ld1(sm, a, tid);
@@ -206,11 +220,22 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
   const int64_t p = blockIdx.x % nP;
   const uint32_t q = P.q[l];
   const uint64_t mu = P.mu[l];
-  const int8_t* ep = e + p * N;
+  const int8_t* ep = e ? e + p * N : nullptr;
   uint32_t b[32];
   load_source<Nt>(b, sm, src, p, tid, [&](uint64_t v) { return delta_m(P, l, v); });
+  if (ep) {  // caller-supplied noise (bit-exact oracle runs)
 #pragma unroll
-  for (int c = 0; c < 32; ++c) b[c] = addmod(lift_small(ep[Nt::j1(tid, c)], q), b[c], q);
+    for (int c = 0; c < 32; ++c) b[c] = addmod(lift_small(ep[Nt::j1(tid, c)], q), b[c], q);
+  } else {  // e ~ CBD(20) from Philox4x32, generated in-kernel: one call covers coefficients j and j+T
+    const uint64_t pp = (uint64_t)p + nonce;
+#pragma unroll
+    for (int c = 0; c < 32; c += 2) {
+      const u32x4 r = philox4x32_10((uint32_t)Nt::j1(tid, c), (uint32_t)pp, (uint32_t)(pp >> 32), 0x454e4333u /* "ENC3" */,
+                                    (uint32_t)seed, (uint32_t)(seed >> 32));
+      b[c] = addmod(lift_small(cbd20(r.v[0], r.v[1]), q), b[c], q);
+      b[c + 1] = addmod(lift_small(cbd20(r.v[2], r.v[3]), q), b[c + 1], q);
+    }
+  }
   Nt::forward(b, sm, P.tw_fwd + (size_t)l * N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
   // c1 = a, c0 = NTT(e + Delta m) - a*s, one 128-bit device-order vector at a
   // time (keeps a and s out of the register file: 32 live residues, not 96)
@@ -274,9 +299,13 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
     __syncthreads();
     const int32_t* pos = out_pos + p * U;
     uint32_t* dst = out32 + (p * L + l) * U;
-    for (int u = tid; u < U; u += Nt::T) {
-      const int j = pos[u];
-      if (j >= 0) dst[u] = mul_shoup(sm[Nt::pad(j)], ni, nis, q);
+    for (int u0 = tid; u0 < U; u0 += 8 * Nt::T) {  // batched position loads
+      int j[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) j[k] = u0 + k * Nt::T < U ? __ldg(pos + u0 + k * Nt::T) : -1;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (j[k] >= 0) dst[u0 + k * Nt::T] = mul_shoup(sm[Nt::pad(j[k])], ni, nis, q);
     }
   }
 }
@@ -484,19 +513,6 @@ int make_pack(const uint64_t* vals, const int32_t* pos, const int32_t* src, int3
 
 // Scratch for device-sampled noise: a per-thread cached buffer reused
 // across calls (stream-ordered use only).
-thread_local int8_t* g_noise = nullptr;
-thread_local size_t g_noise_bytes = 0;
-int8_t* noise_buffer(size_t bytes) {
-  if (bytes > g_noise_bytes) {
-    if (g_noise) cudaFree(g_noise);
-    g_noise = nullptr;
-    g_noise_bytes = 0;
-    if (cudaMalloc(&g_noise, bytes) != cudaSuccess) return nullptr;
-    g_noise_bytes = bytes;
-  }
-  return g_noise;
-}
-
 }  // namespace
 
 // ================================================================ C ABI ===
@@ -557,13 +573,16 @@ extern "C" int pb_encrypt_pk(const pb_ctx* ctx, const uint32_t* pk, const uint64
   if (int s = need_big_n(ctx)) return s;
   if (nP <= 0) return PB_OK;
   const int N = ctx->dev.N;
-  int8_t* buf = noise_buffer((size_t)nP * N * 3);
-  if (!buf) return pb_set_error(PB_ERR_CUDA, "noise scratch allocation failed");
-  int8_t *u = buf, *e1 = buf + nP * N, *e2 = buf + 2 * nP * N;
   cudaStream_t st = pb_stream_of(stream);
+  int8_t* buf = nullptr;  // stream-ordered scratch: safe under concurrent streams and graph capture
+  if (cudaMallocAsync((void**)&buf, (size_t)nP * N * 3, st) != cudaSuccess)
+    return pb_set_error(PB_ERR_CUDA, "noise scratch allocation failed");
+  int8_t *u = buf, *e1 = buf + nP * N, *e2 = buf + 2 * nP * N;
   k_sample_noise<<<pb_grid_1d(nP * N, 256), 256, 0, st>>>(N, nP, seed, seed_dev, nonce, 1, u, e1, e2);
   PB_CHECK_LAUNCH();
-  return pb_encrypt_pk_noise(ctx, pk, vals, pack_pos, pack_src, Z, nP, u, e1, e2, ct, stream);
+  const int rc = pb_encrypt_pk_noise(ctx, pk, vals, pack_pos, pack_src, Z, nP, u, e1, e2, ct, stream);
+  cudaFreeAsync(buf, st);
+  return rc;
 }
 
 extern "C" int pb_encrypt_sk_noise(const pb_ctx* ctx, const uint32_t* sk, const uint64_t* vals,
@@ -588,14 +607,9 @@ extern "C" int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk, const uint64
   if (!sk || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
   if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
   PB_PACK_OR_RETURN(src, vals, pack_pos, pack_src, Z);
-  const int N = ctx->dev.N;
-  int8_t* e = noise_buffer((size_t)nP * N);
-  if (!e) return pb_set_error(PB_ERR_CUDA, "noise scratch allocation failed");
   cudaStream_t st = pb_stream_of(stream);
-  k_sample_noise<<<pb_grid_1d(nP * N, 256), 256, 0, st>>>(N, nP, seed, seed_dev, nonce, 0, nullptr, e, nullptr);
-  PB_CHECK_LAUNCH();
-  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, src, nP, (const uint32_t*)nullptr, e, seed, seed_dev,
-                   nonce, ct, st);
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, src, nP, (const uint32_t*)nullptr,
+                   (const int8_t*)nullptr, seed, seed_dev, nonce, ct, st);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }

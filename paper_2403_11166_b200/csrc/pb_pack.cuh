@@ -27,9 +27,23 @@ __device__ __forceinline__ void load_source(uint32_t (&a)[32], uint32_t* sm, con
     __syncthreads();
     const int32_t* pp = s.pos + p * s.Z;
     const int32_t* ps = s.src + p * s.Z;
-    for (int z = tid; z < s.Z; z += Nt::T) {
-      const int j = __ldg(pp + z);
-      if (j >= 0) sm[Nt::pad(j)] = lift(__ldg(s.vals + __ldg(ps + z)));
+    // batches of 8 slots per thread: all position / source loads are issued
+    // before the dependent value loads (a per-slot pos -> src -> value chain
+    // serialises three L2 round trips per slot)
+    for (int z0 = tid; z0 < s.Z; z0 += 8 * Nt::T) {
+      int j[8], si[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int z = z0 + u * Nt::T;
+        j[u] = z < s.Z ? __ldg(pp + z) : -1;
+        si[u] = z < s.Z ? __ldg(ps + z) : 0;
+      }
+      uint64_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = j[u] >= 0 ? __ldg(s.vals + si[u]) : 0ull;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j[u] >= 0) sm[Nt::pad(j[u])] = lift(v[u]);
     }
     __syncthreads();
     Nt::ld1(sm, a, tid);
