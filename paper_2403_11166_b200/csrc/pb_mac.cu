@@ -7,13 +7,16 @@
 //   k_mask_ntt    one CTA per (output, limb): builds Delta*(mask + filler) in
 //                 shared memory, forward NTT in registers, writes -mask into
 //                 the output's c0 row (device order);
-//   k_mac_tiled   a TB x TO tile of outputs per CTA and a 512-coefficient
-//                 slice of one limb: every ciphertext / plaintext vector is
-//                 loaded once per tile (TB*TO/(TB+TO)-fold reuse instead of
-//                 one reload per output), multiplied in Montgomery form (the
-//                 plaintexts are stored as pt*2^32 mod q, so no Shoup
-//                 companion row is streamed), accumulated in registers and
-//                 written once.
+//   k_mac_pipe    (nI >= 3) a 2x2 tile of outputs per CTA and a 512-coefficient
+//                 slice of one limb: per input block the operand row slices
+//                 are copied into a 3-stage shared-memory ring by the TMA
+//                 engine (cp.async.bulk + mbarrier), every ct / pt vector is
+//                 reused across the tile, products accumulate lazily in u64
+//                 (one IMAD.WIDE per mod-MAC), written once;
+//   k_mac_eager   (nI <= 2) the same tile from registers with per-term
+//                 Montgomery reduction (nothing to amortise a lazy reduction).
+// Plaintexts are stored in Montgomery form (pt*2^32 mod q), so no Shoup
+// companion row is streamed.
 #include "pb_pack.cuh"
 
 namespace {
@@ -135,24 +138,41 @@ template <> struct Vec<2> {
   __device__ __forceinline__ static T zero() { return make_uint2(0, 0); }
 };
 
-// TB x TO output ciphertexts per CTA, V coefficients per thread: every
-// ciphertext vector is loaded once per tile and reused TO times, every
-// plaintext vector reused 2*TB times (c0 and c1).
-//
-// Lazy 64-bit accumulation: a product x * w~ (x < q, w~ = w 2^32 mod q, both
-// < 2^30) is < 2^60, so 14 products plus a reduced residue (< 2^30) fit a u64
-// -- a mod-MAC is ONE IMAD.WIDE.U32 (fma pipe) instead of a Montgomery
-// multiply + two conditional subtractions (alu pipe, which bound the eager
-// version: ncu alu 56%, math-pipe-throttle stalls).  The accumulator is
-// Barrett-reduced every MAC_CHUNK input blocks and once at the end, where one
-// Montgomery step removes the plaintexts' 2^32 factor.
+// Lazy 64-bit accumulation (used by k_mac_pipe): a product x * w~ (x < q,
+// w~ = w 2^32 mod q, both < 2^30) is < 2^60, so 14 products plus a reduced
+// residue (< 2^30) fit a u64 -- a mod-MAC is ONE IMAD.WIDE.U32 (fma pipe)
+// instead of a Montgomery multiply + two conditional subtractions (alu pipe,
+// which bound the eager kernel: ncu alu 56%, math-pipe-throttle stalls).  The
+// accumulator is Barrett-reduced every MAC_CHUNK input blocks and once at the
+// end, where one Montgomery step removes the plaintexts' 2^32 factor.
 constexpr int MAC_CHUNK = 7;  // k-steps per reduction (2 terms x 7 = 14 products)
 
-template <int TB, int TO, int V, int MINB>
+// TMA-pipelined lazy MAC.  A CTA owns a 2x2 output tile and a 512-coefficient
+// slice of one limb; per input block k its operands are 2-KB contiguous row
+// slices (ct c0/c1 per batch block, pt per output block, and the same for the
+// second cross term), copied into a STAGES-deep shared-memory ring by the TMA
+// engine (cp.async.bulk + mbarrier) while the CTA multiplies the previous
+// stages -- the L2 latency that bounded the register-load kernel is off the
+// critical path, and the math is one IMAD.WIDE.U32 per mod-MAC.
+
+template <int TB, int TO, int V>
+struct PipeCfg {
+  static constexpr int SLOT = MAC_THREADS * V * 4;  // bytes per operand slice
+  static constexpr int SLOTS_A = 2 * TB + TO;       // ct c0/c1 per batch block + pt per output block
+  static constexpr int SLOTS_B = 2 * TO + TB;
+};
+
+template <int TB, int TO, int V, int STAGES, int MINB = 1>
 __global__ void __launch_bounds__(MAC_THREADS, MINB)
-    k_mac_tiled(PbDev P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB, int nB,
-                int nO, int nI, uint32_t* ct_out) {
+    k_mac_pipe(PbDev P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB, int nB,
+               int nO, int nI, uint32_t* ct_out) {
+  using C = PipeCfg<TB, TO, V>;
   using VT = typename Vec<V>::T;
+  extern __shared__ __align__(128) uint8_t pipe_sm[];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  // compact slot map per stage: [A: ct(b,c) 2*TB, pt(o) TO][B: ct(o,c) 2*TO, pt(b) TB], absent terms take no space
+  const int CA = 0, PA = 2 * TB, CB = ctA ? C::SLOTS_A : 0, PB = CB + 2 * TO;
+  const int nslots = (ctA ? C::SLOTS_A : 0) + (ctB ? C::SLOTS_B : 0);
   const int N = P.N, L = P.L;
   const int slices = N / (V * MAC_THREADS);
   const int tilesO = (nO + TO - 1) / TO;
@@ -160,12 +180,57 @@ __global__ void __launch_bounds__(MAC_THREADS, MINB)
   const int l = blockIdx.y / slices, sl = blockIdx.y % slices;
   const uint32_t q = P.q[l], qn = P.qn[l];
   const uint64_t mu = P.mu[l];
-  const size_t row = (size_t)N / V;  // vectors per row
-  const size_t v = (size_t)sl * MAC_THREADS + threadIdx.x;
-  const VT* cA = reinterpret_cast<const VT*>(ctA);
-  const VT* pA = reinterpret_cast<const VT*>(ptA);
-  const VT* cB = reinterpret_cast<const VT*>(ctB);
-  const VT* pB = reinterpret_cast<const VT*>(ptB);
+  const int tid = threadIdx.x;
+  const size_t rowb = (size_t)N * 4;        // bytes per residue row
+  const size_t off = (size_t)sl * C::SLOT;  // byte offset of this slice in a row
+  bool okb[TB], oko[TO];
+#pragma unroll
+  for (int i = 0; i < TB; ++i) okb[i] = tb * TB + i < nB;
+#pragma unroll
+  for (int o = 0; o < TO; ++o) oko[o] = to * TO + o < nO;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  auto issue = [&](int k, int s) {
+    const uint8_t* A8 = reinterpret_cast<const uint8_t*>(ctA);
+    const uint8_t* PA8 = reinterpret_cast<const uint8_t*>(ptA);
+    const uint8_t* B8 = reinterpret_cast<const uint8_t*>(ctB);
+    const uint8_t* PB8 = reinterpret_cast<const uint8_t*>(ptB);
+    uint8_t* st = pipe_sm + (size_t)s * nslots * C::SLOT;
+    uint32_t n = 0;
+#pragma unroll
+    for (int i = 0; i < TB; ++i) n += (okb[i] ? 1u : 0u) * ((ctA ? 2u : 0u) + (ctB ? 1u : 0u));
+#pragma unroll
+    for (int o = 0; o < TO; ++o) n += (oko[o] ? 1u : 0u) * ((ctA ? 1u : 0u) + (ctB ? 2u : 0u));
+    mbar_expect_tx(&full[s], n * C::SLOT);
+#pragma unroll
+    for (int i = 0; i < TB; ++i) {
+      if (!okb[i]) continue;
+      const size_t bi = (size_t)((tb * TB + i) * nI + k);
+      if (ctA) {
+        bulk_g2s(st + (CA + 2 * i) * C::SLOT, A8 + ((bi * 2 + 0) * L + l) * rowb + off, C::SLOT, &full[s]);
+        bulk_g2s(st + (CA + 2 * i + 1) * C::SLOT, A8 + ((bi * 2 + 1) * L + l) * rowb + off, C::SLOT, &full[s]);
+      }
+      if (ctB) bulk_g2s(st + (PB + i) * C::SLOT, PB8 + (bi * L + l) * rowb + off, C::SLOT, &full[s]);
+    }
+#pragma unroll
+    for (int o = 0; o < TO; ++o) {
+      if (!oko[o]) continue;
+      const size_t oi = (size_t)((to * TO + o) * nI + k);
+      if (ctA) bulk_g2s(st + (PA + o) * C::SLOT, PA8 + (oi * L + l) * rowb + off, C::SLOT, &full[s]);
+      if (ctB) {
+        bulk_g2s(st + (CB + 2 * o) * C::SLOT, B8 + ((oi * 2 + 0) * L + l) * rowb + off, C::SLOT, &full[s]);
+        bulk_g2s(st + (CB + 2 * o + 1) * C::SLOT, B8 + ((oi * 2 + 1) * L + l) * rowb + off, C::SLOT, &full[s]);
+      }
+    }
+  };
+  if (tid == 0)
+    for (int k = 0; k < STAGES - 1 && k < nI; ++k) issue(k, k);
+
   uint64_t acc[TB][TO][2][V];
 #pragma unroll
   for (int i = 0; i < TB; ++i)
@@ -175,60 +240,42 @@ __global__ void __launch_bounds__(MAC_THREADS, MINB)
       for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int e = 0; e < V; ++e) acc[i][o][c][e] = 0ull;
-  bool okb[TB], oko[TO];
-#pragma unroll
-  for (int i = 0; i < TB; ++i) okb[i] = tb * TB + i < nB;
-#pragma unroll
-  for (int o = 0; o < TO; ++o) oko[o] = to * TO + o < nO;
-
-  auto macv = [&](uint64_t (&a)[V], const VT& x, const VT& w) {
+  auto mac = [&](uint64_t (&a)[V], const VT& x, const VT& w) {
 #pragma unroll
     for (int e = 0; e < V; ++e) a[e] += (uint64_t)Vec<V>::get(x, e) * Vec<V>::get(w, e);
   };
-  const VT z = Vec<V>::zero();
-  for (int k0 = 0; k0 < nI; k0 += MAC_CHUNK) {
-    const int k1 = min(nI, k0 + MAC_CHUNK);
-    for (int k = k0; k < k1; ++k) {
-      if (cA) {  // term A: ctA[b-block] (*) ptA[o-block]
-        VT x0[TB], x1[TB], w[TO];
+  constexpr int SV = C::SLOT / (4 * V);  // vectors per slot
+  for (int k = 0; k < nI; ++k) {
+    const int s = k % STAGES;
+    if (tid == 0 && k + STAGES - 1 < nI) {
+      fence_proxy_async_smem();
+      issue(k + STAGES - 1, (k + STAGES - 1) % STAGES);
+    }
+    mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
+    const VT* st = reinterpret_cast<const VT*>(pipe_sm + (size_t)s * nslots * C::SLOT) + tid;
+    if (ctA) {
+      VT w[TO];
 #pragma unroll
-        for (int i = 0; i < TB; ++i) {
-          const size_t base = ((size_t)((tb * TB + i) * nI + k) * 2 * L + l) * row + v;
-          x0[i] = okb[i] ? __ldg(cA + base) : z;
-          x1[i] = okb[i] ? __ldg(cA + base + (size_t)L * row) : z;
-        }
+      for (int o = 0; o < TO; ++o) w[o] = st[(PA + o) * SV];
 #pragma unroll
-        for (int o = 0; o < TO; ++o)
-          w[o] = oko[o] ? __ldg(pA + ((size_t)((to * TO + o) * nI + k) * L + l) * row + v) : z;
+      for (int i = 0; i < TB; ++i) {
+        const VT x0 = st[(CA + 2 * i) * SV], x1 = st[(CA + 2 * i + 1) * SV];
 #pragma unroll
-        for (int i = 0; i < TB; ++i)
-#pragma unroll
-          for (int o = 0; o < TO; ++o) {
-            macv(acc[i][o][0], x0[i], w[o]);
-            macv(acc[i][o][1], x1[i], w[o]);
-          }
-      }
-      if (cB) {  // term B: ctB[o-block] (*) ptB[b-block]
-        VT y0[TO], y1[TO], u[TB];
-#pragma unroll
-        for (int o = 0; o < TO; ++o) {
-          const size_t base = ((size_t)((to * TO + o) * nI + k) * 2 * L + l) * row + v;
-          y0[o] = oko[o] ? __ldg(cB + base) : z;
-          y1[o] = oko[o] ? __ldg(cB + base + (size_t)L * row) : z;
-        }
-#pragma unroll
-        for (int i = 0; i < TB; ++i)
-          u[i] = okb[i] ? __ldg(pB + ((size_t)((tb * TB + i) * nI + k) * L + l) * row + v) : z;
-#pragma unroll
-        for (int i = 0; i < TB; ++i)
-#pragma unroll
-          for (int o = 0; o < TO; ++o) {
-            macv(acc[i][o][0], y0[o], u[i]);
-            macv(acc[i][o][1], y1[o], u[i]);
-          }
+        for (int o = 0; o < TO; ++o) { mac(acc[i][o][0], x0, w[o]); mac(acc[i][o][1], x1, w[o]); }
       }
     }
-    if (k1 < nI) {  // fold back below q so the next chunk cannot overflow
+    if (ctB) {
+      VT u[TB];
+#pragma unroll
+      for (int i = 0; i < TB; ++i) u[i] = st[(PB + i) * SV];
+#pragma unroll
+      for (int o = 0; o < TO; ++o) {
+        const VT y0 = st[(CB + 2 * o) * SV], y1 = st[(CB + 2 * o + 1) * SV];
+#pragma unroll
+        for (int i = 0; i < TB; ++i) { mac(acc[i][o][0], y0, u[i]); mac(acc[i][o][1], y1, u[i]); }
+      }
+    }
+    if ((k + 1) % MAC_CHUNK == 0 && k + 1 < nI) {  // fold below q: the next 7 blocks cannot overflow
 #pragma unroll
       for (int i = 0; i < TB; ++i)
 #pragma unroll
@@ -238,9 +285,12 @@ __global__ void __launch_bounds__(MAC_THREADS, MINB)
 #pragma unroll
             for (int e = 0; e < V; ++e) acc[i][o][c][e] = reduce64(acc[i][o][c][e], q, mu);
     }
+    __syncthreads();  // stage s fully consumed before it is refilled
   }
   auto fin = [&](uint64_t a) { return csub(mont_lazy(reduce64(a, q, mu), 1u, q, qn), q); };  // x 2^-32 mod q
   VT* out = reinterpret_cast<VT*>(ct_out);
+  const size_t row = (size_t)N / V;
+  const size_t v = (size_t)sl * MAC_THREADS + tid;
 #pragma unroll
   for (int i = 0; i < TB; ++i)
 #pragma unroll
@@ -258,6 +308,21 @@ __global__ void __launch_bounds__(MAC_THREADS, MINB)
       out[b0] = Vec<V>::make(c0);
       out[b0 + (size_t)L * row] = Vec<V>::make(c1);
     }
+}
+
+template <int TB, int TO, int V, int STAGES, int MINB = 1>
+void launch_pipe(const PbDev& P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB,
+                 int nB, int nO, int nI, uint32_t* out, cudaStream_t st) {
+  using C = PipeCfg<TB, TO, V>;
+  const size_t smem = (size_t)STAGES * ((ctA ? C::SLOTS_A : 0) + (ctB ? C::SLOTS_B : 0)) * C::SLOT;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mac_pipe<TB, TO, V, STAGES, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((size_t)STAGES * (C::SLOTS_A + C::SLOTS_B) * C::SLOT));
+    attr = true;
+  }
+  dim3 grid((unsigned)(((nB + TB - 1) / TB) * ((nO + TO - 1) / TO)), (unsigned)(P.L * (P.N / (V * MAC_THREADS))));
+  k_mac_pipe<TB, TO, V, STAGES, MINB><<<grid, MAC_THREADS, smem, st>>>(P, ctA, ptA, ctB, ptB, nB, nO, nI, out);
 }
 
 // Eager variant (Montgomery multiply + reduce per term, u32 accumulators,
@@ -427,9 +492,8 @@ extern "C" int pb_ctpt_mac_tiled(const pb_ctx* ctx, const uint32_t* ctA, const u
   if (nI <= 2) {
     dim3 grid(tiles, (unsigned)(L * (N / (4 * MAC_THREADS))));
     k_mac_eager<2, 2><<<grid, MAC_THREADS, 0, st>>>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out);
-  } else {  // measured on B200: K=16 conv-like 1.09 -> 0.90 ms, FC 784x128 fwd 75 -> 66 us
-    dim3 grid(tiles, (unsigned)(L * (N / (4 * MAC_THREADS))));
-    k_mac_tiled<2, 2, 4, 1><<<grid, MAC_THREADS, 0, st>>>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out);
+  } else {  // TMA-pipelined lazy MAC: K=16 conv-like 1.09 -> 0.65 ms, FC 784x128 fwd 75 -> 48 us (B200)
+    launch_pipe<2, 2, 4, 3, 6>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
   }
   PB_CHECK_LAUNCH();
   return PB_OK;
