@@ -299,10 +299,11 @@ int conv_gemm_launch(int kind, const ConvDims& d, const uint64_t* a, const uint6
   else if (kind == PB_CONV_BWDX) { M = d.ci; N = (int64_t)d.B * d.H * d.W; K = (int64_t)d.co * S * S; }
   else { M = d.co; N = (int64_t)d.ci * S * S; K = (int64_t)d.B * d.oh * d.ow; }
   const int64_t tiles = ((M + 63) / 64) * ((N + 63) / 64);
+  // split K until ~2 waves of 3 resident CTAs per SM are filled (GRADW has a tiny
+  // M x N and K = B*oh*ow; the forward / input-gradient GEMMs of a 64-channel
+  // layer have only 256 tiles) while keeping >= 128 K per split
   int splits = 1;
-  if (kind == PB_CONV_GRADW) {  // fill ~2 waves of 148 SMs, >= 256 K per split
-    while (tiles * splits < 2 * 148 * 2 && K / (splits * 2) >= 256) splits *= 2;
-  }
+  while (tiles * splits < 2 * 148 * 3 && K / (splits * 2) >= 128) splits *= 2;
   const int64_t kps = ((K + splits - 1) / splits + 15) / 16 * 16;
   dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)splits);
   if (splits > 1) cudaMemsetAsync(out, 0, (size_t)(M * N) * sizeof(uint64_t), st);

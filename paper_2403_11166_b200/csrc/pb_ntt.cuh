@@ -47,7 +47,11 @@ struct Ntt {
   static constexpr int N = 1 << LOGN;
   static constexpr int T = N >> 5;
   static constexpr int M = LOGN - 10;
-  static constexpr int SMEM_WORDS = N + (N >> 5);
+  // exchange area (padded row) + the staged twiddles of stages 0..LOGN-6
+  // (tw[1 .. T-1], one uint2 per thread, shared by all threads of the row)
+  static constexpr int TW_OFF = N + (N >> 5);
+  static constexpr int SMEM_WORDS = TW_OFF + 2 * T;
+  __device__ __forceinline__ static uint2* stw(uint32_t* sm) { return reinterpret_cast<uint2*>(sm + TW_OFF); }
 
   __device__ __forceinline__ static int pad(int j) { return j + (j >> 5); }
 
@@ -120,7 +124,7 @@ struct Ntt {
       const int tc = 16 >> s;
       uint2 w[16];
 #pragma unroll
-      for (int g = 0; g < (1 << s); ++g) w[g] = __ldg(tw + (1 << s) + g);
+      for (int g = 0; g < (1 << s); ++g) w[g] = tw[(1 << s) + g];  // shared memory
 #pragma unroll
       for (int c = 0; c < 32; ++c)
         if (!(c & tc)) ct_bfly(a[c], a[c + tc], w[c >> (5 - s)], q, q2);
@@ -135,7 +139,7 @@ struct Ntt {
       const uint2* wb = tw + (1 << s) + (warp << (s + 10 - LOGN));
 #pragma unroll
       for (int c = 0; c < 32; ++c)
-        if (!(c & tc)) ct_bfly(a[c], a[c + tc], __ldg(wb + (fc2(c) >> (LOGN - s))), q, q2);
+        if (!(c & tc)) ct_bfly(a[c], a[c + tc], wb[fc2(c) >> (LOGN - s)], q, q2);
     }
   }
   template <int D>
@@ -162,11 +166,17 @@ struct Ntt {
   // SMEM_WORDS words; the caller syncs before reusing it.
   __device__ __forceinline__ static void forward(uint32_t (&a)[32], uint32_t* sm, const uint2* tw,
                                                  const uint2* t3, int tid, uint32_t q) {
-    fwd_p1(a, tw, q);
+    // P1/P2 twiddles from shared memory: one coalesced load per thread instead of
+    // just-in-time L1/L2 loads before every early stage (ncu: ~50% of the stall
+    // samples sat in the P1 stages)
+    uint2* st = stw(sm);
+    st[tid] = __ldg(tw + tid);
+    __syncthreads();
+    fwd_p1(a, st, q);
     st1(sm, a, tid);
     __syncthreads();
     ld2(sm, a, tid);
-    fwd_p2(a, tw, tid, q);
+    fwd_p2(a, st, tid, q);
     __syncthreads();
     st2(sm, a, tid);
     __syncthreads();
@@ -203,7 +213,7 @@ struct Ntt {
       const uint2* wb = tw + (1 << s) + (warp << (s + 10 - LOGN));
 #pragma unroll
       for (int c = 0; c < 32; ++c)
-        if (!(c & tc)) gs_bfly(a[c], a[c + tc], __ldg(wb + (fc2(c) >> (LOGN - s))), q, q2);
+        if (!(c & tc)) gs_bfly(a[c], a[c + tc], wb[fc2(c) >> (LOGN - s)], q, q2);
     }
   }
   __device__ __forceinline__ static void inv_p1(uint32_t (&a)[32], const uint2* tw, uint32_t q) {
@@ -214,7 +224,7 @@ struct Ntt {
       const int tc = 16 >> s;
       uint2 w[16];
 #pragma unroll
-      for (int g = 0; g < (1 << s); ++g) w[g] = __ldg(tw + (1 << s) + g);
+      for (int g = 0; g < (1 << s); ++g) w[g] = tw[(1 << s) + g];  // shared memory
 #pragma unroll
       for (int c = 0; c < 32; ++c)
         if (!(c & tc)) gs_bfly(a[c], a[c + tc], w[c >> (5 - s)], q, q2);
@@ -225,16 +235,18 @@ struct Ntt {
   // [0, 2q) on entry, P1 layout with values in [0, 2q) on exit.
   __device__ __forceinline__ static void inverse(uint32_t (&a)[32], uint32_t* sm, const uint2* tw,
                                                  const uint2* t3, int tid, uint32_t q) {
+    uint2* st = stw(sm);
+    st[tid] = __ldg(tw + tid);  // consumed after the next barrier (P2/P1)
     inv_p3(a, t3, tid, q);
     st3(sm, a, tid);
     __syncthreads();
     ld2(sm, a, tid);
-    inv_p2(a, tw, tid, q);
+    inv_p2(a, st, tid, q);
     __syncthreads();
     st2(sm, a, tid);
     __syncthreads();
     ld1(sm, a, tid);
-    inv_p1(a, tw, q);
+    inv_p1(a, st, q);
   }
 
   // ---- NTT-domain rows in DEVICE ORDER: bit-reversed index j = tid*32 + 4v + k

@@ -171,3 +171,63 @@ extern "C" int exp_occupancy(int variant, int minb) {
   }
   return occ;
 }
+
+// ---- wide NTT (pb_nttw.cuh) experiments ----
+#include "../paper_2403_11166_b200/csrc/pb_nttw.cuh"
+namespace {
+template <int LOGN, int LOGV>
+__global__ void __launch_bounds__(1 << (LOGN - LOGV)) k_wfwd(PbDev P, uint32_t* rows, int64_t n_rows) {
+  using W = pb::NttW<LOGN, LOGV>;
+  extern __shared__ uint32_t sm[];
+  const int tid = threadIdx.x;
+  for (int64_t r = blockIdx.x; r < n_rows; r += gridDim.x) {
+    const int limb = (int)(r % P.L);
+    const uint32_t q = P.q[limb];
+    uint32_t a[W::V];
+    W::gld1(rows + r * W::N, a, tid);
+    W::forward(a, sm, P.tw_fwd + (size_t)limb * W::N, tid, q);
+#pragma unroll
+    for (int c = 0; c < W::V; ++c) a[c] = pb::canon4(a[c], q);
+    W::gst_dev(rows + r * W::N, a, tid);
+    __syncthreads();
+  }
+}
+template <int LOGN, int LOGV>
+__global__ void __launch_bounds__(1 << (LOGN - LOGV)) k_winv(PbDev P, uint32_t* rows, int64_t n_rows) {
+  using W = pb::NttW<LOGN, LOGV>;
+  extern __shared__ uint32_t sm[];
+  const int tid = threadIdx.x;
+  for (int64_t r = blockIdx.x; r < n_rows; r += gridDim.x) {
+    const int limb = (int)(r % P.L);
+    const uint32_t q = P.q[limb];
+    uint32_t a[W::V];
+    W::gld_dev(rows + r * W::N, a, tid);
+    W::inverse(a, sm, P.tw_inv + (size_t)limb * W::N, tid, q);
+    const uint32_t ni = P.ninv[limb], nis = P.ninv_sh[limb];
+#pragma unroll
+    for (int c = 0; c < W::V; ++c) a[c] = mul_shoup(a[c], ni, nis, q);
+    W::gst1(rows + r * W::N, a, tid);
+    __syncthreads();
+  }
+}
+template <int LOGV>
+int wlaunch(int inv, const PbDev& P, uint32_t* rows, int64_t n, cudaStream_t st) {
+  using W = pb::NttW<13, LOGV>;
+  const size_t smem = W::SMEM_WORDS * 4;
+  if (inv) {
+    cudaFuncSetAttribute(k_winv<13, LOGV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_winv<13, LOGV><<<(unsigned)n, W::T, smem, st>>>(P, rows, n);
+  } else {
+    cudaFuncSetAttribute(k_wfwd<13, LOGV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_wfwd<13, LOGV><<<(unsigned)n, W::T, smem, st>>>(P, rows, n);
+  }
+  return (int)cudaGetLastError();
+}
+}  // namespace
+extern "C" int exp_wntt(const pb_ctx* ctx, int logv, int inv, uint32_t* rows, int64_t n, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (ctx->dev.logN != 13) return -1;
+  if (logv == 3) return wlaunch<3>(inv, ctx->dev, rows, n, st);
+  if (logv == 4) return wlaunch<4>(inv, ctx->dev, rows, n, st);
+  return -2;
+}
