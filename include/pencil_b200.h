@@ -268,6 +268,12 @@ enum { PB_POOL_SUM = 0, PB_POOL_REPLICATE = 1 };
 int pb_pool2(int op, const uint64_t* in, int64_t bc, int32_t H, int32_t W, int32_t ell, uint64_t* out,
              void* stream);
 
+/* Pencil+ online phase (PAPER Alg. 3 steps 7-10): scalar-weighted
+ * sums of mask tensors, out = base (+|-) sum_{i<ma,j<mb} a_i b_j T[i][j][:] mod
+ * 2^ell; b == NULL means weights a_i alone (mb must be 1); base may be NULL. */
+int pb_ring_lincomb(int subtract, uint64_t* out, const uint64_t* base, const uint64_t* a, int32_t ma,
+                    const uint64_t* b, int32_t mb, const uint64_t* T, int64_t n, int32_t ell, void* stream);
+
 /* ------------------------------- dealer-assisted non-linear --- */
 /* The SPEC's dealer OT backend ("fast, insecure, default for benchmarks of
  * non-OT costs"): reconstruct x = mo + do, apply f, reshare with

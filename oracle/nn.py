@@ -204,9 +204,13 @@ def reference_train_step(model: Model, x_enc, labels, lr=1e-2, momentum=0.8):
     return loss, gws, gbs
 
 
-def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, momentum=0.8, trace=None):
-    """SPEC:629-637 with fullhe linear layers (oracle/protocols.py) and the
-    dealer non-linear backend; <X_0>_0 = 0 at MO, <X_0>_1 = X at DO."""
+def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, momentum=0.8, trace=None, prep=None):
+    """SPEC:629-637 with fullhe linear layers (oracle/protocols.py) -- or, with
+    ``prep`` (a preprocessing.PrepState), the HE-free online linear layers of
+    Alg. 4 (mode "prep", SPEC:632) -- and the dealer non-linear backend;
+    <X_0>_0 = 0 at MO, <X_0>_1 = X at DO."""
+    from . import preprocessing as PP
+
     ring, f = model.ring, model.ring.f
     L = model.n_layers
     seg = _segments(model)
@@ -215,7 +219,9 @@ def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, moment
     for l, i in enumerate(model.lin):
         e = model.layers[i]
         acts.append(cur)
-        if e[0] == "fc":
+        if prep is not None:
+            y = PP.prep_linear_forward(ctx, l, prep.banks[l], model.W(l), model.Bias(l), *cur)
+        elif e[0] == "fc":
             y = PR.linear_forward(ctx, l, model.W(l), model.Bias(l), *cur, mo_x_zero=(l == 0))
         else:
             y = PR.conv_forward(ctx, l, model.W(l), model.Bias(l), *cur, e[4], e[5], mo_x_zero=(l == 0))
@@ -237,7 +243,10 @@ def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, moment
     for l in reversed(range(L)):
         e = model.layers[model.lin[l]]
         last = l == L - 1
-        if e[0] == "fc":
+        if prep is not None:
+            gbs[l] = (PR.reveal_grad_bias if e[0] == "fc" else PR.reveal_grad_bias_conv)(ctx, l, gy_mo, gy_do)
+            gw2f = PP.prep_grad_weight(ctx, l, prep.banks[l], *acts[l], gy_mo, gy_do)
+        elif e[0] == "fc":
             gbs[l] = PR.reveal_grad_bias(ctx, l, gy_mo, gy_do)
             gw2f = PR.grad_weight(ctx, l, *acts[l], gy_mo, gy_do, mo_x_zero=(l == 0), mo_gy_zero=last)
         else:
@@ -248,7 +257,9 @@ def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, moment
         if trace is not None:
             trace.append((l, ys[l], gbs[l], gws[l]))
         if l > 0:
-            if e[0] == "fc":
+            if prep is not None:
+                ga = PP.prep_linear_backward_input(ctx, l, prep.banks[l], model.W(l), gy_mo, gy_do)
+            elif e[0] == "fc":
                 ga = PR.linear_backward_input(ctx, l, model.W(l), gy_mo, gy_do, mo_gy_zero=last)
             else:
                 H, Wd = acts[l][1].shape[2:]

@@ -110,7 +110,7 @@ def plan_matmul_blocks(g: MatmulGeometry, N: int, mode: str = "cost"):
         for nob in range(1, min(g.n_o, cap) + 1):
             Bb = min(g.B, cap // nob)
             n_out = (-(-g.B // Bb)) * (-(-g.n_o // nob))
-            cost = 1.3 * (-(-g.B // Bb)) * k + 1.0 * (-(-g.n_o // nob)) * k + 2.0 * n_out + 0.5 * n_out * k
+            cost = 8.0 * (-(-g.B // Bb)) * k + 3.7 * (-(-g.n_o // nob)) * k + 14.0 * n_out + 1.0 * n_out * k
             cand = ((round(cost, 6), n_out, k, -nob), (Bb, nob, nib))
             best = cand if best is None or cand[0] < best[0] else best
     return best[1]

@@ -82,6 +82,7 @@ SIGNATURES = {
     "pb_conv2d": [P, P, I32, I32, I32, I32, I32, I32, I32, P, P],
     "pb_ring_conv": [INT, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P],
     "pb_pool2": [INT, P, I64, I32, I32, I32, P, P],
+    "pb_ring_lincomb": [INT, P, P, P, I32, P, I32, P, I64, I32, P],
     "pb_dealer_op": [INT, P, P, I64, I32, P, P, U64, P, U64, U64, I32, P],
     "pb_sgd_momentum": [P, P, P, I64, I32, F64, F64, I32, I32, P, P, P],
 }

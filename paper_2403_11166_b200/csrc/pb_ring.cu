@@ -97,6 +97,27 @@ __global__ void k_uniform_ring(uint64_t* out, const uint64_t* x, uint64_t* do_ou
   }
 }
 
+// Scalar-weighted sums of mask tensors (Pencil+ online phase, Alg. 3 steps
+// 7-10): out = base (+|-) sum_{i<ma, j<mb} a_i * b_j * T[i][j][:]  mod 2^ell
+// (b == NULL: weights a_i alone).  One thread per element; the <= 64
+// coefficients live in shared memory.
+__global__ void k_ring_lincomb(int sub, uint64_t* out, const uint64_t* base, const uint64_t* a, int ma,
+                               const uint64_t* b, int mb, const uint64_t* T, int64_t n, uint64_t mask) {
+  __shared__ uint64_t coef[256];
+  for (int t = threadIdx.x; t < ma * mb; t += blockDim.x) {
+    const int i = t / mb, j = t - i * mb;
+    coef[t] = a[i] * (b ? b[j] : 1ull);
+  }
+  __syncthreads();
+  const int mm = ma * mb;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t acc = 0;
+    for (int t = 0; t < mm; ++t) acc += coef[t] * __ldg(T + (int64_t)t * n + x);
+    const uint64_t b0 = base ? base[x] : 0ull;
+    out[x] = (sub ? b0 - acc : b0 + acc) & mask;
+  }
+}
+
 // K:206-218 ring GEMM with uint64 wraparound, 16x16 smem tiles.
 template <int TS>
 __global__ void k_ring_matmul(const uint64_t* __restrict__ A, const uint64_t* __restrict__ B, int64_t n, int64_t k,
@@ -384,6 +405,18 @@ extern "C" int pb_sgd_momentum(double* w, double* v, const uint64_t* grad_ring, 
   if (bad_ell(ell)) return pb_set_error(PB_ERR_ARG, "bad ell");
   if (n <= 0) return PB_OK;
   k_sgd<<<RING_GRID(n)>>>(w, v, grad_ring, n, grad_scale, lr, momentum, ell, w_scale, w_ring, range_flag);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_ring_lincomb(int subtract, uint64_t* out, const uint64_t* base, const uint64_t* a, int32_t ma,
+                               const uint64_t* b, int32_t mb, const uint64_t* T, int64_t n, int32_t ell, void* stream) {
+  if (n > 0 && (!out || !a || !T)) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (ma < 1 || mb < 1 || ma * mb > 256) return pb_set_error(PB_ERR_ARG, "ma * mb must be in [1, 256]");
+  if (bad_ell(ell)) return pb_set_error(PB_ERR_ARG, "bad ell");
+  if (n <= 0) return PB_OK;
+  const uint64_t mask = ell >= 64 ? ~0ull : ((1ull << ell) - 1);
+  k_ring_lincomb<<<RING_GRID(n)>>>(subtract ? 1 : 0, out, base, a, ma, b, mb, T, n, mask);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }

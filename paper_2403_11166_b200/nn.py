@@ -24,6 +24,7 @@ from . import _dev, _lib
 from .errors import EncodeRangeError, ShapeError
 from .linear_protocols import (Session, conv_backward_input, conv_forward, conv_grad_weight, grad_weight,
                                linear_backward_input, linear_forward, reveal_grad_bias, reveal_grad_bias_conv)
+from . import preprocessing as PP
 from .nonlinear import avgpool_backward, avgpool_forward, relu_backward, relu_forward, truncate
 from .poly_encoding import conv_out_hw
 from .ring import DO, MO, RingParams, RingTensor, SeededRng, ShareTensor, arith_shift, encode_fixed
@@ -178,8 +179,10 @@ def _unflatten(sh: ShareTensor, chw) -> ShareTensor:  # (C*H*W, B) -> (B, C, H, 
                                                  _canonical=True))
 
 
-def forward_phase(sess: Session, model: Model, x: RingTensor):
-    """Private forward pass; returns (state for the backward pass, logits = MO share + DO share)."""
+def forward_phase(sess: Session, model: Model, x: RingTensor, prep=None):
+    """Private forward pass; returns (state for the backward pass, logits = MO share + DO share).
+    With ``prep`` (a preprocessing.PrepState) the linear layers run Alg. 4's
+    HE-free online protocol (SPEC mode "prep")."""
     ring, f = model.ring, model.ring.f
     L = model.n_layers
     seg = model.segments()
@@ -188,7 +191,9 @@ def forward_phase(sess: Session, model: Model, x: RingTensor):
     for l, i in enumerate(model.lin):
         e = model.layers[i]
         acts.append(cur)
-        if e[0] == "fc":
+        if prep is not None:
+            y = PP.prep_linear_forward(sess, l, prep.banks[l], model.W[l], model.B[l], *cur)
+        elif e[0] == "fc":
             y = linear_forward(sess, l, model.W[l], model.B[l], *cur, mo_x_zero=(l == 0))
         else:
             y = conv_forward(sess, l, model.W[l], model.B[l], *cur, e[4], e[5], mo_x_zero=(l == 0))
@@ -209,7 +214,7 @@ def forward_phase(sess: Session, model: Model, x: RingTensor):
 
 
 def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e-2, momentum=0.8, trace=None,
-                   check=True):
+                   check=True, prep=None):
     """Private backward pass from the DO's loss gradient share (MO share 0) + SGD at the MO."""
     ring, f = model.ring, model.ring.f
     L = model.n_layers
@@ -228,7 +233,10 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
         last = l == L - 1
         gstream.wait_stream(main)
         with torch.cuda.stream(gstream):
-            if e[0] == "fc":
+            if prep is not None:
+                gbs[l] = (reveal_grad_bias if e[0] == "fc" else reveal_grad_bias_conv)(sess, l, gy_mo, gy_do)
+                gw = PP.prep_grad_weight(sess, l, prep.banks[l], *acts[l], gy_mo, gy_do)
+            elif e[0] == "fc":
                 gbs[l] = reveal_grad_bias(sess, l, gy_mo, gy_do)
                 gw = grad_weight(sess, l, *acts[l], gy_mo, gy_do, mo_x_zero=(l == 0), mo_gy_zero=last)
             else:
@@ -240,7 +248,9 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
         if trace is not None:
             trace.append((l, ys[l], gbs[l], gws[l]))
         if l > 0:
-            if e[0] == "fc":
+            if prep is not None:
+                ga = PP.prep_linear_backward_input(sess, l, prep.banks[l], model.W[l], gy_mo, gy_do)
+            elif e[0] == "fc":
                 ga = linear_backward_input(sess, l, model.W[l], gy_mo, gy_do, mo_gy_zero=last)
             else:
                 H, Wd = acts[l][1].shape[2:]
@@ -260,12 +270,13 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
 
 
 def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e-2, momentum=0.8,
-                       trace=None, check=True):
+                       trace=None, check=True, prep=None):
     """One private step; x held by the DO at scale f: (784, B)
-    feature-major for FC-first models, (B, C, H, W) for CNNs."""
-    state, logits = forward_phase(sess, model, x)
+    feature-major for FC-first models, (B, C, H, W) for CNNs.  ``prep``
+    selects SPEC's mode "prep" (Pencil+, Alg. 4) over "fullhe"."""
+    state, logits = forward_phase(sess, model, x, prep)
     loss, g = softmax_ce_grad(logits.numpy(), np.asarray(labels), model.ring)  # DO, float64 (host)
-    gws, gbs = backward_phase(sess, model, state, _dev.u64_to_device(g), lr, momentum, trace, check)
+    gws, gbs = backward_phase(sess, model, state, _dev.u64_to_device(g), lr, momentum, trace, check, prep)
     return loss, gws, gbs
 
 
@@ -277,8 +288,8 @@ class GraphStep:
     every kernel of the step is the same sm_100a kernel the eager path runs:
     the graphs only remove per-launch host overhead."""
 
-    def __init__(self, sess: Session, model: Model, x: RingTensor, lr=1e-2, momentum=0.8):
-        self.sess, self.model, self.lr, self.momentum = sess, model, lr, momentum
+    def __init__(self, sess: Session, model: Model, x: RingTensor, lr=1e-2, momentum=0.8, prep=None):
+        self.sess, self.model, self.lr, self.momentum, self.prep = sess, model, lr, momentum, prep
         sess.enable_graph_mode()
         self.x = x  # device input buffer; callers copy new batches into x.values
         n_cls = model.n_classes
@@ -287,15 +298,15 @@ class GraphStep:
         self.logits_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
         self.g_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
         # warm-up (eager, graph-mode keys): builds plans/maps, sizes scratch buffers
-        st, lg = forward_phase(sess, model, x)
-        backward_phase(sess, model, st, self.g_do, lr, momentum, check=False)
+        st, lg = forward_phase(sess, model, x, prep)
+        backward_phase(sess, model, st, self.g_do, lr, momentum, check=False, prep=prep)
         torch.cuda.synchronize()
         self.g_fwd = torch.cuda.CUDAGraph()
         self.g_bwd = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.g_fwd):
-            self.state, self.logits = forward_phase(sess, model, x)
+            self.state, self.logits = forward_phase(sess, model, x, prep)
         with torch.cuda.graph(self.g_bwd, pool=self.g_fwd.pool()):
-            self.grads = backward_phase(sess, model, self.state, self.g_do, lr, momentum, check=False)
+            self.grads = backward_phase(sess, model, self.state, self.g_do, lr, momentum, check=False, prep=prep)
         torch.cuda.synchronize()
 
     def step(self, seed: int, labels):
