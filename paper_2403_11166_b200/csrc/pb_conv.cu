@@ -174,6 +174,7 @@ struct ConvDims {
 
 template <int S, int KIND>
 struct ConvGemm {  // 32-bit index arithmetic (the launcher checks every tensor has < 2^31 elements)
+  using Dims = ConvDims;
   static constexpr int SS = S * S;
   __device__ __forceinline__ static void mnk(const ConvDims& d, int& M, int& N, int& K) {
     if (KIND == PB_CONV_FWD) { M = d.co; N = d.B * d.oh * d.ow; K = d.ci * SS; }
@@ -224,11 +225,27 @@ struct ConvGemm {  // 32-bit index arithmetic (the launcher checks every tensor 
   }
 };
 
-template <int S, int KIND>
-__global__ void __launch_bounds__(256) k_conv_gemm(ConvDims d, const uint64_t* __restrict__ A,
-                                                   const uint64_t* __restrict__ Bm, int64_t k_per_split, uint64_t m,
-                                                   uint64_t* __restrict__ out) {
-  using G = ConvGemm<S, KIND>;
+// K:206-218 matmul_wrap as the same tiled GEMM: out (n x m) = A (n x k) B (k x m),
+// A / B optionally stored transposed (trans_a: A read as (k x n), trans_b: B as (m x k)).
+struct MatDims {
+  int n, k, m, ta, tb;
+};
+struct MatGemm {
+  using Dims = MatDims;
+  __device__ __forceinline__ static void mnk(const MatDims& d, int& M, int& N, int& K) { M = d.n; N = d.m; K = d.k; }
+  __device__ __forceinline__ static uint64_t a_at(const MatDims& d, const uint64_t* A, int i, int kk) {
+    return __ldg(A + (d.ta ? (size_t)kk * d.n + i : (size_t)i * d.k + kk));
+  }
+  __device__ __forceinline__ static uint64_t b_at(const MatDims& d, const uint64_t* B, int kk, int j) {
+    return __ldg(B + (d.tb ? (size_t)j * d.k + kk : (size_t)kk * d.m + j));
+  }
+  __device__ __forceinline__ static size_t out_at(const MatDims& d, int i, int j) { return (size_t)i * d.m + j; }
+};
+
+template <class G>
+__global__ void __launch_bounds__(256) k_gemm(typename G::Dims d, const uint64_t* __restrict__ A,
+                                              const uint64_t* __restrict__ Bm, int64_t k_per_split, uint64_t m,
+                                              uint64_t* __restrict__ out) {
   constexpr int BM = 64, BN = 64, BK = 16;
   __shared__ uint64_t As[BK][BM];
   __shared__ uint64_t Bs[BK][BN + 1];
@@ -307,9 +324,9 @@ int conv_gemm_launch(int kind, const ConvDims& d, const uint64_t* a, const uint6
   const int64_t kps = ((K + splits - 1) / splits + 15) / 16 * 16;
   dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)splits);
   if (splits > 1) cudaMemsetAsync(out, 0, (size_t)(M * N) * sizeof(uint64_t), st);
-  if (kind == PB_CONV_FWD) k_conv_gemm<S, PB_CONV_FWD><<<grid, 256, 0, st>>>(d, b, a, kps, m, out);  // A = W, B = X
-  else if (kind == PB_CONV_BWDX) k_conv_gemm<S, PB_CONV_BWDX><<<grid, 256, 0, st>>>(d, b, a, kps, m, out);  // A = W, B = dY
-  else k_conv_gemm<S, PB_CONV_GRADW><<<grid, 256, 0, st>>>(d, b, a, kps, m, out);  // A = dY, B = X
+  if (kind == PB_CONV_FWD) k_gemm<ConvGemm<S, PB_CONV_FWD>><<<grid, 256, 0, st>>>(d, b, a, kps, m, out);  // A = W, B = X
+  else if (kind == PB_CONV_BWDX) k_gemm<ConvGemm<S, PB_CONV_BWDX>><<<grid, 256, 0, st>>>(d, b, a, kps, m, out);  // A = W, B = dY
+  else k_gemm<ConvGemm<S, PB_CONV_GRADW>><<<grid, 256, 0, st>>>(d, b, a, kps, m, out);  // A = dY, B = X
   if (splits > 1) k_mask_inplace<<<pb_grid_1d(M * N, 256), 256, 0, st>>>(out, M * N, m);
   return 0;
 }
@@ -381,6 +398,39 @@ extern "C" int pb_pool2(int op, const uint64_t* in, int64_t bc, int32_t H, int32
   if (bc <= 0) return PB_OK;
   const int64_t n = op == PB_POOL_SUM ? bc * (H / 2) * (W / 2) : bc * H * W;
   k_pool2<<<pb_grid_1d(n, 256), 256, 0, pb_stream_of(stream)>>>(op, in, bc, H, W, cmask(ell), out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+void pb_launch_ring_matmul_small(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m, int trans_a,
+                                 int trans_b, uint64_t mask, uint64_t* out, cudaStream_t st);
+
+extern "C" int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m, int trans_a,
+                              int trans_b, int32_t ell, uint64_t* out, void* stream) {
+  if (n > 0 && m > 0 && k > 0 && (!a || !b || !out)) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n <= 0 || m <= 0) return PB_OK;
+  if (k < 0 || n * k >= (1ll << 31) || k * m >= (1ll << 31) || n * m >= (1ll << 31))
+    return pb_set_error(PB_ERR_SHAPE, "bad matmul shape");
+  const uint64_t mask = (ell >= 64 || ell <= 0) ? ~0ull : ((1ull << ell) - 1);
+  cudaStream_t st = pb_stream_of(stream);
+  if (k == 0) {
+    cudaMemsetAsync(out, 0, (size_t)(n * m) * sizeof(uint64_t), st);
+    return PB_OK;
+  }
+  if (n * k * m < (1ll << 24)) {  // the FC layers' local terms: one small launch beats tiles + split-K passes
+    pb_launch_ring_matmul_small(a, b, n, k, m, trans_a, trans_b, mask, out, st);
+    PB_CHECK_LAUNCH();
+    return PB_OK;
+  }
+  const MatDims d{(int)n, (int)k, (int)m, trans_a ? 1 : 0, trans_b ? 1 : 0};
+  const int64_t tiles = ((n + 63) / 64) * ((m + 63) / 64);
+  int splits = 1;  // split the contraction to fill the GPU (the FC weight gradients have small n x m, large k)
+  while (tiles * splits < 2 * 148 * 3 && k / (splits * 2) >= 128) splits *= 2;
+  const int64_t kps = ((k + splits - 1) / splits + 15) / 16 * 16;
+  dim3 grid((unsigned)((m + 63) / 64), (unsigned)((n + 63) / 64), (unsigned)splits);
+  if (splits > 1) cudaMemsetAsync(out, 0, (size_t)(n * m) * sizeof(uint64_t), st);
+  k_gemm<MatGemm><<<grid, 256, 0, st>>>(d, a, b, kps, mask, out);
+  if (splits > 1) k_mask_inplace<<<pb_grid_1d(n * m, 256), 256, 0, st>>>(out, n * m, mask);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }

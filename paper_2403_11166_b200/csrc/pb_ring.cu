@@ -118,7 +118,8 @@ __global__ void k_ring_lincomb(int sub, uint64_t* out, const uint64_t* base, con
   }
 }
 
-// K:206-218 ring GEMM with uint64 wraparound, 16x16 smem tiles.
+// K:206-218 ring GEMM, small shapes: 16x16 smem tiles, one output per thread, one
+// launch (pb_ring_matmul in pb_conv.cu picks it below 2^24 MACs).
 template <int TS>
 __global__ void k_ring_matmul(const uint64_t* __restrict__ A, const uint64_t* __restrict__ B, int64_t n, int64_t k,
                               int64_t m, int ta, int tb, uint64_t mask, uint64_t* __restrict__ C) {
@@ -329,17 +330,6 @@ extern "C" int pb_share(const uint64_t* x, int64_t n, uint64_t seed, const uint6
   return PB_OK;
 }
 
-extern "C" int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m, int trans_a,
-                              int trans_b, int32_t ell, uint64_t* out, void* stream) {
-  if (n > 0 && m > 0 && k > 0 && (!a || !b || !out)) return pb_set_error(PB_ERR_ARG, "null argument");
-  if (n <= 0 || m <= 0) return PB_OK;
-  if (k < 0 || n > (1ll << 31) || m > (1ll << 31)) return pb_set_error(PB_ERR_SHAPE, "bad matmul shape");
-  const uint64_t mask = (ell >= 64 || ell <= 0) ? ~0ull : ((1ull << ell) - 1);
-  dim3 blk(16, 16), grd((unsigned)((m + 15) / 16), (unsigned)((n + 15) / 16));
-  k_ring_matmul<16><<<grd, blk, 0, pb_stream_of(stream)>>>(a, b, n, k, m, trans_a, trans_b, mask, out);
-  PB_CHECK_LAUNCH();
-  return PB_OK;
-}
 
 extern "C" int pb_ring_rowsum(const uint64_t* a, int64_t rows, int64_t cols, int32_t ell, uint64_t* out, void* stream) {
   if (rows > 0 && (!a || !out)) return pb_set_error(PB_ERR_ARG, "null argument");
@@ -419,4 +409,11 @@ extern "C" int pb_ring_lincomb(int subtract, uint64_t* out, const uint64_t* base
   k_ring_lincomb<<<RING_GRID(n)>>>(subtract ? 1 : 0, out, base, a, ma, b, mb, T, n, mask);
   PB_CHECK_LAUNCH();
   return PB_OK;
+}
+
+// Small-shape matmul launcher used by pb_ring_matmul (pb_conv.cu).
+void pb_launch_ring_matmul_small(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m, int trans_a,
+                                 int trans_b, uint64_t mask, uint64_t* out, cudaStream_t st) {
+  dim3 blk(16, 16), grd((unsigned)((m + 15) / 16), (unsigned)((n + 15) / 16));
+  k_ring_matmul<16><<<grd, blk, 0, st>>>(a, b, n, k, m, trans_a, trans_b, mask, out);
 }

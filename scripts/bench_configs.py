@@ -10,6 +10,8 @@ c2  MNIST MLP 784-128-128-10 private training step, B=64
 c3  MNIST CNN (2 x conv5x5 + FC, "mnist_cnn2") private training step, B=64
     (also the paper's 1-conv "mnist_cnn")
 c4  CIFAR-10 CNN (PAPER Fig. 7, 5 conv + FC) private training step, B=64
+c2p/c3p/c4p  the same models in SPEC mode "prep" (Pencil+, Alg. 3/4, m=8):
+    offline bank build time and the HE-free online step
 c5  NTT fwd/inv sweep N=4096..32768, L=2..8 over >= 1 GiB of residues, and
     the ct x pt MAC operator (pb_ctpt_mac_tiled) at FC-like (B_ct=64, O_pt=13,
     K=1) and conv-like (K=16) shapes
@@ -75,7 +77,7 @@ def time_steps(fn, steps, warm=3, flush=None):
     return tot / steps  # ms
 
 
-def model_step(name, steps, cpu):
+def model_step(name, steps, cpu, prep_m=0):
     ring, params = RingParams(), BfvParams()
     sess = Session(params, ring, bfv.keygen(params, SeededRng(SEED, 0)), seed=SEED)
     model = PN.Model(name, ring, seed=SEED)
@@ -85,29 +87,41 @@ def model_step(name, steps, cpu):
         xh, labels = PN.synthetic_images(SEED, B, model.in_shape, ring)
     x = RingTensor(encode_fixed(xh, ring), ring.f, ring, _canonical=True)
     flush = _flush_buf()
+    prep, prep_s = None, None
+    if prep_m:
+        from paper_2403_11166_b200 import preprocessing as PP
+
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        prep = PP.PrepState(sess, model, B, m=prep_m, bank_seed=SEED)
+        torch.cuda.synchronize()
+        prep_s = time.perf_counter() - t0
     # eager (kernel-time breakdown + launch count)
     stats = _lib.CallStats(timed=("pb_ctpt_mac_tiled", "pb_mask_ntt", "pb_decrypt_to_share", "pb_encrypt_sk",
                                   "pb_encode_plain_mont", "pb_ring_conv"))
     for i in range(2):
         sess.reseed(SEED + i)
-        PN.private_train_step(sess, model, x, labels, check=False)
+        PN.private_train_step(sess, model, x, labels, check=False, prep=prep)
     torch.cuda.synchronize()
     _lib.STATS = stats
     flush.zero_()
     sess.reseed(SEED + 7)
     t0 = time.perf_counter()
-    PN.private_train_step(sess, model, x, labels, check=False)
+    PN.private_train_step(sess, model, x, labels, check=False, prep=prep)
     torch.cuda.synchronize()
     eager_s = time.perf_counter() - t0
     _lib.STATS = None
     per = {}
     for nm, s, e, _ in stats.events:
         per[nm] = per.get(nm, 0.0) + s.elapsed_time(e)
-    runner = PN.GraphStep(sess, model, x)
+    runner = PN.GraphStep(sess, model, x, prep=prep)
     ms = time_steps(lambda i: runner.step(SEED + 100 + i, labels), steps, flush=flush)
-    out = {"config": name, "batch": B, "ms_per_step": ms, "samples_per_s": B / (ms / 1e3),
+    out = {"config": name + (f"+prep(m={prep_m})" if prep_m else ""), "batch": B, "ms_per_step": ms, "samples_per_s": B / (ms / 1e3),
            "eager_wall_ms": eager_s * 1e3, "launches_per_step": stats.launches,
            "kernel_ms": {k: round(v, 4) for k, v in sorted(per.items(), key=lambda kv: -kv[1])}}
+    if prep_m:
+        out["offline_bank_build_s"] = prep_s
+        out["online_census_bytes_per_step"] = sum(v[1] for k, v in sess.channel.census.items() if k in (0x42, 0x43)) / 4
     if cpu:
         out["cpu"] = cpu_model_step(name)
     return out
@@ -265,6 +279,12 @@ def main():
             print(json.dumps(model_step("mnist_cnn", a.steps, a.cpu)), flush=True)
         elif w == "c4":
             print(json.dumps(model_step("cifar_cnn", a.steps, False)), flush=True)
+        elif w == "c2p":
+            print(json.dumps(model_step("mnist_mlp", a.steps, False, prep_m=8)), flush=True)
+        elif w == "c3p":
+            print(json.dumps(model_step("mnist_cnn2", a.steps, False, prep_m=8)), flush=True)
+        elif w == "c4p":
+            print(json.dumps(model_step("cifar_cnn", a.steps, False, prep_m=8)), flush=True)
         elif w == "c5":
             for r in sweep(a.steps):
                 print(json.dumps(r), flush=True)
