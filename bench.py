@@ -47,6 +47,32 @@ BATCH = 64
 SEED = 2024
 
 
+# entry point -> device kernels it launches (for the ncu DRAM-traffic lookup)
+ENTRY_KERNELS = {
+    "pb_encrypt_sk": ("k_encrypt_sk",), "pb_encode_plain_mont": ("k_encode_plain_mont",),
+    "pb_mask_ntt": ("k_mask_ntt",), "pb_ctpt_mac_tiled": ("k_mac_pipe", "k_mac_eager"),
+    "pb_decrypt_to_share": ("k_decrypt_inv", "k_decode_gather"),
+}
+
+
+def _traffic(entry):
+    """DRAM bytes per launch of an entry point's kernels from the committed ncu
+    capture of the same step (profiles/r01_step_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_step_traffic.json")) as f:
+            ks = json.load(f)["kernels"]
+    except Exception:
+        return None
+    names = [k for k in ENTRY_KERNELS.get(entry, ()) if k in ks]
+    if not names:
+        return None
+    # kernels of one entry point launch once per call each (k_mac_pipe / k_mac_eager: either)
+    if entry == "pb_ctpt_mac_tiled":
+        tot = sum(ks[k]["dram_bytes_per_launch"] * ks[k]["launches"] for k in names)
+        return tot / max(1, sum(ks[k]["launches"] for k in names))
+    return float(sum(ks[k]["dram_bytes_per_launch"] for k in names))
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -255,7 +281,9 @@ def run_ours(args, rank, world):
     bytes_per_launch = alg.get(dom, 0.0) / max(1, n_launch)
     achieved = bytes_per_launch / (tot_ms / n_launch / 1e3) / 1e9
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+                "frac": achieved / peak, "peak_kind": peak_kind, "traffic": _traffic(dom),
+                "traffic_note": "ncu dram__bytes_read+write per launch (profiles/r01_step_traffic.json); far below "
+                                "the algorithmic bytes because the step's working set is L2-resident",
                 "bytes_per_launch": bytes_per_launch, "launches": n_launch,
                 "ms_per_launch": tot_ms / n_launch, "share_of_step": (tot_ms / prof_steps) / (t_ms / args.steps)}
     kernels = {k: {"ms_per_step": v[0] / prof_steps, "calls_per_step": v[1] / prof_steps,
