@@ -223,6 +223,10 @@ int pb_ring_binary(int op, uint64_t* out, const uint64_t* a, const uint64_t* b, 
                    int64_t b_n, int32_t ell, void* stream);
 int pb_ring_unary(int op, uint64_t* out, const uint64_t* a, uint64_t k, int64_t n, int32_t ell,
                   void* stream);
+/* out[i] = a[i] + b[(i / inner) % bn] mod 2^ell (bias add along an axis: FC (n_o, B) -> inner = B,
+ * bn = n_o; conv (B, c_o, oh, ow) -> inner = oh*ow, bn = c_o). */
+int pb_ring_add_bcast(uint64_t* out, const uint64_t* a, const uint64_t* b, int64_t n, int64_t inner, int64_t bn,
+                      int32_t ell, void* stream);
 /* R:174-182 encode_fixed; *range_flag (device int32) set to 1 on |x| >= limit. */
 int pb_encode_fixed(const double* x, int64_t n, int32_t ell, int32_t scale, uint64_t* out,
                     int32_t* range_flag, void* stream);
@@ -282,8 +286,19 @@ int pb_ring_lincomb(int subtract, uint64_t* out, const uint64_t* base, const uin
  *   PB_DEALER_TRUNC    y = arith_shift(x, k)                       (faithful)
  *   PB_DEALER_SELECT   y = d_in[i] ? x : 0                         (ReLU backward, cached d)
  *   PB_DEALER_RESHARE  y = x
+ *   PB_DEALER_RELU_TRUNC   y = arith_shift(relu(x), k), d_out as RELU  (forward ReLU + truncation;
+ *                          the relu's own reshare is never observed, so the output shares equal
+ *                          the two-step composition's when `stream_id` is the truncation's stream)
+ *   PB_DEALER_TRUNC_SELECT y = d_in[i] ? arith_shift(x, k) : 0          (backward truncation + ReLU')
  * Outputs overwrite mo/do in place. */
-enum { PB_DEALER_RELU = 0, PB_DEALER_TRUNC = 1, PB_DEALER_SELECT = 2, PB_DEALER_RESHARE = 3 };
+enum {
+  PB_DEALER_RELU = 0,
+  PB_DEALER_TRUNC = 1,
+  PB_DEALER_SELECT = 2,
+  PB_DEALER_RESHARE = 3,
+  PB_DEALER_RELU_TRUNC = 4,
+  PB_DEALER_TRUNC_SELECT = 5
+};
 int pb_dealer_op(int op, uint64_t* mo, uint64_t* do_, int64_t n, int32_t k, const uint8_t* d_in,
                  uint8_t* d_out, uint64_t seed, const uint64_t* seed_dev, uint64_t stream_id,
                  uint64_t raw_offset, int32_t ell, void* stream);

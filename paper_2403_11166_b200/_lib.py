@@ -83,6 +83,7 @@ SIGNATURES = {
     "pb_ring_conv": [INT, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P],
     "pb_pool2": [INT, P, I64, I32, I32, I32, P, P],
     "pb_ring_lincomb": [INT, P, P, P, I32, P, I32, P, I64, I32, P],
+    "pb_ring_add_bcast": [P, P, P, I64, I64, I64, I32, P],
     "pb_dealer_op": [INT, P, P, I64, I32, P, P, U64, P, U64, U64, I32, P],
     "pb_sgd_momentum": [P, P, P, I64, I32, F64, F64, I32, I32, P, P, P],
 }
@@ -91,7 +92,7 @@ _RET = {"pb_last_error": ctypes.c_char_p}
 # ring / pointwise / dealer op codes (mirror the enums in pencil_b200.h)
 PW_MUL, PW_MAC, PW_ADD, PW_SUB = 0, 1, 2, 3
 RING_ADD, RING_SUB, RING_MUL, RING_NEG, RING_SCALAR_MUL, RING_MASK, RING_ARITH_SHIFT = range(7)
-DEALER_RELU, DEALER_TRUNC, DEALER_SELECT, DEALER_RESHARE = range(4)
+DEALER_RELU, DEALER_TRUNC, DEALER_SELECT, DEALER_RESHARE, DEALER_RELU_TRUNC, DEALER_TRUNC_SELECT = range(6)
 CONV_FWD, CONV_BWDX, CONV_GRADW = range(3)
 POOL_SUM, POOL_REPLICATE = range(2)
 
@@ -131,7 +132,7 @@ def check(status: int, what: str = "") -> None:
 
 # Device kernels each entry point launches (for the bench's gpu_launches count).
 KERNELS_PER_CALL = {
-    "pb_encrypt_pk": 2, "pb_encrypt_sk": 1, "pb_decrypt": 2, "pb_decrypt_to_share": 2, "pb_unpack": 1,
+    "pb_encrypt_pk": 2, "pb_encrypt_sk": 1, "pb_decrypt": 2, "pb_decrypt_to_share": 1, "pb_unpack": 1,
     "pb_abi_version": 0, "pb_last_error": 0, "pb_device_sm_count": 0, "pb_ctx_create": 0, "pb_ctx_destroy": 0,
 }
 

@@ -10,6 +10,8 @@
 // its result once.
 #include "pb_ntt.cuh"
 
+#include <cooperative_groups.h>
+
 namespace {
 
 // A plaintext source: `vals` is a flat Z_t tensor.  With `pos` set, poly p
@@ -354,6 +356,60 @@ __global__ void k_decode_gather(PbDev P, const uint32_t* x, int64_t nP, int U, c
   }
 }
 
+// Fused decrypt-to-share: one thread-block CLUSTER of L CTAs per output
+// ciphertext, CTA l = limb l.  Each CTA computes x_l = INTT(c0 + c1 s) * N^-1
+// for its limb and leaves the row in its shared memory; after a cluster
+// barrier every CTA decodes a 1/L share of the useful slots, reading the L
+// residues of a coefficient straight from the L CTAs' shared memory (DSMEM),
+// Garner + scale-round (K:158-199), and writes the share element (pi_y^-1).
+// Replaces k_decrypt_inv (mode 1) + k_decode_gather: one launch, no scratch.
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5))
+    k_decrypt_share_cluster(PbDev P, const uint32_t* sk, const uint32_t* ct, int64_t nP, const int32_t* out_pos,
+                            const int64_t* out_dst, int U, uint64_t* share) {
+  namespace cg = cooperative_groups;
+  using Nt = pb::Ntt<LOGN>;
+  constexpr int N = Nt::N;
+  extern __shared__ uint32_t sm[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int tid = threadIdx.x;
+  const int L = P.L;
+  const int l = (int)cluster.block_rank();
+  const int64_t p = blockIdx.x / L;
+  const uint32_t q = P.q[l];
+  const uint64_t mu = P.mu[l];
+  uint32_t a[32], b[32];
+  Nt::gld3(ct + ((p * 2 + 1) * L + l) * N, a, tid);
+  Nt::gld3(sk + (size_t)l * N, b, tid);
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = mulmod(a[c], b[c], q, mu);
+  Nt::gld3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = addmod(a[c], b[c], q);
+  Nt::inverse(a, sm, P.tw_inv + (size_t)l * N, P.tw3_inv + (size_t)l * P.tw3_stride, tid, q);
+  const uint32_t ni = P.ninv[l], nis = P.ninv_sh[l];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = mul_shoup(a[c], ni, nis, q);
+  __syncthreads();
+  Nt::st1(sm, a, tid);
+  cluster.sync();  // every limb's row is in its CTA's shared memory
+  const uint32_t* rows[PB_MAXL];
+#pragma unroll
+  for (int k = 0; k < PB_MAXL; ++k) rows[k] = k < L ? cluster.map_shared_rank(sm, k) : nullptr;
+  const int32_t* pos = out_pos + p * U;
+  const int64_t* dst = out_dst + p * U;
+  for (int u = l * Nt::T + tid; u < U; u += L * Nt::T) {
+    const int j = __ldg(pos + u);
+    if (j < 0) continue;
+    uint32_t x[PB_MAXL], d[PB_MAXL];
+#pragma unroll
+    for (int k = 0; k < PB_MAXL; ++k) x[k] = k < L ? rows[k][Nt::pad(j)] : 0u;
+    garner_dev(P, x, 1, d);
+    share[__ldg(dst + u)] = scale_round_dev(P, d);
+  }
+  cluster.sync();  // peers may still be reading this CTA's shared memory
+}
+
 __global__ void k_decode_dense(PbDev P, const uint32_t* x, int64_t nP, uint64_t* out) {
   const int N = P.N, L = P.L;
   const int64_t total = nP * N;
@@ -471,6 +527,28 @@ void launch_encrypt_sk(const PbDev& P, const uint32_t* sk, PbPack src, int64_t n
   const size_t smem = Nt::SMEM_WORDS * 4;
   set_smem(k_encrypt_sk<LOGN>, smem);
   k_encrypt_sk<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, sk, src, nP, a_in, e, seed, seed_dev, nonce, ct);
+}
+
+template <int LOGN>
+int launch_decrypt_share_cluster(const PbDev& P, const uint32_t* sk, const uint32_t* ct, int64_t nP,
+                                 const int32_t* out_pos, const int64_t* out_dst, int U, uint64_t* share,
+                                 cudaStream_t st) {
+  using Nt = pb::Ntt<LOGN>;
+  const size_t smem = Nt::SMEM_WORDS * 4;
+  set_smem(k_decrypt_share_cluster<LOGN>, smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nP * P.L));
+  cfg.blockDim = dim3(Nt::T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)P.L;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, k_decrypt_share_cluster<LOGN>, P, sk, ct, nP, out_pos, out_dst, U, share);
 }
 
 template <int LOGN>
@@ -643,6 +721,12 @@ extern "C" int pb_decrypt_to_share(const pb_ctx* ctx, const uint32_t* sk, const 
   if (nP <= 0 || U <= 0) return PB_OK;
   if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
   cudaStream_t st = pb_stream_of(stream);
+  if (ctx->dev.logN == 13 && ctx->dev.L >= 2) {  // fused cluster kernel (one launch, DSMEM limb exchange)
+    const int rc = launch_decrypt_share_cluster<13>(ctx->dev, sk, ct, nP, out_pos, out_dst, U, share_out, st);
+    if (rc != 0) return pb_set_error(PB_ERR_CUDA, cudaGetErrorString((cudaError_t)rc));
+    PB_CHECK_LAUNCH();
+    return PB_OK;
+  }
   PB_DISPATCH_LOGN(ctx->dev.logN, launch_decrypt_inv, ctx->dev, sk, ct, nP, 1, out_pos, U, scratch, st);
   PB_CHECK_LAUNCH();
   k_decode_gather<<<pb_grid_1d(nP * U, 128), 128, 0, st>>>(ctx->dev, scratch, nP, U, out_pos, out_dst, share_out);

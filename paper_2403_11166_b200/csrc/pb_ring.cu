@@ -34,6 +34,14 @@ __global__ void k_ring_binary(int op, uint64_t* out, const uint64_t* a, const ui
   }
 }
 
+// out[i] = a[i] + b[(i / inner) % bn] mod 2^ell: bias add along a channel axis.
+__global__ void k_ring_add_bcast(uint64_t* out, const uint64_t* a, const uint64_t* b, int64_t n, int64_t inner,
+                                 int64_t bn, int ell) {
+  const uint64_t m = ring_mask(ell);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (a[i] + b[(i / inner) % bn]) & m;
+}
+
 __global__ void k_ring_unary(int op, uint64_t* out, const uint64_t* a, uint64_t k, int64_t n, int ell) {
   const uint64_t m = ring_mask(ell);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -233,6 +241,13 @@ __global__ void k_dealer(int op, uint64_t* mo, uint64_t* dov, int64_t n, int k, 
       }
       case PB_DEALER_TRUNC: y = (uint64_t)(to_signed(x, ell) >> k) & m; break;
       case PB_DEALER_SELECT: y = d_in[i] ? x : 0ull; break;
+      case PB_DEALER_RELU_TRUNC: {  // trunc_k(relu(x)): the relu reshare is never observed
+        const bool pos = to_signed(x, ell) >= 0;
+        if (d_out) d_out[i] = pos ? 1 : 0;
+        y = pos ? ((uint64_t)(to_signed(x, ell) >> k) & m) : 0ull;
+        break;
+      }
+      case PB_DEALER_TRUNC_SELECT: y = d_in[i] ? ((uint64_t)(to_signed(x, ell) >> k) & m) : 0ull; break;
       default: y = x; break;
     }
     const uint64_t r = philox_np_raw(seed, stream_id, off + (uint64_t)i) >> shift;
@@ -379,8 +394,9 @@ extern "C" int pb_dealer_op(int op, uint64_t* mo, uint64_t* do_, int64_t n, int3
                             uint64_t raw_offset, int32_t ell,
                             void* stream) {
   if (n > 0 && (!mo || !do_)) return pb_set_error(PB_ERR_ARG, "null argument");
-  if (op < PB_DEALER_RELU || op > PB_DEALER_RESHARE) return pb_set_error(PB_ERR_ARG, "bad dealer op");
-  if (op == PB_DEALER_SELECT && !d_in) return pb_set_error(PB_ERR_ARG, "select needs d_in");
+  if (op < PB_DEALER_RELU || op > PB_DEALER_TRUNC_SELECT) return pb_set_error(PB_ERR_ARG, "bad dealer op");
+  if ((op == PB_DEALER_SELECT || op == PB_DEALER_TRUNC_SELECT) && !d_in)
+    return pb_set_error(PB_ERR_ARG, "select needs d_in");
   if (ell < 2 || ell > 63 || k < 0 || k >= ell) return pb_set_error(PB_ERR_ARG, "bad ell / shift");
   if (n <= 0) return PB_OK;
   k_dealer<<<RING_GRID(n)>>>(op, mo, do_, n, k, d_in, d_out, seed, seed_dev, stream_id, raw_offset, ell);
@@ -416,4 +432,14 @@ void pb_launch_ring_matmul_small(const uint64_t* a, const uint64_t* b, int64_t n
                                  int trans_b, uint64_t mask, uint64_t* out, cudaStream_t st) {
   dim3 blk(16, 16), grd((unsigned)((m + 15) / 16), (unsigned)((n + 15) / 16));
   k_ring_matmul<16><<<grd, blk, 0, st>>>(a, b, n, k, m, trans_a, trans_b, mask, out);
+}
+
+extern "C" int pb_ring_add_bcast(uint64_t* out, const uint64_t* a, const uint64_t* b, int64_t n, int64_t inner,
+                                 int64_t bn, int32_t ell, void* stream) {
+  if (n > 0 && (!out || !a || !b)) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (inner < 1 || bn < 1 || bad_ell(ell)) return pb_set_error(PB_ERR_ARG, "bad broadcast / ell");
+  if (n <= 0) return PB_OK;
+  k_ring_add_bcast<<<RING_GRID(n)>>>(out, a, b, n, inner, bn, ell);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
 }

@@ -50,6 +50,11 @@ MSG_GRADB = 0x31
 FRAME_HEADER = 12  # {u16 type, u16 flags, u64 len}
 
 
+import os as _os
+
+_SERIAL = _os.environ.get("PB_SERIAL", "0") == "1"
+
+
 def stream_id(layer: int, op: int, purpose: int) -> int:
     return 1_000_000 + 1000 * layer + 10 * op + purpose
 
@@ -183,7 +188,11 @@ class Session:
 
     def _side_streams(self):
         """The (DO encrypt, MO encode) side streams forked by he_eval, one pair
-        per calling stream so concurrent protocol calls do not serialise."""
+        per calling stream so concurrent protocol calls do not serialise.
+        (PB_SERIAL=1: run everything on the calling stream -- an experiment knob.)"""
+        if _SERIAL:
+            cur = torch.cuda.current_stream()
+            return cur, cur
         key = torch.cuda.current_stream().cuda_stream
         if key not in self._streams:
             self._streams[key] = (torch.cuda.Stream(), torch.cuda.Stream())
@@ -192,6 +201,8 @@ class Session:
     def grad_stream(self) -> torch.cuda.Stream:
         """Stream the training step runs weight-gradient protocols on, concurrently
         with the input-gradient chain (they are independent given grad Y)."""
+        if _os.environ.get("PB_SERIAL_GRAD", "0") == "1":
+            return torch.cuda.current_stream()
         if self._grad_stream is None:
             self._grad_stream = torch.cuda.Stream()
         return self._grad_stream
@@ -319,6 +330,14 @@ def _ring_bin(op, a, b, ell, bn=None) -> torch.Tensor:
     return out
 
 
+def _add_bcast(a: torch.Tensor, b: torch.Tensor, inner: int, ell: int) -> torch.Tensor:
+    """a + b broadcast along an axis (b[(i / inner) % len(b)]), one kernel."""
+    out = torch.empty_like(a)
+    _lib.call("pb_ring_add_bcast", _dev.ptr(out), _dev.ptr(a), _dev.ptr(b), a.numel(), inner, b.numel(), ell,
+              _dev.stream())
+    return out
+
+
 def _check_share_pair(a: ShareTensor, b: ShareTensor):
     if {a.owner_role, b.owner_role} != {MO, DO}:
         raise DesyncError("need one MO share and one DO share")
@@ -353,8 +372,7 @@ def linear_forward(sess: Session, layer: int, W: RingTensor, b: RingTensor, x_a:
         s_eff = _ring_bin(_lib.RING_SUB, s, _ring_matmul(W.values, x_mo.value.values, n_o, n_i, B, ring.ell), ring.ell)
     y_do = _dev.empty_u64(n_o, B)
     sess.he_matmul(layer, OP_FWD, MatmulGeometry(n_i, n_o, B), y_do, s_eff, v_ct=x_do.value.values, w_pt=W.values)
-    bb = b.values.reshape(n_o, 1).expand(n_o, B).contiguous()
-    y_mo = _ring_bin(_lib.RING_ADD, s, bb, ring.ell)
+    y_mo = _add_bcast(s, b.values, B, ring.ell)
     return (ShareTensor(MO, RingTensor(y_mo, 2 * ring.f, ring, _canonical=True)),
             ShareTensor(DO, RingTensor(y_do, 2 * ring.f, ring, _canonical=True)))
 
@@ -477,8 +495,7 @@ def conv_forward(sess: Session, layer: int, W: RingTensor, b: RingTensor, x_a: S
     plan = plan_conv_layer("fwd", B, c_i, c_o, H, Wd, s, pad, stride, sess.p.N)
     y_do = _dev.empty_u64(B, c_o, oh, ow)
     sess.he_eval(layer, OP_FWD, plan, y_do, s_eff, v_ct=x_do.value.values, w_pt=W.values)
-    bb = b.values.reshape(1, c_o, 1, 1).expand(B, c_o, oh, ow).contiguous()
-    y_mo = _ring_bin(_lib.RING_ADD, msk, bb, ring.ell)
+    y_mo = _add_bcast(msk, b.values, oh * ow, ring.ell)
     return (ShareTensor(MO, RingTensor(y_mo, 2 * ring.f, ring, _canonical=True)),
             ShareTensor(DO, RingTensor(y_do, 2 * ring.f, ring, _canonical=True)))
 

@@ -25,7 +25,8 @@ from .errors import EncodeRangeError, ShapeError
 from .linear_protocols import (Session, conv_backward_input, conv_forward, conv_grad_weight, grad_weight,
                                linear_backward_input, linear_forward, reveal_grad_bias, reveal_grad_bias_conv)
 from . import preprocessing as PP
-from .nonlinear import avgpool_backward, avgpool_forward, relu_backward, relu_forward, truncate
+from .nonlinear import (avgpool_backward, avgpool_forward, relu_backward, relu_forward, relu_truncate, truncate,
+                        truncate_relu_backward)
 from .poly_encoding import conv_out_hw
 from .ring import DO, MO, RingParams, RingTensor, SeededRng, ShareTensor, arith_shift, encode_fixed
 
@@ -199,8 +200,7 @@ def forward_phase(sess: Session, model: Model, x: RingTensor, prep=None):
             y = conv_forward(sess, l, model.W[l], model.B[l], *cur, e[4], e[5], mo_x_zero=(l == 0))
         ys.append(y)
         if l < L - 1:
-            z_mo, z_do, d = relu_forward(sess, l, *y)
-            cur = truncate(sess, l, z_mo, z_do, f)
+            *cur, d = relu_truncate(sess, l, *y, f)  # ReLU + truncation, one dealer round
             ds.append(d)
             for k in seg[l]:
                 if model.layers[k][0] == "pool":
@@ -255,14 +255,21 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
             else:
                 H, Wd = acts[l][1].shape[2:]
                 ga = conv_backward_input(sess, l, model.W[l], gy_mo, gy_do, H, Wd, e[4], e[5], mo_gy_zero=last)
-            t_mo, t_do = truncate(sess, l, *ga, f, backward=True)
-            for k in reversed(seg[l - 1]):
-                if model.layers[k][0] == "pool":
-                    t_mo, t_do = avgpool_backward(sess, l - 1, t_mo, t_do)
-                elif model.layers[k][0] == "flatten":
+            if any(model.layers[k][0] == "pool" for k in seg[l - 1]):
+                t_mo, t_do = truncate(sess, l, *ga, f, backward=True)
+                for k in reversed(seg[l - 1]):
+                    if model.layers[k][0] == "pool":
+                        t_mo, t_do = avgpool_backward(sess, l - 1, t_mo, t_do)
+                    elif model.layers[k][0] == "flatten":
+                        chw = model.io[k][0]
+                        t_mo, t_do = _unflatten(t_mo, chw), _unflatten(t_do, chw)
+                gy_mo, gy_do = relu_backward(sess, l - 1, ds[l - 1], t_mo, t_do)
+            else:  # truncation + ReLU' in one dealer round (a flatten in between is a pure permutation)
+                t_mo, t_do = ga
+                for k in reversed(seg[l - 1]):
                     chw = model.io[k][0]
                     t_mo, t_do = _unflatten(t_mo, chw), _unflatten(t_do, chw)
-            gy_mo, gy_do = relu_backward(sess, l - 1, ds[l - 1], t_mo, t_do)
+                gy_mo, gy_do = truncate_relu_backward(sess, l - 1, ds[l - 1], t_mo, t_do, f)
     main.wait_stream(gstream)
     del keep
     model.sgd(gws, gbs, lr, momentum, check=check)

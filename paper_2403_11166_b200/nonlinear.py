@@ -101,3 +101,25 @@ def avgpool_backward(sess: Session, layer: int, a: ShareTensor, b: ShareTensor):
                             ShareTensor(DO, RingTensor(rd, s, ring, _canonical=True)), k=2)
     return (ShareTensor(MO, RingTensor(x_mo, s, ring, _canonical=True)),
             ShareTensor(DO, RingTensor(x_do, s, ring, _canonical=True)))
+
+
+def relu_truncate(sess: Session, layer: int, a: ShareTensor, b: ShareTensor, bits: int):
+    """ReLU followed by the forward truncation in ONE dealer round: the
+    output shares are the truncation's reshare (stream (layer, OP_TRUNC_F)) of
+    arith_shift(relu(x), bits) -- exactly the two-step composition's, since the
+    ReLU's own reshare is consumed by the truncation and never observed."""
+    x_mo, x_do, d = _dealer(sess, layer, OP_TRUNC_F, _lib.DEALER_RELU_TRUNC, a, b, k=bits, want_d=True)
+    s = a.scale - bits
+    return (ShareTensor(MO, RingTensor(x_mo, s, sess.ring, _canonical=True)),
+            ShareTensor(DO, RingTensor(x_do, s, sess.ring, _canonical=True)), d)
+
+
+def truncate_relu_backward(sess: Session, layer_relu: int, d: torch.Tensor, a: ShareTensor, b: ShareTensor,
+                           bits: int):
+    """Backward truncation of grad X followed by ReLU' (cached d) in ONE dealer
+    round; output shares = the ReLU-backward reshare (stream (layer_relu,
+    OP_RELU_B)) of d * arith_shift(x, bits), as the two-step composition."""
+    x_mo, x_do, _ = _dealer(sess, layer_relu, OP_RELU_B, _lib.DEALER_TRUNC_SELECT, a, b, k=bits, d_in=d)
+    s = a.scale - bits
+    return (ShareTensor(MO, RingTensor(x_mo, s, sess.ring, _canonical=True)),
+            ShareTensor(DO, RingTensor(x_do, s, sess.ring, _canonical=True)))

@@ -201,12 +201,6 @@ class PrepState:
             self.banks.append([prep_operator(sess, l, Operator(spec, op, B, hw), m, bank_seed) for op in range(4)])
 
 
-def _bias_bcast(b: RingTensor, shape, fc: bool) -> torch.Tensor:
-    if fc:
-        return b.values.reshape(-1, 1).expand(*shape).contiguous()
-    return b.values.reshape(1, -1, 1, 1).expand(*shape).contiguous()
-
-
 def _add(a, b, ell):
     out = torch.empty_like(a)
     _lib.call("pb_ring_binary", _lib.RING_ADD, _dev.ptr(out), _dev.ptr(a), _dev.ptr(b), a.numel(), a.numel(), ell,
@@ -220,8 +214,10 @@ def prep_linear_forward(sess, layer: int, banks, W: RingTensor, b: RingTensor, x
     ring = sess.ring
     opd = banks[FWD].opd
     p0, p1 = online_shared_product(sess, layer, banks[FWD], W.values, x_do.value.values)
-    y0 = _add(_add(p0, opd.apply(W.values, x_mo.value.values, ring.ell), ring.ell),
-              _bias_bcast(b, p0.shape, opd.is_fc), ring.ell)
+    from .linear_protocols import _add_bcast
+
+    inner = p0.shape[1] if opd.is_fc else p0.shape[2] * p0.shape[3]
+    y0 = _add_bcast(_add(p0, opd.apply(W.values, x_mo.value.values, ring.ell), ring.ell), b.values, inner, ring.ell)
     return (ShareTensor(MO, RingTensor(y0, 2 * ring.f, ring, _canonical=True)),
             ShareTensor(DO, RingTensor(p1, 2 * ring.f, ring, _canonical=True)))
 
