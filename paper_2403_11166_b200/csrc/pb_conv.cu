@@ -17,6 +17,8 @@
 // accumulators in registers and reduces them through shared memory.
 #include "pb_common.cuh"
 
+#include <stdlib.h>
+
 namespace {
 
 __host__ __device__ __forceinline__ uint64_t cmask(int ell) { return ell >= 64 ? ~0ull : ((1ull << ell) - 1); }
@@ -333,6 +335,22 @@ int conv_gemm_launch(int kind, const ConvDims& d, const uint64_t* a, const uint6
 
 }  // namespace
 
+int pb_imma_conv(int kind, const uint64_t* a, const uint64_t* b, int B, int ci, int co, int H, int W, int s, int p,
+                 int st_, int oh, int ow, int ell, uint64_t* out, cudaStream_t st);
+int pb_imma_matmul(const uint64_t* a, const uint64_t* b, int n, int k, int m, int ta, int tb, int ell, uint64_t* out,
+                   cudaStream_t st);
+
+// int8-limb tensor-core path for large ring GEMMs (pb_imma.cu); PB_IMMA=0 disables it.
+static bool imma_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PB_IMMA");
+    on = e ? atoi(e) : 1;
+  }
+  return on != 0;
+}
+constexpr int64_t IMMA_MIN_MACS = 1ll << 27;
+
 extern "C" int pb_ring_conv(int kind, const uint64_t* a, const uint64_t* b, int32_t B, int32_t c_i, int32_t c_o,
                             int32_t H, int32_t W, int32_t s, int32_t pad, int32_t stride, int32_t ell, uint64_t* out,
                             void* stream) {
@@ -348,6 +366,15 @@ extern "C" int pb_ring_conv(int kind, const uint64_t* a, const uint64_t* b, int3
   const int64_t big = (int64_t)B * (c_i > c_o ? c_i : c_o) * (H > oh ? H : oh) * (W > ow ? W : ow);
   if (big >= (1ll << 31) || (int64_t)c_o * c_i * s * s >= (1ll << 31))
     return pb_set_error(PB_ERR_GEOMETRY, "conv tensor too large for 32-bit indexing");
+  {
+    const int64_t macs = (int64_t)B * c_o * c_i * s * s * oh * ow;
+    // the weight gradient's skinny int8 GEMMs (64 x 1600 outputs, K = B*oh*ow) lose to the CUDA-core path
+    if (imma_enabled() && kind != PB_CONV_GRADW && macs >= IMMA_MIN_MACS &&
+        pb_imma_conv(kind, a, b, B, c_i, c_o, H, W, s, pad, stride, oh, ow, ell, out, st) == PB_OK) {
+      PB_CHECK_LAUNCH();
+      return PB_OK;
+    }
+  }
   switch (s) {  // tiled implicit GEMM for the kernel sizes the models use
     case 1: conv_gemm_launch<1>(kind, d, a, b, m, out, st); PB_CHECK_LAUNCH(); return PB_OK;
     case 3: conv_gemm_launch<3>(kind, d, a, b, m, out, st); PB_CHECK_LAUNCH(); return PB_OK;
@@ -419,6 +446,11 @@ extern "C" int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, i
   }
   if (n * k * m < (1ll << 24)) {  // the FC layers' local terms: one small launch beats tiles + split-K passes
     pb_launch_ring_matmul_small(a, b, n, k, m, trans_a, trans_b, mask, out, st);
+    PB_CHECK_LAUNCH();
+    return PB_OK;
+  }
+  if (imma_enabled() && n * k * m >= IMMA_MIN_MACS &&
+      pb_imma_matmul(a, b, (int)n, (int)k, (int)m, trans_a, trans_b, ell, out, st) == PB_OK) {
     PB_CHECK_LAUNCH();
     return PB_OK;
   }

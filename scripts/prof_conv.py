@@ -32,3 +32,13 @@ torch.cuda.synchronize()
 macs = B * co * ci * s * s * H * W
 print("fwd/bwdx/gradw ms", [round(ev[i].elapsed_time(ev[i + 1]), 3) for i in range(3)], "MAC/s",
       [f"{macs / (ev[i].elapsed_time(ev[i + 1]) / 1e3):.3e}" for i in range(3)])
+# per-operator timing loop (10 reps each) for steadier numbers
+for kind, shp, xa, xb in ((_lib.CONV_FWD, (B, co, H, W), x, w), (_lib.CONV_BWDX, (B, ci, H, W), gy, w),
+                          (_lib.CONV_GRADW, (co, ci, s, s), x, gy)):
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(10):
+        _ring_conv(kind, xa, xb, *args, shp)
+    s1.record()
+    torch.cuda.synchronize()
+    print("kind", kind, "ms", round(s0.elapsed_time(s1) / 10, 3))
