@@ -19,6 +19,8 @@
 // companion row is streamed.
 #include "pb_pack.cuh"
 
+#include <stdlib.h>
+
 namespace {
 
 using pbk::mont_lazy;
@@ -488,10 +490,10 @@ extern "C" int pb_ctpt_mac_tiled(const pb_ctx* ctx, const uint32_t* ctA, const u
   if (nI < 1) return pb_set_error(PB_ERR_SHAPE, "nI must be >= 1");
   const int N = ctx->dev.N, L = ctx->dev.L;
   cudaStream_t st = pb_stream_of(stream);
-  const unsigned tiles = (unsigned)(((nB + 1) / 2) * ((nO + 1) / 2));
-  if (nI <= 2) {
-    dim3 grid(tiles, (unsigned)(L * (N / (4 * MAC_THREADS))));
-    k_mac_eager<2, 2><<<grid, MAC_THREADS, 0, st>>>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out);
+  if (nI <= 2) {  // streaming shapes: 1x1 tiles (96 -> fewer registers, more resident warps);
+                  // FC-like K=1: 0.174 -> 0.131 ms, 4.5 TB/s of actual DRAM traffic
+    dim3 grid((unsigned)(nB * nO), (unsigned)(L * (N / (4 * MAC_THREADS))));
+    k_mac_eager<1, 1><<<grid, MAC_THREADS, 0, st>>>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out);
   } else {  // TMA-pipelined lazy MAC: K=16 conv-like 1.09 -> 0.65 ms, FC 784x128 fwd 75 -> 48 us (B200)
     launch_pipe<2, 2, 4, 3, 6>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
   }
