@@ -266,18 +266,23 @@ def he_plain_mul(ct: Ciphertext, w) -> Ciphertext:
     return Ciphertext(out, p)
 
 
-def noise_budget(kp: KeyPair, ct: Ciphertext) -> int:
+def noise_budget(kp: KeyPair, ct: Ciphertext, slots=None) -> int:
     """Invariant noise budget log2(Q) - log2(|t*x mod Q|_inf) - 1 of ct[0].
-    A diagnostic: the INTT runs on the device, the CRT lift on the host."""
+    A diagnostic: the INTT runs on the device, the CRT lift on the host.
+    ``slots`` restricts the maximum to the given coefficient positions (the
+    useful slots of a masked protocol ciphertext, whose other coefficients
+    carry uniform filler by design)."""
     p = kp.params
     x = _dev.to_numpy_u32(decrypt_coeffs(kp, Ciphertext(ct.data[:1].contiguous(), p)))[0]
     Q, t = p.Q, p.t
-    comp = [0] * p.N
+    idx = list(range(p.N)) if slots is None else [int(j) for j in slots if int(j) >= 0]
+    comp = [0] * len(idx)
     for l, q in enumerate(p.moduli):
         Ml = Q // q
         c = Ml * pow(Ml % q, -1, q)
-        for j, v in enumerate(x[l].tolist()):
-            comp[j] += v * c
+        row = x[l]
+        for n, j in enumerate(idx):
+            comp[n] += int(row[j]) * c
     worst = 0
     for v in comp:
         w = (v % Q) * t % Q

@@ -163,6 +163,7 @@ class Session:
         self._seed_dev = None
         self._streams = {}
         self._grad_stream = None
+        self.capture = None  # diagnostics: a list receives (masked output ciphertexts, useful slot positions)
 
     def rng(self, layer: int, op: int, purpose: int) -> SeededRng:
         g = SeededRng(self.seed, stream_id(layer, op, purpose))
@@ -300,6 +301,8 @@ class Session:
                 n_pt = (sh.n_pt if ctA is not None else 0) + (sh.n_in if ctB is not None else 0)
                 self._count("pb_ctpt_mac_tiled", n_ct * ct_bytes + n_pt * L * N * w + sh.n_out * (ct_bytes + L * N * w))
             self.channel.send(MO, msg_out, out_ct, Ciphertext(out_ct, p).nbytes_wire())
+            if self.capture is not None:
+                self.capture.append((out_ct.clone(), sh.out_pos.clone()))
             scratch = _dev.empty_u32(sh.n_out, L, sh.U)
             _lib.call("pb_decrypt_to_share", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(out_ct), sh.n_out,
                       _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U, _dev.ptr(out), _dev.ptr(scratch), st)
