@@ -289,11 +289,10 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   Nt::gld3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = addmod(a[c], b[c], q);
-  Nt::inverse(a, sm, P.tw_inv + (size_t)l * N, P.tw3_inv + (size_t)l * P.tw3_stride, tid, q);
   const uint32_t ni = P.ninv[l], nis = P.ninv_sh[l];
+  Nt::inverse_scaled(a, sm, P.tw_inv + (size_t)l * N, P.tw3_inv + (size_t)l * P.tw3_stride, tid, q, ni, nis,
+                     P.w0n[l], P.w0n_sh[l]);
   if (mode == 0) {
-#pragma unroll
-    for (int c = 0; c < 32; ++c) a[c] = mul_shoup(a[c], ni, nis, q);
     Nt::gst1(out32 + (p * L + l) * N, a, tid);
   } else {
     __syncthreads();
@@ -307,7 +306,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
       for (int k = 0; k < 8; ++k) j[k] = u0 + k * Nt::T < U ? __ldg(pos + u0 + k * Nt::T) : -1;
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (j[k] >= 0) dst[u0 + k * Nt::T] = mul_shoup(sm[Nt::pad(j[k])], ni, nis, q);
+        if (j[k] >= 0) dst[u0 + k * Nt::T] = sm[Nt::pad(j[k])];  // already scaled by N^-1
     }
   }
 }
@@ -386,10 +385,8 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   Nt::gld3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = addmod(a[c], b[c], q);
-  Nt::inverse(a, sm, P.tw_inv + (size_t)l * N, P.tw3_inv + (size_t)l * P.tw3_stride, tid, q);
-  const uint32_t ni = P.ninv[l], nis = P.ninv_sh[l];
-#pragma unroll
-  for (int c = 0; c < 32; ++c) a[c] = mul_shoup(a[c], ni, nis, q);
+  Nt::inverse_scaled(a, sm, P.tw_inv + (size_t)l * N, P.tw3_inv + (size_t)l * P.tw3_stride, tid, q, P.ninv[l],
+                     P.ninv_sh[l], P.w0n[l], P.w0n_sh[l]);
   __syncthreads();
   Nt::st1(sm, a, tid);
   cluster.sync();  // every limb's row is in its CTA's shared memory

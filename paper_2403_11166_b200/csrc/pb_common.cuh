@@ -19,6 +19,7 @@ struct PbDev {
   uint64_t t_mask;
   uint32_t q[PB_MAXL];
   uint32_t ninv[PB_MAXL], ninv_sh[PB_MAXL];    // N^-1 mod q and its Shoup quotient
+  uint32_t w0n[PB_MAXL], w0n_sh[PB_MAXL];      // last inverse stage's twiddle psi^-brv(1) * N^-1 (+ Shoup)
   uint32_t delta[PB_MAXL], delta_sh[PB_MAXL];  // floor(Q/t) mod q_i
   uint64_t mu[PB_MAXL];                        // floor(2^64 / q) (Barrett)
   double inv_q32[PB_MAXL];                     // 2^32 / q (Shoup quotient estimate)

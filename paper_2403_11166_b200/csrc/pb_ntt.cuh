@@ -249,6 +249,44 @@ struct Ntt {
     inv_p1(a, st, q);
   }
 
+  // Inverse with the N^-1 scaling folded into the last (stage-0) GS butterfly:
+  // x' = (x + y) N^-1, y' = (x - y) (w N^-1) -- 16 Shoup products per thread
+  // instead of the 32 of a separate scaling pass.  Canonical [0, q) output in
+  // P1 layout.  (wn, wns) = psi^-brv(1) N^-1 and its Shoup quotient.
+  __device__ __forceinline__ static void inverse_scaled(uint32_t (&a)[32], uint32_t* sm, const uint2* tw,
+                                                        const uint2* t3, int tid, uint32_t q, uint32_t ni,
+                                                        uint32_t nis, uint32_t wn, uint32_t wns) {
+    uint2* st = stw(sm);
+    st[tid] = __ldg(tw + tid);
+    inv_p3(a, t3, tid, q);
+    st3(sm, a, tid);
+    __syncthreads();
+    ld2(sm, a, tid);
+    inv_p2(a, st, tid, q);
+    __syncthreads();
+    st2(sm, a, tid);
+    __syncthreads();
+    ld1(sm, a, tid);
+    const uint32_t q2 = 2 * q;
+#pragma unroll
+    for (int ss = 0; ss < 4; ++ss) {  // stages 4..1 as in inv_p1
+      const int s = 4 - ss;
+      const int tc = 16 >> s;
+      uint2 w[16];
+#pragma unroll
+      for (int g = 0; g < (1 << s); ++g) w[g] = st[(1 << s) + g];
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (!(c & tc)) gs_bfly(a[c], a[c + tc], w[c >> (5 - s)], q, q2);
+    }
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {  // stage 0 with the scaling folded in
+      const uint32_t x = a[c], y = a[c + 16];  // [0, 2q)
+      a[c] = mul_shoup(x + y, ni, nis, q);
+      a[c + 16] = mul_shoup(x - y + q2, wn, wns, q);
+    }
+  }
+
   // ---- NTT-domain rows in DEVICE ORDER: bit-reversed index j = tid*32 + 4v + k
   // (the P3 layout) is stored at address v*4T + tid*4 + k, so a P3-layout
   // register file moves to/from HBM with fully coalesced 128-bit accesses.

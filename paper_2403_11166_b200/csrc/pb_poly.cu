@@ -124,6 +124,9 @@ extern "C" int pb_ctx_create(const pb_params* p, pb_ctx** out) {
       h_f[(size_t)l * N + k] = make_uint2(wf, h_shoup(wf, (uint32_t)q));
       h_i[(size_t)l * N + k] = make_uint2(wi, h_shoup(wi, (uint32_t)q));
     }
+    // N^-1 folded into the last inverse stage (pb_ntt.cuh inverse_scaled)
+    d.w0n[l] = (uint32_t)h_mulmod(h_i[(size_t)l * N + 1].x, d.ninv[l], q);
+    d.w0n_sh[l] = h_shoup(d.w0n[l], (uint32_t)q);
   }
   free(pw); free(ipw);
   // P3-stage tables (register NTT, N >= 2048): stage D (s = logN-5+D) at
@@ -234,10 +237,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN)) k_ntt_inv(PbD
     uint32_t* row = rows + r * Nt::N;
     uint32_t a[32];
     Nt::gld3(row, a, tid);
-    Nt::inverse(a, sm, tw, t3, tid, q);
-    const uint32_t ni = P.ninv[limb], nis = P.ninv_sh[limb];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) a[c] = mul_shoup(a[c], ni, nis, q);
+    Nt::inverse_scaled(a, sm, tw, t3, tid, q, P.ninv[limb], P.ninv_sh[limb], P.w0n[limb], P.w0n_sh[limb]);
     Nt::gst1(row, a, tid);
     __syncthreads();
   }
