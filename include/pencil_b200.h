@@ -162,6 +162,20 @@ int pb_encrypt_sk_noise(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint64_
                         const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int64_t P,
                         const uint32_t* a, const int8_t* e, uint32_t* ct, void* stream);
 
+/* Split symmetric encryption: the ciphertexts of pb_encrypt_sk_noise, with
+ * the message-independent work moved off the protocol's critical path.
+ * pb_encrypt_sk_zero precomputes, elementwise (no NTT), ct = (-a*s, a) with
+ * a the same uniform draw pb_encrypt_sk makes under (seed, nonce), and the
+ * noise e int8 [P][N] (CBD(20), one draw per polynomial).  pb_encrypt_sk_add
+ * then sets c0 += NTT(e + Delta m) in place: the result equals
+ * pb_encrypt_sk_noise(m, a, e) bit for bit.  Replaces the same SPEC:139-147
+ * encrypt as pb_encrypt_sk (mode "sk"). */
+int pb_encrypt_sk_zero(const pb_ctx* ctx, const uint32_t* sk_ntt, int64_t P, uint64_t seed,
+                       const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct, int8_t* e, void* stream);
+int pb_encrypt_sk_add(const pb_ctx* ctx, const uint64_t* vals, const int32_t* pack_pos,
+                      const int32_t* pack_src, int32_t Z, int64_t P, const int8_t* e, uint32_t* ct,
+                      void* stream);
+
 /* x = INTT(c0 + c1*s) in coefficient form, x [P][L][N]. */
 int pb_decrypt_coeffs(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint32_t* ct, int64_t P,
                       uint32_t* x, void* stream);

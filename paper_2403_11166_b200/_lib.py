@@ -61,6 +61,8 @@ SIGNATURES = {
     "pb_encrypt_pk": [P, P, P, P, P, I32, I64, U64, P, U64, P, P],
     "pb_encrypt_pk_noise": [P, P, P, P, P, I32, I64, P, P, P, P, P],
     "pb_encrypt_sk": [P, P, P, P, P, I32, I64, U64, P, U64, P, P],
+    "pb_encrypt_sk_zero": [P, P, I64, U64, P, U64, P, P, P],
+    "pb_encrypt_sk_add": [P, P, P, P, I32, I64, P, P, P],
     "pb_encrypt_sk_noise": [P, P, P, P, P, I32, I64, P, P, P, P],
     "pb_decrypt_coeffs": [P, P, P, I64, P, P],
     "pb_decrypt": [P, P, P, I64, P, P, P],

@@ -163,6 +163,37 @@ def encrypt(kp: KeyPair, m: torch.Tensor, rng=None, *, pack=None, mode: str = "p
     return Ciphertext(ct, params)
 
 
+def encrypt_zero(kp: KeyPair, P: int, rng, nonce: int | None = None):
+    """The message-independent half of ``encrypt(mode="sk")`` for P
+    ciphertexts: returns (ct = (-a s, a), e int8 [P, N]).  ``a`` is the draw
+    ``encrypt`` makes under the same (rng, nonce); the engine keeps a pool of
+    these off the protocol's critical path."""
+    params = kp.params
+    ct = _dev.empty_u32(P, 2, params.L, params.N)
+    e = torch.empty(P, params.N, dtype=torch.int8, device=_dev.device())
+    seed, sptr = rng.dev_args()
+    if nonce is None:
+        nonce = rng.reserve(P)
+    _lib.call("pb_encrypt_sk_zero", _ctx(params), _dev.ptr(kp.sk_ntt), P, seed, sptr, nonce, _dev.ptr(ct),
+              _dev.ptr(e), _dev.stream())
+    return Ciphertext(ct, params), e
+
+
+def encrypt_add(pre, m: torch.Tensor, *, pack=None) -> Ciphertext:
+    """In place on ``pre`` = encrypt_zero(...): c0 += NTT(e + Delta m), giving
+    the ciphertext ``encrypt(..., mode="sk", noise=(a, e))`` would."""
+    ct, e = pre
+    params = ct.params
+    m = m.contiguous()
+    pp, ps, Z, Pk = _pack_args(pack)
+    P = Pk if Pk is not None else m.numel() // params.N
+    if P != ct.data.shape[0] or P != e.shape[0]:
+        raise ShapeError(f"{P} message polynomials for {ct.data.shape[0]} ciphertexts")
+    _lib.call("pb_encrypt_sk_add", _ctx(params), _dev.ptr(m), pp, ps, Z, P, _dev.ptr(e), _dev.ptr(ct.data),
+              _dev.stream())
+    return ct
+
+
 def to_reference_order(params: BfvParams, ntt_rows: torch.Tensor) -> np.ndarray:
     """NTT-domain device rows -> host uint64 array in the reference's
     bit-reversed order (what K's ntt_forward produces)."""

@@ -228,14 +228,17 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
   if (ep) {  // caller-supplied noise (bit-exact oracle runs)
 #pragma unroll
     for (int c = 0; c < 32; ++c) b[c] = addmod(lift_small(ep[Nt::j1(tid, c)], q), b[c], q);
-  } else {  // e ~ CBD(20) from Philox4x32, generated in-kernel: one call covers coefficients j and j+T
+  } else {  // e ~ CBD(20) from Philox4x32, generated in-kernel: one call covers three of this thread's coefficients
     const uint64_t pp = (uint64_t)p + nonce;
 #pragma unroll
-    for (int c = 0; c < 32; c += 2) {
-      const u32x4 r = philox4x32_10((uint32_t)Nt::j1(tid, c), (uint32_t)pp, (uint32_t)(pp >> 32), 0x454e4333u /* "ENC3" */,
-                                    (uint32_t)seed, (uint32_t)(seed >> 32));
-      b[c] = addmod(lift_small(cbd20(r.v[0], r.v[1]), q), b[c], q);
-      b[c + 1] = addmod(lift_small(cbd20(r.v[2], r.v[3]), q), b[c + 1], q);
+    for (int g = 0; g < 11; ++g) {
+      const u32x4 r = philox4x32_10(((uint32_t)tid << 4) | (uint32_t)g, (uint32_t)pp, (uint32_t)(pp >> 32),
+                                    0x454e4335u /* "ENC5" */, (uint32_t)seed, (uint32_t)(seed >> 32));
+      int sv[3];
+      cbd20x3(r, sv);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        if (3 * g + i < 32) b[3 * g + i] = addmod(lift_small(sv[i], q), b[3 * g + i], q);
     }
   }
   Nt::forward(b, sm, P.tw_fwd + (size_t)l * N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
@@ -252,8 +255,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
       const uint4 x = __ldg(a4 + v * Nt::T);
       a[0] = x.x; a[1] = x.y; a[2] = x.z; a[3] = x.w;
     } else {
-      uniform_pair(seed, nonce, p, l, (tid << 4) + 2 * v, q, 0x53454e43u, a[0], a[1]);
-      uniform_pair(seed, nonce, p, l, (tid << 4) + 2 * v + 1, q, 0x53454e43u, a[2], a[3]);
+      uniform_quad(seed, (uint64_t)p + nonce, l, (tid << 3) + v, q, 0x53454e44u /* "SEND" */, a);
     }
     const uint4 sv = __ldg(s4 + v * Nt::T);
     const uint32_t sk_[4] = {sv.x, sv.y, sv.z, sv.w};
@@ -262,6 +264,80 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
     for (int k = 0; k < 4; ++k) o[k] = submod(pb::canon4(b[4 * v + k], q), mulmod(a[k], sk_[k], q, mu), q);
     c0[v * Nt::T] = make_uint4(o[0], o[1], o[2], o[3]);
     c1[v * Nt::T] = make_uint4(a[0], a[1], a[2], a[3]);
+  }
+}
+
+// Split symmetric encryption.  The message-independent part of
+// k_encrypt_sk -- a (uniform, NTT domain), -a*s and the noise e -- is
+// precomputed elementwise by k_encrypt_pre (no NTT: one thread per 128-bit
+// device-order quad, e drawn once per polynomial instead of once per limb);
+// k_encrypt_add then does the message-dependent rest on the critical path:
+// c0 = -a*s + NTT(e + Delta m).  Same a as k_encrypt_sk under (seed, nonce),
+// so k_encrypt_add(pre) == k_encrypt_sk with caller noise (a, e) bit for bit.
+// grid (ceil(N/4 / 256), L, nP): one thread per 128-bit device-order quad.
+__global__ void __launch_bounds__(256) k_encrypt_pre(PbDev P, const uint32_t* sk, uint64_t seed_arg,
+                                                     const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct,
+                                                     int8_t* e) {
+  const uint64_t seed = dev_key(seed_arg, seed_dev);
+  const int N = P.N, L = P.L, T = N >> 5;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;  // quad k = v*T + tid of the row, as k_encrypt_sk's stores
+  if (k >= (N >> 2)) return;
+  const int l = blockIdx.y;
+  const int64_t p = blockIdx.z;
+  const int v = k / T, tid = k - v * T;
+  const uint32_t q = P.q[l];
+  const uint64_t mu = P.mu[l];
+  const uint64_t pp = (uint64_t)p + nonce;
+  uint32_t a[4];
+  uniform_quad(seed, pp, l, (tid << 3) + v, q, 0x53454e44u /* "SEND" */, a);
+  const uint4 sv = __ldg(reinterpret_cast<const uint4*>(sk + (size_t)l * N) + k);
+  const uint32_t sk_[4] = {sv.x, sv.y, sv.z, sv.w};
+  uint32_t o[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) o[c] = submod(0u, mulmod(a[c], sk_[c], q, mu), q);
+  reinterpret_cast<uint4*>(ct + ((p * 2 + 0) * L + l) * N)[k] = make_uint4(o[0], o[1], o[2], o[3]);
+  reinterpret_cast<uint4*>(ct + ((p * 2 + 1) * L + l) * N)[k] = make_uint4(a[0], a[1], a[2], a[3]);
+  if (l == 0 && k < (N + 11) / 12) {  // e ~ CBD(20), once per polynomial: coefficients 12k .. 12k+11
+    int8_t* ep = e + p * N + 12 * k;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const u32x4 r = philox4x32_10(4u * k + g, (uint32_t)pp, (uint32_t)(pp >> 32), 0x454e4334u /* "ENC4" */,
+                                    (uint32_t)seed, (uint32_t)(seed >> 32));
+      int sv[3];
+      cbd20x3(r, sv);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        if (12 * k + 3 * g + i < N) ep[3 * g + i] = (int8_t)sv[i];
+    }
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
+    k_encrypt_add(PbDev P, PbPack src, int64_t nP, const int8_t* e, uint32_t* ct) {
+  using Nt = pb::Ntt<LOGN>;
+  constexpr int N = Nt::N;
+  extern __shared__ uint32_t sm[];
+  const int tid = threadIdx.x;
+  const int L = P.L;
+  const int l = (int)(blockIdx.x / nP);  // limb-major: co-resident CTAs share one limb's twiddles
+  const int64_t p = blockIdx.x % nP;
+  const uint32_t q = P.q[l];
+  uint4* c0 = reinterpret_cast<uint4*>(ct + ((p * 2 + 0) * L + l) * N) + tid;
+#pragma unroll
+  for (int v = 0; v < 8; ++v) asm volatile("prefetch.global.L2 [%0];" ::"l"(c0 + v * Nt::T));
+  const int8_t* ep = e + p * N;
+  uint32_t b[32];
+  load_source<Nt>(b, sm, src, p, tid, [&](uint64_t v) { return delta_m(P, l, v); });
+#pragma unroll
+  for (int c = 0; c < 32; ++c) b[c] = addmod(lift_small(ep[Nt::j1(tid, c)], q), b[c], q);
+  Nt::forward(b, sm, P.tw_fwd + (size_t)l * N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    const uint4 x = c0[v * Nt::T];
+    c0[v * Nt::T] = make_uint4(addmod(x.x, pb::canon4(b[4 * v], q), q), addmod(x.y, pb::canon4(b[4 * v + 1], q), q),
+                               addmod(x.z, pb::canon4(b[4 * v + 2], q), q),
+                               addmod(x.w, pb::canon4(b[4 * v + 3], q), q));
   }
 }
 
@@ -527,6 +603,14 @@ void launch_encrypt_sk(const PbDev& P, const uint32_t* sk, PbPack src, int64_t n
 }
 
 template <int LOGN>
+void launch_encrypt_add(const PbDev& P, PbPack src, int64_t nP, const int8_t* e, uint32_t* ct, cudaStream_t st) {
+  using Nt = pb::Ntt<LOGN>;
+  const size_t smem = Nt::SMEM_WORDS * 4;
+  set_smem(k_encrypt_add<LOGN>, smem);
+  k_encrypt_add<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, src, nP, e, ct);
+}
+
+template <int LOGN>
 int launch_decrypt_share_cluster(const PbDev& P, const uint32_t* sk, const uint32_t* ct, int64_t nP,
                                  const int32_t* out_pos, const int64_t* out_dst, int U, uint64_t* share,
                                  cudaStream_t st) {
@@ -685,6 +769,30 @@ extern "C" int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk, const uint64
   cudaStream_t st = pb_stream_of(stream);
   PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, src, nP, (const uint32_t*)nullptr,
                    (const int8_t*)nullptr, seed, seed_dev, nonce, ct, st);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+extern "C" int pb_encrypt_sk_zero(const pb_ctx* ctx, const uint32_t* sk, int64_t nP, uint64_t seed,
+                                  const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct, int8_t* e, void* stream) {
+  if (int s = need_big_n(ctx)) return s;
+  if (nP <= 0) return PB_OK;
+  if (!sk || !ct || !e) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  if (nP > 65535) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  const dim3 grid((unsigned)((ctx->dev.N / 4 + 255) / 256), (unsigned)ctx->dev.L, (unsigned)nP);
+  k_encrypt_pre<<<grid, 256, 0, pb_stream_of(stream)>>>(ctx->dev, sk, seed, seed_dev, nonce, ct, e);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+extern "C" int pb_encrypt_sk_add(const pb_ctx* ctx, const uint64_t* vals, const int32_t* pack_pos,
+                                 const int32_t* pack_src, int32_t Z, int64_t nP, const int8_t* e, uint32_t* ct,
+                                 void* stream) {
+  if (int s = need_big_n(ctx)) return s;
+  if (nP <= 0) return PB_OK;
+  if (!ct || !e) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
+  PB_PACK_OR_RETURN(src, vals, pack_pos, pack_src, Z);
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_add, ctx->dev, src, nP, e, ct, pb_stream_of(stream));
   PB_CHECK_LAUNCH();
   return PB_OK;
 }

@@ -67,6 +67,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
@@ -185,6 +188,42 @@ __device__ __forceinline__ u32x4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_
   u32x4 o;
   o.v[0] = c0; o.v[1] = c1; o.v[2] = c2; o.v[3] = c3;
   return o;
+}
+
+// Four uniform residues mod q (q < 2^30) from one Philox4x32 call at counter
+// (jq | l << 24, pp, domain): each word is masked to bitlen(q) bits and kept
+// when < q (exactly uniform; rejection probability < 2^-10 for the 30-bit NTT
+// primes, < 1/2 for any q); a rejected word is redrawn as a 64-bit
+// multiply-high sample from its own domain-separated call (statistical
+// distance 2^-34).  Half the Philox work of one 64-bit draw per residue.
+__device__ __forceinline__ void uniform_quad(uint64_t seed, uint64_t pp, int l, int jq, uint32_t q, uint32_t domain,
+                                             uint32_t (&x)[4]) {
+  const uint32_t c0 = (uint32_t)jq | ((uint32_t)l << 24);
+  const u32x4 r = philox4x32_10(c0, (uint32_t)pp, (uint32_t)(pp >> 32), domain, (uint32_t)seed, (uint32_t)(seed >> 32));
+  const uint32_t mask = (2u << (31 - __clz(q))) - 1u;
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    x[i] = r.v[i] & mask;
+    bad |= x[i] >= q;
+  }
+  if (bad) {
+    for (int i = 0; i < 4; ++i) {
+      if (x[i] < q) continue;
+      const u32x4 s = philox4x32_10(c0, (uint32_t)pp, (uint32_t)(pp >> 32), domain ^ (0x80000000u | (uint32_t)i),
+                                    (uint32_t)seed, (uint32_t)(seed >> 32));
+      x[i] = (uint32_t)__umul64hi(((uint64_t)s.v[1] << 32) | s.v[0], q);
+    }
+  }
+}
+
+// Centred binomial CBD(20) samples: three per Philox4x32 output (120 of its
+// 128 bits, disjoint 20-bit halves).
+__device__ __forceinline__ void cbd20x3(const u32x4& r, int (&s)[3]) {
+  s[0] = __popc(r.v[0] & 0xFFFFFu) - __popc(r.v[1] & 0xFFFFFu);
+  s[1] = __popc(r.v[2] & 0xFFFFFu) - __popc(r.v[3] & 0xFFFFFu);
+  s[2] = __popc(((r.v[0] >> 20) | (r.v[1] >> 20) << 12) & 0xFFFFFu) -
+         __popc(((r.v[2] >> 20) | (r.v[3] >> 20) << 12) & 0xFFFFFu);
 }
 
 // ------------------------------------------------------- seed indirection ---

@@ -30,17 +30,6 @@ __device__ __forceinline__ uint32_t delta_m(const PbDev& P, int l, uint64_t m) {
   return mul_shoup(reduce64(m, q, P.mu[l]), P.delta[l], P.delta_sh[l], q);
 }
 
-__device__ __forceinline__ void uniform_pair(uint64_t seed, int64_t p, int l, int jpair, uint32_t q, uint32_t domain,
-                                             uint32_t& x0, uint32_t& x1) {
-  const uint64_t pp = (uint64_t)p;
-  const u32x4 r = philox4x32_10((uint32_t)jpair | ((uint32_t)l << 24), (uint32_t)pp, (uint32_t)(pp >> 32), domain,
-                                (uint32_t)seed, (uint32_t)(seed >> 32));
-  const uint64_t a = ((uint64_t)r.v[1] << 32) | r.v[0];
-  const uint64_t b = ((uint64_t)r.v[3] << 32) | r.v[2];
-  x0 = (uint32_t)__umul64hi(a, q);
-  x1 = (uint32_t)__umul64hi(b, q);
-}
-
 // ------------------------------------------------ plaintexts, Montgomery ---
 template <int LOGN>
 __global__ void __launch_bounds__(1 << (LOGN - 5))
@@ -79,11 +68,11 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   const uint32_t q = P.q[l];
   if (filler) {
     const uint64_t fseed = dev_key(filler_arg, seed_dev);
-    for (int jp = tid; jp < N / 2; jp += Nt::T) {
-      uint32_t x0, x1;
-      uniform_pair(fseed, p, l, jp, q, 0x4d41534bu /* "MASK" */, x0, x1);
-      sm[Nt::pad(2 * jp)] = x0;
-      sm[Nt::pad(2 * jp + 1)] = x1;
+    for (int jq = tid; jq < N / 4; jq += Nt::T) {
+      uint32_t x[4];
+      uniform_quad(fseed, (uint64_t)p, l, jq, q, 0x4d41534cu /* "MASL" */, x);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sm[Nt::pad(4 * jq + i)] = x[i];
     }
   } else {
     for (int j = tid; j < N; j += Nt::T) sm[Nt::pad(j)] = 0u;
@@ -312,6 +301,185 @@ __global__ void __launch_bounds__(MAC_THREADS, MINB)
     }
 }
 
+// Warp-specialised variant of k_mac_pipe: a fifth warp only issues the TMA
+// copies (per-copy address = base + k * stride, precomputed), gated per stage
+// by an "empty" mbarrier the four consumer warps arrive on, so the consumers
+// never wait for the issuing thread at a CTA barrier (ncu on k_mac_pipe: 26%
+// of stall samples were the per-k __syncthreads behind thread 0's issue work).
+template <int TB, int TO, int V, int STAGES, int MINB = 1>
+__global__ void __launch_bounds__(MAC_THREADS + 32, MINB)
+    k_mac_ws(PbDev P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB, int nB,
+             int nO, int nI, uint32_t* ct_out) {
+  using C = PipeCfg<TB, TO, V>;
+  using VT = typename Vec<V>::T;
+  extern __shared__ __align__(128) uint8_t pipe_sm[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int CA = 0, PA = 2 * TB, CB = ctA ? C::SLOTS_A : 0, PB = CB + 2 * TO;
+  const int nslots = (ctA ? C::SLOTS_A : 0) + (ctB ? C::SLOTS_B : 0);
+  const int N = P.N, L = P.L;
+  const int slices = N / (V * MAC_THREADS);
+  const int tilesO = (nO + TO - 1) / TO;
+  const int tb = blockIdx.x / tilesO, to = blockIdx.x % tilesO;
+  const int l = blockIdx.y / slices, sl = blockIdx.y % slices;
+  const int tid = threadIdx.x;
+  bool okb[TB], oko[TO];
+#pragma unroll
+  for (int i = 0; i < TB; ++i) okb[i] = tb * TB + i < nB;
+#pragma unroll
+  for (int o = 0; o < TO; ++o) oko[o] = to * TO + o < nO;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], MAC_THREADS / 32);
+    }
+    mbar_init_fence();
+  }
+  __syncthreads();
+
+  if (tid >= MAC_THREADS) {  // ---- producer warp (one thread; slot table in registers)
+    if (tid != MAC_THREADS) return;
+    constexpr int NS = C::SLOTS_A + C::SLOTS_B;
+    const size_t rowb = (size_t)N * 4;
+    const size_t off = (size_t)sl * C::SLOT + (size_t)l * rowb;
+    const size_t ct_k = 2 * (size_t)L * rowb, pt_k = (size_t)L * rowb;  // bytes per k step
+    const uint8_t* base[NS];
+    uint32_t dsto[NS];
+    bool on[NS];
+    uint32_t bytes = 0;
+#pragma unroll
+    for (int i = 0; i < TB; ++i) {
+      const size_t bi = (size_t)(tb * TB + i) * nI;
+      const uint8_t* a = reinterpret_cast<const uint8_t*>(ctA) + bi * ct_k + off;
+      base[2 * i] = a, base[2 * i + 1] = a + (size_t)L * rowb;
+      dsto[2 * i] = (CA + 2 * i) * C::SLOT, dsto[2 * i + 1] = (CA + 2 * i + 1) * C::SLOT;
+      on[2 * i] = on[2 * i + 1] = ctA && okb[i];
+      base[C::SLOTS_A + 2 * TO + i] = reinterpret_cast<const uint8_t*>(ptB) + bi * pt_k + off;
+      dsto[C::SLOTS_A + 2 * TO + i] = (PB + i) * C::SLOT;
+      on[C::SLOTS_A + 2 * TO + i] = ctB && okb[i];
+    }
+#pragma unroll
+    for (int o = 0; o < TO; ++o) {
+      const size_t oi = (size_t)(to * TO + o) * nI;
+      base[2 * TB + o] = reinterpret_cast<const uint8_t*>(ptA) + oi * pt_k + off;
+      dsto[2 * TB + o] = (PA + o) * C::SLOT;
+      on[2 * TB + o] = ctA && oko[o];
+      const uint8_t* b = reinterpret_cast<const uint8_t*>(ctB) + oi * ct_k + off;
+      base[C::SLOTS_A + 2 * o] = b, base[C::SLOTS_A + 2 * o + 1] = b + (size_t)L * rowb;
+      dsto[C::SLOTS_A + 2 * o] = (CB + 2 * o) * C::SLOT, dsto[C::SLOTS_A + 2 * o + 1] = (CB + 2 * o + 1) * C::SLOT;
+      on[C::SLOTS_A + 2 * o] = on[C::SLOTS_A + 2 * o + 1] = ctB && oko[o];
+    }
+#pragma unroll
+    for (int c = 0; c < NS; ++c) bytes += on[c] ? (uint32_t)C::SLOT : 0u;
+    for (int k = 0; k < nI; ++k) {
+      const int s = k % STAGES;
+      if (k >= STAGES) mbar_wait(&empty[s], (uint32_t)((k / STAGES - 1) & 1));
+      mbar_expect_tx(&full[s], bytes);
+      uint8_t* st = pipe_sm + (size_t)s * nslots * C::SLOT;
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        // slots [2TB ct | TO pt] of term A advance by ct_k / pt_k, term B [2TO ct | TB pt] likewise
+        const size_t stride = (c < 2 * TB || (c >= C::SLOTS_A && c < C::SLOTS_A + 2 * TO)) ? ct_k : pt_k;
+        if (on[c]) bulk_g2s(st + dsto[c], base[c] + (size_t)k * stride, C::SLOT, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warps
+  const uint32_t q = P.q[l], qn = P.qn[l];
+  const uint64_t mu = P.mu[l];
+  uint64_t acc[TB][TO][2][V];
+#pragma unroll
+  for (int i = 0; i < TB; ++i)
+#pragma unroll
+    for (int o = 0; o < TO; ++o)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[i][o][c][e] = 0ull;
+  auto mac = [&](uint64_t (&a)[V], const VT& x, const VT& w) {
+#pragma unroll
+    for (int e = 0; e < V; ++e) a[e] += (uint64_t)Vec<V>::get(x, e) * Vec<V>::get(w, e);
+  };
+  constexpr int SV = C::SLOT / (4 * V);
+  for (int k = 0; k < nI; ++k) {
+    const int s = k % STAGES;
+    mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
+    const VT* st = reinterpret_cast<const VT*>(pipe_sm + (size_t)s * nslots * C::SLOT) + tid;
+    if (ctA) {
+      VT w[TO];
+#pragma unroll
+      for (int o = 0; o < TO; ++o) w[o] = st[(PA + o) * SV];
+#pragma unroll
+      for (int i = 0; i < TB; ++i) {
+        const VT x0 = st[(CA + 2 * i) * SV], x1 = st[(CA + 2 * i + 1) * SV];
+#pragma unroll
+        for (int o = 0; o < TO; ++o) { mac(acc[i][o][0], x0, w[o]); mac(acc[i][o][1], x1, w[o]); }
+      }
+    }
+    if (ctB) {
+      VT u[TB];
+#pragma unroll
+      for (int i = 0; i < TB; ++i) u[i] = st[(PB + i) * SV];
+#pragma unroll
+      for (int o = 0; o < TO; ++o) {
+        const VT y0 = st[(CB + 2 * o) * SV], y1 = st[(CB + 2 * o + 1) * SV];
+#pragma unroll
+        for (int i = 0; i < TB; ++i) { mac(acc[i][o][0], y0, u[i]); mac(acc[i][o][1], y1, u[i]); }
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // this warp is done reading stage s
+    if ((k + 1) % MAC_CHUNK == 0 && k + 1 < nI) {
+#pragma unroll
+      for (int i = 0; i < TB; ++i)
+#pragma unroll
+        for (int o = 0; o < TO; ++o)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[i][o][c][e] = reduce64(acc[i][o][c][e], q, mu);
+    }
+  }
+  auto fin = [&](uint64_t a) { return csub(mont_lazy(reduce64(a, q, mu), 1u, q, qn), q); };
+  VT* out = reinterpret_cast<VT*>(ct_out);
+  const size_t row = (size_t)N / V;
+  const size_t v = (size_t)sl * MAC_THREADS + tid;
+#pragma unroll
+  for (int i = 0; i < TB; ++i)
+#pragma unroll
+    for (int o = 0; o < TO; ++o) {
+      if (!(okb[i] && oko[o])) continue;
+      const size_t r = (size_t)(tb * TB + i) * nO + (to * TO + o);
+      const size_t b0 = (r * 2 * L + l) * row + v;
+      const VT m = out[b0];
+      uint32_t c0[V], c1[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        c0[e] = addmod(fin(acc[i][o][0][e]), Vec<V>::get(m, e), q);
+        c1[e] = fin(acc[i][o][1][e]);
+      }
+      out[b0] = Vec<V>::make(c0);
+      out[b0 + (size_t)L * row] = Vec<V>::make(c1);
+    }
+}
+
+template <int TB, int TO, int V, int STAGES, int MINB = 1>
+void launch_ws(const PbDev& P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB,
+               int nB, int nO, int nI, uint32_t* out, cudaStream_t st) {
+  using C = PipeCfg<TB, TO, V>;
+  const size_t smem = (size_t)STAGES * ((ctA ? C::SLOTS_A : 0) + (ctB ? C::SLOTS_B : 0)) * C::SLOT;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mac_ws<TB, TO, V, STAGES, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((size_t)STAGES * (C::SLOTS_A + C::SLOTS_B) * C::SLOT));
+    attr = true;
+  }
+  dim3 grid((unsigned)(((nB + TB - 1) / TB) * ((nO + TO - 1) / TO)), (unsigned)(P.L * (P.N / (V * MAC_THREADS))));
+  k_mac_ws<TB, TO, V, STAGES, MINB><<<grid, MAC_THREADS + 32, smem, st>>>(P, ctA, ptA, ctB, ptB, nB, nO, nI, out);
+}
+
 template <int TB, int TO, int V, int STAGES, int MINB = 1>
 void launch_pipe(const PbDev& P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB,
                  int nB, int nO, int nI, uint32_t* out, cudaStream_t st) {
@@ -494,8 +662,18 @@ extern "C" int pb_ctpt_mac_tiled(const pb_ctx* ctx, const uint32_t* ctA, const u
                   // FC-like K=1: 0.174 -> 0.131 ms, 4.5 TB/s of actual DRAM traffic
     dim3 grid((unsigned)(nB * nO), (unsigned)(L * (N / (4 * MAC_THREADS))));
     k_mac_eager<1, 1><<<grid, MAC_THREADS, 0, st>>>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out);
-  } else {  // TMA-pipelined lazy MAC: K=16 conv-like 1.09 -> 0.65 ms, FC 784x128 fwd 75 -> 48 us (B200)
-    launch_pipe<2, 2, 4, 3, 6>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
+  } else {
+    // Warp-specialised TMA-pipelined lazy MAC (B200, graph-timed): FC 784x128 fwd
+    // 52.7 -> 39.3 us, its grad-W 51.1 -> 45.7 us, conv-like K=16 646 -> 587 us vs
+    // the single-role k_mac_pipe (PB_MAC_VARIANT=1 keeps it for comparison).
+    static const int variant = [] {
+      const char* e = getenv("PB_MAC_VARIANT");
+      return e ? atoi(e) : 0;
+    }();
+    if (variant == 1)
+      launch_pipe<2, 2, 4, 3, 6>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
+    else
+      launch_ws<2, 2, 4, 4, 4>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
   }
   PB_CHECK_LAUNCH();
   return PB_OK;

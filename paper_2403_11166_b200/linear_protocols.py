@@ -9,7 +9,9 @@ Alg. 1, Alg. 2).
     sample_dp_noise         N(0, sigma^2 C^2 / B)
 
 Per protocol message the work is three fused device kernels:
-    DO   pb_encrypt_sk        pack (pi_v / pi_W gather) + Delta m + NTT + key mul
+    DO   pb_encrypt_sk_add    pack (pi_v / pi_W gather) + e + Delta m + NTT, added onto
+                          pooled (-a s, a) (pb_encrypt_sk_zero: the encryption
+                          randomness a, e, a*s, precomputed off the critical path)
     MO   pb_ctpt_mac_mask     sum_k ct (*) pt  -  Delta NTT(pi_y(mask) + filler)
     DO   pb_decrypt_to_share  c0 + c1 s + INTT + Garner/scale-round + pi_y^-1
 plus the MO's plaintext encoding (pb_encode_plain) and ring GEMMs for the
@@ -39,7 +41,7 @@ from .poly_encoding import MatmulGeometry, conv_out_hw, plan_conv_layer, plan_ma
 from .ring import DO, MO, RingParams, RingTensor, SeededRng, ShareTensor
 
 OP_FWD, OP_BWD_X, OP_GRAD_W, OP_GRAD_B, OP_RELU, OP_TRUNC_F, OP_TRUNC_B, OP_RELU_B, OP_POOL_F, OP_POOL_B = range(10)
-P_MASK, P_ENC, P_DEALER, P_DP = range(4)
+P_MASK, P_ENC, P_DEALER, P_DP, P_POOL = range(5)
 
 # SPEC:372 message codes
 MSG_FWD_INPUT_CT = 0x10
@@ -53,6 +55,7 @@ FRAME_HEADER = 12  # {u16 type, u16 flags, u64 len}
 import os as _os
 
 _SERIAL = _os.environ.get("PB_SERIAL", "0") == "1"
+_ENC_POOL = _os.environ.get("PB_ENC_POOL", "0") == "1"
 
 
 def stream_id(layer: int, op: int, purpose: int) -> int:
@@ -164,6 +167,17 @@ class Session:
         self._streams = {}
         self._grad_stream = None
         self.capture = None  # diagnostics: a list receives (masked output ciphertexts, useful slot positions)
+        # DO's pool of precomputed encryption randomness ((-a s, a), e), one
+        # buffer per (layer, op, term, size): consumed in place by
+        # pb_encrypt_sk_add, refilled on a side stream once the MAC has read it
+        self.enc_pool = _ENC_POOL
+        self._pool = {}
+        self._pool_ev = {}  # key -> event after its pending refill (cleared by join_pool)
+        self._pool_streams = {}
+        self._pool_active = {}
+        self._pool_ctr = 0
+        self.pool_defer = False  # True: refills wait for refill_pool() (the forward pass defers them)
+        self._pool_dirty = []
 
     def rng(self, layer: int, op: int, purpose: int) -> SeededRng:
         g = SeededRng(self.seed, stream_id(layer, op, purpose))
@@ -208,6 +222,73 @@ class Session:
             self._grad_stream = torch.cuda.Stream()
         return self._grad_stream
 
+    # ------------------------- encryption-randomness pool (DO side) ---
+    def _pool_fill(self, buf):
+        """buf = (ct, e) <- fresh (-a s, a), e on the current stream.  Key: the step seed
+        (device word in graph mode) on stream P_POOL; nonce: a session-wide
+        counter, so no (key, nonce) pair is ever reused."""
+        ct, e = buf
+        n = ct.shape[0]
+        seed, sptr = self.rng(0, 0, P_POOL).dev_args()
+        nonce = self._pool_ctr + self.rank * n
+        self._pool_ctr += n * self.world
+        _lib.call("pb_encrypt_sk_zero", self.ctx.handle, _dev.ptr(self.kp.sk_ntt), n, seed, sptr, nonce,
+                  _dev.ptr(ct), _dev.ptr(e), _dev.stream())
+        self._count("pb_encrypt_sk_zero", n * (2 * self.p.L * self.p.N * 4 + self.p.N))
+
+    def _pool_take(self, key, n: int, s_enc: torch.cuda.Stream):
+        """n pooled (ct = (-a s, a), e) for ``key``, ready in stream order on s_enc."""
+        buf = self._pool.get(key)
+        dirty = [d for d in self._pool_dirty if d[0] == key]
+        if buf is None or dirty:  # first use, or consumed and not yet refilled: fill inline
+            if buf is None:
+                buf = self._pool[key] = (_dev.empty_u32(n, 2, self.p.L, self.p.N),
+                                         torch.empty(n, self.p.N, dtype=torch.int8, device=_dev.device()))
+            for d in dirty:
+                s_enc.wait_event(d[2])
+                self._pool_dirty.remove(d)
+            with torch.cuda.stream(s_enc):
+                self._pool_fill(buf)
+        else:
+            ev = self._pool_ev.pop(key, None)
+            if ev is not None:
+                s_enc.wait_event(ev)
+        return buf
+
+    def _pool_refill(self, key, buf, after=None):
+        """Refill ``buf`` after ``after`` (an event), else after the work enqueued
+        so far on the current stream (the MAC that reads it), on a side stream
+        off the critical path."""
+        cur = torch.cuda.current_stream()
+        sp = self._pool_streams.get(cur.cuda_stream)
+        if sp is None:
+            sp = self._pool_streams[cur.cuda_stream] = torch.cuda.Stream()
+        if after is None:
+            sp.wait_stream(cur)
+        else:
+            sp.wait_event(after)
+        self._pool_active[cur.cuda_stream] = sp
+        with torch.cuda.stream(sp):
+            self._pool_fill(buf)
+        ev = torch.cuda.Event()
+        ev.record(sp)
+        self._pool_ev[key] = ev
+
+    def refill_pool(self):
+        """Refill every deferred pool buffer (after all work enqueued so far)."""
+        dirty, self._pool_dirty = self._pool_dirty, []
+        for key, buf, _ev in dirty:  # all their MACs were enqueued before this call
+            self._pool_refill(key, buf)
+
+    def join_pool(self):
+        """Make the current stream wait for every pending pool refill (ends a
+        step; required before a CUDA-graph capture closes)."""
+        cur = torch.cuda.current_stream()
+        for sp in self._pool_active.values():  # only streams used since the last join (capture-safe)
+            cur.wait_stream(sp)
+        self._pool_active.clear()
+        self._pool_ev.clear()
+
     def _count(self, name, nbytes):
         if _lib.STATS is not None:
             self.alg_bytes[name] = self.alg_bytes.get(name, 0.0) + float(nbytes)
@@ -250,31 +331,44 @@ class Session:
         # MO's mask NTT, and the MAC joins all three (the graph keeps the fork).
         has_a = sh.n_out and v_ct is not None
         has_b = sh.n_out and w_ct is not None
-        if has_a:
-            ctA = _dev.empty_u32(sh.n_in, 2, L, N)
-            ptA = _dev.empty_u32(sh.n_pt, L, N)
-        if has_b:
-            ctB = _dev.empty_u32(sh.n_pt, 2, L, N)
-            ptB = _dev.empty_u32(sh.n_in, L, N)
-        out_ct = _dev.empty_u32(sh.n_out, 2, L, N) if sh.n_out else None
         main = torch.cuda.current_stream()
+        pooled = []
         if has_a or has_b:
             s_enc, s_pt = self._side_streams()
-            s_enc.wait_stream(main)
+            s_enc.wait_stream(main)  # covers every buffer allocated below
             s_pt.wait_stream(main)
+        if has_a:
+            keyA = (layer, op, 0, sh.n_in)
+            preA = self._pool_take(keyA, sh.n_in, s_enc) if self.enc_pool else None
+            ctA = preA[0] if preA else _dev.empty_u32(sh.n_in, 2, L, N)
+            ptA = _dev.empty_u32(sh.n_pt, L, N)
+        if has_b:
+            keyB = (layer, op, 1, sh.n_pt)
+            preB = self._pool_take(keyB, sh.n_pt, s_enc) if self.enc_pool else None
+            ctB = preB[0] if preB else _dev.empty_u32(sh.n_pt, 2, L, N)
+            ptB = _dev.empty_u32(sh.n_in, L, N)
+        out_ct = _dev.empty_u32(sh.n_out, 2, L, N) if sh.n_out else None
+        if has_a or has_b:
             with torch.cuda.stream(s_enc):  # DO
                 se = _dev.stream()
-                if has_a:  # term A: Enc_DO(pi_v(v)) (x) pi_W(W)
-                    _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(v_ct), *_pk(sh.in_pack),
-                              sh.n_in, *enc_rng.dev_args(), base + self.rank * plan.n_in, _dev.ptr(ctA), se)
-                    self._count("pb_encrypt_sk", sh.n_in * (ct_bytes + 8 * N))
-                    self.channel.send(DO, msg_in, ctA, Ciphertext(ctA, p).nbytes_wire())
-                if has_b:  # term B: Enc_DO(pi_W(W)) (x) pi_v(v)
-                    _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(w_ct), *_pk(sh.pt_pack),
-                              sh.n_pt, *enc_rng.dev_args(), base + self.world * plan.n_in + self.rank * plan.n_pt,
-                              _dev.ptr(ctB), se)
-                    self._count("pb_encrypt_sk", sh.n_pt * (ct_bytes + 8 * N))
-                    self.channel.send(DO, msg_in, ctB, Ciphertext(ctB, p).nbytes_wire())
+                for ct, src, pack, n, nonce, key, pre in (
+                        (ctA, v_ct, sh.in_pack, sh.n_in, base + self.rank * plan.n_in, has_a and keyA,
+                         has_a and preA),
+                        (ctB, w_ct, sh.pt_pack, sh.n_pt, base + self.world * plan.n_in + self.rank * plan.n_pt,
+                         has_b and keyB, has_b and preB)):
+                    if ct is None:
+                        continue
+                    # term A: Enc_DO(pi_v(v)) (x) pi_W(W);  term B: Enc_DO(pi_W(W)) (x) pi_v(v)
+                    if self.enc_pool:
+                        _lib.call("pb_encrypt_sk_add", h, _dev.ptr(src), *_pk(pack), n, _dev.ptr(pre[1]),
+                                  _dev.ptr(ct), se)
+                        self._count("pb_encrypt_sk_add", n * (ct_bytes + 9 * N))
+                        pooled.append((key, pre))
+                    else:
+                        _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(src), *_pk(pack), n,
+                                  *enc_rng.dev_args(), nonce, _dev.ptr(ct), se)
+                        self._count("pb_encrypt_sk", n * (ct_bytes + 8 * N))
+                    self.channel.send(DO, msg_in, ct, Ciphertext(ct, p).nbytes_wire())
             with torch.cuda.stream(s_pt):  # MO
                 sp = _dev.stream()
                 if has_a:
@@ -300,6 +394,13 @@ class Session:
                 n_ct = (sh.n_in if ctA is not None else 0) + (sh.n_pt if ctB is not None else 0)
                 n_pt = (sh.n_pt if ctA is not None else 0) + (sh.n_in if ctB is not None else 0)
                 self._count("pb_ctpt_mac_tiled", n_ct * ct_bytes + n_pt * L * N * w + sh.n_out * (ct_bytes + L * N * w))
+            for key, pre in pooled:  # the MAC has consumed them: precompute the next (a, -a s, e)
+                if self.pool_defer:
+                    ev = torch.cuda.Event()
+                    ev.record(main)
+                    self._pool_dirty.append((key, pre, ev))
+                else:
+                    self._pool_refill(key, pre)
             self.channel.send(MO, msg_out, out_ct, Ciphertext(out_ct, p).nbytes_wire())
             if self.capture is not None:
                 self.capture.append((out_ct.clone(), sh.out_pos.clone()))

@@ -185,10 +185,24 @@ def forward_phase(sess: Session, model: Model, x: RingTensor, prep=None):
     With ``prep`` (a preprocessing.PrepState) the linear layers run Alg. 4's
     HE-free online protocol (SPEC mode "prep")."""
     ring, f = model.ring, model.ring.f
-    L = model.n_layers
     seg = model.segments()
     cur = (ShareTensor(MO, RingTensor(torch.zeros_like(x.values), f, ring, _canonical=True)), ShareTensor(DO, x))
     acts, ds, ys = [], [], []
+    # Enc(0) pool refills of the forward layers are deferred to the backward
+    # pass (they would otherwise run beside the tail the DO waits on for the logits)
+    defer, sess.pool_defer = sess.pool_defer, True
+    try:
+        _forward_layers(sess, model, prep, cur, acts, ds, ys, seg)
+    finally:
+        sess.pool_defer = defer
+    # the MO sends its share of the logits; the DO reconstructs them (SPEC:614)
+    y_mo, y_do = ys[-1]
+    logits = y_mo.value + y_do.value
+    return (acts, ds, ys), logits
+
+
+def _forward_layers(sess, model, prep, cur, acts, ds, ys, seg):
+    f, L = model.ring.f, model.n_layers
     for l, i in enumerate(model.lin):
         e = model.layers[i]
         acts.append(cur)
@@ -207,10 +221,6 @@ def forward_phase(sess: Session, model: Model, x: RingTensor, prep=None):
                     cur = avgpool_forward(sess, l, *cur)
                 elif model.layers[k][0] == "flatten":
                     cur = (_flatten(cur[0]), _flatten(cur[1]))
-    # the MO sends its share of the logits; the DO reconstructs them
-    y_mo, y_do = ys[-1]
-    logits = y_mo.value + y_do.value
-    return (acts, ds, ys), logits
 
 
 def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e-2, momentum=0.8, trace=None,
@@ -227,6 +237,7 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
     # input-gradient chain to layer l-1 are independent given grad Y_l: Alg.2
     # runs on the session's grad stream, overlapping the chain on this stream.
     main, gstream = torch.cuda.current_stream(), sess.grad_stream()
+    sess.refill_pool()  # the forward pass's deferred Enc(0) refills, beside the backward chain
     keep = []  # grad Y shares read on the grad stream stay referenced until the join
     for l in reversed(range(L)):
         e = model.layers[model.lin[l]]
@@ -273,6 +284,7 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
     main.wait_stream(gstream)
     del keep
     model.sgd(gws, gbs, lr, momentum, check=check)
+    sess.join_pool()
     return gws, gbs
 
 
@@ -298,7 +310,9 @@ class GraphStep:
     def __init__(self, sess: Session, model: Model, x: RingTensor, lr=1e-2, momentum=0.8, prep=None):
         self.sess, self.model, self.lr, self.momentum, self.prep = sess, model, lr, momentum, prep
         sess.enable_graph_mode()
-        self.x = x  # device input buffer; callers copy new batches into x.values
+        self.x = x  # device input buffer; callers copy new batches into x.values (or use load_batch)
+        self._stage = None
+        self._flag_pending = False
         n_cls = model.n_classes
         B = x.shape[1] if len(model.in_shape) == 1 else x.shape[0]
         self.g_do = torch.zeros(n_cls, B, dtype=torch.int64, device=x.values.device)
@@ -316,11 +330,34 @@ class GraphStep:
             self.grads = backward_phase(sess, model, self.state, self.g_do, lr, momentum, check=False, prep=prep)
         torch.cuda.synchronize()
 
+    def load_batch(self, x_host: torch.Tensor):
+        """Stage a new real-valued batch (host float64, pinned for an async
+        copy; the DO's input, same shape as x) into the graphs' input buffer:
+        H2D copy + fixed-point encode on the device, no host sync -- the
+        encode's range flag is checked at the next step's logits sync."""
+        from .ring import encode_fixed_into
+
+        if self._stage is None:
+            self._stage = torch.empty(tuple(self.x.values.shape), dtype=torch.float64, device=self.x.values.device)
+            self._flag = torch.zeros(1, dtype=torch.int32, device=self.x.values.device)
+            self._flag_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self._stage.copy_(x_host, non_blocking=True)
+        encode_fixed_into(self._stage, self.model.ring, self.x.values, self._flag)
+        self._flag_host.copy_(self._flag, non_blocking=True)
+        self._flag_pending = True
+
     def step(self, seed: int, labels):
         self.sess.reseed(seed)
         self.g_fwd.replay()
         self.logits_host.copy_(self.logits.values, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+        if self._flag_pending:
+            self._flag_pending = False
+            if int(self._flag_host[0]):
+                from .errors import EncodeRangeError
+
+                limit = float(1 << (self.model.ring.ell - 1)) / float(1 << self.model.ring.f)
+                raise EncodeRangeError(f"|x| must stay below {limit}")
         loss, g = softmax_ce_grad(self.logits_host.numpy().view(np.uint64), np.asarray(labels), self.model.ring)
         self.g_host.numpy().view(np.uint64)[...] = g
         self.g_do.copy_(self.g_host, non_blocking=True)

@@ -314,6 +314,20 @@ def encode_fixed(x, params: RingParams, scale: int | None = None) -> torch.Tenso
     return out
 
 
+def encode_fixed_into(xd: torch.Tensor, params: RingParams, out: torch.Tensor, flag: torch.Tensor,
+                      scale: int | None = None) -> None:
+    """encode_fixed of a contiguous device float64 tensor into ``out`` (int64,
+    same size), asynchronously: ``flag`` (device int32[1]) is zeroed and set
+    when some |x| is out of range -- the caller checks it at its next sync."""
+    scale = params.f if scale is None else scale
+    if xd.dtype != torch.float64 or not xd.is_contiguous() or out.numel() != xd.numel():
+        raise ValueError("encode_fixed_into needs a contiguous float64 input and an output of the same size")
+    flag.zero_()
+    if xd.numel():
+        _lib.call("pb_encode_fixed", _dev.ptr(xd), xd.numel(), params.ell, scale, _dev.ptr(out), _dev.ptr(flag),
+                  _dev.stream())
+
+
 def decode_fixed(v, params: RingParams, scale: int | None = None) -> torch.Tensor:  # R:185-191
     scale = params.f if scale is None else scale
     t = _as_device_u64(v).contiguous()

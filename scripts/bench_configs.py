@@ -98,7 +98,7 @@ def model_step(name, steps, cpu, prep_m=0):
         prep_s = time.perf_counter() - t0
     # eager (kernel-time breakdown + launch count)
     stats = _lib.CallStats(timed=("pb_ctpt_mac_tiled", "pb_mask_ntt", "pb_decrypt_to_share", "pb_encrypt_sk",
-                                  "pb_encode_plain_mont", "pb_ring_conv"))
+                                  "pb_encrypt_sk_add", "pb_encrypt_sk_zero", "pb_encode_plain_mont", "pb_ring_conv"))
     for i in range(2):
         sess.reseed(SEED + i)
         PN.private_train_step(sess, model, x, labels, check=False, prep=prep)

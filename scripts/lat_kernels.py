@@ -61,6 +61,7 @@ def main():
         plan = plan_matmul(MatmulGeometry(*g), N)
         sh = _Shard(plan, 0, 1)
         ct = _dev.empty_u32(sh.n_in, 2, L, N)
+        ebuf = torch.zeros(sh.n_in, N, dtype=torch.int8, device=ct.device)
         pt = _dev.empty_u32(sh.n_pt, L, N)
         out = _dev.empty_u32(sh.n_out, 2, L, N)
         share = _dev.empty_u64(g[1] * g[2])
@@ -69,6 +70,10 @@ def main():
         fns = {
             "encrypt_sk": lambda: _lib.call("pb_encrypt_sk", h, _dev.ptr(kp.sk_ntt), _dev.ptr(vals), *_pk(sh.in_pack),
                                             sh.n_in, 5, None, 0, _dev.ptr(ct), _dev.stream()),
+            "encrypt_add": lambda: _lib.call("pb_encrypt_sk_add", h, _dev.ptr(vals), *_pk(sh.in_pack), sh.n_in,
+                                             _dev.ptr(ebuf), _dev.ptr(ct), _dev.stream()),
+            "encrypt_zero": lambda: _lib.call("pb_encrypt_sk_zero", h, _dev.ptr(kp.sk_ntt), sh.n_in, 5, None, 0,
+                                              _dev.ptr(ct), _dev.ptr(ebuf), _dev.stream()),
             "encode_mont": lambda: _lib.call("pb_encode_plain_mont", h, _dev.ptr(vals), *_pk(sh.pt_pack), sh.n_pt,
                                              _dev.ptr(pt), _dev.stream()),
             "mask_ntt": lambda: _lib.call("pb_mask_ntt", h, sh.n_out, _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U,

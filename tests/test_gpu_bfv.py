@@ -105,6 +105,47 @@ def test_device_randomness_roundtrip_and_ctpt(setup, mode):
     assert not np.array_equal(_dev.to_numpy_u32(ct.data), _dev.to_numpy_u32(ct2.data))
 
 
+def test_split_encrypt_sk(setup):
+    """Precomputed (a, -a s, e) + online add (pb_encrypt_sk_zero / _add):
+    same a as pb_encrypt_sk under (key, nonce); the ciphertext equals
+    pb_encrypt_sk_noise with that (a, e) bit for bit; dense and packed
+    sources; decrypts to m; e is a small centred draw."""
+    from paper_2403_11166_b200 import _dev, bfv, ring
+    from paper_2403_11166_b200.poly_encoding import compact
+
+    s = setup
+    N, L, P = s["N"], s["L"], 5
+    kp = s["pkp"]
+    m = OR.SeededRng(12, 2).uniform_ring((P, N), OR.RingParams())
+    md = _dev.u64_to_device(m)
+    ref = bfv.encrypt(kp, md, ring.SeededRng(13, 0), mode="sk", nonce=77)
+    ct, e = bfv.encrypt_zero(kp, P, ring.SeededRng(13, 0), nonce=77)
+    assert np.array_equal(_dev.to_numpy_u32(ct.data[:, 1]), _dev.to_numpy_u32(ref.data[:, 1]))  # same a
+    en = e.cpu().numpy()
+    assert np.abs(en).max() <= 20 and abs(en.mean()) < 0.1 and 8.0 < en.var() < 12.0  # CBD(20): var 10
+    a_ref = bfv.to_reference_order(s["pp"], ct.data[:, 1].contiguous()).reshape(P, L, N)
+    want = bfv.encrypt(kp, md, noise=(a_ref, en), mode="sk")
+    got = bfv.encrypt_add((ct, e), md)
+    assert np.array_equal(_dev.to_numpy_u32(got.data), _dev.to_numpy_u32(want.data))
+    assert np.array_equal(_dev.to_numpy_u64(bfv.decrypt(kp, got)), m)
+    # packed source: poly p takes flat values at a ragged set of slots
+    rs = np.random.default_rng(3)
+    flat = OR.SeededRng(12, 3).uniform_ring((300,), OR.RingParams())
+    src = np.full((P, N), -1, np.int64)
+    for p in range(P):
+        k = rs.integers(0, 120)
+        src[p, rs.choice(N, size=k, replace=False)] = rs.integers(0, 300, size=k)
+    pack = tuple(_dev.i32_to_device(a) for a in compact(src))
+    dense = np.where(src >= 0, flat[np.maximum(src, 0)], 0).astype(np.uint64)
+    fd = _dev.u64_to_device(flat)
+    pre = bfv.encrypt_zero(kp, P, ring.SeededRng(14, 0), nonce=5)
+    a_ref = bfv.to_reference_order(s["pp"], pre[0].data[:, 1].contiguous()).reshape(P, L, N)
+    want = bfv.encrypt(kp, fd, noise=(a_ref, pre[1].cpu().numpy()), mode="sk", pack=pack)
+    got = bfv.encrypt_add(pre, fd, pack=pack)
+    assert np.array_equal(_dev.to_numpy_u32(got.data), _dev.to_numpy_u32(want.data))
+    assert np.array_equal(_dev.to_numpy_u64(bfv.decrypt(kp, got)), dense)
+
+
 def test_he_add_and_plain(setup):
     from paper_2403_11166_b200 import _dev, bfv, ring
 

@@ -44,3 +44,36 @@ def test_graph_step_matches_eager_and_reference():
             assert np.array_equal(m1.W[l].numpy(), m2.W[l].numpy())
             assert np.array_equal(m2.W[l].numpy(), om.W(l))
             assert np.array_equal(m2.w[l].cpu().numpy(), om.w[l])
+
+
+def test_graph_step_load_batch():
+    """load_batch (pinned H2D + device encode, deferred range check) feeds the
+    graphs the same input as encode_fixed; an out-of-range batch raises at
+    the step's sync."""
+    import torch
+
+    from paper_2403_11166_b200 import bfv
+    from paper_2403_11166_b200 import nn as PN
+    from paper_2403_11166_b200.errors import EncodeRangeError
+    from paper_2403_11166_b200.linear_protocols import Session
+    from paper_2403_11166_b200.params import BfvParams
+    from paper_2403_11166_b200.ring import RingParams, RingTensor, SeededRng, encode_fixed
+
+    ring, params = RingParams(), BfvParams()
+    kp = bfv.keygen(params, SeededRng(3, 0))
+    sizes, B = [784, 32, 10], 8
+    xh, labels = PN.synthetic_mnist(7, B, ring)
+    x2h, _ = PN.synthetic_mnist(8, B, ring)
+    s1, s2 = Session(params, ring, kp, seed=1), Session(params, ring, kp, seed=1)
+    m1, m2 = PN.Model(sizes, ring, seed=4), PN.Model(sizes, ring, seed=4)
+    r1 = PN.GraphStep(s1, m1, RingTensor(encode_fixed(xh, ring), 25, ring, _canonical=True))
+    r2 = PN.GraphStep(s2, m2, RingTensor(encode_fixed(xh, ring), 25, ring, _canonical=True))
+    r1.x.values.copy_(encode_fixed(x2h, ring))
+    r2.load_batch(torch.from_numpy(np.ascontiguousarray(x2h)).pin_memory())
+    assert r1.step(5, labels) == r2.step(5, labels)
+    assert np.array_equal(r1.x.values.cpu().numpy(), r2.x.values.cpu().numpy())
+    bad = np.ascontiguousarray(x2h).copy()
+    bad[0, 0] = 1e30
+    r2.load_batch(torch.from_numpy(bad).pin_memory())
+    with pytest.raises(EncodeRangeError):
+        r2.step(6, labels)
