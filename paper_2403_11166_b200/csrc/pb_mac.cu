@@ -137,6 +137,11 @@ template <> struct Vec<2> {
 // accumulator is Barrett-reduced every MAC_CHUNK input blocks and once at the
 // end, where one Montgomery step removes the plaintexts' 2^32 factor.
 constexpr int MAC_CHUNK = 7;  // k-steps per reduction (2 terms x 7 = 14 products)
+// k_mac_ws folds with ONE IMAD.WIDE per accumulator instead of a Barrett
+// reduction: a = lo + hi * (2^32 mod q) < q 2^32, after which m more products
+// (< q^2 each) keep a < q (2^32 + m q) < 2^64 for m <= 12 (q < 2^30).
+constexpr int MAC_FOLD1 = 12;  // k-steps between folds, one term
+constexpr int MAC_FOLD2 = 6;   // two terms (two products per k-step)
 
 // TMA-pipelined lazy MAC.  A CTA owns a 2x2 output tile and a 512-coefficient
 // slice of one limb; per input block k its operands are 2-KB contiguous row
@@ -403,6 +408,9 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, MINB)
     for (int e = 0; e < V; ++e) a[e] += (uint64_t)Vec<V>::get(x, e) * Vec<V>::get(w, e);
   };
   constexpr int SV = C::SLOT / (4 * V);
+  const int chunk = (ctA && ctB) ? MAC_FOLD2 : MAC_FOLD1;  // k-steps between folds
+  const uint32_t r32 = reduce64(1ull << 32, q, mu);            // 2^32 mod q
+  int since = 0;
   for (int k = 0; k < nI; ++k) {
     const int s = k % STAGES;
     mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
@@ -431,7 +439,8 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, MINB)
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // this warp is done reading stage s
-    if ((k + 1) % MAC_CHUNK == 0 && k + 1 < nI) {
+    if (++since == chunk && k + 1 < nI) {
+      since = 0;
 #pragma unroll
       for (int i = 0; i < TB; ++i)
 #pragma unroll
@@ -439,7 +448,10 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, MINB)
 #pragma unroll
           for (int c = 0; c < 2; ++c)
 #pragma unroll
-            for (int e = 0; e < V; ++e) acc[i][o][c][e] = reduce64(acc[i][o][c][e], q, mu);
+            for (int e = 0; e < V; ++e) {
+              const uint64_t a = acc[i][o][c][e];
+              acc[i][o][c][e] = (uint64_t)(uint32_t)(a >> 32) * r32 + (uint32_t)a;
+            }
     }
   }
   auto fin = [&](uint64_t a) { return csub(mont_lazy(reduce64(a, q, mu), 1u, q, qn), q); };
