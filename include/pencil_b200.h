@@ -258,6 +258,12 @@ int pb_share(const uint64_t* x, int64_t n, uint64_t seed, const uint64_t* seed_d
  * trans_a / trans_b read a as (k,n) / b as (m,k) row-major. */
 int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m,
                    int trans_a, int trans_b, int32_t ell, uint64_t* out, void* stream);
+/* out = c + sign * (a @ b) mod 2^ell (sign +1 / -1; c == NULL or sign == 0:
+ * plain pb_ring_matmul) -- the protocols' "s - W <X>_0" and "msg + gY X^T"
+ * local terms with the add fused into the GEMM epilogue. */
+int pb_ring_matmul_add(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m,
+                       int trans_a, int trans_b, const uint64_t* c, int32_t sign, int32_t ell,
+                       uint64_t* out, void* stream);
 /* Row reduction: out[i] = sum_j a[i][j] mod 2^ell  (reveal_grad_bias). */
 int pb_ring_rowsum(const uint64_t* a, int64_t rows, int64_t cols, int32_t ell, uint64_t* out,
                    void* stream);
@@ -316,6 +322,12 @@ enum {
 int pb_dealer_op(int op, uint64_t* mo, uint64_t* do_, int64_t n, int32_t k, const uint8_t* d_in,
                  uint8_t* d_out, uint64_t seed, const uint64_t* seed_dev, uint64_t stream_id,
                  uint64_t raw_offset, int32_t ell, void* stream);
+/* The same with the input shares read from in_mo / in_do (out of place; the
+ * inputs may alias the outputs). */
+int pb_dealer_op_out(int op, const uint64_t* in_mo, const uint64_t* in_do, uint64_t* mo, uint64_t* do_,
+                     int64_t n, int32_t k, const uint8_t* d_in, uint8_t* d_out, uint64_t seed,
+                     const uint64_t* seed_dev, uint64_t stream_id, uint64_t raw_offset, int32_t ell,
+                     void* stream);
 
 /* SGD with momentum in float64 + re-quantisation:
  * v = mu*v + g; w = w - lr*v; w_ring = encode_fixed(w, scale). */

@@ -78,6 +78,7 @@ SIGNATURES = {
     "pb_uniform_ring": [P, I64, U64, P, U64, U64, I32, P],
     "pb_share": [P, I64, U64, P, U64, U64, I32, P, P, P],
     "pb_ring_matmul": [P, P, I64, I64, I64, INT, INT, I32, P, P],
+    "pb_ring_matmul_add": [P, P, I64, I64, I64, INT, INT, P, I32, I32, P, P],
     "pb_ring_rowsum": [P, I64, I64, I32, P, P],
     "pb_im2col": [P, I32, I32, I32, I32, I32, I32, P, P],
     "pb_col2im": [P, I32, I32, I32, I32, I32, I32, P, P],
@@ -87,6 +88,7 @@ SIGNATURES = {
     "pb_ring_lincomb": [INT, P, P, P, I32, P, I32, P, I64, I32, P],
     "pb_ring_add_bcast": [P, P, P, I64, I64, I64, I32, P],
     "pb_dealer_op": [INT, P, P, I64, I32, P, P, U64, P, U64, U64, I32, P],
+    "pb_dealer_op_out": [INT, P, P, P, P, I64, I32, P, P, U64, P, U64, U64, I32, P],
     "pb_sgd_momentum": [P, P, P, I64, I32, F64, F64, I32, I32, P, P, P],
 }
 _RET = {"pb_last_error": ctypes.c_char_p}

@@ -430,7 +430,30 @@ extern "C" int pb_pool2(int op, const uint64_t* in, int64_t bc, int32_t H, int32
 }
 
 void pb_launch_ring_matmul_small(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m, int trans_a,
-                                 int trans_b, uint64_t mask, uint64_t* out, cudaStream_t st);
+                                 int trans_b, const uint64_t* c, int sign, uint64_t mask, uint64_t* out,
+                                 cudaStream_t st);
+
+// out = c + sign * (a b) mod 2^ell: the small shapes fuse the add into the
+// GEMM epilogue; larger ones run pb_ring_matmul then one elementwise kernel.
+extern "C" int pb_ring_matmul_add(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m, int trans_a,
+                                  int trans_b, const uint64_t* c, int32_t sign, int32_t ell, uint64_t* out,
+                                  void* stream) {
+  if (!c || sign == 0) return pb_ring_matmul(a, b, n, k, m, trans_a, trans_b, ell, out, stream);
+  if (n > 0 && m > 0 && k > 0 && (!a || !b || !out)) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n <= 0 || m <= 0) return PB_OK;
+  if (k < 0 || n * k >= (1ll << 31) || k * m >= (1ll << 31) || n * m >= (1ll << 31))
+    return pb_set_error(PB_ERR_SHAPE, "bad matmul shape");
+  const uint64_t mask = (ell >= 64 || ell <= 0) ? ~0ull : ((1ull << ell) - 1);
+  cudaStream_t st = pb_stream_of(stream);
+  if (n * k * m < (1ll << 24)) {
+    pb_launch_ring_matmul_small(a, b, n, k, m, trans_a, trans_b, c, sign, mask, out, st);
+    PB_CHECK_LAUNCH();
+    return PB_OK;
+  }
+  if (c == out) return pb_set_error(PB_ERR_ARG, "large shapes need out != c");
+  if (int s = pb_ring_matmul(a, b, n, k, m, trans_a, trans_b, ell, out, stream)) return s;
+  return pb_ring_binary(sign > 0 ? PB_RING_ADD : PB_RING_SUB, out, c, out, n * m, n * m, ell, stream);
+}
 
 extern "C" int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m, int trans_a,
                               int trans_b, int32_t ell, uint64_t* out, void* stream) {
@@ -445,7 +468,7 @@ extern "C" int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, i
     return PB_OK;
   }
   if (n * k * m < (1ll << 24)) {  // the FC layers' local terms: one small launch beats tiles + split-K passes
-    pb_launch_ring_matmul_small(a, b, n, k, m, trans_a, trans_b, mask, out, st);
+    pb_launch_ring_matmul_small(a, b, n, k, m, trans_a, trans_b, nullptr, 0, mask, out, st);
     PB_CHECK_LAUNCH();
     return PB_OK;
   }

@@ -139,6 +139,33 @@ class _Shard:
         self.out_dst = _dev.i64_to_device(m["out_dst"])
 
 
+class _Aux:
+    def __init__(self, sess):
+        self.sess = sess
+
+    def __enter__(self):
+        self.main = torch.cuda.current_stream()
+        if _SERIAL:
+            self.stream = self.main
+            return self
+        key = self.main.cuda_stream
+        st = self.sess._aux_streams.get(key)
+        if st is None:
+            st = self.sess._aux_streams[key] = torch.cuda.Stream()
+        self.stream = st
+        st.wait_stream(self.main)
+        return self
+
+    def run(self, fn):
+        with torch.cuda.stream(self.stream):
+            return fn()
+
+    def __exit__(self, *exc):
+        if self.stream is not self.main:
+            self.main.wait_stream(self.stream)
+        return False
+
+
 class Session:
     """Both parties' protocol state: BFV keys (DO), ring params, seeds, channel.
 
@@ -166,6 +193,7 @@ class Session:
         self._seed_dev = None
         self._streams = {}
         self._grad_stream = None
+        self._aux_streams = {}
         self.capture = None  # diagnostics: a list receives (masked output ciphertexts, useful slot positions)
         # DO's pool of precomputed encryption randomness ((-a s, a), e), one
         # buffer per (layer, op, term, size): consumed in place by
@@ -212,6 +240,14 @@ class Session:
         if key not in self._streams:
             self._streams[key] = (torch.cuda.Stream(), torch.cuda.Stream())
         return self._streams[key]
+
+    def aux(self):
+        """Context for work that overlaps the protocol's critical path: inside
+        ``with sess.aux() as a``, ``a.run(fn)`` enqueues fn on an auxiliary
+        stream forked from the current one (after everything enqueued so far);
+        the current stream joins it when the block exits.  Outputs must be
+        allocated on the current stream before the block.  (PB_SERIAL=1: inline.)"""
+        return _Aux(self)
 
     def grad_stream(self) -> torch.cuda.Stream:
         """Stream the training step runs weight-gradient protocols on, concurrently
@@ -419,10 +455,13 @@ class Session:
 
 # ----------------------------------------------------------------- helpers ---
 
-def _ring_matmul(a: torch.Tensor, b: torch.Tensor, n, k, m, ell, ta=False, tb=False) -> torch.Tensor:
-    out = _dev.empty_u64(n, m)
-    _lib.call("pb_ring_matmul", _dev.ptr(a), _dev.ptr(b), n, k, m, 1 if ta else 0, 1 if tb else 0, ell,
-              _dev.ptr(out), _dev.stream())
+def _ring_matmul(a: torch.Tensor, b: torch.Tensor, n, k, m, ell, ta=False, tb=False, c=None, sign=0,
+                 out=None) -> torch.Tensor:
+    """a @ b mod 2^ell, or c + sign * (a @ b) with the add fused into the GEMM."""
+    if out is None:
+        out = _dev.empty_u64(n, m)
+    _lib.call("pb_ring_matmul_add", _dev.ptr(a), _dev.ptr(b), n, k, m, 1 if ta else 0, 1 if tb else 0,
+              _dev.ptr(c) if c is not None else None, sign if c is not None else 0, ell, _dev.ptr(out), _dev.stream())
     return out
 
 
@@ -434,9 +473,9 @@ def _ring_bin(op, a, b, ell, bn=None) -> torch.Tensor:
     return out
 
 
-def _add_bcast(a: torch.Tensor, b: torch.Tensor, inner: int, ell: int) -> torch.Tensor:
+def _add_bcast(a: torch.Tensor, b: torch.Tensor, inner: int, ell: int, out=None) -> torch.Tensor:
     """a + b broadcast along an axis (b[(i / inner) % len(b)]), one kernel."""
-    out = torch.empty_like(a)
+    out = torch.empty_like(a) if out is None else out
     _lib.call("pb_ring_add_bcast", _dev.ptr(out), _dev.ptr(a), _dev.ptr(b), a.numel(), inner, b.numel(), ell,
               _dev.stream())
     return out
@@ -473,10 +512,13 @@ def linear_forward(sess: Session, layer: int, W: RingTensor, b: RingTensor, x_a:
     if mo_x_zero:
         s_eff = s
     else:
-        s_eff = _ring_bin(_lib.RING_SUB, s, _ring_matmul(W.values, x_mo.value.values, n_o, n_i, B, ring.ell), ring.ell)
+        s_eff = _ring_matmul(W.values, x_mo.value.values, n_o, n_i, B, ring.ell, c=s, sign=-1)
     y_do = _dev.empty_u64(n_o, B)
-    sess.he_matmul(layer, OP_FWD, MatmulGeometry(n_i, n_o, B), y_do, s_eff, v_ct=x_do.value.values, w_pt=W.values)
-    y_mo = _add_bcast(s, b.values, B, ring.ell)
+    y_mo = _dev.empty_u64(n_o, B)
+    with sess.aux() as aux:  # MO's output share s + b: off the critical path
+        aux.run(lambda: _add_bcast(s, b.values, B, ring.ell, out=y_mo))
+        sess.he_matmul(layer, OP_FWD, MatmulGeometry(n_i, n_o, B), y_do, s_eff, v_ct=x_do.value.values,
+                       w_pt=W.values)
     return (ShareTensor(MO, RingTensor(y_mo, 2 * ring.f, ring, _canonical=True)),
             ShareTensor(DO, RingTensor(y_do, 2 * ring.f, ring, _canonical=True)))
 
@@ -492,8 +534,7 @@ def linear_backward_input(sess: Session, layer: int, W: RingTensor, gy_a: ShareT
     if mo_gy_zero:
         s_eff = s
     else:
-        s_eff = _ring_bin(_lib.RING_SUB, s,
-                          _ring_matmul(W.values, gy_mo.value.values, n_i, n_o, B, ring.ell, ta=True), ring.ell)
+        s_eff = _ring_matmul(W.values, gy_mo.value.values, n_i, n_o, B, ring.ell, ta=True, c=s, sign=-1)
     g_do = _dev.empty_u64(n_i, B)
     # W^T (n_i, n_o) addressed in W's storage through strides (1, n_i)
     sess.he_matmul(layer, OP_BWD_X, MatmulGeometry(n_o, n_i, B), g_do, s_eff, v_ct=gy_do.value.values,
@@ -529,23 +570,27 @@ def grad_weight(sess: Session, layer: int, x_a: ShareTensor, x_b: ShareTensor, g
     g = MatmulGeometry(B, n_o, n_i)  # v = X^T (B x n_i) via strides (1, B); W = gY (n_o x B)
     s = sess.rng(layer, OP_GRAD_W, P_MASK).uniform_ring((n_o, n_i), ring)
     cross_do = _dev.empty_u64(n_o, n_i)
-    sess.he_matmul(layer, OP_GRAD_W, g, cross_do, s,
-                   v_ct=None if mo_gy_zero else x_do.value.values, v_strides=(1, B),
-                   w_pt=None if mo_gy_zero else gy_mo.value.values,
-                   w_ct=None if mo_x_zero else gy_do.value.values,
-                   v_pt=None if mo_x_zero else x_mo.value.values,
-                   msg_in=MSG_GRADW, msg_out=MSG_GRADW)
+    loc_do = _dev.empty_u64(n_o, n_i)
+    loc_mo = _dev.empty_u64(n_o, n_i) if not (mo_x_zero or mo_gy_zero) else s
+    with sess.aux() as aux:  # the local terms do not depend on the HE result: overlap them with it
+        aux.run(lambda: _ring_matmul(gy_do.value.values, x_do.value.values, n_o, B, n_i, ring.ell, tb=True,
+                                     out=loc_do))
+        if loc_mo is not s:  # MO: s + gY_0 X_0^T
+            aux.run(lambda: _ring_matmul(gy_mo.value.values, x_mo.value.values, n_o, B, n_i, ring.ell, tb=True,
+                                         c=s, sign=1, out=loc_mo))
+        sess.he_matmul(layer, OP_GRAD_W, g, cross_do, s,
+                       v_ct=None if mo_gy_zero else x_do.value.values, v_strides=(1, B),
+                       w_pt=None if mo_gy_zero else gy_mo.value.values,
+                       w_ct=None if mo_x_zero else gy_do.value.values,
+                       v_pt=None if mo_x_zero else x_mo.value.values,
+                       msg_in=MSG_GRADW, msg_out=MSG_GRADW)
     # DO: + local term gY_1 X_1^T (+ e), sends the masked sum
-    msg = _ring_bin(_lib.RING_ADD, cross_do,
-                    _ring_matmul(gy_do.value.values, x_do.value.values, n_o, B, n_i, ring.ell, tb=True), ring.ell)
+    msg = _ring_bin(_lib.RING_ADD, cross_do, loc_do, ring.ell)
     if e is not None:
         msg = _ring_bin(_lib.RING_ADD, msg, e, ring.ell)
     sess.channel.send(DO, MSG_GRADW, msg, msg.numel() * 8)
     # MO: + s + local term gY_0 X_0^T
-    out = _ring_bin(_lib.RING_ADD, msg, s, ring.ell)
-    if not (mo_x_zero or mo_gy_zero):
-        out = _ring_bin(_lib.RING_ADD, out,
-                        _ring_matmul(gy_mo.value.values, x_mo.value.values, n_o, B, n_i, ring.ell, tb=True), ring.ell)
+    out = _ring_bin(_lib.RING_ADD, msg, loc_mo, ring.ell)
     return RingTensor(out, 2 * ring.f, ring, _canonical=True)
 
 

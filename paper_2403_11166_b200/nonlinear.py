@@ -30,15 +30,15 @@ def _dealer(sess: Session, layer: int, op_code: int, kind: int, a: ShareTensor, 
             d_in: torch.Tensor | None = None, want_d: bool = False):
     mo, do = _split(a, b)
     ring = sess.ring
-    x_mo = mo.value.values.clone()
-    x_do = do.value.values.clone()
+    in_mo, in_do = mo.value.values.contiguous(), do.value.values.contiguous()
+    x_mo, x_do = torch.empty_like(in_mo), torch.empty_like(in_do)  # fresh outputs: no input copies
     n = x_mo.numel()
     d_out = torch.empty(x_mo.shape, dtype=torch.uint8, device=x_mo.device) if want_d else None
     rng = sess.rng(layer, op_code, P_DEALER)
     off = rng.reserve(n)
     sd, sp = rng.np_args()
-    _lib.call("pb_dealer_op", kind, _dev.ptr(x_mo), _dev.ptr(x_do), n, k, _dev.ptr(d_in), _dev.ptr(d_out), sd, sp,
-              rng.stream, off, ring.ell, _dev.stream())
+    _lib.call("pb_dealer_op_out", kind, _dev.ptr(in_mo), _dev.ptr(in_do), _dev.ptr(x_mo), _dev.ptr(x_do), n, k,
+              _dev.ptr(d_in), _dev.ptr(d_out), sd, sp, rng.stream, off, ring.ell, _dev.stream())
     return x_mo, x_do, d_out
 
 
