@@ -126,62 +126,91 @@ __global__ void k_ring_lincomb(int sub, uint64_t* out, const uint64_t* base, con
   }
 }
 
-// K:206-218 ring GEMM, small shapes: 16x16 smem tiles, one output per thread, one
-// launch (pb_ring_matmul in pb_conv.cu picks it below 2^24 MACs).
+// K:206-218 ring GEMM for the FC layers' local terms (n k m < 2^24): a CTA
+// owns a 16x16 output tile and stages a whole 128-deep slab of its A rows and
+// B columns in shared memory with every load issued at once (coalesced in
+// the operand's contiguous direction), then each thread runs the slab's MACs
+// from shared memory with two accumulators -- one global round trip per 128
+// of k instead of one per 16 (the 16x16 k-tile loop was latency-bound: 9.9 us
+// for 128x128x64).  Fused epilogue: out = C + sign * (A B)  (C may be NULL).
+// TS = 8: 4 lanes per output split each slab (kk = lane mod 4) and combine
+// with two shuffles -- 4x the CTAs and a quarter of the serial MACs for the
+// mid-size local terms (128x128x64: 32 -> 128 CTAs).
+constexpr int MM_KC = 128;
 template <int TS>
-__global__ void k_ring_matmul(const uint64_t* __restrict__ A, const uint64_t* __restrict__ B, int64_t n, int64_t k,
-                              int64_t m, int ta, int tb, uint64_t mask, uint64_t* __restrict__ C) {
-  __shared__ uint64_t sa[TS][TS + 1];
-  __shared__ uint64_t sb[TS][TS + 1];
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int64_t row = (int64_t)blockIdx.y * TS + ty;
-  const int64_t col = (int64_t)blockIdx.x * TS + tx;
-  uint64_t acc = 0;
-  for (int64_t k0 = 0; k0 < k; k0 += TS) {
-    const int64_t ak = k0 + tx, bk = k0 + ty;
-    sa[ty][tx] = (row < n && ak < k) ? (ta ? A[ak * n + row] : A[row * k + ak]) : 0ull;
-    sb[ty][tx] = (bk < k && col < m) ? (tb ? B[col * k + bk] : B[bk * m + col]) : 0ull;
+__global__ void __launch_bounds__(256) k_ring_mm_tile(const uint64_t* __restrict__ A, const uint64_t* __restrict__ B,
+                                                      int n, int k, int m, int ta, int tb,
+                                                      const uint64_t* __restrict__ C, int sign, uint64_t mask,
+                                                      uint64_t* __restrict__ out) {
+  constexpr int LK = 256 / (TS * TS);  // lanes per output
+  __shared__ uint64_t sa[TS][MM_KC + 1];
+  __shared__ uint64_t sb[MM_KC][TS + 1];
+  const int tid = threadIdx.x, lane = tid % LK, oi = tid / LK, tx = oi % TS, ty = oi / TS;
+  const int row0 = blockIdx.y * TS, col0 = blockIdx.x * TS;
+  uint64_t acc0 = 0, acc1 = 0;
+  for (int k0 = 0; k0 < k; k0 += MM_KC) {
+    const int kc = min(MM_KC, k - k0);
+#pragma unroll 4
+    for (int idx = tid; idx < TS * MM_KC; idx += 256) {
+      int r, kk;
+      if (ta) kk = idx / TS, r = idx % TS;  // A stored (k, n): rows contiguous
+      else r = idx / MM_KC, kk = idx % MM_KC;  // A stored (n, k): k contiguous
+      const int gr = row0 + r, gk = k0 + kk;
+      sa[r][kk] = (gr < n && kk < kc) ? (ta ? __ldg(A + (int64_t)gk * n + gr) : __ldg(A + (int64_t)gr * k + gk)) : 0ull;
+      int c, kb;
+      if (tb) c = idx / MM_KC, kb = idx % MM_KC;  // B stored (m, k): k contiguous
+      else kb = idx / TS, c = idx % TS;           // B stored (k, m): columns contiguous
+      const int gc = col0 + c, gkb = k0 + kb;
+      sb[kb][c] = (gc < m && kb < kc) ? (tb ? __ldg(B + (int64_t)gc * k + gkb) : __ldg(B + (int64_t)gkb * m + gc)) : 0ull;
+    }
     __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < TS; ++kk) acc += sa[ty][kk] * sb[kk][tx];
+    int kk = lane;
+    for (; kk + LK < kc; kk += 2 * LK) {
+      acc0 += sa[ty][kk] * sb[kk][tx];
+      acc1 += sa[ty][kk + LK] * sb[kk + LK][tx];
+    }
+    if (kk < kc) acc0 += sa[ty][kk] * sb[kk][tx];
     __syncthreads();
   }
-  if (row < n && col < m) C[row * m + col] = acc & mask;
+  uint64_t v = acc0 + acc1;
+#pragma unroll
+  for (int off = LK / 2; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off, LK);
+  const int row = row0 + ty, col = col0 + tx;
+  if (lane == 0 && row < n && col < m) {
+    const int64_t o = (int64_t)row * m + col;
+    out[o] = (C ? (sign >= 0 ? C[o] + v : C[o] - v) : v) & mask;
+  }
 }
 
-// K:206-218 ring GEMM for the FC layers' local terms (small n x m, k <= a few
-// hundred): G lanes per output element split the contraction (lane j takes
-// k = j, j+G, ...; two independent accumulators), then a shuffle reduction.
-// One load round trip + ~k/G MACs of latency instead of a serial k-tile loop
-// (16x16 tiles: 9.9 us for 128x128x64 on B200, latency-bound).  Optional
-// fused epilogue: out = C + sign * (A B)  (sign = +1 / -1; C may be NULL).
+// Latency variant for few outputs (n m < 2^14): G lanes per output split the
+// contraction, each lane issues all loads of its next 8 k-values at once, MACs
+// them, and a shuffle tree combines the lanes -- one global round trip per 8 G
+// of k (the CTA-tile kernel needs 7.4 us for 128x128x64 with 32 CTAs on B200).
 template <int G>
-__global__ void __launch_bounds__(256) k_ring_mm_grp(const uint64_t* __restrict__ A, const uint64_t* __restrict__ B,
-                                                     int n, int k, int m, int ta, int tb,
-                                                     const uint64_t* __restrict__ C, int sign, uint64_t mask,
-                                                     uint64_t* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_ring_mm_lanes(const uint64_t* __restrict__ A, const uint64_t* __restrict__ B,
+                                                       int n, int k, int m, int ta, int tb,
+                                                       const uint64_t* __restrict__ C, int sign, uint64_t mask,
+                                                       uint64_t* __restrict__ out) {
   const int lane = threadIdx.x % G;
   const int64_t o = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
   const bool valid = o < (int64_t)n * m;
   const int row = valid ? (int)(o / m) : 0, col = valid ? (int)(o % m) : 0;
-  auto at = [&](int kk) { return ta ? __ldg(A + (int64_t)kk * n + row) : __ldg(A + (int64_t)row * k + kk); };
-  auto bt = [&](int kk) { return tb ? __ldg(B + (int64_t)col * k + kk) : __ldg(B + (int64_t)kk * m + col); };
-  uint64_t acc0 = 0, acc1 = 0;
-  int kk = lane;
-  for (; kk + G < k; kk += 2 * G) {
-    const uint64_t a0 = at(kk), b0 = bt(kk), a1 = at(kk + G), b1 = bt(kk + G);
-    acc0 += a0 * b0;
-    acc1 += a1 * b1;
+  uint64_t acc = 0;
+  for (int k0 = 0; k0 < k; k0 += 8 * G) {
+    uint64_t av[8], bv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int kk = k0 + j * G + lane;
+      const bool in = kk < k;
+      av[j] = in ? (ta ? __ldg(A + (int64_t)kk * n + row) : __ldg(A + (int64_t)row * k + kk)) : 0ull;
+      bv[j] = in ? (tb ? __ldg(B + (int64_t)col * k + kk) : __ldg(B + (int64_t)kk * m + col)) : 0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += av[j] * bv[j];
   }
-  if (kk < k) acc0 += at(kk) * bt(kk);
-  uint64_t acc = acc0 + acc1;
 #pragma unroll
   for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
-  if (lane == 0 && valid) {
-    uint64_t v = acc;
-    if (C) v = sign >= 0 ? C[o] + acc : C[o] - acc;
-    out[o] = v & mask;
-  }
+  if (lane == 0 && valid) out[o] = (C ? (sign >= 0 ? C[o] + acc : C[o] - acc) : acc) & mask;
 }
 
 __global__ void k_rowsum(const uint64_t* a, int64_t rows, int64_t cols, uint64_t mask, uint64_t* out) {
@@ -476,19 +505,32 @@ void pb_launch_ring_matmul_small(const uint64_t* a, const uint64_t* b, int64_t n
                                  int trans_b, const uint64_t* c, int sign, uint64_t mask, uint64_t* out,
                                  cudaStream_t st) {
   const int64_t outs = n * m;
+  if (outs >= (1 << 16)) {  // enough outputs to fill the GPU with 16x16 tiles
+    dim3 grd((unsigned)((m + 15) / 16), (unsigned)((n + 15) / 16));
+    k_ring_mm_tile<16><<<grd, 256, 0, st>>>(a, b, (int)n, (int)k, (int)m, trans_a, trans_b, c, sign, mask, out);
+    return;
+  }
+  if (outs >= (1 << 12)) {  // mid-size: 8x8 tiles, 4 lanes per output
+    dim3 grd((unsigned)((m + 7) / 8), (unsigned)((n + 7) / 8));
+    k_ring_mm_tile<8><<<grd, 256, 0, st>>>(a, b, (int)n, (int)k, (int)m, trans_a, trans_b, c, sign, mask, out);
+    return;
+  }
   auto go = [&](auto kern, int g) {
-    const int64_t threads = outs * g;
-    kern<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a, b, (int)n, (int)k, (int)m, trans_a, trans_b, c, sign,
-                                                            mask, out);
+    kern<<<(unsigned)((outs * g + 255) / 256), 256, 0, st>>>(a, b, (int)n, (int)k, (int)m, trans_a, trans_b, c, sign,
+                                                             mask, out);
   };
   if (k <= 8)
-    go(k_ring_mm_grp<1>, 1);
+    go(k_ring_mm_lanes<1>, 1);
+  else if (k <= 16)
+    go(k_ring_mm_lanes<2>, 2);
   else if (k <= 32)
-    go(k_ring_mm_grp<4>, 4);
+    go(k_ring_mm_lanes<4>, 4);
+  else if (k <= 64)
+    go(k_ring_mm_lanes<8>, 8);
   else if (k <= 128)
-    go(k_ring_mm_grp<16>, 16);
+    go(k_ring_mm_lanes<16>, 16);
   else
-    go(k_ring_mm_grp<32>, 32);
+    go(k_ring_mm_lanes<32>, 32);
 }
 
 extern "C" int pb_ring_add_bcast(uint64_t* out, const uint64_t* a, const uint64_t* b, int64_t n, int64_t inner,

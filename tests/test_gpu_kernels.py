@@ -124,3 +124,27 @@ def test_large_matmul(kc):
     a = rng.integers(0, 1 << 63, size=(128, 784), dtype=np.uint64)
     b = rng.integers(0, 1 << 63, size=(784, 64), dtype=np.uint64)
     assert np.array_equal(kc.matmul_wrap(a, b), OK.matmul_wrap(a, b))
+
+
+@pytest.mark.parametrize("n,k,m", [(1, 1, 1), (10, 128, 64), (128, 128, 64), (17, 300, 33), (128, 64, 784),
+                                   (5, 7, 3), (64, 129, 16)])
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_ring_matmul_add_transposes(n, k, m, ta, tb):
+    """pb_ring_matmul_add: c +/- (A B) mod 2^ell for every transpose flag, ragged
+    tiles and k across the 128-deep slab, against numpy's wrapping u64 GEMM."""
+    from paper_2403_11166_b200 import _dev, _lib
+
+    rng = np.random.default_rng(n * 1000 + k * 10 + m + ta * 7 + tb * 3)
+    a = rng.integers(0, 1 << 63, size=(n, k), dtype=np.uint64)
+    b = rng.integers(0, 1 << 63, size=(k, m), dtype=np.uint64)
+    c = rng.integers(0, 1 << 63, size=(n, m), dtype=np.uint64)
+    ab = OK.matmul_wrap(a, b)
+    mask = np.uint64((1 << 59) - 1)
+    da = _dev.u64_to_device(np.ascontiguousarray(a.T) if ta else a)
+    db = _dev.u64_to_device(np.ascontiguousarray(b.T) if tb else b)
+    dc = _dev.u64_to_device(c)
+    for sign, want in ((1, (c + ab) & mask), (-1, (c - ab) & mask), (0, ab & mask)):
+        out = _dev.empty_u64(n, m)
+        _lib.call("pb_ring_matmul_add", _dev.ptr(da), _dev.ptr(db), n, k, m, ta, tb, _dev.ptr(dc) if sign else None,
+                  sign, 59, _dev.ptr(out), _dev.stream())
+        assert np.array_equal(_dev.to_numpy_u64(out), want)
