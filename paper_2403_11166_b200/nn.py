@@ -135,15 +135,22 @@ class Model:
         return seg
 
     def sgd(self, gws, gbs, lr=1e-2, momentum=0.8, check=True):
+        for l in range(self.n_layers):
+            self.sgd_layer(l, gws[l], gbs[l], lr, momentum)
+        if check:
+            self.check_range()
+
+    def sgd_layer(self, l: int, gw: RingTensor, gb: RingTensor, lr=1e-2, momentum=0.8):
+        """SGD with momentum for layer l's (W, b) on the current stream (no host sync)."""
         ring = self.ring
         st = _dev.stream()
-        for l in range(self.n_layers):
-            for w, v, g, ring_t, scale in ((self.w[l], self.vw[l], gws[l], self.W[l], ring.f),
-                                           (self.b[l], self.vb[l], gbs[l], self.B[l], 2 * ring.f)):
-                _lib.call("pb_sgd_momentum", _dev.ptr(w), _dev.ptr(v), _dev.ptr(g.values), w.numel(), g.scale,
-                          float(lr), float(momentum), ring.ell, scale, _dev.ptr(ring_t.values), _dev.ptr(self._flag),
-                          st)
-        if check and int(self._flag.item()):
+        for w, v, g, ring_t, scale in ((self.w[l], self.vw[l], gw, self.W[l], ring.f),
+                                       (self.b[l], self.vb[l], gb, self.B[l], 2 * ring.f)):
+            _lib.call("pb_sgd_momentum", _dev.ptr(w), _dev.ptr(v), _dev.ptr(g.values), w.numel(), g.scale,
+                      float(lr), float(momentum), ring.ell, scale, _dev.ptr(ring_t.values), _dev.ptr(self._flag), st)
+
+    def check_range(self):
+        if int(self._flag.item()):
             raise EncodeRangeError("weights left the fixed-point range")
 
 
@@ -266,6 +273,12 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
             else:
                 H, Wd = acts[l][1].shape[2:]
                 ga = conv_backward_input(sess, l, model.W[l], gy_mo, gy_do, H, Wd, e[4], e[5], mo_gy_zero=last)
+        # the MO's SGD for layer l as soon as both grad W_l (grad stream) and
+        # the last use of W_l (this layer's input-gradient protocol) are enqueued
+        gstream.wait_stream(main)
+        with torch.cuda.stream(gstream):
+            model.sgd_layer(l, gws[l], gbs[l], lr, momentum)
+        if l > 0:
             if any(model.layers[k][0] == "pool" for k in seg[l - 1]):
                 t_mo, t_do = truncate(sess, l, *ga, f, backward=True)
                 for k in reversed(seg[l - 1]):
@@ -283,7 +296,8 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
                 gy_mo, gy_do = truncate_relu_backward(sess, l - 1, ds[l - 1], t_mo, t_do, f)
     main.wait_stream(gstream)
     del keep
-    model.sgd(gws, gbs, lr, momentum, check=check)
+    if check:
+        model.check_range()
     sess.join_pool()
     return gws, gbs
 
