@@ -350,6 +350,14 @@ static bool imma_enabled() {
   return on != 0;
 }
 constexpr int64_t IMMA_MIN_MACS = 1ll << 27;
+static bool imma_gradw() {  // PB_IMMA_GRADW=1: weight gradients on the int8 path too (CIFAR conv2: 1.62 ms
+  static int on = -1;         // vs 0.59 ms on the CUDA-core GEMM -- the K = B*oh*ow digit planes are HBM-bound)
+  if (on < 0) {
+    const char* e = getenv("PB_IMMA_GRADW");
+    on = e ? atoi(e) : 0;
+  }
+  return on != 0;
+}
 
 extern "C" int pb_ring_conv(int kind, const uint64_t* a, const uint64_t* b, int32_t B, int32_t c_i, int32_t c_o,
                             int32_t H, int32_t W, int32_t s, int32_t pad, int32_t stride, int32_t ell, uint64_t* out,
@@ -369,7 +377,7 @@ extern "C" int pb_ring_conv(int kind, const uint64_t* a, const uint64_t* b, int3
   {
     const int64_t macs = (int64_t)B * c_o * c_i * s * s * oh * ow;
     // the weight gradient's skinny int8 GEMMs (64 x 1600 outputs, K = B*oh*ow) lose to the CUDA-core path
-    if (imma_enabled() && kind != PB_CONV_GRADW && macs >= IMMA_MIN_MACS &&
+    if (imma_enabled() && (kind != PB_CONV_GRADW || imma_gradw()) && macs >= IMMA_MIN_MACS &&
         pb_imma_conv(kind, a, b, B, c_i, c_o, H, W, s, pad, stride, oh, ow, ell, out, st) == PB_OK) {
       PB_CHECK_LAUNCH();
       return PB_OK;

@@ -168,14 +168,17 @@ LtState& lt() {
 // C (cm x cn, column-major, int32) = A_op^T B_op: A_op = rows of `a` (K int8 each, stride lda),
 // B_op = rows of `b` (K each, stride ldb).  Descriptors + the heuristic's algorithm are cached
 // per shape (the heuristic query costs far more than a small GEMM).  Returns 0 on success.
+constexpr int LT_CANDIDATES = 12;
 struct LtPlan {
   cublasLtMatmulDesc_t op = nullptr;
   cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
   cublasLtMatmulAlgo_t algo;
-  bool ok = false;
+  cublasLtMatmulAlgo_t cand[LT_CANDIDATES];
+  int ncand = 0;
+  bool ok = false, tuned = false;
 };
 
-const LtPlan& lt_plan(int cm, int lda, int cn, int ldb, int K) {
+LtPlan& lt_plan(int cm, int lda, int cn, int ldb, int K) {
   static std::map<std::tuple<int, int, int, int, int>, LtPlan> cache;
   static std::mutex mu;
   std::lock_guard<std::mutex> g(mu);
@@ -186,7 +189,7 @@ const LtPlan& lt_plan(int cm, int lda, int cn, int ldb, int K) {
   LtState& L = lt();
   const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
   cublasLtMatmulPreference_t pref = nullptr;
-  cublasLtMatmulHeuristicResult_t heur = {};
+  cublasLtMatmulHeuristicResult_t heur[LT_CANDIDATES] = {};
   int found = 0;
   if (cublasLtMatmulDescCreate(&P.op, CUBLAS_COMPUTE_32I, CUDA_R_32I) != CUBLAS_STATUS_SUCCESS) return P;
   cublasLtMatmulDescSetAttribute(P.op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof(tA));
@@ -197,10 +200,12 @@ const LtPlan& lt_plan(int cm, int lda, int cn, int ldb, int K) {
   if (cublasLtMatmulPreferenceCreate(&pref) != CUBLAS_STATUS_SUCCESS) return P;
   cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &L.ws_bytes,
                                        sizeof(L.ws_bytes));
-  if (cublasLtMatmulAlgoGetHeuristic(L.h, P.op, P.la, P.lb, P.lc, P.lc, pref, 1, &heur, &found) ==
+  if (cublasLtMatmulAlgoGetHeuristic(L.h, P.op, P.la, P.lb, P.lc, P.lc, pref, LT_CANDIDATES, heur, &found) ==
           CUBLAS_STATUS_SUCCESS &&
       found > 0) {
-    P.algo = heur.algo;
+    P.algo = heur[0].algo;
+    for (int i = 0; i < found; ++i)
+      if (heur[i].state == CUBLAS_STATUS_SUCCESS) P.cand[P.ncand++] = heur[i].algo;
     P.ok = true;
   }
   cublasLtMatmulPreferenceDestroy(pref);
@@ -211,9 +216,37 @@ int lt_gemm_tn(const int8_t* a, int cm, int lda, const int8_t* b, int cn, int ld
                cudaStream_t st) {
   LtState& L = lt();
   if (!L.ok) return -1;
-  const LtPlan& P = lt_plan(cm, lda, cn, ldb, K);
+  LtPlan& P = lt_plan(cm, lda, cn, ldb, K);
   if (!P.ok) return -1;
   const int32_t alpha = 1, beta = 0;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (!P.tuned && P.ncand > 1 && cudaStreamIsCapturing(st, &cap) == cudaSuccess &&
+      cap == cudaStreamCaptureStatusNone) {
+    // first eager use of this shape: time the heuristic's candidates on the real
+    // operands and keep the fastest (its first pick is often a 256x256-tile kernel
+    // that leaves most of a 64-row GEMM idle); graph capture reuses the choice
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int i = 0; i < P.ncand; ++i) {
+      float ms = 0.f, tot = 0.f;
+      bool good = true;
+      for (int r = 0; r < 3 && good; ++r) {
+        cudaEventRecord(e0, st);
+        good = cublasLtMatmul(L.h, P.op, &alpha, a, P.la, b, P.lb, &beta, c, P.lc, c, P.lc, &P.cand[i], ws, L.ws_bytes,
+                              st) == CUBLAS_STATUS_SUCCESS;
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0) tot += ms;  // the first run warms up
+      }
+      if (good && tot < best) best = tot, P.algo = P.cand[i];
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    P.tuned = true;
+  }
   return cublasLtMatmul(L.h, P.op, &alpha, a, P.la, b, P.lb, &beta, c, P.lc, c, P.lc, &P.algo, ws, L.ws_bytes, st) ==
                  CUBLAS_STATUS_SUCCESS
              ? 0
