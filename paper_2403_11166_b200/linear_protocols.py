@@ -9,9 +9,7 @@ Alg. 1, Alg. 2).
     sample_dp_noise         N(0, sigma^2 C^2 / B)
 
 Per protocol message the work is three fused device kernels:
-    DO   pb_encrypt_sk_add    pack (pi_v / pi_W gather) + e + Delta m + NTT, added onto
-                          pooled (-a s, a) (pb_encrypt_sk_zero: the encryption
-                          randomness a, e, a*s, precomputed off the critical path)
+    DO   pb_encrypt_sk        pack (pi_v / pi_W gather) + Delta m + NTT + key mul
     MO   pb_ctpt_mac_mask     sum_k ct (*) pt  -  Delta NTT(pi_y(mask) + filler)
     DO   pb_decrypt_to_share  c0 + c1 s + INTT + Garner/scale-round + pi_y^-1
 plus the MO's plaintext encoding (pb_encode_plain) and ring GEMMs for the
@@ -41,7 +39,7 @@ from .poly_encoding import MatmulGeometry, conv_out_hw, plan_conv_layer, plan_ma
 from .ring import DO, MO, RingParams, RingTensor, SeededRng, ShareTensor
 
 OP_FWD, OP_BWD_X, OP_GRAD_W, OP_GRAD_B, OP_RELU, OP_TRUNC_F, OP_TRUNC_B, OP_RELU_B, OP_POOL_F, OP_POOL_B = range(10)
-P_MASK, P_ENC, P_DEALER, P_DP, P_POOL = range(5)
+P_MASK, P_ENC, P_DEALER, P_DP = range(4)
 
 # SPEC:372 message codes
 MSG_FWD_INPUT_CT = 0x10
@@ -55,7 +53,6 @@ FRAME_HEADER = 12  # {u16 type, u16 flags, u64 len}
 import os as _os
 
 _SERIAL = _os.environ.get("PB_SERIAL", "0") == "1"
-_ENC_POOL = _os.environ.get("PB_ENC_POOL", "0") == "1"
 
 
 def stream_id(layer: int, op: int, purpose: int) -> int:
@@ -194,18 +191,12 @@ class Session:
         self._streams = {}
         self._grad_stream = None
         self._aux_streams = {}
+        self._prep_stream = None
         self.capture = None  # diagnostics: a list receives (masked output ciphertexts, useful slot positions)
-        # DO's pool of precomputed encryption randomness ((-a s, a), e), one
-        # buffer per (layer, op, term, size): consumed in place by
-        # pb_encrypt_sk_add, refilled on a side stream once the MAC has read it
-        self.enc_pool = _ENC_POOL
-        self._pool = {}
-        self._pool_ev = {}  # key -> event after its pending refill (cleared by join_pool)
-        self._pool_streams = {}
-        self._pool_active = {}
-        self._pool_ctr = 0
-        self.pool_defer = False  # True: refills wait for refill_pool() (the forward pass defers them)
-        self._pool_dirty = []
+        # operands prepared ahead of their protocol (prepare_operand): key
+        # (layer, op, role) -> (device tensor, event or None); buffers persist
+        self._prepared = {}
+        self._prep_bufs = {}
 
     def rng(self, layer: int, op: int, purpose: int) -> SeededRng:
         g = SeededRng(self.seed, stream_id(layer, op, purpose))
@@ -249,6 +240,14 @@ class Session:
         allocated on the current stream before the block.  (PB_SERIAL=1: inline.)"""
         return _Aux(self)
 
+    def prep_stream(self) -> torch.cuda.Stream:
+        """Stream the eager training step prepares backward operands on."""
+        if _SERIAL:
+            return torch.cuda.current_stream()
+        if self._prep_stream is None:
+            self._prep_stream = torch.cuda.Stream()
+        return self._prep_stream
+
     def grad_stream(self) -> torch.cuda.Stream:
         """Stream the training step runs weight-gradient protocols on, concurrently
         with the input-gradient chain (they are independent given grad Y)."""
@@ -258,72 +257,60 @@ class Session:
             self._grad_stream = torch.cuda.Stream()
         return self._grad_stream
 
-    # ------------------------- encryption-randomness pool (DO side) ---
-    def _pool_fill(self, buf):
-        """buf = (ct, e) <- fresh (-a s, a), e on the current stream.  Key: the step seed
-        (device word in graph mode) on stream P_POOL; nonce: a session-wide
-        counter, so no (key, nonce) pair is ever reused."""
-        ct, e = buf
-        n = ct.shape[0]
-        seed, sptr = self.rng(0, 0, P_POOL).dev_args()
-        nonce = self._pool_ctr + self.rank * n
-        self._pool_ctr += n * self.world
-        _lib.call("pb_encrypt_sk_zero", self.ctx.handle, _dev.ptr(self.kp.sk_ntt), n, seed, sptr, nonce,
-                  _dev.ptr(ct), _dev.ptr(e), _dev.stream())
-        self._count("pb_encrypt_sk_zero", n * (2 * self.p.L * self.p.N * 4 + self.p.N))
+    # ------------------------------------------------- operand preparation ---
+    _ROLES = ("A_ct", "A_pt", "B_ct", "B_pt")
 
-    def _pool_take(self, key, n: int, s_enc: torch.cuda.Stream):
-        """n pooled (ct = (-a s, a), e) for ``key``, ready in stream order on s_enc."""
-        buf = self._pool.get(key)
-        dirty = [d for d in self._pool_dirty if d[0] == key]
-        if buf is None or dirty:  # first use, or consumed and not yet refilled: fill inline
-            if buf is None:
-                buf = self._pool[key] = (_dev.empty_u32(n, 2, self.p.L, self.p.N),
-                                         torch.empty(n, self.p.N, dtype=torch.int8, device=_dev.device()))
-            for d in dirty:
-                s_enc.wait_event(d[2])
-                self._pool_dirty.remove(d)
-            with torch.cuda.stream(s_enc):
-                self._pool_fill(buf)
+    def _operand_layout(self, plan, role):
+        """(pack, count, is_ct, nonce offset) of one MAC operand of a block plan:
+        A_ct = Enc(pi_v(v)), A_pt = pi_W(W), B_ct = Enc(pi_W(W)), B_pt = pi_v(v)."""
+        sh = self._shard(plan)
+        if role == "A_ct":
+            return sh.in_pack, sh.n_in, True, self.rank * plan.n_in
+        if role == "A_pt":
+            return sh.pt_pack, sh.n_pt, False, 0
+        if role == "B_ct":
+            return sh.pt_pack, sh.n_pt, True, self.world * plan.n_in + self.rank * plan.n_pt
+        if role == "B_pt":
+            return sh.in_pack, sh.n_in, False, 0
+        raise ValueError(f"unknown operand role {role!r}")
+
+    def _make_operand(self, layer, op, plan, role, src, buf):
+        """Enqueue the DO's encryption / the MO's encoding of one operand into buf (current stream)."""
+        pack, n, is_ct, off = self._operand_layout(plan, role)
+        h, L, N = self.ctx.handle, self.p.L, self.p.N
+        if is_ct:
+            enc_rng = self.rng(layer, op, P_ENC)
+            base = enc_rng.reserve((plan.n_in + plan.n_pt) * self.world)
+            _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(src), *_pk(pack), n,
+                      *enc_rng.dev_args(), base + off, _dev.ptr(buf), _dev.stream())
+            self._count("pb_encrypt_sk", n * (2 * L * N * 4 + 8 * N))
         else:
-            ev = self._pool_ev.pop(key, None)
-            if ev is not None:
-                s_enc.wait_event(ev)
-        return buf
+            _lib.call("pb_encode_plain_mont", h, _dev.ptr(src), *_pk(pack), n, _dev.ptr(buf), _dev.stream())
+            self._count("pb_encode_plain_mont", n * (L * N * 4 + 8 * N))
 
-    def _pool_refill(self, key, buf, after=None):
-        """Refill ``buf`` after ``after`` (an event), else after the work enqueued
-        so far on the current stream (the MAC that reads it), on a side stream
-        off the critical path."""
-        cur = torch.cuda.current_stream()
-        sp = self._pool_streams.get(cur.cuda_stream)
-        if sp is None:
-            sp = self._pool_streams[cur.cuda_stream] = torch.cuda.Stream()
-        if after is None:
-            sp.wait_stream(cur)
-        else:
-            sp.wait_event(after)
-        self._pool_active[cur.cuda_stream] = sp
-        with torch.cuda.stream(sp):
-            self._pool_fill(buf)
-        ev = torch.cuda.Event()
-        ev.record(sp)
-        self._pool_ev[key] = ev
+    def prepare_operand(self, layer: int, op: int, plan, role: str, src: torch.Tensor):
+        """Encrypt / encode one operand of the protocol (layer, op) ahead of time,
+        on the current stream, into a persistent buffer; the next he_eval of
+        (layer, op) uses it instead of producing it on its critical path.  The
+        value is the one he_eval would compute (same packing, key and nonce),
+        so the protocol's output is unchanged."""
+        pack, n, is_ct, _ = self._operand_layout(plan, role)
+        if not self._shard(plan).n_out or n == 0:
+            return
+        key = (layer, op, role)
+        shape = (n, 2, self.p.L, self.p.N) if is_ct else (n, self.p.L, self.p.N)
+        buf = self._prep_bufs.get(key)
+        if buf is None or tuple(buf.shape) != shape:
+            buf = self._prep_bufs[key] = torch.empty(shape, dtype=torch.int32, device=_dev.device())
+        self._make_operand(layer, op, plan, role, src, buf)
+        ev = None
+        if not torch.cuda.is_current_stream_capturing():
+            ev = torch.cuda.Event()
+            ev.record()
+        self._prepared[key] = (buf, ev)
 
-    def refill_pool(self):
-        """Refill every deferred pool buffer (after all work enqueued so far)."""
-        dirty, self._pool_dirty = self._pool_dirty, []
-        for key, buf, _ev in dirty:  # all their MACs were enqueued before this call
-            self._pool_refill(key, buf)
-
-    def join_pool(self):
-        """Make the current stream wait for every pending pool refill (ends a
-        step; required before a CUDA-graph capture closes)."""
-        cur = torch.cuda.current_stream()
-        for sp in self._pool_active.values():  # only streams used since the last join (capture-safe)
-            cur.wait_stream(sp)
-        self._pool_active.clear()
-        self._pool_ev.clear()
+    def clear_prepared(self):
+        self._prepared.clear()
 
     def _count(self, name, nbytes):
         if _lib.STATS is not None:
@@ -357,62 +344,38 @@ class Session:
         N, L = p.N, p.L
         w = 4  # bytes per residue
         ct_bytes = 2 * L * N * w
-        enc_rng = self.rng(layer, op, P_ENC)
-        base = enc_rng.reserve((plan.n_in + plan.n_pt) * self.world)
-        ctA = ptA = ctB = ptB = None
         if self.world > 1 or plan.kind == "conv":
             out.zero_()  # conv plans may leave structural-zero outputs without a slot
         # Buffers are allocated on the main stream; the DO's encryptions and the
         # MO's plaintext encodings run on two side streams concurrently with the
         # MO's mask NTT, and the MAC joins all three (the graph keeps the fork).
-        has_a = sh.n_out and v_ct is not None
-        has_b = sh.n_out and w_ct is not None
+        # Operands prepared ahead of time (prepare_operand) are used as they are.
+        has_a = bool(sh.n_out) and v_ct is not None
+        has_b = bool(sh.n_out) and w_ct is not None
         main = torch.cuda.current_stream()
-        pooled = []
+        ops = {}
         if has_a or has_b:
             s_enc, s_pt = self._side_streams()
             s_enc.wait_stream(main)  # covers every buffer allocated below
             s_pt.wait_stream(main)
-        if has_a:
-            keyA = (layer, op, 0, sh.n_in)
-            preA = self._pool_take(keyA, sh.n_in, s_enc) if self.enc_pool else None
-            ctA = preA[0] if preA else _dev.empty_u32(sh.n_in, 2, L, N)
-            ptA = _dev.empty_u32(sh.n_pt, L, N)
-        if has_b:
-            keyB = (layer, op, 1, sh.n_pt)
-            preB = self._pool_take(keyB, sh.n_pt, s_enc) if self.enc_pool else None
-            ctB = preB[0] if preB else _dev.empty_u32(sh.n_pt, 2, L, N)
-            ptB = _dev.empty_u32(sh.n_in, L, N)
+            todo = ((("A_ct", v_ct), ("A_pt", w_pt)) if has_a else ()) + ((("B_ct", w_ct), ("B_pt", v_pt)) if has_b else ())
+            for role, src in todo:
+                _, n, is_ct, _ = self._operand_layout(plan, role)
+                side = s_enc if is_ct else s_pt  # DO / MO
+                pre = self._prepared.pop((layer, op, role), None)
+                if pre is not None:
+                    buf, ev = pre
+                    if ev is not None:
+                        side.wait_event(ev)
+                else:
+                    buf = _dev.empty_u32(n, 2, L, N) if is_ct else _dev.empty_u32(n, L, N)
+                    with torch.cuda.stream(side):
+                        self._make_operand(layer, op, plan, role, src, buf)
+                if is_ct:
+                    self.channel.send(DO, msg_in, buf, Ciphertext(buf, p).nbytes_wire())
+                ops[role] = buf
+        ctA, ptA, ctB, ptB = ops.get("A_ct"), ops.get("A_pt"), ops.get("B_ct"), ops.get("B_pt")
         out_ct = _dev.empty_u32(sh.n_out, 2, L, N) if sh.n_out else None
-        if has_a or has_b:
-            with torch.cuda.stream(s_enc):  # DO
-                se = _dev.stream()
-                for ct, src, pack, n, nonce, key, pre in (
-                        (ctA, v_ct, sh.in_pack, sh.n_in, base + self.rank * plan.n_in, has_a and keyA,
-                         has_a and preA),
-                        (ctB, w_ct, sh.pt_pack, sh.n_pt, base + self.world * plan.n_in + self.rank * plan.n_pt,
-                         has_b and keyB, has_b and preB)):
-                    if ct is None:
-                        continue
-                    # term A: Enc_DO(pi_v(v)) (x) pi_W(W);  term B: Enc_DO(pi_W(W)) (x) pi_v(v)
-                    if self.enc_pool:
-                        _lib.call("pb_encrypt_sk_add", h, _dev.ptr(src), *_pk(pack), n, _dev.ptr(pre[1]),
-                                  _dev.ptr(ct), se)
-                        self._count("pb_encrypt_sk_add", n * (ct_bytes + 9 * N))
-                        pooled.append((key, pre))
-                    else:
-                        _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(src), *_pk(pack), n,
-                                  *enc_rng.dev_args(), nonce, _dev.ptr(ct), se)
-                        self._count("pb_encrypt_sk", n * (ct_bytes + 8 * N))
-                    self.channel.send(DO, msg_in, ct, Ciphertext(ct, p).nbytes_wire())
-            with torch.cuda.stream(s_pt):  # MO
-                sp = _dev.stream()
-                if has_a:
-                    _lib.call("pb_encode_plain_mont", h, _dev.ptr(w_pt), *_pk(sh.pt_pack), sh.n_pt, _dev.ptr(ptA), sp)
-                    self._count("pb_encode_plain_mont", sh.n_pt * (L * N * w + 8 * N))
-                if has_b:
-                    _lib.call("pb_encode_plain_mont", h, _dev.ptr(v_pt), *_pk(sh.in_pack), sh.n_in, _dev.ptr(ptB), sp)
-                    self._count("pb_encode_plain_mont", sh.n_in * (L * N * w + 8 * N))
         if sh.n_out:
             # MO: out.c0 = -Delta NTT(mask + filler), then the tiled MAC accumulates onto it
             fseed, fptr = self.rng(layer, op, P_MASK).dev_args()
@@ -430,13 +393,6 @@ class Session:
                 n_ct = (sh.n_in if ctA is not None else 0) + (sh.n_pt if ctB is not None else 0)
                 n_pt = (sh.n_pt if ctA is not None else 0) + (sh.n_in if ctB is not None else 0)
                 self._count("pb_ctpt_mac_tiled", n_ct * ct_bytes + n_pt * L * N * w + sh.n_out * (ct_bytes + L * N * w))
-            for key, pre in pooled:  # the MAC has consumed them: precompute the next (a, -a s, e)
-                if self.pool_defer:
-                    ev = torch.cuda.Event()
-                    ev.record(main)
-                    self._pool_dirty.append((key, pre, ev))
-                else:
-                    self._pool_refill(key, pre)
             self.channel.send(MO, msg_out, out_ct, Ciphertext(out_ct, p).nbytes_wire())
             if self.capture is not None:
                 self.capture.append((out_ct.clone(), sh.out_pos.clone()))
@@ -445,7 +401,7 @@ class Session:
                       _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U, _dev.ptr(out), _dev.ptr(scratch), st)
             self._count("pb_decrypt_to_share", sh.n_out * (ct_bytes + 8 * sh.U))
             # operands stay referenced until here, i.e. until every kernel is enqueued
-            del ctA, ptA, ctB, ptB, out_ct, scratch
+            del ctA, ptA, ctB, ptB, ops, out_ct, scratch
         if self.world > 1:
             import torch.distributed as dist
 

@@ -22,12 +22,13 @@ import torch
 
 from . import _dev, _lib
 from .errors import EncodeRangeError, ShapeError
-from .linear_protocols import (Session, conv_backward_input, conv_forward, conv_grad_weight, grad_weight,
-                               linear_backward_input, linear_forward, reveal_grad_bias, reveal_grad_bias_conv)
+from .linear_protocols import (OP_BWD_X, OP_GRAD_W, Session, conv_backward_input, conv_forward, conv_grad_weight,
+                               grad_weight, linear_backward_input, linear_forward, reveal_grad_bias,
+                               reveal_grad_bias_conv)
 from . import preprocessing as PP
 from .nonlinear import (avgpool_backward, avgpool_forward, relu_backward, relu_forward, relu_truncate, truncate,
                         truncate_relu_backward)
-from .poly_encoding import conv_out_hw
+from .poly_encoding import MatmulGeometry, conv_out_hw, plan_matmul
 from .ring import DO, MO, RingParams, RingTensor, SeededRng, ShareTensor, arith_shift, encode_fixed
 
 MODELS = {
@@ -195,13 +196,7 @@ def forward_phase(sess: Session, model: Model, x: RingTensor, prep=None):
     seg = model.segments()
     cur = (ShareTensor(MO, RingTensor(torch.zeros_like(x.values), f, ring, _canonical=True)), ShareTensor(DO, x))
     acts, ds, ys = [], [], []
-    # Enc(0) pool refills of the forward layers are deferred to the backward
-    # pass (they would otherwise run beside the tail the DO waits on for the logits)
-    defer, sess.pool_defer = sess.pool_defer, True
-    try:
-        _forward_layers(sess, model, prep, cur, acts, ds, ys, seg)
-    finally:
-        sess.pool_defer = defer
+    _forward_layers(sess, model, prep, cur, acts, ds, ys, seg)
     # the MO sends its share of the logits; the DO reconstructs them
     y_mo, y_do = ys[-1]
     logits = y_mo.value + y_do.value
@@ -244,7 +239,6 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
     # input-gradient chain to layer l-1 are independent given grad Y_l: Alg.2
     # runs on the session's grad stream, overlapping the chain on this stream.
     main, gstream = torch.cuda.current_stream(), sess.grad_stream()
-    sess.refill_pool()  # the forward pass's deferred Enc(0) refills, beside the backward chain
     keep = []  # grad Y shares read on the grad stream stay referenced until the join
     for l in reversed(range(L)):
         e = model.layers[model.lin[l]]
@@ -298,8 +292,40 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
     del keep
     if check:
         model.check_range()
-    sess.join_pool()
+    sess.clear_prepared()
     return gws, gbs
+
+
+def prepare_backward(sess: Session, model: Model, state, prep=None):
+    """Produce, ahead of the loss gradient, every backward-pass HE operand that
+    depends only on the forward pass: the MO's encodings of W_l (input-gradient
+    protocols) and of its activation shares, the DO's encryptions of its
+    activation shares (weight-gradient cross terms).  Enqueued on the current
+    stream; the backward protocols pick them up (Session.prepare_operand) and
+    only the gradient-dependent operands remain on their critical path.  FC
+    layers of mode "fullhe"; other layers prepare nothing."""
+    sess.clear_prepared()
+    if prep is not None:
+        return
+    acts = state[0]
+    L = model.n_layers
+    N = sess.p.N
+    for l in range(L):
+        if model.layers[model.lin[l]][0] != "fc":
+            continue
+        n_o, n_i = model.W[l].shape
+        x_mo, x_do = acts[l]
+        if x_mo.owner_role != MO:
+            x_mo, x_do = x_do, x_mo
+        B = x_do.shape[1]
+        if l > 0:  # linear_backward_input: W^T through strides (1, n_i)
+            plan = plan_matmul(MatmulGeometry(n_o, n_i, B), N, None, (1, n_i), None)
+            sess.prepare_operand(l, OP_BWD_X, plan, "A_pt", model.W[l].values)
+        plan = plan_matmul(MatmulGeometry(B, n_o, n_i), N, (1, B), None, None)  # grad_weight
+        if l < L - 1:  # term A: Enc(X_1) (x) gY_0
+            sess.prepare_operand(l, OP_GRAD_W, plan, "A_ct", x_do.value.values)
+        if l > 0:  # term B: Enc(gY_1) (x) X_0
+            sess.prepare_operand(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values)
 
 
 def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e-2, momentum=0.8,
@@ -308,7 +334,12 @@ def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e
     feature-major for FC-first models, (B, C, H, W) for CNNs.  ``prep``
     selects SPEC's mode "prep" (Pencil+, Alg. 4) over "fullhe"."""
     state, logits = forward_phase(sess, model, x, prep)
+    main, side = torch.cuda.current_stream(), sess.prep_stream()
+    side.wait_stream(main)
+    with torch.cuda.stream(side):  # overlaps the host's loss computation
+        prepare_backward(sess, model, state, prep)
     loss, g = softmax_ce_grad(logits.numpy(), np.asarray(labels), model.ring)  # DO, float64 (host)
+    main.wait_stream(side)
     gws, gbs = backward_phase(sess, model, state, _dev.u64_to_device(g), lr, momentum, trace, check, prep)
     return loss, gws, gbs
 
@@ -334,14 +365,19 @@ class GraphStep:
         self.g_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
         # warm-up (eager, graph-mode keys): builds plans/maps, sizes scratch buffers
         st, lg = forward_phase(sess, model, x, prep)
+        prepare_backward(sess, model, st, prep)
         backward_phase(sess, model, st, self.g_do, lr, momentum, check=False, prep=prep)
         torch.cuda.synchronize()
         self.g_fwd = torch.cuda.CUDAGraph()
+        self.g_pre = torch.cuda.CUDAGraph()
         self.g_bwd = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.g_fwd):
             self.state, self.logits = forward_phase(sess, model, x, prep)
+        with torch.cuda.graph(self.g_pre, pool=self.g_fwd.pool()):
+            prepare_backward(sess, model, self.state, prep)
         with torch.cuda.graph(self.g_bwd, pool=self.g_fwd.pool()):
             self.grads = backward_phase(sess, model, self.state, self.g_do, lr, momentum, check=False, prep=prep)
+        self._pre_stream = torch.cuda.Stream()
         torch.cuda.synchronize()
 
     def load_batch(self, x_host: torch.Tensor):
@@ -362,9 +398,13 @@ class GraphStep:
 
     def step(self, seed: int, labels):
         self.sess.reseed(seed)
+        main = torch.cuda.current_stream()
         self.g_fwd.replay()
+        self._pre_stream.wait_stream(main)
+        with torch.cuda.stream(self._pre_stream):  # backward operands, beside the host's loss
+            self.g_pre.replay()
         self.logits_host.copy_(self.logits.values, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        main.synchronize()
         if self._flag_pending:
             self._flag_pending = False
             if int(self._flag_host[0]):
@@ -375,6 +415,7 @@ class GraphStep:
         loss, g = softmax_ce_grad(self.logits_host.numpy().view(np.uint64), np.asarray(labels), self.model.ring)
         self.g_host.numpy().view(np.uint64)[...] = g
         self.g_do.copy_(self.g_host, non_blocking=True)
+        main.wait_stream(self._pre_stream)
         self.g_bwd.replay()
         return loss
 
