@@ -557,8 +557,9 @@ def grad_weight(sess: Session, layer: int, x_a: ShareTensor, x_b: ShareTensor, g
 # folded into the plan maps (poly_encoding.plan_conv_layer), through the same
 # fused kernels as the FC protocols; local terms use pb_ring_conv.
 
-def _ring_conv(kind: int, a: torch.Tensor, b: torch.Tensor, B, c_i, c_o, H, W, s, pad, stride, ell, out_shape):
-    out = _dev.empty_u64(*out_shape)
+def _ring_conv(kind: int, a: torch.Tensor, b: torch.Tensor, B, c_i, c_o, H, W, s, pad, stride, ell, out_shape,
+               out=None):
+    out = _dev.empty_u64(*out_shape) if out is None else out
     _lib.call("pb_ring_conv", kind, _dev.ptr(a), _dev.ptr(b), B, c_i, c_o, H, W, s, pad, stride, ell, _dev.ptr(out),
               _dev.stream())
     return out
@@ -599,8 +600,10 @@ def conv_forward(sess: Session, layer: int, W: RingTensor, b: RingTensor, x_a: S
         s_eff = _ring_bin(_lib.RING_SUB, msk, loc, ring.ell)
     plan = plan_conv_layer("fwd", B, c_i, c_o, H, Wd, s, pad, stride, sess.p.N)
     y_do = _dev.empty_u64(B, c_o, oh, ow)
-    sess.he_eval(layer, OP_FWD, plan, y_do, s_eff, v_ct=x_do.value.values, w_pt=W.values)
-    y_mo = _add_bcast(msk, b.values, oh * ow, ring.ell)
+    y_mo = _dev.empty_u64(B, c_o, oh, ow)
+    with sess.aux() as aux:  # MO's output share s + b: off the critical path
+        aux.run(lambda: _add_bcast(msk, b.values, oh * ow, ring.ell, out=y_mo))
+        sess.he_eval(layer, OP_FWD, plan, y_do, s_eff, v_ct=x_do.value.values, w_pt=W.values)
     return (ShareTensor(MO, RingTensor(y_mo, 2 * ring.f, ring, _canonical=True)),
             ShareTensor(DO, RingTensor(y_do, 2 * ring.f, ring, _canonical=True)))
 
@@ -642,21 +645,26 @@ def conv_grad_weight(sess: Session, layer: int, x_a: ShareTensor, x_b: ShareTens
     msk = sess.rng(layer, OP_GRAD_W, P_MASK).uniform_ring((c_o, c_i, s, s), ring)
     plan = plan_conv_layer("gradw", B, c_i, c_o, H, Wd, s, pad, stride, sess.p.N)
     cross_do = _dev.empty_u64(c_o, c_i, s, s)
-    sess.he_eval(layer, OP_GRAD_W, plan, cross_do, msk,
-                 v_ct=None if mo_gy_zero else x_do.value.values, w_pt=None if mo_gy_zero else gy_mo.value.values,
-                 w_ct=None if mo_x_zero else gy_do.value.values, v_pt=None if mo_x_zero else x_mo.value.values,
-                 msg_in=MSG_GRADW, msg_out=MSG_GRADW)
     shp = (c_o, c_i, s, s)
-    loc_do = _ring_conv(_lib.CONV_GRADW, x_do.value.values, gy_do.value.values, B, c_i, c_o, H, Wd, s, pad, stride,
-                        ring.ell, shp)
+    loc_do = _dev.empty_u64(*shp)
+    two = not (mo_x_zero or mo_gy_zero)
+    loc_mo = _dev.empty_u64(*shp) if two else None
+    with sess.aux() as aux:  # the local terms do not depend on the HE result: overlap them with it
+        aux.run(lambda: _ring_conv(_lib.CONV_GRADW, x_do.value.values, gy_do.value.values, B, c_i, c_o, H, Wd, s,
+                                   pad, stride, ring.ell, shp, out=loc_do))
+        if two:
+            aux.run(lambda: _ring_conv(_lib.CONV_GRADW, x_mo.value.values, gy_mo.value.values, B, c_i, c_o, H, Wd,
+                                       s, pad, stride, ring.ell, shp, out=loc_mo))
+        sess.he_eval(layer, OP_GRAD_W, plan, cross_do, msk,
+                     v_ct=None if mo_gy_zero else x_do.value.values, w_pt=None if mo_gy_zero else gy_mo.value.values,
+                     w_ct=None if mo_x_zero else gy_do.value.values, v_pt=None if mo_x_zero else x_mo.value.values,
+                     msg_in=MSG_GRADW, msg_out=MSG_GRADW)
     msg = _ring_bin(_lib.RING_ADD, cross_do, loc_do, ring.ell)  # DO: + local term (+ e)
     if e is not None:
         msg = _ring_bin(_lib.RING_ADD, msg, e, ring.ell)
     sess.channel.send(DO, MSG_GRADW, msg, msg.numel() * 8)
     out = _ring_bin(_lib.RING_ADD, msg, msk, ring.ell)  # MO: + s + local term
-    if not (mo_x_zero or mo_gy_zero):
-        loc_mo = _ring_conv(_lib.CONV_GRADW, x_mo.value.values, gy_mo.value.values, B, c_i, c_o, H, Wd, s, pad,
-                            stride, ring.ell, shp)
+    if two:
         out = _ring_bin(_lib.RING_ADD, out, loc_mo, ring.ell)
     return RingTensor(out, 2 * ring.f, ring, _canonical=True)
 

@@ -28,7 +28,7 @@ from .linear_protocols import (OP_BWD_X, OP_GRAD_W, Session, conv_backward_input
 from . import preprocessing as PP
 from .nonlinear import (avgpool_backward, avgpool_forward, relu_backward, relu_forward, relu_truncate, truncate,
                         truncate_relu_backward)
-from .poly_encoding import MatmulGeometry, conv_out_hw, plan_matmul
+from .poly_encoding import MatmulGeometry, conv_out_hw, plan_conv_layer, plan_matmul
 from .ring import DO, MO, RingParams, RingTensor, SeededRng, ShareTensor, arith_shift, encode_fixed
 
 MODELS = {
@@ -303,7 +303,7 @@ def prepare_backward(sess: Session, model: Model, state, prep=None):
     activation shares (weight-gradient cross terms).  Enqueued on the current
     stream; the backward protocols pick them up (Session.prepare_operand) and
     only the gradient-dependent operands remain on their critical path.  FC
-    layers of mode "fullhe"; other layers prepare nothing."""
+    and conv layers of mode "fullhe"; Pencil+ (prep) prepares nothing."""
     sess.clear_prepared()
     if prep is not None:
         return
@@ -311,12 +311,26 @@ def prepare_backward(sess: Session, model: Model, state, prep=None):
     L = model.n_layers
     N = sess.p.N
     for l in range(L):
-        if model.layers[model.lin[l]][0] != "fc":
-            continue
-        n_o, n_i = model.W[l].shape
+        e = model.layers[model.lin[l]]
         x_mo, x_do = acts[l]
         if x_mo.owner_role != MO:
             x_mo, x_do = x_do, x_mo
+        if e[0] == "conv":
+            B, c_i, H, Wd = x_do.shape
+            c_o, s = model.W[l].shape[0], model.W[l].shape[2]
+            pad, stride = e[4], e[5]
+            if l > 0:  # conv_backward_input
+                plan = plan_conv_layer("bwdx", B, c_i, c_o, H, Wd, s, pad, stride, N)
+                sess.prepare_operand(l, OP_BWD_X, plan, "A_pt", model.W[l].values)
+            plan = plan_conv_layer("gradw", B, c_i, c_o, H, Wd, s, pad, stride, N)  # conv_grad_weight
+            if l < L - 1:
+                sess.prepare_operand(l, OP_GRAD_W, plan, "A_ct", x_do.value.values)
+            if l > 0:
+                sess.prepare_operand(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values)
+            continue
+        if e[0] != "fc":
+            continue
+        n_o, n_i = model.W[l].shape
         B = x_do.shape[1]
         if l > 0:  # linear_backward_input: W^T through strides (1, n_i)
             plan = plan_matmul(MatmulGeometry(n_o, n_i, B), N, None, (1, n_i), None)
