@@ -151,9 +151,9 @@ constexpr int MAC_FOLD2 = 6;   // two terms (two products per k-step)
 // stages -- the L2 latency that bounded the register-load kernel is off the
 // critical path, and the math is one IMAD.WIDE.U32 per mod-MAC.
 
-template <int TB, int TO, int V>
+template <int TB, int TO, int V, int CT = MAC_THREADS>
 struct PipeCfg {
-  static constexpr int SLOT = MAC_THREADS * V * 4;  // bytes per operand slice
+  static constexpr int SLOT = CT * V * 4;  // bytes per operand slice
   static constexpr int SLOTS_A = 2 * TB + TO;       // ct c0/c1 per batch block + pt per output block
   static constexpr int SLOTS_B = 2 * TO + TB;
 };
@@ -311,18 +311,18 @@ __global__ void __launch_bounds__(MAC_THREADS, MINB)
 // by an "empty" mbarrier the four consumer warps arrive on, so the consumers
 // never wait for the issuing thread at a CTA barrier (ncu on k_mac_pipe: 26%
 // of stall samples were the per-k __syncthreads behind thread 0's issue work).
-template <int TB, int TO, int V, int STAGES, int MINB = 1>
-__global__ void __launch_bounds__(MAC_THREADS + 32, MINB)
+template <int TB, int TO, int V, int STAGES, int MINB = 1, int CT = MAC_THREADS>
+__global__ void __launch_bounds__(CT + 32, MINB)
     k_mac_ws(PbDev P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB, int nB,
              int nO, int nI, uint32_t* ct_out) {
-  using C = PipeCfg<TB, TO, V>;
+  using C = PipeCfg<TB, TO, V, CT>;
   using VT = typename Vec<V>::T;
   extern __shared__ __align__(128) uint8_t pipe_sm[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const int CA = 0, PA = 2 * TB, CB = ctA ? C::SLOTS_A : 0, PB = CB + 2 * TO;
   const int nslots = (ctA ? C::SLOTS_A : 0) + (ctB ? C::SLOTS_B : 0);
   const int N = P.N, L = P.L;
-  const int slices = N / (V * MAC_THREADS);
+  const int slices = N / (V * CT);
   const int tilesO = (nO + TO - 1) / TO;
   const int tb = blockIdx.x / tilesO, to = blockIdx.x % tilesO;
   const int l = blockIdx.y / slices, sl = blockIdx.y % slices;
@@ -336,14 +336,14 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, MINB)
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MAC_THREADS / 32);
+      mbar_init(&empty[s], CT / 32);
     }
     mbar_init_fence();
   }
   __syncthreads();
 
-  if (tid >= MAC_THREADS) {  // ---- producer warp (one thread; slot table in registers)
-    if (tid != MAC_THREADS) return;
+  if (tid >= CT) {  // ---- producer warp (one thread; slot table in registers)
+    if (tid != CT) return;
     constexpr int NS = C::SLOTS_A + C::SLOTS_B;
     const size_t rowb = (size_t)N * 4;
     const size_t off = (size_t)sl * C::SLOT + (size_t)l * rowb;
@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, MINB)
   auto fin = [&](uint64_t a) { return csub(mont_lazy(reduce64(a, q, mu), 1u, q, qn), q); };
   VT* out = reinterpret_cast<VT*>(ct_out);
   const size_t row = (size_t)N / V;
-  const size_t v = (size_t)sl * MAC_THREADS + tid;
+  const size_t v = (size_t)sl * CT + tid;
 #pragma unroll
   for (int i = 0; i < TB; ++i)
 #pragma unroll
@@ -477,19 +477,19 @@ __global__ void __launch_bounds__(MAC_THREADS + 32, MINB)
     }
 }
 
-template <int TB, int TO, int V, int STAGES, int MINB = 1>
+template <int TB, int TO, int V, int STAGES, int MINB = 1, int CT = MAC_THREADS>
 void launch_ws(const PbDev& P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB,
                int nB, int nO, int nI, uint32_t* out, cudaStream_t st) {
-  using C = PipeCfg<TB, TO, V>;
+  using C = PipeCfg<TB, TO, V, CT>;
   const size_t smem = (size_t)STAGES * ((ctA ? C::SLOTS_A : 0) + (ctB ? C::SLOTS_B : 0)) * C::SLOT;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_mac_ws<TB, TO, V, STAGES, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_mac_ws<TB, TO, V, STAGES, MINB, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)((size_t)STAGES * (C::SLOTS_A + C::SLOTS_B) * C::SLOT));
     attr = true;
   }
-  dim3 grid((unsigned)(((nB + TB - 1) / TB) * ((nO + TO - 1) / TO)), (unsigned)(P.L * (P.N / (V * MAC_THREADS))));
-  k_mac_ws<TB, TO, V, STAGES, MINB><<<grid, MAC_THREADS + 32, smem, st>>>(P, ctA, ptA, ctB, ptB, nB, nO, nI, out);
+  dim3 grid((unsigned)(((nB + TB - 1) / TB) * ((nO + TO - 1) / TO)), (unsigned)(P.L * (P.N / (V * CT))));
+  k_mac_ws<TB, TO, V, STAGES, MINB, CT><<<grid, CT + 32, smem, st>>>(P, ctA, ptA, ctB, ptB, nB, nO, nI, out);
 }
 
 template <int TB, int TO, int V, int STAGES, int MINB = 1>
