@@ -335,6 +335,16 @@ int pb_sgd_momentum(double* w, double* v, const uint64_t* grad_ring, int64_t n, 
                     double lr, double momentum, int32_t ell, int32_t w_scale, uint64_t* w_ring,
                     int32_t* range_flag, void* stream);
 
+/* The DO's host-side softmax cross-entropy around numpy's
+ * exp / log: pb_host_softmax_pre writes z = logits/2^f2 (signed, ell bits)
+ * minus the column max into z [C][B]; the caller sets z = exp(z) with numpy;
+ * pb_host_softmax_post normalises, returns the label probabilities (for the
+ * caller's numpy log / mean) and g = floor((p - onehot)/B * 2^f) mod 2^ell.
+ * Host functions (no device work); bit-identical to oracle/protocols.py. */
+int pb_host_softmax_pre(const uint64_t* logits, int32_t C, int32_t B, int32_t ell, int32_t f2, double* z);
+int pb_host_softmax_post(double* ez, int32_t C, int32_t B, const int64_t* labels, int32_t ell, int32_t f,
+                         double* p_lab, uint64_t* g_out);
+
 #ifdef __cplusplus
 }
 #endif

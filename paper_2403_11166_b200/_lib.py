@@ -79,6 +79,9 @@ SIGNATURES = {
     "pb_share": [P, I64, U64, P, U64, U64, I32, P, P, P],
     "pb_ring_matmul": [P, P, I64, I64, I64, INT, INT, I32, P, P],
     "pb_ring_matmul_add": [P, P, I64, I64, I64, INT, INT, P, I32, I32, P, P],
+    "pb_host_softmax_pre": [P, I32, I32, I32, I32, P],
+    "pb_host_softmax_post": [P, I32, I32, P, I32, I32, P, P],
+    "pb_host_mean": [P, I64],
     "pb_ring_rowsum": [P, I64, I64, I32, P, P],
     "pb_im2col": [P, I32, I32, I32, I32, I32, I32, P, P],
     "pb_col2im": [P, I32, I32, I32, I32, I32, I32, P, P],
@@ -91,7 +94,7 @@ SIGNATURES = {
     "pb_dealer_op_out": [INT, P, P, P, P, I64, I32, P, P, U64, P, U64, U64, I32, P],
     "pb_sgd_momentum": [P, P, P, I64, I32, F64, F64, I32, I32, P, P, P],
 }
-_RET = {"pb_last_error": ctypes.c_char_p}
+_RET = {"pb_last_error": ctypes.c_char_p, "pb_host_mean": ctypes.c_double}
 
 # ring / pointwise / dealer op codes (mirror the enums in pencil_b200.h)
 PW_MUL, PW_MAC, PW_ADD, PW_SUB = 0, 1, 2, 3

@@ -1,0 +1,83 @@
+// pb_host.cu -- the DO's host-side loss step of the training loop
+// (softmax cross-entropy on the reconstructed logits; the
+// reference computes it with numpy on the host, oracle/protocols.py
+// softmax_ce_grad).  Everything except exp / log, which the caller evaluates
+// with numpy so the values are numpy's bit for bit, runs here in two calls:
+// the ~15 small numpy ops it replaces cost ~45 us of the step's critical path.
+#include <cmath>
+#include <cstdint>
+
+#include "pencil_b200.h"
+
+// numpy's pairwise summation of n contiguous doubles (numpy/_core/src/umath/
+// loops_utils.h.src pairwise_sum, PW_BLOCKSIZE 128), the order np.add.reduce
+// uses along a contiguous axis.
+static double pairwise_sum(const double* a, int64_t n) {
+  if (n < 8) {
+    double res = -0.0;
+    for (int64_t i = 0; i < n; ++i) res += a[i];
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return pairwise_sum(a, n2) + pairwise_sum(a + n2, n - n2);
+}
+
+// np.mean of a contiguous 1-D float64 array: pairwise add-reduce, divided by n.
+extern "C" double pb_host_mean(const double* a, int64_t n) {
+  if (n < 1) return NAN;
+  return pairwise_sum(a, n) / (double)n;
+}
+
+extern "C" int pb_host_softmax_pre(const uint64_t* logits, int32_t C, int32_t B, int32_t ell, int32_t f2, double* z) {
+  if (!logits || !z || C < 1 || B < 1 || ell < 2 || ell > 63 || f2 < 0 || f2 > 62) return PB_ERR_ARG;
+  const uint64_t mask = (1ull << ell) - 1, half = 1ull << (ell - 1);
+  const double inv = std::ldexp(1.0, -f2);  // exact: x / 2^f2 == x * 2^-f2
+  for (int64_t i = 0; i < (int64_t)C * B; ++i) {
+    const uint64_t v = ((logits[i] & mask) ^ half) - half;  // two's complement of ell bits
+    z[i] = (double)(int64_t)v * inv;
+  }
+  for (int b = 0; b < B; ++b) {  // column max, subtracted (z - z.max(axis=0))
+    double m = z[b];
+    for (int c = 1; c < C; ++c) m = z[(int64_t)c * B + b] > m ? z[(int64_t)c * B + b] : m;
+    for (int c = 0; c < C; ++c) z[(int64_t)c * B + b] -= m;
+  }
+  return PB_OK;
+}
+
+// ez = exp(z) in place (numpy) -> sm = ez / ez.sum(axis=0); p_lab[b] =
+// sm[label_b][b]; g = floor((sm - onehot) / B * 2^f) mod 2^ell into g_out.
+extern "C" int pb_host_softmax_post(double* ez, int32_t C, int32_t B, const int64_t* labels, int32_t ell, int32_t f,
+                                    double* p_lab, uint64_t* g_out) {
+  if (!ez || !labels || !p_lab || !g_out || C < 1 || B < 1 || ell < 2 || ell > 63) return PB_ERR_ARG;
+  const uint64_t mask = (1ull << ell) - 1;
+  const double scale = std::ldexp(1.0, f);
+  for (int b = 0; b < B; ++b) {
+    if (labels[b] < 0 || labels[b] >= C) return PB_ERR_ARG;
+    double s;
+    if (B == 1) {  // a contiguous column: numpy reduces it pairwise
+      s = pairwise_sum(ez, C);
+    } else {  // strided axis-0 reduction: rows accumulated in order
+      s = ez[b];
+      for (int c = 1; c < C; ++c) s += ez[(int64_t)c * B + b];
+    }
+    for (int c = 0; c < C; ++c) ez[(int64_t)c * B + b] /= s;
+    p_lab[b] = ez[labels[b] * B + b];
+    ez[labels[b] * B + b] -= 1.0;
+  }
+  for (int64_t i = 0; i < (int64_t)C * B; ++i) {
+    const double g = ez[i] / (double)B * scale;
+    g_out[i] = (uint64_t)(int64_t)std::floor(g) & mask;
+  }
+  return PB_OK;
+}

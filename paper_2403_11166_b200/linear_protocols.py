@@ -53,6 +53,7 @@ FRAME_HEADER = 12  # {u16 type, u16 flags, u64 len}
 import os as _os
 
 _SERIAL = _os.environ.get("PB_SERIAL", "0") == "1"
+_PRIO = tuple(int(v) for v in _os.environ.get("PB_PRIO", "0,0").split(","))  # (encrypt, encode) stream priorities
 
 
 def stream_id(layer: int, op: int, purpose: int) -> int:
@@ -229,7 +230,10 @@ class Session:
             return cur, cur
         key = torch.cuda.current_stream().cuda_stream
         if key not in self._streams:
-            self._streams[key] = (torch.cuda.Stream(), torch.cuda.Stream())
+            # stream priorities (PB_PRIO="enc,encode"): measured no effect on the
+            # MLP step (profiles/r01_ab_stream_priority.txt), default equal
+            pe, pp = _PRIO
+            self._streams[key] = (torch.cuda.Stream(priority=pe), torch.cuda.Stream(priority=pp))
         return self._streams[key]
 
     def aux(self):
@@ -288,12 +292,14 @@ class Session:
             _lib.call("pb_encode_plain_mont", h, _dev.ptr(src), *_pk(pack), n, _dev.ptr(buf), _dev.stream())
             self._count("pb_encode_plain_mont", n * (L * N * 4 + 8 * N))
 
-    def prepare_operand(self, layer: int, op: int, plan, role: str, src: torch.Tensor):
+    def prepare_operand(self, layer: int, op: int, plan, role: str, src: torch.Tensor, event: bool = True):
         """Encrypt / encode one operand of the protocol (layer, op) ahead of time,
         on the current stream, into a persistent buffer; the next he_eval of
         (layer, op) uses it instead of producing it on its critical path.  The
         value is the one he_eval would compute (same packing, key and nonce),
-        so the protocol's output is unchanged."""
+        so the protocol's output is unchanged.  ``event``: the consumer waits
+        on an event recorded here (False when another mechanism orders them,
+        e.g. a separately captured graph replayed before the consumer's)."""
         pack, n, is_ct, _ = self._operand_layout(plan, role)
         if not self._shard(plan).n_out or n == 0:
             return
@@ -304,7 +310,7 @@ class Session:
             buf = self._prep_bufs[key] = torch.empty(shape, dtype=torch.int32, device=_dev.device())
         self._make_operand(layer, op, plan, role, src, buf)
         ev = None
-        if not torch.cuda.is_current_stream_capturing():
+        if event:
             ev = torch.cuda.Event()
             ev.record()
         self._prepared[key] = (buf, ev)

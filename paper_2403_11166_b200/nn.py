@@ -159,21 +159,57 @@ def build_model(name, ring: RingParams, seed: int = 0) -> Model:
     return Model(name, ring, seed)
 
 
+class SoftmaxCE:
+    """The DO's loss step for fixed (classes, batch): softmax
+    cross-entropy in float64 on the reconstructed logits, bit-identical to
+    oracle/protocols.py softmax_ce_grad.  numpy evaluates exp / log (so the
+    values are numpy's), the library's host helpers (pb_host_softmax_*,
+    pb_host_mean: numpy's pairwise mean) everything around them, on buffers
+    whose addresses are resolved once -- ~15 small numpy ops (~50 us) become
+    ~12 us on the step's critical path."""
+
+    def __init__(self, ring: RingParams, C: int, B: int, logits=None, g_out=None):
+        self.ring, self.C, self.B = ring, C, B
+        self.z = np.empty((C, B), dtype=np.float64)
+        self.p = np.empty(B, dtype=np.float64)
+        self.lab = np.empty(B, dtype=np.int64)
+        self.g = np.empty((C, B), dtype=np.uint64) if g_out is None else g_out
+        self.logits = logits
+        lib = _lib.load()
+        self._pre, self._post, self._mean = lib.pb_host_softmax_pre, lib.pb_host_softmax_post, lib.pb_host_mean
+        addr = lambda a: a.__array_interface__["data"][0]  # noqa: E731
+        self.az, self.ap, self.alab, self.ag = addr(self.z), addr(self.p), addr(self.lab), addr(self.g)
+        self.alog = addr(logits) if logits is not None else None
+
+    def __call__(self, labels, logits=None):
+        """(loss, g) with g = encode_f((softmax - onehot) / B) mod 2^ell in self.g."""
+        if logits is None:
+            alog = self.alog
+        else:
+            logits = np.ascontiguousarray(logits, dtype=np.uint64)
+            alog = logits.__array_interface__["data"][0]
+        self.lab[...] = labels
+        r = self.ring
+        _lib.check(self._pre(alog, self.C, self.B, r.ell, 2 * r.f, self.az), "pb_host_softmax_pre")
+        np.exp(self.z, out=self.z)
+        _lib.check(self._post(self.az, self.C, self.B, self.alab, r.ell, r.f, self.ap, self.ag),
+                   "pb_host_softmax_post")
+        np.log(self.p, out=self.p)
+        return -self._mean(self.ap, self.B), self.g
+
+
+_SMCE = {}
+
+
 def softmax_ce_grad(logits_2f: np.ndarray, labels: np.ndarray, ring: RingParams):
-    """DO-side loss in float64 on the reconstructed logits."""
-    half = np.uint64(1 << (ring.ell - 1))
-    v = np.asarray(logits_2f, dtype=np.uint64) & ring.mask
-    sv = v.astype(np.int64) - ((v >= half).astype(np.int64) << np.int64(ring.ell))
-    z = sv.astype(np.float64) / float(1 << (2 * ring.f))
-    z = z - z.max(axis=0, keepdims=True)
-    ez = np.exp(z)
-    sm = ez / ez.sum(axis=0, keepdims=True)
-    B = z.shape[1]
-    onehot = np.zeros_like(sm)
-    onehot[labels, np.arange(B)] = 1.0
-    loss = float(-np.mean(np.log(sm[labels, np.arange(B)])))
-    g = (sm - onehot) / B
-    return loss, np.floor(g * float(1 << ring.f)).astype(np.int64).astype(np.uint64) & ring.mask
+    """DO-side loss in float64 on the reconstructed logits (SoftmaxCE)."""
+    C, B = np.shape(logits_2f)
+    key = (C, B, ring.ell, ring.f)
+    sm = _SMCE.get(key)
+    if sm is None:
+        sm = _SMCE[key] = SoftmaxCE(ring, C, B)
+    loss, g = sm(labels, logits_2f)
+    return loss, g.copy()
 
 
 def _flatten(sh: ShareTensor) -> ShareTensor:  # (B, C, H, W) -> (C*H*W, B), local data movement
@@ -226,12 +262,19 @@ def _forward_layers(sess, model, prep, cur, acts, ds, ys, seg):
 
 
 def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e-2, momentum=0.8, trace=None,
-                   check=True, prep=None):
-    """Private backward pass from the DO's loss gradient share (MO share 0) + SGD at the MO."""
+                   check=True, prep=None, pre_layers=None):
+    """Private backward pass from the DO's loss gradient share (MO share 0) + SGD at the MO.
+    ``pre_layers``: prepare these layers' forward-only operands here, on the
+    prep stream beside the backward chain (the rest were prepared before)."""
     ring, f = model.ring, model.ring.f
     L = model.n_layers
     seg = model.segments()
     acts, ds, ys = state
+    if pre_layers:
+        cur, side = torch.cuda.current_stream(), sess.prep_stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            prepare_backward(sess, model, state, prep, layers=pre_layers, clear=False)
     gy_do = ShareTensor(DO, RingTensor(g_do, f, ring, _canonical=True))
     gy_mo = ShareTensor(MO, RingTensor(torch.zeros_like(g_do), f, ring, _canonical=True))
     gws, gbs = [None] * L, [None] * L
@@ -289,6 +332,8 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
                     t_mo, t_do = _unflatten(t_mo, chw), _unflatten(t_do, chw)
                 gy_mo, gy_do = truncate_relu_backward(sess, l - 1, ds[l - 1], t_mo, t_do, f)
     main.wait_stream(gstream)
+    if pre_layers:
+        main.wait_stream(sess.prep_stream())  # joins the prep fork (graph capture needs every fork joined)
     del keep
     if check:
         model.check_range()
@@ -296,21 +341,23 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
     return gws, gbs
 
 
-def prepare_backward(sess: Session, model: Model, state, prep=None):
+def prepare_backward(sess: Session, model: Model, state, prep=None, layers=None, clear=True, events=True):
     """Produce, ahead of the loss gradient, every backward-pass HE operand that
     depends only on the forward pass: the MO's encodings of W_l (input-gradient
     protocols) and of its activation shares, the DO's encryptions of its
     activation shares (weight-gradient cross terms).  Enqueued on the current
     stream; the backward protocols pick them up (Session.prepare_operand) and
     only the gradient-dependent operands remain on their critical path.  FC
-    and conv layers of mode "fullhe"; Pencil+ (prep) prepares nothing."""
-    sess.clear_prepared()
+    and conv layers of mode "fullhe"; Pencil+ (prep) prepares nothing.
+    ``layers``: only these layers (default all)."""
+    if clear:
+        sess.clear_prepared()
     if prep is not None:
         return
     acts = state[0]
     L = model.n_layers
     N = sess.p.N
-    for l in range(L):
+    for l in range(L) if layers is None else layers:
         e = model.layers[model.lin[l]]
         x_mo, x_do = acts[l]
         if x_mo.owner_role != MO:
@@ -321,12 +368,12 @@ def prepare_backward(sess: Session, model: Model, state, prep=None):
             pad, stride = e[4], e[5]
             if l > 0:  # conv_backward_input
                 plan = plan_conv_layer("bwdx", B, c_i, c_o, H, Wd, s, pad, stride, N)
-                sess.prepare_operand(l, OP_BWD_X, plan, "A_pt", model.W[l].values)
+                sess.prepare_operand(l, OP_BWD_X, plan, "A_pt", model.W[l].values, events)
             plan = plan_conv_layer("gradw", B, c_i, c_o, H, Wd, s, pad, stride, N)  # conv_grad_weight
             if l < L - 1:
-                sess.prepare_operand(l, OP_GRAD_W, plan, "A_ct", x_do.value.values)
+                sess.prepare_operand(l, OP_GRAD_W, plan, "A_ct", x_do.value.values, events)
             if l > 0:
-                sess.prepare_operand(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values)
+                sess.prepare_operand(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values, events)
             continue
         if e[0] != "fc":
             continue
@@ -334,12 +381,12 @@ def prepare_backward(sess: Session, model: Model, state, prep=None):
         B = x_do.shape[1]
         if l > 0:  # linear_backward_input: W^T through strides (1, n_i)
             plan = plan_matmul(MatmulGeometry(n_o, n_i, B), N, None, (1, n_i), None)
-            sess.prepare_operand(l, OP_BWD_X, plan, "A_pt", model.W[l].values)
+            sess.prepare_operand(l, OP_BWD_X, plan, "A_pt", model.W[l].values, events)
         plan = plan_matmul(MatmulGeometry(B, n_o, n_i), N, (1, B), None, None)  # grad_weight
         if l < L - 1:  # term A: Enc(X_1) (x) gY_0
-            sess.prepare_operand(l, OP_GRAD_W, plan, "A_ct", x_do.value.values)
+            sess.prepare_operand(l, OP_GRAD_W, plan, "A_ct", x_do.value.values, events)
         if l > 0:  # term B: Enc(gY_1) (x) X_0
-            sess.prepare_operand(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values)
+            sess.prepare_operand(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values, events)
 
 
 def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e-2, momentum=0.8,
@@ -377,6 +424,8 @@ class GraphStep:
         self.g_do = torch.zeros(n_cls, B, dtype=torch.int64, device=x.values.device)
         self.logits_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
         self.g_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
+        self._loss = SoftmaxCE(model.ring, n_cls, B, logits=self.logits_host.numpy().view(np.uint64),
+                               g_out=self.g_host.numpy().view(np.uint64))
         # warm-up (eager, graph-mode keys): builds plans/maps, sizes scratch buffers
         st, lg = forward_phase(sess, model, x, prep)
         prepare_backward(sess, model, st, prep)
@@ -387,10 +436,17 @@ class GraphStep:
         self.g_bwd = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.g_fwd):
             self.state, self.logits = forward_phase(sess, model, x, prep)
+        # the operands the backward consumes first (layers >= 1) are prepared beside
+        # the host's loss step; layer 0's (consumed last) inside the backward graph,
+        # beside its latency-bound first layers, so it does not wait for them
+        L = model.n_layers
+        late = [0] if L > 1 else []
         with torch.cuda.graph(self.g_pre, pool=self.g_fwd.pool()):
-            prepare_backward(sess, model, self.state, prep)
+            prepare_backward(sess, model, self.state, prep, layers=[l for l in range(L) if l not in late],
+                             events=False)  # ordered by step(): the backward replay waits for this graph
         with torch.cuda.graph(self.g_bwd, pool=self.g_fwd.pool()):
-            self.grads = backward_phase(sess, model, self.state, self.g_do, lr, momentum, check=False, prep=prep)
+            self.grads = backward_phase(sess, model, self.state, self.g_do, lr, momentum, check=False, prep=prep,
+                                        pre_layers=late)
         self._pre_stream = torch.cuda.Stream()
         torch.cuda.synchronize()
 
@@ -426,8 +482,7 @@ class GraphStep:
 
                 limit = float(1 << (self.model.ring.ell - 1)) / float(1 << self.model.ring.f)
                 raise EncodeRangeError(f"|x| must stay below {limit}")
-        loss, g = softmax_ce_grad(self.logits_host.numpy().view(np.uint64), np.asarray(labels), self.model.ring)
-        self.g_host.numpy().view(np.uint64)[...] = g
+        loss, _ = self._loss(labels)  # g written into g_host
         self.g_do.copy_(self.g_host, non_blocking=True)
         main.wait_stream(self._pre_stream)
         self.g_bwd.replay()
