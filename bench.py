@@ -52,7 +52,7 @@ ENTRY_KERNELS = {
     "pb_encrypt_sk": ("k_encrypt_sk",), "pb_encrypt_sk_zero": ("k_encrypt_sk",),
     "pb_encrypt_sk_add": ("k_encrypt_add",), "pb_encode_plain_mont": ("k_encode_plain_mont",),
     "pb_mask_ntt": ("k_mask_ntt",), "pb_ctpt_mac_tiled": ("k_mac_ws", "k_mac_pipe", "k_mac_eager"),
-    "pb_decrypt_to_share": ("k_decrypt_share_cluster",),
+    "pb_decrypt_to_share": ("k_decrypt_share_cluster", "k_decrypt_inv", "k_decode_gather"),
 }
 
 

@@ -155,8 +155,11 @@ class CallStats:
         self.events = []  # (name, start_event, end_event, tag)
         self.tag = None
 
-    def before(self, name):
-        self.launches += KERNELS_PER_CALL.get(name, 1)
+    def before(self, name, args=()):
+        k = KERNELS_PER_CALL.get(name, 1)
+        if name == "pb_decrypt_to_share" and len(args) > 6 and int(args[6]) >= 384:
+            k = 2  # INTT + separate decode kernel for slot-heavy ciphertexts (pb_bfv.cu)
+        self.launches += k
         self.calls[name] = self.calls.get(name, 0) + 1
         if name in self.timed:
             import torch
@@ -184,6 +187,6 @@ def call(name: str, *args) -> None:
     if st is None:
         check(getattr(load(), name)(*args), name)
         return
-    ev = st.before(name)
+    ev = st.before(name, args)
     check(getattr(load(), name)(*args), name)
     st.after(name, ev)

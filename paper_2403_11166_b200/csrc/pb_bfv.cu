@@ -11,6 +11,7 @@
 #include "pb_ntt.cuh"
 
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 namespace {
 
@@ -471,14 +472,30 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   for (int k = 0; k < PB_MAXL; ++k) rows[k] = k < L ? cluster.map_shared_rank(sm, k) : nullptr;
   const int32_t* pos = out_pos + p * U;
   const int64_t* dst = out_dst + p * U;
-  for (int u = l * Nt::T + tid; u < U; u += L * Nt::T) {
-    const int j = __ldg(pos + u);
-    if (j < 0) continue;
-    uint32_t x[PB_MAXL], d[PB_MAXL];
+  // CTA l decodes the contiguous block [u0, u1) of the useful slots (balanced
+  // across the cluster: a strided split left the remainder to one CTA, whose
+  // peers then idled at the closing barrier), two slots per thread per pass
+  // with both slots' loads in flight together
+  const int per = (U + L - 1) / L;
+  const int u0 = l * per, u1 = min(U, u0 + per);
+  for (int u = u0 + tid; u < u1; u += 2 * Nt::T) {
+    const int ub = u + Nt::T;
+    const int ja = __ldg(pos + u), jb = ub < u1 ? __ldg(pos + ub) : -1;
+    const int64_t da = __ldg(dst + u), db = ub < u1 ? __ldg(dst + ub) : 0;
+    uint32_t xa[PB_MAXL], xb[PB_MAXL], d[PB_MAXL];
 #pragma unroll
-    for (int k = 0; k < PB_MAXL; ++k) x[k] = k < L ? rows[k][Nt::pad(j)] : 0u;
-    garner_dev(P, x, 1, d);
-    share[__ldg(dst + u)] = scale_round_dev(P, d);
+    for (int k = 0; k < PB_MAXL; ++k) {
+      xa[k] = (k < L && ja >= 0) ? rows[k][Nt::pad(ja)] : 0u;
+      xb[k] = (k < L && jb >= 0) ? rows[k][Nt::pad(jb)] : 0u;
+    }
+    if (ja >= 0) {
+      garner_dev(P, xa, 1, d);
+      share[da] = scale_round_dev(P, d);
+    }
+    if (jb >= 0) {
+      garner_dev(P, xb, 1, d);
+      share[db] = scale_round_dev(P, d);
+    }
   }
   cluster.sync();  // peers may still be reading this CTA's shared memory
 }
@@ -826,7 +843,15 @@ extern "C" int pb_decrypt_to_share(const pb_ctx* ctx, const uint32_t* sk, const 
   if (nP <= 0 || U <= 0) return PB_OK;
   if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
   cudaStream_t st = pb_stream_of(stream);
-  if (ctx->dev.logN == 13 && ctx->dev.L >= 2) {  // fused cluster kernel (one launch, DSMEM limb exchange)
+  static const int cluster_on = [] {  // PB_DEC_CLUSTER=0: the two-kernel path (INTT to scratch, then decode)
+    const char* v = getenv("PB_DEC_CLUSTER");
+    return v ? atoi(v) : 1;
+  }();
+  // fused cluster kernel (one launch, DSMEM limb exchange) when the decode is
+  // light; with many useful slots per ciphertext the separate decode kernel's
+  // parallelism wins (B200, graph-timed: U = 256 x 32 cts 12.3 vs 13.9 us,
+  // U = 512 x 16 cts 12.2 vs 10.7 us, U = 2041 x 50 cts 27.5 vs 19.2 us)
+  if (cluster_on && U < 384 && ctx->dev.logN == 13 && ctx->dev.L >= 2) {
     const int rc = launch_decrypt_share_cluster<13>(ctx->dev, sk, ct, nP, out_pos, out_dst, U, share_out, st);
     if (rc != 0) return pb_set_error(PB_ERR_CUDA, cudaGetErrorString((cudaError_t)rc));
     PB_CHECK_LAUNCH();
