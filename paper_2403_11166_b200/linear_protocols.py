@@ -53,6 +53,7 @@ FRAME_HEADER = 12  # {u16 type, u16 flags, u64 len}
 import os as _os
 
 _SERIAL = _os.environ.get("PB_SERIAL", "0") == "1"
+_MASK_PREFETCH = _os.environ.get("PB_MASK_PREFETCH", "1") == "1"
 _PRIO = tuple(int(v) for v in _os.environ.get("PB_PRIO", "0,0").split(","))  # (encrypt, encode) stream priorities
 
 
@@ -198,6 +199,8 @@ class Session:
         # (layer, op, role) -> (device tensor, event or None); buffers persist
         self._prepared = {}
         self._prep_bufs = {}
+        self._masks = {}  # (layer, op, shape) -> (prefetched mask, event or None)
+        self._mask_bufs = {}
 
     def rng(self, layer: int, op: int, purpose: int) -> SeededRng:
         g = SeededRng(self.seed, stream_id(layer, op, purpose))
@@ -317,6 +320,45 @@ class Session:
 
     def clear_prepared(self):
         self._prepared.clear()
+        self._masks.clear()
+
+    # ------------------------------------------------------- mask prefetch ---
+    def prefetch_masks(self, specs, event: bool = True):
+        """Draw the MO masks s of protocols (layer, op) ahead of them -- they
+        depend only on the step seed -- on an auxiliary stream; ``specs`` =
+        [(layer, op, shape)].  The protocol's ``mask()`` call returns the
+        same values it would have drawn itself (stream (layer, op, P_MASK))."""
+        if not _MASK_PREFETCH:
+            return
+        # persistent buffers (never returned to the caching allocator): a prefetched
+        # mask is consumed on other streams (grad stream, side streams) than the
+        # one that allocated it, so a freed block could be reused under them
+        bufs = []
+        for layer, op, shape in specs:
+            key = (layer, op, tuple(shape))
+            buf = self._mask_bufs.get(key)
+            if buf is None:
+                buf = self._mask_bufs[key] = _dev.empty_u64(*shape)
+            bufs.append((layer, op, tuple(shape), buf))
+        with self.aux() as aux:
+            for layer, op, shape, buf in bufs:
+                aux.run(lambda: self.rng(layer, op, P_MASK).uniform_ring(shape, self.ring, out=buf))
+                ev = None
+                if event:
+                    ev = torch.cuda.Event()
+                    ev.record(aux.stream)
+                self._masks[(layer, op, shape)] = (buf, ev)
+
+    def mask(self, layer: int, op: int, shape) -> torch.Tensor:
+        """The MO's uniform mask of protocol (layer, op): prefetched or drawn now."""
+        shape = tuple(shape)
+        pre = self._masks.pop((layer, op, shape), None)
+        if pre is None:
+            return self.rng(layer, op, P_MASK).uniform_ring(shape, self.ring)
+        buf, ev = pre
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
+        return buf
 
     def _count(self, name, nbytes):
         if _lib.STATS is not None:
@@ -470,7 +512,7 @@ def linear_forward(sess: Session, layer: int, W: RingTensor, b: RingTensor, x_a:
     if x_do.shape[0] != n_i:
         raise ShapeError(f"X has {x_do.shape[0]} features, W expects {n_i}")
     B = x_do.shape[1]
-    s = sess.rng(layer, OP_FWD, P_MASK).uniform_ring((n_o, B), ring)
+    s = sess.mask(layer, OP_FWD, (n_o, B))
     if mo_x_zero:
         s_eff = s
     else:
@@ -492,7 +534,7 @@ def linear_backward_input(sess: Session, layer: int, W: RingTensor, gy_a: ShareT
     ring = sess.ring
     n_o, n_i = W.shape
     B = gy_do.shape[1]
-    s = sess.rng(layer, OP_BWD_X, P_MASK).uniform_ring((n_i, B), ring)
+    s = sess.mask(layer, OP_BWD_X, (n_i, B))
     if mo_gy_zero:
         s_eff = s
     else:
@@ -530,7 +572,7 @@ def grad_weight(sess: Session, layer: int, x_a: ShareTensor, x_b: ShareTensor, g
     n_i, B = x_do.shape
     n_o = gy_do.shape[0]
     g = MatmulGeometry(B, n_o, n_i)  # v = X^T (B x n_i) via strides (1, B); W = gY (n_o x B)
-    s = sess.rng(layer, OP_GRAD_W, P_MASK).uniform_ring((n_o, n_i), ring)
+    s = sess.mask(layer, OP_GRAD_W, (n_o, n_i))
     cross_do = _dev.empty_u64(n_o, n_i)
     loc_do = _dev.empty_u64(n_o, n_i)
     loc_mo = _dev.empty_u64(n_o, n_i) if not (mo_x_zero or mo_gy_zero) else s
@@ -597,7 +639,7 @@ def conv_forward(sess: Session, layer: int, W: RingTensor, b: RingTensor, x_a: S
     if ci2 != c_i:
         raise ShapeError(f"X has {c_i} channels, W expects {ci2}")
     oh, ow = conv_out_hw(H, Wd, s, pad, stride)
-    msk = sess.rng(layer, OP_FWD, P_MASK).uniform_ring((B, c_o, oh, ow), ring)
+    msk = sess.mask(layer, OP_FWD, (B, c_o, oh, ow))
     if mo_x_zero:
         s_eff = msk
     else:
@@ -621,7 +663,7 @@ def conv_backward_input(sess: Session, layer: int, W: RingTensor, gy_a: ShareTen
     ring = sess.ring
     B, c_o = gy_do.shape[:2]
     c_i, s = W.shape[1], W.shape[2]
-    msk = sess.rng(layer, OP_BWD_X, P_MASK).uniform_ring((B, c_i, H, Wd), ring)
+    msk = sess.mask(layer, OP_BWD_X, (B, c_i, H, Wd))
     plan = plan_conv_layer("bwdx", B, c_i, c_o, H, Wd, s, pad, stride, sess.p.N)
     cov = _covered(plan, B * c_i * H * Wd)
     if cov is not None:  # input positions no output reads: gradient exactly 0, MO share 0 too
@@ -648,7 +690,7 @@ def conv_grad_weight(sess: Session, layer: int, x_a: ShareTensor, x_b: ShareTens
     ring = sess.ring
     B, c_i, H, Wd = x_do.shape
     c_o = gy_do.shape[1]
-    msk = sess.rng(layer, OP_GRAD_W, P_MASK).uniform_ring((c_o, c_i, s, s), ring)
+    msk = sess.mask(layer, OP_GRAD_W, (c_o, c_i, s, s))
     plan = plan_conv_layer("gradw", B, c_i, c_o, H, Wd, s, pad, stride, sess.p.N)
     cross_do = _dev.empty_u64(c_o, c_i, s, s)
     shp = (c_o, c_i, s, s)

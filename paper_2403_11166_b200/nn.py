@@ -22,8 +22,8 @@ import torch
 
 from . import _dev, _lib
 from .errors import EncodeRangeError, ShapeError
-from .linear_protocols import (OP_BWD_X, OP_GRAD_W, Session, conv_backward_input, conv_forward, conv_grad_weight,
-                               grad_weight, linear_backward_input, linear_forward, reveal_grad_bias,
+from .linear_protocols import (OP_BWD_X, OP_FWD, OP_GRAD_W, Session, conv_backward_input, conv_forward,
+                               conv_grad_weight, grad_weight, linear_backward_input, linear_forward, reveal_grad_bias,
                                reveal_grad_bias_conv)
 from . import preprocessing as PP
 from .nonlinear import (avgpool_backward, avgpool_forward, relu_backward, relu_forward, relu_truncate, truncate,
@@ -232,6 +232,9 @@ def forward_phase(sess: Session, model: Model, x: RingTensor, prep=None):
     seg = model.segments()
     cur = (ShareTensor(MO, RingTensor(torch.zeros_like(x.values), f, ring, _canonical=True)), ShareTensor(DO, x))
     acts, ds, ys = [], [], []
+    if prep is None:  # every layer's MO mask depends only on the seed: draw them all up front
+        B = x.shape[1] if len(model.in_shape) == 1 else x.shape[0]
+        sess.prefetch_masks(_mask_specs(model, B, (OP_FWD,)))
     _forward_layers(sess, model, prep, cur, acts, ds, ys, seg)
     # the MO sends its share of the logits; the DO reconstructs them
     y_mo, y_do = ys[-1]
@@ -341,6 +344,23 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
     return gws, gbs
 
 
+def _mask_specs(model: Model, B: int, ops, layers=None):
+    """(layer, op, shape) of the MO masks the protocols of ``ops`` draw (fullhe mode)."""
+    out = []
+    for l in range(model.n_layers) if layers is None else layers:
+        k = model.lin[l]
+        e = model.layers[k]
+        (shp_in, shp_out), conv = model.io[k], e[0] == "conv"
+        for op in ops:
+            if op == OP_FWD:
+                out.append((l, op, (B, *shp_out) if conv else (shp_out[0], B)))
+            elif op == OP_BWD_X and l > 0:
+                out.append((l, op, (B, *shp_in) if conv else (shp_in[0], B)))
+            elif op == OP_GRAD_W:
+                out.append((l, op, tuple(model.W[l].shape)))
+    return out
+
+
 def prepare_backward(sess: Session, model: Model, state, prep=None, layers=None, clear=True, events=True):
     """Produce, ahead of the loss gradient, every backward-pass HE operand that
     depends only on the forward pass: the MO's encodings of W_l (input-gradient
@@ -357,6 +377,9 @@ def prepare_backward(sess: Session, model: Model, state, prep=None, layers=None,
     acts = state[0]
     L = model.n_layers
     N = sess.p.N
+    x0 = acts[0][1].value if acts[0][1].owner_role == DO else acts[0][0].value
+    B = x0.shape[1] if len(model.in_shape) == 1 else x0.shape[0]
+    sess.prefetch_masks(_mask_specs(model, B, (OP_BWD_X, OP_GRAD_W), layers), events)
     for l in range(L) if layers is None else layers:
         e = model.layers[model.lin[l]]
         x_mo, x_do = acts[l]

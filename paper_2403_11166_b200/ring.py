@@ -139,10 +139,10 @@ class SeededRng:  # R:48-90
         self._host_pos = self._pos
 
     # -- draws ----------------------------------------------------------------
-    def uniform_ring(self, shape, params: RingParams) -> torch.Tensor:  # R:60-61, on device
+    def uniform_ring(self, shape, params: RingParams, out: torch.Tensor | None = None) -> torch.Tensor:  # R:60-61
         shape = tuple(shape) if isinstance(shape, (tuple, list)) else (int(shape),)
         n = int(np.prod(shape)) if shape else 1
-        out = _dev.empty_u64(n)
+        out = _dev.empty_u64(n) if out is None else out.view(-1)
         off = self.reserve(n)
         sd, sp = self.np_args()
         _lib.call("pb_uniform_ring", _dev.ptr(out), n, sd, sp, self.stream, off, params.ell, _dev.stream())
