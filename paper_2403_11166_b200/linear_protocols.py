@@ -201,6 +201,8 @@ class Session:
         self._prep_bufs = {}
         self._masks = {}  # (layer, op, shape) -> (prefetched mask, event or None)
         self._mask_bufs = {}
+        self._mask_streams = {}
+        self._pending_join = []
 
     def rng(self, layer: int, op: int, purpose: int) -> SeededRng:
         g = SeededRng(self.seed, stream_id(layer, op, purpose))
@@ -319,6 +321,7 @@ class Session:
         self._prepared[key] = (buf, ev)
 
     def clear_prepared(self):
+        """Drop unconsumed prepared operands and masks."""
         self._prepared.clear()
         self._masks.clear()
 
@@ -340,14 +343,35 @@ class Session:
             if buf is None:
                 buf = self._mask_bufs[key] = _dev.empty_u64(*shape)
             bufs.append((layer, op, tuple(shape), buf))
-        with self.aux() as aux:
+        cur = torch.cuda.current_stream()
+        if _SERIAL:
+            side = cur
+        else:
+            side = self._mask_streams.get(cur.cuda_stream)
+            if side is None:
+                side = self._mask_streams[cur.cuda_stream] = torch.cuda.Stream()
+            side.wait_stream(cur)
+        with torch.cuda.stream(side):
             for layer, op, shape, buf in bufs:
-                aux.run(lambda: self.rng(layer, op, P_MASK).uniform_ring(shape, self.ring, out=buf))
+                self.rng(layer, op, P_MASK).uniform_ring(shape, self.ring, out=buf)
                 ev = None
                 if event:
                     ev = torch.cuda.Event()
-                    ev.record(aux.stream)
+                    ev.record(side)
                 self._masks[(layer, op, shape)] = (buf, ev)
+        if side is not cur:
+            if event:  # consumers wait on the events; the fork is joined at the phase end (join_side)
+                self._pending_join.append(side)
+            else:
+                cur.wait_stream(side)
+
+    def join_side(self):
+        """Join the mask-prefetch forks into the current stream (a CUDA-graph
+        capture needs every fork joined before it ends)."""
+        cur = torch.cuda.current_stream()
+        for st in self._pending_join:
+            cur.wait_stream(st)
+        self._pending_join.clear()
 
     def mask(self, layer: int, op: int, shape) -> torch.Tensor:
         """The MO's uniform mask of protocol (layer, op): prefetched or drawn now."""

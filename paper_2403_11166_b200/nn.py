@@ -236,6 +236,7 @@ def forward_phase(sess: Session, model: Model, x: RingTensor, prep=None):
         B = x.shape[1] if len(model.in_shape) == 1 else x.shape[0]
         sess.prefetch_masks(_mask_specs(model, B, (OP_FWD,)))
     _forward_layers(sess, model, prep, cur, acts, ds, ys, seg)
+    sess.join_side()
     # the MO sends its share of the logits; the DO reconstructs them
     y_mo, y_do = ys[-1]
     logits = y_mo.value + y_do.value
@@ -337,11 +338,13 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
     main.wait_stream(gstream)
     if pre_layers:
         main.wait_stream(sess.prep_stream())  # joins the prep fork (graph capture needs every fork joined)
+    sess.join_side()
     del keep
     if check:
         model.check_range()
     sess.clear_prepared()
     return gws, gbs
+
 
 
 def _mask_specs(model: Model, B: int, ops, layers=None):
@@ -472,6 +475,7 @@ class GraphStep:
                                         pre_layers=late)
         self._pre_stream = torch.cuda.Stream()
         torch.cuda.synchronize()
+        sess.clear_prepared()
 
     def load_batch(self, x_host: torch.Tensor):
         """Stage a new real-valued batch (host float64, pinned for an async
