@@ -445,6 +445,7 @@ class GraphStep:
         self.x = x  # device input buffer; callers copy new batches into x.values (or use load_batch)
         self._stage = None
         self._flag_pending = False
+        self._batch_pending = False
         n_cls = model.n_classes
         B = x.shape[1] if len(model.in_shape) == 1 else x.shape[0]
         self.g_do = torch.zeros(n_cls, B, dtype=torch.int64, device=x.values.device)
@@ -479,23 +480,42 @@ class GraphStep:
 
     def load_batch(self, x_host: torch.Tensor):
         """Stage a new real-valued batch (host float64, pinned for an async
-        copy; the DO's input, same shape as x) into the graphs' input buffer:
-        H2D copy + fixed-point encode on the device, no host sync -- the
-        encode's range flag is checked at the next step's logits sync."""
+        copy; the DO's input, same shape as x) for the next step: the H2D copy
+        runs on a copy stream, overlapping the previous step's backward still
+        on the GPU; the next step() encodes it into the graphs' input buffer on
+        the device.  No host sync -- the encode's range flag is checked at
+        that step's logits sync."""
+        if self._stage is None:
+            dev = self.x.values.device
+            self._stage = torch.empty(tuple(self.x.values.shape), dtype=torch.float64, device=dev)
+            self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
+            self._flag_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+            self._copy_stream = torch.cuda.Stream()
+            self._ev_loaded, self._ev_free = torch.cuda.Event(), None
+        if self._ev_free is not None:  # the previous batch's encode has read the stage
+            self._copy_stream.wait_event(self._ev_free)
+        with torch.cuda.stream(self._copy_stream):
+            self._stage.copy_(x_host, non_blocking=True)
+            self._ev_loaded.record()
+        self._batch_pending = True
+
+    def _encode_batch(self, main):
         from .ring import encode_fixed_into
 
-        if self._stage is None:
-            self._stage = torch.empty(tuple(self.x.values.shape), dtype=torch.float64, device=self.x.values.device)
-            self._flag = torch.zeros(1, dtype=torch.int32, device=self.x.values.device)
-            self._flag_host = torch.zeros(1, dtype=torch.int32).pin_memory()
-        self._stage.copy_(x_host, non_blocking=True)
+        main.wait_event(self._ev_loaded)
         encode_fixed_into(self._stage, self.model.ring, self.x.values, self._flag)
+        if self._ev_free is None:
+            self._ev_free = torch.cuda.Event()
+        self._ev_free.record(main)
         self._flag_host.copy_(self._flag, non_blocking=True)
+        self._batch_pending = False
         self._flag_pending = True
 
     def step(self, seed: int, labels):
         self.sess.reseed(seed)
         main = torch.cuda.current_stream()
+        if self._batch_pending:
+            self._encode_batch(main)
         self.g_fwd.replay()
         self._pre_stream.wait_stream(main)
         with torch.cuda.stream(self._pre_stream):  # backward operands, beside the host's loss
