@@ -21,7 +21,8 @@ def main():
     res = {"variant": int(os.environ.get("PB_MAC_VARIANT", "0"))}
     # (name, nB, nO, nI, two_terms)
     for name, nB, nO, nI, two in (("fwd0", 4, 8, 25, False), ("gw0", 5, 10, 16, False), ("fwd1", 2, 8, 8, False),
-                                  ("gw1", 4, 8, 8, True), ("conv", 64, 13, 16, False), ("cifar", 16, 16, 9, True)):
+                                  ("gw1", 4, 8, 8, True), ("conv", 64, 13, 16, False), ("cifar", 16, 16, 9, True),
+                                  ("cifar_gw2", 13, 32, 32, True)):
         q = p.moduli[-1]
         ctA = torch.randint(0, q, (nB * nI, 2, L, N), dtype=torch.int32, device="cuda", generator=g)
         ptA = torch.randint(0, q, (nO * nI, L, N), dtype=torch.int32, device="cuda", generator=g)
