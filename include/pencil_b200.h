@@ -345,6 +345,12 @@ int pb_host_softmax_pre(const uint64_t* logits, int32_t C, int32_t B, int32_t el
 int pb_host_softmax_post(double* ez, int32_t C, int32_t B, const int64_t* labels, int32_t ell, int32_t f,
                          double* p_lab, uint64_t* g_out);
 
+/* Cap the grid of the one-CTA-per-row kernels (encrypt, plaintext encoding)
+ * launched afterwards from this host thread at max_ctas (0: no cap); the
+ * kernels then loop over rows.  For background work (operands prepared off
+ * the critical path) that must leave SM slots to concurrent kernels. */
+int pb_set_launch_cap(int32_t max_ctas);
+
 #ifdef __cplusplus
 }
 #endif

@@ -219,8 +219,10 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
   extern __shared__ uint32_t sm[];
   const int tid = threadIdx.x;
   const int L = P.L;
-  const int l = (int)(blockIdx.x / nP);  // limb-major: co-resident CTAs share one limb's twiddles
-  const int64_t p = blockIdx.x % nP;
+  for (int64_t row = blockIdx.x; row < nP * L; row += gridDim.x) {  // one row per CTA unless capped
+  if (row != blockIdx.x) __syncthreads();  // shared memory of the previous row is free
+  const int l = (int)(row / nP);  // limb-major: co-resident CTAs share one limb's twiddles
+  const int64_t p = row % nP;
   const uint32_t q = P.q[l];
   const uint64_t mu = P.mu[l];
   const int8_t* ep = e ? e + p * N : nullptr;
@@ -265,6 +267,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
     for (int k = 0; k < 4; ++k) o[k] = submod(pb::canon4(b[4 * v + k], q), mulmod(a[k], sk_[k], q, mu), q);
     c0[v * Nt::T] = make_uint4(o[0], o[1], o[2], o[3]);
     c1[v * Nt::T] = make_uint4(a[0], a[1], a[2], a[3]);
+  }
   }
 }
 
@@ -616,7 +619,8 @@ void launch_encrypt_sk(const PbDev& P, const uint32_t* sk, PbPack src, int64_t n
   using Nt = pb::Ntt<LOGN>;
   const size_t smem = Nt::SMEM_WORDS * 4;
   set_smem(k_encrypt_sk<LOGN>, smem);
-  k_encrypt_sk<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, sk, src, nP, a_in, e, seed, seed_dev, nonce, ct);
+  k_encrypt_sk<LOGN><<<(unsigned)pb_row_grid(nP * P.L), Nt::T, smem, st>>>(P, sk, src, nP, a_in, e, seed, seed_dev,
+                                                                           nonce, ct);
 }
 
 template <int LOGN>

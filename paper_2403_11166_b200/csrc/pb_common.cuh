@@ -259,6 +259,11 @@ int pb_set_error(int code, const char* msg);
 
 static inline cudaStream_t pb_stream_of(void* s) { return (cudaStream_t)s; }
 
+// Grid of a one-CTA-per-row kernel: all rows, or at most the cap set by
+// pb_set_launch_cap (background work that must leave SMs to the critical
+// path; the kernels loop over rows with a grid stride).
+int64_t pb_row_grid(int64_t rows);
+
 static inline int pb_grid_1d(int64_t n, int threads, int64_t cap = 148 * 32) {
   int64_t g = (n + threads - 1) / threads;
   if (g > cap) g = cap;

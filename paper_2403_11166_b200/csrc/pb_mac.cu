@@ -38,19 +38,22 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   extern __shared__ uint32_t sm[];
   const int tid = threadIdx.x;
   const int L = P.L;
-  const int l = (int)(blockIdx.x / nP);  // limb-major: co-resident CTAs share one limb's twiddles
-  const int64_t p = blockIdx.x % nP;
-  const uint32_t q = P.q[l];
-  const uint64_t mu = P.mu[l];
-  const uint32_t tm = P.tmod[l];
   const int ell = P.ell;
-  uint32_t a[32];
-  pbk::load_source<Nt>(a, sm, src, p, tid, [&](uint64_t v) { return lift_centered(v, ell, q, mu, tm); });
-  Nt::forward(a, sm, P.tw_fwd + (size_t)l * Nt::N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
-  const uint32_t r2 = P.r2[l], r2s = P.r2_sh[l];
+  for (int64_t row = blockIdx.x; row < nP * L; row += gridDim.x) {  // one row per CTA unless capped
+    if (row != blockIdx.x) __syncthreads();  // shared memory of the previous row is free
+    const int l = (int)(row / nP);  // limb-major: co-resident CTAs share one limb's twiddles
+    const int64_t p = row % nP;
+    const uint32_t q = P.q[l];
+    const uint64_t mu = P.mu[l];
+    const uint32_t tm = P.tmod[l];
+    uint32_t a[32];
+    pbk::load_source<Nt>(a, sm, src, p, tid, [&](uint64_t v) { return lift_centered(v, ell, q, mu, tm); });
+    Nt::forward(a, sm, P.tw_fwd + (size_t)l * Nt::N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
+    const uint32_t r2 = P.r2[l], r2s = P.r2_sh[l];
 #pragma unroll
-  for (int c = 0; c < 32; ++c) a[c] = mul_shoup(pb::canon4(a[c], q), r2, r2s, q);
-  Nt::gst3(pt + (p * L + l) * Nt::N, a, tid);
+    for (int c = 0; c < 32; ++c) a[c] = mul_shoup(pb::canon4(a[c], q), r2, r2s, q);
+    Nt::gst3(pt + (p * L + l) * Nt::N, a, tid);
+  }
 }
 
 // ----------------------------------------------------------- mask NTT ----
@@ -611,7 +614,7 @@ void launch_encode_mont(const PbDev& P, pbk::Pack src, int64_t nP, uint32_t* pt,
   using Nt = pb::Ntt<LOGN>;
   const size_t smem = Nt::SMEM_WORDS * 4;
   set_smem(k_encode_plain_mont<LOGN>, smem);
-  k_encode_plain_mont<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, src, nP, pt);
+  k_encode_plain_mont<LOGN><<<(unsigned)pb_row_grid(nP * P.L), Nt::T, smem, st>>>(P, src, nP, pt);
 }
 
 template <int LOGN>

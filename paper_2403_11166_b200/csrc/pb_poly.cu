@@ -511,3 +511,14 @@ extern "C" int pb_negacyclic_mul_wrap(const uint64_t* a, const uint64_t* b, int6
   PB_CHECK_LAUNCH();
   return PB_OK;
 }
+
+// ------------------------------------------------------------- launch cap ---
+static thread_local int32_t g_launch_cap = 0;
+
+int64_t pb_row_grid(int64_t rows) { return g_launch_cap > 0 && rows > g_launch_cap ? g_launch_cap : rows; }
+
+extern "C" int pb_set_launch_cap(int32_t max_ctas) {
+  if (max_ctas < 0) return pb_set_error(PB_ERR_ARG, "launch cap must be >= 0");
+  g_launch_cap = max_ctas;
+  return PB_OK;
+}

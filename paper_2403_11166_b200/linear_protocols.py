@@ -54,6 +54,7 @@ import os as _os
 
 _SERIAL = _os.environ.get("PB_SERIAL", "0") == "1"
 _MASK_PREFETCH = _os.environ.get("PB_MASK_PREFETCH", "1") == "1"
+_BG_CAP = int(_os.environ.get("PB_BG_CAP", "148"))  # CTA cap of background operand preparation (0: none)
 _PRIO = tuple(int(v) for v in _os.environ.get("PB_PRIO", "0,0").split(","))  # (encrypt, encode) stream priorities
 
 
@@ -297,14 +298,17 @@ class Session:
             _lib.call("pb_encode_plain_mont", h, _dev.ptr(src), *_pk(pack), n, _dev.ptr(buf), _dev.stream())
             self._count("pb_encode_plain_mont", n * (L * N * 4 + 8 * N))
 
-    def prepare_operand(self, layer: int, op: int, plan, role: str, src: torch.Tensor, event: bool = True):
+    def prepare_operand(self, layer: int, op: int, plan, role: str, src: torch.Tensor, event: bool = True,
+                        background: bool = False):
         """Encrypt / encode one operand of the protocol (layer, op) ahead of time,
         on the current stream, into a persistent buffer; the next he_eval of
         (layer, op) uses it instead of producing it on its critical path.  The
         value is the one he_eval would compute (same packing, key and nonce),
         so the protocol's output is unchanged.  ``event``: the consumer waits
         on an event recorded here (False when another mechanism orders them,
-        e.g. a separately captured graph replayed before the consumer's)."""
+        e.g. a separately captured graph replayed before the consumer's).
+        ``background``: launch with at most PB_BG_CAP CTAs (pb_set_launch_cap),
+        leaving SM slots to the concurrently running critical path."""
         pack, n, is_ct, _ = self._operand_layout(plan, role)
         if not self._shard(plan).n_out or n == 0:
             return
@@ -313,7 +317,14 @@ class Session:
         buf = self._prep_bufs.get(key)
         if buf is None or tuple(buf.shape) != shape:
             buf = self._prep_bufs[key] = torch.empty(shape, dtype=torch.int32, device=_dev.device())
-        self._make_operand(layer, op, plan, role, src, buf)
+        if background and _BG_CAP > 0:
+            _lib.call("pb_set_launch_cap", _BG_CAP)
+            try:
+                self._make_operand(layer, op, plan, role, src, buf)
+            finally:
+                _lib.call("pb_set_launch_cap", 0)
+        else:
+            self._make_operand(layer, op, plan, role, src, buf)
         ev = None
         if event:
             ev = torch.cuda.Event()

@@ -278,7 +278,7 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
         cur, side = torch.cuda.current_stream(), sess.prep_stream()
         side.wait_stream(cur)
         with torch.cuda.stream(side):
-            prepare_backward(sess, model, state, prep, layers=pre_layers, clear=False)
+            prepare_backward(sess, model, state, prep, layers=pre_layers, clear=False, background=True)
     gy_do = ShareTensor(DO, RingTensor(g_do, f, ring, _canonical=True))
     gy_mo = ShareTensor(MO, RingTensor(torch.zeros_like(g_do), f, ring, _canonical=True))
     gws, gbs = [None] * L, [None] * L
@@ -364,7 +364,8 @@ def _mask_specs(model: Model, B: int, ops, layers=None):
     return out
 
 
-def prepare_backward(sess: Session, model: Model, state, prep=None, layers=None, clear=True, events=True):
+def prepare_backward(sess: Session, model: Model, state, prep=None, layers=None, clear=True, events=True,
+                     background=False):
     """Produce, ahead of the loss gradient, every backward-pass HE operand that
     depends only on the forward pass: the MO's encodings of W_l (input-gradient
     protocols) and of its activation shares, the DO's encryptions of its
@@ -394,12 +395,12 @@ def prepare_backward(sess: Session, model: Model, state, prep=None, layers=None,
             pad, stride = e[4], e[5]
             if l > 0:  # conv_backward_input
                 plan = plan_conv_layer("bwdx", B, c_i, c_o, H, Wd, s, pad, stride, N)
-                sess.prepare_operand(l, OP_BWD_X, plan, "A_pt", model.W[l].values, events)
+                sess.prepare_operand(l, OP_BWD_X, plan, "A_pt", model.W[l].values, events, background)
             plan = plan_conv_layer("gradw", B, c_i, c_o, H, Wd, s, pad, stride, N)  # conv_grad_weight
             if l < L - 1:
-                sess.prepare_operand(l, OP_GRAD_W, plan, "A_ct", x_do.value.values, events)
+                sess.prepare_operand(l, OP_GRAD_W, plan, "A_ct", x_do.value.values, events, background)
             if l > 0:
-                sess.prepare_operand(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values, events)
+                sess.prepare_operand(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values, events, background)
             continue
         if e[0] != "fc":
             continue
@@ -407,12 +408,12 @@ def prepare_backward(sess: Session, model: Model, state, prep=None, layers=None,
         B = x_do.shape[1]
         if l > 0:  # linear_backward_input: W^T through strides (1, n_i)
             plan = plan_matmul(MatmulGeometry(n_o, n_i, B), N, None, (1, n_i), None)
-            sess.prepare_operand(l, OP_BWD_X, plan, "A_pt", model.W[l].values, events)
+            sess.prepare_operand(l, OP_BWD_X, plan, "A_pt", model.W[l].values, events, background)
         plan = plan_matmul(MatmulGeometry(B, n_o, n_i), N, (1, B), None, None)  # grad_weight
         if l < L - 1:  # term A: Enc(X_1) (x) gY_0
-            sess.prepare_operand(l, OP_GRAD_W, plan, "A_ct", x_do.value.values, events)
+            sess.prepare_operand(l, OP_GRAD_W, plan, "A_ct", x_do.value.values, events, background)
         if l > 0:  # term B: Enc(gY_1) (x) X_0
-            sess.prepare_operand(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values, events)
+            sess.prepare_operand(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values, events, background)
 
 
 def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e-2, momentum=0.8,
