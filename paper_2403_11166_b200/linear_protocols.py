@@ -204,6 +204,7 @@ class Session:
         self._mask_bufs = {}
         self._mask_streams = {}
         self._pending_join = []
+        self._fork_pools = {}
 
     def rng(self, layer: int, op: int, purpose: int) -> SeededRng:
         g = SeededRng(self.seed, stream_id(layer, op, purpose))
@@ -370,11 +371,22 @@ class Session:
                     ev = torch.cuda.Event()
                     ev.record(side)
                 self._masks[(layer, op, shape)] = (buf, ev)
-        if side is not cur:
-            if event:  # consumers wait on the events; the fork is joined at the phase end (join_side)
-                self._pending_join.append(side)
-            else:
-                cur.wait_stream(side)
+        if side is not cur:  # joined at the phase end (join_side); consumers wait on the events
+            self._pending_join.append(side)
+
+    def fork_pool(self, n: int = 3):
+        """n streams forked from the current one (registered for join_side), for
+        independent background work enqueued round-robin."""
+        cur = torch.cuda.current_stream()
+        if _SERIAL:
+            return [cur]
+        pool = self._fork_pools.get(cur.cuda_stream)
+        if pool is None:
+            pool = self._fork_pools[cur.cuda_stream] = [torch.cuda.Stream() for _ in range(n)]
+        for st in pool:
+            st.wait_stream(cur)
+            self._pending_join.append(st)
+        return pool
 
     def join_side(self):
         """Join the mask-prefetch forks into the current stream (a CUDA-graph

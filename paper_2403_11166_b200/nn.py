@@ -384,6 +384,13 @@ def prepare_backward(sess: Session, model: Model, state, prep=None, layers=None,
     x0 = acts[0][1].value if acts[0][1].owner_role == DO else acts[0][0].value
     B = x0.shape[1] if len(model.in_shape) == 1 else x0.shape[0]
     sess.prefetch_masks(_mask_specs(model, B, (OP_BWD_X, OP_GRAD_W), layers), events)
+    pool, jobs = sess.fork_pool(), []
+
+    def prepare(*args):  # independent preparations run concurrently, round-robin over the pool
+        with torch.cuda.stream(pool[len(jobs) % len(pool)]):
+            sess.prepare_operand(*args, events, background)
+        jobs.append(args)
+
     for l in range(L) if layers is None else layers:
         e = model.layers[model.lin[l]]
         x_mo, x_do = acts[l]
@@ -395,12 +402,12 @@ def prepare_backward(sess: Session, model: Model, state, prep=None, layers=None,
             pad, stride = e[4], e[5]
             if l > 0:  # conv_backward_input
                 plan = plan_conv_layer("bwdx", B, c_i, c_o, H, Wd, s, pad, stride, N)
-                sess.prepare_operand(l, OP_BWD_X, plan, "A_pt", model.W[l].values, events, background)
+                prepare(l, OP_BWD_X, plan, "A_pt", model.W[l].values)
             plan = plan_conv_layer("gradw", B, c_i, c_o, H, Wd, s, pad, stride, N)  # conv_grad_weight
             if l < L - 1:
-                sess.prepare_operand(l, OP_GRAD_W, plan, "A_ct", x_do.value.values, events, background)
+                prepare(l, OP_GRAD_W, plan, "A_ct", x_do.value.values)
             if l > 0:
-                sess.prepare_operand(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values, events, background)
+                prepare(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values)
             continue
         if e[0] != "fc":
             continue
@@ -408,12 +415,14 @@ def prepare_backward(sess: Session, model: Model, state, prep=None, layers=None,
         B = x_do.shape[1]
         if l > 0:  # linear_backward_input: W^T through strides (1, n_i)
             plan = plan_matmul(MatmulGeometry(n_o, n_i, B), N, None, (1, n_i), None)
-            sess.prepare_operand(l, OP_BWD_X, plan, "A_pt", model.W[l].values, events, background)
+            prepare(l, OP_BWD_X, plan, "A_pt", model.W[l].values)
         plan = plan_matmul(MatmulGeometry(B, n_o, n_i), N, (1, B), None, None)  # grad_weight
         if l < L - 1:  # term A: Enc(X_1) (x) gY_0
-            sess.prepare_operand(l, OP_GRAD_W, plan, "A_ct", x_do.value.values, events, background)
+            prepare(l, OP_GRAD_W, plan, "A_ct", x_do.value.values)
         if l > 0:  # term B: Enc(gY_1) (x) X_0
-            sess.prepare_operand(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values, events, background)
+            prepare(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values)
+    if not events:  # ordered by a stream join instead of events: join every fork now
+        sess.join_side()
 
 
 def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e-2, momentum=0.8,
