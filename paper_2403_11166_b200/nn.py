@@ -441,6 +441,9 @@ def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e
     return loss, gws, gbs
 
 
+_LATE_PREP = __import__("os").environ.get("PB_LATE_PREP", "1") == "1"
+
+
 class GraphStep:
     """A private training step replayed from two CUDA graphs (forward up to
     the logits, backward + SGD from the DO's loss gradient), with the DO's
@@ -477,7 +480,7 @@ class GraphStep:
         # the host's loss step; layer 0's (consumed last) inside the backward graph,
         # beside its latency-bound first layers, so it does not wait for them
         L = model.n_layers
-        late = [0] if L > 1 else []
+        late = [0] if L > 1 and _LATE_PREP else []
         with torch.cuda.graph(self.g_pre, pool=self.g_fwd.pool()):
             prepare_backward(sess, model, self.state, prep, layers=[l for l in range(L) if l not in late],
                              events=False)  # ordered by step(): the backward replay waits for this graph
