@@ -285,12 +285,14 @@ class Session:
             return sh.in_pack, sh.n_in, False, 0
         raise ValueError(f"unknown operand role {role!r}")
 
-    def _make_operand(self, layer, op, plan, role, src, buf):
-        """Enqueue the DO's encryption / the MO's encoding of one operand into buf (current stream)."""
+    def _make_operand(self, layer, op, plan, role, src, buf, rng=None):
+        """Enqueue the DO's encryption / the MO's encoding of one operand into buf
+        (current stream); ``rng``: the encryption's key stream instead of the
+        step's (layer, op, P_ENC) stream."""
         pack, n, is_ct, off = self._operand_layout(plan, role)
         h, L, N = self.ctx.handle, self.p.L, self.p.N
         if is_ct:
-            enc_rng = self.rng(layer, op, P_ENC)
+            enc_rng = self.rng(layer, op, P_ENC) if rng is None else rng
             base = enc_rng.reserve((plan.n_in + plan.n_pt) * self.world)
             _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(src), *_pk(pack), n,
                       *enc_rng.dev_args(), base + off, _dev.ptr(buf), _dev.stream())
@@ -300,7 +302,7 @@ class Session:
             self._count("pb_encode_plain_mont", n * (L * N * 4 + 8 * N))
 
     def prepare_operand(self, layer: int, op: int, plan, role: str, src: torch.Tensor, event: bool = True,
-                        background: bool = False):
+                        background: bool = False, rng=None):
         """Encrypt / encode one operand of the protocol (layer, op) ahead of time,
         on the current stream, into a persistent buffer; the next he_eval of
         (layer, op) uses it instead of producing it on its critical path.  The
@@ -321,11 +323,11 @@ class Session:
         if background and _BG_CAP > 0:
             _lib.call("pb_set_launch_cap", _BG_CAP)
             try:
-                self._make_operand(layer, op, plan, role, src, buf)
+                self._make_operand(layer, op, plan, role, src, buf, rng)
             finally:
                 _lib.call("pb_set_launch_cap", 0)
         else:
-            self._make_operand(layer, op, plan, role, src, buf)
+            self._make_operand(layer, op, plan, role, src, buf, rng)
         ev = None
         if event:
             ev = torch.cuda.Event()

@@ -442,17 +442,29 @@ def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e
 
 
 _LATE_PREP = __import__("os").environ.get("PB_LATE_PREP", "1") == "1"
+_PREFETCH_BG = __import__("os").environ.get("PB_PREFETCH_BG", "1") == "1"
 
 
 class GraphStep:
-    """A private training step replayed from two CUDA graphs (forward up to
-    the logits, backward + SGD from the DO's loss gradient), with the DO's
-    float64 softmax-CE on the host in between.  All randomness is re-keyed
-    per step through the device seed word (Session.enable_graph_mode), and
-    every kernel of the step is the same sm_100a kernel the eager path runs:
-    the graphs only remove per-launch host overhead."""
+    """A private training step replayed from CUDA graphs (forward up to the
+    logits; the backward operands prepared beside the host's loss; backward +
+    SGD from the DO's loss gradient), with the DO's float64 softmax-CE on the
+    host in between.  All randomness is re-keyed per step through the device
+    seed word (Session.enable_graph_mode), and every kernel of the step is the
+    same sm_100a kernel the eager path runs: the graphs only remove per-launch
+    host overhead.
 
-    def __init__(self, sess: Session, model: Model, x: RingTensor, lr=1e-2, momentum=0.8, prep=None):
+    ``prefetch_input=True`` also takes the DO's encryption of the first
+    layer's input off the step: it is produced on a copy stream beside the
+    previous step's backward -- right after ``load_batch`` stages a batch, or
+    (input resident, no ``load_batch``) at the end of ``step`` -- from a
+    DO-owned key stream (a per-encryption counter in its own device seed
+    word), and the forward graph consumes it.  In that mode the input must be
+    supplied through ``load_batch`` (direct writes to ``x.values`` are not
+    seen by the prefetched encryption)."""
+
+    def __init__(self, sess: Session, model: Model, x: RingTensor, lr=1e-2, momentum=0.8, prep=None,
+                 prefetch_input: bool = False):
         self.sess, self.model, self.lr, self.momentum, self.prep = sess, model, lr, momentum, prep
         sess.enable_graph_mode()
         self.x = x  # device input buffer; callers copy new batches into x.values (or use load_batch)
@@ -461,16 +473,40 @@ class GraphStep:
         self._batch_pending = False
         n_cls = model.n_classes
         B = x.shape[1] if len(model.in_shape) == 1 else x.shape[0]
-        self.g_do = torch.zeros(n_cls, B, dtype=torch.int64, device=x.values.device)
+        dev = x.values.device
+        self.g_do = torch.zeros(n_cls, B, dtype=torch.int64, device=dev)
         self.logits_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
         self.g_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
         self._loss = SoftmaxCE(model.ring, n_cls, B, logits=self.logits_host.numpy().view(np.uint64),
                                g_out=self.g_host.numpy().view(np.uint64))
+        first = model.layers[model.lin[0]]
+        self.prefetch = bool(prefetch_input) and prep is None and first[0] in ("fc", "conv")
         # warm-up (eager, graph-mode keys): builds plans/maps, sizes scratch buffers
         st, lg = forward_phase(sess, model, x, prep)
         prepare_backward(sess, model, st, prep)
         backward_phase(sess, model, st, self.g_do, lr, momentum, check=False, prep=prep)
         torch.cuda.synchronize()
+        self._copy_stream = torch.cuda.Stream()
+        if self.prefetch:
+            self._x_next = x.values.clone()  # the next step's input (ring encoded)
+            self._enc_seed_host = torch.zeros(4, dtype=torch.int64).pin_memory()
+            self._enc_seed_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+            self._enc_rng = SeededRng(0, 999_001).bind(self._enc_seed_dev.data_ptr())
+            self._enc_count = 0
+            self._enc_base = (int(sess.seed) * 0x9E3779B9 + 12345) & ((1 << 62) - 1)
+            if first[0] == "fc":
+                n_o, n_i = model.W[0].shape
+                self._enc_plan = plan_matmul(MatmulGeometry(n_i, n_o, B), sess.p.N)
+            else:
+                _, c_i, H, Wd = x.shape
+                c_o, s = model.W[0].shape[0], model.W[0].shape[2]
+                self._enc_plan = plan_conv_layer("fwd", B, c_i, c_o, H, Wd, s, first[4], first[5], sess.p.N)
+            self._prefetch_encrypt()  # eager once: allocates the persistent operand buffer
+            torch.cuda.synchronize()
+            sess.clear_prepared()
+            self.g_enc = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.g_enc):
+                self._prefetch_encrypt()  # leaves the prepared entry the forward capture consumes
         self.g_fwd = torch.cuda.CUDAGraph()
         self.g_pre = torch.cuda.CUDAGraph()
         self.g_bwd = torch.cuda.CUDAGraph()
@@ -488,23 +524,55 @@ class GraphStep:
             self.grads = backward_phase(sess, model, self.state, self.g_do, lr, momentum, check=False, prep=prep,
                                         pre_layers=late)
         self._pre_stream = torch.cuda.Stream()
+        self._ev_fwd = torch.cuda.Event()
+        self._ev_ready = torch.cuda.Event()
+        self._loaded_last = False
         torch.cuda.synchronize()
         sess.clear_prepared()
+        if self.prefetch:
+            self._schedule_encrypt()
+
+    def _prefetch_encrypt(self):
+        self.sess.prepare_operand(0, OP_FWD, self._enc_plan, "A_ct", self._x_next, event=False, rng=self._enc_rng,
+                                  background=_PREFETCH_BG)
+
+    def _schedule_encrypt(self):
+        """On the copy stream: a fresh DO key word, then the prefetch graph."""
+        slot = self._enc_count % 4
+        self._enc_seed_host[slot] = self._enc_base + self._enc_count
+        self._enc_count += 1
+        with torch.cuda.stream(self._copy_stream):
+            self._enc_seed_dev.copy_(self._enc_seed_host[slot:slot + 1], non_blocking=True)
+            self.g_enc.replay()
+            self._ev_ready.record()
 
     def load_batch(self, x_host: torch.Tensor):
         """Stage a new real-valued batch (host float64, pinned for an async
         copy; the DO's input, same shape as x) for the next step: the H2D copy
         runs on a copy stream, overlapping the previous step's backward still
-        on the GPU; the next step() encodes it into the graphs' input buffer on
-        the device.  No host sync -- the encode's range flag is checked at
+        on the GPU (with ``prefetch_input`` so do the encode and the DO's
+        encryption); otherwise the next step() encodes it into the graphs'
+        input buffer.  No host sync -- the encode's range flag is checked at
         that step's logits sync."""
         if self._stage is None:
             dev = self.x.values.device
             self._stage = torch.empty(tuple(self.x.values.shape), dtype=torch.float64, device=dev)
             self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
             self._flag_host = torch.zeros(1, dtype=torch.int32).pin_memory()
-            self._copy_stream = torch.cuda.Stream()
             self._ev_loaded, self._ev_free = torch.cuda.Event(), None
+        if self.prefetch:
+            from .ring import encode_fixed_into
+
+            # the previous forward has read x_next (copied into x) and the prepared ciphertext
+            self._copy_stream.wait_event(self._ev_fwd)
+            with torch.cuda.stream(self._copy_stream):
+                self._stage.copy_(x_host, non_blocking=True)
+                encode_fixed_into(self._stage, self.model.ring, self._x_next, self._flag)
+                self._flag_host.copy_(self._flag, non_blocking=True)
+            self._schedule_encrypt()
+            self._flag_pending = True
+            self._loaded_last = True
+            return
         if self._ev_free is not None:  # the previous batch's encode has read the stage
             self._copy_stream.wait_event(self._ev_free)
         with torch.cuda.stream(self._copy_stream):
@@ -527,9 +595,13 @@ class GraphStep:
     def step(self, seed: int, labels):
         self.sess.reseed(seed)
         main = torch.cuda.current_stream()
-        if self._batch_pending:
+        if self.prefetch:
+            main.wait_event(self._ev_ready)  # this step's input and its encryption
+            self.x.values.copy_(self._x_next)
+        elif self._batch_pending:
             self._encode_batch(main)
         self.g_fwd.replay()
+        self._ev_fwd.record(main)
         self._pre_stream.wait_stream(main)
         with torch.cuda.stream(self._pre_stream):  # backward operands, beside the host's loss
             self.g_pre.replay()
@@ -546,6 +618,10 @@ class GraphStep:
         self.g_do.copy_(self.g_host, non_blocking=True)
         main.wait_stream(self._pre_stream)
         self.g_bwd.replay()
+        if self.prefetch and not self._loaded_last:  # resident input: encrypt it afresh for the next step
+            self._copy_stream.wait_event(self._ev_fwd)
+            self._schedule_encrypt()
+        self._loaded_last = False
         return loss
 
 

@@ -77,3 +77,46 @@ def test_graph_step_load_batch():
     r2.load_batch(torch.from_numpy(bad).pin_memory())
     with pytest.raises(EncodeRangeError):
         r2.step(6, labels)
+
+
+def test_graph_step_prefetched_input_encryption():
+    """prefetch_input: the first layer's input encryption is produced beside the
+    previous step (DO-owned key stream); losses and weights still equal the
+    eager step's and the oracle's -- with the input resident and via load_batch."""
+    import torch
+
+    from oracle import nn as ON
+    from oracle import ring as OR
+    from paper_2403_11166_b200 import bfv
+    from paper_2403_11166_b200 import nn as PN
+    from paper_2403_11166_b200.linear_protocols import Session
+    from paper_2403_11166_b200.params import BfvParams
+    from paper_2403_11166_b200.ring import RingParams, RingTensor, SeededRng, encode_fixed
+
+    ring, params = RingParams(), BfvParams()
+    kp = bfv.keygen(params, SeededRng(3, 0))
+    sizes, B = [784, 32, 10], 16
+    xh, labels = PN.synthetic_mnist(7, B, ring)
+    x2h, labels2 = PN.synthetic_mnist(8, B, ring)
+    s1, s2 = Session(params, ring, kp, seed=1), Session(params, ring, kp, seed=1)
+    m1, m2 = PN.Model(sizes, ring, seed=4), PN.Model(sizes, ring, seed=4)
+    x1 = RingTensor(encode_fixed(xh, ring), 25, ring, _canonical=True)
+    runner = PN.GraphStep(s2, m2, RingTensor(encode_fixed(xh, ring), 25, ring, _canonical=True), prefetch_input=True)
+    om = ON.Model(sizes, OR.RingParams(), seed=4)
+    xo, _ = ON.synthetic_mnist(7, B, OR.RingParams())
+    x2o, _ = ON.synthetic_mnist(8, B, OR.RingParams())
+    for step in range(4):
+        if step >= 2:  # switch to a new batch through load_batch
+            x1 = RingTensor(encode_fixed(x2h, ring), 25, ring, _canonical=True)
+            runner.load_batch(torch.from_numpy(np.ascontiguousarray(x2h)).pin_memory())
+            xo, lab = x2o, labels2
+        else:
+            lab = labels
+        s1.reseed(200 + step)
+        l1, _, _ = PN.private_train_step(s1, m1, x1, lab)
+        l2 = runner.step(200 + step, lab)
+        l3, _, _ = ON.reference_train_step(om, xo, lab)
+        assert l1 == l2 == l3
+        for l in range(len(sizes) - 1):
+            assert np.array_equal(m1.W[l].numpy(), m2.W[l].numpy())
+            assert np.array_equal(m2.W[l].numpy(), om.W(l))
