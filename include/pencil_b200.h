@@ -351,6 +351,9 @@ int pb_host_softmax_post(double* ez, int32_t C, int32_t B, const int64_t* labels
  * the critical path) that must leave SM slots to concurrent kernels. */
 int pb_set_launch_cap(int32_t max_ctas);
 
+/* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream). */
+int pb_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,7 @@ SIGNATURES = {
     "pb_host_softmax_post": [P, I32, I32, P, I32, I32, P, P],
     "pb_host_mean": [P, I64],
     "pb_set_launch_cap": [I32],
+    "pb_copy_async": [P, P, I64, P],
     "pb_ring_rowsum": [P, I64, I64, I32, P, P],
     "pb_im2col": [P, I32, I32, I32, I32, I32, I32, P, P],
     "pb_col2im": [P, I32, I32, I32, I32, I32, I32, P, P],
@@ -141,7 +142,7 @@ def check(status: int, what: str = "") -> None:
 # Device kernels each entry point launches (for the bench's gpu_launches count).
 KERNELS_PER_CALL = {
     "pb_encrypt_pk": 2, "pb_encrypt_sk": 1, "pb_decrypt": 2, "pb_decrypt_to_share": 1, "pb_unpack": 1,
-    "pb_abi_version": 0, "pb_last_error": 0, "pb_set_launch_cap": 0, "pb_host_softmax_pre": 0,
+    "pb_abi_version": 0, "pb_last_error": 0, "pb_set_launch_cap": 0, "pb_copy_async": 0, "pb_host_softmax_pre": 0,
     "pb_host_softmax_post": 0, "pb_host_mean": 0, "pb_device_sm_count": 0, "pb_ctx_create": 0, "pb_ctx_destroy": 0,
 }
 

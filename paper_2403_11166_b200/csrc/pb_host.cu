@@ -7,6 +7,8 @@
 #include <cmath>
 #include <cstdint>
 
+#include <cuda_runtime.h>
+
 #include "pencil_b200.h"
 
 // numpy's pairwise summation of n contiguous doubles (numpy/_core/src/umath/
@@ -80,4 +82,14 @@ extern "C" int pb_host_softmax_post(double* ez, int32_t C, int32_t B, const int6
     g_out[i] = (uint64_t)(int64_t)std::floor(g) & mask;
   }
   return PB_OK;
+}
+
+// Async copy (any direction, unified addressing) on a stream: the DO's loss
+// gradient H2D between the forward and backward graphs, without the
+// framework's per-copy host overhead.
+extern "C" int pb_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes < 0 || ((!dst || !src) && bytes)) return PB_ERR_ARG;
+  if (!bytes) return PB_OK;
+  return cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream) == cudaSuccess ? PB_OK
+                                                                                                         : PB_ERR_CUDA;
 }

@@ -443,6 +443,7 @@ def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e
 
 _LATE_PREP = __import__("os").environ.get("PB_LATE_PREP", "1") == "1"
 _PREFETCH_BG = __import__("os").environ.get("PB_PREFETCH_BG", "1") == "1"
+_SPIN_WAIT = __import__("os").environ.get("PB_SPIN_WAIT", "1") == "1"
 
 
 class GraphStep:
@@ -526,6 +527,10 @@ class GraphStep:
         self._pre_stream = torch.cuda.Stream()
         self._ev_fwd = torch.cuda.Event()
         self._ev_ready = torch.cuda.Event()
+        self._ev_logits = torch.cuda.Event()
+        self._ev_pre = torch.cuda.Event()
+        self._g_dev_ptr, self._g_host_ptr = self.g_do.data_ptr(), self.g_host.data_ptr()
+        self._g_bytes = self.g_do.numel() * 8
         self._loaded_last = False
         torch.cuda.synchronize()
         sess.clear_prepared()
@@ -592,9 +597,18 @@ class GraphStep:
         self._batch_pending = False
         self._flag_pending = True
 
+    timing = None  # diagnostics: a list receives (label, CUDA event) at the step's phase boundaries
+
+    def _mark(self, label):
+        if self.timing is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.timing.append((label, ev))
+
     def step(self, seed: int, labels):
         self.sess.reseed(seed)
         main = torch.cuda.current_stream()
+        self._mark("start")
         if self.prefetch:
             main.wait_event(self._ev_ready)  # this step's input and its encryption
             self.x.values.copy_(self._x_next)
@@ -602,11 +616,18 @@ class GraphStep:
             self._encode_batch(main)
         self.g_fwd.replay()
         self._ev_fwd.record(main)
+        self._mark("fwd")
         self._pre_stream.wait_stream(main)
         with torch.cuda.stream(self._pre_stream):  # backward operands, beside the host's loss
             self.g_pre.replay()
+            self._ev_pre.record()
         self.logits_host.copy_(self.logits.values, non_blocking=True)
-        main.synchronize()
+        self._ev_logits.record(main)
+        if _SPIN_WAIT:  # busy-poll: a blocking sync can sleep past the copy's completion
+            while not self._ev_logits.query():
+                pass
+        else:
+            self._ev_logits.synchronize()
         if self._flag_pending:
             self._flag_pending = False
             if int(self._flag_host[0]):
@@ -615,9 +636,12 @@ class GraphStep:
                 limit = float(1 << (self.model.ring.ell - 1)) / float(1 << self.model.ring.f)
                 raise EncodeRangeError(f"|x| must stay below {limit}")
         loss, _ = self._loss(labels)  # g written into g_host
-        self.g_do.copy_(self.g_host, non_blocking=True)
-        main.wait_stream(self._pre_stream)
+        _lib.load().pb_copy_async(self._g_dev_ptr, self._g_host_ptr, self._g_bytes, main.cuda_stream)
+        self._mark("host")
+        main.wait_event(self._ev_pre)
+        self._mark("pre")
         self.g_bwd.replay()
+        self._mark("bwd")
         if self.prefetch and not self._loaded_last:  # resident input: encrypt it afresh for the next step
             self._copy_stream.wait_event(self._ev_fwd)
             self._schedule_encrypt()
