@@ -117,11 +117,19 @@ struct Ntt {
   }
 
   // =========================== forward ===========================
-  __device__ __forceinline__ static void fwd_p1(uint32_t (&a)[32], const uint2* tw, uint32_t q) {
+  // skip: leading stages whose upper butterfly inputs are structurally zero
+  // (input supported on [0, N / 2^skip)): (x, 0) -> (x, x), no multiply.
+  __device__ __forceinline__ static void fwd_p1(uint32_t (&a)[32], const uint2* tw, uint32_t q, int skip = 0) {
     const uint32_t q2 = 2 * q;
 #pragma unroll
     for (int s = 0; s < 5; ++s) {
       const int tc = 16 >> s;
+      if (s < skip) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          if (!(c & tc)) a[c + tc] = a[c];
+        continue;
+      }
       uint2 w[16];
 #pragma unroll
       for (int g = 0; g < (1 << s); ++g) w[g] = tw[(1 << s) + g];  // shared memory
@@ -129,6 +137,12 @@ struct Ntt {
       for (int c = 0; c < 32; ++c)
         if (!(c & tc)) ct_bfly(a[c], a[c + tc], w[c >> (5 - s)], q, q2);
     }
+  }
+  // leading forward stages that are trivial for an input supported on [0, support)
+  __device__ __forceinline__ static int trivial_stages(int support) {
+    int k = 0;
+    while (k < 5 && support <= (N >> (k + 1))) ++k;
+    return k;
   }
   __device__ __forceinline__ static void fwd_p2(uint32_t (&a)[32], const uint2* tw, int tid, uint32_t q) {
     const uint32_t q2 = 2 * q;
@@ -165,14 +179,14 @@ struct Ntt {
   // lazily reduced ([0,4q)) result in P3 layout on exit.  `sm` needs
   // SMEM_WORDS words; the caller syncs before reusing it.
   __device__ __forceinline__ static void forward(uint32_t (&a)[32], uint32_t* sm, const uint2* tw,
-                                                 const uint2* t3, int tid, uint32_t q) {
+                                                 const uint2* t3, int tid, uint32_t q, int support = N) {
     // P1/P2 twiddles from shared memory: one coalesced load per thread instead of
     // just-in-time L1/L2 loads before every early stage (ncu: ~50% of the stall
     // samples sat in the P1 stages)
     uint2* st = stw(sm);
     st[tid] = __ldg(tw + tid);
     __syncthreads();
-    fwd_p1(a, st, q);
+    fwd_p1(a, st, q, trivial_stages(support));
     st1(sm, a, tid);
     __syncthreads();
     ld2(sm, a, tid);
