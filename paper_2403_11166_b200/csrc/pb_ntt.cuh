@@ -117,14 +117,16 @@ struct Ntt {
   }
 
   // =========================== forward ===========================
-  // skip: leading stages whose upper butterfly inputs are structurally zero
-  // (input supported on [0, N / 2^skip)): (x, 0) -> (x, x), no multiply.
-  __device__ __forceinline__ static void fwd_p1(uint32_t (&a)[32], const uint2* tw, uint32_t q, int skip = 0) {
+  // bits: OR of the input's occupied indices.  Stage s butterflies index bit
+  // logN-1-s; when that bit is 0 in every occupied position (earlier stages
+  // only touch higher bits) the upper inputs are zero: (x, 0) -> (x, x).
+  __device__ __forceinline__ static bool trivial(int bits, int s) { return !((bits >> (LOGN - 1 - s)) & 1); }
+  __device__ __forceinline__ static void fwd_p1(uint32_t (&a)[32], const uint2* tw, uint32_t q, int bits = N - 1) {
     const uint32_t q2 = 2 * q;
 #pragma unroll
     for (int s = 0; s < 5; ++s) {
       const int tc = 16 >> s;
-      if (s < skip) {
+      if (trivial(bits, s)) {
 #pragma unroll
         for (int c = 0; c < 32; ++c)
           if (!(c & tc)) a[c + tc] = a[c];
@@ -138,18 +140,20 @@ struct Ntt {
         if (!(c & tc)) ct_bfly(a[c], a[c + tc], w[c >> (5 - s)], q, q2);
     }
   }
-  // leading forward stages that are trivial for an input supported on [0, support)
-  __device__ __forceinline__ static int trivial_stages(int support) {
-    int k = 0;
-    while (k < 5 && support <= (N >> (k + 1))) ++k;
-    return k;
-  }
-  __device__ __forceinline__ static void fwd_p2(uint32_t (&a)[32], const uint2* tw, int tid, uint32_t q) {
+
+  __device__ __forceinline__ static void fwd_p2(uint32_t (&a)[32], const uint2* tw, int tid, uint32_t q,
+                                                int bits = N - 1) {
     const uint32_t q2 = 2 * q;
     const int warp = tid >> 5;
 #pragma unroll
     for (int s = 5; s < 5 + M; ++s) {
       const int tc = 1 << (LOGN - 6 - s);
+      if (trivial(bits, s)) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          if (!(c & tc)) a[c + tc] = a[c];
+        continue;
+      }
       const uint2* wb = tw + (1 << s) + (warp << (s + 10 - LOGN));
 #pragma unroll
       for (int c = 0; c < 32; ++c)
@@ -179,18 +183,18 @@ struct Ntt {
   // lazily reduced ([0,4q)) result in P3 layout on exit.  `sm` needs
   // SMEM_WORDS words; the caller syncs before reusing it.
   __device__ __forceinline__ static void forward(uint32_t (&a)[32], uint32_t* sm, const uint2* tw,
-                                                 const uint2* t3, int tid, uint32_t q, int support = N) {
+                                                 const uint2* t3, int tid, uint32_t q, int bits = N - 1) {
     // P1/P2 twiddles from shared memory: one coalesced load per thread instead of
     // just-in-time L1/L2 loads before every early stage (ncu: ~50% of the stall
     // samples sat in the P1 stages)
     uint2* st = stw(sm);
     st[tid] = __ldg(tw + tid);
     __syncthreads();
-    fwd_p1(a, st, q, trivial_stages(support));
+    fwd_p1(a, st, q, bits);
     st1(sm, a, tid);
     __syncthreads();
     ld2(sm, a, tid);
-    fwd_p2(a, st, tid, q);
+    fwd_p2(a, st, tid, q, bits);
     __syncthreads();
     st2(sm, a, tid);
     __syncthreads();

@@ -19,8 +19,9 @@ struct Pack {
 
 // Loads the lifted source polynomial p into a[] in the NTT's P1 layout; the
 // packed path builds the row in shared memory and leaves `sm` free.  Returns
-// the support bound (1 + the largest occupied coefficient; N when dense), from
-// which the forward NTT skips its trivially-zero leading stages.
+// the OR of the occupied coefficient indices (N - 1 when dense): a forward NTT
+// stage whose index bit is 0 in every occupied position has structurally zero
+// upper inputs and is skipped (Ntt::forward).
 template <class Nt, class Lift>
 __device__ __forceinline__ int load_source(uint32_t (&a)[32], uint32_t* sm, const Pack& s, int64_t p, int tid,
                                            Lift lift) {
@@ -29,7 +30,7 @@ __device__ __forceinline__ int load_source(uint32_t (&a)[32], uint32_t* sm, cons
     if (tid == 0) *sup = 0;
     for (int j = tid; j < Nt::N; j += Nt::T) sm[Nt::pad(j)] = 0u;
     __syncthreads();
-    int jmax = -1;
+    int jor = 0;
     const int32_t* pp = s.pos + p * s.Z;
     const int32_t* ps = s.src + p * s.Z;
     // batches of 8 slots per thread: all position / source loads are issued
@@ -48,19 +49,19 @@ __device__ __forceinline__ int load_source(uint32_t (&a)[32], uint32_t* sm, cons
       for (int u = 0; u < 8; ++u) v[u] = j[u] >= 0 ? __ldg(s.vals + si[u]) : 0ull;
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (j[u] >= 0) sm[Nt::pad(j[u])] = lift(v[u]), jmax = max(jmax, j[u]);
+        if (j[u] >= 0) sm[Nt::pad(j[u])] = lift(v[u]), jor |= j[u];
     }
-    if (jmax >= 0) atomicMax(sup, jmax + 1);
+    if (jor) atomicOr(sup, jor);
     __syncthreads();
-    const int support = *sup;
+    const int bits = *sup;
     Nt::ld1(sm, a, tid);
     __syncthreads();
-    return support;
+    return bits;
   }
   const uint64_t* v = s.vals + p * Nt::N;
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = lift(__ldg(v + Nt::j1(tid, c)));
-  return Nt::N;
+  return Nt::N - 1;
 }
 
 // Montgomery multiplication with R = 2^32: returns a*b*R^-1 mod q in [0, 2q)
