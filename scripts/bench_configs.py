@@ -183,9 +183,23 @@ def fc_round(steps, cpu):
         LP.grad_weight(sess, 1, *xs, *gs)
         LP.linear_backward_input(sess, 1, W, *gs)
 
-    ms = time_steps(rnd, steps, flush=_flush_buf())
+    ms_eager = time_steps(rnd, steps, flush=_flush_buf())
+    # the same round replayed from one CUDA graph (seed indirection re-keys it per replay)
+    sess.enable_graph_mode()
+    for i in range(2):
+        rnd(100 + i)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        rnd(200)
+
+    def replay(i):
+        sess.reseed(SEED + 300 + i)
+        g.replay()
+
+    ms = time_steps(replay, steps, flush=_flush_buf())
     out = {"config": "fc784x128_round", "batch": B, "ms_per_round": ms, "samples_per_s": B / (ms / 1e3),
-           "note": "eager launches (no graph)"}
+           "eager_ms_per_round": ms_eager, "note": "graph replay; eager_ms_per_round: the same calls launched eagerly"}
     if cpu:
         out["cpu"] = cpu_fc_round()
     return out
