@@ -345,6 +345,55 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
   }
 }
 
+__constant__ int g_prune_inv = 1;  // (a device constant so an experiment can switch it off)
+
+// Number of low index bits (<= 5) that are 1 in every useful slot of a ciphertext:
+// its inverse NTT can be output-pruned by that many stages (Ntt::inverse_pruned).
+// Block-wide AND over the slot list; `flag` is a shared int (synchronised).
+template <class Nt>
+__device__ __forceinline__ int common_low_ones(const int32_t* pos, int U, int tid, int* flag) {
+  if (!g_prune_inv) return 0;
+  if (tid == 0) *flag = -1;
+  __syncthreads();
+  int acc = -1;
+  for (int u0 = tid; u0 < U; u0 += 8 * Nt::T) {  // batched: eight independent loads in flight
+    int j[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) j[k] = u0 + k * Nt::T < U ? __ldg(pos + u0 + k * Nt::T) : -1;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (j[k] >= 0) acc &= j[k];
+  }
+  if (acc != -1) atomicAnd(flag, acc);
+  __syncthreads();
+  const int v = *flag;
+  __syncthreads();
+  int t = 0;
+  while (t < 5 && ((v >> t) & 1)) ++t;
+  // one pruned stage leaves N/2 values for the shared-memory stages: slower than
+  // the register inverse (B200: U = 4096 x 2 cts 11.7 -> 15.1 us); from two on it pays
+  return t >= 2 ? t : 0;
+}
+
+// inverse_scaled, or the output-pruned inverse for TT common low one-bits:
+// returns TT (0: full inverse, result in a[] in P1 layout; else the compact
+// array A[n >> TT] in sm).
+template <class Nt>
+__device__ __forceinline__ int inverse_for_slots(uint32_t (&a)[32], uint32_t* sm, const PbDev& P, int l, int tid,
+                                                 uint32_t q, int tt) {
+  const uint2* tw = P.tw_inv + (size_t)l * Nt::N;
+  const uint2* t3 = P.tw3_inv + (size_t)l * P.tw3_stride;
+  const uint32_t ni = P.ninv[l], nis = P.ninv_sh[l], wn = P.w0n[l], wns = P.w0n_sh[l];
+  switch (tt) {
+    case 1: Nt::template inverse_pruned<1>(a, sm, tw, t3, tid, q, ni, nis, wn, wns); return 1;
+    case 2: Nt::template inverse_pruned<2>(a, sm, tw, t3, tid, q, ni, nis, wn, wns); return 2;
+    case 3: Nt::template inverse_pruned<3>(a, sm, tw, t3, tid, q, ni, nis, wn, wns); return 3;
+    case 4: Nt::template inverse_pruned<4>(a, sm, tw, t3, tid, q, ni, nis, wn, wns); return 4;
+    case 5: Nt::template inverse_pruned<5>(a, sm, tw, t3, tid, q, ni, nis, wn, wns); return 5;
+    default: Nt::inverse_scaled(a, sm, tw, t3, tid, q, ni, nis, wn, wns); return 0;
+  }
+}
+
 // --------------------------------------------------------------- decrypt ---
 // mode 0: write x = INTT(c0 + c1 s) for all coefficients to out32 [P][L][N].
 // mode 1: write only the useful slots out_pos[p][u] to out32 [P][L][U].
@@ -369,24 +418,28 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   Nt::gld3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = addmod(a[c], b[c], q);
-  const uint32_t ni = P.ninv[l], nis = P.ninv_sh[l];
-  Nt::inverse_scaled(a, sm, P.tw_inv + (size_t)l * N, P.tw3_inv + (size_t)l * P.tw3_stride, tid, q, ni, nis,
-                     P.w0n[l], P.w0n_sh[l]);
   if (mode == 0) {
+    const uint32_t ni = P.ninv[l], nis = P.ninv_sh[l];
+    Nt::inverse_scaled(a, sm, P.tw_inv + (size_t)l * N, P.tw3_inv + (size_t)l * P.tw3_stride, tid, q, ni, nis,
+                       P.w0n[l], P.w0n_sh[l]);
     Nt::gst1(out32 + (p * L + l) * N, a, tid);
   } else {
-    __syncthreads();
-    Nt::st1(sm, a, tid);
-    __syncthreads();
     const int32_t* pos = out_pos + p * U;
+    const int tt = inverse_for_slots<Nt>(a, sm, P, l, tid, q,
+                                         common_low_ones<Nt>(pos, U, tid, reinterpret_cast<int*>(sm + Nt::TW_OFF)));
+    if (tt == 0) {
+      __syncthreads();
+      Nt::st1(sm, a, tid);
+    }
+    __syncthreads();
     uint32_t* dst = out32 + (p * L + l) * U;
     for (int u0 = tid; u0 < U; u0 += 8 * Nt::T) {  // batched position loads
       int j[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) j[k] = u0 + k * Nt::T < U ? __ldg(pos + u0 + k * Nt::T) : -1;
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (j[k] >= 0) dst[u0 + k * Nt::T] = sm[Nt::pad(j[k])];  // already scaled by N^-1
+      for (int k = 0; k < 8; ++k)  // already scaled by N^-1
+        if (j[k] >= 0) dst[u0 + k * Nt::T] = tt ? sm[j[k] >> tt] : sm[Nt::pad(j[k])];
     }
   }
 }
@@ -465,15 +518,17 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   Nt::gld3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = addmod(a[c], b[c], q);
-  Nt::inverse_scaled(a, sm, P.tw_inv + (size_t)l * N, P.tw3_inv + (size_t)l * P.tw3_stride, tid, q, P.ninv[l],
-                     P.ninv_sh[l], P.w0n[l], P.w0n_sh[l]);
-  __syncthreads();
-  Nt::st1(sm, a, tid);
-  cluster.sync();  // every limb's row is in its CTA's shared memory
+  const int32_t* pos = out_pos + p * U;
+  const int tt = inverse_for_slots<Nt>(a, sm, P, l, tid, q,
+                                       common_low_ones<Nt>(pos, U, tid, reinterpret_cast<int*>(sm + Nt::TW_OFF)));
+  if (tt == 0) {
+    __syncthreads();
+    Nt::st1(sm, a, tid);
+  }
+  cluster.sync();  // every limb's row (or its compact useful part) is in its CTA's shared memory
   const uint32_t* rows[PB_MAXL];
 #pragma unroll
   for (int k = 0; k < PB_MAXL; ++k) rows[k] = k < L ? cluster.map_shared_rank(sm, k) : nullptr;
-  const int32_t* pos = out_pos + p * U;
   const int64_t* dst = out_dst + p * U;
   // CTA l decodes the contiguous block [u0, u1) of the useful slots (balanced
   // across the cluster: a strided split left the remainder to one CTA, whose
@@ -486,10 +541,11 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
     const int ja = __ldg(pos + u), jb = ub < u1 ? __ldg(pos + ub) : -1;
     const int64_t da = __ldg(dst + u), db = ub < u1 ? __ldg(dst + ub) : 0;
     uint32_t xa[PB_MAXL], xb[PB_MAXL], d[PB_MAXL];
+    const int ia = ja < 0 ? 0 : (tt ? ja >> tt : Nt::pad(ja)), ib = jb < 0 ? 0 : (tt ? jb >> tt : Nt::pad(jb));
 #pragma unroll
     for (int k = 0; k < PB_MAXL; ++k) {
-      xa[k] = (k < L && ja >= 0) ? rows[k][Nt::pad(ja)] : 0u;
-      xb[k] = (k < L && jb >= 0) ? rows[k][Nt::pad(jb)] : 0u;
+      xa[k] = (k < L && ja >= 0) ? rows[k][ia] : 0u;
+      xb[k] = (k < L && jb >= 0) ? rows[k][ib] : 0u;
     }
     if (ja >= 0) {
       garner_dev(P, xa, 1, d);
@@ -851,6 +907,15 @@ extern "C" int pb_decrypt_to_share(const pb_ctx* ctx, const uint32_t* sk, const 
     const char* v = getenv("PB_DEC_CLUSTER");
     return v ? atoi(v) : 1;
   }();
+  static const bool prune_set = [] {  // PB_PRUNE_INV=0: full inverse NTTs (experiment knob)
+    const char* v = getenv("PB_PRUNE_INV");
+    if (v && atoi(v) == 0) {
+      const int off = 0;
+      cudaMemcpyToSymbol(g_prune_inv, &off, sizeof(off));
+    }
+    return true;
+  }();
+  (void)prune_set;
   // fused cluster kernel (one launch, DSMEM limb exchange) when the decode is
   // light; with many useful slots per ciphertext the separate decode kernel's
   // parallelism wins (B200, graph-timed: U = 256 x 32 cts 12.3 vs 13.9 us,

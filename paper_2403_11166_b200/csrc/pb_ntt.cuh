@@ -305,6 +305,68 @@ struct Ntt {
     }
   }
 
+  // ---- Output-pruned inverse.  The GS inverse decides output-index bit b in
+  // its stage of distance 2^b (the difference branch makes bit b = 1).  When
+  // only outputs n = 2^TT - 1 (mod 2^TT) are needed (the matmul packings'
+  // useful slots), the first TT stages keep only the difference branch and
+  // everything after runs on the N / 2^TT surviving values: the P3 stages on
+  // the surviving registers, the remaining log N - 5 stages on a compact
+  // shared-memory array A[m] = x[m 2^TT + 2^TT - 1] (same twiddles, same N^-1
+  // folded into the last stage).  Result: canonical A[0 .. N >> TT) in sm. ----
+  template <int TT, int D>
+  __device__ __forceinline__ static void inv_p3_stage_pruned(uint32_t (&a)[32], const uint2* tw, int tid,
+                                                             uint32_t q, uint32_t q2) {
+    constexpr int b = 4 - D, tc = 1 << b;  // this stage butterflies index bit b
+    uint2 w[16];
+    tw3<D>(tw, tid, w);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      if (c & tc) continue;
+      if (b < TT) {  // keep the difference branch (upper register) of the surviving pairs
+        if ((c & (tc - 1)) == tc - 1) a[c + tc] = mul_shoup_lazy(a[c] - a[c + tc] + q2, w[c >> (5 - D)].x,
+                                                                 w[c >> (5 - D)].y, q);
+      } else if ((c & ((1 << TT) - 1)) == (1 << TT) - 1) {
+        gs_bfly(a[c], a[c + tc], w[c >> (5 - D)], q, q2);
+      }
+    }
+  }
+  template <int TT>
+  __device__ __forceinline__ static void inverse_pruned(uint32_t (&a)[32], uint32_t* sm, const uint2* tw,
+                                                        const uint2* t3, int tid, uint32_t q, uint32_t ni,
+                                                        uint32_t nis, uint32_t wn, uint32_t wns) {
+    static_assert(TT >= 1 && TT <= 5, "prune 1..5 stages");
+    const uint32_t q2 = 2 * q;
+    uint2* st = stw(sm);
+    st[tid] = __ldg(tw + tid);  // stage twiddles tw[1 .. T) (the compact stages use indices < T)
+    inv_p3_stage_pruned<TT, 4>(a, t3, tid, q, q2);
+    inv_p3_stage_pruned<TT, 3>(a, t3, tid, q, q2);
+    inv_p3_stage_pruned<TT, 2>(a, t3, tid, q, q2);
+    inv_p3_stage_pruned<TT, 1>(a, t3, tid, q, q2);
+    inv_p3_stage_pruned<TT, 0>(a, t3, tid, q, q2);
+    constexpr int R = (1 << TT) - 1, NP = N >> TT;
+#pragma unroll
+    for (int c = R; c < 32; c += 1 << TT) sm[tid * (32 >> TT) + (c >> TT)] = a[c];  // compact index n >> TT
+    __syncthreads();
+#pragma unroll 1
+    for (int bb = 5; bb < LOGN; ++bb) {  // remaining stages: index bits 5 .. logN-1
+      const int d = 1 << (bb - TT);       // compact pair distance
+      const int h = N >> (bb + 1);        // twiddle groups of this stage
+      for (int k = tid; k < NP / 2; k += T) {
+        const int m = ((k >> (bb - TT)) << (bb - TT + 1)) | (k & (d - 1));
+        uint32_t x = sm[m], y = sm[m + d];
+        if (bb < LOGN - 1) {
+          gs_bfly(x, y, st[h + (m >> (bb + 1 - TT))], q, q2);
+          sm[m] = x;
+          sm[m + d] = y;
+        } else {  // last stage with N^-1 folded in (as inverse_scaled)
+          sm[m] = mul_shoup(x + y, ni, nis, q);
+          sm[m + d] = mul_shoup(x - y + q2, wn, wns, q);
+        }
+      }
+      __syncthreads();
+    }
+  }
+
   // ---- NTT-domain rows in DEVICE ORDER: bit-reversed index j = tid*32 + 4v + k
   // (the P3 layout) is stored at address v*4T + tid*4 + k, so a P3-layout
   // register file moves to/from HBM with fully coalesced 128-bit accesses.
