@@ -55,7 +55,13 @@ import os as _os
 _SERIAL = _os.environ.get("PB_SERIAL", "0") == "1"
 _MASK_PREFETCH = _os.environ.get("PB_MASK_PREFETCH", "1") == "1"
 _BG_CAP = int(_os.environ.get("PB_BG_CAP", "148"))  # CTA cap of background operand preparation (0: none)
-_PRIO = tuple(int(v) for v in _os.environ.get("PB_PRIO", "0,0").split(","))  # (encrypt, encode) stream priorities
+_PRIO = tuple(int(v) for v in _os.environ["PB_PRIO"].split(",")) if "PB_PRIO" in _os.environ else None
+
+
+def _stream_like(cur: torch.cuda.Stream) -> torch.cuda.Stream:
+    """A new stream with the priority of ``cur``: forks of the critical chain
+    inherit its (higher) priority, forks of the grad-W chain its lower one."""
+    return torch.cuda.Stream(priority=cur.priority)
 
 
 def stream_id(layer: int, op: int, purpose: int) -> int:
@@ -151,7 +157,7 @@ class _Aux:
         key = self.main.cuda_stream
         st = self.sess._aux_streams.get(key)
         if st is None:
-            st = self.sess._aux_streams[key] = torch.cuda.Stream()
+            st = self.sess._aux_streams[key] = _stream_like(self.main)
         self.stream = st
         st.wait_stream(self.main)
         return self
@@ -237,10 +243,14 @@ class Session:
             return cur, cur
         key = torch.cuda.current_stream().cuda_stream
         if key not in self._streams:
-            # stream priorities (PB_PRIO="enc,encode"): measured no effect on the
-            # MLP step (profiles/r01_ab_stream_priority.txt), default equal
-            pe, pp = _PRIO
-            self._streams[key] = (torch.cuda.Stream(priority=pe), torch.cuda.Stream(priority=pp))
+            # the calling stream's priority (the critical chain's forks outrank the
+            # grad-W chain's; PB_PRIO="enc,encode" overrides -- relative priorities
+            # inside one protocol measured no effect, profiles/r01_ab_stream_priority.txt)
+            cur = torch.cuda.current_stream()
+            if _PRIO is None:
+                self._streams[key] = (_stream_like(cur), _stream_like(cur))
+            else:
+                self._streams[key] = (torch.cuda.Stream(priority=_PRIO[0]), torch.cuda.Stream(priority=_PRIO[1]))
         return self._streams[key]
 
     def aux(self):
@@ -363,7 +373,7 @@ class Session:
         else:
             side = self._mask_streams.get(cur.cuda_stream)
             if side is None:
-                side = self._mask_streams[cur.cuda_stream] = torch.cuda.Stream()
+                side = self._mask_streams[cur.cuda_stream] = _stream_like(cur)
             side.wait_stream(cur)
         with torch.cuda.stream(side):
             for layer, op, shape, buf in bufs:
@@ -384,7 +394,7 @@ class Session:
             return [cur]
         pool = self._fork_pools.get(cur.cuda_stream)
         if pool is None:
-            pool = self._fork_pools[cur.cuda_stream] = [torch.cuda.Stream() for _ in range(n)]
+            pool = self._fork_pools[cur.cuda_stream] = [_stream_like(cur) for _ in range(n)]
         for st in pool:
             st.wait_stream(cur)
             self._pending_join.append(st)

@@ -290,7 +290,13 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
     for l in reversed(range(L)):
         e = model.layers[model.lin[l]]
         last = l == L - 1
-        gstream.wait_stream(main)
+        ev_gy = torch.cuda.Event()
+        ev_gy.record(main)  # grad Y_l is available: both chains fork here
+        # the input-gradient protocol (the critical chain) is enqueued first, so its
+        # kernels come first in the graph's launch order when both chains are ready
+        if l > 0 and _BX_FIRST:
+            ga = _backward_input(sess, model, l, e, acts, gy_mo, gy_do, last, prep)
+        gstream.wait_event(ev_gy)
         with torch.cuda.stream(gstream):
             if prep is not None:
                 gbs[l] = (reveal_grad_bias if e[0] == "fc" else reveal_grad_bias_conv)(sess, l, gy_mo, gy_do)
@@ -306,14 +312,8 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
         keep.append((gy_mo, gy_do))
         if trace is not None:
             trace.append((l, ys[l], gbs[l], gws[l]))
-        if l > 0:
-            if prep is not None:
-                ga = PP.prep_linear_backward_input(sess, l, prep.banks[l], model.W[l], gy_mo, gy_do)
-            elif e[0] == "fc":
-                ga = linear_backward_input(sess, l, model.W[l], gy_mo, gy_do, mo_gy_zero=last)
-            else:
-                H, Wd = acts[l][1].shape[2:]
-                ga = conv_backward_input(sess, l, model.W[l], gy_mo, gy_do, H, Wd, e[4], e[5], mo_gy_zero=last)
+        if l > 0 and not _BX_FIRST:
+            ga = _backward_input(sess, model, l, e, acts, gy_mo, gy_do, last, prep)
         # the MO's SGD for layer l as soon as both grad W_l (grad stream) and
         # the last use of W_l (this layer's input-gradient protocol) are enqueued
         gstream.wait_stream(main)
@@ -362,6 +362,15 @@ def _mask_specs(model: Model, B: int, ops, layers=None):
             elif op == OP_GRAD_W:
                 out.append((l, op, tuple(model.W[l].shape)))
     return out
+
+
+def _backward_input(sess, model, l, e, acts, gy_mo, gy_do, last, prep):
+    if prep is not None:
+        return PP.prep_linear_backward_input(sess, l, prep.banks[l], model.W[l], gy_mo, gy_do)
+    if e[0] == "fc":
+        return linear_backward_input(sess, l, model.W[l], gy_mo, gy_do, mo_gy_zero=last)
+    H, Wd = acts[l][1].shape[2:]
+    return conv_backward_input(sess, l, model.W[l], gy_mo, gy_do, H, Wd, e[4], e[5], mo_gy_zero=last)
 
 
 def prepare_backward(sess: Session, model: Model, state, prep=None, layers=None, clear=True, events=True,
@@ -444,6 +453,8 @@ def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e
 _LATE_PREP = __import__("os").environ.get("PB_LATE_PREP", "1") == "1"
 _PREFETCH_BG = __import__("os").environ.get("PB_PREFETCH_BG", "1") == "1"
 _SPIN_WAIT = __import__("os").environ.get("PB_SPIN_WAIT", "1") == "1"
+_BX_FIRST = __import__("os").environ.get("PB_BX_FIRST", "1") == "1"
+_CHAIN_PRIO = int(__import__("os").environ.get("PB_CHAIN_PRIO", "0"))  # e.g. -2: critical chain at higher priority (measured no gain)
 
 
 class GraphStep:
@@ -511,7 +522,11 @@ class GraphStep:
         self.g_fwd = torch.cuda.CUDAGraph()
         self.g_pre = torch.cuda.CUDAGraph()
         self.g_bwd = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.g_fwd):
+        # the forward and the input-gradient chain are captured on a high-priority
+        # stream (their forks inherit it); the grad-W chain's stream keeps the
+        # default, lower priority, so the block scheduler serves the critical chain first
+        hp = torch.cuda.Stream(priority=_CHAIN_PRIO) if _CHAIN_PRIO else None
+        with torch.cuda.graph(self.g_fwd, stream=hp):
             self.state, self.logits = forward_phase(sess, model, x, prep)
         # the operands the backward consumes first (layers >= 1) are prepared beside
         # the host's loss step; layer 0's (consumed last) inside the backward graph,
@@ -521,7 +536,7 @@ class GraphStep:
         with torch.cuda.graph(self.g_pre, pool=self.g_fwd.pool()):
             prepare_backward(sess, model, self.state, prep, layers=[l for l in range(L) if l not in late],
                              events=False)  # ordered by step(): the backward replay waits for this graph
-        with torch.cuda.graph(self.g_bwd, pool=self.g_fwd.pool()):
+        with torch.cuda.graph(self.g_bwd, pool=self.g_fwd.pool(), stream=hp):
             self.grads = backward_phase(sess, model, self.state, self.g_do, lr, momentum, check=False, prep=prep,
                                         pre_layers=late)
         self._pre_stream = torch.cuda.Stream()
