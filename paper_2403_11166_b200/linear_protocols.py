@@ -54,6 +54,7 @@ import os as _os
 
 _SERIAL = _os.environ.get("PB_SERIAL", "0") == "1"
 _MASK_PREFETCH = _os.environ.get("PB_MASK_PREFETCH", "1") == "1"
+_GRADW_FLIP = _os.environ.get("PB_GRADW_FLIP", "0") == "1"
 _BG_CAP = int(_os.environ.get("PB_BG_CAP", "148"))  # CTA cap of background operand preparation (0: none)
 _PRIO = tuple(int(v) for v in _os.environ["PB_PRIO"].split(",")) if "PB_PRIO" in _os.environ else None
 
@@ -621,6 +622,27 @@ def reveal_grad_bias(sess: Session, layer: int, gy_a: ShareTensor, gy_b: ShareTe
     return RingTensor(_ring_bin(_lib.RING_ADD, sm, sd, ring.ell), gy_do.scale, ring, _canonical=True)
 
 
+def grad_w_flipped(mo_x_zero: bool, mo_gy_zero: bool) -> bool:
+    """Whether Alg.2's HE matmul runs transposed (grad W^T = X gY^T), PB_GRADW_FLIP=1:
+    for the two-cross-term layers it puts the gradient on the packing side with
+    fewer polynomials (128x128x64: 16 instead of 64 gradient ciphertexts and
+    plaintexts), the forward-only X side (prepared beside the loss) grows to 64.
+    Measured on the MLP step: 1.5 % slower (the larger host-gap preparation
+    delays the backward; profiles/r01_ab_gradw_flip.txt), so off by default;
+    one-term layers never flip (the first layer's X side would grow 80 -> 208)."""
+    return _GRADW_FLIP and not (mo_x_zero or mo_gy_zero)
+
+
+def grad_w_geometry(n_o: int, n_i: int, B: int, flipped: bool):
+    """(geometry, v_strides, y_strides) of Alg.2's HE matmul for an (n_o, n_i)
+    layer: grad W = gY X^T with gY (n_o, B) in the W role and X^T (strides
+    (1, B)) in the v role; flipped: grad W^T = X gY^T with X (n_i, B) in the W
+    role, gY^T in the v role and the output written transposed."""
+    if flipped:
+        return MatmulGeometry(B, n_i, n_o), (1, B), (1, n_i)
+    return MatmulGeometry(B, n_o, n_i), (1, B), None
+
+
 def grad_weight(sess: Session, layer: int, x_a: ShareTensor, x_b: ShareTensor, gy_a: ShareTensor,
                 gy_b: ShareTensor, e: torch.Tensor | None = None, mo_x_zero: bool = False,
                 mo_gy_zero: bool = False) -> RingTensor:  # Alg.2, SPEC:339-347
@@ -630,7 +652,6 @@ def grad_weight(sess: Session, layer: int, x_a: ShareTensor, x_b: ShareTensor, g
     ring = sess.ring
     n_i, B = x_do.shape
     n_o = gy_do.shape[0]
-    g = MatmulGeometry(B, n_o, n_i)  # v = X^T (B x n_i) via strides (1, B); W = gY (n_o x B)
     s = sess.mask(layer, OP_GRAD_W, (n_o, n_i))
     cross_do = _dev.empty_u64(n_o, n_i)
     loc_do = _dev.empty_u64(n_o, n_i)
@@ -641,12 +662,23 @@ def grad_weight(sess: Session, layer: int, x_a: ShareTensor, x_b: ShareTensor, g
         if loc_mo is not s:  # MO: s + gY_0 X_0^T
             aux.run(lambda: _ring_matmul(gy_mo.value.values, x_mo.value.values, n_o, B, n_i, ring.ell, tb=True,
                                          c=s, sign=1, out=loc_mo))
-        sess.he_matmul(layer, OP_GRAD_W, g, cross_do, s,
-                       v_ct=None if mo_gy_zero else x_do.value.values, v_strides=(1, B),
-                       w_pt=None if mo_gy_zero else gy_mo.value.values,
-                       w_ct=None if mo_x_zero else gy_do.value.values,
-                       v_pt=None if mo_x_zero else x_mo.value.values,
-                       msg_in=MSG_GRADW, msg_out=MSG_GRADW)
+        # grad W^T = X gY^T: W-role X (n_i x B), v-role gY^T through strides (1, B),
+        # output written transposed (y strides (1, n_i)).  The gradient sits on the
+        # packing side with fewer polynomials (e.g. 16 instead of 64 ciphertexts +
+        # plaintexts for 128x128), the forward-only X side is prepared ahead.
+        # Cross terms: Enc(gY_1) (x) X_0 (term A) and Enc(X_1) (x) gY_0 (term B).
+        flip = grad_w_flipped(mo_x_zero, mo_gy_zero)
+        g, vs, ys = grad_w_geometry(n_o, n_i, B, flip)
+        xd = None if mo_gy_zero else x_do.value.values  # cross term gY_0 X_1^T
+        gm = None if mo_gy_zero else gy_mo.value.values
+        gd = None if mo_x_zero else gy_do.value.values  # cross term gY_1 X_0^T
+        xm = None if mo_x_zero else x_mo.value.values
+        if flip:  # term A: Enc(gY_1) (x) X_0, term B: Enc(X_1) (x) gY_0
+            sess.he_matmul(layer, OP_GRAD_W, g, cross_do, s, v_ct=gd, v_strides=vs, w_pt=xm, w_ct=xd, v_pt=gm,
+                           y_strides=ys, msg_in=MSG_GRADW, msg_out=MSG_GRADW)
+        else:  # term A: Enc(X_1) (x) gY_0, term B: Enc(gY_1) (x) X_0
+            sess.he_matmul(layer, OP_GRAD_W, g, cross_do, s, v_ct=xd, v_strides=vs, w_pt=gm, w_ct=gd, v_pt=xm,
+                           y_strides=ys, msg_in=MSG_GRADW, msg_out=MSG_GRADW)
     # DO: + local term gY_1 X_1^T (+ e), sends the masked sum
     msg = _ring_bin(_lib.RING_ADD, cross_do, loc_do, ring.ell)
     if e is not None:

@@ -23,8 +23,8 @@ import torch
 from . import _dev, _lib
 from .errors import EncodeRangeError, ShapeError
 from .linear_protocols import (OP_BWD_X, OP_FWD, OP_GRAD_W, Session, conv_backward_input, conv_forward,
-                               conv_grad_weight, grad_weight, linear_backward_input, linear_forward, reveal_grad_bias,
-                               reveal_grad_bias_conv)
+                               conv_grad_weight, grad_w_flipped, grad_w_geometry, grad_weight, linear_backward_input,
+                               linear_forward, reveal_grad_bias, reveal_grad_bias_conv)
 from . import preprocessing as PP
 from .nonlinear import (avgpool_backward, avgpool_forward, relu_backward, relu_forward, relu_truncate, truncate,
                         truncate_relu_backward)
@@ -425,11 +425,13 @@ def prepare_backward(sess: Session, model: Model, state, prep=None, layers=None,
         if l > 0:  # linear_backward_input: W^T through strides (1, n_i)
             plan = plan_matmul(MatmulGeometry(n_o, n_i, B), N, None, (1, n_i), None)
             prepare(l, OP_BWD_X, plan, "A_pt", model.W[l].values)
-        plan = plan_matmul(MatmulGeometry(B, n_o, n_i), N, (1, B), None, None)  # grad_weight
-        if l < L - 1:  # term A: Enc(X_1) (x) gY_0
-            prepare(l, OP_GRAD_W, plan, "A_ct", x_do.value.values)
-        if l > 0:  # term B: Enc(gY_1) (x) X_0
-            prepare(l, OP_GRAD_W, plan, "B_pt", x_mo.value.values)
+        flip = grad_w_flipped(l == 0, l == L - 1)  # grad_weight's orientation and plan
+        g, vs, ys = grad_w_geometry(n_o, n_i, B, flip)
+        plan = plan_matmul(g, N, vs, None, ys)
+        if l < L - 1:  # Enc(X_1) (x) gY_0: term B flipped, term A otherwise
+            prepare(l, OP_GRAD_W, plan, "B_ct" if flip else "A_ct", x_do.value.values)
+        if l > 0:  # Enc(gY_1) (x) X_0: X_0 is term A's plaintext flipped, term B's otherwise
+            prepare(l, OP_GRAD_W, plan, "A_pt" if flip else "B_pt", x_mo.value.values)
     if not events:  # ordered by a stream join instead of events: join every fork now
         sess.join_side()
 
