@@ -114,7 +114,7 @@ def model_step(name, steps, cpu, prep_m=0):
     per = {}
     for nm, s, e, _ in stats.events:
         per[nm] = per.get(nm, 0.0) + s.elapsed_time(e)
-    runner = PN.GraphStep(sess, model, x, prep=prep)
+    runner = PN.GraphStep(sess, model, x, prep=prep, prefetch_input=prep is None)  # as bench.py
     ms = time_steps(lambda i: runner.step(SEED + 100 + i, labels), steps, flush=flush)
     out = {"config": name + (f"+prep(m={prep_m})" if prep_m else ""), "batch": B, "ms_per_step": ms, "samples_per_s": B / (ms / 1e3),
            "eager_wall_ms": eager_s * 1e3, "launches_per_step": stats.launches,
