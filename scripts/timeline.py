@@ -39,7 +39,7 @@ def main(name="mnist_mlp", B=64, steps=3):
     else:
         xh, labels = PN.synthetic_images(1, B, model.in_shape, ring)
     x = RingTensor(encode_fixed(xh, ring), ring.f, ring, _canonical=True)
-    r = PN.GraphStep(sess, model, x)
+    r = PN.GraphStep(sess, model, x, prefetch_input=os.environ.get("PB_PREFETCH_INPUT", "1") == "1")
     for i in range(5):
         r.step(100 + i, labels)
     torch.cuda.synchronize()
@@ -68,7 +68,9 @@ def main(name="mnist_mlp", B=64, steps=3):
             gaps.append((b["ts"] - end, b["ts"]))
     big = sorted(gaps, reverse=True)[: 2 * steps - 1]
     cuts = sorted(t for _, t in big)
-    last_start = cuts[-2] if len(cuts) >= 2 else t0  # start of the last step's forward
+    # start of the last step's backward (cuts[-2]) or, with PB_TIMELINE_FULL=1, its forward (cuts[-3])
+    back = 3 if os.environ.get("PB_TIMELINE_FULL") == "1" else 2
+    last_start = cuts[-back] if len(cuts) >= back else t0
     step_ks = [k for k in ks if k["ts"] >= last_start]
     s0 = step_ks[0]["ts"]
     s1 = max(k["ts"] + k["dur"] for k in step_ks)
