@@ -219,10 +219,28 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
   extern __shared__ uint32_t sm[];
   const int tid = threadIdx.x;
   const int L = P.L;
-  for (int64_t row = blockIdx.x; row < nP * L; row += gridDim.x) {  // one row per CTA unless capped
-  if (row != blockIdx.x) __syncthreads();  // shared memory of the previous row is free
-  const int l = (int)(row / nP);  // limb-major: co-resident CTAs share one limb's twiddles
-  const int64_t p = row % nP;
+  const int64_t rows = nP * L;
+  // Rows per CTA: 1 (one row per CTA, limb-major so co-resident CTAs share one
+  // limb's twiddles), or R > 1 under a launch cap: then a CTA takes R
+  // consecutive rows in polynomial-major order and draws each polynomial's
+  // noise once, packed int8 in shared memory past the NTT's area, for all of
+  // its limbs (the noise is the same integer polynomial in every limb).
+  const int64_t R = (rows + gridDim.x - 1) / gridDim.x;
+  uint32_t* e_sm = sm + Nt::SMEM_WORDS;  // [8][T] words: word k of thread tid holds its coefficients 4k..4k+3
+  int64_t noise_p = -1;
+  for (int64_t it = 0; it < R; ++it) {
+  int l;
+  int64_t p;
+  if (R == 1) {
+    l = (int)(blockIdx.x / nP);
+    p = blockIdx.x % nP;
+  } else {
+    const int64_t row = blockIdx.x * R + it;
+    if (row >= rows) break;
+    p = row / L;
+    l = (int)(row - p * L);
+    if (it) __syncthreads();  // shared memory of the previous row is free
+  }
   const uint32_t q = P.q[l];
   const uint64_t mu = P.mu[l];
   const int8_t* ep = e ? e + p * N : nullptr;
@@ -231,7 +249,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
   if (ep) {  // caller-supplied noise (bit-exact oracle runs)
 #pragma unroll
     for (int c = 0; c < 32; ++c) b[c] = addmod(lift_small(ep[Nt::j1(tid, c)], q), b[c], q);
-  } else {  // e ~ CBD(20) from Philox4x32, generated in-kernel: one call covers three of this thread's coefficients
+  } else if (R == 1) {  // e ~ CBD(20) from Philox4x32, generated in-kernel: one call covers three of this thread's coefficients
     const uint64_t pp = (uint64_t)p + nonce;
 #pragma unroll
     for (int g = 0; g < 11; ++g) {
@@ -242,6 +260,33 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
 #pragma unroll
       for (int i = 0; i < 3; ++i)
         if (3 * g + i < 32) b[3 * g + i] = addmod(lift_small(sv[i], q), b[3 * g + i], q);
+    }
+  } else {  // the same draw, once per polynomial (thread-private words: no barrier)
+    if (p != noise_p) {
+      noise_p = p;
+      const uint64_t pp = (uint64_t)p + nonce;
+      uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int g = 0; g < 11; ++g) {
+        const u32x4 r = philox4x32_10(((uint32_t)tid << 4) | (uint32_t)g, (uint32_t)pp, (uint32_t)(pp >> 32),
+                                      0x454e4335u /* "ENC5" */, (uint32_t)seed, (uint32_t)(seed >> 32));
+        int sv[3];
+        cbd20x3(r, sv);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const int c = 3 * g + i;
+          if (c < 32) w[c >> 2] |= ((uint32_t)sv[i] & 0xFFu) << (8 * (c & 3));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) e_sm[k * Nt::T + tid] = w[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t w = e_sm[k * Nt::T + tid];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        b[4 * k + i] = addmod(lift_small((int)(w << (24 - 8 * i)) >> 24, q), b[4 * k + i], q);
     }
   }
   Nt::forward(b, sm, P.tw_fwd + (size_t)l * N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
@@ -673,10 +718,10 @@ template <int LOGN>
 void launch_encrypt_sk(const PbDev& P, const uint32_t* sk, PbPack src, int64_t nP, const uint32_t* a_in, const int8_t* e,
                        uint64_t seed, const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct, cudaStream_t st) {
   using Nt = pb::Ntt<LOGN>;
-  const size_t smem = Nt::SMEM_WORDS * 4;
-  set_smem(k_encrypt_sk<LOGN>, smem);
-  k_encrypt_sk<LOGN><<<(unsigned)pb_row_grid(nP * P.L), Nt::T, smem, st>>>(P, sk, src, nP, a_in, e, seed, seed_dev,
-                                                                           nonce, ct);
+  const int64_t grid = pb_row_grid(nP * P.L);
+  const size_t smem = Nt::SMEM_WORDS * 4 + (grid < nP * P.L ? Nt::N : 0);  // + packed noise when capped
+  set_smem(k_encrypt_sk<LOGN>, Nt::SMEM_WORDS * 4 + Nt::N);
+  k_encrypt_sk<LOGN><<<(unsigned)grid, Nt::T, smem, st>>>(P, sk, src, nP, a_in, e, seed, seed_dev, nonce, ct);
 }
 
 template <int LOGN>

@@ -196,3 +196,25 @@ def test_decrypt_to_share_gather(setup):
         for u in range(U):
             want = 0 if pos[p, u] < 0 else m[p, pos[p, u]]
             assert got[p, u] == want
+
+
+def test_encrypt_sk_launch_cap(setup):
+    """Under a launch cap (background preparation) pb_encrypt_sk's CTAs take
+    consecutive polynomial-major rows and draw each polynomial's noise once
+    for all limbs: the ciphertext is bit-identical to the uncapped one."""
+    from paper_2403_11166_b200 import _dev, _lib, bfv, ring
+
+    s = setup
+    N, P = s["N"], 5
+    kp = s["pkp"]
+    m = OR.SeededRng(12, 4).uniform_ring((P, N), OR.RingParams())
+    md = _dev.u64_to_device(m)
+    ref = _dev.to_numpy_u32(bfv.encrypt(kp, md, ring.SeededRng(14, 0), mode="sk", nonce=5).data)
+    for cap in (1, 3, 8, 34):
+        _lib.call("pb_set_launch_cap", cap)
+        try:
+            got = bfv.encrypt(kp, md, ring.SeededRng(14, 0), mode="sk", nonce=5)
+        finally:
+            _lib.call("pb_set_launch_cap", 0)
+        assert np.array_equal(_dev.to_numpy_u32(got.data), ref), cap
+    assert np.array_equal(_dev.to_numpy_u64(bfv.decrypt(kp, got)), m)
