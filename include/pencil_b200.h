@@ -354,6 +354,18 @@ int pb_set_launch_cap(int32_t max_ctas);
 /* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream). */
 int pb_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
 
+/* Host -> device handoff inside a CUDA graph launched ahead of the host:
+ * one CTA waits until the pinned host word flag_host[0] equals *seq_dev + 1
+ * (system-scope acquire), stores that into *seq_dev, acks it into
+ * flag_host[1] and copies n u64 from pinned host memory src_host to dst.
+ * The host releases the k-th replay by writing src then flag_host[0] = k.
+ * After timeout_ns the kernel gives up, acks (and sets *seq_dev to)
+ * UINT32_MAX and copies whatever src holds (the caller checks the ack).
+ * Replaces the loss-gradient H2D copy + graph launch between the DO's host
+ * loss and the backward pass. */
+int pb_host_handoff(uint32_t* flag_host, uint32_t* seq_dev, const uint64_t* src_host, uint64_t* dst,
+                    int64_t n, int64_t timeout_ns, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

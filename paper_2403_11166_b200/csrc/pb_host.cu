@@ -93,3 +93,70 @@ extern "C" int pb_copy_async(void* dst, const void* src, int64_t bytes, void* st
   return cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream) == cudaSuccess ? PB_OK
                                                                                                          : PB_ERR_CUDA;
 }
+
+// --------------------------------------------------------- host handoff ---
+// The backward graph is launched before the host has the loss gradient; its
+// first kernel waits for it here.  Thread 0 polls a pinned host word (mapped:
+// unified addressing) with system-scope acquire loads until it equals the
+// device step counter + 1, then the CTA copies the gradient from pinned host
+// memory with uncached system-scope loads.  The counter advances every
+// replay, so the host releases step k by storing k; the kernel acks into the
+// next host word.  After timeout_ns without the value it acks UINT32_MAX,
+// poisons *seq (no later handoff matches) and proceeds: a host that dies
+// between launch and release cannot wedge the GPU, and the host sees the
+// failed ack.
+namespace {
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(1024) k_host_handoff(uint32_t* flag, uint32_t* seq, const uint64_t* src,
+                                                      uint64_t* dst, int64_t n, int64_t timeout_ns) {
+  if (threadIdx.x == 0) {
+    const uint32_t want = *seq + 1;
+    const uint64_t t0 = global_ns();
+    uint32_t got;
+    while ((got = ld_acquire_sys(flag)) != want) {
+      if ((int64_t)(global_ns() - t0) > timeout_ns) break;
+      __nanosleep(100);
+    }
+    const uint32_t res = got == want ? want : 0xFFFFFFFFu;
+    *seq = res;
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(flag + 1), "r"(res) : "memory");  // the ack word
+  }
+  __syncthreads();
+  // every load issued before any store: one PCIe round trip for n <= 4 * blockDim
+  uint64_t v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t i = threadIdx.x + (int64_t)k * blockDim.x;
+    v[k] = i < n ? ld_relaxed_sys(src + i) : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t i = threadIdx.x + (int64_t)k * blockDim.x;
+    if (i < n) dst[i] = v[k];
+  }
+  for (int64_t i = threadIdx.x + 4 * (int64_t)blockDim.x; i < n; i += blockDim.x) dst[i] = ld_relaxed_sys(src + i);
+}
+}  // namespace
+
+extern "C" int pb_host_handoff(uint32_t* flag_host, uint32_t* seq_dev, const uint64_t* src_host, uint64_t* dst,
+                               int64_t n, int64_t timeout_ns, void* stream) {
+  if (!flag_host || !seq_dev || n < 0 || (n && (!src_host || !dst)) || timeout_ns < 0) return PB_ERR_ARG;
+  const int threads = (int)(n >= 4096 ? 1024 : n <= 128 ? 32 : ((n + 127) / 128) * 32);
+  k_host_handoff<<<1, threads, 0, (cudaStream_t)stream>>>(flag_host, seq_dev, src_host, dst, n, timeout_ns);
+  return cudaPeekAtLastError() == cudaSuccess ? PB_OK : PB_ERR_CUDA;
+}

@@ -266,19 +266,28 @@ def _forward_layers(sess, model, prep, cur, acts, ds, ys, seg):
 
 
 def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e-2, momentum=0.8, trace=None,
-                   check=True, prep=None, pre_layers=None):
+                   check=True, prep=None, pre_layers=None, on_start=None, early_layers=None):
     """Private backward pass from the DO's loss gradient share (MO share 0) + SGD at the MO.
     ``pre_layers``: prepare these layers' forward-only operands here, on the
-    prep stream beside the backward chain (the rest were prepared before)."""
+    prep stream beside the backward chain (the rest were prepared before).
+    ``early_layers``: prepare these layers' operands here too, at full width
+    and ahead of ``pre_layers``, ordered by per-operand events.
+    ``on_start``: enqueued on this stream after those forks, before anything
+    that reads ``g_do`` (GraphStep's host handoff)."""
     ring, f = model.ring, model.ring.f
     L = model.n_layers
     seg = model.segments()
     acts, ds, ys = state
-    if pre_layers:
+    if early_layers or pre_layers:
         cur, side = torch.cuda.current_stream(), sess.prep_stream()
         side.wait_stream(cur)
         with torch.cuda.stream(side):
-            prepare_backward(sess, model, state, prep, layers=pre_layers, clear=False, background=True)
+            if early_layers:
+                prepare_backward(sess, model, state, prep, layers=early_layers, clear=False)
+            if pre_layers:
+                prepare_backward(sess, model, state, prep, layers=pre_layers, clear=False, background=True)
+    if on_start is not None:
+        on_start()
     gy_do = ShareTensor(DO, RingTensor(g_do, f, ring, _canonical=True))
     gy_mo = ShareTensor(MO, RingTensor(torch.zeros_like(g_do), f, ring, _canonical=True))
     gws, gbs = [None] * L, [None] * L
@@ -336,7 +345,7 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
                     t_mo, t_do = _unflatten(t_mo, chw), _unflatten(t_do, chw)
                 gy_mo, gy_do = truncate_relu_backward(sess, l - 1, ds[l - 1], t_mo, t_do, f)
     main.wait_stream(gstream)
-    if pre_layers:
+    if early_layers or pre_layers:
         main.wait_stream(sess.prep_stream())  # joins the prep fork (graph capture needs every fork joined)
     sess.join_side()
     del keep
@@ -456,6 +465,8 @@ _LATE_PREP = __import__("os").environ.get("PB_LATE_PREP", "1") == "1"
 _PREFETCH_BG = __import__("os").environ.get("PB_PREFETCH_BG", "1") == "1"
 _SPIN_WAIT = __import__("os").environ.get("PB_SPIN_WAIT", "1") == "1"
 _BX_FIRST = __import__("os").environ.get("PB_BX_FIRST", "1") == "1"
+_HANDOFF = __import__("os").environ.get("PB_HANDOFF", "1") == "1"
+_HANDOFF_TIMEOUT_NS = 30_000_000_000  # a backward waiting this long for the host's loss gives up (ack fails)
 _CHAIN_PRIO = int(__import__("os").environ.get("PB_CHAIN_PRIO", "0"))  # e.g. -2: critical chain at higher priority (measured no gain)
 
 
@@ -535,19 +546,39 @@ class GraphStep:
         # beside its latency-bound first layers, so it does not wait for them
         L = model.n_layers
         late = [0] if L > 1 and _LATE_PREP else []
-        with torch.cuda.graph(self.g_pre, pool=self.g_fwd.pool()):
-            prepare_backward(sess, model, self.state, prep, layers=[l for l in range(L) if l not in late],
-                             events=False)  # ordered by step(): the backward replay waits for this graph
+        early = [l for l in range(L) if l not in late]
+        self.handoff = _HANDOFF
+        if not self.handoff:
+            with torch.cuda.graph(self.g_pre, pool=self.g_fwd.pool()):
+                prepare_backward(sess, model, self.state, prep, layers=early,
+                                 events=False)  # ordered by step(): the backward replay waits for this graph
+        self._g_dev_ptr, self._g_host_ptr = self.g_do.data_ptr(), self.g_host.data_ptr()
+        self._g_bytes = self.g_do.numel() * 8
+        # handoff: the backward graph is launched right behind the forward; its
+        # operand preparation (all layers) runs during the host's loss and its
+        # chain starts with a kernel that waits for the host's release word,
+        # then reads the gradient from pinned memory (no H2D copy and no graph
+        # launch between the host loss and the backward)
+        on_start = None
+        if self.handoff:
+            self._hflag = torch.zeros(2, dtype=torch.int32).pin_memory()  # [release, ack]
+            self._hflag_np = self._hflag.numpy().view(np.uint32)
+            self._hseq_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+            self._hseq = 0
+            n_g = self.g_do.numel()
+
+            def on_start():
+                _lib.call("pb_host_handoff", self._hflag.data_ptr(), self._hseq_dev.data_ptr(), self._g_host_ptr,
+                          self._g_dev_ptr, n_g, _HANDOFF_TIMEOUT_NS, torch.cuda.current_stream().cuda_stream)
         with torch.cuda.graph(self.g_bwd, pool=self.g_fwd.pool(), stream=hp):
             self.grads = backward_phase(sess, model, self.state, self.g_do, lr, momentum, check=False, prep=prep,
-                                        pre_layers=late)
+                                        pre_layers=late, on_start=on_start,
+                                        early_layers=early if self.handoff else None)
         self._pre_stream = torch.cuda.Stream()
         self._ev_fwd = torch.cuda.Event()
         self._ev_ready = torch.cuda.Event()
         self._ev_logits = torch.cuda.Event()
         self._ev_pre = torch.cuda.Event()
-        self._g_dev_ptr, self._g_host_ptr = self.g_do.data_ptr(), self.g_host.data_ptr()
-        self._g_bytes = self.g_do.numel() * 8
         self._loaded_last = False
         torch.cuda.synchronize()
         sess.clear_prepared()
@@ -622,6 +653,24 @@ class GraphStep:
             ev.record()
             self.timing.append((label, ev))
 
+    def _wait_logits(self):
+        if _SPIN_WAIT:  # busy-poll: a blocking sync can sleep past the copy's completion
+            while not self._ev_logits.query():
+                pass
+        else:
+            self._ev_logits.synchronize()
+
+    def _host_loss(self, labels):
+        if self._flag_pending:
+            self._flag_pending = False
+            if int(self._flag_host[0]):
+                from .errors import EncodeRangeError
+
+                limit = float(1 << (self.model.ring.ell - 1)) / float(1 << self.model.ring.f)
+                raise EncodeRangeError(f"|x| must stay below {limit}")
+        loss, _ = self._loss(labels)
+        return loss
+
     def step(self, seed: int, labels):
         self.sess.reseed(seed)
         main = torch.cuda.current_stream()
@@ -634,31 +683,33 @@ class GraphStep:
         self.g_fwd.replay()
         self._ev_fwd.record(main)
         self._mark("fwd")
-        self._pre_stream.wait_stream(main)
-        with torch.cuda.stream(self._pre_stream):  # backward operands, beside the host's loss
-            self.g_pre.replay()
-            self._ev_pre.record()
+        if not self.handoff:
+            self._pre_stream.wait_stream(main)
+            with torch.cuda.stream(self._pre_stream):  # backward operands, beside the host's loss
+                self.g_pre.replay()
+                self._ev_pre.record()
         self.logits_host.copy_(self.logits.values, non_blocking=True)
         self._ev_logits.record(main)
-        if _SPIN_WAIT:  # busy-poll: a blocking sync can sleep past the copy's completion
-            while not self._ev_logits.query():
-                pass
+        if self.handoff:  # the backward goes now; its chain waits on the device for the release below
+            self.g_bwd.replay()
+            self._mark("bwd")
+            self._hseq += 1
+            try:
+                self._wait_logits()
+                if self._hseq > 1 and int(self._hflag_np[1]) != self._hseq - 1:
+                    raise RuntimeError("backward graph: the previous step's loss handoff timed out")
+                loss = self._host_loss(labels)  # g written into g_host
+            finally:  # release the backward even on error (it then computes on a stale g)
+                self._hflag_np[0] = self._hseq & 0xFFFFFFFF
         else:
-            self._ev_logits.synchronize()
-        if self._flag_pending:
-            self._flag_pending = False
-            if int(self._flag_host[0]):
-                from .errors import EncodeRangeError
-
-                limit = float(1 << (self.model.ring.ell - 1)) / float(1 << self.model.ring.f)
-                raise EncodeRangeError(f"|x| must stay below {limit}")
-        loss, _ = self._loss(labels)  # g written into g_host
-        _lib.load().pb_copy_async(self._g_dev_ptr, self._g_host_ptr, self._g_bytes, main.cuda_stream)
-        self._mark("host")
-        main.wait_event(self._ev_pre)
-        self._mark("pre")
-        self.g_bwd.replay()
-        self._mark("bwd")
+            self._wait_logits()
+            loss = self._host_loss(labels)
+            _lib.load().pb_copy_async(self._g_dev_ptr, self._g_host_ptr, self._g_bytes, main.cuda_stream)
+            self._mark("host")
+            main.wait_event(self._ev_pre)
+            self._mark("pre")
+            self.g_bwd.replay()
+            self._mark("bwd")
         if self.prefetch and not self._loaded_last:  # resident input: encrypt it afresh for the next step
             self._copy_stream.wait_event(self._ev_fwd)
             self._schedule_encrypt()
