@@ -363,6 +363,11 @@ int pb_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
  * UINT32_MAX and copies whatever src holds (the caller checks the ack).
  * Replaces the loss-gradient H2D copy + graph launch between the DO's host
  * loss and the backward pass. */
+/* Step prologue for a replayed graph: *dev_word = *host_word (pinned host
+ * memory read by the kernel; host_word NULL: skipped) and a D2D copy of
+ * `bytes` (multiple of 16, 16-byte aligned) from src to dst, one launch. */
+int pb_step_prologue(const uint64_t* host_word, uint64_t* dev_word, const void* src, void* dst, int64_t bytes,
+                     void* stream);
 int pb_host_handoff(uint32_t* flag_host, uint32_t* seq_dev, const uint64_t* src_host, uint64_t* dst,
                     int64_t n, int64_t timeout_ns, void* stream);
 

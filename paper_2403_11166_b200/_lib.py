@@ -85,6 +85,7 @@ SIGNATURES = {
     "pb_set_launch_cap": [I32],
     "pb_copy_async": [P, P, I64, P],
     "pb_host_handoff": [P, P, P, P, I64, I64, P],
+    "pb_step_prologue": [P, P, P, P, I64, P],
     "pb_ring_rowsum": [P, I64, I64, I32, P, P],
     "pb_im2col": [P, I32, I32, I32, I32, I32, I32, P, P],
     "pb_col2im": [P, I32, I32, I32, I32, I32, I32, P, P],

@@ -160,3 +160,30 @@ extern "C" int pb_host_handoff(uint32_t* flag_host, uint32_t* seq_dev, const uin
   k_host_handoff<<<1, threads, 0, (cudaStream_t)stream>>>(flag_host, seq_dev, src_host, dst, n, timeout_ns);
   return cudaPeekAtLastError() == cudaSuccess ? PB_OK : PB_ERR_CUDA;
 }
+
+// --------------------------------------------------------- step prologue ---
+// First kernel of a replayed forward graph: the step's seed word from pinned
+// host memory (one system-scope load; the host wrote it before the launch)
+// into the device word the captured kernels read, plus the D2D copy of the
+// prefetched input into the graph's input buffer -- one launch instead of an
+// H2D copy + a copy kernel between the previous backward and this forward.
+namespace {
+__global__ void __launch_bounds__(256) k_step_prologue(const uint64_t* host_word, uint64_t* dev_word,
+                                                       const uint4* src, uint4* dst, int64_t n16) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && host_word) *dev_word = ld_relaxed_sys(host_word);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+}  // namespace
+
+extern "C" int pb_step_prologue(const uint64_t* host_word, uint64_t* dev_word, const void* src, void* dst,
+                                int64_t bytes, void* stream) {
+  if ((host_word && !dev_word) || bytes < 0 || (bytes & 15) || (bytes && (!src || !dst))) return PB_ERR_ARG;
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) return PB_ERR_ARG;
+  const int64_t n16 = bytes / 16;
+  const int64_t blocks = n16 ? (n16 + 255) / 256 < 148 ? (n16 + 255) / 256 : 148 : 1;
+  k_step_prologue<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(host_word, dev_word,
+                                                                     reinterpret_cast<const uint4*>(src),
+                                                                     reinterpret_cast<uint4*>(dst), n16);
+  return cudaPeekAtLastError() == cudaSuccess ? PB_OK : PB_ERR_CUDA;
+}

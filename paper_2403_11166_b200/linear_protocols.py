@@ -217,14 +217,18 @@ class Session:
         g = SeededRng(self.seed, stream_id(layer, op, purpose))
         return g.bind(self._seed_dev.data_ptr()) if self.graph_mode else g
 
-    def reseed(self, seed: int):
+    def reseed(self, seed: int, device_copy: bool = True):
         """Start a new step: every mask / share / noise stream is re-keyed.
         In graph mode the seed is also written to the device word the
-        captured kernels read (seed indirection, pb_common.cuh)."""
+        captured kernels read (seed indirection, pb_common.cuh); with
+        ``device_copy=False`` only to the pinned host word (a replayed graph
+        copies it itself: pb_step_prologue)."""
         self.seed = int(seed)
         self.steps_seen += 1
         if self._seed_dev is not None:
             self._seed_host[0] = self.seed
+            if not device_copy:
+                return
             self._seed_dev.copy_(self._seed_host, non_blocking=True)
 
     def enable_graph_mode(self):

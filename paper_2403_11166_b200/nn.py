@@ -466,6 +466,7 @@ _PREFETCH_BG = __import__("os").environ.get("PB_PREFETCH_BG", "1") == "1"
 _SPIN_WAIT = __import__("os").environ.get("PB_SPIN_WAIT", "1") == "1"
 _BX_FIRST = __import__("os").environ.get("PB_BX_FIRST", "1") == "1"
 _HANDOFF = __import__("os").environ.get("PB_HANDOFF", "1") == "1"
+_PROLOGUE = __import__("os").environ.get("PB_PROLOGUE", "1") == "1"
 _HANDOFF_TIMEOUT_NS = 30_000_000_000  # a backward waiting this long for the host's loss gives up (ack fails)
 _CHAIN_PRIO = int(__import__("os").environ.get("PB_CHAIN_PRIO", "0"))  # e.g. -2: critical chain at higher priority (measured no gain)
 
@@ -539,7 +540,16 @@ class GraphStep:
         # stream (their forks inherit it); the grad-W chain's stream keeps the
         # default, lower priority, so the block scheduler serves the critical chain first
         hp = torch.cuda.Stream(priority=_CHAIN_PRIO) if _CHAIN_PRIO else None
+        # prologue: the replayed forward graph fetches the step seed from the pinned
+        # host word and copies the prefetched input itself (no H2D copy and copy
+        # kernel ahead of the launch)
+        self.prologue = _PROLOGUE
         with torch.cuda.graph(self.g_fwd, stream=hp):
+            if self.prologue:
+                nbytes = x.values.numel() * 8 if self.prefetch else 0
+                _lib.call("pb_step_prologue", sess._seed_host.data_ptr(), sess._seed_dev.data_ptr(),
+                          self._x_next.data_ptr() if self.prefetch else None, x.values.data_ptr(), nbytes,
+                          torch.cuda.current_stream().cuda_stream)
             self.state, self.logits = forward_phase(sess, model, x, prep)
         # the operands the backward consumes first (layers >= 1) are prepared beside
         # the host's loss step; layer 0's (consumed last) inside the backward graph,
@@ -672,12 +682,13 @@ class GraphStep:
         return loss
 
     def step(self, seed: int, labels):
-        self.sess.reseed(seed)
+        self.sess.reseed(seed, device_copy=not self.prologue)
         main = torch.cuda.current_stream()
         self._mark("start")
         if self.prefetch:
             main.wait_event(self._ev_ready)  # this step's input and its encryption
-            self.x.values.copy_(self._x_next)
+            if not self.prologue:
+                self.x.values.copy_(self._x_next)
         elif self._batch_pending:
             self._encode_batch(main)
         self.g_fwd.replay()
