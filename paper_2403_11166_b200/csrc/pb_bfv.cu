@@ -176,6 +176,8 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
 #pragma unroll
   for (int c = 0; c < 32; ++c) U[c] = lift_small(up[Nt::j1(tid, c)], q);
   Nt::forward(U, sm, tw, t3, tid, q);
+#pragma unroll
+  for (int c = 0; c < 32; ++c) U[c] = pb::canon4(U[c], q);  // mulmod_lt needs operands < q
   __syncthreads();
   // c1 = pk1 * U + NTT(e2)
 #pragma unroll
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   Nt::forward(b, sm, tw, t3, tid, q);
   Nt::gld3(pk + ((size_t)1 * L + l) * N, k, tid);
 #pragma unroll
-  for (int c = 0; c < 32; ++c) b[c] = addmod(mulmod(k[c], U[c], q, mu), pb::canon4(b[c], q), q);
+  for (int c = 0; c < 32; ++c) b[c] = addmod(mulmod_lt(k[c], U[c], q, mu), pb::canon4(b[c], q), q);
   Nt::gst3(ct + ((p * 2 + 1) * L + l) * N, b, tid);
   __syncthreads();
   // c0 = pk0 * U + NTT(e1 + Delta m)
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   Nt::forward(b, sm, tw, t3, tid, q);
   Nt::gld3(pk + (size_t)l * N, k, tid);
 #pragma unroll
-  for (int c = 0; c < 32; ++c) b[c] = addmod(mulmod(k[c], U[c], q, mu), pb::canon4(b[c], q), q);
+  for (int c = 0; c < 32; ++c) b[c] = addmod(mulmod_lt(k[c], U[c], q, mu), pb::canon4(b[c], q), q);
   Nt::gst3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
 }
 
@@ -309,7 +311,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
     const uint32_t sk_[4] = {sv.x, sv.y, sv.z, sv.w};
     uint32_t o[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) o[k] = submod(pb::canon4(b[4 * v + k], q), mulmod(a[k], sk_[k], q, mu), q);
+    for (int k = 0; k < 4; ++k) o[k] = submod(pb::canon4(b[4 * v + k], q), mulmod_lt(a[k], sk_[k], q, mu), q);
     c0[v * Nt::T] = make_uint4(o[0], o[1], o[2], o[3]);
     c1[v * Nt::T] = make_uint4(a[0], a[1], a[2], a[3]);
   }
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(256) k_encrypt_pre(PbDev P, const uint32_t* sk
   const uint32_t sk_[4] = {sv.x, sv.y, sv.z, sv.w};
   uint32_t o[4];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) o[c] = submod(0u, mulmod(a[c], sk_[c], q, mu), q);
+  for (int c = 0; c < 4; ++c) o[c] = submod(0u, mulmod_lt(a[c], sk_[c], q, mu), q);
   reinterpret_cast<uint4*>(ct + ((p * 2 + 0) * L + l) * N)[k] = make_uint4(o[0], o[1], o[2], o[3]);
   reinterpret_cast<uint4*>(ct + ((p * 2 + 1) * L + l) * N)[k] = make_uint4(a[0], a[1], a[2], a[3]);
   if (l == 0 && k < (N + 11) / 12) {  // e ~ CBD(20), once per polynomial: coefficients 12k .. 12k+11
@@ -459,7 +461,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   Nt::gld3(ct + ((p * 2 + 1) * L + l) * N, a, tid);
   Nt::gld3(sk + (size_t)l * N, b, tid);
 #pragma unroll
-  for (int c = 0; c < 32; ++c) a[c] = mulmod(a[c], b[c], q, mu);
+  for (int c = 0; c < 32; ++c) a[c] = mulmod_lt(a[c], b[c], q, mu);
   Nt::gld3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = addmod(a[c], b[c], q);
@@ -559,7 +561,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   Nt::gld3(ct + ((p * 2 + 1) * L + l) * N, a, tid);
   Nt::gld3(sk + (size_t)l * N, b, tid);
 #pragma unroll
-  for (int c = 0; c < 32; ++c) a[c] = mulmod(a[c], b[c], q, mu);
+  for (int c = 0; c < 32; ++c) a[c] = mulmod_lt(a[c], b[c], q, mu);
   Nt::gld3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = addmod(a[c], b[c], q);

@@ -121,6 +121,21 @@ __device__ __forceinline__ uint32_t mulmod(uint32_t a, uint32_t b, uint32_t q, u
   return reduce64((uint64_t)a * b, q, mu);
 }
 
+// a*b mod q for a, b < q (so ab < 2^2k, k = bit length of q <= 30): Barrett
+// with 32-bit operands -- floor(2^2k / q) is a shift of mu = floor(2^64 / q)
+// (both hoisted out of loops over one limb) -- two IMAD.WIDE instead of the
+// 64x64-bit high product of reduce64.  Result == mulmod(a, b, q, mu).
+__device__ __forceinline__ uint32_t mulmod_lt(uint32_t a, uint32_t b, uint32_t q, uint64_t mu) {
+  const int k = 32 - __clz(q);
+  const uint32_t m = (uint32_t)(mu >> (64 - 2 * k));  // < 2^(k+1)
+  const uint64_t x = (uint64_t)a * b;
+  const uint32_t b1 = (uint32_t)(x >> (k - 1));       // < 2^(k+1)
+  const uint32_t qh = (uint32_t)(((uint64_t)b1 * m) >> (k + 1));
+  uint32_t r = (uint32_t)x - qh * q;                  // [0, 3q): floor(ab/q) - qh in {0,1,2}
+  r = min(r, r - q);
+  return min(r, r - q);
+}
+
 __device__ __forceinline__ uint32_t addmod(uint32_t a, uint32_t b, uint32_t q) {  // a,b < q
   return csub(a + b, q);
 }
