@@ -686,8 +686,15 @@ extern "C" int pb_ctpt_mac_tiled(const pb_ctx* ctx, const uint32_t* ctA, const u
       const char* e = getenv("PB_MAC_VARIANT");
       return e ? atoi(e) : 0;
     }();
+    // Tiles: 2x2, except large two-term evaluations (Alg. 2 cross terms, twice
+    // the staged operands per k-step): 1x2, CIFAR conv grad-W 1148 -> 1106 us
+    // (profiles/r01_mac_ws_sweep.txt).  The MLP's small two-term grad-W keeps
+    // 2x2: 1x2 is 4% faster alone but its extra CTAs crowd the concurrent
+    // input-gradient chain (step A/B).  PB_MAC_VARIANT=2: 2x2 always.
     if (variant == 1)
       launch_pipe<2, 2, 4, 3, 6>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
+    else if (ctA && ctB && (int64_t)nB * nO * nI >= 1024 && variant != 2)
+      launch_ws<1, 2, 4, 4, 4>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
     else
       launch_ws<2, 2, 4, 4, 4>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
   }
