@@ -1,8 +1,11 @@
 """Where the private step's time goes (graph replay through GraphStep.step,
-prefetched input encryption as in bench.py): forward graph, host loss
-round trip (logits D2H, float64 softmax-CE, gradient H2D), the wait for the
-backward-operand preparation, backward graph -- CUDA events at the phase
-boundaries (GraphStep.timing), with and without an L2 flush before the step."""
+prefetched input encryption as in bench.py) -- CUDA events at the phase
+boundaries (GraphStep.timing), with and without an L2 flush before the step.
+With the device-side host handoff (default, PB_HANDOFF=1) the phases are the
+forward graph and the backward graph, whose chain waits on the device for the
+host's float64 softmax-CE (so "bwd" includes the host loss); with
+PB_HANDOFF=0 also the host round trip ("host": logits D2H, loss, gradient
+H2D) and the wait for the separately replayed operand-preparation graph ("pre")."""
 import json
 import os
 import sys
