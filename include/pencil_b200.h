@@ -371,6 +371,29 @@ int pb_step_prologue(const uint64_t* host_word, uint64_t* dev_word, const void* 
 int pb_host_handoff(uint32_t* flag_host, uint32_t* seq_dev, const uint64_t* src_host, uint64_t* dst,
                     int64_t n, int64_t timeout_ns, void* stream);
 
+/* PBFV wire format (the serialize boundary of SPEC:194 and the
+ * frame payload whose size the census counts).  One frame per
+ * object: {magic "PBFV", version u16 = PB_WIRE_VERSION, N u32, L u8, form u8}
+ * (12 bytes, packed little-endian) then n_polys (2: ciphertext c0, c1; 1:
+ * plaintext) x L x N little-endian u64 residues.  form PB_WIRE_NTT rows are
+ * in the reference's bit-reversed NTT order (K:ntt_forward), converted from
+ * the device order inside the kernel; PB_WIRE_COEFF rows are written as
+ * given (the caller passes coefficient-form rows).  `out` / `in` may be
+ * device memory or pinned host memory (UVA: the kernel then does the
+ * transfer itself); 4-byte aligned; polys 16-byte aligned.
+ * pb_wire_deserialize zeroes *bad (device int32) and ORs PB_WIRE_BAD_* into
+ * it; the caller reads it after the stream and raises (HandshakeError-class
+ * header faults, ParamsError, FormError, EncodeRangeError). */
+#define PB_WIRE_VERSION 1
+enum { PB_WIRE_COEFF = 0, PB_WIRE_NTT = 1 };
+enum { PB_WIRE_BAD_HEADER = 1, PB_WIRE_BAD_PARAMS = 2, PB_WIRE_BAD_FORM = 4, PB_WIRE_BAD_RESIDUE = 8 };
+#define PB_WIRE_FRAME_SIZE(N, L, n_polys) (12 + (int64_t)(n_polys) * (L) * (N) * 8)
+int pb_wire_frame_bytes(const pb_ctx* ctx, int32_t n_polys, int64_t* out_host);
+int pb_wire_serialize(const pb_ctx* ctx, const uint32_t* polys, int64_t P, int32_t n_polys, int32_t form,
+                      uint8_t* out, void* stream);
+int pb_wire_deserialize(const pb_ctx* ctx, const uint8_t* in, int64_t P, int32_t n_polys, int32_t form,
+                        uint32_t* polys, int32_t* bad, void* stream);
+
 #ifdef __cplusplus
 }
 #endif
