@@ -371,6 +371,16 @@ int pb_step_prologue(const uint64_t* host_word, uint64_t* dev_word, const void* 
 int pb_host_handoff(uint32_t* flag_host, uint32_t* seq_dev, const uint64_t* src_host, uint64_t* dst,
                     int64_t n, int64_t timeout_ns, void* stream);
 
+/* SPEC:196 response compaction (modulus switch, OFF by default): ct rows
+ * [n_polys][L][N] (NTT form, device order) under Q = q_0..q_{L-1} ->
+ * out [n_polys][L-1][N] under Q' = Q / q_{L-1}, c' = round(c Q'/Q), i.e.
+ * c'_i = (c_i - [c]_{q_{L-1}}) q_{L-1}^-1 mod q_i with the centered
+ * coefficient-form residue of the dropped limb.  ctx_low: the context of
+ * q_0..q_{L-2}; ctx_last: the 1-limb context of q_{L-1}; scratch [n_polys][N].
+ * Decrypt the result under ctx_low with the first L-1 key rows. */
+int pb_mod_switch_drop(const pb_ctx* ctx_low, const pb_ctx* ctx_last, const uint32_t* ct, int64_t n_polys,
+                       uint32_t* out, uint32_t* scratch, void* stream);
+
 /* PBFV wire format (the serialize boundary of SPEC:194 and the
  * frame payload whose size the census counts).  One frame per
  * object: {magic "PBFV", version u16 = PB_WIRE_VERSION, N u32, L u8, form u8}

@@ -259,3 +259,29 @@ def noise_budget(p: OracleBfvParams, kp: KeyPair, ct, ar: Arith) -> int:  # SPEC
     if worst == 0:
         return int(math.log2(Q)) - 1
     return max(0, int(math.floor(math.log2(Q) - math.log2(worst) - 1)))
+
+
+def mod_switch_drop(p: OracleBfvParams, ct):
+    """SPEC:196 response compaction (OFF by default; the reference ships no
+    implementation, so this restates the textbook BFV modulus switch):
+    ct (P, 2, L, N) NTT form, reference order -> (params', ct') under
+    Q' = Q / q_{L-1}, c'_i = (c_i - [c]_{q_{L-1}}) * q_{L-1}^-1 mod q_i with the
+    centered coefficient-form residue of the dropped limb."""
+    from .params import make_params
+
+    ct = np.asarray(ct, dtype=np.uint64)
+    P, _, L, N = ct.shape
+    q_last = int(p.moduli[-1])
+    lo = make_params(N, ell=p.ell, moduli=p.moduli[:-1])
+    last = make_params(N, ell=p.ell, moduli=(q_last,))
+    a = ct[:, :, L - 1, :].reshape(P * 2, 1, N).copy()
+    Arith(last).ntt_inv(a)
+    a = a.reshape(P * 2, N).astype(np.int64)
+    ac = np.where(a > q_last // 2, a - q_last, a)
+    x = np.stack([np.mod(ac, q) for q in lo.moduli], axis=1).astype(np.uint64)
+    Arith(lo).ntt_fwd(x)
+    qv = np.array(lo.moduli, dtype=np.uint64)[None, :, None]
+    inv = np.array([pow(q_last, -1, int(q)) for q in lo.moduli], dtype=np.uint64)[None, :, None]
+    c = ct[:, :, : L - 1, :].reshape(P * 2, L - 1, N)
+    out = ((c + qv - x) % qv) * inv % qv
+    return lo, out.reshape(P, 2, L - 1, N)

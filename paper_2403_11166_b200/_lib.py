@@ -87,6 +87,7 @@ SIGNATURES = {
     "pb_host_handoff": [P, P, P, P, I64, I64, P],
     "pb_step_prologue": [P, P, P, P, I64, P],
     "pb_wire_frame_bytes": [P, I32, P],
+    "pb_mod_switch_drop": [P, P, P, I64, P, P, P],
     "pb_wire_serialize": [P, P, I64, I32, I32, P, P],
     "pb_wire_deserialize": [P, P, I64, I32, I32, P, P, P],
     "pb_ring_rowsum": [P, I64, I64, I32, P, P],

@@ -321,3 +321,30 @@ def noise_budget(kp: KeyPair, ct: Ciphertext, slots=None) -> int:
     if worst == 0:
         return int(math.log2(Q)) - 1
     return max(0, int(math.floor(math.log2(Q) - math.log2(worst) - 1)))
+
+
+def drop_params(params: BfvParams) -> BfvParams:
+    """The parameter set after one modulus switch: q_0..q_{L-2}."""
+    if params.L < 2:
+        raise ParamsError("modulus switching needs at least 2 limbs")
+    return BfvParams(N=params.N, ell=params.ell, moduli=params.moduli[:-1])
+
+
+def drop_keys(kp: KeyPair) -> KeyPair:
+    """The key pair restricted to q_0..q_{L-2} (the NTT rows of the kept limbs)."""
+    p = drop_params(kp.params)
+    return KeyPair(p, kp.sk_coeff, kp.sk_ntt[: p.L].contiguous(), kp.pk[:, : p.L].contiguous())
+
+
+def mod_switch_drop(ct: Ciphertext) -> Ciphertext:  # SPEC:196
+    """Response compaction: drop the last RNS limb, c' = round(c * Q'/Q).
+    Decrypts under ``drop_keys(kp)`` to the same plaintext; wire bytes
+    shrink by 1/L.  OFF by default in the protocols, as SPEC:196 says."""
+    p = ct.params
+    lo = drop_params(p)
+    last = BfvParams(N=p.N, ell=p.ell, moduli=p.moduli[-1:])
+    out = _dev.empty_u32(ct.count, 2, lo.L, p.N)
+    scratch = _dev.empty_u32(ct.count * 2, p.N)
+    _lib.call("pb_mod_switch_drop", _ctx(lo), _ctx(last), _dev.ptr(ct.data.contiguous()), 2 * ct.count,
+              _dev.ptr(out), _dev.ptr(scratch), _dev.stream())
+    return Ciphertext(out, lo)

@@ -99,6 +99,14 @@ def main(Ps):
                 line.update(frac_hbm=gbs / pk, peak_kind=kind)
             print(json.dumps(line), flush=True)
         assert torch.equal(back, ct.data) and int(bad.item()) == 0
+        # SPEC:196 response compaction on the same ciphertexts: L rows read, L-1 written per polynomial
+        ms = timed(lambda: bfv.mod_switch_drop(ct))
+        alg = P * 2 * pp.N * 4 * (2 * pp.L - 1)
+        print(json.dumps({"kernel": "mod_switch_drop", "N": pp.N, "L": pp.L, "ciphertexts": P, "ms": ms,
+                          "alg_GB_s": alg / (ms * 1e-3) / 1e9, "frac_hbm": alg / (ms * 1e-3) / 1e9 / pk,
+                          "peak_kind": kind, "ct_per_s": P / (ms * 1e-3),
+                          "note": "memcpy2D + 1-limb INTT + lift + (L-1)-limb NTT + finish; includes allocation"}),
+              flush=True)
 
 
 if __name__ == "__main__":
