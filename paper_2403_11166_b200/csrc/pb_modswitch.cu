@@ -12,21 +12,29 @@
 
 namespace {
 
-// x[p][i][n] = centered(a[p][n]) mod q_i, a in [0, q_last).
-__global__ void k_ms_lift(PbDev P, const uint32_t* __restrict__ a, uint32_t q_last, int64_t n_polys,
-                          uint32_t* __restrict__ x) {
-  const int N = P.N, L = P.L;
-  const int64_t total = n_polys * (int64_t)N;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = g / N;
-    const int n = (int)(g - p * N);
-    const uint32_t v = a[g];
-    const bool neg = v > (q_last >> 1);
-    const uint32_t mag = neg ? q_last - v : v;  // |centered value| < q_last / 2
-    for (int i = 0; i < L; ++i) {
-      const uint32_t q = P.q[i];
-      const uint32_t r = mag >= q ? mag % q : mag;
-      x[(p * L + i) * N + n] = (neg && r) ? q - r : r;
+// x[p][i][n] = centered(a[p][n]) mod q_i, a in [0, q_last).  One CTA per
+// polynomial (grid-stride), 16-byte loads and stores.
+__device__ __forceinline__ uint32_t ms_center(uint32_t v, uint32_t q_last, uint32_t q) {
+  const bool neg = v > (q_last >> 1);
+  const uint32_t mag = neg ? q_last - v : v;  // |centered value| < q_last / 2
+  const uint32_t r = mag >= q ? mag % q : mag;
+  return (neg && r) ? q - r : r;
+}
+
+__global__ void __launch_bounds__(256) k_ms_lift(PbDev P, const uint32_t* __restrict__ a, uint32_t q_last,
+                                                 int64_t n_polys, uint32_t* __restrict__ x) {
+  const int N4 = P.N >> 2, L = P.L;
+  for (int64_t p = blockIdx.x; p < n_polys; p += gridDim.x) {
+    const uint4* a4 = reinterpret_cast<const uint4*>(a) + p * N4;
+    uint4* x4 = reinterpret_cast<uint4*>(x) + p * L * N4;
+    for (int k = threadIdx.x; k < N4; k += blockDim.x) {
+      const uint4 v = a4[k];
+      for (int i = 0; i < L; ++i) {
+        const uint32_t q = P.q[i];
+        x4[(int64_t)i * N4 + k] =
+            make_uint4(ms_center(v.x, q_last, q), ms_center(v.y, q_last, q), ms_center(v.z, q_last, q),
+                       ms_center(v.w, q_last, q));
+      }
     }
   }
 }
@@ -44,26 +52,32 @@ struct MsConsts {
   uint32_t qinv[PB_MAXL], qinv_sh[PB_MAXL];
 };
 
-// out[p][i] = (c[p][i] - x[p][i]) * q_last^-1 mod q_i, x (NTT form) in place in out.
-__global__ void k_ms_finish_v(PbDev P, const uint32_t* __restrict__ c, int c_limbs, int64_t n_polys, MsConsts k,
-                              uint32_t* out) {
-  const int N = P.N, L = P.L;
-  const int64_t total = n_polys * (int64_t)L * N;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = g / N;
-    const int n = (int)(g - row * N);
+// out[p][i] = (c[p][i] - x[p][i]) * q_last^-1 mod q_i, x (NTT form) in place
+// in out.  One CTA per output row (grid-stride), 16-byte accesses.
+__device__ __forceinline__ uint32_t ms_fin(uint32_t cv, uint32_t xv, uint32_t w, uint32_t ws, uint32_t q) {
+  return mul_shoup(cv >= xv ? cv - xv : cv + q - xv, w, ws, q);
+}
+
+__global__ void __launch_bounds__(256) k_ms_finish_v(PbDev P, const uint32_t* __restrict__ c, int c_limbs,
+                                                     int64_t n_polys, MsConsts k, uint32_t* out) {
+  const int N4 = P.N >> 2, L = P.L;
+  for (int64_t row = blockIdx.x; row < n_polys * L; row += gridDim.x) {
     const int64_t p = row / L;
     const int i = (int)(row - p * L);
-    const uint32_t q = P.q[i];
-    const uint32_t cv = c[(p * c_limbs + i) * N + n], xv = out[g];
-    const uint32_t d = cv >= xv ? cv - xv : cv + q - xv;
-    out[g] = mul_shoup(d, k.qinv[i], k.qinv_sh[i], q);
+    const uint32_t q = P.q[i], w = k.qinv[i], ws = k.qinv_sh[i];
+    const uint4* c4 = reinterpret_cast<const uint4*>(c) + (p * c_limbs + i) * N4;
+    uint4* o4 = reinterpret_cast<uint4*>(out) + row * N4;
+    for (int j = threadIdx.x; j < N4; j += blockDim.x) {
+      const uint4 cv = c4[j], xv = o4[j];
+      o4[j] = make_uint4(ms_fin(cv.x, xv.x, w, ws, q), ms_fin(cv.y, xv.y, w, ws, q), ms_fin(cv.z, xv.z, w, ws, q),
+                         ms_fin(cv.w, xv.w, w, ws, q));
+    }
   }
 }
 
-int ms_grid(int64_t n) {
-  const int64_t b = (n + 255) / 256, cap = 148 * 16;
-  return (int)(b < 1 ? 1 : (b < cap ? b : cap));
+int ms_rows_grid(int64_t rows) {  // one CTA per row, up to 8 resident per SM
+  const int64_t cap = 148 * 8;
+  return (int)(rows < cap ? rows : cap);
 }
 
 }  // namespace
@@ -76,6 +90,9 @@ extern "C" int pb_mod_switch_drop(const pb_ctx* ctx_low, const pb_ctx* ctx_last,
   if (n_polys < 0) return pb_set_error(PB_ERR_SHAPE, "negative polynomial count");
   if (n_polys == 0) return PB_OK;
   if (!ct || !out || !scratch) return pb_set_error(PB_ERR_ARG, "null argument");
+  if ((reinterpret_cast<uintptr_t>(ct) | reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(scratch)) & 15)
+    return pb_set_error(PB_ERR_ARG, "ct, out and scratch must be 16-byte aligned");
+  if (ctx_low->dev.N < 4) return pb_set_error(PB_ERR_PARAMS, "N >= 4");
   const int N = ctx_low->dev.N, Ll = ctx_low->dev.L, Lc = Ll + 1;
   const uint32_t q_last = ctx_last->dev.q[0];
   for (int i = 0; i < Ll; ++i)
@@ -87,7 +104,7 @@ extern "C" int pb_mod_switch_drop(const pb_ctx* ctx_low, const pb_ctx* ctx_last,
   PB_CHECK_LAUNCH();
   int s = pb_ntt_inverse(ctx_last, scratch, n_polys, nullptr, st);
   if (s) return s;
-  k_ms_lift<<<ms_grid(n_polys * N), 256, 0, st>>>(ctx_low->dev, scratch, q_last, n_polys, out);
+  k_ms_lift<<<ms_rows_grid(n_polys), 256, 0, st>>>(ctx_low->dev, scratch, q_last, n_polys, out);
   PB_CHECK_LAUNCH();
   s = pb_ntt_forward(ctx_low, out, n_polys * Ll, nullptr, st);
   if (s) return s;
@@ -97,7 +114,7 @@ extern "C" int pb_mod_switch_drop(const pb_ctx* ctx_low, const pb_ctx* ctx_last,
     k.qinv[i] = inv_mod(q_last % q, q);
     k.qinv_sh[i] = (uint32_t)(((uint64_t)k.qinv[i] << 32) / q);
   }
-  k_ms_finish_v<<<ms_grid(n_polys * Ll * N), 256, 0, st>>>(ctx_low->dev, ct, Lc, n_polys, k, out);
+  k_ms_finish_v<<<ms_rows_grid(n_polys * Ll), 256, 0, st>>>(ctx_low->dev, ct, Lc, n_polys, k, out);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }
