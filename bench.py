@@ -268,6 +268,8 @@ def run_ours(args, rank, world):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         loss = runner.step(SEED + 1000 + i, labels)
+        if hasattr(runner, "join_prefetch"):
+            runner.join_prefetch()  # the next step's prefetched input encryption is inside this window
         e.record()
         evs.append((s, e))
     torch.cuda.synchronize()
@@ -305,6 +307,8 @@ def run_ours(args, rank, world):
         else:
             x_dev.values.copy_(encode_fixed(x_pin.to(dev, non_blocking=True), ring))
         loss = runner.step(SEED + 2000 + i, labels)
+        if hasattr(runner, "join_prefetch"):
+            runner.join_prefetch()
         e.record()
         evs.append((s, e))
     torch.cuda.synchronize()

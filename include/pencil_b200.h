@@ -330,10 +330,12 @@ int pb_dealer_op_out(int op, const uint64_t* in_mo, const uint64_t* in_do, uint6
                      void* stream);
 
 /* SGD with momentum in float64 + re-quantisation:
- * v = mu*v + g; w = w - lr*v; w_ring = encode_fixed(w, scale). */
+ * v = mu*v + g; w = w - lr*v; w_ring = encode_fixed(w, scale).  skip
+ * (nullable device word): nonzero -> no-op (an aborted step, see
+ * pb_host_handoff). */
 int pb_sgd_momentum(double* w, double* v, const uint64_t* grad_ring, int64_t n, int32_t grad_scale,
                     double lr, double momentum, int32_t ell, int32_t w_scale, uint64_t* w_ring,
-                    int32_t* range_flag, void* stream);
+                    int32_t* range_flag, const uint32_t* skip, void* stream);
 
 /* The DO's host-side softmax cross-entropy around numpy's
  * exp / log: pb_host_softmax_pre writes z = logits/2^f2 (signed, ell bits)
@@ -361,6 +363,10 @@ int pb_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
  * The host releases the k-th replay by writing src then flag_host[0] = k.
  * After timeout_ns the kernel gives up, acks (and sets *seq_dev to)
  * UINT32_MAX and copies whatever src holds (the caller checks the ack).
+ * *skip_dev (nullable) = 1 after a timeout or when the host set the abort
+ * word flag_host[2] before releasing (its loss raised), else 0; every
+ * pb_sgd_momentum of the step reads it and then leaves w, v, w_ring as
+ * they were, so an aborted step never applies a stale gradient.
  * Replaces the loss-gradient H2D copy + graph launch between the DO's host
  * loss and the backward pass. */
 /* Step prologue for a replayed graph: *dev_word = *host_word (pinned host
@@ -369,7 +375,7 @@ int pb_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
 int pb_step_prologue(const uint64_t* host_word, uint64_t* dev_word, const void* src, void* dst, int64_t bytes,
                      void* stream);
 int pb_host_handoff(uint32_t* flag_host, uint32_t* seq_dev, const uint64_t* src_host, uint64_t* dst,
-                    int64_t n, int64_t timeout_ns, void* stream);
+                    int64_t n, int64_t timeout_ns, uint32_t* skip_dev, void* stream);
 
 /* SPEC:196 response compaction (modulus switch, OFF by default): ct rows
  * [n_polys][L][N] (NTT form, device order) under Q = q_0..q_{L-1} ->

@@ -156,8 +156,19 @@ def _segments(model):
     return seg
 
 
-def reference_train_step(model: Model, x_enc, labels, lr=1e-2, momentum=0.8):
-    """the exact Z_t fixed-point pipeline, no cryptography."""
+def _dp_noise(dp, seed, l, kind, shape, ring):
+    """(grad-b noise at f, grad-W noise at 2f) of layer l: the DO's DP hook."""
+    if dp is None or not dp.enabled:
+        return None, None
+    return (PR.dp_noise(seed, l, PR.OP_GRAD_B, (shape[0],), ring.f, dp, ring),
+            PR.dp_noise(seed, l, PR.OP_GRAD_W, shape, 2 * ring.f, dp, ring))
+
+
+def reference_train_step(model: Model, x_enc, labels, lr=1e-2, momentum=0.8, dp=None, dp_seed=0):
+    """the exact Z_t fixed-point pipeline, no cryptography.
+    ``dp`` (a DpConfig) adds the DO's perturbation drawn from
+    the streams the private step uses under session seed ``dp_seed``
+    ("same DP hook", SPEC:626)."""
     ring, f = model.ring, model.ring.f
     L = model.n_layers
     seg = _segments(model)
@@ -181,12 +192,17 @@ def reference_train_step(model: Model, x_enc, labels, lr=1e-2, momentum=0.8):
     gws, gbs = [None] * L, [None] * L
     for l in reversed(range(L)):
         e = model.layers[model.lin[l]]
+        wshape = (e[2], e[1]) if e[0] == "fc" else (e[2], e[1], e[3], e[3])
+        eb, ew = _dp_noise(dp, dp_seed, l, e[0], wshape, ring)
         if e[0] == "fc":
             gbs[l] = _m(gy.sum(axis=1, dtype=np.uint64), ring)
-            gws[l] = _shift(_m(OK.matmul_wrap(gy, np.ascontiguousarray(acts[l].T)), ring), f, ring)
+            gw = _m(OK.matmul_wrap(gy, np.ascontiguousarray(acts[l].T)), ring)
         else:
             gbs[l] = _m(gy.sum(axis=(0, 2, 3), dtype=np.uint64), ring)
-            gws[l] = _shift(_m(CO.conv_gradw(acts[l], gy, e[3], e[4], e[5]), ring), f, ring)
+            gw = _m(CO.conv_gradw(acts[l], gy, e[3], e[4], e[5]), ring)
+        if eb is not None:
+            gbs[l], gw = _m(gbs[l] + eb, ring), _m(gw + ew, ring)
+        gws[l] = _shift(gw, f, ring)
         if l > 0:
             if e[0] == "fc":
                 ga = _m(OK.matmul_wrap(np.ascontiguousarray(model.W(l).T), gy), ring)
@@ -204,11 +220,13 @@ def reference_train_step(model: Model, x_enc, labels, lr=1e-2, momentum=0.8):
     return loss, gws, gbs
 
 
-def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, momentum=0.8, trace=None, prep=None):
+def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, momentum=0.8, trace=None, prep=None,
+                       dp=None):
     """SPEC:629-637 with fullhe linear layers (oracle/protocols.py) -- or, with
     ``prep`` (a preprocessing.PrepState), the HE-free online linear layers of
     Alg. 4 (mode "prep", SPEC:632) -- and the dealer non-linear backend;
-    <X_0>_0 = 0 at MO, <X_0>_1 = X at DO."""
+    <X_0>_0 = 0 at MO, <X_0>_1 = X at DO.  ``dp``: the DO's DP perturbation of
+    the revealed gradients, drawn from the ctx.seed streams."""
     from . import preprocessing as PP
 
     ring, f = model.ring, model.ring.f
@@ -243,15 +261,17 @@ def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, moment
     for l in reversed(range(L)):
         e = model.layers[model.lin[l]]
         last = l == L - 1
+        wshape = (e[2], e[1]) if e[0] == "fc" else (e[2], e[1], e[3], e[3])
+        eb, ew = _dp_noise(dp, ctx.seed, l, e[0], wshape, ring)
         if prep is not None:
-            gbs[l] = (PR.reveal_grad_bias if e[0] == "fc" else PR.reveal_grad_bias_conv)(ctx, l, gy_mo, gy_do)
-            gw2f = PP.prep_grad_weight(ctx, l, prep.banks[l], *acts[l], gy_mo, gy_do)
+            gbs[l] = (PR.reveal_grad_bias if e[0] == "fc" else PR.reveal_grad_bias_conv)(ctx, l, gy_mo, gy_do, e=eb)
+            gw2f = PP.prep_grad_weight(ctx, l, prep.banks[l], *acts[l], gy_mo, gy_do, e=ew)
         elif e[0] == "fc":
-            gbs[l] = PR.reveal_grad_bias(ctx, l, gy_mo, gy_do)
-            gw2f = PR.grad_weight(ctx, l, *acts[l], gy_mo, gy_do, mo_x_zero=(l == 0), mo_gy_zero=last)
+            gbs[l] = PR.reveal_grad_bias(ctx, l, gy_mo, gy_do, e=eb)
+            gw2f = PR.grad_weight(ctx, l, *acts[l], gy_mo, gy_do, e=ew, mo_x_zero=(l == 0), mo_gy_zero=last)
         else:
-            gbs[l] = PR.reveal_grad_bias_conv(ctx, l, gy_mo, gy_do)
-            gw2f = PR.conv_grad_weight(ctx, l, *acts[l], gy_mo, gy_do, e[3], e[4], e[5], mo_x_zero=(l == 0),
+            gbs[l] = PR.reveal_grad_bias_conv(ctx, l, gy_mo, gy_do, e=eb)
+            gw2f = PR.conv_grad_weight(ctx, l, *acts[l], gy_mo, gy_do, e[3], e[4], e[5], e=ew, mo_x_zero=(l == 0),
                                        mo_gy_zero=last)
         gws[l] = _shift(gw2f, f, ring)  # MO: plaintext shift
         if trace is not None:

@@ -31,7 +31,7 @@ from . import bfv as OB
 from . import convops as CO
 from . import kernels as OK
 from . import packing as PK
-from .ring import DO, MO, RingParams, SeededRng, to_signed
+from .ring import DO, MO, RingParams, SeededRng, encode_fixed, to_signed
 
 OP_FWD, OP_BWD_X, OP_GRAD_W, OP_GRAD_B, OP_RELU, OP_TRUNC_F, OP_TRUNC_B, OP_RELU_B, OP_POOL_F, OP_POOL_B = range(10)
 P_MASK, P_ENC, P_DEALER, P_DP = range(4)
@@ -57,6 +57,31 @@ class Ctx:
 
 def _mask(v, ring):
     return np.asarray(v, dtype=np.uint64) & ring.mask
+
+
+class DpConfig:
+    def __init__(self, sigma=0.0, C=1.0, B=1, enabled=False):
+        if sigma < 0 or C <= 0:
+            raise ValueError("DpConfig needs sigma >= 0 and C > 0")
+        self.sigma, self.C, self.B, self.enabled = float(sigma), float(C), int(B), bool(enabled)
+
+
+def sample_dp_noise(shape, dp, rng):
+    """e ~ N(0, sigma^2 C^2 / B) per element via R:80-81 ``normal`` (zeros when disabled or sigma = 0)."""
+    if dp is None or not dp.enabled or dp.sigma == 0.0:
+        return np.zeros(shape)
+    return rng.normal(shape, dp.sigma * dp.C / np.sqrt(dp.B))
+
+
+def dp_noise(seed, layer, op, shape, scale, dp, ring):
+    """The DO's encoded DP perturbation for one reveal: drawn
+    from SeededRng(seed, stream_id(layer, op, P_DP)), encoded at the scale of
+    the revealed value (grad b: f, grad W before the shift: 2f); None when DP
+    is off.  The reference engine draws the same stream ("same DP hook")."""
+    if dp is None or not dp.enabled:
+        return None
+    e = sample_dp_noise(shape, dp, SeededRng(seed, stream_id(layer, op, P_DP)))
+    return encode_fixed(e, ring, scale)
 
 
 def he_matmul(ctx: Ctx, v_ct_vals, v_pt_vals, W_pt_vals, W_ct_vals, g: PK.MatmulGeometry, s_eff, enc_rng):

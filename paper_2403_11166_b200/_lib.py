@@ -84,7 +84,7 @@ SIGNATURES = {
     "pb_host_mean": [P, I64],
     "pb_set_launch_cap": [I32],
     "pb_copy_async": [P, P, I64, P],
-    "pb_host_handoff": [P, P, P, P, I64, I64, P],
+    "pb_host_handoff": [P, P, P, P, I64, I64, P, P],
     "pb_step_prologue": [P, P, P, P, I64, P],
     "pb_wire_frame_bytes": [P, I32, P],
     "pb_mod_switch_drop": [P, P, P, I64, P, P, P],
@@ -100,7 +100,7 @@ SIGNATURES = {
     "pb_ring_add_bcast": [P, P, P, I64, I64, I64, I32, P],
     "pb_dealer_op": [INT, P, P, I64, I32, P, P, U64, P, U64, U64, I32, P],
     "pb_dealer_op_out": [INT, P, P, P, P, I64, I32, P, P, U64, P, U64, U64, I32, P],
-    "pb_sgd_momentum": [P, P, P, I64, I32, F64, F64, I32, I32, P, P, P],
+    "pb_sgd_momentum": [P, P, P, I64, I32, F64, F64, I32, I32, P, P, P, P],
 }
 _RET = {"pb_last_error": ctypes.c_char_p, "pb_host_mean": ctypes.c_double}
 

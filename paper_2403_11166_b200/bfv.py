@@ -18,6 +18,7 @@ bytes match the oracle exactly when the oracle's noise is passed in
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -154,9 +155,13 @@ def encrypt(kp: KeyPair, m: torch.Tensor, rng=None, *, pack=None, mode: str = "p
             _lib.call("pb_encrypt_sk_noise", h, _dev.ptr(kp.sk_ntt), _dev.ptr(m), pp, ps, Z, P, _dev.ptr(a),
                       _dev.ptr(e), _dev.ptr(ct), st)
         return Ciphertext(ct, params)
-    seed, sptr = rng.dev_args() if rng is not None else (0, None)
-    if nonce is None:
-        nonce = rng.reserve(P) if rng is not None else 0
+    if rng is not None:
+        seed, sptr = rng.dev_args()
+        if nonce is None:
+            nonce = rng.reserve(P)
+    else:  # SPEC:139-147's encrypt(pk, m) has no rng: fresh OS entropy per call (randomized encryption)
+        seed, sptr = int.from_bytes(os.urandom(8), "little"), None
+        nonce = int.from_bytes(os.urandom(4), "little") if nonce is None else nonce
     fn = "pb_encrypt_pk" if mode == "pk" else "pb_encrypt_sk"
     key = _dev.ptr(kp.pk) if mode == "pk" else _dev.ptr(kp.sk_ntt)
     _lib.call(fn, h, key, _dev.ptr(m), pp, ps, Z, P, seed, sptr, nonce, _dev.ptr(ct), st)

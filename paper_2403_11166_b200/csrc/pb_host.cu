@@ -102,9 +102,11 @@ extern "C" int pb_copy_async(void* dst, const void* src, int64_t bytes, void* st
 // memory with uncached system-scope loads.  The counter advances every
 // replay, so the host releases step k by storing k; the kernel acks into the
 // next host word.  After timeout_ns without the value it acks UINT32_MAX,
-// poisons *seq (no later handoff matches) and proceeds: a host that dies
-// between launch and release cannot wedge the GPU, and the host sees the
-// failed ack.
+// poisons *seq (no later handoff matches), sets the step's skip word and
+// proceeds: a host that dies between launch and release cannot wedge the GPU,
+// the host sees the failed ack, and the SGD launches of that step (which read
+// the skip word) leave the model untouched.  A host whose loss raised writes
+// flag[2] = 1 before releasing: same skip.
 namespace {
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
@@ -123,7 +125,8 @@ __device__ __forceinline__ uint64_t global_ns() {
 }
 
 __global__ void __launch_bounds__(1024) k_host_handoff(uint32_t* flag, uint32_t* seq, const uint64_t* src,
-                                                      uint64_t* dst, int64_t n, int64_t timeout_ns) {
+                                                      uint64_t* dst, int64_t n, int64_t timeout_ns,
+                                                      uint32_t* skip) {
   if (threadIdx.x == 0) {
     const uint32_t want = *seq + 1;
     const uint64_t t0 = global_ns();
@@ -134,6 +137,11 @@ __global__ void __launch_bounds__(1024) k_host_handoff(uint32_t* flag, uint32_t*
     }
     const uint32_t res = got == want ? want : 0xFFFFFFFFu;
     *seq = res;
+    // flag[2] (abort): written by the host before the release word when its loss
+    // raised; the acquire load above orders this read after it.  A timed-out or
+    // aborted step runs its backward on no fresh gradient, so every SGD launch of
+    // the step reads *skip and leaves the weights untouched.
+    if (skip) *skip = (got != want || ld_acquire_sys(flag + 2) != 0u) ? 1u : 0u;
     asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(flag + 1), "r"(res) : "memory");  // the ack word
   }
   __syncthreads();
@@ -154,10 +162,11 @@ __global__ void __launch_bounds__(1024) k_host_handoff(uint32_t* flag, uint32_t*
 }  // namespace
 
 extern "C" int pb_host_handoff(uint32_t* flag_host, uint32_t* seq_dev, const uint64_t* src_host, uint64_t* dst,
-                               int64_t n, int64_t timeout_ns, void* stream) {
+                               int64_t n, int64_t timeout_ns, uint32_t* skip_dev, void* stream) {
   if (!flag_host || !seq_dev || n < 0 || (n && (!src_host || !dst)) || timeout_ns < 0) return PB_ERR_ARG;
   const int threads = (int)(n >= 4096 ? 1024 : n <= 128 ? 32 : ((n + 127) / 128) * 32);
-  k_host_handoff<<<1, threads, 0, (cudaStream_t)stream>>>(flag_host, seq_dev, src_host, dst, n, timeout_ns);
+  k_host_handoff<<<1, threads, 0, (cudaStream_t)stream>>>(flag_host, seq_dev, src_host, dst, n, timeout_ns,
+                                                           skip_dev);
   return cudaPeekAtLastError() == cudaSuccess ? PB_OK : PB_ERR_CUDA;
 }
 

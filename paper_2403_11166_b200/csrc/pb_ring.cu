@@ -322,7 +322,8 @@ __global__ void k_dealer(int op, const uint64_t* in_mo, const uint64_t* in_do, u
 }
 
 __global__ void k_sgd(double* w, double* v, const uint64_t* g, int64_t n, int gscale, double lr, double mom, int ell,
-                      int wscale, uint64_t* w_ring, int32_t* flag) {
+                      int wscale, uint64_t* w_ring, int32_t* flag, const uint32_t* skip) {
+  if (skip && *skip) return;  // the step was aborted before its gradient was released: keep w, v, W
   const double gs = ldexp(1.0, gscale), ws = ldexp(1.0, wscale);
   const double limit = ldexp(1.0, ell - 1) / ws;
   const uint64_t m = ring_mask(ell);
@@ -479,11 +480,11 @@ extern "C" int pb_dealer_op_out(int op, const uint64_t* in_mo, const uint64_t* i
 
 extern "C" int pb_sgd_momentum(double* w, double* v, const uint64_t* grad_ring, int64_t n, int32_t grad_scale, double lr,
                                double momentum, int32_t ell, int32_t w_scale, uint64_t* w_ring, int32_t* range_flag,
-                               void* stream) {
+                               const uint32_t* skip, void* stream) {
   if (n > 0 && (!w || !v || !grad_ring || !w_ring)) return pb_set_error(PB_ERR_ARG, "null argument");
   if (bad_ell(ell)) return pb_set_error(PB_ERR_ARG, "bad ell");
   if (n <= 0) return PB_OK;
-  k_sgd<<<RING_GRID(n)>>>(w, v, grad_ring, n, grad_scale, lr, momentum, ell, w_scale, w_ring, range_flag);
+  k_sgd<<<RING_GRID(n)>>>(w, v, grad_ring, n, grad_scale, lr, momentum, ell, w_scale, w_ring, range_flag, skip);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }

@@ -33,10 +33,10 @@ import torch
 
 from . import _dev, _lib
 from .bfv import Ciphertext, KeyPair
-from .errors import DesyncError, ScaleError, ShapeError
+from .errors import DesyncError, ParamsError, ScaleError, ShapeError
 from .params import BfvParams, context
 from .poly_encoding import MatmulGeometry, conv_out_hw, plan_conv_layer, plan_matmul
-from .ring import DO, MO, RingParams, RingTensor, SeededRng, ShareTensor
+from .ring import DO, MO, RingParams, RingTensor, SeededRng, ShareTensor, encode_fixed
 
 OP_FWD, OP_BWD_X, OP_GRAD_W, OP_GRAD_B, OP_RELU, OP_TRUNC_F, OP_TRUNC_B, OP_RELU_B, OP_POOL_F, OP_POOL_B = range(10)
 P_MASK, P_ENC, P_DEALER, P_DP = range(4)
@@ -96,6 +96,10 @@ class DpConfig:
     C: float = 1.0
     B: int = 1
     enabled: bool = False
+
+    def __post_init__(self):
+        if self.sigma < 0 or self.C <= 0:
+            raise ParamsError("DpConfig needs sigma >= 0 and C > 0")
 
 
 def _pk(pack):
@@ -202,6 +206,7 @@ class Session:
         self._grad_stream = None
         self._aux_streams = {}
         self._prep_stream = None
+        self.dp = None  # DpConfig: the DO's DP perturbation of revealed gradients, off by default
         self.capture = None  # diagnostics: a list receives (masked output ciphertexts, useful slot positions)
         # operands prepared ahead of their protocol (prepare_operand): key
         # (layer, op, role) -> (device tensor, event or None); buffers persist
@@ -835,6 +840,21 @@ def reveal_grad_bias_conv(sess: Session, layer: int, gy_a: ShareTensor, gy_b: Sh
 
 def sample_dp_noise(shape, dp: DpConfig, rng: SeededRng) -> np.ndarray:
     """e ~ N(0, (sigma C)^2 / B) per element (host float64, encoded by the caller)."""
-    if not dp.enabled or dp.sigma == 0.0:
+    if dp is None or not dp.enabled or dp.sigma == 0.0:
         return np.zeros(shape)
     return rng.normal(shape, dp.sigma * dp.C / np.sqrt(dp.B))
+
+
+def dp_noise(sess: Session, layer: int, op: int, shape, scale: int) -> torch.Tensor | None:
+    """The DO's encoded DP perturbation of one reveal: e drawn
+    on the host from the session's (layer, op, P_DP) stream -- R:80-81's numpy
+    ``normal``, the reference's own sampler -- encoded at the revealed value's
+    scale (grad b: f; grad W before the MO's shift: 2f) and moved to the
+    device; None when the session's DP is off."""
+    dp = sess.dp
+    if dp is None or not dp.enabled:
+        return None
+    if sess.graph_mode:
+        raise ParamsError("DP noise is a per-step host draw: run DP steps eagerly (private_train_step)")
+    e = sample_dp_noise(tuple(shape), dp, sess.rng(layer, op, P_DP))
+    return encode_fixed(e, sess.ring, scale)

@@ -21,9 +21,9 @@ import numpy as np
 import torch
 
 from . import _dev, _lib
-from .errors import EncodeRangeError, ShapeError
-from .linear_protocols import (OP_BWD_X, OP_FWD, OP_GRAD_W, Session, conv_backward_input, conv_forward,
-                               conv_grad_weight, grad_w_flipped, grad_w_geometry, grad_weight, linear_backward_input,
+from .errors import EncodeRangeError, ParamsError, ShapeError
+from .linear_protocols import (OP_BWD_X, OP_FWD, OP_GRAD_B, OP_GRAD_W, Session, conv_backward_input, conv_forward,
+                               conv_grad_weight, dp_noise, grad_w_flipped, grad_w_geometry, grad_weight, linear_backward_input,
                                linear_forward, reveal_grad_bias, reveal_grad_bias_conv)
 from . import preprocessing as PP
 from .nonlinear import (avgpool_backward, avgpool_forward, relu_backward, relu_forward, relu_truncate, truncate,
@@ -114,6 +114,8 @@ class Model:
         self.W = [RingTensor(encode_fixed(w, ring), ring.f, ring, _canonical=True) for w in self.w]
         self.B = [RingTensor(encode_fixed(b, ring, 2 * ring.f), 2 * ring.f, ring, _canonical=True) for b in self.b]
         self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        # step-abort word (GraphStep's loss handoff): nonzero -> the SGD kernels are no-ops
+        self.skip = torch.zeros(1, dtype=torch.int32, device=dev)
 
     @property
     def sizes(self):  # MLP compatibility
@@ -148,7 +150,8 @@ class Model:
         for w, v, g, ring_t, scale in ((self.w[l], self.vw[l], gw, self.W[l], ring.f),
                                        (self.b[l], self.vb[l], gb, self.B[l], 2 * ring.f)):
             _lib.call("pb_sgd_momentum", _dev.ptr(w), _dev.ptr(v), _dev.ptr(g.values), w.numel(), g.scale,
-                      float(lr), float(momentum), ring.ell, scale, _dev.ptr(ring_t.values), _dev.ptr(self._flag), st)
+                      float(lr), float(momentum), ring.ell, scale, _dev.ptr(ring_t.values), _dev.ptr(self._flag),
+                      _dev.ptr(self.skip), st)
 
     def check_range(self):
         if int(self._flag.item()):
@@ -307,15 +310,19 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
             ga = _backward_input(sess, model, l, e, acts, gy_mo, gy_do, last, prep)
         gstream.wait_event(ev_gy)
         with torch.cuda.stream(gstream):
+            # the DO's DP perturbation (None unless sess.dp is enabled)
+            wshape = (e[2], e[1]) if e[0] == "fc" else (e[2], e[1], e[3], e[3])
+            eb = dp_noise(sess, l, OP_GRAD_B, (e[2],), f)
+            ew = dp_noise(sess, l, OP_GRAD_W, wshape, 2 * f)
             if prep is not None:
-                gbs[l] = (reveal_grad_bias if e[0] == "fc" else reveal_grad_bias_conv)(sess, l, gy_mo, gy_do)
-                gw = PP.prep_grad_weight(sess, l, prep.banks[l], *acts[l], gy_mo, gy_do)
+                gbs[l] = (reveal_grad_bias if e[0] == "fc" else reveal_grad_bias_conv)(sess, l, gy_mo, gy_do, e=eb)
+                gw = PP.prep_grad_weight(sess, l, prep.banks[l], *acts[l], gy_mo, gy_do, e=ew)
             elif e[0] == "fc":
-                gbs[l] = reveal_grad_bias(sess, l, gy_mo, gy_do)
-                gw = grad_weight(sess, l, *acts[l], gy_mo, gy_do, mo_x_zero=(l == 0), mo_gy_zero=last)
+                gbs[l] = reveal_grad_bias(sess, l, gy_mo, gy_do, e=eb)
+                gw = grad_weight(sess, l, *acts[l], gy_mo, gy_do, e=ew, mo_x_zero=(l == 0), mo_gy_zero=last)
             else:
-                gbs[l] = reveal_grad_bias_conv(sess, l, gy_mo, gy_do)
-                gw = conv_grad_weight(sess, l, *acts[l], gy_mo, gy_do, e[3], e[4], e[5], mo_x_zero=(l == 0),
+                gbs[l] = reveal_grad_bias_conv(sess, l, gy_mo, gy_do, e=eb)
+                gw = conv_grad_weight(sess, l, *acts[l], gy_mo, gy_do, e[3], e[4], e[5], e=ew, mo_x_zero=(l == 0),
                                       mo_gy_zero=last)
             gws[l] = arith_shift(gw, f)
         keep.append((gy_mo, gy_do))
@@ -492,6 +499,8 @@ class GraphStep:
     def __init__(self, sess: Session, model: Model, x: RingTensor, lr=1e-2, momentum=0.8, prep=None,
                  prefetch_input: bool = False):
         self.sess, self.model, self.lr, self.momentum, self.prep = sess, model, lr, momentum, prep
+        if sess.dp is not None and sess.dp.enabled:  # a per-step host draw cannot be captured
+            raise ParamsError("GraphStep replays fixed launches: run DP (sigma > 0) steps with private_train_step")
         sess.enable_graph_mode()
         self.x = x  # device input buffer; callers copy new batches into x.values (or use load_batch)
         self._stage = None
@@ -571,7 +580,7 @@ class GraphStep:
         # launch between the host loss and the backward)
         on_start = None
         if self.handoff:
-            self._hflag = torch.zeros(2, dtype=torch.int32).pin_memory()  # [release, ack]
+            self._hflag = torch.zeros(3, dtype=torch.int32).pin_memory()  # [release, ack, abort]
             self._hflag_np = self._hflag.numpy().view(np.uint32)
             self._hseq_dev = torch.zeros(1, dtype=torch.int32, device=dev)
             self._hseq = 0
@@ -579,7 +588,8 @@ class GraphStep:
 
             def on_start():
                 _lib.call("pb_host_handoff", self._hflag.data_ptr(), self._hseq_dev.data_ptr(), self._g_host_ptr,
-                          self._g_dev_ptr, n_g, _HANDOFF_TIMEOUT_NS, torch.cuda.current_stream().cuda_stream)
+                          self._g_dev_ptr, n_g, _HANDOFF_TIMEOUT_NS, self.model.skip.data_ptr(),
+                          torch.cuda.current_stream().cuda_stream)
         with torch.cuda.graph(self.g_bwd, pool=self.g_fwd.pool(), stream=hp):
             self.grads = backward_phase(sess, model, self.state, self.g_do, lr, momentum, check=False, prep=prep,
                                         pre_layers=late, on_start=on_start,
@@ -655,6 +665,13 @@ class GraphStep:
         self._batch_pending = False
         self._flag_pending = True
 
+    def join_prefetch(self):
+        """Make the current stream wait for the background work step() queued
+        on the copy stream (the next step's input encryption), so a timing
+        event recorded after this covers it."""
+        if self.prefetch:
+            torch.cuda.current_stream().wait_event(self._ev_ready)
+
     timing = None  # diagnostics: a list receives (label, CUDA event) at the step's phase boundaries
 
     def _mark(self, label):
@@ -705,13 +722,21 @@ class GraphStep:
             self.g_bwd.replay()
             self._mark("bwd")
             self._hseq += 1
+            abort = 1
             try:
                 self._wait_logits()
                 if self._hseq > 1 and int(self._hflag_np[1]) != self._hseq - 1:
                     raise RuntimeError("backward graph: the previous step's loss handoff timed out")
                 loss = self._host_loss(labels)  # g written into g_host
-            finally:  # release the backward even on error (it then computes on a stale g)
+                abort = 0
+            finally:
+                # release the backward even on error, so the GPU never waits for the
+                # timeout; with the abort word set it runs on no fresh gradient and its
+                # SGD launches (reading the skip word the handoff writes) are no-ops
+                self._hflag_np[2] = abort
                 self._hflag_np[0] = self._hseq & 0xFFFFFFFF
+                if abort:  # after the skipped SGDs: later (eager) updates apply again
+                    self.model.skip.zero_()
         else:
             self._wait_logits()
             loss = self._host_loss(labels)

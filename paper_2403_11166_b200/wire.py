@@ -67,6 +67,9 @@ def serialize(obj, params: BfvParams | None = None, *, form: str = NTT, out: tor
         out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     elif out.numel() < nbytes or out.dtype != torch.uint8:
         raise ShapeError(f"wire buffer holds {out.numel()} bytes, {P} frames need {nbytes}")
+    if not out.is_cuda and not stage and not out.is_pinned():
+        # the kernel would store straight into pageable memory: an illegal address
+        raise ShapeError("serialize(stage=False) needs a CUDA or pinned host `out`")
     # A host destination is staged in HBM and moved by the copy engine: on
     # B200 the DMA beats the kernel's own zero-copy stores over the host link
     # (profiles/r01_wire_bench.jsonl: 54.6 vs 50.3 GB/s of frames).

@@ -131,6 +131,16 @@ def ring_vectors() -> dict:
     out["share_rec"] = R.reconstruct_tensor(mo, do).values
     y = R.RingTensor(R.encode_fixed(np.linspace(-5, 5, 11), P, 50), 50, P)
     out["shift_in"], out["shift_out"] = y.values, R.arith_shift(y, 25).values
+    # R:140-145 __neg__ / scalar_mul and R:185-198 on edge residues (round 2)
+    edge = np.array([0, 1, (1 << 58) - 1, 1 << 58, (1 << 58) + 1, (1 << 59) - 1, 12345, 1 << 40], dtype=np.uint64)
+    e = R.RingTensor(edge, 25, P)
+    out["edge_in"], out["edge_neg"] = edge, (-e).values
+    out["edge_smul_ks"] = np.array([3, -7, (1 << 59) - 1, 1 << 40], dtype=np.int64)
+    out["edge_smul"] = np.stack([e.scalar_mul(int(k)).values for k in out["edge_smul_ks"]])
+    out["edge_signed"] = R.to_signed(edge, P)
+    out["edge_dec_f50"] = R.decode_fixed(edge, P, 50)
+    # R:80-81 normal: the DP hook's sampler
+    out["rng_normal"] = R.SeededRng(2024, 1000003).normal((16,), 0.5)
     return out
 
 

@@ -120,3 +120,96 @@ def test_graph_step_prefetched_input_encryption():
         for l in range(len(sizes) - 1):
             assert np.array_equal(m1.W[l].numpy(), m2.W[l].numpy())
             assert np.array_equal(m2.W[l].numpy(), om.W(l))
+
+
+def test_graph_step_abort_leaves_weights_untouched():
+    """A step whose host loss raises (EncodeRangeError from load_batch) still
+    releases the already-launched backward graph, but with the abort word set:
+    its SGD launches are no-ops, so weights, master weights and momentum stay
+    bit-identical; the next good step matches the eager engine and the oracle
+    (which never saw the bad batch)."""
+    import torch
+
+    from oracle import nn as ON
+    from oracle import ring as OR
+    from paper_2403_11166_b200 import bfv
+    from paper_2403_11166_b200 import nn as PN
+    from paper_2403_11166_b200.errors import EncodeRangeError
+    from paper_2403_11166_b200.linear_protocols import Session
+    from paper_2403_11166_b200.params import BfvParams
+    from paper_2403_11166_b200.ring import RingParams, RingTensor, SeededRng, encode_fixed
+
+    ring, params = RingParams(), BfvParams()
+    kp = bfv.keygen(params, SeededRng(3, 0))
+    sizes, B = [784, 32, 10], 8
+    xh, labels = PN.synthetic_mnist(7, B, ring)
+    s1, s2 = Session(params, ring, kp, seed=1), Session(params, ring, kp, seed=1)
+    m1, m2 = PN.Model(sizes, ring, seed=4), PN.Model(sizes, ring, seed=4)
+    x1 = RingTensor(encode_fixed(xh, ring), 25, ring, _canonical=True)
+    runner = PN.GraphStep(s2, m2, RingTensor(encode_fixed(xh, ring), 25, ring, _canonical=True))
+    om = ON.Model(sizes, OR.RingParams(), seed=4)
+    xo, _ = ON.synthetic_mnist(7, B, OR.RingParams())
+
+    def snap(m):
+        return [t.detach().cpu().numpy().copy() for l in range(len(sizes) - 1)
+                for t in (m.W[l].values if hasattr(m.W[l], "values") else m.W[l], m.w[l], m.vw[l], m.b[l], m.vb[l])]
+
+    s1.reseed(300)
+    PN.private_train_step(s1, m1, x1, labels)
+    runner.step(300, labels)
+    ON.reference_train_step(om, xo, labels)
+    before = snap(m2)
+    bad = np.ascontiguousarray(xh).copy()
+    bad[0, 0] = 1e30
+    runner.load_batch(torch.from_numpy(bad).pin_memory())
+    with pytest.raises(EncodeRangeError):
+        runner.step(301, labels)
+    torch.cuda.synchronize()
+    after = snap(m2)
+    assert all(np.array_equal(a, b) for a, b in zip(before, after)), "aborted step changed the model"
+    assert int(m2.skip.item()) == 0
+    # recovery: a good batch again; the step equals eager and the oracle
+    runner.load_batch(torch.from_numpy(np.ascontiguousarray(xh)).pin_memory())
+    s1.reseed(302)
+    l1, _, _ = PN.private_train_step(s1, m1, x1, labels)
+    l2 = runner.step(302, labels)
+    l3, _, _ = ON.reference_train_step(om, xo, labels)
+    assert l1 == l2 == l3
+    for l in range(len(sizes) - 1):
+        assert np.array_equal(m1.W[l].numpy(), m2.W[l].numpy())
+        assert np.array_equal(m2.W[l].numpy(), om.W(l))
+
+
+def test_host_handoff_timeout_sets_skip():
+    """pb_host_handoff with no release: after the timeout it acks UINT32_MAX and
+    sets the skip word, and pb_sgd_momentum under that word is a no-op."""
+    import torch
+
+    from paper_2403_11166_b200 import _lib
+
+    dev = torch.device("cuda:0")
+    flag = torch.zeros(3, dtype=torch.int32).pin_memory()
+    seq = torch.zeros(1, dtype=torch.int32, device=dev)
+    src = torch.arange(16, dtype=torch.int64).pin_memory()
+    dst = torch.zeros(16, dtype=torch.int64, device=dev)
+    skip = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("pb_host_handoff", flag.data_ptr(), seq.data_ptr(), src.data_ptr(), dst.data_ptr(), 16,
+              2_000_000, skip.data_ptr(), st)  # 2 ms, never released
+    torch.cuda.synchronize()
+    assert int(skip.item()) == 1 and int(flag[1]) == -1
+    w = torch.ones(8, dtype=torch.float64, device=dev)
+    v = torch.zeros(8, dtype=torch.float64, device=dev)
+    g = torch.full((8,), 1 << 25, dtype=torch.int64, device=dev)
+    wr = torch.zeros(8, dtype=torch.int64, device=dev)
+    fl = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.call("pb_sgd_momentum", w.data_ptr(), v.data_ptr(), g.data_ptr(), 8, 25, 0.5, 0.8, 59, 25, wr.data_ptr(),
+              fl.data_ptr(), skip.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert torch.all(w == 1) and torch.all(v == 0) and torch.all(wr == 0)
+    # released on time: skip cleared, gradient copied
+    flag[0] = 0  # seq was poisoned to UINT32_MAX: the next want is 0
+    _lib.call("pb_host_handoff", flag.data_ptr(), seq.data_ptr(), src.data_ptr(), dst.data_ptr(), 16,
+              2_000_000_000, skip.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert int(skip.item()) == 0 and torch.equal(dst.cpu(), src)

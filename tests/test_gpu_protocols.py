@@ -158,3 +158,116 @@ def test_private_step_shares_match_oracle_private_step(env):
         assert l1 == l2
         assert np.array_equal(y2[1].value.numpy(), y1[1]) and np.array_equal(y2[0].value.numpy(), y1[0])
         assert np.array_equal(gw2.numpy(), gw1) and np.array_equal(gb2.numpy(), gb1)
+
+
+# ----------------------------------------------------------- DP hook ---
+# the DO's perturbation e of the bias reveal and of Alg. 2.
+
+def test_dp_noise_statistics_on_device_path(env):
+    """sigma=0.01, C=8, B=64: the encoded noise the engine adds decodes to
+    draws with std within 5 % of sigma C / sqrt(B) and a mean within 4
+    standard errors of 0, and sigma=0 adds nothing."""
+    from paper_2403_11166_b200 import linear_protocols as LP
+
+    sess = env["sess"]
+    try:
+        sess.dp = LP.DpConfig(sigma=0.01, C=8.0, B=64, enabled=True)
+        e = LP.dp_noise(sess, 0, LP.OP_GRAD_W, (1000, 1000), 50)
+        v = OR.decode_fixed(e.cpu().numpy().view(np.uint64), RING, 50)
+        assert abs(v.std() - 0.01) <= 0.05 * 0.01 and abs(v.mean()) <= 4 * 0.01 / 1000
+        sess.dp = LP.DpConfig(sigma=0.0, C=8.0, B=64, enabled=True)
+        assert not LP.dp_noise(sess, 0, LP.OP_GRAD_W, (10, 10), 50).cpu().numpy().any()
+    finally:
+        sess.dp = None
+
+
+@pytest.mark.parametrize("sigma", [0.01, 0.5])
+def test_reveal_grad_bias_and_grad_weight_with_given_e_equal_oracle(env, sigma):
+    """With a given e both reveals equal the oracle's bit for bit."""
+    from paper_2403_11166_b200 import linear_protocols as LP
+    from paper_2403_11166_b200.ring import RingTensor
+
+    pr, sess, octx = env["pr"], env["sess"], env["octx"]
+    n_i, n_o, B = 96, 24, 16
+    x, x_mo, x_do = _rand_shares(21, (n_i, B))
+    g, g_mo, g_do = _rand_shares(22, (n_o, B), 0.1)
+    dp = OPR.DpConfig(sigma=sigma, C=4.0, B=B, enabled=True)
+    eb = OPR.dp_noise(5, 1, OPR.OP_GRAD_B, (n_o,), 25, dp, RING)
+    ew = OPR.dp_noise(5, 1, OPR.OP_GRAD_W, (n_o, n_i), 50, dp, RING)
+    sess.reseed(77)
+    octx.seed = 77
+    gb = LP.reveal_grad_bias(sess, 1, *_shares(pr, g_mo, g_do, 25), e=RingTensor(eb, 25, pr).values)
+    assert np.array_equal(gb.numpy(), OPR.reveal_grad_bias(octx, 1, g_mo, g_do, e=eb))
+    gw = LP.grad_weight(sess, 1, *_shares(pr, x_mo, x_do, 25), *_shares(pr, g_mo, g_do, 25),
+                        e=RingTensor(ew, 50, pr).values)
+    want = OPR.grad_weight(octx, 1, x_mo, x_do, g_mo, g_do, e=ew)
+    assert np.array_equal(gw.numpy(), want)
+    # and the perturbation is exactly e on top of the sigma = 0 reveal
+    plain = (OK.matmul_wrap(g, np.ascontiguousarray(x.T)) + ew) & RING.mask
+    assert np.array_equal(gw.numpy(), plain)
+
+
+def test_private_step_with_dp_matches_reference_engine(env):
+    """sigma > 0: revealed gradients, master weights and re-quantised weights of
+    a private MLP step equal the reference engine's with the same DP streams."""
+    from paper_2403_11166_b200 import linear_protocols as LP
+    from paper_2403_11166_b200 import nn as PN
+    from paper_2403_11166_b200.ring import RingTensor, encode_fixed
+
+    pr, sess = env["pr"], env["sess"]
+    sizes, B = [784, 32, 10], 8
+    om, pm = ON.Model(sizes, RING, seed=3), PN.Model(sizes, pr, seed=3)
+    xo, labels = ON.synthetic_mnist(5, B, RING)
+    xh, _ = PN.synthetic_mnist(5, B, pr)
+    xp = RingTensor(encode_fixed(xh, pr), 25, pr, _canonical=True)
+    dp = OPR.DpConfig(sigma=1.0, C=2.0, B=B, enabled=True)
+    try:
+        sess.dp = LP.DpConfig(sigma=1.0, C=2.0, B=B, enabled=True)
+        for step in range(2):
+            sess.reseed(3000 + step)
+            ref_loss, ref_gw, ref_gb = ON.reference_train_step(om, xo, labels, dp=dp, dp_seed=3000 + step)
+            loss, gw, gb = PN.private_train_step(sess, pm, xp, labels)
+            assert loss == ref_loss
+            for l in range(len(sizes) - 1):
+                assert np.array_equal(gw[l].numpy(), ref_gw[l]) and np.array_equal(gb[l].numpy(), ref_gb[l])
+                assert np.array_equal(pm.w[l].cpu().numpy(), om.w[l])
+                assert np.array_equal(pm.W[l].numpy(), om.W(l))
+        with pytest.raises(Exception):
+            PN.GraphStep(sess, pm, xp)  # DP steps are eager-only (per-step host draw)
+    finally:
+        sess.dp = None
+
+
+# ------------------------------------------------- ring API on the device ---
+# R:140-145 (__neg__, scalar_mul) and R:185-198 (decode_fixed, to_signed).
+
+def test_ring_neg_scalar_mul_decode_to_signed_match_reference():
+    from paper_2403_11166_b200 import ring as PRG
+
+    pr = PRG.RingParams()
+    rng = np.random.default_rng(5)
+    edge = np.array([0, 1, (1 << 58) - 1, 1 << 58, (1 << 58) + 1, (1 << 59) - 1], dtype=np.uint64)
+    v = np.concatenate([edge, rng.integers(0, 1 << 59, size=4096, dtype=np.uint64)])
+    ot = OR.RingTensor(v, 25, RING)
+    dt = PRG.RingTensor(v, 25, pr)
+    assert np.array_equal((-dt).numpy(), (-ot).values)
+    for k in (0, 1, 3, -7, (1 << 59) - 1, 1 << 40, 123456789):
+        assert np.array_equal(dt.scalar_mul(k).numpy(), ot.scalar_mul(k).values), k
+    assert np.array_equal(PRG.to_signed(dt.values, pr).cpu().numpy(), OR.to_signed(v, RING))
+    for scale in (25, 50, 0):
+        got = PRG.decode_fixed(dt.values, pr, scale).cpu().numpy()
+        assert np.array_equal(got, OR.decode_fixed(v, RING, scale)), scale
+    # the reference's own outputs on edge residues (tests/golden/ring.npz, generated from R)
+    g = dict(np.load(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "ring.npz")))
+    e = PRG.RingTensor(g["edge_in"], 25, pr)
+    assert np.array_equal((-e).numpy(), g["edge_neg"])
+    for k, want in zip(g["edge_smul_ks"], g["edge_smul"]):
+        assert np.array_equal(e.scalar_mul(int(k)).numpy(), want)
+    assert np.array_equal(PRG.to_signed(e.values, pr).cpu().numpy(), g["edge_signed"])
+    assert np.array_equal(PRG.decode_fixed(e.values, pr, 50).cpu().numpy(), g["edge_dec_f50"])
+    assert np.array_equal(PRG.decode_fixed(g["enc_f25"], pr).cpu().numpy(), g["dec_f25"])
+    # round trip through the device encoder, including the range edge
+    x = np.array([0.0, -1.0, 2.5, -(2.0 ** 33) + 2.0 ** -25, 2.0 ** 33 - 2.0 ** -25, 1e-9, -1e-9])
+    enc = PRG.encode_fixed(x, pr)
+    assert np.array_equal(enc.cpu().numpy().view(np.uint64), OR.encode_fixed(x, RING))
+    assert np.array_equal(PRG.decode_fixed(enc, pr).cpu().numpy(), OR.decode_fixed(OR.encode_fixed(x, RING), RING))

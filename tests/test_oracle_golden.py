@@ -110,6 +110,13 @@ def test_ring_layer_matches_reference(golden):
     assert np.array_equal(OR.reconstruct_tensor(mo, do).values, g["share_rec"])
     y = OR.RingTensor(g["shift_in"], 50, P)
     assert np.array_equal(OR.arith_shift(y, 25).values, g["shift_out"])
+    e = OR.RingTensor(g["edge_in"], 25, P)
+    assert np.array_equal((-e).values, g["edge_neg"])
+    for k, want in zip(g["edge_smul_ks"], g["edge_smul"]):
+        assert np.array_equal(e.scalar_mul(int(k)).values, want)
+    assert np.array_equal(OR.to_signed(g["edge_in"], P), g["edge_signed"])
+    assert np.array_equal(OR.decode_fixed(g["edge_in"], P, 50), g["edge_dec_f50"])
+    assert np.array_equal(OR.SeededRng(2024, 1000003).normal((16,), 0.5), g["rng_normal"])
 
 
 def test_spec_ring_kats():
