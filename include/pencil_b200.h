@@ -286,6 +286,17 @@ int pb_conv2d(const uint64_t* x, const uint64_t* w, int32_t B, int32_t Ci, int32
 enum { PB_CONV_FWD = 0, PB_CONV_BWDX = 1, PB_CONV_GRADW = 2 };
 int pb_ring_conv(int kind, const uint64_t* a, const uint64_t* b, int32_t B, int32_t c_i, int32_t c_o, int32_t H,
                  int32_t W, int32_t s, int32_t pad, int32_t stride, int32_t ell, uint64_t* out, void* stream);
+/* The ring GEMMs of pb_ring_matmul / pb_ring_conv with the kernel family
+ * chosen explicitly: PB_BACKEND_AUTO (what the plain entry points do: a
+ * function of the shape alone), PB_BACKEND_CUDA_CORE (u64 IMAD tiles),
+ * PB_BACKEND_TENSOR (tcgen05 kind::i8 on balanced base-256 digit planes,
+ * TMEM accumulators; pb_tc.cu).  Every backend is bit-exact mod 2^ell. */
+enum { PB_BACKEND_AUTO = 0, PB_BACKEND_CUDA_CORE = 1, PB_BACKEND_TENSOR = 2 };
+int pb_ring_conv_ex(int kind, const uint64_t* a, const uint64_t* b, int32_t B, int32_t c_i, int32_t c_o, int32_t H,
+                    int32_t W, int32_t s, int32_t pad, int32_t stride, int32_t ell, uint64_t* out, int32_t backend,
+                    void* stream);
+int pb_ring_matmul_ex(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m, int trans_a,
+                      int trans_b, int32_t ell, uint64_t* out, int32_t backend, void* stream);
 /* AvgPool2 local steps: PB_POOL_SUM in (bc,H,W) -> out (bc,H/2,W/2)
  * 2x2 window sums; PB_POOL_REPLICATE in (bc,H/2,W/2) -> out (bc,H,W). */
 enum { PB_POOL_SUM = 0, PB_POOL_REPLICATE = 1 };

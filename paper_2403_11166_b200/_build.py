@@ -69,7 +69,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + ".tmp"
     cuda_lib = os.path.join(os.path.dirname(os.path.dirname(nvcc)), "lib64")
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC", *objs,
-           f"-L{cuda_lib}", "-lcublasLt", f"-Xlinker=-rpath={cuda_lib}", "-o", tmp]
+           f"-L{cuda_lib}", f"-Xlinker=-rpath={cuda_lib}", "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}{r.stderr}")

@@ -78,6 +78,7 @@ SIGNATURES = {
     "pb_uniform_ring": [P, I64, U64, P, U64, U64, I32, P],
     "pb_share": [P, I64, U64, P, U64, U64, I32, P, P, P],
     "pb_ring_matmul": [P, P, I64, I64, I64, INT, INT, I32, P, P],
+    "pb_ring_matmul_ex": [P, P, I64, I64, I64, INT, INT, I32, P, I32, P],
     "pb_ring_matmul_add": [P, P, I64, I64, I64, INT, INT, P, I32, I32, P, P],
     "pb_host_softmax_pre": [P, I32, I32, I32, I32, P],
     "pb_host_softmax_post": [P, I32, I32, P, I32, I32, P, P],
@@ -95,6 +96,7 @@ SIGNATURES = {
     "pb_col2im": [P, I32, I32, I32, I32, I32, I32, P, P],
     "pb_conv2d": [P, P, I32, I32, I32, I32, I32, I32, I32, P, P],
     "pb_ring_conv": [INT, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P],
+    "pb_ring_conv_ex": [INT, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P, I32, P],
     "pb_pool2": [INT, P, I64, I32, I32, I32, P, P],
     "pb_ring_lincomb": [INT, P, P, P, I32, P, I32, P, I64, I32, P],
     "pb_ring_add_bcast": [P, P, P, I64, I64, I64, I32, P],
@@ -109,6 +111,7 @@ PW_MUL, PW_MAC, PW_ADD, PW_SUB = 0, 1, 2, 3
 RING_ADD, RING_SUB, RING_MUL, RING_NEG, RING_SCALAR_MUL, RING_MASK, RING_ARITH_SHIFT = range(7)
 DEALER_RELU, DEALER_TRUNC, DEALER_SELECT, DEALER_RESHARE, DEALER_RELU_TRUNC, DEALER_TRUNC_SELECT = range(6)
 CONV_FWD, CONV_BWDX, CONV_GRADW = range(3)
+BACKEND_AUTO, BACKEND_CUDA_CORE, BACKEND_TENSOR = range(3)
 POOL_SUM, POOL_REPLICATE = range(2)
 
 _lib = None

@@ -335,33 +335,33 @@ int conv_gemm_launch(int kind, const ConvDims& d, const uint64_t* a, const uint6
 
 }  // namespace
 
-int pb_imma_conv(int kind, const uint64_t* a, const uint64_t* b, int B, int ci, int co, int H, int W, int s, int p,
-                 int st_, int oh, int ow, int ell, uint64_t* out, cudaStream_t st);
-int pb_imma_matmul(const uint64_t* a, const uint64_t* b, int n, int k, int m, int ta, int tb, int ell, uint64_t* out,
-                   cudaStream_t st);
+int pb_tc_conv(int kind, const uint64_t* a, const uint64_t* b, int B, int ci, int co, int H, int W, int s, int p,
+               int st_, int oh, int ow, int ell, uint64_t* out, cudaStream_t st);
+int pb_tc_matmul(const uint64_t* a, const uint64_t* b, int n, int k, int m, int ta, int tb, int ell, uint64_t* out,
+                 cudaStream_t st);
 
-// int8-limb tensor-core path for large ring GEMMs (pb_imma.cu); PB_IMMA=0 disables it.
-static bool imma_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("PB_IMMA");
-    on = e ? atoi(e) : 1;
-  }
-  return on != 0;
-}
-constexpr int64_t IMMA_MIN_MACS = 1ll << 27;
-static bool imma_gradw() {  // PB_IMMA_GRADW=1: weight gradients on the int8 path too (CIFAR conv2: 1.62 ms
-  static int on = -1;         // vs 0.59 ms on the CUDA-core GEMM -- the K = B*oh*ow digit planes are HBM-bound)
-  if (on < 0) {
-    const char* e = getenv("PB_IMMA_GRADW");
-    on = e ? atoi(e) : 0;
-  }
-  return on != 0;
+// Backend choice is a function of the shape alone (no environment switch, no
+// fallback): ring GEMMs of >= 2^26 u64 MACs run on the tcgen05 int8 tensor
+// cores (pb_tc.cu), conv weight gradients (skinny outputs, long K: the
+// CUDA-core tiles need split-K atomics) from 2^24; smaller ones on the u64
+// CUDA-core kernels, whose single launch beats the tensor path's digit-plane
+// passes there (profiles/r02_ring_gemm_backends.jsonl).  pb_ring_conv_ex /
+// pb_ring_matmul_ex take the backend explicitly (the parity tests run every
+// backend on every shape).
+static int auto_backend(int kind, int64_t macs) {
+  const int64_t min_macs = kind == PB_CONV_GRADW ? (1ll << 24) : (1ll << 26);
+  return macs >= min_macs ? PB_BACKEND_TENSOR : PB_BACKEND_CUDA_CORE;
 }
 
 extern "C" int pb_ring_conv(int kind, const uint64_t* a, const uint64_t* b, int32_t B, int32_t c_i, int32_t c_o,
                             int32_t H, int32_t W, int32_t s, int32_t pad, int32_t stride, int32_t ell, uint64_t* out,
                             void* stream) {
+  return pb_ring_conv_ex(kind, a, b, B, c_i, c_o, H, W, s, pad, stride, ell, out, PB_BACKEND_AUTO, stream);
+}
+
+extern "C" int pb_ring_conv_ex(int kind, const uint64_t* a, const uint64_t* b, int32_t B, int32_t c_i, int32_t c_o,
+                               int32_t H, int32_t W, int32_t s, int32_t pad, int32_t stride, int32_t ell, uint64_t* out,
+                               int32_t backend, void* stream) {
   if (!a || !b || !out) return pb_set_error(PB_ERR_ARG, "null argument");
   if (B < 1 || c_i < 1 || c_o < 1 || s < 1 || pad < 0 || stride < 1 || H + 2 * pad < s || W + 2 * pad < s)
     return pb_set_error(PB_ERR_GEOMETRY, "bad conv geometry");
@@ -374,15 +374,9 @@ extern "C" int pb_ring_conv(int kind, const uint64_t* a, const uint64_t* b, int3
   const int64_t big = (int64_t)B * (c_i > c_o ? c_i : c_o) * (H > oh ? H : oh) * (W > ow ? W : ow);
   if (big >= (1ll << 31) || (int64_t)c_o * c_i * s * s >= (1ll << 31))
     return pb_set_error(PB_ERR_GEOMETRY, "conv tensor too large for 32-bit indexing");
-  {
-    const int64_t macs = (int64_t)B * c_o * c_i * s * s * oh * ow;
-    // the weight gradient's skinny int8 GEMMs (64 x 1600 outputs, K = B*oh*ow) lose to the CUDA-core path
-    if (imma_enabled() && (kind != PB_CONV_GRADW || imma_gradw()) && macs >= IMMA_MIN_MACS &&
-        pb_imma_conv(kind, a, b, B, c_i, c_o, H, W, s, pad, stride, oh, ow, ell, out, st) == PB_OK) {
-      PB_CHECK_LAUNCH();
-      return PB_OK;
-    }
-  }
+  if (backend < PB_BACKEND_AUTO || backend > PB_BACKEND_TENSOR) return pb_set_error(PB_ERR_ARG, "bad backend");
+  if (backend == PB_BACKEND_AUTO) backend = auto_backend(kind, (int64_t)B * c_o * c_i * s * s * oh * ow);
+  if (backend == PB_BACKEND_TENSOR) return pb_tc_conv(kind, a, b, B, c_i, c_o, H, W, s, pad, stride, oh, ow, ell, out, st);
   switch (s) {  // tiled implicit GEMM for the kernel sizes the models use
     case 1: conv_gemm_launch<1>(kind, d, a, b, m, out, st); PB_CHECK_LAUNCH(); return PB_OK;
     case 3: conv_gemm_launch<3>(kind, d, a, b, m, out, st); PB_CHECK_LAUNCH(); return PB_OK;
@@ -465,6 +459,11 @@ extern "C" int pb_ring_matmul_add(const uint64_t* a, const uint64_t* b, int64_t 
 
 extern "C" int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m, int trans_a,
                               int trans_b, int32_t ell, uint64_t* out, void* stream) {
+  return pb_ring_matmul_ex(a, b, n, k, m, trans_a, trans_b, ell, out, PB_BACKEND_AUTO, stream);
+}
+
+extern "C" int pb_ring_matmul_ex(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m, int trans_a,
+                                 int trans_b, int32_t ell, uint64_t* out, int32_t backend, void* stream) {
   if (n > 0 && m > 0 && k > 0 && (!a || !b || !out)) return pb_set_error(PB_ERR_ARG, "null argument");
   if (n <= 0 || m <= 0) return PB_OK;
   if (k < 0 || n * k >= (1ll << 31) || k * m >= (1ll << 31) || n * m >= (1ll << 31))
@@ -475,13 +474,12 @@ extern "C" int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, i
     cudaMemsetAsync(out, 0, (size_t)(n * m) * sizeof(uint64_t), st);
     return PB_OK;
   }
+  if (backend < PB_BACKEND_AUTO || backend > PB_BACKEND_TENSOR) return pb_set_error(PB_ERR_ARG, "bad backend");
+  if (backend == PB_BACKEND_AUTO) backend = auto_backend(-1, n * k * m);
+  if (backend == PB_BACKEND_TENSOR)
+    return pb_tc_matmul(a, b, (int)n, (int)k, (int)m, trans_a, trans_b, ell, out, st);
   if (n * k * m < (1ll << 24)) {  // the FC layers' local terms: one small launch beats tiles + split-K passes
     pb_launch_ring_matmul_small(a, b, n, k, m, trans_a, trans_b, nullptr, 0, mask, out, st);
-    PB_CHECK_LAUNCH();
-    return PB_OK;
-  }
-  if (imma_enabled() && n * k * m >= IMMA_MIN_MACS &&
-      pb_imma_matmul(a, b, (int)n, (int)k, (int)m, trans_a, trans_b, ell, out, st) == PB_OK) {
     PB_CHECK_LAUNCH();
     return PB_OK;
   }

@@ -1,0 +1,354 @@
+// pb_tc.cu — the Z_{2^64} ring GEMMs of the conv / FC local terms
+// (K:206-218 matmul_wrap, K:260-278 conv2d_wrap and the protocols' im2col
+// lowerings) on the int8 TENSOR CORES, hand-written for sm_100a:
+// tcgen05.mma kind::i8 with TMA-staged operands and TMEM accumulators.
+//
+// A u64 operand < 2^59 is written in balanced base-256 digits
+// a = sum_{i<8} a_i 256^i, a_i in [-128, 127], so
+//   a * b mod 2^64 = sum_{s<8} 256^s C_s,   C_s = sum_{i+j=s} a_i b_j
+// (digit pairs with i + j >= 8 vanish mod 2^64): 36 int8 x int8 -> int32
+// products per K step.  One CTA owns a 128 x 64 output tile and keeps ALL
+// EIGHT C_s accumulators in tensor memory at once (8 x 64 columns = the
+// whole 512-column TMEM), so the shift-and-add combine runs in the epilogue
+// straight out of TMEM (tcgen05.ld) -- no int32 partial products in HBM.
+// Exactness: |C_s| <= (s+1) K_cta 2^14 with balanced digits; C_0..C_3 must be
+// exact (they are shifted by < 32 bits) which holds for K_cta <= 16384
+// (|C_3| <= 2^30); C_4..C_7 are only needed mod 2^(64-8s) <= 2^32, so int32
+// wrap-around is harmless.  Longer contractions are split over CTAs
+// (gridDim.z) and summed with u64 atomics (exact mod 2^64).
+//
+// Pipeline per CTA (128 threads, one CTA per SM: 192 KB of shared memory):
+//   warp 0 lane 0  TMA producer: per 64-byte K block one 3-D tensor copy of
+//                  the 8 digit planes of the 128-row P tile and one of the
+//                  64-row Q tile (SWIZZLE_64B), 2-stage full/empty mbarriers
+//   warp 1 lane 0  MMA issuer: 2 x 36 tcgen05.mma (M=128, N=64, K=32) per
+//                  block, tcgen05.commit releases the stage
+//   warps 0-3      epilogue: tcgen05.ld 32x32b of the 8 accumulators,
+//                  u64 combine, scatter through the operator's output map.
+// The digit planes ([8][rows][Kp] int8, plane-major) are produced by
+// k_tc_digits from the u64 operands with the conv pad / stride / dilation
+// gathers applied on the fly (no im2col buffer of u64 values).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "pb_common.cuh"
+#include "pb_gemm_maps.cuh"
+
+namespace {
+
+constexpr int TC_BM = 128;              // P rows per tile (UMMA M)
+constexpr int TC_BN = 64;               // Q rows per tile (UMMA N)
+constexpr int TC_BK = 64;               // K bytes per pipeline stage (SWIZZLE_64B row)
+constexpr int TC_STAGES = 2;
+constexpr int TC_A_PLANE = TC_BM * TC_BK;        // 8 KB
+constexpr int TC_B_PLANE = TC_BN * TC_BK;        // 4 KB
+constexpr int TC_A_STAGE = 8 * TC_A_PLANE;       // 64 KB
+constexpr int TC_B_STAGE = 8 * TC_B_PLANE;       // 32 KB
+constexpr int TC_STAGE = TC_A_STAGE + TC_B_STAGE;
+constexpr int TC_SMEM = TC_STAGES * TC_STAGE + 1024 + 128;
+constexpr int TC_KMAX = 16384;          // contraction per CTA keeping C_0..C_3 exact in int32
+
+// instruction descriptor: D s32, A/B signed int8, both K-major, M = 128, N = 64
+constexpr uint32_t TC_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
+                              ((uint32_t)(TC_BM >> 4) << 24);
+
+// shared-memory matrix descriptor, K-major SWIZZLE_64B: 8-row atoms of 64-byte
+// rows (512 B, the stride-dimension byte offset), version 1 (sm_100)
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(TC_IDESC), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15},"
+      " [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+// Output-map of one launch: D[p][q] (P side rows x Q side rows) is element
+// (row, col) = swap ? (q, p) : (p, q) of the operator's n x m output.
+struct TcEpi {
+  GemmMap d;
+  int swap;
+};
+
+__global__ void __launch_bounds__(128, 1)
+    k_tc_ring_gemm(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ, TcEpi e, int P,
+                   int Q, int kb_per_split, int kb_total, uint64_t mask, int atomic, uint64_t* __restrict__ out) {
+  extern __shared__ uint8_t tc_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE);
+  uint64_t* empty = full + TC_STAGES;
+  uint64_t* done = empty + TC_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p0 = blockIdx.x * TC_BM, q0 = blockIdx.y * TC_BN;
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int nkb = min(kb_total, kb0 + kb_per_split) - kb0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    mbar_init_fence();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmP)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
+  }
+  if (warp == 0) {  // the whole TMEM: 8 accumulators x 64 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {  // ---- TMA producer
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % TC_STAGES;
+      const uint32_t ph = (uint32_t)(i / TC_STAGES) & 1u;
+      if (i >= TC_STAGES) mbar_wait(&empty[s], ph ^ 1u);
+      uint8_t* st = smem + s * TC_STAGE;
+      mbar_expect_tx(&full[s], TC_STAGE);
+      const int kc = (kb0 + i) * TC_BK;
+      tma_load_3d(st, &tmP, kc, p0, 0, &full[s]);
+      tma_load_3d(st + TC_A_STAGE, &tmQ, kc, q0, 0, &full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {  // ---- MMA issuer
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % TC_STAGES;
+      const uint32_t ph = (uint32_t)(i / TC_STAGES) & 1u;
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      const uint32_t a0 = smem_addr(smem + s * TC_STAGE), b0 = a0 + TC_A_STAGE;
+#pragma unroll
+      for (int kk = 0; kk < TC_BK / 32; ++kk) {
+        // A digit d against B digits 0 .. 7-d: consecutive MMAs feed different
+        // accumulators C_{d+e} (no read-after-write chain on one TMEM tile)
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          const uint64_t da = tc_desc(a0 + d * TC_A_PLANE + kk * 32);
+#pragma unroll
+          for (int e = 0; e < 8 - d; ++e) {
+            const uint64_t db = tc_desc(b0 + e * TC_B_PLANE + kk * 32);
+            tc_mma(tmem + (d + e) * TC_BN, da, db, (i > 0 || kk > 0 || d > 0) ? 1u : 0u);
+          }
+        }
+      }
+      tc_commit(&empty[s]);  // the stage is free once these MMAs have read it
+    }
+    tc_commit(done);
+  }
+  __syncwarp();
+  // ---- epilogue: warp w reads TMEM lanes 32w..32w+31 = tile rows p0 + 32w + lane
+  mbar_wait(done, 0);
+  tc_fence_after();
+  const int p = p0 + warp * 32 + lane;
+  const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+  for (int c = 0; c < TC_BN / 16; ++c) {
+    uint32_t v[8][16];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) tmem_ld16(tl + s * TC_BN + c * 16, v[s]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (p < P) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int q = q0 + c * 16 + j;
+        if (q >= Q) break;
+        uint64_t acc = 0;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) acc += (uint64_t)(int64_t)(int32_t)v[s][j] << (8 * s);
+        const size_t o = e.swap ? gemm_out(e.d, q, p) : gemm_out(e.d, p, q);
+        if (atomic) atomicAdd(reinterpret_cast<unsigned long long*>(out + o), (unsigned long long)acc);
+        else out[o] = acc & mask;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+// Balanced base-256 digit planes of one side, plane-major [8][rows][Kp]:
+// side 0 = the output-row operand (gemm_a), side 1 = the output-column one
+// (gemm_b); entries k >= kc (the chunk's tail up to Kp) are zero.  Four
+// consecutive contraction entries per thread: one 32-bit store per plane.
+__global__ void k_tc_digits(GemmMap d, int side, const uint64_t* __restrict__ src, int rows, int k0, int kc, int Kp,
+                            uint64_t mask, int8_t* __restrict__ out) {
+  const int q4 = Kp / 4;
+  const int64_t total = (int64_t)rows * q4;
+  const size_t plane = (size_t)rows * Kp;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(e / q4), kk = 4 * (int)(e - (int64_t)row * q4);
+    uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int k = kk + t;
+      uint64_t v = 0;
+      if (k < kc) v = (side == 0 ? gemm_a(d, src, row, k0 + k) : gemm_b(d, src, k0 + k, row)) & mask;
+      int8_t g[8];
+      digits8(v, g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] |= (uint32_t)(uint8_t)g[i] << (8 * t);
+    }
+    uint32_t* o = reinterpret_cast<uint32_t*>(out + (size_t)row * Kp + kk);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i * (plane / 4)] = w[i];
+  }
+}
+
+__global__ void k_tc_mask(uint64_t* v, int64_t n, uint64_t m) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] &= m;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// Tensor map over planes [8][rows][Kp] int8: box = 64 K bytes x box_rows x 8 planes, SWIZZLE_64B.
+bool plane_map(CUtensorMap* tm, const int8_t* base, int rows, int Kp, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, 8};
+  const cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)rows * (cuuint64_t)Kp};
+  const cuuint32_t box[3] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows, 8};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+// out (n x m, through d's output map) = A (n x K) . B (K x m) mod 2^ell on the
+// tensor cores.  Contractions are processed in chunks whose digit planes stay
+// under ~512 MB; within a chunk the K blocks split over gridDim.z so that the
+// grid covers the GPU, partial sums meeting in u64 atomics.
+int pb_tc_ring_gemm(const GemmMap& d, const uint64_t* A, const uint64_t* Bm, int n, int64_t K, int m, int ell,
+                    uint64_t* out, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_tc_ring_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) != cudaSuccess)
+      return pb_set_error(PB_ERR_CUDA, "tcgen05 GEMM: shared-memory opt-in failed");
+    // the digit planes are stream-ordered allocations: keep them cached in the
+    // device's default pool instead of unmapping at every synchronisation
+    // (re-mapping hundreds of MB per call costs milliseconds)
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    attr = true;
+  }
+  if (!encode_fn()) return pb_set_error(PB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const uint64_t mask = ell >= 64 ? ~0ull : ((1ull << ell) - 1);
+  const int swap = n < m;  // the longer output side takes the 128-row UMMA M dimension
+  const int P = swap ? m : n, Q = swap ? n : m;
+  const int p_side = swap ? 1 : 0;
+  // chunk the contraction: planes of one chunk (8 (P + Q) Kc bytes) <= 512 MB
+  int64_t Kc = ((int64_t)512 << 20) / (8 * (int64_t)(P + Q));
+  Kc = Kc / TC_BK * TC_BK;
+  if (Kc < TC_BK) Kc = TC_BK;
+  if (Kc > K) Kc = (K + TC_BK - 1) / TC_BK * TC_BK;
+  const int nchunks = (int)((K + Kc - 1) / Kc);
+  const int tiles = ((P + TC_BM - 1) / TC_BM) * ((Q + TC_BN - 1) / TC_BN);
+  const int kb_chunk = (int)(Kc / TC_BK);
+  int kps = kb_chunk;  // K blocks per CTA
+  while (kps > 1 && (kps * TC_BK > TC_KMAX || (int64_t)tiles * ((kb_chunk + kps - 1) / kps) < 148)) kps = (kps + 1) / 2;
+  while (kps * TC_BK > TC_KMAX) kps = (kps + 1) / 2;
+  const int splits = (kb_chunk + kps - 1) / kps;
+  const int atomic = nchunks > 1 || splits > 1;
+  int8_t *dp = nullptr, *dq = nullptr;
+  if (cudaMallocAsync((void**)&dp, (size_t)8 * P * Kc, st) != cudaSuccess ||
+      cudaMallocAsync((void**)&dq, (size_t)8 * Q * Kc, st) != cudaSuccess)
+    return pb_set_error(PB_ERR_CUDA, "tcgen05 GEMM: digit-plane allocation failed");
+  CUtensorMap tmP, tmQ;
+  if (!plane_map(&tmP, dp, P, (int)Kc, TC_BM) || !plane_map(&tmQ, dq, Q, (int)Kc, TC_BN)) {
+    cudaFreeAsync(dq, st);
+    cudaFreeAsync(dp, st);
+    return pb_set_error(PB_ERR_CUDA, "tcgen05 GEMM: tensor-map encoding failed");
+  }
+  const TcEpi e{d, swap};
+  if (atomic) cudaMemsetAsync(out, 0, (size_t)n * m * sizeof(uint64_t), st);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int64_t k0 = (int64_t)ch * Kc;
+    const int kc = (int)((K - k0) < Kc ? (K - k0) : Kc);
+    const int kb = (kc + TC_BK - 1) / TC_BK;
+    const int sp = (kb + kps - 1) / kps;
+    k_tc_digits<<<pb_grid_1d((int64_t)P * Kc / 4, 256), 256, 0, st>>>(d, p_side, p_side == 0 ? A : Bm, P, (int)k0, kc,
+                                                                       (int)Kc, mask, dp);
+    k_tc_digits<<<pb_grid_1d((int64_t)Q * Kc / 4, 256), 256, 0, st>>>(d, 1 - p_side, p_side == 0 ? Bm : A, Q, (int)k0,
+                                                                       kc, (int)Kc, mask, dq);
+    dim3 grid((unsigned)((P + TC_BM - 1) / TC_BM), (unsigned)((Q + TC_BN - 1) / TC_BN), (unsigned)sp);
+    k_tc_ring_gemm<<<grid, 128, TC_SMEM, st>>>(tmP, tmQ, e, P, Q, kps, kb, mask, atomic, out);
+  }
+  if (atomic) {
+    const int64_t no = (int64_t)n * m;
+    k_tc_mask<<<pb_grid_1d(no, 256), 256, 0, st>>>(out, no, mask);
+  }
+  cudaFreeAsync(dq, st);
+  cudaFreeAsync(dp, st);
+  return cudaPeekAtLastError() == cudaSuccess ? PB_OK : pb_set_error(PB_ERR_CUDA, "tcgen05 GEMM launch failed");
+}
+
+int pb_tc_conv(int kind, const uint64_t* a, const uint64_t* b, int B, int ci, int co, int H, int W, int s, int p,
+               int st_, int oh, int ow, int ell, uint64_t* out, cudaStream_t st) {
+  GemmMap d = {};
+  d.kind = kind, d.B = B, d.ci = ci, d.co = co, d.H = H, d.W = W, d.s = s, d.p = p, d.st = st_, d.oh = oh, d.ow = ow;
+  int n, m;
+  int64_t K;
+  const uint64_t *A, *Bm;
+  if (kind == PB_CONV_FWD) { n = co; K = (int64_t)ci * s * s; m = B * oh * ow; A = b; Bm = a; }      // A = W, B = X
+  else if (kind == PB_CONV_BWDX) { n = ci; K = (int64_t)co * s * s; m = B * H * W; A = b; Bm = a; }  // A = W, B = dY
+  else { n = co; K = (int64_t)B * oh * ow; m = ci * s * s; A = b; Bm = a; }                          // A = dY, B = X
+  return pb_tc_ring_gemm(d, A, Bm, n, K, m, ell, out, st);
+}
+
+int pb_tc_matmul(const uint64_t* a, const uint64_t* b, int n, int k, int m, int ta, int tb, int ell, uint64_t* out,
+                 cudaStream_t st) {
+  GemmMap d = {};
+  d.kind = 3, d.n = n, d.k = k, d.m = m, d.ta = ta, d.tb = tb;
+  return pb_tc_ring_gemm(d, a, b, n, k, m, ell, out, st);
+}

@@ -218,3 +218,21 @@ def test_encrypt_sk_launch_cap(setup):
             _lib.call("pb_set_launch_cap", 0)
         assert np.array_equal(_dev.to_numpy_u32(got.data), ref), cap
     assert np.array_equal(_dev.to_numpy_u64(bfv.decrypt(kp, got)), m)
+
+
+@pytest.mark.parametrize("mode", ["pk", "sk"])
+def test_encrypt_without_rng_is_randomized(setup, mode):
+    """SPEC:139-147's encrypt(pk, m) takes no rng: two default-argument
+    encryptions of the same m differ (fresh entropy per call) and both decrypt to m."""
+    import torch
+
+    from paper_2403_11166_b200 import bfv
+
+    N = setup["N"]
+    m = torch.from_numpy((np.arange(2 * N, dtype=np.uint64) * 977 & T_MASK).view(np.int64)).cuda()
+    c1 = bfv.encrypt(setup["pkp"], m, mode=mode)
+    c2 = bfv.encrypt(setup["pkp"], m, mode=mode)
+    assert not torch.equal(c1.data, c2.data)
+    assert not torch.equal(c1.data[:, 1], c2.data[:, 1])
+    for c in (c1, c2):
+        assert torch.equal(bfv.decrypt(setup["pkp"], c), m.view(2, N))

@@ -267,7 +267,7 @@ def test_ring_neg_scalar_mul_decode_to_signed_match_reference():
     assert np.array_equal(PRG.decode_fixed(e.values, pr, 50).cpu().numpy(), g["edge_dec_f50"])
     assert np.array_equal(PRG.decode_fixed(g["enc_f25"], pr).cpu().numpy(), g["dec_f25"])
     # round trip through the device encoder, including the range edge
-    x = np.array([0.0, -1.0, 2.5, -(2.0 ** 33) + 2.0 ** -25, 2.0 ** 33 - 2.0 ** -25, 1e-9, -1e-9])
+    x = np.array([0.0, -1.0, 2.5, -(2.0 ** 33) + 2.0 ** -18, 2.0 ** 33 - 2.0 ** -18, 1e-9, -1e-9])
     enc = PRG.encode_fixed(x, pr)
     assert np.array_equal(enc.cpu().numpy().view(np.uint64), OR.encode_fixed(x, RING))
     assert np.array_equal(PRG.decode_fixed(enc, pr).cpu().numpy(), OR.decode_fixed(OR.encode_fixed(x, RING), RING))
