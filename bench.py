@@ -246,7 +246,7 @@ def run_ours(args, rank, world):
     # ---- timed region: the same step replayed from CUDA graphs (GraphStep),
     #      batch resident in HBM, per-step CUDA events, L2 flushed between steps
     try:
-        runner = PN.GraphStep(sess, model, x_dev, prefetch_input=os.environ.get("PB_PREFETCH_INPUT", "1") == "1")
+        runner = PN.GraphStep(sess, model, x_dev, prefetch_input=True)
         replay = "CUDA graphs"
     except Exception as exc:  # e.g. a collective backend that cannot be captured
         if world == 1:

@@ -211,6 +211,40 @@ __device__ __forceinline__ void uniform_pair(uint64_t seed, uint64_t nonce, int6
   x1 = (uint32_t)__umul64hi(b, q);
 }
 
+// The encryption noise e ~ CBD(20) of P polynomials, int8 [P][N], drawn ONCE
+// per polynomial (it is the same integer polynomial in every RNS limb) by
+// T = N/32 threads per polynomial: thread tid owns coefficients tid + T c,
+// c < 32, three per Philox4x32-10 call keyed (seed, "ENC5") at counter
+// ((tid << 4) | g, p + nonce).  k_encrypt_sk's L limb CTAs then read it from
+// L2 instead of each redrawing it (7x less RNG work for the noise at L = 7).
+__global__ void __launch_bounds__(256) k_enc_noise(int logN, int64_t nP, uint64_t seed_arg, const uint64_t* seed_dev,
+                                                   uint64_t nonce, int8_t* __restrict__ e) {
+  const uint64_t seed = dev_key(seed_arg, seed_dev);
+  const int T = 1 << (logN - 5);
+  const int64_t total = nP * T;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = x >> (logN - 5);
+    const int tid = (int)(x & (T - 1));
+    const uint64_t pp = (uint64_t)p + nonce;
+    int8_t* ep = e + (p << logN) + tid;
+#pragma unroll
+    for (int g = 0; g < 11; ++g) {
+      const u32x4 r = philox4x32_10(((uint32_t)tid << 4) | (uint32_t)g, (uint32_t)pp, (uint32_t)(pp >> 32),
+                                    0x454e4335u /* "ENC5" */, (uint32_t)seed, (uint32_t)(seed >> 32));
+      int sv[3];
+      cbd20x3(r, sv);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        if (3 * g + i < 32) ep[(size_t)(3 * g + i) * T] = (int8_t)sv[i];
+    }
+  }
+}
+
+// Symmetric encryption, one CTA per (polynomial, limb) row: c0 = NTT(e +
+// Delta m) - a s, c1 = a, with e from k_enc_noise (or the caller's noise in
+// the bit-exact oracle runs) and a uniform in the NTT domain drawn here (four
+// residues per Philox call).  Under a launch cap (background preparation) a
+// CTA loops over R consecutive rows in polynomial-major order.
 template <int LOGN>
 __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
     k_encrypt_sk(PbDev P, const uint32_t* sk, PbPack src, int64_t nP, const uint32_t* a_in, const int8_t* e,
@@ -222,19 +256,12 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
   const int tid = threadIdx.x;
   const int L = P.L;
   const int64_t rows = nP * L;
-  // Rows per CTA: 1 (one row per CTA, limb-major so co-resident CTAs share one
-  // limb's twiddles), or R > 1 under a launch cap: then a CTA takes R
-  // consecutive rows in polynomial-major order and draws each polynomial's
-  // noise once, packed int8 in shared memory past the NTT's area, for all of
-  // its limbs (the noise is the same integer polynomial in every limb).
   const int64_t R = (rows + gridDim.x - 1) / gridDim.x;
-  uint32_t* e_sm = sm + Nt::SMEM_WORDS;  // [8][T] words: word k of thread tid holds its coefficients 4k..4k+3
-  int64_t noise_p = -1;
   for (int64_t it = 0; it < R; ++it) {
   int l;
   int64_t p;
   if (R == 1) {
-    l = (int)(blockIdx.x / nP);
+    l = (int)(blockIdx.x / nP);  // limb-major: co-resident CTAs share one limb's twiddles
     p = blockIdx.x % nP;
   } else {
     const int64_t row = blockIdx.x * R + it;
@@ -245,52 +272,14 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
   }
   const uint32_t q = P.q[l];
   const uint64_t mu = P.mu[l];
-  const int8_t* ep = e ? e + p * N : nullptr;
+  const int8_t* ep = e + p * N;
+  int8_t ev[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) ev[c] = ep[Nt::j1(tid, c)];  // issued ahead of the source gather
   uint32_t b[32];
   load_source<Nt>(b, sm, src, p, tid, [&](uint64_t v) { return delta_m(P, l, v); });
-  if (ep) {  // caller-supplied noise (bit-exact oracle runs)
 #pragma unroll
-    for (int c = 0; c < 32; ++c) b[c] = addmod(lift_small(ep[Nt::j1(tid, c)], q), b[c], q);
-  } else if (R == 1) {  // e ~ CBD(20) from Philox4x32, generated in-kernel: one call covers three of this thread's coefficients
-    const uint64_t pp = (uint64_t)p + nonce;
-#pragma unroll
-    for (int g = 0; g < 11; ++g) {
-      const u32x4 r = philox4x32_10(((uint32_t)tid << 4) | (uint32_t)g, (uint32_t)pp, (uint32_t)(pp >> 32),
-                                    0x454e4335u /* "ENC5" */, (uint32_t)seed, (uint32_t)(seed >> 32));
-      int sv[3];
-      cbd20x3(r, sv);
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-        if (3 * g + i < 32) b[3 * g + i] = addmod(lift_small(sv[i], q), b[3 * g + i], q);
-    }
-  } else {  // the same draw, once per polynomial (thread-private words: no barrier)
-    if (p != noise_p) {
-      noise_p = p;
-      const uint64_t pp = (uint64_t)p + nonce;
-      uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-      for (int g = 0; g < 11; ++g) {
-        const u32x4 r = philox4x32_10(((uint32_t)tid << 4) | (uint32_t)g, (uint32_t)pp, (uint32_t)(pp >> 32),
-                                      0x454e4335u /* "ENC5" */, (uint32_t)seed, (uint32_t)(seed >> 32));
-        int sv[3];
-        cbd20x3(r, sv);
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          const int c = 3 * g + i;
-          if (c < 32) w[c >> 2] |= ((uint32_t)sv[i] & 0xFFu) << (8 * (c & 3));
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) e_sm[k * Nt::T + tid] = w[k];
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t w = e_sm[k * Nt::T + tid];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        b[4 * k + i] = addmod(lift_small((int)(w << (24 - 8 * i)) >> 24, q), b[4 * k + i], q);
-    }
-  }
+  for (int c = 0; c < 32; ++c) b[c] = addmod(lift_small(ev[c], q), b[c], q);
   Nt::forward(b, sm, P.tw_fwd + (size_t)l * N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
   // c1 = a, c0 = NTT(e + Delta m) - a*s, one 128-bit device-order vector at a
   // time (keeps a and s out of the register file: 32 live residues, not 96)
@@ -392,14 +381,11 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
   }
 }
 
-__constant__ int g_prune_inv = 1;  // (a device constant so an experiment can switch it off)
-
 // Number of low index bits (<= 5) that are 1 in every useful slot of a ciphertext:
 // its inverse NTT can be output-pruned by that many stages (Ntt::inverse_pruned).
 // Block-wide AND over the slot list; `flag` is a shared int (synchronised).
 template <class Nt>
 __device__ __forceinline__ int common_low_ones(const int32_t* pos, int U, int tid, int* flag) {
-  if (!g_prune_inv) return 0;
   if (tid == 0) *flag = -1;
   __syncthreads();
   int acc = -1;
@@ -721,8 +707,8 @@ void launch_encrypt_sk(const PbDev& P, const uint32_t* sk, PbPack src, int64_t n
                        uint64_t seed, const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct, cudaStream_t st) {
   using Nt = pb::Ntt<LOGN>;
   const int64_t grid = pb_row_grid(nP * P.L);
-  const size_t smem = Nt::SMEM_WORDS * 4 + (grid < nP * P.L ? Nt::N : 0);  // + packed noise when capped
-  set_smem(k_encrypt_sk<LOGN>, Nt::SMEM_WORDS * 4 + Nt::N);
+  const size_t smem = Nt::SMEM_WORDS * 4;
+  set_smem(k_encrypt_sk<LOGN>, smem);
   k_encrypt_sk<LOGN><<<(unsigned)grid, Nt::T, smem, st>>>(P, sk, src, nP, a_in, e, seed, seed_dev, nonce, ct);
 }
 
@@ -891,8 +877,15 @@ extern "C" int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk, const uint64
   if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
   PB_PACK_OR_RETURN(src, vals, pack_pos, pack_src, Z);
   cudaStream_t st = pb_stream_of(stream);
+  // the noise polynomials first (stream-ordered scratch, graph-capturable)
+  int8_t* e = nullptr;
+  if (cudaMallocAsync((void**)&e, (size_t)nP << ctx->dev.logN, st) != cudaSuccess)
+    return pb_set_error(PB_ERR_CUDA, "encryption noise scratch allocation failed");
+  const int64_t thr = nP << (ctx->dev.logN - 5);
+  k_enc_noise<<<pb_row_grid((thr + 255) / 256), 256, 0, st>>>(ctx->dev.logN, nP, seed, seed_dev, nonce, e);
   PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, src, nP, (const uint32_t*)nullptr,
-                   (const int8_t*)nullptr, seed, seed_dev, nonce, ct, st);
+                   (const int8_t*)e, seed, seed_dev, nonce, ct, st);
+  cudaFreeAsync(e, st);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }
@@ -950,24 +943,11 @@ extern "C" int pb_decrypt_to_share(const pb_ctx* ctx, const uint32_t* sk, const 
   if (nP <= 0 || U <= 0) return PB_OK;
   if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
   cudaStream_t st = pb_stream_of(stream);
-  static const int cluster_on = [] {  // PB_DEC_CLUSTER=0: the two-kernel path (INTT to scratch, then decode)
-    const char* v = getenv("PB_DEC_CLUSTER");
-    return v ? atoi(v) : 1;
-  }();
-  static const bool prune_set = [] {  // PB_PRUNE_INV=0: full inverse NTTs (experiment knob)
-    const char* v = getenv("PB_PRUNE_INV");
-    if (v && atoi(v) == 0) {
-      const int off = 0;
-      cudaMemcpyToSymbol(g_prune_inv, &off, sizeof(off));
-    }
-    return true;
-  }();
-  (void)prune_set;
   // fused cluster kernel (one launch, DSMEM limb exchange) when the decode is
   // light; with many useful slots per ciphertext the separate decode kernel's
   // parallelism wins (B200, graph-timed: U = 256 x 32 cts 12.3 vs 13.9 us,
   // U = 512 x 16 cts 12.2 vs 10.7 us, U = 2041 x 50 cts 27.5 vs 19.2 us)
-  if (cluster_on && U < 384 && ctx->dev.logN == 13 && ctx->dev.L >= 2) {
+  if (U < 384 && ctx->dev.logN == 13 && ctx->dev.L >= 2) {
     const int rc = launch_decrypt_share_cluster<13>(ctx->dev, sk, ct, nP, out_pos, out_dst, U, share_out, st);
     if (rc != 0) return pb_set_error(PB_ERR_CUDA, cudaGetErrorString((cudaError_t)rc));
     PB_CHECK_LAUNCH();

@@ -7,12 +7,13 @@
 //   k_mask_ntt    one CTA per (output, limb): builds Delta*(mask + filler) in
 //                 shared memory, forward NTT in registers, writes -mask into
 //                 the output's c0 row (device order);
-//   k_mac_pipe    (nI >= 3) a 2x2 tile of outputs per CTA and a 512-coefficient
-//                 slice of one limb: per input block the operand row slices
-//                 are copied into a 3-stage shared-memory ring by the TMA
-//                 engine (cp.async.bulk + mbarrier), every ct / pt vector is
-//                 reused across the tile, products accumulate lazily in u64
-//                 (one IMAD.WIDE per mod-MAC), written once;
+//   k_mac_ws      (nI >= 3) a 2x2 (or 1x2) tile of outputs per CTA and a
+//                 512-coefficient slice of one limb: per input block the
+//                 operand row slices are copied into a 4-stage shared-memory
+//                 ring by a producer warp driving the TMA engine
+//                 (cp.async.bulk + mbarrier), every ct / pt vector is reused
+//                 across the tile, products accumulate lazily in u64 (one
+//                 IMAD.WIDE per mod-MAC), written once;
 //   k_mac_eager   (nI <= 2) the same tile from registers with per-term
 //                 Montgomery reduction (nothing to amortise a lazy reduction).
 // Plaintexts are stored in Montgomery form (pt*2^32 mod q), so no Shoup
@@ -133,7 +134,7 @@ template <> struct Vec<2> {
   __device__ __forceinline__ static T zero() { return make_uint2(0, 0); }
 };
 
-// Lazy 64-bit accumulation (used by k_mac_pipe): a product x * w~ (x < q,
+// Lazy 64-bit accumulation (k_mac_ws): a product x * w~ (x < q,
 // w~ = w 2^32 mod q, both < 2^30) is < 2^60, so 14 products plus a reduced
 // residue (< 2^30) fit a u64 -- a mod-MAC is ONE IMAD.WIDE.U32 (fma pipe)
 // instead of a Montgomery multiply + two conditional subtractions (alu pipe,
@@ -162,158 +163,11 @@ struct PipeCfg {
   static constexpr int SLOTS_B = 2 * TO + TB;
 };
 
-template <int TB, int TO, int V, int STAGES, int MINB = 1>
-__global__ void __launch_bounds__(MAC_THREADS, MINB)
-    k_mac_pipe(PbDev P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB, int nB,
-               int nO, int nI, uint32_t* ct_out) {
-  using C = PipeCfg<TB, TO, V>;
-  using VT = typename Vec<V>::T;
-  extern __shared__ __align__(128) uint8_t pipe_sm[];
-  __shared__ __align__(8) uint64_t full[STAGES];
-  // compact slot map per stage: [A: ct(b,c) 2*TB, pt(o) TO][B: ct(o,c) 2*TO, pt(b) TB], absent terms take no space
-  const int CA = 0, PA = 2 * TB, CB = ctA ? C::SLOTS_A : 0, PB = CB + 2 * TO;
-  const int nslots = (ctA ? C::SLOTS_A : 0) + (ctB ? C::SLOTS_B : 0);
-  const int N = P.N, L = P.L;
-  const int slices = N / (V * MAC_THREADS);
-  const int tilesO = (nO + TO - 1) / TO;
-  const int tb = blockIdx.x / tilesO, to = blockIdx.x % tilesO;
-  const int l = blockIdx.y / slices, sl = blockIdx.y % slices;
-  const uint32_t q = P.q[l], qn = P.qn[l];
-  const uint64_t mu = P.mu[l];
-  const int tid = threadIdx.x;
-  const size_t rowb = (size_t)N * 4;        // bytes per residue row
-  const size_t off = (size_t)sl * C::SLOT;  // byte offset of this slice in a row
-  bool okb[TB], oko[TO];
-#pragma unroll
-  for (int i = 0; i < TB; ++i) okb[i] = tb * TB + i < nB;
-#pragma unroll
-  for (int o = 0; o < TO; ++o) oko[o] = to * TO + o < nO;
-
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
-    mbar_init_fence();
-  }
-  __syncthreads();
-  auto issue = [&](int k, int s) {
-    const uint8_t* A8 = reinterpret_cast<const uint8_t*>(ctA);
-    const uint8_t* PA8 = reinterpret_cast<const uint8_t*>(ptA);
-    const uint8_t* B8 = reinterpret_cast<const uint8_t*>(ctB);
-    const uint8_t* PB8 = reinterpret_cast<const uint8_t*>(ptB);
-    uint8_t* st = pipe_sm + (size_t)s * nslots * C::SLOT;
-    uint32_t n = 0;
-#pragma unroll
-    for (int i = 0; i < TB; ++i) n += (okb[i] ? 1u : 0u) * ((ctA ? 2u : 0u) + (ctB ? 1u : 0u));
-#pragma unroll
-    for (int o = 0; o < TO; ++o) n += (oko[o] ? 1u : 0u) * ((ctA ? 1u : 0u) + (ctB ? 2u : 0u));
-    mbar_expect_tx(&full[s], n * C::SLOT);
-#pragma unroll
-    for (int i = 0; i < TB; ++i) {
-      if (!okb[i]) continue;
-      const size_t bi = (size_t)((tb * TB + i) * nI + k);
-      if (ctA) {
-        bulk_g2s(st + (CA + 2 * i) * C::SLOT, A8 + ((bi * 2 + 0) * L + l) * rowb + off, C::SLOT, &full[s]);
-        bulk_g2s(st + (CA + 2 * i + 1) * C::SLOT, A8 + ((bi * 2 + 1) * L + l) * rowb + off, C::SLOT, &full[s]);
-      }
-      if (ctB) bulk_g2s(st + (PB + i) * C::SLOT, PB8 + (bi * L + l) * rowb + off, C::SLOT, &full[s]);
-    }
-#pragma unroll
-    for (int o = 0; o < TO; ++o) {
-      if (!oko[o]) continue;
-      const size_t oi = (size_t)((to * TO + o) * nI + k);
-      if (ctA) bulk_g2s(st + (PA + o) * C::SLOT, PA8 + (oi * L + l) * rowb + off, C::SLOT, &full[s]);
-      if (ctB) {
-        bulk_g2s(st + (CB + 2 * o) * C::SLOT, B8 + ((oi * 2 + 0) * L + l) * rowb + off, C::SLOT, &full[s]);
-        bulk_g2s(st + (CB + 2 * o + 1) * C::SLOT, B8 + ((oi * 2 + 1) * L + l) * rowb + off, C::SLOT, &full[s]);
-      }
-    }
-  };
-  if (tid == 0)
-    for (int k = 0; k < STAGES - 1 && k < nI; ++k) issue(k, k);
-
-  uint64_t acc[TB][TO][2][V];
-#pragma unroll
-  for (int i = 0; i < TB; ++i)
-#pragma unroll
-    for (int o = 0; o < TO; ++o)
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int e = 0; e < V; ++e) acc[i][o][c][e] = 0ull;
-  auto mac = [&](uint64_t (&a)[V], const VT& x, const VT& w) {
-#pragma unroll
-    for (int e = 0; e < V; ++e) a[e] += (uint64_t)Vec<V>::get(x, e) * Vec<V>::get(w, e);
-  };
-  constexpr int SV = C::SLOT / (4 * V);  // vectors per slot
-  for (int k = 0; k < nI; ++k) {
-    const int s = k % STAGES;
-    if (tid == 0 && k + STAGES - 1 < nI) {
-      fence_proxy_async_smem();
-      issue(k + STAGES - 1, (k + STAGES - 1) % STAGES);
-    }
-    mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
-    const VT* st = reinterpret_cast<const VT*>(pipe_sm + (size_t)s * nslots * C::SLOT) + tid;
-    if (ctA) {
-      VT w[TO];
-#pragma unroll
-      for (int o = 0; o < TO; ++o) w[o] = st[(PA + o) * SV];
-#pragma unroll
-      for (int i = 0; i < TB; ++i) {
-        const VT x0 = st[(CA + 2 * i) * SV], x1 = st[(CA + 2 * i + 1) * SV];
-#pragma unroll
-        for (int o = 0; o < TO; ++o) { mac(acc[i][o][0], x0, w[o]); mac(acc[i][o][1], x1, w[o]); }
-      }
-    }
-    if (ctB) {
-      VT u[TB];
-#pragma unroll
-      for (int i = 0; i < TB; ++i) u[i] = st[(PB + i) * SV];
-#pragma unroll
-      for (int o = 0; o < TO; ++o) {
-        const VT y0 = st[(CB + 2 * o) * SV], y1 = st[(CB + 2 * o + 1) * SV];
-#pragma unroll
-        for (int i = 0; i < TB; ++i) { mac(acc[i][o][0], y0, u[i]); mac(acc[i][o][1], y1, u[i]); }
-      }
-    }
-    if ((k + 1) % MAC_CHUNK == 0 && k + 1 < nI) {  // fold below q: the next 7 blocks cannot overflow
-#pragma unroll
-      for (int i = 0; i < TB; ++i)
-#pragma unroll
-        for (int o = 0; o < TO; ++o)
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-#pragma unroll
-            for (int e = 0; e < V; ++e) acc[i][o][c][e] = reduce64(acc[i][o][c][e], q, mu);
-    }
-    __syncthreads();  // stage s fully consumed before it is refilled
-  }
-  auto fin = [&](uint64_t a) { return csub(mont_lazy(reduce64(a, q, mu), 1u, q, qn), q); };  // x 2^-32 mod q
-  VT* out = reinterpret_cast<VT*>(ct_out);
-  const size_t row = (size_t)N / V;
-  const size_t v = (size_t)sl * MAC_THREADS + tid;
-#pragma unroll
-  for (int i = 0; i < TB; ++i)
-#pragma unroll
-    for (int o = 0; o < TO; ++o) {
-      if (!(okb[i] && oko[o])) continue;
-      const size_t r = (size_t)(tb * TB + i) * nO + (to * TO + o);
-      const size_t b0 = (r * 2 * L + l) * row + v;
-      const VT m = out[b0];  // -mask written by k_mask_ntt
-      uint32_t c0[V], c1[V];
-#pragma unroll
-      for (int e = 0; e < V; ++e) {
-        c0[e] = addmod(fin(acc[i][o][0][e]), Vec<V>::get(m, e), q);
-        c1[e] = fin(acc[i][o][1][e]);
-      }
-      out[b0] = Vec<V>::make(c0);
-      out[b0 + (size_t)L * row] = Vec<V>::make(c1);
-    }
-}
-
-// Warp-specialised variant of k_mac_pipe: a fifth warp only issues the TMA
+// Warp-specialised TMA-pipelined MAC: a fifth warp only issues the TMA
 // copies (per-copy address = base + k * stride, precomputed), gated per stage
 // by an "empty" mbarrier the four consumer warps arrive on, so the consumers
-// never wait for the issuing thread at a CTA barrier (ncu on k_mac_pipe: 26%
+// never wait for the issuing thread at a CTA barrier (ncu on the round-1
+// single-role kernel: 26%
 // of stall samples were the per-k __syncthreads behind thread 0's issue work).
 template <int TB, int TO, int V, int STAGES, int MINB = 1, int CT = MAC_THREADS>
 __global__ void __launch_bounds__(CT + 32, MINB)
@@ -496,21 +350,6 @@ void launch_ws(const PbDev& P, const uint32_t* ctA, const uint32_t* ptA, const u
   k_mac_ws<TB, TO, V, STAGES, MINB, CT><<<grid, CT + 32, smem, st>>>(P, ctA, ptA, ctB, ptB, nB, nO, nI, out);
 }
 
-template <int TB, int TO, int V, int STAGES, int MINB = 1>
-void launch_pipe(const PbDev& P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB,
-                 int nB, int nO, int nI, uint32_t* out, cudaStream_t st) {
-  using C = PipeCfg<TB, TO, V>;
-  const size_t smem = (size_t)STAGES * ((ctA ? C::SLOTS_A : 0) + (ctB ? C::SLOTS_B : 0)) * C::SLOT;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_mac_pipe<TB, TO, V, STAGES, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((size_t)STAGES * (C::SLOTS_A + C::SLOTS_B) * C::SLOT));
-    attr = true;
-  }
-  dim3 grid((unsigned)(((nB + TB - 1) / TB) * ((nO + TO - 1) / TO)), (unsigned)(P.L * (P.N / (V * MAC_THREADS))));
-  k_mac_pipe<TB, TO, V, STAGES, MINB><<<grid, MAC_THREADS, smem, st>>>(P, ctA, ptA, ctB, ptB, nB, nO, nI, out);
-}
-
 // Eager variant (Montgomery multiply + reduce per term, u32 accumulators,
 // 96 registers): faster than the lazy kernel when nI <= 2 (no reduction to
 // amortise; the K=1 FC shape is HBM/latency-bound).
@@ -681,19 +520,13 @@ extern "C" int pb_ctpt_mac_tiled(const pb_ctx* ctx, const uint32_t* ctA, const u
   } else {
     // Warp-specialised TMA-pipelined lazy MAC (B200, graph-timed): FC 784x128 fwd
     // 52.7 -> 39.3 us, its grad-W 51.1 -> 45.7 us, conv-like K=16 646 -> 587 us vs
-    // the single-role k_mac_pipe (PB_MAC_VARIANT=1 keeps it for comparison).
-    static const int variant = [] {
-      const char* e = getenv("PB_MAC_VARIANT");
-      return e ? atoi(e) : 0;
-    }();
+    // a single-role pipelined kernel (round 1, removed).
     // Tiles: 2x2, except large two-term evaluations (Alg. 2 cross terms, twice
     // the staged operands per k-step): 1x2, CIFAR conv grad-W 1148 -> 1106 us
     // (profiles/r01_mac_ws_sweep.txt).  The MLP's small two-term grad-W keeps
     // 2x2: 1x2 is 4% faster alone but its extra CTAs crowd the concurrent
-    // input-gradient chain (step A/B).  PB_MAC_VARIANT=2: 2x2 always.
-    if (variant == 1)
-      launch_pipe<2, 2, 4, 3, 6>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
-    else if (ctA && ctB && (int64_t)nB * nO * nI >= 1024 && variant != 2)
+    // input-gradient chain (step A/B).
+    if (ctA && ctB && (int64_t)nB * nO * nI >= 1024)
       launch_ws<1, 2, 4, 4, 4>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
     else
       launch_ws<2, 2, 4, 4, 4>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);

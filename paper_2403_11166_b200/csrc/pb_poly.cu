@@ -51,8 +51,24 @@ static uint32_t h_bitrev(uint32_t x, int bits) {
 }
 
 // ------------------------------------------------------------------ context --
+// Stream-ordered scratch (encryption noise, digit planes) comes from the
+// device's default memory pool: keep freed blocks cached there instead of
+// unmapping them at every synchronisation.
+void pb_keep_pool() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done = true;
+}
+
 extern "C" int pb_ctx_create(const pb_params* p, pb_ctx** out) {
   if (!p || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  pb_keep_pool();
   const int N = p->N, L = p->L;
   int logN = 0;
   while ((1 << logN) < N) ++logN;

@@ -36,6 +36,8 @@
 #include "pb_common.cuh"
 #include "pb_gemm_maps.cuh"
 
+void pb_keep_pool();
+
 namespace {
 
 constexpr int TC_BM = 128;              // P rows per tile (UMMA M)
@@ -272,14 +274,8 @@ int pb_tc_ring_gemm(const GemmMap& d, const uint64_t* A, const uint64_t* Bm, int
     if (cudaFuncSetAttribute(k_tc_ring_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) != cudaSuccess)
       return pb_set_error(PB_ERR_CUDA, "tcgen05 GEMM: shared-memory opt-in failed");
     // the digit planes are stream-ordered allocations: keep them cached in the
-    // device's default pool instead of unmapping at every synchronisation
-    // (re-mapping hundreds of MB per call costs milliseconds)
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
+    // device's default pool (re-mapping hundreds of MB per call costs milliseconds)
+    pb_keep_pool();
     attr = true;
   }
   if (!encode_fn()) return pb_set_error(PB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");

@@ -50,13 +50,11 @@ MSG_GRADB = 0x31
 FRAME_HEADER = 12  # {u16 type, u16 flags, u64 len}
 
 
-import os as _os
-
-_SERIAL = _os.environ.get("PB_SERIAL", "0") == "1"
-_MASK_PREFETCH = _os.environ.get("PB_MASK_PREFETCH", "1") == "1"
-_GRADW_FLIP = _os.environ.get("PB_GRADW_FLIP", "0") == "1"
-_BG_CAP = int(_os.environ.get("PB_BG_CAP", "148"))  # CTA cap of background operand preparation (0: none)
-_PRIO = tuple(int(v) for v in _os.environ["PB_PRIO"].split(",")) if "PB_PRIO" in _os.environ else None
+# Scheduling constants (round-1 A/B measurements under profiles/r01_ab_*):
+_SERIAL = False        # True: every protocol fork on the calling stream (debugging)
+_MASK_PREFETCH = True  # draw all MO masks of a phase up front on a fork
+_GRADW_FLIP = False    # Alg. 2 HE matmul transposed: measured 1.5 % slower
+_BG_CAP = 148          # CTA cap of background operand preparation (0: none)
 
 
 def _stream_like(cur: torch.cuda.Stream) -> torch.cuda.Stream:
@@ -247,20 +245,17 @@ class Session:
     def _side_streams(self):
         """The (DO encrypt, MO encode) side streams forked by he_eval, one pair
         per calling stream so concurrent protocol calls do not serialise.
-        (PB_SERIAL=1: run everything on the calling stream -- an experiment knob.)"""
+        (_SERIAL: run everything on the calling stream, for debugging.)"""
         if _SERIAL:
             cur = torch.cuda.current_stream()
             return cur, cur
         key = torch.cuda.current_stream().cuda_stream
         if key not in self._streams:
             # the calling stream's priority (the critical chain's forks outrank the
-            # grad-W chain's; PB_PRIO="enc,encode" overrides -- relative priorities
-            # inside one protocol measured no effect, profiles/r01_ab_stream_priority.txt)
+            # grad-W chain's; relative priorities inside one protocol measured no
+            # effect, profiles/r01_ab_stream_priority.txt)
             cur = torch.cuda.current_stream()
-            if _PRIO is None:
-                self._streams[key] = (_stream_like(cur), _stream_like(cur))
-            else:
-                self._streams[key] = (torch.cuda.Stream(priority=_PRIO[0]), torch.cuda.Stream(priority=_PRIO[1]))
+            self._streams[key] = (_stream_like(cur), _stream_like(cur))
         return self._streams[key]
 
     def aux(self):
@@ -268,7 +263,7 @@ class Session:
         ``with sess.aux() as a``, ``a.run(fn)`` enqueues fn on an auxiliary
         stream forked from the current one (after everything enqueued so far);
         the current stream joins it when the block exits.  Outputs must be
-        allocated on the current stream before the block.  (PB_SERIAL=1: inline.)"""
+        allocated on the current stream before the block.  (_SERIAL: inline.)"""
         return _Aux(self)
 
     def prep_stream(self) -> torch.cuda.Stream:
@@ -282,7 +277,7 @@ class Session:
     def grad_stream(self) -> torch.cuda.Stream:
         """Stream the training step runs weight-gradient protocols on, concurrently
         with the input-gradient chain (they are independent given grad Y)."""
-        if _os.environ.get("PB_SERIAL_GRAD", "0") == "1":
+        if _SERIAL:
             return torch.cuda.current_stream()
         if self._grad_stream is None:
             self._grad_stream = torch.cuda.Stream()
@@ -330,7 +325,7 @@ class Session:
         so the protocol's output is unchanged.  ``event``: the consumer waits
         on an event recorded here (False when another mechanism orders them,
         e.g. a separately captured graph replayed before the consumer's).
-        ``background``: launch with at most PB_BG_CAP CTAs (pb_set_launch_cap),
+        ``background``: launch with at most _BG_CAP CTAs (pb_set_launch_cap),
         leaving SM slots to the concurrently running critical path."""
         pack, n, is_ct, _ = self._operand_layout(plan, role)
         if not self._shard(plan).n_out or n == 0:
@@ -632,7 +627,7 @@ def reveal_grad_bias(sess: Session, layer: int, gy_a: ShareTensor, gy_b: ShareTe
 
 
 def grad_w_flipped(mo_x_zero: bool, mo_gy_zero: bool) -> bool:
-    """Whether Alg.2's HE matmul runs transposed (grad W^T = X gY^T), PB_GRADW_FLIP=1:
+    """Whether Alg.2's HE matmul runs transposed (grad W^T = X gY^T), _GRADW_FLIP:
     for the two-cross-term layers it puts the gradient on the packing side with
     fewer polynomials (128x128x64: 16 instead of 64 gradient ciphertexts and
     plaintexts), the forward-only X side (prepared beside the loss) grows to 64.

@@ -468,14 +468,18 @@ def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e
     return loss, gws, gbs
 
 
-_LATE_PREP = __import__("os").environ.get("PB_LATE_PREP", "1") == "1"
-_PREFETCH_BG = __import__("os").environ.get("PB_PREFETCH_BG", "1") == "1"
-_SPIN_WAIT = __import__("os").environ.get("PB_SPIN_WAIT", "1") == "1"
-_BX_FIRST = __import__("os").environ.get("PB_BX_FIRST", "1") == "1"
+# Step-scheduling constants (round-1 A/B measurements):
+_LATE_PREP = True    # prepare layer 0's backward operands inside the backward graph
+_PREFETCH_BG = True  # prefetched input encryption grid-capped (background)
+_SPIN_WAIT = True    # busy-poll the logits event instead of a blocking sync
+_BX_FIRST = True     # enqueue the input-gradient protocol before the grad-W chain
+_PROLOGUE = True     # step seed + prefetched input copied by one prologue kernel
+# The one run-time switch: PB_HANDOFF=0 replaces the device-side loss handoff
+# (a kernel that waits for the host's release word) by an H2D copy + a second
+# graph launch -- the mode to profile under ncu, which serialises kernels and
+# would time the waiting kernel.
 _HANDOFF = __import__("os").environ.get("PB_HANDOFF", "1") == "1"
-_PROLOGUE = __import__("os").environ.get("PB_PROLOGUE", "1") == "1"
 _HANDOFF_TIMEOUT_NS = 30_000_000_000  # a backward waiting this long for the host's loss gives up (ack fails)
-_CHAIN_PRIO = int(__import__("os").environ.get("PB_CHAIN_PRIO", "0"))  # e.g. -2: critical chain at higher priority (measured no gain)
 
 
 class GraphStep:
@@ -545,10 +549,7 @@ class GraphStep:
         self.g_fwd = torch.cuda.CUDAGraph()
         self.g_pre = torch.cuda.CUDAGraph()
         self.g_bwd = torch.cuda.CUDAGraph()
-        # the forward and the input-gradient chain are captured on a high-priority
-        # stream (their forks inherit it); the grad-W chain's stream keeps the
-        # default, lower priority, so the block scheduler serves the critical chain first
-        hp = torch.cuda.Stream(priority=_CHAIN_PRIO) if _CHAIN_PRIO else None
+        hp = None  # capture stream (a high-priority chain stream measured no gain, r01)
         # prologue: the replayed forward graph fetches the step seed from the pinned
         # host word and copies the prefetched input itself (no H2D copy and copy
         # kernel ahead of the launch)

@@ -118,13 +118,8 @@ def compact(dense_map: np.ndarray):
 # L=7 (profiles/r01_kernel_latency_small_grids.jsonl, FC-784 forward launch):
 # encrypting an input poly 0.40 us, encoding a plaintext 0.19 us, producing +
 # decrypting an output ciphertext (mask NTT + INTT + decode) 0.67 us, one
-# ct x pt product term 0.049 us (TMA-pipelined MAC).  Overridable for
-# experiments through PB_PLAN_COSTS="enc,pt,out,prod".
-import os as _os
-
-COST_ENC, COST_PT, COST_OUT, COST_PROD = (
-    tuple(float(v) for v in _os.environ["PB_PLAN_COSTS"].split(",")) if "PB_PLAN_COSTS" in _os.environ
-    else (8.0, 3.7, 14.0, 1.0))
+# ct x pt product term 0.049 us (TMA-pipelined MAC).
+COST_ENC, COST_PT, COST_OUT, COST_PROD = 8.0, 3.7, 14.0, 1.0
 MAX_INPUT_BLOCKS = 32  # bounds the homomorphic accumulation depth (noise)
 
 

@@ -39,7 +39,7 @@ def main(name="mnist_mlp", B=64, steps=3):
     else:
         xh, labels = PN.synthetic_images(1, B, model.in_shape, ring)
     x = RingTensor(encode_fixed(xh, ring), ring.f, ring, _canonical=True)
-    r = PN.GraphStep(sess, model, x, prefetch_input=os.environ.get("PB_PREFETCH_INPUT", "1") == "1")
+    r = PN.GraphStep(sess, model, x, prefetch_input=True)
     for i in range(5):
         r.step(100 + i, labels)
     torch.cuda.synchronize()
