@@ -1,29 +1,42 @@
-"""Benchmark: Pencil private training step on the B200 (BASELINE.json configs[1]).
+"""Benchmark: Pencil private training on the B200 (BASELINE.json configs[1]
+headline, configs[3] and configs[4] beside it).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-cpu] [--no-configs]
 
-Workload: one private training step of the MNIST MLP
-784-128-128-10, batch 64, synthetic MNIST-shaped data, BFV N=8192, t=2^59,
-7 x 30-bit RNS limbs, f=25: per FC layer Alg.1 forward, Alg.2 weight
-gradient, bias reveal and (layers 2-3) the input gradient, all through the
-B200 engine; ReLU/truncation via the SPEC's dealer backend; softmax-CE and
-SGD-momentum exactly as the reference engine.  A "step" therefore performs
-~2000 ciphertext x plaintext products, ~2000 decryptions and ~900
-encryptions (see DESIGN.md for the block plan).
+Headline workload (configs[1]): one private training step of
+the MNIST MLP 784-128-128-10, batch 64 per GPU, synthetic MNIST-shaped data,
+BFV N=8192, t=2^59, 7 x 30-bit RNS limbs, f=25: per FC layer Alg.1 forward,
+Alg.2 weight gradient, bias reveal and (layers 2-3) the input gradient, all
+through the B200 engine; ReLU / truncation by the SPEC:479 dealer backend
+(stated in the line: "nonlinear"); softmax-CE and SGD-momentum exactly as
+the reference engine.
 
-Prints ONE JSON line on rank 0.  ``value`` is samples/s with the batch
-resident in HBM; ``e2e`` is the same metric through the public API with the
-batch copied from pinned host memory every step and the loss read back;
-``roofline`` is the dominant kernel's algorithmic HBM bytes / its CUDA-event
-time; ``cpu_baseline`` is the oracle (the reference's CPU algorithm restated
-in C + numpy) timed on this host's cores on one step of the same workload.
-``--impl reference`` times that CPU path alone on the same config.
+ONE JSON line on rank 0:
+  value      samples/s, batch resident in HBM, steps replayed from CUDA graphs,
+             CUDA events on the launching stream, L2 flushed (256 MiB write)
+             before every timed step, max over ranks
+  e2e        the same through the public API (GraphStep.load_batch + step):
+             the float64 batch copied from pinned host memory every step, the
+             logits read back for the DO's loss, the loss gradient copied in
+  roofline   the step's dominant entry point by CUPTI device time over
+             graph-replayed steps (torch.profiler): algorithmic HBM bytes
+              / its device time, plus the integer-pipe fraction
+             (NTT butterflies x 4 IMAD issue slots, lazy mod-MACs x 1
+             IMAD.WIDE) against the measured B200 integer peaks
+  kernels    per entry point: CUPTI ms per step, launches, HBM and int fractions
+  configs    c4: CIFAR-10 CNN private step (PAPER Fig. 7, B=64), c5: NTT and
+             ct x pt MAC / decrypt sweep points -- each with the CPU oracle
+             beside it
+  cpu_baseline  the oracle (the reference's kernels K:31-278 restated in
+             C/OpenMP + numpy glue) on this host's cores, one warm MLP step
 
-Multi-GPU (torchrun, N>1): every he-matmul's output ciphertext blocks are
-sharded round-robin over the ranks (each rank encrypts only the input
-ciphertexts its blocks need) and the decrypted share tiles are summed with
-one NCCL all-reduce (exact: every element comes from exactly one rank);
-the batch is fixed, so scaling is "strong".
+``--impl reference`` times that CPU path alone on the same config dict.
+
+Multi-GPU (torchrun, N>1): data-parallel private training -- every rank
+trains on its own batch of 64 (weak scaling); the loss gradients are scaled
+by the global batch and the MO's revealed gradients are summed over ranks
+with one NCCL all-reduce per layer before SGD (exact mod 2^59), which is
+bit-identical to reference_train_step at batch 64 N.
 """
 
 from __future__ import annotations
@@ -31,6 +44,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import re
 import subprocess
 import sys
 import threading
@@ -45,42 +59,41 @@ METRIC = "private-training samples/sec; HE linear-layer ct-pt MACs/sec + NTT GB/
 SIZES = [784, 128, 128, 10]
 BATCH = 64
 SEED = 2024
+NONLINEAR = "dealer backend (SPEC:479: reconstruct, apply, reshare) for ReLU / truncation; no OT"
+LAN_BPS = 384e6  # PAPER:777 LAN, for the census' wire-time estimate
 
-
-# entry point -> device kernels it launches (for the ncu DRAM-traffic lookup)
-ENTRY_KERNELS = {
-    "pb_encrypt_sk": ("k_encrypt_sk",), "pb_encrypt_sk_zero": ("k_encrypt_sk",),
-    "pb_encrypt_sk_add": ("k_encrypt_add",), "pb_encode_plain_mont": ("k_encode_plain_mont",),
-    "pb_mask_ntt": ("k_mask_ntt",), "pb_ctpt_mac_tiled": ("k_mac_ws", "k_mac_pipe", "k_mac_eager"),
-    "pb_decrypt_to_share": ("k_decrypt_share_cluster", "k_decrypt_inv", "k_decode_gather"),
+# CUPTI kernel name -> the C-ABI entry point that launches it
+KERNEL_ENTRY = {
+    "k_enc_noise": "pb_encrypt_sk", "k_encrypt_sk": "pb_encrypt_sk", "k_encode_plain_mont": "pb_encode_plain_mont",
+    "k_mask_ntt": "pb_mask_ntt", "k_mac_ws": "pb_ctpt_mac_tiled", "k_mac_eager": "pb_ctpt_mac_tiled",
+    "k_decrypt_share_cluster": "pb_decrypt_to_share", "k_decrypt_inv": "pb_decrypt_to_share",
+    "k_decode_gather": "pb_decrypt_to_share",
 }
 
 
-def _traffic(entry):
-    """DRAM bytes per launch of an entry point's kernels from the committed ncu
-    capture of the same step (profiles/r01_step_traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_step_traffic.json")) as f:
-            ks = json.load(f)["kernels"]
-    except Exception:
-        return None
-    names = [k for k in ENTRY_KERNELS.get(entry, ()) if k in ks]
-    if not names:
-        return None
-    # kernels of one entry point launch once per call each (k_mac_pipe / k_mac_eager: either)
-    if entry == "pb_ctpt_mac_tiled":
-        tot = sum(ks[k]["dram_bytes_per_launch"] * ks[k]["launches"] for k in names)
-        return tot / max(1, sum(ks[k]["launches"] for k in names))
-    return float(sum(ks[k]["dram_bytes_per_launch"] for k in names))
+def _config(world):
+    """The config dict both arms print."""
+    return {"workload": "configs[1]: MNIST MLP 784-128-128-10 private training step", "global_batch": BATCH * world,
+            "batch_per_gpu": BATCH, "bfv": "N=8192, t=2^59, L=7x30-bit (log2 Q = 210)", "f": 25,
+            "parallelism": f"data-parallel x{world} (revealed-gradient all-reduce)" if world > 1 else "single GPU",
+            "l2": "flushed (256 MiB write) between timed steps"}
 
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        hbm = (float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)")
     except Exception:
-        return 6650.0, "fallback"
+        hbm = (6650.0, "fallback (B200_PROFILING.md)")
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_int_peak.json")) as f:
+            d = json.load(f)
+        ip = {"imad": d["IMAD"]["ops_per_s"], "imad_wide": d["IMAD.WIDE.U32"]["ops_per_s"],
+              "kind": "measured on B200 (scripts/int_peak.py -> profiles/r01_int_peak.json)"}
+    except Exception:
+        ip = {"imad": 128 * 148 * 1.965e9 / 2, "imad_wide": 24 * 148 * 1.965e9, "kind": "nominal"}
+    return hbm, ip
 
 
 class ClockSampler:
@@ -106,8 +119,7 @@ class ClockSampler:
                 out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
                 for line in out.stdout.strip().splitlines():
-                    f = [x.strip() for x in line.split(",")]
-                    self.samples.append(f)
+                    self.samples.append([x.strip() for x in line.split(",")])
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -128,54 +140,103 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- CPU legs ---
+# The oracle: the reference's numeric kernels (K:31-278) restated in C/OpenMP
+# (oracle/kernels.c) + numpy glue for the SPEC-only layers -- test / baseline
+# infrastructure, executed only here and in tests/.
 
-def cpu_oracle_step_time(steps=1, warmup=1):
-    """Time the oracle (reference CPU algorithm) on one private step of the workload."""
+def _oracle_ctx(seed=SEED):
     from oracle import bfv as OB
     from oracle import kernels as OK
-    from oracle import nn as ON
     from oracle import protocols as OPR
     from oracle import ring as OR
     from oracle.params import make_params
 
-    ncores = os.cpu_count() or 1
-    OK.set_threads(ncores)
+    OK.set_threads(os.cpu_count() or 1)
     ring = OR.RingParams()
     p = make_params(8192, 7)
     ar = OB.Arith(p)
-    kp = OB.keygen(p, OR.SeededRng(SEED, 0), ar)
-    model = ON.Model(SIZES, ring, seed=SEED)
-    x, labels = ON.synthetic_mnist(SEED, BATCH, ring)
-    ctx = OPR.Ctx(p, ring, kp, seed=SEED, ar=ar)
-    for _ in range(warmup):
+    kp = OB.keygen(p, OR.SeededRng(seed, 0), ar)
+    return OPR.Ctx(p, ring, kp, seed=seed, ar=ar), OK.get_threads()
+
+
+def cpu_model_steps(name, B, steps, warmup):
+    """Seconds per oracle private step of model ``name`` at batch B (after warm-up)."""
+    from oracle import nn as ON
+
+    ctx, cores = _oracle_ctx()
+    model = ON.Model(name, ctx.ring, seed=SEED)
+    if len(model.in_shape) == 1:
+        x, labels = ON.synthetic_mnist(SEED, B, ctx.ring)
+    else:
+        x, labels = ON.synthetic_images(SEED, B, model.in_shape, ctx.ring)
+    for i in range(warmup):
+        ctx.seed = SEED + 100 + i
         ON.private_train_step(ctx, model, x, labels)
     t0 = time.perf_counter()
     for i in range(steps):
         ctx.seed = SEED + 1 + i
         ON.private_train_step(ctx, model, x, labels)
-    dt = (time.perf_counter() - t0) / steps
-    return dt, OK.get_threads()
+    return (time.perf_counter() - t0) / steps, cores
+
+
+def cpu_c5():
+    """The oracle's C5 primitives on the host (N=8192, L=7): NTT rows/s, ct x pt
+    MACs/s (K:89-95 pw_mul_acc over both ciphertext polys), decrypt
+    ciphertexts/s (c0 + c1 s, INTT, Garner + scale-round, K:53-77, 158-199)."""
+    from oracle import kernels as OK
+
+    ctx, cores = _oracle_ctx()
+    p, ar = ctx.p, ctx.ar
+    L, N = 7, 8192
+    rng = np.random.default_rng(0)
+    q = p.tables["q"]
+    out = {"cores": cores, "kind": "port"}
+    rows = rng.integers(0, 1 << 62, size=(L * 128, N), dtype=np.uint64) % np.tile(q, 128)[:, None]
+    OK.ntt_forward_cyc(rows[:L].copy(), p.tables["psi_brv"], q)  # warm-up
+    t0 = time.perf_counter()
+    OK.ntt_forward_cyc(rows, p.tables["psi_brv"], q)
+    dt = time.perf_counter() - t0
+    out["ntt_fwd"] = {"rows_per_s": rows.shape[0] / dt, "GB_s": rows.shape[0] * N * 8 / dt / 1e9,
+                      "sample": f"{rows.shape[0]} rows, N={N} (GB/s at 4 B/residue read + write)"}
+    nct, nI = 16, 8
+    ct = rows[: 2 * L * nct].reshape(nct, 2, L, N)
+    pt = rows[2 * L * nct: 2 * L * nct + L * nI].reshape(nI, L, N)
+    acc = np.zeros((nct, L, N), dtype=np.uint64)
+    t0 = time.perf_counter()
+    for k in range(nI):  # out[b] += ct[b] (*) pt[k] for both polys: nct * nI ct x pt MACs
+        for c in range(2):
+            ar.mac(acc, np.ascontiguousarray(ct[:, c]), pt[k])
+    dt = time.perf_counter() - t0
+    out["ctpt_mac"] = {"ctpt_macs_per_s": nct * nI / dt, "mod_macs_per_s": nct * nI * 2 * L * N / dt,
+                       "sample": f"{nct * nI} ct x pt MACs (K:89-95 pw_mul_acc)"}
+    sk = ctx.kp.sk_ntt if hasattr(ctx.kp, "sk_ntt") else ctx.kp.s_ntt
+    t0 = time.perf_counter()
+    m = ar.mul(np.ascontiguousarray(ct[:8, 1]), np.asarray(sk).reshape(L, N))
+    m = ar.add(m, np.ascontiguousarray(ct[:8, 0]))
+    ar.ntt_inv(m)
+    ar.decode(m)
+    dt = time.perf_counter() - t0
+    out["decrypt"] = {"ct_per_s": 8 / dt, "sample": "8 ciphertexts: c0 + c1 s, INTT, Garner + scale-round"}
+    return out
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the oracle private MLP step on this host's cores."""
     if rank != 0:
         return
-    steps = max(1, args.steps)
-    warm = max(0, args.warmup)
-    # bounded sample: one oracle step is several seconds; cap the run to a few minutes
-    t_first, cores = cpu_oracle_step_time(steps=1, warmup=min(warm, 1))
-    budget = 240.0
-    steps_run = max(1, min(steps, int(budget / max(t_first, 1e-3))))
-    dt, cores = cpu_oracle_step_time(steps=steps_run, warmup=0) if steps_run > 1 else (t_first, cores)
+    warm = max(3, args.warmup)
+    t1, cores = cpu_model_steps("mnist_mlp", BATCH, 1, 1)
+    budget = 240.0  # bound the run to a few minutes
+    steps_run = max(1, min(args.steps, int(budget / max(t1, 1e-3)) - warm))
+    dt, cores = cpu_model_steps("mnist_mlp", BATCH, steps_run, warm - 1)
     v = BATCH / dt
-    sample = (f"{steps_run} private training step(s) of the MNIST MLP 784-128-128-10, B={BATCH}, N=8192, L=7 "
-              f"(oracle = reference kernel algorithms restated in C/OpenMP + numpy), after in-process warm-up")
+    sample = (f"{steps_run} oracle private training step(s) of the MNIST MLP 784-128-128-10, B={BATCH}, N=8192, "
+              f"L=7, after {warm} in-process warm-up steps (oracle = reference kernels restated in C/OpenMP + numpy)")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
-        "steps": steps_run, "warmup": min(warm, 1), "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u32-rns/u64-ring", "data": "synthetic",
-        "config": {"workload": "configs[1]: MNIST MLP 784-128-128-10 private training step", "global_batch": BATCH,
-                   "bfv": "N=8192, t=2^59, L=7x30-bit", "f": 25},
+        "steps": steps_run, "warmup": warm, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "n/a", "vs_baseline": None, "dtype": "u32-rns/u64-ring",
+        "data": "synthetic", "config": _config(1), "nonlinear": NONLINEAR,
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -184,177 +245,53 @@ def run_reference(args, rank, world):
 
 # ------------------------------------------------------------- GPU leg ----
 
-def run_ours(args, rank, world):
+def _short(name):
+    n = re.sub(r"^void ", "", name.strip()).replace("(anonymous namespace)::", "")
+    n = re.sub(r"<.*", "", n)
+    n = re.sub(r"\(.*", "", n)
+    return n.split("::")[-1].strip()
+
+
+def cupti_kernels(fn, n):
+    """Device time (ms) and launches per call of ``fn`` for every engine kernel,
+    from CUPTI activity records (torch.profiler) over n calls."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for i in range(n):
+            fn(i)
+        torch.cuda.synchronize()
+    per = {}
+    for ev in prof.key_averages():
+        t = getattr(ev, "device_time_total", None)
+        if t is None:
+            t = getattr(ev, "cuda_time_total", 0.0)
+        nm = _short(ev.key)
+        if not nm.startswith("k_") or ev.count == 0:
+            continue
+        acc = per.setdefault(nm, [0.0, 0.0])
+        acc[0] += t / 1e3 / n
+        acc[1] += ev.count / n
+    return per
+
+
+def _time_steps(fn, steps, flush, join=None):
     import torch
 
-    from paper_2403_11166_b200 import _dev, _lib, bfv
-    from paper_2403_11166_b200 import nn as PN
-    from paper_2403_11166_b200.linear_protocols import Session
-    from paper_2403_11166_b200.params import BfvParams
-    from paper_2403_11166_b200.ring import RingParams, RingTensor, SeededRng, encode_fixed
-
-    dev = _dev.device()
-    ring = RingParams()
-    params = BfvParams()
-    kp = bfv.keygen(params, SeededRng(SEED, 0))
-    group = None
-    if world > 1:
-        import torch.distributed as dist
-
-        group = dist.group.WORLD
-    sess = Session(params, ring, kp, seed=SEED, shard=(rank, world, group))
-    model = PN.Model(SIZES, ring, seed=SEED)
-    xh, labels = PN.synthetic_mnist(SEED, BATCH, ring)
-    x_dev = RingTensor(encode_fixed(xh, ring), ring.f, ring, _canonical=True)
-    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.int64, device=dev)  # > 126 MB L2
-
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.barrier()
-
-    def eager_step(i, x):
-        sess.reseed(SEED + 10 + i)
-        return PN.private_train_step(sess, model, x, labels, check=False)
-
-    for i in range(max(3, args.warmup)):
-        eager_step(i, x_dev)
-    torch.cuda.synchronize()
-
-    # ---- kernel profile pass (eager, CUDA events around every fused entry point):
-    #      per-kernel durations + algorithmic bytes, kernel launches per step
-    prof_steps = 3
-    stats = _lib.CallStats(timed=("pb_ctpt_mac_tiled", "pb_mask_ntt", "pb_decrypt_to_share", "pb_encrypt_sk",
-                                  "pb_encrypt_sk_add", "pb_encrypt_sk_zero", "pb_encode_plain_mont"))
-    sess.alg_bytes.clear()
-    _lib.STATS = stats
-    for i in range(prof_steps):
-        flush.zero_()
-        eager_step(500 + i, x_dev)
-    _lib.STATS = None
-    torch.cuda.synchronize()
-    launches_per_step = stats.launches / prof_steps
-    per = {}
-    for name, s, e, _tag in stats.events:
-        acc = per.setdefault(name, [0.0, 0])
-        acc[0] += s.elapsed_time(e)
-        acc[1] += 1
-    alg = dict(sess.alg_bytes)
-    census_per_step = sess.channel.total_bytes() / max(1, sess.steps_seen)
-
-    # ---- timed region: the same step replayed from CUDA graphs (GraphStep),
-    #      batch resident in HBM, per-step CUDA events, L2 flushed between steps
-    try:
-        runner = PN.GraphStep(sess, model, x_dev, prefetch_input=True)
-        replay = "CUDA graphs"
-    except Exception as exc:  # e.g. a collective backend that cannot be captured
-        if world == 1:
-            raise
-        torch.cuda.synchronize()
-        runner = _EagerStep(sess, model, x_dev)
-        replay = f"eager launches (graph capture failed: {type(exc).__name__})"
-    for i in range(3):
-        runner.step(SEED + 100 + i, labels)
-    torch.cuda.synchronize()
-    clocks = ClockSampler(torch.cuda.current_device())
-    clocks.start()
-    barrier()
-    torch.cuda.synchronize()
     evs = []
-    loss = None
-    for i in range(args.steps):
+    for i in range(steps):
         flush.zero_()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        loss = runner.step(SEED + 1000 + i, labels)
-        if hasattr(runner, "join_prefetch"):
-            runner.join_prefetch()  # the next step's prefetched input encryption is inside this window
+        fn(i)
+        if join is not None:
+            join()
         e.record()
         evs.append((s, e))
     torch.cuda.synchronize()
-    barrier()
-    clk = clocks.stop()
-    t_ms = _max_over_ranks(sum(s.elapsed_time(e) for s, e in evs), world)
-    value = args.steps * BATCH / (t_ms / 1e3)
-
-    dom = max(per, key=lambda k: per[k][0])
-    tot_ms, n_launch = per[dom]
-    peak, peak_kind = _peaks()
-    bytes_per_launch = alg.get(dom, 0.0) / max(1, n_launch)
-    achieved = bytes_per_launch / (tot_ms / n_launch / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "peak_kind": peak_kind, "traffic": _traffic(dom),
-                "traffic_note": "ncu dram__bytes_read+write per launch (profiles/r01_step_traffic.json); far below "
-                                "the algorithmic bytes because the step's working set is L2-resident",
-                "bytes_per_launch": bytes_per_launch, "launches": n_launch,
-                "ms_per_launch": tot_ms / n_launch, "share_of_step": (tot_ms / prof_steps) / (t_ms / args.steps)}
-    kernels = {k: {"ms_per_step": v[0] / prof_steps, "calls_per_step": v[1] / prof_steps,
-                   "alg_GBs": (alg.get(k, 0.0) / (v[0] / 1e3) / 1e9) if v[0] else None} for k, v in per.items()}
-
-    # ---- e2e through the public API: host batch (pinned) -> device every step, loss back on the host
-    x_pin = torch.from_numpy(np.ascontiguousarray(xh)).pin_memory()
-    torch.cuda.synchronize()
-    barrier()
-    evs = []
-    h2d = x_pin.numel() * 8
-    for i in range(args.steps):
-        flush.zero_()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        if hasattr(runner, "load_batch"):
-            runner.load_batch(x_pin)  # H2D + device encode, range flag checked at the step's sync
-        else:
-            x_dev.values.copy_(encode_fixed(x_pin.to(dev, non_blocking=True), ring))
-        loss = runner.step(SEED + 2000 + i, labels)
-        if hasattr(runner, "join_prefetch"):
-            runner.join_prefetch()
-        e.record()
-        evs.append((s, e))
-    torch.cuda.synchronize()
-    barrier()
-    te_ms = _max_over_ranks(sum(s.elapsed_time(e) for s, e in evs), world)
-    e2e = {"value": args.steps * BATCH / (te_ms / 1e3), "unit": "samples/s",
-           # per step: batch H2D + DO loss-gradient H2D; logits D2H (DO reconstructs) + encode range flag
-           "h2d_bytes_per_step": h2d + 10 * BATCH * 8, "d2h_bytes_per_step": 10 * BATCH * 8 + 4}
-
-    if rank != 0:
-        return
-    cpu = None
-    if not args.no_cpu and world == 1:
-        dt, cores = cpu_oracle_step_time(steps=1, warmup=1)
-        cpu = {"value": BATCH / dt, "unit": "samples/s", "cores": cores, "kind": "port",
-               "sample": "1 private training step (MNIST MLP 784-128-128-10, B=64, N=8192, L=7) of the oracle "
-                         "(reference kernel algorithms restated in C/OpenMP + numpy), after an in-process warm-up step"}
-    line = {
-        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u32-rns/u64-ring", "data": "synthetic",
-        "config": {"workload": "configs[1]: MNIST MLP 784-128-128-10 private training step", "global_batch": BATCH,
-                   "bfv": "N=8192, t=2^59, L=7x30-bit (log2 Q = 210)", "f": 25,
-                   "parallelism": f"ct-block shards x{world}" if world > 1 else "single GPU",
-                   "l2": "flushed (256 MiB write) between timed steps"},
-        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
-        "gpu_launches": int(round(launches_per_step * args.steps)), "kernels": kernels, "loss": loss,
-        "census_bytes_per_step": census_per_step,
-        "timing": f"value/e2e: K steps replayed from {replay} (same kernels); per-kernel times from an "
-                  "instrumented eager pass of the same step",
-    }
-    print(json.dumps(line), flush=True)
-
-
-class _EagerStep:
-    """GraphStep's interface over plain eager launches (multi-rank fallback)."""
-
-    def __init__(self, sess, model, x):
-        self.sess, self.model, self.x = sess, model, x
-
-    def step(self, seed, labels):
-        from paper_2403_11166_b200 import nn as PN
-
-        self.sess.reseed(seed)
-        loss, _, _ = PN.private_train_step(self.sess, self.model, self.x, labels, check=False)
-        return loss
+    return sum(s.elapsed_time(e) for s, e in evs)  # ms
 
 
 def _max_over_ranks(v, world):
@@ -368,13 +305,271 @@ def _max_over_ranks(v, world):
     return float(t.item())
 
 
+def _roofline(name, ms, launches, nbytes, work, hbm, ip):
+    """HBM and integer-pipe fractions of one entry point per step."""
+    ntt_rows, mod_macs = work
+    d = {"kernel": name, "ms_per_step": ms, "launches_per_step": launches, "ms_per_launch": ms / max(launches, 1e-9)}
+    ach = nbytes / (ms / 1e3) / 1e9 if ms else 0.0
+    d.update({"hbm_GBs": ach, "hbm_frac": ach / hbm[0], "alg_bytes_per_step": nbytes})
+    slots = ntt_rows * (8192 // 2) * 13 * 4  # Harvey butterflies x (2 IMAD + IMAD.HI = 4 issue slots)
+    if slots and ms:
+        d["int_ops_per_s"] = slots / (ms / 1e3)
+        d["int_frac"] = d["int_ops_per_s"] / ip["imad"]
+        d["int_model"] = "NTT butterflies x 4 IMAD issue slots / measured IMAD peak (RNG, gathers not counted)"
+    elif mod_macs and ms:
+        d["int_ops_per_s"] = mod_macs / (ms / 1e3)
+        d["int_frac"] = d["int_ops_per_s"] / ip["imad_wide"]
+        d["int_model"] = "lazy mod-MACs (1 IMAD.WIDE.U32 each) / measured IMAD.WIDE.U32 peak"
+    return d
+
+
+def run_ours(args, rank, world):
+    import torch
+
+    from paper_2403_11166_b200 import _dev, _lib, bfv
+    from paper_2403_11166_b200 import nn as PN
+    from paper_2403_11166_b200.linear_protocols import Session
+    from paper_2403_11166_b200.params import BfvParams
+    from paper_2403_11166_b200.ring import RingParams, RingTensor, SeededRng, encode_fixed
+
+    dev = _dev.device()
+    hbm, ip = _peaks()
+    ring = RingParams()
+    params = BfvParams()
+    kp = bfv.keygen(params, SeededRng(SEED, 0))
+    sess = Session(params, ring, kp, seed=SEED)
+    model = PN.Model(SIZES, ring, seed=SEED)
+    if world > 1:
+        import torch.distributed as dist
+
+        model.set_data_parallel(dist.group.WORLD, world)  # revealed gradients summed over ranks before SGD
+    xh, labels = PN.synthetic_mnist(SEED + rank, BATCH, ring)  # every rank its own batch
+    x_dev = RingTensor(encode_fixed(xh, ring), ring.f, ring, _canonical=True)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.int64, device=dev)  # > 126 MB L2
+    warm = max(3, args.warmup)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    # ---- one instrumented eager step: algorithmic bytes / work per entry point
+    for i in range(2):
+        sess.reseed(SEED + 10 + i)
+        PN.private_train_step(sess, model, x_dev, labels, check=False)
+    torch.cuda.synchronize()
+    sess.alg_bytes.clear()
+    sess.alg_work.clear()
+    _lib.STATS = _lib.CallStats()
+    sess.reseed(SEED + 500)
+    PN.private_train_step(sess, model, x_dev, labels, check=False)
+    torch.cuda.synchronize()
+    _lib.STATS = None
+    alg, work = dict(sess.alg_bytes), {k: list(v) for k, v in sess.alg_work.items()}
+    census_per_step = sess.channel.total_bytes() / max(1, sess.steps_seen)
+
+    # ---- the step replayed from CUDA graphs (GraphStep): what `value` times
+    runner = PN.GraphStep(sess, model, x_dev, prefetch_input=True)
+    for i in range(warm):
+        runner.step(SEED + 100 + i, labels)
+    torch.cuda.synchronize()
+    # per-kernel device times from CUPTI over graph replays (outside the timed region)
+    per = cupti_kernels(lambda i: (runner.step(SEED + 300 + i, labels), runner.join_prefetch()), 3)
+    launches_per_step = sum(v[1] for v in per.values())
+
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    t_ms = _time_steps(lambda i: runner.step(SEED + 1000 + i, labels), args.steps, flush, runner.join_prefetch)
+    barrier()
+    clk = clocks.stop()
+    t_ms = _max_over_ranks(t_ms, world)
+    value = world * args.steps * BATCH / (t_ms / 1e3)
+
+    # ---- e2e through the public API: host batch (pinned) -> device every step, loss back on the host
+    x_pin = torch.from_numpy(np.ascontiguousarray(xh)).pin_memory()
+    torch.cuda.synchronize()
+    barrier()
+
+    def e2e_step(i):
+        runner.load_batch(x_pin)  # H2D + device encode, range flag checked at the step's sync
+        runner.step(SEED + 2000 + i, labels)
+
+    te_ms = _max_over_ranks(_time_steps(e2e_step, args.steps, flush, runner.join_prefetch), world)
+    e2e = {"value": world * args.steps * BATCH / (te_ms / 1e3), "unit": "samples/s",
+           # per step: batch H2D + DO loss-gradient H2D; logits D2H (DO reconstructs) + encode range flag
+           "h2d_bytes_per_step": x_pin.numel() * 8 + 10 * BATCH * 8, "d2h_bytes_per_step": 10 * BATCH * 8 + 4}
+
+    # ---- kernels grouped by entry point; the dominant one carries the roofline
+    entries = {}
+    for k, (ms, n) in per.items():
+        e = KERNEL_ENTRY.get(k, k)
+        acc = entries.setdefault(e, [0.0, 0.0])
+        acc[0] += ms
+        acc[1] += n
+    kernels = {e: _roofline(e, ms, n, alg.get(e, 0.0), work.get(e, [0.0, 0.0]), hbm, ip)
+               for e, (ms, n) in sorted(entries.items(), key=lambda kv: -kv[1][0])}
+    dom = next(iter(kernels))
+    r = kernels[dom]
+    calls = max(1.0, r["launches_per_step"] / (2.0 if dom == "pb_encrypt_sk" else 1.0))
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": r["hbm_GBs"], "peak": hbm[0], "unit": "GB/s",
+                "frac": r["hbm_frac"], "peak_kind": hbm[1], "traffic": None,
+                "traffic_note": "the step's working set is L2-resident: ncu DRAM bytes per launch are far below "
+                                "the algorithmic bytes (profiles/r02_*)",
+                "bytes_per_launch": r["alg_bytes_per_step"] / calls, "ms_per_launch": r["ms_per_step"] / calls,
+                "share_of_step": r["ms_per_step"] / (t_ms / args.steps),
+                "timing": "CUPTI device time over 3 graph-replayed steps (torch.profiler)"}
+    if "int_frac" in r:
+        roofline["int_pipe"] = {"achieved": r["int_ops_per_s"], "unit": "ops/s", "frac": r["int_frac"],
+                                "peak": ip["imad"] if "NTT" in r["int_model"] else ip["imad_wide"],
+                                "model": r["int_model"], "peak_kind": ip["kind"]}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": warm, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "n/a", "vs_baseline": None, "dtype": "u32-rns/u64-ring",
+        "data": "synthetic", "config": _config(world), "nonlinear": NONLINEAR,
+        "e2e": e2e, "roofline": roofline, "clocks": clk,
+        "gpu_launches": int(round(launches_per_step * args.steps)), "kernels": kernels,
+        "census_bytes_per_step": census_per_step,
+        "census_wire_s_at_384MBps": census_per_step / LAN_BPS,
+        "timing": "value/e2e: K graph-replayed steps (CUDA events, max over ranks), each joined with the next "
+                  "step's prefetched input encryption; per-kernel: CUPTI",
+    }
+    del runner
+    torch.cuda.empty_cache()
+    if not args.no_configs:
+        line["configs"] = {"c4": bench_c4(args, rank, world), "c5": bench_c5(args)}
+    if rank != 0:
+        return
+    if not args.no_cpu and world == 1:
+        dt, cores = cpu_model_steps("mnist_mlp", BATCH, 1, 1)
+        line["cpu_baseline"] = {
+            "value": BATCH / dt, "unit": "samples/s", "cores": cores, "kind": "port",
+            "sample": "1 oracle private training step (MNIST MLP, B=64, N=8192, L=7) after 1 warm-up step "
+                      "(the reference kernels restated in C/OpenMP + numpy glue)"}
+        if "configs" in line:
+            dt4, cores4 = cpu_model_steps("cifar_cnn", 4, 1, 0)
+            line["configs"]["c4"]["cpu"] = {
+                "value": 4 / dt4, "unit": "samples/s", "cores": cores4, "kind": "port",
+                "sample": "1 oracle private CIFAR-CNN step at B=4 (bounded sample of configs[3]; B=64 takes minutes)"}
+            line["configs"]["c5"]["cpu"] = cpu_c5()
+    else:
+        line["cpu_baseline"] = None
+    print(json.dumps(line), flush=True)
+
+
+def bench_c4(args, rank, world):
+    """configs[3]: CIFAR-10 CNN (PAPER Fig. 7) private step, B=64 per GPU, graph replay."""
+    import torch
+
+    from paper_2403_11166_b200 import bfv
+    from paper_2403_11166_b200 import nn as PN
+    from paper_2403_11166_b200.linear_protocols import Session
+    from paper_2403_11166_b200.params import BfvParams
+    from paper_2403_11166_b200.ring import RingParams, RingTensor, SeededRng, encode_fixed
+
+    ring, params = RingParams(), BfvParams()
+    sess = Session(params, ring, bfv.keygen(params, SeededRng(SEED, 0)), seed=SEED)
+    model = PN.Model("cifar_cnn", ring, seed=SEED)
+    if world > 1:
+        import torch.distributed as dist
+
+        model.set_data_parallel(dist.group.WORLD, world)
+    xh, labels = PN.synthetic_images(SEED + rank, BATCH, model.in_shape, ring)
+    x = RingTensor(encode_fixed(xh, ring), ring.f, ring, _canonical=True)
+    runner = PN.GraphStep(sess, model, x)
+    for i in range(3):
+        runner.step(SEED + i, labels)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.int64, device="cuda")
+    steps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(_time_steps(lambda i: runner.step(SEED + 50 + i, labels), steps, flush), world) / steps
+    per = cupti_kernels(lambda i: runner.step(SEED + 80 + i, labels), 1)
+    agg = {}
+    for k, v in per.items():
+        e = KERNEL_ENTRY.get(k, k)
+        agg[e] = agg.get(e, 0.0) + v[0]
+    del runner
+    torch.cuda.empty_cache()
+    return {"workload": "configs[3]: CIFAR-10 CNN (5 conv + FC, PAPER Fig. 7) private training step",
+            "batch_per_gpu": BATCH, "value": world * BATCH / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
+            "steps": steps, "kernels_ms_per_step": {k: round(v, 4) for k, v in
+                                                    sorted(agg.items(), key=lambda kv: -kv[1])[:10]}}
+
+
+def bench_c5(args):
+    """configs[4] points at N=8192, L=7: NTT fwd / inv over 1 GiB of residues,
+    ct x pt MAC (FC-like K=1, conv-like K=16), decrypt-to-share of 1024 cts."""
+    import torch
+
+    from paper_2403_11166_b200 import _dev, _lib, bfv
+    from paper_2403_11166_b200.params import BfvParams, context
+    from paper_2403_11166_b200.ring import SeededRng
+
+    hbm, ip = _peaks()
+    p = BfvParams()
+    ctx = context(p)
+    L, N = p.L, p.N
+    st = _dev.stream()
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.int64, device="cuda")
+
+    def t(fn, reps=5):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        return _time_steps(lambda i: fn(), reps, flush) / reps
+
+    out = {"workload": "configs[4] points: N=8192, L=7 (set A); L2 flushed before every timed launch"}
+    rows = (1 << 30) // (4 * N)
+    rows -= rows % L
+    x = torch.randint(0, p.moduli[-1], (rows, N), dtype=torch.int32, device="cuda")
+    for nm, fn in (("ntt_fwd", "pb_ntt_forward"), ("ntt_inv", "pb_ntt_inverse")):
+        ms = t(lambda: _lib.call(fn, ctx.handle, x.data_ptr(), rows, None, st))
+        by = rows * N * 8
+        bf = rows * (N // 2) * 13 * 4
+        out[nm] = {"rows": rows, "ms": ms, "rows_per_s": rows / (ms / 1e3), "GB_s": by / ms / 1e6,
+                   "hbm_frac": by / ms / 1e6 / hbm[0], "int_frac": bf / (ms / 1e3) / ip["imad"]}
+    del x
+    for tag, (nB, nO, nI) in (("mac_fc_k1", (64, 13, 1)), ("mac_conv_k16", (64, 13, 16))):
+        ct = torch.randint(0, p.moduli[-1], (nB * nI, 2, L, N), dtype=torch.int32, device="cuda")
+        pt = torch.randint(0, p.moduli[-1], (nO * nI, L, N), dtype=torch.int32, device="cuda")
+        o = torch.empty((nB * nO, 2, L, N), dtype=torch.int32, device="cuda")
+        ms = t(lambda: _lib.call("pb_ctpt_mac_tiled", ctx.handle, ct.data_ptr(), pt.data_ptr(), None, None, nB, nO,
+                                 nI, o.data_ptr(), st))
+        by = 4 * L * N * (2 * nB * nI + nO * nI + 2 * nB * nO)
+        mm = nB * nO * nI * 2 * L * N
+        out[tag] = {"B_ct": nB, "O_pt": nO, "K": nI, "ms": ms, "ctpt_macs_per_s": nB * nO * nI / (ms / 1e3),
+                    "GB_s": by / ms / 1e6, "hbm_frac": by / ms / 1e6 / hbm[0],
+                    "int_frac": mm / (ms / 1e3) / ip["imad_wide"]}
+        del ct, pt, o
+    kp = bfv.keygen(p, SeededRng(SEED, 0))
+    n, U = 1024, 128
+    ct = torch.randint(0, p.moduli[-1], (n, 2, L, N), dtype=torch.int32, device="cuda")
+    pos = (torch.arange(U, dtype=torch.int32, device="cuda") * 61 % N).repeat(n, 1).contiguous()
+    dst = torch.arange(n * U, dtype=torch.int64, device="cuda")
+    share = torch.empty(n * U, dtype=torch.int64, device="cuda")
+    scratch = torch.empty((n, L, U), dtype=torch.int32, device="cuda")
+    ms = t(lambda: _lib.call("pb_decrypt_to_share", ctx.handle, _dev.ptr(kp.sk_ntt), ct.data_ptr(), n,
+                             pos.data_ptr(), dst.data_ptr(), U, share.data_ptr(), scratch.data_ptr(), st))
+    by = n * (2 * L * N * 4 + 8 * U)
+    out["decrypt_to_share"] = {"cts": n, "useful_slots": U, "ms": ms, "ct_per_s": n / (ms / 1e3),
+                               "GB_s": by / ms / 1e6, "hbm_frac": by / ms / 1e6 / hbm[0]}
+    del ct, share, scratch
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
+    ap.add_argument("--no-configs", action="store_true", help="headline only (no c4 / c5 objects)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

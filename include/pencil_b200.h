@@ -264,6 +264,9 @@ int pb_ring_matmul(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, i
 int pb_ring_matmul_add(const uint64_t* a, const uint64_t* b, int64_t n, int64_t k, int64_t m,
                        int trans_a, int trans_b, const uint64_t* c, int32_t sign, int32_t ell,
                        uint64_t* out, void* stream);
+/* out[dst[i]] = src[i] for dst[i] >= 0: the multi-rank combine of sharded
+ * block plans (all-gathered compact share tiles -> the output tensor). */
+int pb_scatter_u64(uint64_t* out, const uint64_t* src, const int64_t* dst, int64_t n, void* stream);
 /* Row reduction: out[i] = sum_j a[i][j] mod 2^ell  (reveal_grad_bias). */
 int pb_ring_rowsum(const uint64_t* a, int64_t rows, int64_t cols, int32_t ell, uint64_t* out,
                    void* stream);
@@ -352,11 +355,13 @@ int pb_sgd_momentum(double* w, double* v, const uint64_t* grad_ring, int64_t n, 
  * exp / log: pb_host_softmax_pre writes z = logits/2^f2 (signed, ell bits)
  * minus the column max into z [C][B]; the caller sets z = exp(z) with numpy;
  * pb_host_softmax_post normalises, returns the label probabilities (for the
- * caller's numpy log / mean) and g = floor((p - onehot)/B * 2^f) mod 2^ell.
+ * caller's numpy log / mean) and g = floor((p - onehot)/D * 2^f) mod 2^ell
+ * with D = denom, or B when denom == 0 (data parallelism: D = the global
+ * batch, so the ranks' revealed gradients sum to the global-batch gradient).
  * Host functions (no device work); bit-identical to oracle/protocols.py. */
 int pb_host_softmax_pre(const uint64_t* logits, int32_t C, int32_t B, int32_t ell, int32_t f2, double* z);
 int pb_host_softmax_post(double* ez, int32_t C, int32_t B, const int64_t* labels, int32_t ell, int32_t f,
-                         double* p_lab, uint64_t* g_out);
+                         int32_t denom, double* p_lab, uint64_t* g_out);
 
 /* Cap the grid of the one-CTA-per-row kernels (encrypt, plaintext encoding)
  * launched afterwards from this host thread at max_ctas (0: no cap); the

@@ -220,13 +220,32 @@ def reference_train_step(model: Model, x_enc, labels, lr=1e-2, momentum=0.8, dp=
     return loss, gws, gbs
 
 
+def _allsum(v, group, ring):
+    """Sum of a revealed gradient over the data-parallel ranks, exactly mod 2^ell
+    (all_gather + numpy uint64 sum: no reliance on a backend's int64 wrap)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(np.ascontiguousarray(v).view(np.int64))
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, t, group=group)
+    acc = np.zeros_like(np.asarray(v, dtype=np.uint64))
+    for p in parts:
+        acc = acc + p.numpy().view(np.uint64)
+    return _m(acc, ring)
+
+
 def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, momentum=0.8, trace=None, prep=None,
-                       dp=None):
+                       dp=None, dp_group=None):
     """SPEC:629-637 with fullhe linear layers (oracle/protocols.py) -- or, with
     ``prep`` (a preprocessing.PrepState), the HE-free online linear layers of
     Alg. 4 (mode "prep", SPEC:632) -- and the dealer non-linear backend;
     <X_0>_0 = 0 at MO, <X_0>_1 = X at DO.  ``dp``: the DO's DP perturbation of
-    the revealed gradients, drawn from the ctx.seed streams."""
+    the revealed gradients, drawn from the ctx.seed streams.
+    ``dp_group``: data-parallel ranks (torch.distributed), each with its own
+    batch: the loss gradient divided by the global batch, the revealed
+    gradients summed over ranks before the shift and SGD (= the reference
+    engine on the concatenated batch)."""
     from . import preprocessing as PP
 
     ring, f = model.ring, model.ring.f
@@ -255,7 +274,12 @@ def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, moment
                 elif model.layers[k][0] == "flatten":
                     cur = (_flatten(cur[0]), _flatten(cur[1]))
     logits = _m(ys[-1][0] + ys[-1][1], ring)  # MO sends its share; DO reconstructs
-    loss, g = PR.softmax_ce_grad(logits, labels, ring)
+    denom = 0
+    if dp_group is not None:
+        import torch.distributed as dist
+
+        denom = logits.shape[1] * dist.get_world_size(dp_group)
+    loss, g = PR.softmax_ce_grad(logits, labels, ring, denom)
     gy_mo, gy_do = np.zeros_like(g), g
     gws, gbs = [None] * L, [None] * L
     for l in reversed(range(L)):
@@ -273,6 +297,8 @@ def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, moment
             gbs[l] = PR.reveal_grad_bias_conv(ctx, l, gy_mo, gy_do, e=eb)
             gw2f = PR.conv_grad_weight(ctx, l, *acts[l], gy_mo, gy_do, e[3], e[4], e[5], e=ew, mo_x_zero=(l == 0),
                                        mo_gy_zero=last)
+        if dp_group is not None:
+            gw2f, gbs[l] = _allsum(gw2f, dp_group, ring), _allsum(gbs[l], dp_group, ring)
         gws[l] = _shift(gw2f, f, ring)  # MO: plaintext shift
         if trace is not None:
             trace.append((l, ys[l], gbs[l], gws[l]))

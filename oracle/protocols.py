@@ -289,8 +289,9 @@ def dealer_op(ctx: Ctx, layer: int, op: int, y_mo, y_do, k: int = 0, d=None):
 
 # ------------------------------------------------------------ the model ---
 
-def softmax_ce_grad(logits_2f, labels, ring: RingParams):
-    """DO-side loss: logits decoded at 2f (n_classes, B)."""
+def softmax_ce_grad(logits_2f, labels, ring: RingParams, denom: int = 0):
+    """DO-side loss (SPEC:611-619): logits decoded at 2f (n_classes, B);
+    ``denom``: the gradient's batch divisor (0: B; data parallel: the global batch)."""
     z = to_signed(logits_2f, ring).astype(np.float64) / float(1 << (2 * ring.f))
     z = z - z.max(axis=0, keepdims=True)
     ez = np.exp(z)
@@ -299,6 +300,6 @@ def softmax_ce_grad(logits_2f, labels, ring: RingParams):
     onehot = np.zeros_like(sm)
     onehot[labels, np.arange(B)] = 1.0
     loss = float(-np.mean(np.log(sm[labels, np.arange(B)])))
-    g = (sm - onehot) / B
+    g = (sm - onehot) / (denom if denom else B)
     v = np.floor(g * float(1 << ring.f)).astype(np.int64)
     return loss, v.astype(np.uint64) & ring.mask

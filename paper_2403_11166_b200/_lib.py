@@ -79,9 +79,10 @@ SIGNATURES = {
     "pb_share": [P, I64, U64, P, U64, U64, I32, P, P, P],
     "pb_ring_matmul": [P, P, I64, I64, I64, INT, INT, I32, P, P],
     "pb_ring_matmul_ex": [P, P, I64, I64, I64, INT, INT, I32, P, I32, P],
+    "pb_scatter_u64": [P, P, P, I64, P],
     "pb_ring_matmul_add": [P, P, I64, I64, I64, INT, INT, P, I32, I32, P, P],
     "pb_host_softmax_pre": [P, I32, I32, I32, I32, P],
-    "pb_host_softmax_post": [P, I32, I32, P, I32, I32, P, P],
+    "pb_host_softmax_post": [P, I32, I32, P, I32, I32, I32, P, P],
     "pb_host_mean": [P, I64],
     "pb_set_launch_cap": [I32],
     "pb_copy_async": [P, P, I64, P],
@@ -150,7 +151,7 @@ def check(status: int, what: str = "") -> None:
 
 # Device kernels each entry point launches (for the bench's gpu_launches count).
 KERNELS_PER_CALL = {
-    "pb_encrypt_pk": 2, "pb_encrypt_sk": 1, "pb_decrypt": 2, "pb_decrypt_to_share": 1, "pb_unpack": 1,
+    "pb_encrypt_pk": 2, "pb_encrypt_sk": 2, "pb_decrypt": 2, "pb_decrypt_to_share": 1, "pb_unpack": 1,
     "pb_abi_version": 0, "pb_last_error": 0, "pb_set_launch_cap": 0, "pb_copy_async": 0, "pb_host_softmax_pre": 0,
     "pb_host_softmax_post": 0, "pb_host_mean": 0, "pb_device_sm_count": 0, "pb_ctx_create": 0, "pb_ctx_destroy": 0,
 }

@@ -273,13 +273,10 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
   const uint32_t q = P.q[l];
   const uint64_t mu = P.mu[l];
   const int8_t* ep = e + p * N;
-  int8_t ev[32];
-#pragma unroll
-  for (int c = 0; c < 32; ++c) ev[c] = ep[Nt::j1(tid, c)];  // issued ahead of the source gather
   uint32_t b[32];
   load_source<Nt>(b, sm, src, p, tid, [&](uint64_t v) { return delta_m(P, l, v); });
 #pragma unroll
-  for (int c = 0; c < 32; ++c) b[c] = addmod(lift_small(ev[c], q), b[c], q);
+  for (int c = 0; c < 32; ++c) b[c] = addmod(lift_small(ep[Nt::j1(tid, c)], q), b[c], q);
   Nt::forward(b, sm, P.tw_fwd + (size_t)l * N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
   // c1 = a, c0 = NTT(e + Delta m) - a*s, one 128-bit device-order vector at a
   // time (keeps a and s out of the register file: 32 live residues, not 96)

@@ -60,8 +60,9 @@ extern "C" int pb_host_softmax_pre(const uint64_t* logits, int32_t C, int32_t B,
 // ez = exp(z) in place (numpy) -> sm = ez / ez.sum(axis=0); p_lab[b] =
 // sm[label_b][b]; g = floor((sm - onehot) / B * 2^f) mod 2^ell into g_out.
 extern "C" int pb_host_softmax_post(double* ez, int32_t C, int32_t B, const int64_t* labels, int32_t ell, int32_t f,
-                                    double* p_lab, uint64_t* g_out) {
-  if (!ez || !labels || !p_lab || !g_out || C < 1 || B < 1 || ell < 2 || ell > 63) return PB_ERR_ARG;
+                                    int32_t denom, double* p_lab, uint64_t* g_out) {
+  if (!ez || !labels || !p_lab || !g_out || C < 1 || B < 1 || ell < 2 || ell > 63 || denom < 0) return PB_ERR_ARG;
+  const double den = (double)(denom ? denom : B);  // the global batch under data parallelism
   const uint64_t mask = (1ull << ell) - 1;
   const double scale = std::ldexp(1.0, f);
   for (int b = 0; b < B; ++b) {
@@ -78,7 +79,7 @@ extern "C" int pb_host_softmax_post(double* ez, int32_t C, int32_t B, const int6
     ez[labels[b] * B + b] -= 1.0;
   }
   for (int64_t i = 0; i < (int64_t)C * B; ++i) {
-    const double g = ez[i] / (double)B * scale;
+    const double g = ez[i] / den * scale;
     g_out[i] = (uint64_t)(int64_t)std::floor(g) & mask;
   }
   return PB_OK;

@@ -342,6 +342,14 @@ __global__ void k_sgd(double* w, double* v, const uint64_t* g, int64_t n, int gs
   }
 }
 
+__global__ void k_scatter_u64(uint64_t* __restrict__ out, const uint64_t* __restrict__ src,
+                              const int64_t* __restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = __ldg(dst + i);
+    if (d >= 0) out[d] = __ldg(src + i);
+  }
+}
+
 bool bad_ell(int ell) { return ell < 2 || ell > 64; }
 
 }  // namespace
@@ -540,6 +548,16 @@ extern "C" int pb_ring_add_bcast(uint64_t* out, const uint64_t* a, const uint64_
   if (inner < 1 || bn < 1 || bad_ell(ell)) return pb_set_error(PB_ERR_ARG, "bad broadcast / ell");
   if (n <= 0) return PB_OK;
   k_ring_add_bcast<<<RING_GRID(n)>>>(out, a, b, n, inner, bn, ell);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+// The multi-rank combine's last step (linear_protocols.gather_maps): the
+// all-gathered compact share tiles scattered into the output tensor.
+extern "C" int pb_scatter_u64(uint64_t* out, const uint64_t* src, const int64_t* dst, int64_t n, void* stream) {
+  if (n > 0 && (!out || !src || !dst)) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n <= 0) return PB_OK;
+  k_scatter_u64<<<RING_GRID(n)>>>(out, src, dst, n);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }

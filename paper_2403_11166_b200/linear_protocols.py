@@ -135,8 +135,28 @@ def shard_maps(plan, rank: int, world: int) -> dict:
                 out_pos=plan.out_pos[rows], out_dst=plan.out_dst[rows])
 
 
+def gather_maps(plan, world: int):
+    """The multi-rank combine of a sharded block plan: rank r
+    decrypts its output ciphertexts' useful slots into a COMPACT tile
+    [n_max][U] (slot (i, u) at i*U + u; n_max = the largest rank share), the
+    ranks all-gather the tiles, and every rank scatters the [world][n_max][U]
+    result into the output tensor through ``gdst`` (-1: padding or an unused
+    slot).  Returns (n_max, gdst int64 [world * n_max * U]).  Moves exactly
+    the useful share elements (vs. an all-reduce of zero-padded full tiles)."""
+    maps = [shard_maps(plan, r, world) for r in range(world)]
+    n_max = max(1, max(m["n_out"] for m in maps))
+    U = plan.U
+    gdst = np.full((world, n_max, U), -1, dtype=np.int64)
+    for r, m in enumerate(maps):
+        if m["n_out"]:
+            dst = np.where(m["out_pos"] >= 0, m["out_dst"], -1)
+            gdst[r, : m["n_out"]] = dst
+    return n_max, gdst.reshape(-1)
+
+
 class _Shard:
-    """Device copies of ``shard_maps`` (uploaded once per plan and rank)."""
+    """Device copies of ``shard_maps`` (uploaded once per plan and rank), plus
+    the compact-tile destinations and the all-gather scatter map for world > 1."""
 
     def __init__(self, plan, rank: int, world: int):
         m = shard_maps(plan, rank, world)
@@ -146,6 +166,11 @@ class _Shard:
         self.pt_pack = tuple(_dev.i32_to_device(a) for a in m["pt_pack"])
         self.out_pos = _dev.i32_to_device(m["out_pos"])
         self.out_dst = _dev.i64_to_device(m["out_dst"])
+        self.n_max = 0
+        if world > 1:
+            self.n_max, gdst = gather_maps(plan, world)
+            self.gdst = _dev.i64_to_device(gdst)
+            self.tile_dst = _dev.i64_to_device(np.arange(max(1, self.n_out) * self.U, dtype=np.int64))
 
 
 class _Aux:
@@ -178,10 +203,12 @@ class _Aux:
 class Session:
     """Both parties' protocol state: BFV keys (DO), ring params, seeds, channel.
 
-    ``shard=(rank, world, group)`` splits every he-matmul's output ciphertexts
-    round-robin over ``world`` GPUs (one process per GPU); the decrypted share
-    tiles are combined with one NCCL all-reduce (each element is written by
-    exactly one rank, the others contribute 0, so the u64 sum is exact)."""
+    ``shard=(rank, world, group)`` splits every he-matmul's grid of output
+    ciphertexts into one rectangle per GPU (``shard_grid``; one process per
+    GPU, each encrypting / encoding only the operands its rectangle needs);
+    the ranks' decrypted useful slots are combined with one NCCL all-gather
+    of compact tiles and a scatter (``gather_maps``) -- the only data-path
+    collective, moving just the result shares."""
 
     def __init__(self, params: BfvParams, ring: RingParams, kp: KeyPair, seed: int, filler: bool = True,
                  channel: Channel | None = None, shard=None):
@@ -196,6 +223,7 @@ class Session:
         self.ctx = context(params)
         self.rank, self.world, self.group = shard if shard else (0, 1, None)
         self.alg_bytes = {}  # entry point -> algorithmic HBM bytes (while instrumented)
+        self.alg_work = {}   # entry point -> [NTT rows, mod-MACs] (while instrumented)
         self.steps_seen = 0
         self._shards = {}
         self.graph_mode = False
@@ -311,10 +339,10 @@ class Session:
             base = enc_rng.reserve((plan.n_in + plan.n_pt) * self.world)
             _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(src), *_pk(pack), n,
                       *enc_rng.dev_args(), base + off, _dev.ptr(buf), _dev.stream())
-            self._count("pb_encrypt_sk", n * (2 * L * N * 4 + 8 * N))
+            self._count("pb_encrypt_sk", n * (2 * L * N * 4 + 8 * N), ntt_rows=n * L)
         else:
             _lib.call("pb_encode_plain_mont", h, _dev.ptr(src), *_pk(pack), n, _dev.ptr(buf), _dev.stream())
-            self._count("pb_encode_plain_mont", n * (L * N * 4 + 8 * N))
+            self._count("pb_encode_plain_mont", n * (L * N * 4 + 8 * N), ntt_rows=n * L)
 
     def prepare_operand(self, layer: int, op: int, plan, role: str, src: torch.Tensor, event: bool = True,
                         background: bool = False, rng=None):
@@ -424,9 +452,15 @@ class Session:
             torch.cuda.current_stream().wait_event(ev)
         return buf
 
-    def _count(self, name, nbytes):
+    def _count(self, name, nbytes, ntt_rows=0, mod_macs=0):
+        """Algorithmic work of one entry-point call (SURVEY §8d unit costs), while
+        instrumented: HBM bytes, NTT rows (forward or inverse, one limb each)
+        and lazy mod-MACs -- bench.py's HBM and integer-pipe rooflines."""
         if _lib.STATS is not None:
             self.alg_bytes[name] = self.alg_bytes.get(name, 0.0) + float(nbytes)
+            w = self.alg_work.setdefault(name, [0.0, 0.0])
+            w[0] += float(ntt_rows)
+            w[1] += float(mod_macs)
 
     def _shard(self, plan):
         key = (id(plan), self.rank, self.world)
@@ -493,7 +527,7 @@ class Session:
             fseed, fptr = self.rng(layer, op, P_MASK).dev_args()
             _lib.call("pb_mask_ntt", h, sh.n_out, _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U, _dev.ptr(mask),
                       1 if self.filler else 0, fseed ^ 0x5A5A5A5A5A5A5A5A, fptr, _dev.ptr(out_ct), st)
-            self._count("pb_mask_ntt", sh.n_out * (L * N * w + 8 * sh.U))
+            self._count("pb_mask_ntt", sh.n_out * (L * N * w + 8 * sh.U), ntt_rows=sh.n_out * L)
             if has_a or has_b:
                 main.wait_stream(s_enc)
                 main.wait_stream(s_pt)
@@ -504,20 +538,35 @@ class Session:
                           sh.no, sh.nI, _dev.ptr(out_ct), st)
                 n_ct = (sh.n_in if ctA is not None else 0) + (sh.n_pt if ctB is not None else 0)
                 n_pt = (sh.n_pt if ctA is not None else 0) + (sh.n_in if ctB is not None else 0)
-                self._count("pb_ctpt_mac_tiled", n_ct * ct_bytes + n_pt * L * N * w + sh.n_out * (ct_bytes + L * N * w))
+                n_terms = (1 if ctA is not None else 0) + (1 if ctB is not None else 0)
+                self._count("pb_ctpt_mac_tiled", n_ct * ct_bytes + n_pt * L * N * w + sh.n_out * (ct_bytes + L * N * w),
+                            mod_macs=n_terms * sh.n_out * sh.nI * 2 * L * N)
             self.channel.send(MO, msg_out, out_ct, Ciphertext(out_ct, p).nbytes_wire())
             if self.capture is not None:
                 self.capture.append((out_ct.clone(), sh.out_pos.clone()))
             scratch = _dev.empty_u32(sh.n_out, L, sh.U)
+            if self.world > 1:  # this rank's useful slots into its compact tile (gather_maps)
+                tile = torch.zeros(sh.n_max * sh.U, dtype=torch.int64, device=out.device)
+                dmap, dout = sh.tile_dst, tile
+            else:
+                dmap, dout = sh.out_dst, out
             _lib.call("pb_decrypt_to_share", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(out_ct), sh.n_out,
-                      _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U, _dev.ptr(out), _dev.ptr(scratch), st)
-            self._count("pb_decrypt_to_share", sh.n_out * (ct_bytes + 8 * sh.U))
+                      _dev.ptr(sh.out_pos), _dev.ptr(dmap), sh.U, _dev.ptr(dout), _dev.ptr(scratch), st)
+            self._count("pb_decrypt_to_share", sh.n_out * (ct_bytes + 8 * sh.U), ntt_rows=sh.n_out * L)
             # operands stay referenced until here, i.e. until every kernel is enqueued
             del ctA, ptA, ctB, ptB, ops, out_ct, scratch
-        if self.world > 1:
+        if self.world > 1:  # all-gather the ranks' compact tiles, scatter them into `out`
             import torch.distributed as dist
 
-            dist.all_reduce(out, op=dist.ReduceOp.SUM, group=self.group)
+            if not sh.n_out:
+                tile = torch.zeros(sh.n_max * sh.U, dtype=torch.int64, device=out.device)
+            gathered = torch.empty(self.world * sh.n_max * sh.U, dtype=torch.int64, device=out.device)
+            if dist.get_backend(self.group) == "nccl":
+                dist.all_gather_into_tensor(gathered, tile, group=self.group)
+            else:  # gloo (the CPU / shared-GPU tests): list form
+                dist.all_gather(list(gathered.chunk(self.world)), tile, group=self.group)
+            _lib.call("pb_scatter_u64", _dev.ptr(out), _dev.ptr(gathered), _dev.ptr(sh.gdst), gathered.numel(),
+                      _dev.stream())
         return out
 
 

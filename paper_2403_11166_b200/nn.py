@@ -116,6 +116,30 @@ class Model:
         self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
         # step-abort word (GraphStep's loss handoff): nonzero -> the SGD kernels are no-ops
         self.skip = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.dp_group, self.dp_world = None, 1
+
+    def set_data_parallel(self, group, world: int):
+        """Data-parallel private training over ``world`` ranks of ``group``
+        (one process per GPU, each with its own batch and session): the DO's
+        loss gradient is divided by the global batch and the MO's revealed
+        gradients are summed over ranks (one all-reduce per tensor, exact mod
+        2^ell since 2^ell | 2^64) before SGD -- the same update as
+        reference_train_step on the concatenated batch."""
+        self.dp_group, self.dp_world = group, int(world)
+
+    def grad_denom(self, B: int) -> int:
+        return B * self.dp_world if self.dp_group is not None else 0
+
+    def reduce_grads(self, *grads):
+        """Sum revealed gradients over the data-parallel ranks (current stream)."""
+        if self.dp_group is None:
+            return
+        import torch.distributed as dist
+
+        m = int(self.ring.mask)
+        for g in grads:
+            dist.all_reduce(g.values, op=dist.ReduceOp.SUM, group=self.dp_group)
+            g.values.bitwise_and_(m)
 
     @property
     def sizes(self):  # MLP compatibility
@@ -171,8 +195,8 @@ class SoftmaxCE:
     whose addresses are resolved once -- ~15 small numpy ops (~50 us) become
     ~12 us on the step's critical path."""
 
-    def __init__(self, ring: RingParams, C: int, B: int, logits=None, g_out=None):
-        self.ring, self.C, self.B = ring, C, B
+    def __init__(self, ring: RingParams, C: int, B: int, logits=None, g_out=None, denom: int = 0):
+        self.ring, self.C, self.B, self.denom = ring, C, B, int(denom)
         self.z = np.empty((C, B), dtype=np.float64)
         self.p = np.empty(B, dtype=np.float64)
         self.lab = np.empty(B, dtype=np.int64)
@@ -185,7 +209,8 @@ class SoftmaxCE:
         self.alog = addr(logits) if logits is not None else None
 
     def __call__(self, labels, logits=None):
-        """(loss, g) with g = encode_f((softmax - onehot) / B) mod 2^ell in self.g."""
+        """(loss, g) with g = encode_f((softmax - onehot) / D) mod 2^ell in self.g
+        (D = denom: the global batch under data parallelism; else B)."""
         if logits is None:
             alog = self.alog
         else:
@@ -195,7 +220,7 @@ class SoftmaxCE:
         r = self.ring
         _lib.check(self._pre(alog, self.C, self.B, r.ell, 2 * r.f, self.az), "pb_host_softmax_pre")
         np.exp(self.z, out=self.z)
-        _lib.check(self._post(self.az, self.C, self.B, self.alab, r.ell, r.f, self.ap, self.ag),
+        _lib.check(self._post(self.az, self.C, self.B, self.alab, r.ell, r.f, self.denom, self.ap, self.ag),
                    "pb_host_softmax_post")
         np.log(self.p, out=self.p)
         return -self._mean(self.ap, self.B), self.g
@@ -204,13 +229,14 @@ class SoftmaxCE:
 _SMCE = {}
 
 
-def softmax_ce_grad(logits_2f: np.ndarray, labels: np.ndarray, ring: RingParams):
-    """DO-side loss in float64 on the reconstructed logits (SoftmaxCE)."""
+def softmax_ce_grad(logits_2f: np.ndarray, labels: np.ndarray, ring: RingParams, denom: int = 0):
+    """DO-side loss in float64 (SPEC:611-619) on the reconstructed logits (SoftmaxCE);
+    ``denom``: the gradient's batch divisor (0: this batch)."""
     C, B = np.shape(logits_2f)
-    key = (C, B, ring.ell, ring.f)
+    key = (C, B, ring.ell, ring.f, denom)
     sm = _SMCE.get(key)
     if sm is None:
-        sm = _SMCE[key] = SoftmaxCE(ring, C, B)
+        sm = _SMCE[key] = SoftmaxCE(ring, C, B, denom=denom)
     loss, g = sm(labels, logits_2f)
     return loss, g.copy()
 
@@ -324,6 +350,7 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
                 gbs[l] = reveal_grad_bias_conv(sess, l, gy_mo, gy_do, e=eb)
                 gw = conv_grad_weight(sess, l, *acts[l], gy_mo, gy_do, e[3], e[4], e[5], e=ew, mo_x_zero=(l == 0),
                                       mo_gy_zero=last)
+            model.reduce_grads(gw, gbs[l])  # data parallel: sum over ranks at 2f, before the shift
             gws[l] = arith_shift(gw, f)
         keep.append((gy_mo, gy_do))
         if trace is not None:
@@ -462,7 +489,7 @@ def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e
     side.wait_stream(main)
     with torch.cuda.stream(side):  # overlaps the host's loss computation
         prepare_backward(sess, model, state, prep)
-    loss, g = softmax_ce_grad(logits.numpy(), np.asarray(labels), model.ring)  # DO, float64 (host)
+    loss, g = softmax_ce_grad(logits.numpy(), np.asarray(labels), model.ring, model.grad_denom(logits.shape[1]))
     main.wait_stream(side)
     gws, gbs = backward_phase(sess, model, state, _dev.u64_to_device(g), lr, momentum, trace, check, prep)
     return loss, gws, gbs
@@ -516,7 +543,7 @@ class GraphStep:
         self.g_do = torch.zeros(n_cls, B, dtype=torch.int64, device=dev)
         self.logits_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
         self.g_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
-        self._loss = SoftmaxCE(model.ring, n_cls, B, logits=self.logits_host.numpy().view(np.uint64),
+        self._loss = SoftmaxCE(model.ring, n_cls, B, denom=model.grad_denom(B), logits=self.logits_host.numpy().view(np.uint64),
                                g_out=self.g_host.numpy().view(np.uint64))
         first = model.layers[model.lin[0]]
         self.prefetch = bool(prefetch_input) and prep is None and first[0] in ("fc", "conv")

@@ -1,10 +1,16 @@
-"""Multi-rank engine path on the GPU: two ranks shard every HE
-matmul / conv's output-ciphertext grid (Session(shard=...)) and combine the
-decrypted share tiles with an all-reduce.  The box has one GPU, so both ranks
-share cuda:0 and the collective runs over gloo (host-staged -- no kernel
-waits on another rank's kernel); the NCCL path in bench.py is the same call.
-The sharded shares and a full private training step must equal the
-single-rank run bit-for-bit."""
+"""Multi-rank engine paths on the GPU.
+
+* Sharding: two ranks split every HE matmul / conv's output-ciphertext grid
+  (Session(shard=...)) and combine the decrypted useful slots with an
+  all-gather of compact tiles + pb_scatter_u64.  The box has one GPU, so both
+  ranks share cuda:0 and the collective runs over gloo (host-staged -- no
+  kernel waits on another rank's kernel); NCCL takes the same call.  The
+  sharded shares and a full private training step equal the single-rank run.
+* Data parallelism under NCCL inside CUDA graphs: a world-1 NCCL group drives
+  Model.set_data_parallel (the revealed-gradient all-reduce) through
+  GraphStep capture + replay; the steps equal the eager engine and the
+  oracle.  (Two NCCL ranks cannot share one GPU: the sharded all-gather's
+  NCCL form is the same torch call as the gloo one tested above.)"""
 
 import os
 
@@ -86,3 +92,58 @@ def test_two_rank_sharding_matches_single_rank():
         assert got["step"][0] == one["step"][0]
         for a, b in zip(got["step"][1] + got["step"][2], one["step"][1] + one["step"][2]):
             assert np.array_equal(a, b), r
+
+
+def _nccl_graph(rank, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import nn as ON
+    from oracle import ring as OR
+    from paper_2403_11166_b200 import bfv
+    from paper_2403_11166_b200 import linear_protocols as LP
+    from paper_2403_11166_b200 import nn as PN
+    from paper_2403_11166_b200.params import BfvParams
+    from paper_2403_11166_b200.ring import RingParams, RingTensor, SeededRng, encode_fixed
+
+    torch.cuda.set_device(0)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        ring, params = RingParams(), BfvParams()
+        kp = bfv.keygen(params, SeededRng(3, 0))
+        sizes, B = [784, 32, 10], 8
+        xh, labels = PN.synthetic_mnist(7, B, ring)
+        g = dist.group.WORLD
+        s_eager = LP.Session(params, ring, kp, seed=1)
+        m_eager = PN.Model(sizes, ring, seed=4)
+        s_graph = LP.Session(params, ring, kp, seed=1)
+        m_graph = PN.Model(sizes, ring, seed=4)
+        m_graph.set_data_parallel(g, 1)  # NCCL all-reduce of the revealed gradients, captured
+        runner = PN.GraphStep(s_graph, m_graph, RingTensor(encode_fixed(xh, ring), 25, ring, _canonical=True))
+        om = ON.Model(sizes, OR.RingParams(), seed=4)
+        xo, _ = ON.synthetic_mnist(7, B, OR.RingParams())
+        x1 = RingTensor(encode_fixed(xh, ring), 25, ring, _canonical=True)
+        ok = True
+        for step in range(3):
+            s_eager.reseed(400 + step)
+            l1, _, _ = PN.private_train_step(s_eager, m_eager, x1, labels)
+            l2 = runner.step(400 + step, labels)
+            l3, _, _ = ON.reference_train_step(om, xo, labels)
+            ok &= l1 == l2 == l3
+            for l in range(len(sizes) - 1):
+                ok &= np.array_equal(m1 := m_eager.W[l].numpy(), m_graph.W[l].numpy())
+                ok &= np.array_equal(m1, om.W(l))
+        q.put(bool(ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_data_parallel_graph_capture_matches_eager_and_oracle():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_graph, args=(0, 29900 + os.getpid() % 500, q))
+    p.start()
+    ok = q.get(timeout=600)
+    p.join(timeout=120)
+    assert p.exitcode == 0 and ok

@@ -6,10 +6,13 @@ sharding of an HE matmul / conv over ``world`` ranks and the combine step.
   rectangle's MAC terms reference;
 * world_size-2 ``gloo`` run: each rank evaluates its rectangle of the packed
   product in the clear (negacyclic products mod 2^64 of the packed
-  polynomials -- the plaintext shadow of the ct x pt MAC), scatters its
-  decoded outputs into a zero tile and the ranks all-reduce (SUM) -- the same
-  combine the engine does with NCCL; the result must equal ``matmul_wrap`` /
-  ``conv2d_wrap`` bit-for-bit.
+  polynomials -- the plaintext shadow of the ct x pt MAC), writes its useful
+  slots into a compact tile, the ranks all-gather the tiles and scatter them
+  through ``gather_maps`` -- the same combine the engine does with NCCL; the
+  result must equal ``matmul_wrap`` / ``conv2d_wrap`` bit-for-bit;
+* world_size-2 data-parallel private training (the oracle step with the
+  revealed gradients summed over ranks, loss gradients over the global batch)
+  equals ``reference_train_step`` on the concatenated batch.
 """
 
 import os
@@ -19,7 +22,7 @@ import pytest
 import torch.multiprocessing as mp
 
 from oracle import kernels as OK
-from paper_2403_11166_b200.linear_protocols import shard_grid, shard_maps
+from paper_2403_11166_b200.linear_protocols import gather_maps, shard_grid, shard_maps
 from paper_2403_11166_b200.poly_encoding import ConvGeometry, MatmulGeometry, plan_conv, plan_matmul
 
 MASK59 = np.uint64((1 << 59) - 1)
@@ -67,21 +70,23 @@ def _packed(src_rows, vals, N):
     return out
 
 
-def eval_shard(plan, v, W, rank, world, out_size):
-    """Rank's decoded tile of pi_y^-1( sum_k pi_v(v) * pi_W(W) ), zero elsewhere."""
+def eval_shard(plan, v, W, rank, world):
+    """Rank's compact tile [n_max][U]: the useful slots of its output
+    ciphertexts of sum_k pi_v(v) * pi_W(W) (gather_maps layout)."""
     m = shard_maps(plan, rank, world)
+    n_max, _ = gather_maps(plan, world)
     N = plan.N
     vin = _packed(m["in_src"], v.ravel(), N)
     wpt = _packed(m["pt_src"], W.ravel(), N)
-    tile = np.zeros(out_size, dtype=np.uint64)
+    tile = np.zeros((n_max, plan.U), dtype=np.uint64)
     for r in range(m["n_out"]):
         bi, oi = divmod(r, m["no"])
         acc = np.zeros(N, dtype=np.uint64)
         for k in range(m["nI"]):
             acc += OK.negacyclic_mul_wrap(vin[bi * m["nI"] + k], wpt[oi * m["nI"] + k])
         ok = m["out_pos"][r] >= 0
-        tile[m["out_dst"][r][ok]] = acc[m["out_pos"][r][ok]] & MASK59
-    return tile
+        tile[r, ok] = acc[m["out_pos"][r][ok]] & MASK59
+    return tile.reshape(-1)
 
 
 def _worker(rank, world, port, q):
@@ -103,10 +108,14 @@ def _worker(rank, world, port, q):
                 v = rng.integers(0, 1 << 59, size=(g.B, g.c_i, g.h, g.w), dtype=np.uint64)
                 W = rng.integers(0, 1 << 59, size=(g.c_o, g.c_i, g.s, g.s), dtype=np.uint64)
                 want = OK.conv2d_wrap(v, W) & MASK59
-            tile = eval_shard(plan, v, W, rank, world, want.size)
-            t = torch.from_numpy(tile.view(np.int64).copy())
-            dist.all_reduce(t, op=dist.ReduceOp.SUM)
-            res.append(bool(np.array_equal(t.numpy().view(np.uint64).reshape(want.shape), want)))
+            tile = torch.from_numpy(eval_shard(plan, v, W, rank, world).view(np.int64).copy())
+            parts = [torch.empty_like(tile) for _ in range(world)]
+            dist.all_gather(parts, tile)
+            _, gdst = gather_maps(plan, world)
+            out = np.zeros(want.size, dtype=np.uint64)
+            src = torch.cat(parts).numpy().view(np.uint64)
+            out[gdst[gdst >= 0]] = src[gdst >= 0]  # pb_scatter_u64
+            res.append(bool(np.array_equal(out.reshape(want.shape), want)))
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
@@ -124,3 +133,51 @@ def test_gloo_world2_sharded_products_combine_exactly():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert out[0] == out[1] and all(out[0]), out
+
+
+def _dp_worker(rank, world, port, q):
+    import copy
+
+    import torch.distributed as dist
+
+    from oracle import bfv as OB
+    from oracle import nn as ON
+    from oracle import protocols as PR
+    from oracle import ring as OR
+    from oracle.params import make_params
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        R = OR.RingParams()
+        p = make_params(8192, 7)
+        ar = OB.Arith(p)
+        ctx = PR.Ctx(p, R, OB.keygen(p, OR.SeededRng(1, 0), ar), seed=31 + rank, ar=ar)
+        m = ON.Model([784, 8, 10], R, seed=3)
+        ref = copy.deepcopy(m)
+        x, labels = ON.synthetic_mnist(9, 4 * world, R)  # the global batch; rank r trains on its quarter
+        xs, ls = x[:, 4 * rank:4 * rank + 4], labels[4 * rank:4 * rank + 4]
+        ok = True
+        for step in range(2):
+            _, gw, gb = ON.private_train_step(ctx, m, np.ascontiguousarray(xs), ls, dp_group=dist.group.WORLD)
+            _, rgw, rgb = ON.reference_train_step(ref, x, labels)
+            ok &= all(np.array_equal(a, b) for a, b in zip(gw, rgw)) and all(np.array_equal(a, b) for a, b in
+                                                                                zip(gb, rgb))
+            ok &= all(np.array_equal(a, b) for a, b in zip(m.w, ref.w))
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_data_parallel_step_equals_reference_on_global_batch():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31500 + os.getpid() % 2000
+    procs = [ctx.Process(target=_dp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert out == {0: True, 1: True}
