@@ -66,6 +66,7 @@ LAN_BPS = 384e6  # PAPER:777 LAN, for the census' wire-time estimate
 KERNEL_ENTRY = {
     "k_enc_noise": "pb_encrypt_sk", "k_encrypt_sk": "pb_encrypt_sk", "k_encode_plain_mont": "pb_encode_plain_mont",
     "k_mask_ntt": "pb_mask_ntt", "k_mac_ws": "pb_ctpt_mac_tiled", "k_mac_eager": "pb_ctpt_mac_tiled",
+    "k_mask_mac": "pb_mask_mac",
     "k_decrypt_share_cluster": "pb_decrypt_to_share", "k_decrypt_inv": "pb_decrypt_to_share",
     "k_decode_gather": "pb_decrypt_to_share",
 }
@@ -544,6 +545,19 @@ def bench_c5(args):
         out[tag] = {"B_ct": nB, "O_pt": nO, "K": nI, "ms": ms, "ctpt_macs_per_s": nB * nO * nI / (ms / 1e3),
                     "GB_s": by / ms / 1e6, "hbm_frac": by / ms / 1e6 / hbm[0],
                     "int_frac": mm / (ms / 1e3) / ip["imad_wide"]}
+        if nI == 1:  # the MO's whole K=1 evaluation fused with the mask NTT (pb_mask_mac)
+            U = 128
+            pos = (torch.arange(U, dtype=torch.int32, device="cuda") * 61 % N).repeat(nB * nO, 1).contiguous()
+            dst = torch.arange(nB * nO * U, dtype=torch.int64, device="cuda")
+            mask = torch.randint(0, 1 << 59, (nB * nO * U,), dtype=torch.int64, device="cuda")
+            ms = t(lambda: _lib.call("pb_mask_mac", ctx.handle, ct.data_ptr(), pt.data_ptr(), None, None, nB, nO, nI,
+                                     pos.data_ptr(), dst.data_ptr(), U, mask.data_ptr(), 1, 7, None, o.data_ptr(), st))
+            by2 = by + 8 * nB * nO * U
+            out["mask_mac_fc_k1"] = {"B_ct": nB, "O_pt": nO, "K": nI, "ms": ms,
+                                     "ctpt_macs_per_s": nB * nO * nI / (ms / 1e3), "GB_s": by2 / ms / 1e6,
+                                     "hbm_frac": by2 / ms / 1e6 / hbm[0],
+                                     "note": "mask NTT (-Delta NTT(mask + filler)) + K=1 MAC in one pass"}
+            del pos, dst, mask
         del ct, pt, o
     kp = bfv.keygen(p, SeededRng(SEED, 0))
     n, U = 1024, 128

@@ -221,6 +221,15 @@ int pb_mask_ntt(const pb_ctx* ctx, int64_t P, const int32_t* out_pos, const int6
 int pb_ctpt_mac_tiled(const pb_ctx* ctx, const uint32_t* ctA, const uint32_t* ptA_mont, const uint32_t* ctB,
                       const uint32_t* ptB_mont, int32_t nB, int32_t nO, int32_t nI, uint32_t* ct_out,
                       void* stream);
+/* Both steps in ONE pass for the streaming shapes (nI <= 2, e.g. FC-like
+ * K = 1): per output row the -Delta*NTT(mask) row is built in registers and
+ * the MAC terms added before the single store of c0 and c1 -- no -mask row
+ * round trip through HBM.  Bit-identical to pb_mask_ntt + pb_ctpt_mac_tiled
+ * with the same arguments. */
+int pb_mask_mac(const pb_ctx* ctx, const uint32_t* ctA, const uint32_t* ptA_mont, const uint32_t* ctB,
+                const uint32_t* ptB_mont, int32_t nB, int32_t nO, int32_t nI, const int32_t* out_pos,
+                const int64_t* out_dst, int32_t U, const uint64_t* mask_vals, int filler, uint64_t filler_seed,
+                const uint64_t* seed_dev, uint32_t* ct_out, void* stream);
 
 /* ------------------------------------------- ring Z_{2^ell} (R:93-233) --- */
 enum {

@@ -80,6 +80,7 @@ SIGNATURES = {
     "pb_ring_matmul": [P, P, I64, I64, I64, INT, INT, I32, P, P],
     "pb_ring_matmul_ex": [P, P, I64, I64, I64, INT, INT, I32, P, I32, P],
     "pb_scatter_u64": [P, P, P, I64, P],
+    "pb_mask_mac": [P, P, P, P, P, I32, I32, I32, P, P, I32, P, INT, U64, P, P, P],
     "pb_ring_matmul_add": [P, P, I64, I64, I64, INT, INT, P, I32, I32, P, P],
     "pb_host_softmax_pre": [P, I32, I32, I32, I32, P],
     "pb_host_softmax_post": [P, I32, I32, P, I32, I32, I32, P, P],

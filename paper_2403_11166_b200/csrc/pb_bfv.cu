@@ -212,31 +212,31 @@ __device__ __forceinline__ void uniform_pair(uint64_t seed, uint64_t nonce, int6
 }
 
 // The encryption noise e ~ CBD(20) of P polynomials, int8 [P][N], drawn ONCE
-// per polynomial (it is the same integer polynomial in every RNS limb) by
-// T = N/32 threads per polynomial: thread tid owns coefficients tid + T c,
-// c < 32, three per Philox4x32-10 call keyed (seed, "ENC5") at counter
-// ((tid << 4) | g, p + nonce).  k_encrypt_sk's L limb CTAs then read it from
-// L2 instead of each redrawing it (7x less RNG work for the noise at L = 7).
+// per polynomial (it is the same integer polynomial in every RNS limb).
+// Coefficient tid + T c (T = N/32, c < 32) comes from Philox4x32-10 keyed
+// (seed, "ENC5") at counter ((tid << 4) | g, p + nonce), g = c / 3, three
+// samples per call; one thread per call, consecutive threads consecutive tid
+// (coalesced byte stores).  k_encrypt_sk's L limb CTAs then read it from L2
+// instead of each redrawing it (7x less RNG work for the noise at L = 7).
 __global__ void __launch_bounds__(256) k_enc_noise(int logN, int64_t nP, uint64_t seed_arg, const uint64_t* seed_dev,
                                                    uint64_t nonce, int8_t* __restrict__ e) {
   const uint64_t seed = dev_key(seed_arg, seed_dev);
   const int T = 1 << (logN - 5);
-  const int64_t total = nP * T;
+  const int64_t total = nP * 11 * T;
   for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = x >> (logN - 5);
     const int tid = (int)(x & (T - 1));
+    const int64_t pg = x >> (logN - 5);
+    const int64_t p = pg / 11;
+    const int g = (int)(pg - p * 11);
     const uint64_t pp = (uint64_t)p + nonce;
+    const u32x4 r = philox4x32_10(((uint32_t)tid << 4) | (uint32_t)g, (uint32_t)pp, (uint32_t)(pp >> 32),
+                                  0x454e4335u /* "ENC5" */, (uint32_t)seed, (uint32_t)(seed >> 32));
+    int sv[3];
+    cbd20x3(r, sv);
     int8_t* ep = e + (p << logN) + tid;
 #pragma unroll
-    for (int g = 0; g < 11; ++g) {
-      const u32x4 r = philox4x32_10(((uint32_t)tid << 4) | (uint32_t)g, (uint32_t)pp, (uint32_t)(pp >> 32),
-                                    0x454e4335u /* "ENC5" */, (uint32_t)seed, (uint32_t)(seed >> 32));
-      int sv[3];
-      cbd20x3(r, sv);
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-        if (3 * g + i < 32) ep[(size_t)(3 * g + i) * T] = (int8_t)sv[i];
-    }
+    for (int i = 0; i < 3; ++i)
+      if (3 * g + i < 32) ep[(size_t)(3 * g + i) * T] = (int8_t)sv[i];
   }
 }
 
@@ -878,7 +878,7 @@ extern "C" int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk, const uint64
   int8_t* e = nullptr;
   if (cudaMallocAsync((void**)&e, (size_t)nP << ctx->dev.logN, st) != cudaSuccess)
     return pb_set_error(PB_ERR_CUDA, "encryption noise scratch allocation failed");
-  const int64_t thr = nP << (ctx->dev.logN - 5);
+  const int64_t thr = (nP * 11) << (ctx->dev.logN - 5);
   k_enc_noise<<<pb_row_grid((thr + 255) / 256), 256, 0, st>>>(ctx->dev.logN, nP, seed, seed_dev, nonce, e);
   PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, src, nP, (const uint32_t*)nullptr,
                    (const int8_t*)e, seed, seed_dev, nonce, ct, st);

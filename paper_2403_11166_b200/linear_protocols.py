@@ -55,6 +55,7 @@ _SERIAL = False        # True: every protocol fork on the calling stream (debugg
 _MASK_PREFETCH = True  # draw all MO masks of a phase up front on a fork
 _GRADW_FLIP = False    # Alg. 2 HE matmul transposed: measured 1.5 % slower
 _BG_CAP = 148          # CTA cap of background operand preparation (0: none)
+_FUSE_MIN_ROWS = 4 * 148  # output rows (ciphertexts x limbs) from which nI <= 2 evaluations fuse mask + MAC
 
 
 def _stream_like(cur: torch.cuda.Stream) -> torch.cuda.Stream:
@@ -522,17 +523,31 @@ class Session:
                 ops[role] = buf
         ctA, ptA, ctB, ptB = ops.get("A_ct"), ops.get("A_pt"), ops.get("B_ct"), ops.get("B_pt")
         out_ct = _dev.empty_u32(sh.n_out, 2, L, N) if sh.n_out else None
+        # streaming shapes (nI <= 2) that fill the GPU: mask NTT and MAC fused in
+        # one pass (pb_mask_mac, no -mask row round trip); smaller ones keep the
+        # mask NTT concurrent with the encryptions (latency over traffic)
+        fused = (has_a or has_b) and sh.nI <= 2 and sh.n_out * L >= _FUSE_MIN_ROWS
         if sh.n_out:
-            # MO: out.c0 = -Delta NTT(mask + filler), then the tiled MAC accumulates onto it
             fseed, fptr = self.rng(layer, op, P_MASK).dev_args()
-            _lib.call("pb_mask_ntt", h, sh.n_out, _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U, _dev.ptr(mask),
-                      1 if self.filler else 0, fseed ^ 0x5A5A5A5A5A5A5A5A, fptr, _dev.ptr(out_ct), st)
-            self._count("pb_mask_ntt", sh.n_out * (L * N * w + 8 * sh.U), ntt_rows=sh.n_out * L)
+            if not fused:  # MO: out.c0 = -Delta NTT(mask + filler), then the tiled MAC accumulates onto it
+                _lib.call("pb_mask_ntt", h, sh.n_out, _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U,
+                          _dev.ptr(mask), 1 if self.filler else 0, fseed ^ 0x5A5A5A5A5A5A5A5A, fptr,
+                          _dev.ptr(out_ct), st)
+                self._count("pb_mask_ntt", sh.n_out * (L * N * w + 8 * sh.U), ntt_rows=sh.n_out * L)
             if has_a or has_b:
                 main.wait_stream(s_enc)
                 main.wait_stream(s_pt)
             if ctA is None and ctB is None:  # no cross term: the DO decrypts an encryption of -mask
                 out_ct[:, 1].zero_()
+            elif fused:
+                _lib.call("pb_mask_mac", h, _dev.ptr(ctA), _dev.ptr(ptA), _dev.ptr(ctB), _dev.ptr(ptB), sh.nb, sh.no,
+                          sh.nI, _dev.ptr(sh.out_pos), _dev.ptr(sh.out_dst), sh.U, _dev.ptr(mask),
+                          1 if self.filler else 0, fseed ^ 0x5A5A5A5A5A5A5A5A, fptr, _dev.ptr(out_ct), st)
+                n_ct = (sh.n_in if ctA is not None else 0) + (sh.n_pt if ctB is not None else 0)
+                n_pt = (sh.n_pt if ctA is not None else 0) + (sh.n_in if ctB is not None else 0)
+                n_terms = (1 if ctA is not None else 0) + (1 if ctB is not None else 0)
+                self._count("pb_mask_mac", n_ct * ct_bytes + n_pt * L * N * w + sh.n_out * (ct_bytes + 8 * sh.U),
+                            ntt_rows=sh.n_out * L, mod_macs=n_terms * sh.n_out * sh.nI * 2 * L * N)
             else:
                 _lib.call("pb_ctpt_mac_tiled", h, _dev.ptr(ctA), _dev.ptr(ptA), _dev.ptr(ctB), _dev.ptr(ptB), sh.nb,
                           sh.no, sh.nI, _dev.ptr(out_ct), st)

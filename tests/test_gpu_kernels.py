@@ -148,3 +148,45 @@ def test_ring_matmul_add_transposes(n, k, m, ta, tb):
         _lib.call("pb_ring_matmul_add", _dev.ptr(da), _dev.ptr(db), n, k, m, ta, tb, _dev.ptr(dc) if sign else None,
                   sign, 59, _dev.ptr(out), _dev.stream())
         assert np.array_equal(_dev.to_numpy_u64(out), want)
+
+
+@pytest.mark.parametrize("nB,nO,nI,terms", [(4, 3, 1, "A"), (3, 5, 2, "A"), (2, 3, 1, "AB"), (5, 2, 2, "AB"),
+                                            (3, 2, 1, "B")])
+def test_mask_mac_fused_equals_two_step(nB, nO, nI, terms):
+    """pb_mask_mac (mask NTT + streaming MAC in one pass) is bit-identical to
+    pb_mask_ntt followed by pb_ctpt_mac_tiled."""
+    import torch
+
+    from paper_2403_11166_b200 import _lib
+    from paper_2403_11166_b200.params import BfvParams, context
+
+    p = BfvParams()
+    h = context(p).handle
+    L, N = p.L, p.N
+    g = torch.Generator(device="cuda").manual_seed(nB * 100 + nO * 10 + nI)
+    q = min(p.moduli)
+
+    def rnd(*shape):
+        return torch.randint(0, q, shape, dtype=torch.int32, device="cuda", generator=g)
+
+    ctA = rnd(nB * nI, 2, L, N) if "A" in terms else None
+    ptA = rnd(nO * nI, L, N) if "A" in terms else None
+    ctB = rnd(nO * nI, 2, L, N) if "B" in terms else None
+    ptB = rnd(nB * nI, L, N) if "B" in terms else None
+    U = 77
+    n_out = nB * nO
+    pos = torch.stack([torch.randperm(N, device="cuda", generator=g)[:U] for _ in range(n_out)]).to(torch.int32)
+    pos[:, ::7] = -1
+    dst = torch.arange(n_out * U, dtype=torch.int64, device="cuda").reshape(n_out, U)
+    mask = torch.randint(0, 1 << 59, (n_out * U,), dtype=torch.int64, device="cuda", generator=g)
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    st = torch.cuda.current_stream().cuda_stream
+    two = torch.zeros(n_out, 2, L, N, dtype=torch.int32, device="cuda")
+    _lib.call("pb_mask_ntt", h, n_out, pos.data_ptr(), dst.data_ptr(), U, mask.data_ptr(), 1, 99, None,
+              two.data_ptr(), st)
+    _lib.call("pb_ctpt_mac_tiled", h, ptr(ctA), ptr(ptA), ptr(ctB), ptr(ptB), nB, nO, nI, two.data_ptr(), st)
+    one = torch.full((n_out, 2, L, N), 7, dtype=torch.int32, device="cuda")
+    _lib.call("pb_mask_mac", h, ptr(ctA), ptr(ptA), ptr(ctB), ptr(ptB), nB, nO, nI, pos.data_ptr(), dst.data_ptr(), U,
+              mask.data_ptr(), 1, 99, None, one.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert torch.equal(one, two)
