@@ -352,6 +352,24 @@ int pb_dealer_op_out(int op, const uint64_t* in_mo, const uint64_t* in_do, uint6
                      const uint64_t* seed_dev, uint64_t stream_id, uint64_t raw_offset, int32_t ell,
                      void* stream);
 
+/* OT-based non-linear protocols with the
+ * SPEC:479 dealer OT backend, one thread per element (pb_nonlinear.cu):
+ *   PB_NL_DRELU       XOR shares of 1{x >= 0} (millionaires' comparison in
+ *                     4-bit blocks, 1-of-16 leaf OTs, Beaver-AND tree) -> d_out
+ *                     (bit 0: P0 = MO share, bit 1: P1 = DO share)
+ *   PB_NL_MUX         arithmetic shares of d * x (two 1-of-2 OTs), d from d_in
+ *   PB_NL_TRUNC       faithful arith_shift(x, k) (wrap + low-carry comparisons, B2A)
+ *   PB_NL_RELU_TRUNC  DReLU, MUX, TRUNC fused (d_out as DRELU)
+ *   PB_NL_TRUNC_MUX   TRUNC then MUX with d_in (the backward ReLU')
+ * x0 / x1: the MO's / DO's shares (n u64 < 2^ell); y0 / y1: output shares.
+ * Randomness: raw draws raw_offset + i * pb_nl_words(op) + k of the
+ * numpy-identical Philox stream (seed (+ *seed_dev), stream_id). */
+enum { PB_NL_DRELU = 0, PB_NL_MUX = 1, PB_NL_TRUNC = 2, PB_NL_RELU_TRUNC = 3, PB_NL_TRUNC_MUX = 4 };
+int pb_nl_words(int op);
+int pb_nl_op(int op, const uint64_t* x0, const uint64_t* x1, int64_t n, int32_t ell, int32_t k, const uint8_t* d_in,
+             uint8_t* d_out, uint64_t seed, const uint64_t* seed_dev, uint64_t stream_id, uint64_t raw_offset,
+             uint64_t* y0, uint64_t* y1, void* stream);
+
 /* SGD with momentum in float64 + re-quantisation:
  * v = mu*v + g; w = w - lr*v; w_ring = encode_fixed(w, scale).  skip
  * (nullable device word): nonzero -> no-op (an aborted step, see

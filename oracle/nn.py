@@ -236,7 +236,7 @@ def _allsum(v, group, ring):
 
 
 def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, momentum=0.8, trace=None, prep=None,
-                       dp=None, dp_group=None):
+                       dp=None, dp_group=None, nonlinear="dealer"):
     """SPEC:629-637 with fullhe linear layers (oracle/protocols.py) -- or, with
     ``prep`` (a preprocessing.PrepState), the HE-free online linear layers of
     Alg. 4 (mode "prep", SPEC:632) -- and the dealer non-linear backend;
@@ -245,7 +245,10 @@ def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, moment
     ``dp_group``: data-parallel ranks (torch.distributed), each with its own
     batch: the loss gradient divided by the global batch, the revealed
     gradients summed over ranks before the shift and SGD (= the reference
-    engine on the concatenated batch)."""
+    engine on the concatenated batch).  ``nonlinear="ot"``: ReLU / truncation /
+    pooling through the OT-based protocols (oracle/nonlinear.py), composed
+    exactly as the engine composes them (nn.py: ReLU + truncation fused, the
+    backward truncation fused with ReLU' unless a pooling sits in between)."""
     from . import preprocessing as PP
 
     ring, f = model.ring, model.ring.f
@@ -264,13 +267,20 @@ def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, moment
             y = PR.conv_forward(ctx, l, model.W(l), model.Bias(l), *cur, e[4], e[5], mo_x_zero=(l == 0))
         ys.append(y)
         if l < L - 1:
-            z_mo, z_do, d = PR.dealer_op(ctx, l, PR.OP_RELU, *y)
-            a_mo, a_do, _ = PR.dealer_op(ctx, l, PR.OP_TRUNC_F, z_mo, z_do, k=f)
+            if nonlinear == "ot":
+                a_mo, a_do, d = PR.ot_op(ctx, l, PR.OP_TRUNC_F, "relu_trunc", *y, k=f)
+            else:
+                z_mo, z_do, d = PR.dealer_op(ctx, l, PR.OP_RELU, *y)
+                a_mo, a_do, _ = PR.dealer_op(ctx, l, PR.OP_TRUNC_F, z_mo, z_do, k=f)
             ds.append(d)
             cur = (a_mo, a_do)
             for k in seg[l]:
                 if model.layers[k][0] == "pool":
-                    cur = PR.avgpool_forward(ctx, l, *cur)
+                    if nonlinear == "ot":
+                        s_mo, s_do = CO.pool_sum(cur[0]), CO.pool_sum(cur[1])
+                        cur = PR.ot_op(ctx, l, PR.OP_POOL_F, "trunc", s_mo, s_do, k=2)[:2]
+                    else:
+                        cur = PR.avgpool_forward(ctx, l, *cur)
                 elif model.layers[k][0] == "flatten":
                     cur = (_flatten(cur[0]), _flatten(cur[1]))
     logits = _m(ys[-1][0] + ys[-1][1], ring)  # MO sends its share; DO reconstructs
@@ -310,13 +320,31 @@ def private_train_step(ctx: PR.Ctx, model: Model, x_enc, labels, lr=1e-2, moment
             else:
                 H, Wd = acts[l][1].shape[2:]
                 ga = PR.conv_backward_input(ctx, l, model.W(l), gy_mo, gy_do, H, Wd, e[4], e[5], mo_gy_zero=last)
-            t_mo, t_do, _ = PR.dealer_op(ctx, l, PR.OP_TRUNC_B, *ga, k=f)
-            for k in reversed(seg[l - 1]):
-                if model.layers[k][0] == "pool":
-                    t_mo, t_do = PR.avgpool_backward(ctx, l - 1, t_mo, t_do)
-                elif model.layers[k][0] == "flatten":
-                    t_mo, t_do = _unflatten(t_mo, model.io[k][0]), _unflatten(t_do, model.io[k][0])
-            gy_mo, gy_do, _ = PR.dealer_op(ctx, l - 1, PR.OP_RELU_B, t_mo, t_do, d=ds[l - 1])
+            pooled = any(model.layers[k][0] == "pool" for k in seg[l - 1])
+            if nonlinear == "ot" and not pooled:  # truncation + ReLU' fused (the engine's composition)
+                t_mo, t_do = ga
+                for k in reversed(seg[l - 1]):
+                    if model.layers[k][0] == "flatten":
+                        t_mo, t_do = _unflatten(t_mo, model.io[k][0]), _unflatten(t_do, model.io[k][0])
+                gy_mo, gy_do, _ = PR.ot_op(ctx, l - 1, PR.OP_RELU_B, "trunc_mux", t_mo, t_do, k=f, d=ds[l - 1])
+            else:
+                if nonlinear == "ot":
+                    t_mo, t_do, _ = PR.ot_op(ctx, l, PR.OP_TRUNC_B, "trunc", *ga, k=f)
+                else:
+                    t_mo, t_do, _ = PR.dealer_op(ctx, l, PR.OP_TRUNC_B, *ga, k=f)
+                for k in reversed(seg[l - 1]):
+                    if model.layers[k][0] == "pool":
+                        if nonlinear == "ot":
+                            r_mo, r_do = CO.pool_replicate(t_mo), CO.pool_replicate(t_do)
+                            t_mo, t_do, _ = PR.ot_op(ctx, l - 1, PR.OP_POOL_B, "trunc", r_mo, r_do, k=2)
+                        else:
+                            t_mo, t_do = PR.avgpool_backward(ctx, l - 1, t_mo, t_do)
+                    elif model.layers[k][0] == "flatten":
+                        t_mo, t_do = _unflatten(t_mo, model.io[k][0]), _unflatten(t_do, model.io[k][0])
+                if nonlinear == "ot":
+                    gy_mo, gy_do, _ = PR.ot_op(ctx, l - 1, PR.OP_RELU_B, "mux", t_mo, t_do, d=ds[l - 1])
+                else:
+                    gy_mo, gy_do, _ = PR.dealer_op(ctx, l - 1, PR.OP_RELU_B, t_mo, t_do, d=ds[l - 1])
     model.sgd(gws, gbs, lr, momentum)
     return loss, gws, gbs
 

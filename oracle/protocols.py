@@ -34,7 +34,7 @@ from . import packing as PK
 from .ring import DO, MO, RingParams, SeededRng, encode_fixed, to_signed
 
 OP_FWD, OP_BWD_X, OP_GRAD_W, OP_GRAD_B, OP_RELU, OP_TRUNC_F, OP_TRUNC_B, OP_RELU_B, OP_POOL_F, OP_POOL_B = range(10)
-P_MASK, P_ENC, P_DEALER, P_DP = range(4)
+P_MASK, P_ENC, P_DEALER, P_DP, P_OT = range(5)
 
 
 def stream_id(layer: int, op: int, purpose: int) -> int:
@@ -267,6 +267,21 @@ def avgpool_backward(ctx: Ctx, layer: int, g_mo, g_do):
 
 
 # ----------------------------------------------------- dealer non-linear ---
+
+def ot_op(ctx: Ctx, layer: int, op: int, kind: str, y_mo, y_do, k: int = 0, d=None):
+    """The OT-protocol backend (oracle/nonlinear.py) on stream (layer, op, P_OT):
+    kind in drelu / mux / trunc / relu_trunc / trunc_mux; returns (mo, do, d)."""
+    from . import nonlinear as NL
+
+    shape = np.shape(y_mo)
+    y0, y1, dd = NL.nl_op(kind, y_mo, y_do, ctx.ring.ell, k=k, d=d, seed=ctx.seed,
+                          stream=stream_id(layer, op, P_OT))
+    if dd is not None:
+        dd = dd.reshape(shape)
+    if y0 is None:
+        return None, None, dd
+    return y0.reshape(shape), y1.reshape(shape), dd
+
 
 def dealer_op(ctx: Ctx, layer: int, op: int, y_mo, y_do, k: int = 0, d=None):
     """Reconstruct, apply, reshare with r = uniform_ring(stream(layer, op, dealer))."""

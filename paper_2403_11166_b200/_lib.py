@@ -81,6 +81,8 @@ SIGNATURES = {
     "pb_ring_matmul_ex": [P, P, I64, I64, I64, INT, INT, I32, P, I32, P],
     "pb_scatter_u64": [P, P, P, I64, P],
     "pb_mask_mac": [P, P, P, P, P, I32, I32, I32, P, P, I32, P, INT, U64, P, P, P],
+    "pb_nl_words": [INT],
+    "pb_nl_op": [INT, P, P, I64, I32, I32, P, P, U64, P, U64, U64, P, P, P],
     "pb_ring_matmul_add": [P, P, I64, I64, I64, INT, INT, P, I32, I32, P, P],
     "pb_host_softmax_pre": [P, I32, I32, I32, I32, P],
     "pb_host_softmax_post": [P, I32, I32, P, I32, I32, I32, P, P],
@@ -114,6 +116,7 @@ RING_ADD, RING_SUB, RING_MUL, RING_NEG, RING_SCALAR_MUL, RING_MASK, RING_ARITH_S
 DEALER_RELU, DEALER_TRUNC, DEALER_SELECT, DEALER_RESHARE, DEALER_RELU_TRUNC, DEALER_TRUNC_SELECT = range(6)
 CONV_FWD, CONV_BWDX, CONV_GRADW = range(3)
 BACKEND_AUTO, BACKEND_CUDA_CORE, BACKEND_TENSOR = range(3)
+NL_DRELU, NL_MUX, NL_TRUNC, NL_RELU_TRUNC, NL_TRUNC_MUX = range(5)
 POOL_SUM, POOL_REPLICATE = range(2)
 
 _lib = None

@@ -1,0 +1,221 @@
+// pb_nonlinear.cu — the OT-based non-linear protocols of SPEC:491-581 /
+// PAPER:1248-1268 (CrypTFlow2-style) on the B200, with SPEC:479's dealer OT
+// backend ("local correlated-randomness generator ... fast, insecure") as the
+// oblivious-transfer functionality: the receiver obtains message[choice].
+// Both parties run in this process, so every round of a protocol instance is
+// evaluated by one thread per element -- each party's messages computed only
+// from that party's inputs and randomness, the opened values from both
+// parties' messages -- and the communication is counted by the caller's census.
+//
+//   secure comparison  1{a < b}, a at P0 (the MO), b at P1 (the DO): 4-bit
+//                      blocks, per block one 1-of-16 OT of P0's (lt, eq) table
+//                      masked with P0's random bits, the blocks combined in a
+//                      tree lt = lt_hi ^ (eq_hi & lt_lo), eq = eq_hi & eq_lo
+//                      with Beaver bit triples from the dealer (XOR shares)
+//   DReLU              1{x >= 0} = 1 ^ MSB(x0) ^ MSB(x1) ^ carry, carry =
+//                      1{2^(l-1) - 1 - x0' < x1'} over l-1 bits
+//   MUX / bit inject   d * x from XOR-shared d with two 1-of-2 OTs (CrypTFlow2
+//                      Alg. 6): z0 = r0 - r1 + d x1, z1 = r1 - r0 + d x0
+//   faithful trunc     arith_shift(x, k) = ((x0' >> k) + (x1 >> k) + c
+//                      - w 2^(l-k)) - 2^(l-1-k), x0' = x0 + 2^(l-1): wrap w and
+//                      low carry c by two comparisons, B2A by the MUX
+//
+// Every random word comes from the numpy-identical Philox4x64 stream
+// (seed, stream_id) at raw index elem * WORDS + k, so oracle/nonlinear.py
+// restates each protocol bit for bit.
+#include "pb_common.cuh"
+
+namespace {
+
+struct Rng {
+  uint64_t seed, stream, base;
+  __device__ __forceinline__ uint64_t w(int k) const { return philox_np_raw(seed, stream, base + (uint64_t)k); }
+};
+
+// Beaver AND of XOR-shared bits with triple (u0, u1, v0, v1, w0): the parties
+// open d = x ^ u and e = y ^ v.
+__device__ __forceinline__ void and_gate(uint32_t x0, uint32_t x1, uint32_t y0, uint32_t y1, uint32_t t,
+                                         uint32_t& z0, uint32_t& z1) {
+  const uint32_t u0 = t & 1, u1 = (t >> 1) & 1, v0 = (t >> 2) & 1, v1 = (t >> 3) & 1, w0 = (t >> 4) & 1;
+  const uint32_t w1 = ((u0 ^ u1) & (v0 ^ v1)) ^ w0;  // the dealer's second triple share
+  const uint32_t d = (x0 ^ u0) ^ (x1 ^ u1), e = (y0 ^ v0) ^ (y1 ^ v1);  // opened
+  z0 = w0 ^ (d & v0) ^ (e & u0) ^ (d & e);
+  z1 = w1 ^ (d & v1) ^ (e & u1);
+}
+
+// 5 triple bits number t from the little-endian bit string of words tw[0..3]
+__device__ __forceinline__ uint32_t triple_bits(const uint64_t (&tw)[4], int t) {
+  const int bit = 5 * t, i = bit >> 6, o = bit & 63;
+  uint64_t v = tw[i] >> o;
+  if (o > 59) v |= tw[i + 1] << (64 - o);
+  return (uint32_t)(v & 31u);
+}
+
+// XOR shares (c0 at P0, c1 at P1) of 1{a < b} over nbits <= 64 bits.
+// lt0 / eq0: P0's random leaf masks (bit j = block j); tw: triple words.
+__device__ __forceinline__ void cmp_lt(uint64_t a, uint64_t b, int nbits, uint32_t lt0m, uint32_t eq0m,
+                                       const uint64_t (&tw)[4], uint32_t& c0, uint32_t& c1) {
+  const int q = (nbits + 3) >> 2;
+  uint32_t L0 = 0, L1 = 0, E0 = 0, E1 = 0;  // node j's shares at bit j
+  for (int j = 0; j < q; ++j) {  // leaf OTs: P1 (choice b_j) learns P0's table entry
+    const uint32_t aj = (uint32_t)(a >> (4 * j)) & 15u, bj = (uint32_t)(b >> (4 * j)) & 15u;
+    const uint32_t l0 = (lt0m >> j) & 1u, e0 = (eq0m >> j) & 1u;
+    const uint32_t lt_table = (0xFFFEu << aj) & 0xFFFFu;  // bit k: 1{a_j < k}
+    const uint32_t eq_table = 1u << aj;                   // bit k: 1{a_j == k}
+    L0 |= l0 << j;
+    E0 |= e0 << j;
+    L1 |= (l0 ^ ((lt_table >> bj) & 1u)) << j;
+    E1 |= (e0 ^ ((eq_table >> bj) & 1u)) << j;
+  }
+  int cnt = q, t = 0;
+  while (cnt > 1) {  // combine (lo = 2i, hi = 2i + 1) pairs; an odd last node passes through
+    uint32_t nL0 = 0, nL1 = 0, nE0 = 0, nE1 = 0;
+    int nc = 0;
+    for (int i = 0; i + 1 < cnt; i += 2, ++nc) {
+      const uint32_t ll0 = (L0 >> i) & 1u, ll1 = (L1 >> i) & 1u, el0 = (E0 >> i) & 1u, el1 = (E1 >> i) & 1u;
+      const uint32_t lh0 = (L0 >> (i + 1)) & 1u, lh1 = (L1 >> (i + 1)) & 1u;
+      const uint32_t eh0 = (E0 >> (i + 1)) & 1u, eh1 = (E1 >> (i + 1)) & 1u;
+      uint32_t a0, a1, b0, b1;
+      and_gate(eh0, eh1, ll0, ll1, triple_bits(tw, t++), a0, a1);  // eq_hi & lt_lo
+      and_gate(eh0, eh1, el0, el1, triple_bits(tw, t++), b0, b1);  // eq_hi & eq_lo
+      nL0 |= (lh0 ^ a0) << nc;
+      nL1 |= (lh1 ^ a1) << nc;
+      nE0 |= b0 << nc;
+      nE1 |= b1 << nc;
+    }
+    if (cnt & 1) {
+      nL0 |= ((L0 >> (cnt - 1)) & 1u) << nc;
+      nL1 |= ((L1 >> (cnt - 1)) & 1u) << nc;
+      nE0 |= ((E0 >> (cnt - 1)) & 1u) << nc;
+      nE1 |= ((E1 >> (cnt - 1)) & 1u) << nc;
+      ++nc;
+    }
+    L0 = nL0, L1 = nL1, E0 = nE0, E1 = nE1, cnt = nc;
+  }
+  c0 = L0 & 1u;
+  c1 = L1 & 1u;
+}
+
+__device__ __forceinline__ uint64_t lmask(int ell) { return ell >= 64 ? ~0ull : ((1ull << ell) - 1); }
+
+// DReLU (4 words: leaf masks, 3 triple words): XOR shares of 1{x >= 0}.
+__device__ __forceinline__ void drelu(uint64_t x0, uint64_t x1, int ell, const Rng& r, int off, uint32_t& d0,
+                                      uint32_t& d1) {
+  const int h = ell - 1;
+  const uint64_t hm = (1ull << h) - 1;
+  const uint64_t lw = r.w(off);
+  const uint64_t tw[4] = {r.w(off + 1), r.w(off + 2), r.w(off + 3), 0ull};
+  uint32_t c0, c1;
+  cmp_lt(hm - (x0 & hm), x1 & hm, h, (uint32_t)(lw & 0xFFFFu), (uint32_t)((lw >> 16) & 0xFFFFu), tw, c0, c1);
+  d0 = 1u ^ (uint32_t)((x0 >> h) & 1u) ^ c0;
+  d1 = (uint32_t)((x1 >> h) & 1u) ^ c1;
+}
+
+// MUX (2 words: r0, r1): arithmetic shares of d * x from XOR-shared d.
+__device__ __forceinline__ void mux(uint32_t d0, uint32_t d1, uint64_t x0, uint64_t x1, uint64_t m, const Rng& r,
+                                    int off, uint64_t& z0, uint64_t& z1) {
+  const uint64_t r0 = r.w(off) & m, r1 = r.w(off + 1) & m;
+  const uint64_t m0[2] = {(uint64_t)(0 - r0) + (d0 ? x0 : 0ull), (uint64_t)(0 - r0) + (d0 ? 0ull : x0)};  // P0 sends
+  const uint64_t m1[2] = {(uint64_t)(0 - r1) + (d1 ? x1 : 0ull), (uint64_t)(0 - r1) + (d1 ? 0ull : x1)};  // P1 sends
+  const uint64_t y1 = m0[d1], y0 = m1[d0];  // 1-of-2 OTs: P1 chooses with d1, P0 with d0
+  z0 = (r0 + y0) & m;
+  z1 = (r1 + y1) & m;
+}
+
+// Faithful arithmetic shift by k (9 words: leaves, 3 + 1 triple words, 2 x 2 MUX words).
+__device__ __forceinline__ void trunc(uint64_t x0, uint64_t x1, int ell, int k, const Rng& r, int off, uint64_t& y0,
+                                      uint64_t& y1) {
+  const uint64_t m = lmask(ell), km = (1ull << k) - 1;
+  const uint64_t xb = (x0 + (1ull << (ell - 1))) & m;  // P0's biased share: signed -> unsigned order
+  const uint64_t lw = r.w(off);
+  const uint64_t tw1[4] = {r.w(off + 1), r.w(off + 2), r.w(off + 3), 0ull};
+  const uint64_t tw2[4] = {r.w(off + 4), 0ull, 0ull, 0ull};
+  uint32_t w0, w1, c0, c1;
+  cmp_lt(m - xb, x1, ell, (uint32_t)(lw & 0xFFFFu), (uint32_t)((lw >> 16) & 0xFFFFu), tw1, w0, w1);  // wrap
+  cmp_lt(km - (xb & km), x1 & km, k, (uint32_t)((lw >> 32) & 0xFFFFu), (uint32_t)((lw >> 48) & 0xFFFFu), tw2, c0,
+         c1);  // low carry
+  uint64_t C0, C1, W0, W1;
+  mux(c0, c1, 1ull, 0ull, m, r, off + 5, C0, C1);                // B2A(c)
+  mux(w0, w1, 1ull << (ell - k), 0ull, m, r, off + 7, W0, W1);   // B2A(w) * 2^(l-k)
+  y0 = ((xb >> k) + C0 - W0 - (1ull << (ell - 1 - k))) & m;
+  y1 = ((x1 >> k) + C1 - W1) & m;
+}
+
+constexpr int W_DRELU = 4, W_MUX = 2, W_TRUNC = 9;
+
+// op: 0 DReLU (d out), 1 MUX (d in), 2 TRUNC, 3 RELU + TRUNC (d out), 4 TRUNC + MUX (d in)
+__global__ void __launch_bounds__(256) k_nl(int op, const uint64_t* __restrict__ x0, const uint64_t* __restrict__ x1,
+                                            int64_t n, int ell, int k, const uint8_t* __restrict__ d_in,
+                                            uint8_t* __restrict__ d_out, uint64_t seed_arg, const uint64_t* seed_dev,
+                                            uint64_t stream_id, uint64_t raw_offset, int words,
+                                            uint64_t* __restrict__ y0, uint64_t* __restrict__ y1) {
+  const uint64_t seed = np_seed(seed_arg, seed_dev);
+  const uint64_t m = lmask(ell);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const Rng r{seed, stream_id, raw_offset + (uint64_t)i * words};
+    const uint64_t a = x0[i] & m, b = x1[i] & m;
+    uint32_t d0 = 0, d1 = 0;
+    uint64_t z0 = a, z1 = b;
+    if (op == 1 || op == 4) {
+      d0 = d_in[i] & 1u;
+      d1 = (d_in[i] >> 1) & 1u;
+    }
+    switch (op) {
+      case 0: drelu(a, b, ell, r, 0, d0, d1); break;
+      case 1: mux(d0, d1, a, b, m, r, 0, z0, z1); break;
+      case 2: trunc(a, b, ell, k, r, 0, z0, z1); break;
+      case 3: {
+        drelu(a, b, ell, r, 0, d0, d1);
+        uint64_t u0, u1;
+        mux(d0, d1, a, b, m, r, W_DRELU, u0, u1);
+        trunc(u0, u1, ell, k, r, W_DRELU + W_MUX, z0, z1);
+        break;
+      }
+      default: {
+        uint64_t u0, u1;
+        trunc(a, b, ell, k, r, 0, u0, u1);
+        mux(d0, d1, u0, u1, m, r, W_TRUNC, z0, z1);
+        break;
+      }
+    }
+    if (op == 0 || op == 3) d_out[i] = (uint8_t)(d0 | (d1 << 1));
+    if (op != 0) {
+      y0[i] = z0;
+      y1[i] = z1;
+    }
+  }
+}
+
+}  // namespace
+
+// Random words per element of each op (the caller reserves n * words raw draws).
+extern "C" int pb_nl_words(int op) {
+  switch (op) {
+    case PB_NL_DRELU: return W_DRELU;
+    case PB_NL_MUX: return W_MUX;
+    case PB_NL_TRUNC: return W_TRUNC;
+    case PB_NL_RELU_TRUNC: return W_DRELU + W_MUX + W_TRUNC;
+    case PB_NL_TRUNC_MUX: return W_TRUNC + W_MUX;
+    default: return -1;
+  }
+}
+
+extern "C" int pb_nl_op(int op, const uint64_t* x0, const uint64_t* x1, int64_t n, int32_t ell, int32_t k,
+                        const uint8_t* d_in, uint8_t* d_out, uint64_t seed, const uint64_t* seed_dev,
+                        uint64_t stream_id, uint64_t raw_offset, uint64_t* y0, uint64_t* y1, void* stream) {
+  const int words = pb_nl_words(op);
+  if (words < 0) return pb_set_error(PB_ERR_ARG, "bad non-linear op");
+  if (ell < 4 || ell > 62) return pb_set_error(PB_ERR_ARG, "ell must be in [4, 62]");
+  const bool tr = op == PB_NL_TRUNC || op == PB_NL_RELU_TRUNC || op == PB_NL_TRUNC_MUX;
+  // the low-carry comparison's 2 (ceil(k/4) - 1) triples live in one 64-bit word
+  if (tr && (k < 1 || k >= ell - 1 || k > 28)) return pb_set_error(PB_ERR_ARG, "truncation bits must be in [1, 28]");
+  if (n <= 0) return PB_OK;
+  if (!x0 || !x1) return pb_set_error(PB_ERR_ARG, "null argument");
+  if ((op == PB_NL_MUX || op == PB_NL_TRUNC_MUX) && !d_in) return pb_set_error(PB_ERR_ARG, "MUX needs d shares");
+  if ((op == PB_NL_DRELU || op == PB_NL_RELU_TRUNC) && !d_out) return pb_set_error(PB_ERR_ARG, "null d_out");
+  if (op != PB_NL_DRELU && (!y0 || !y1)) return pb_set_error(PB_ERR_ARG, "null output");
+  k_nl<<<pb_grid_1d(n, 256), 256, 0, pb_stream_of(stream)>>>(op, x0, x1, n, ell, k, d_in, d_out, seed, seed_dev,
+                                                             stream_id, raw_offset, words, y0, y1);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}

@@ -39,7 +39,7 @@ from .poly_encoding import MatmulGeometry, conv_out_hw, plan_conv_layer, plan_ma
 from .ring import DO, MO, RingParams, RingTensor, SeededRng, ShareTensor, encode_fixed
 
 OP_FWD, OP_BWD_X, OP_GRAD_W, OP_GRAD_B, OP_RELU, OP_TRUNC_F, OP_TRUNC_B, OP_RELU_B, OP_POOL_F, OP_POOL_B = range(10)
-P_MASK, P_ENC, P_DEALER, P_DP = range(4)
+P_MASK, P_ENC, P_DEALER, P_DP, P_OT = range(5)
 
 # SPEC:372 message codes
 MSG_FWD_INPUT_CT = 0x10
@@ -234,6 +234,9 @@ class Session:
         self._aux_streams = {}
         self._prep_stream = None
         self.dp = None  # DpConfig: the DO's DP perturbation of revealed gradients, off by default
+        # non-linear backend: "dealer" (SPEC:479 reconstruct / apply / reshare) or
+        # "ot" (the OT-based protocols SPEC:491-581 with the dealer OT functionality)
+        self.nonlinear = "dealer"
         self.capture = None  # diagnostics: a list receives (masked output ciphertexts, useful slot positions)
         # operands prepared ahead of their protocol (prepare_operand): key
         # (layer, op, role) -> (device tensor, event or None); buffers persist
