@@ -66,7 +66,7 @@ LAN_BPS = 384e6  # PAPER:777 LAN, for the census' wire-time estimate
 KERNEL_ENTRY = {
     "k_enc_noise": "pb_encrypt_sk", "k_encrypt_sk": "pb_encrypt_sk", "k_encode_plain_mont": "pb_encode_plain_mont",
     "k_mask_ntt": "pb_mask_ntt", "k_mac_ws": "pb_ctpt_mac_tiled", "k_mac_eager": "pb_ctpt_mac_tiled",
-    "k_mask_mac": "pb_mask_mac",
+    "k_mask_mac": "pb_mask_mac", "k_nl": "pb_nl_op", "k_dealer": "pb_dealer_op_out",
     "k_decrypt_share_cluster": "pb_decrypt_to_share", "k_decrypt_inv": "pb_decrypt_to_share",
     "k_decode_gather": "pb_decrypt_to_share",
 }
@@ -442,7 +442,9 @@ def run_ours(args, rank, world):
     del runner
     torch.cuda.empty_cache()
     if not args.no_configs:
-        line["configs"] = {"c4": bench_c4(args, rank, world), "c5": bench_c5(args)}
+        line["configs"] = {"c4": bench_c4(args, rank, world), "c5": bench_c5(args),
+                           "c2_ot_nonlinear": bench_c4(args, rank, world, "mnist_mlp", "ot"),
+                           "c4_ot_nonlinear": bench_c4(args, rank, world, "cifar_cnn", "ot")}
     if rank != 0:
         return
     if not args.no_cpu and world == 1:
@@ -462,8 +464,11 @@ def run_ours(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def bench_c4(args, rank, world):
-    """configs[3]: CIFAR-10 CNN (PAPER Fig. 7) private step, B=64 per GPU, graph replay."""
+def bench_c4(args, rank, world, name="cifar_cnn", nonlinear="dealer"):
+    """configs[3]: CIFAR-10 CNN (PAPER Fig. 7) private step, B=64 per GPU, graph
+    replay; ``nonlinear="ot"``: ReLU / truncation / pooling through the
+    OT-based protocols (dealer OT functionality) instead of the
+    dealer's reconstruct-reshare."""
     import torch
 
     from paper_2403_11166_b200 import bfv
@@ -474,12 +479,16 @@ def bench_c4(args, rank, world):
 
     ring, params = RingParams(), BfvParams()
     sess = Session(params, ring, bfv.keygen(params, SeededRng(SEED, 0)), seed=SEED)
-    model = PN.Model("cifar_cnn", ring, seed=SEED)
+    sess.nonlinear = nonlinear
+    model = PN.Model(name, ring, seed=SEED)
     if world > 1:
         import torch.distributed as dist
 
         model.set_data_parallel(dist.group.WORLD, world)
-    xh, labels = PN.synthetic_images(SEED + rank, BATCH, model.in_shape, ring)
+    if len(model.in_shape) == 1:
+        xh, labels = PN.synthetic_mnist(SEED + rank, BATCH, ring)
+    else:
+        xh, labels = PN.synthetic_images(SEED + rank, BATCH, model.in_shape, ring)
     x = RingTensor(encode_fixed(xh, ring), ring.f, ring, _canonical=True)
     runner = PN.GraphStep(sess, model, x)
     for i in range(3):
@@ -495,8 +504,9 @@ def bench_c4(args, rank, world):
         agg[e] = agg.get(e, 0.0) + v[0]
     del runner
     torch.cuda.empty_cache()
-    return {"workload": "configs[3]: CIFAR-10 CNN (5 conv + FC, PAPER Fig. 7) private training step",
-            "batch_per_gpu": BATCH, "value": world * BATCH / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
+    wl = {"cifar_cnn": "configs[3]: CIFAR-10 CNN (5 conv + FC, PAPER Fig. 7) private training step",
+          "mnist_mlp": "configs[1]: MNIST MLP 784-128-128-10 private training step"}[name]
+    return {"workload": wl, "nonlinear": nonlinear, "batch_per_gpu": BATCH, "value": world * BATCH / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
             "steps": steps, "kernels_ms_per_step": {k: round(v, 4) for k, v in
                                                     sorted(agg.items(), key=lambda kv: -kv[1])[:10]}}
 

@@ -35,6 +35,14 @@ struct PbDev {
   const uint2* tw3_fwd;                        // [L][31*N/32] P3-stage twiddles, interleaved
   const uint2* tw3_inv;
   int tw3_stride;                              // uint2 per limb in tw3_* (0 when N < 2048)
+  // N = 32768 only: the two independent N/2-point transforms the rows split into
+  // after the cross-half stage (2-CTA cluster NTT): half b's tables [2][L][N/2]
+  // with entry I = psi^brv(I + (1 + b) 2^floor(log2 I)), and their P3 tables
+  const uint2* tws_fwd;
+  const uint2* tws_inv;
+  const uint2* tw3s_fwd;
+  const uint2* tw3s_inv;
+  int tw3s_stride;
 };
 
 struct pb_ctx {
@@ -43,6 +51,7 @@ struct pb_ctx {
   uint2* d_tw_inv;
   uint2* d_tw3_fwd;
   uint2* d_tw3_inv;
+  uint2* d_tws;  // [fwd | inv] half-transform tables (N = 32768), one allocation
   pb_params host;   // the descriptor the context was created from
 };
 

@@ -27,9 +27,24 @@
 
 namespace {
 
+// An element's random words, generated block-wise: raw draws base .. base+n-1
+// of the numpy Philox4x64 stream come from ceil-covering 4-word counter
+// blocks, each computed once (not once per word as philox_np_raw would).
+constexpr int W_MAX = 16;
 struct Rng {
-  uint64_t seed, stream, base;
-  __device__ __forceinline__ uint64_t w(int k) const { return philox_np_raw(seed, stream, base + (uint64_t)k); }
+  uint64_t v[W_MAX];
+  __device__ __forceinline__ uint64_t w(int k) const { return v[k]; }
+  __device__ __forceinline__ void fill(uint64_t seed, uint64_t stream, uint64_t base, int n) {
+    const uint64_t b0 = base >> 2, b1 = (base + n - 1) >> 2;
+    for (uint64_t blk = b0; blk <= b1; ++blk) {
+      const u64x4 o = philox4x64_10(blk + 1, 0, 0, 0, seed, stream);  // numpy pre-increments the counter
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t k = (int64_t)(blk * 4 + j) - (int64_t)base;
+        if (k >= 0 && k < n) v[k] = o.v[j];
+      }
+    }
+  }
 };
 
 // Beaver AND of XOR-shared bits with triple (u0, u1, v0, v1, w0): the parties
@@ -152,7 +167,8 @@ __global__ void __launch_bounds__(256) k_nl(int op, const uint64_t* __restrict__
   const uint64_t seed = np_seed(seed_arg, seed_dev);
   const uint64_t m = lmask(ell);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const Rng r{seed, stream_id, raw_offset + (uint64_t)i * words};
+    Rng r;
+    r.fill(seed, stream_id, raw_offset + (uint64_t)i * words, words);
     const uint64_t a = x0[i] & m, b = x1[i] & m;
     uint32_t d0 = 0, d1 = 0;
     uint64_t z0 = a, z1 = b;

@@ -6,6 +6,8 @@
 
 #include "pb_ntt.cuh"
 
+#include <cooperative_groups.h>
+
 // ------------------------------------------------------------------ errors --
 static thread_local char g_err[512] = "";
 
@@ -180,9 +182,58 @@ extern "C" int pb_ctx_create(const pb_params* p, pb_ctx** out) {
     if (e == cudaSuccess) e = cudaMemcpy(c->d_tw3_fwd, h3f, (size_t)L * n3 * sizeof(uint2), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(c->d_tw3_inv, h3i, (size_t)L * n3 * sizeof(uint2), cudaMemcpyHostToDevice);
   }
+  // N = 32768: tables of the two half transforms (pb_ntt k_ntt_*_c2).  Half b,
+  // stage s' (m' = 2^s' groups) of the N/2-point transform is stage s' + 1 of
+  // the full one restricted to groups b m' .. (b+1) m' - 1, twiddle index
+  // 2 m' + b m' + g = I + (1 + b) m' for local index I = m' + g.
+  if (e == cudaSuccess && logN == 15) {
+    const int Nh = N / 2, Th = Nh / 32;
+    const size_t n3s = (size_t)31 * Th;
+    const size_t per_dir = (size_t)2 * L * (Nh + n3s);
+    uint2* hs = (uint2*)calloc(2 * per_dir, sizeof(uint2));
+    if (!hs) e = cudaErrorMemoryAllocation;
+    for (int dir = 0; hs && dir < 2; ++dir) {
+      uint2* tab = hs + dir * per_dir;                 // [2][L][Nh]
+      uint2* t3 = tab + (size_t)2 * L * Nh;            // [2][L][n3s]
+      uint2* full = dir ? h_i : h_f;
+      for (int b = 0; b < 2; ++b)
+        for (int l = 0; l < L; ++l) {
+          uint2* sub = tab + ((size_t)b * L + l) * Nh;
+          for (int I = 1; I < Nh; ++I) {
+            int mp = 1;
+            while (2 * mp <= I) mp *= 2;
+            sub[I] = full[(size_t)l * N + I + (1 + b) * mp];
+          }
+          uint2* s3 = t3 + ((size_t)b * L + l) * n3s;
+          for (int D = 0; D < 5; ++D) {
+            const int s = 14 - 5 + D;
+            const size_t off = (size_t)((1 << D) - 1) * Th;
+            for (int tid = 0; tid < Th; ++tid)
+              for (int r = 0; r < (1 << D); ++r) {
+                const size_t src = (1u << s) + ((size_t)tid << D) + r;
+                const size_t dst = (D == 0) ? off + tid : off + 2 * ((size_t)(r >> 1) * Th + tid) + (r & 1);
+                s3[dst] = sub[src];
+              }
+          }
+        }
+    }
+    if (hs) {
+      e = cudaMalloc(&c->d_tws, 2 * per_dir * sizeof(uint2));
+      if (e == cudaSuccess) e = cudaMemcpy(c->d_tws, hs, 2 * per_dir * sizeof(uint2), cudaMemcpyHostToDevice);
+      free(hs);
+      if (e == cudaSuccess) {
+        d.tws_fwd = c->d_tws;
+        d.tw3s_fwd = c->d_tws + (size_t)2 * L * Nh;
+        d.tws_inv = c->d_tws + per_dir;
+        d.tw3s_inv = d.tws_inv + (size_t)2 * L * Nh;
+        d.tw3s_stride = (int)n3s;
+      }
+    }
+  }
   free(h_f); free(h_i); free(h3f); free(h3i);
   if (e != cudaSuccess) {
-    cudaFree(c->d_tw_fwd); cudaFree(c->d_tw_inv); cudaFree(c->d_tw3_fwd); cudaFree(c->d_tw3_inv); delete c;
+    cudaFree(c->d_tw_fwd); cudaFree(c->d_tw_inv); cudaFree(c->d_tw3_fwd); cudaFree(c->d_tw3_inv);
+    cudaFree(c->d_tws); delete c;
     return pb_set_cuda_error(e);
   }
   d.tw_fwd = c->d_tw_fwd;
@@ -200,6 +251,7 @@ extern "C" int pb_ctx_destroy(pb_ctx* c) {
   cudaFree(c->d_tw_inv);
   cudaFree(c->d_tw3_fwd);
   cudaFree(c->d_tw3_inv);
+  cudaFree(c->d_tws);
   delete c;
   return PB_OK;
 }
@@ -259,6 +311,99 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN)) k_ntt_inv(PbD
   }
 }
 
+// N = 32768 as a CLUSTER of two 512-thread CTAs per row (one CTA of 1024
+// threads at 64 registers leaves one CTA per SM whose every barrier stalls the
+// whole SM).  The forward's first stage (distance N/2, twiddle psi^brv(1))
+// pairs the two halves: each CTA stages its half in shared memory and reads
+// the partner's through DSMEM (cluster barrier on both sides); after it the
+// halves are independent N/2-point transforms (P.tws_* tables), run as the
+// register NTT Ntt<14> by each CTA.  Same arithmetic as K:31-77 (Harvey lazy
+// butterflies), bit-identical output in the device order of the full row:
+// half b's P3 register v of thread t is uint4 #(v * 1024 + b * 512 + t).
+namespace cg = cooperative_groups;
+
+__device__ __forceinline__ int64_t limb_major_row(const PbDev& P, const int32_t* row_limb, int64_t n_rows,
+                                                  int64_t b) {
+  const uint32_t per = (row_limb == nullptr && n_rows % P.L == 0 && n_rows < (1ll << 31)) ? (uint32_t)(n_rows / P.L) : 0;
+  return per ? (int64_t)((uint32_t)b % per) * P.L + (uint32_t)b / per : b;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 2)
+    k_ntt_fwd_c2(PbDev P, uint32_t* rows, int64_t n_rows, const int32_t* row_limb) {
+  using Nt = pb::Ntt<14>;
+  extern __shared__ uint32_t sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int half = (int)cl.block_rank();
+  const int tid = threadIdx.x;
+  const uint32_t* peer = cl.map_shared_rank(sm, half ^ 1);
+  for (int64_t c = blockIdx.x >> 1; c < n_rows; c += gridDim.x >> 1) {
+    const int64_t r = limb_major_row(P, row_limb, n_rows, c);
+    const int limb = row_limb_of(P, row_limb, r);
+    const uint32_t q = P.q[limb], q2 = 2 * q;
+    uint32_t* row = rows + r * 32768;
+    uint32_t a[32];
+    Nt::gld1(row + half * 16384, a, tid);  // natural index half N/2 + tid + 512 c
+#pragma unroll
+    for (int k = 0; k < 32; ++k) sm[k * 512 + tid] = a[k];
+    cl.sync();
+    const uint2 w = __ldg(P.tw_fwd + (size_t)limb * 32768 + 1);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {  // stage 0: (x, y) -> (x + w y, x - w y), inputs < q
+      const uint32_t o = peer[k * 512 + tid];
+      const uint32_t tt = mul_shoup_lazy(half ? a[k] : o, w.x, w.y, q);  // [0, 2q)
+      a[k] = half ? o - tt + q2 : a[k] + tt;                             // [0, 3q)
+    }
+    cl.sync();  // the partner has read this CTA's half: shared memory is free
+    const size_t sub = (size_t)half * P.L + limb;
+    Nt::forward(a, sm, P.tws_fwd + sub * 16384, P.tw3s_fwd + sub * P.tw3s_stride, tid, q);
+    uint4* p = reinterpret_cast<uint4*>(row) + half * 512 + tid;
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+      p[v * 1024] = make_uint4(pb::canon4(a[4 * v], q), pb::canon4(a[4 * v + 1], q), pb::canon4(a[4 * v + 2], q),
+                               pb::canon4(a[4 * v + 3], q));
+    __syncthreads();
+  }
+}
+
+// The inverse in reverse: the two half transforms (GS, unscaled), then the
+// cross-half stage with N^-1 folded in: x' = (x + y) N^-1, y' = (x - y) w N^-1.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 2)
+    k_ntt_inv_c2(PbDev P, uint32_t* rows, int64_t n_rows, const int32_t* row_limb) {
+  using Nt = pb::Ntt<14>;
+  extern __shared__ uint32_t sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int half = (int)cl.block_rank();
+  const int tid = threadIdx.x;
+  const uint32_t* peer = cl.map_shared_rank(sm, half ^ 1);
+  for (int64_t c = blockIdx.x >> 1; c < n_rows; c += gridDim.x >> 1) {
+    const int64_t r = limb_major_row(P, row_limb, n_rows, c);
+    const int limb = row_limb_of(P, row_limb, r);
+    const uint32_t q = P.q[limb], q2 = 2 * q;
+    uint32_t* row = rows + r * 32768;
+    uint32_t a[32];
+    const uint4* p = reinterpret_cast<const uint4*>(row) + half * 512 + tid;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const uint4 x = __ldg(p + v * 1024);
+      a[4 * v] = x.x; a[4 * v + 1] = x.y; a[4 * v + 2] = x.z; a[4 * v + 3] = x.w;
+    }
+    const size_t sub = (size_t)half * P.L + limb;
+    Nt::inverse(a, sm, P.tws_inv + sub * 16384, P.tw3s_inv + sub * P.tw3s_stride, tid, q);  // [0, 2q), P1 layout
+    __syncthreads();  // every thread is past the inverse's last shared-memory read
+#pragma unroll
+    for (int k = 0; k < 32; ++k) sm[k * 512 + tid] = a[k];
+    cl.sync();
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const uint32_t o = peer[k * 512 + tid];
+      a[k] = half ? mul_shoup(o - a[k] + q2, P.w0n[limb], P.w0n_sh[limb], q)
+                  : mul_shoup(a[k] + o, P.ninv[limb], P.ninv_sh[limb], q);
+    }
+    cl.sync();
+    Nt::gst1(row + half * 16384, a, tid);
+  }
+}
+
 // Small-N path (N <= 1024): one CTA per row, one radix-2 stage per barrier,
 // fully reduced arithmetic.  Used for tests / tiny parameter sets.
 __global__ void k_ntt_small(PbDev P, uint32_t* rows, int64_t n_rows, const int32_t* row_limb, int inverse) {
@@ -298,6 +443,19 @@ __global__ void k_ntt_small(PbDev P, uint32_t* rows, int64_t n_rows, const int32
 template <int LOGN>
 static void launch_ntt(const PbDev& P, uint32_t* rows, int64_t n_rows, const int32_t* row_limb,
                        cudaStream_t st, bool inverse) {
+  if (LOGN == 15 && P.tws_fwd) {  // two-CTA cluster per row
+    const size_t smem = pb::Ntt<14>::SMEM_WORDS * 4;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_ntt_fwd_c2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_ntt_inv_c2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    const int64_t clusters = n_rows < 148 * 64 ? n_rows : 148 * 64;
+    if (inverse) k_ntt_inv_c2<<<(unsigned)(2 * clusters), 512, smem, st>>>(P, rows, n_rows, row_limb);
+    else k_ntt_fwd_c2<<<(unsigned)(2 * clusters), 512, smem, st>>>(P, rows, n_rows, row_limb);
+    return;
+  }
   using Nt = pb::Ntt<LOGN>;
   const size_t smem = Nt::SMEM_WORDS * sizeof(uint32_t);
   const int grid = (int)(n_rows < (1 << 30) ? n_rows : (1 << 30));
