@@ -444,7 +444,9 @@ def run_ours(args, rank, world):
     if not args.no_configs:
         line["configs"] = {"c4": bench_c4(args, rank, world), "c5": bench_c5(args),
                            "c2_ot_nonlinear": bench_c4(args, rank, world, "mnist_mlp", "ot"),
-                           "c4_ot_nonlinear": bench_c4(args, rank, world, "cifar_cnn", "ot")}
+                           "c4_ot_nonlinear": bench_c4(args, rank, world, "cifar_cnn", "ot"),
+                           "c2_prep_online": bench_c4(args, rank, world, "mnist_mlp", prep_m=8),
+                           "c4_prep_online": bench_c4(args, rank, world, "cifar_cnn", prep_m=8)}
     if rank != 0:
         return
     if not args.no_cpu and world == 1:
@@ -464,11 +466,14 @@ def run_ours(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def bench_c4(args, rank, world, name="cifar_cnn", nonlinear="dealer"):
+def bench_c4(args, rank, world, name="cifar_cnn", nonlinear="dealer", prep_m=0):
     """configs[3]: CIFAR-10 CNN (PAPER Fig. 7) private step, B=64 per GPU, graph
     replay; ``nonlinear="ot"``: ReLU / truncation / pooling through the
     OT-based protocols (dealer OT functionality) instead of the
-    dealer's reconstruct-reshare."""
+    dealer's reconstruct-reshare; ``prep_m``: SPEC mode "prep" (Pencil+,
+    PAPER Alg. 3/4) -- the offline mask banks (m^2 HE evaluations per
+    operator) built first and timed separately, the step is the HE-free
+    online phase."""
     import torch
 
     from paper_2403_11166_b200 import bfv
@@ -490,7 +495,16 @@ def bench_c4(args, rank, world, name="cifar_cnn", nonlinear="dealer"):
     else:
         xh, labels = PN.synthetic_images(SEED + rank, BATCH, model.in_shape, ring)
     x = RingTensor(encode_fixed(xh, ring), ring.f, ring, _canonical=True)
-    runner = PN.GraphStep(sess, model, x)
+    prep, bank_s = None, None
+    if prep_m:
+        from paper_2403_11166_b200 import preprocessing as PP
+
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        prep = PP.PrepState(sess, model, BATCH, m=prep_m, bank_seed=SEED)
+        torch.cuda.synchronize()
+        bank_s = time.perf_counter() - t0
+    runner = PN.GraphStep(sess, model, x, prep=prep)
     for i in range(3):
         runner.step(SEED + i, labels)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.int64, device="cuda")
@@ -506,7 +520,8 @@ def bench_c4(args, rank, world, name="cifar_cnn", nonlinear="dealer"):
     torch.cuda.empty_cache()
     wl = {"cifar_cnn": "configs[3]: CIFAR-10 CNN (5 conv + FC, PAPER Fig. 7) private training step",
           "mnist_mlp": "configs[1]: MNIST MLP 784-128-128-10 private training step"}[name]
-    return {"workload": wl, "nonlinear": nonlinear, "batch_per_gpu": BATCH, "value": world * BATCH / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
+    extra = {"mode": f"prep (Pencil+, m={prep_m})", "offline_bank_build_s": bank_s} if prep_m else {"mode": "fullhe"}
+    return {"workload": wl, "nonlinear": nonlinear, **extra, "batch_per_gpu": BATCH, "value": world * BATCH / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
             "steps": steps, "kernels_ms_per_step": {k: round(v, 4) for k, v in
                                                     sorted(agg.items(), key=lambda kv: -kv[1])[:10]}}
 

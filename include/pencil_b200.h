@@ -320,6 +320,11 @@ int pb_pool2(int op, const uint64_t* in, int64_t bc, int32_t H, int32_t W, int32
  * 2^ell; b == NULL means weights a_i alone (mb must be 1); base may be NULL. */
 int pb_ring_lincomb(int subtract, uint64_t* out, const uint64_t* base, const uint64_t* a, int32_t ma,
                     const uint64_t* b, int32_t mb, const uint64_t* T, int64_t n, int32_t ell, void* stream);
+/* The online scalars of one operator in one launch: k[i] (stream_k) and l[j]
+ * (stream_l), i, j < m, = uniform_ring draws 0..m-1 of each numpy-identical
+ * stream (R:60-61), 0 mapped to 1. */
+int pb_prep_scalars(uint64_t* k_out, uint64_t* l_out, int32_t m, uint64_t seed, const uint64_t* seed_dev,
+                    uint64_t stream_k, uint64_t stream_l, int32_t ell, void* stream);
 
 /* ------------------------------- dealer-assisted non-linear --- */
 /* The SPEC's dealer OT backend ("fast, insecure, default for benchmarks of

@@ -82,6 +82,7 @@ SIGNATURES = {
     "pb_scatter_u64": [P, P, P, I64, P],
     "pb_mask_mac": [P, P, P, P, P, I32, I32, I32, P, P, I32, P, INT, U64, P, P, P],
     "pb_nl_words": [INT],
+    "pb_prep_scalars": [P, P, I32, U64, P, U64, U64, I32, P],
     "pb_nl_op": [INT, P, P, I64, I32, I32, P, P, U64, P, U64, U64, P, P, P],
     "pb_ring_matmul_add": [P, P, I64, I64, I64, INT, INT, P, I32, I32, P, P],
     "pb_host_softmax_pre": [P, I32, I32, I32, I32, P],

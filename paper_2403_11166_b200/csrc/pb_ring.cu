@@ -561,3 +561,28 @@ extern "C" int pb_scatter_u64(uint64_t* out, const uint64_t* src, const int64_t*
   PB_CHECK_LAUNCH();
   return PB_OK;
 }
+
+// Pencil+ online scalars of one operator in one launch: k_i (the MO's, stream
+// stream_k) and l_j (the DO's, stream_l), i, j < m, each the first m
+// uniform_ring draws of its numpy-identical stream (R:60-61, raw >> (64 - ell))
+// with 0 replaced by 1 (the weights must be nonzero; P[0] = 2^-ell).
+namespace {
+__global__ void k_prep_scalars(uint64_t* k_out, uint64_t* l_out, int m, uint64_t seed_arg, const uint64_t* seed_dev,
+                               uint64_t stream_k, uint64_t stream_l, int ell) {
+  const uint64_t seed = np_seed(seed_arg, seed_dev);
+  const int t = threadIdx.x;
+  if (t >= 2 * m) return;
+  const int who = t >= m, i = t - who * m;
+  const uint64_t v = philox_np_raw(seed, who ? stream_l : stream_k, (uint64_t)i) >> (64 - ell);
+  (who ? l_out : k_out)[i] = v ? v : 1ull;
+}
+}  // namespace
+
+extern "C" int pb_prep_scalars(uint64_t* k_out, uint64_t* l_out, int32_t m, uint64_t seed, const uint64_t* seed_dev,
+                               uint64_t stream_k, uint64_t stream_l, int32_t ell, void* stream) {
+  if (!k_out || !l_out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (m < 1 || m > 256 || bad_ell(ell) || ell > 63) return pb_set_error(PB_ERR_ARG, "bad m / ell");
+  k_prep_scalars<<<1, 2 * m, 0, pb_stream_of(stream)>>>(k_out, l_out, m, seed, seed_dev, stream_k, stream_l, ell);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}

@@ -278,7 +278,7 @@ def _forward_layers(sess, model, prep, cur, acts, ds, ys, seg):
         e = model.layers[i]
         acts.append(cur)
         if prep is not None:
-            y = PP.prep_linear_forward(sess, l, prep.banks[l], model.W[l], model.B[l], *cur)
+            y = PP.prep_linear_forward(sess, l, prep.banks[l], model.W[l], model.B[l], *cur, mo_x_zero=(l == 0))
         elif e[0] == "fc":
             y = linear_forward(sess, l, model.W[l], model.B[l], *cur, mo_x_zero=(l == 0))
         else:
@@ -342,7 +342,8 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
             ew = dp_noise(sess, l, OP_GRAD_W, wshape, 2 * f)
             if prep is not None:
                 gbs[l] = (reveal_grad_bias if e[0] == "fc" else reveal_grad_bias_conv)(sess, l, gy_mo, gy_do, e=eb)
-                gw = PP.prep_grad_weight(sess, l, prep.banks[l], *acts[l], gy_mo, gy_do, e=ew)
+                gw = PP.prep_grad_weight(sess, l, prep.banks[l], *acts[l], gy_mo, gy_do, e=ew, mo_x_zero=(l == 0),
+                                         mo_gy_zero=last)
             elif e[0] == "fc":
                 gbs[l] = reveal_grad_bias(sess, l, gy_mo, gy_do, e=eb)
                 gw = grad_weight(sess, l, *acts[l], gy_mo, gy_do, e=ew, mo_x_zero=(l == 0), mo_gy_zero=last)
@@ -409,7 +410,7 @@ def _mask_specs(model: Model, B: int, ops, layers=None):
 
 def _backward_input(sess, model, l, e, acts, gy_mo, gy_do, last, prep):
     if prep is not None:
-        return PP.prep_linear_backward_input(sess, l, prep.banks[l], model.W[l], gy_mo, gy_do)
+        return PP.prep_linear_backward_input(sess, l, prep.banks[l], model.W[l], gy_mo, gy_do, mo_gy_zero=last)
     if e[0] == "fc":
         return linear_backward_input(sess, l, model.W[l], gy_mo, gy_do, mo_gy_zero=last)
     H, Wd = acts[l][1].shape[2:]

@@ -70,27 +70,31 @@ class Operator:
     def is_fc(self):
         return self.spec[0] == "fc"
 
-    def apply(self, u: torch.Tensor, v: torch.Tensor, ell: int) -> torch.Tensor:
-        """The plaintext operator on the device, mod 2^ell."""
+    def apply(self, u: torch.Tensor, v: torch.Tensor, ell: int, c: torch.Tensor | None = None) -> torch.Tensor:
+        """The plaintext operator on the device, mod 2^ell; ``c``: + c (fused
+        into the FC GEMM's epilogue)."""
         if self.is_fc:
             n_i, n_o = self.fc
             B = self.B
+            kw = dict(c=c, sign=1) if c is not None else {}
             if self.op == FWD:
-                return _ring_matmul(u, v, n_o, n_i, B, ell)
+                return _ring_matmul(u, v, n_o, n_i, B, ell, **kw)
             if self.op == BWDX:
-                return _ring_matmul(u, v, n_i, n_o, B, ell, ta=True)
+                return _ring_matmul(u, v, n_i, n_o, B, ell, ta=True, **kw)
             if self.op == GRADW:  # gY (n_o,B) X^T
-                return _ring_matmul(u, v, n_o, B, n_i, ell, tb=True)
-            return _ring_matmul(v, u, n_o, B, n_i, ell, tb=True)  # u = X, v = gY
+                return _ring_matmul(u, v, n_o, B, n_i, ell, tb=True, **kw)
+            return _ring_matmul(v, u, n_o, B, n_i, ell, tb=True, **kw)  # u = X, v = gY
         B, c_i, c_o, H, Wd, s, p, st = self.conv
         args = (B, c_i, c_o, H, Wd, s, p, st, ell)
         if self.op == FWD:
-            return _ring_conv(_lib.CONV_FWD, v, u, *args, self.out_shape)
-        if self.op == BWDX:
-            return _ring_conv(_lib.CONV_BWDX, v, u, *args, self.out_shape)
-        if self.op == GRADW:
-            return _ring_conv(_lib.CONV_GRADW, v, u, *args, self.out_shape)
-        return _ring_conv(_lib.CONV_GRADW, u, v, *args, self.out_shape)
+            out = _ring_conv(_lib.CONV_FWD, v, u, *args, self.out_shape)
+        elif self.op == BWDX:
+            out = _ring_conv(_lib.CONV_BWDX, v, u, *args, self.out_shape)
+        elif self.op == GRADW:
+            out = _ring_conv(_lib.CONV_GRADW, v, u, *args, self.out_shape)
+        else:
+            out = _ring_conv(_lib.CONV_GRADW, u, v, *args, self.out_shape)
+        return out if c is None else _add(out, c, ell)
 
     def he(self, sess, layer: int, u: torch.Tensor, v: torch.Tensor, s_mask: torch.Tensor) -> torch.Tensor:
         """DO's decryption of u o Enc(v) - s through the Alg. 1/2 evaluator."""
@@ -161,28 +165,56 @@ def _lincomb(out, base, a, b, T, ell, subtract):
     return out
 
 
-def _scalars(sess, layer: int, op: int, who: int, m: int) -> torch.Tensor:
-    k = sess.rng(layer, OP_ONLINE + op, who).uniform_ring((m,), sess.ring)
-    return torch.where(k == 0, torch.ones_like(k), k)  # nonzero (P[0] = 2^-59)
+def _scalars(sess, layer: int, op: int, m: int):
+    """(k, l): the MO's and the DO's nonzero online scalars (streams
+    (layer, OP_ONLINE + op, 0 / 1)), one launch."""
+    rk, rl = sess.rng(layer, OP_ONLINE + op, 0), sess.rng(layer, OP_ONLINE + op, 1)
+    k, lj = _dev.empty_u64(m), _dev.empty_u64(m)
+    seed, sptr = rk.np_args()
+    rk.reserve(m)
+    rl.reserve(m)
+    _lib.call("pb_prep_scalars", _dev.ptr(k), _dev.ptr(lj), m, seed, sptr, rk.stream, rl.stream, sess.ring.ell,
+              _dev.stream())
+    return k, lj
 
 
 def online_shared_product(sess, layer: int, bank: MaskBank, u: torch.Tensor, v: torch.Tensor):  # Alg. 3 P_online
-    """(MO share, DO share) of u o v with u at the MO, v at the DO: no HE."""
+    """(MO share, DO share) of u o v with u at the MO, v at the DO: no HE.
+    The MO's chain (u~, then u o v~ + sum k_i l_j s_ij) runs on the calling
+    stream, the DO's (sum_j l_j v'_j, v~ = v - that, then u~ o (v - v~) +
+    sum k_i l_j D_ij) on an auxiliary stream; each waits only for the message
+    it receives.  The mask-weighted sums are folded into the FC GEMMs'
+    epilogues."""
     ring, opd, m = sess.ring, bank.opd, bank.m
     ell = ring.ell
     if tuple(u.shape) != opd.u_shape or tuple(v.shape) != opd.v_shape:
         raise ShapeError(f"bank expects u {opd.u_shape}, v {opd.v_shape}")
-    k = _scalars(sess, layer, opd.op, 0, m)   # MO
-    lj = _scalars(sess, layer, opd.op, 1, m)  # DO
-    u_t = _lincomb(torch.empty_like(u), u, k, None, bank.u, ell, True)   # MO -> DO: u~, k
-    sess.channel.send(MO, MSG_ONLINE_U, u_t, 8 * (u_t.numel() + m))
-    v_t = _lincomb(torch.empty_like(v), v, lj, None, bank.v, ell, True)  # DO -> MO: v~, l
-    sess.channel.send(DO, MSG_ONLINE_V, v_t, 8 * (v_t.numel() + m))
-    mo = opd.apply(u, v_t, ell)
-    mo = _lincomb(mo, mo, k, lj, bank.s, ell, False)
-    vmask = _lincomb(torch.empty_like(v), None, lj, None, bank.v, ell, False)  # DO: sum_j l_j v'_j (= v - v~)
-    do = opd.apply(u_t, vmask, ell)
-    do = _lincomb(do, do, k, lj, bank.d, ell, False)
+    k, lj = _scalars(sess, layer, opd.op, m)
+    main = torch.cuda.current_stream()
+    # every buffer is allocated on the calling stream before the fork (the aux
+    # stream waits for it; the join orders any reuse after the aux work)
+    vmask, v_t, u_t = torch.empty_like(v), torch.empty_like(v), torch.empty_like(u)
+    t_d, t_s = _dev.empty_u64(*opd.out_shape), _dev.empty_u64(*opd.out_shape)
+    with sess.aux() as aux:
+        def do_side():  # DO: sum_j l_j v'_j (= v - v~), then v~ = v - it; sum k_i l_j D_ij
+            _lincomb(vmask, None, lj, None, bank.v, ell, False)
+            _lib.call("pb_ring_binary", _lib.RING_SUB, _dev.ptr(v_t), _dev.ptr(v), _dev.ptr(vmask), v.numel(),
+                      v.numel(), ell, _dev.stream())
+            _lincomb(t_d, None, k, lj, bank.d, ell, False)
+            ev = torch.cuda.Event()
+            ev.record()
+            return ev
+        ev_vt = aux.run(do_side)
+        _lincomb(u_t, u, k, None, bank.u, ell, True)  # MO -> DO: u~, k
+        sess.channel.send(MO, MSG_ONLINE_U, u_t, 8 * (u_t.numel() + m))
+        sess.channel.send(DO, MSG_ONLINE_V, v_t, 8 * (v_t.numel() + m))  # DO -> MO: v~, l
+        _lincomb(t_s, None, k, lj, bank.s, ell, False)
+        ev_ut = torch.cuda.Event()
+        ev_ut.record(main)
+        main.wait_event(ev_vt)
+        mo = opd.apply(u, v_t, ell, c=t_s)  # MO: u o v~ + sum k_i l_j s_ij
+        aux.stream.wait_event(ev_ut)
+        do = aux.run(lambda: opd.apply(u_t, vmask, ell, c=t_d))  # DO: u~ o (v - v~) + sum k_i l_j D_ij
     bank.n_used += 1
     return mo, do
 
@@ -208,8 +240,10 @@ def _add(a, b, ell):
     return out
 
 
-def prep_linear_forward(sess, layer: int, banks, W: RingTensor, b: RingTensor, x_a: ShareTensor, x_b: ShareTensor):
-    """Alg. 4 forward: <Y>_0 = <W o X_1>_0 + W o X_0 + b,  <Y>_1 = <W o X_1>_1 (scale 2f)."""
+def prep_linear_forward(sess, layer: int, banks, W: RingTensor, b: RingTensor, x_a: ShareTensor, x_b: ShareTensor,
+                        mo_x_zero: bool = False):
+    """Alg. 4 forward: <Y>_0 = <W o X_1>_0 + W o X_0 + b,  <Y>_1 = <W o X_1>_1 (scale 2f).
+    ``mo_x_zero``: the MO's input share is zero (the first layer): no W o X_0."""
     x_mo, x_do = _split(x_a, x_b)
     ring = sess.ring
     opd = banks[FWD].opd
@@ -217,35 +251,54 @@ def prep_linear_forward(sess, layer: int, banks, W: RingTensor, b: RingTensor, x
     from .linear_protocols import _add_bcast
 
     inner = p0.shape[1] if opd.is_fc else p0.shape[2] * p0.shape[3]
-    y0 = _add_bcast(_add(p0, opd.apply(W.values, x_mo.value.values, ring.ell), ring.ell), b.values, inner, ring.ell)
+    if not mo_x_zero:
+        p0 = opd.apply(W.values, x_mo.value.values, ring.ell, c=p0)  # the add fused into the FC GEMM
+    y0 = _add_bcast(p0, b.values, inner, ring.ell)
     return (ShareTensor(MO, RingTensor(y0, 2 * ring.f, ring, _canonical=True)),
             ShareTensor(DO, RingTensor(p1, 2 * ring.f, ring, _canonical=True)))
 
 
-def prep_linear_backward_input(sess, layer: int, banks, W: RingTensor, gy_a: ShareTensor, gy_b: ShareTensor):
+def prep_linear_backward_input(sess, layer: int, banks, W: RingTensor, gy_a: ShareTensor, gy_b: ShareTensor,
+                               mo_gy_zero: bool = False):
     gy_mo, gy_do = _split(gy_a, gy_b)
     ring = sess.ring
     p0, p1 = online_shared_product(sess, layer, banks[BWDX], W.values, gy_do.value.values)
-    g0 = _add(p0, banks[BWDX].opd.apply(W.values, gy_mo.value.values, ring.ell), ring.ell)
+    g0 = p0 if mo_gy_zero else banks[BWDX].opd.apply(W.values, gy_mo.value.values, ring.ell, c=p0)
     return (ShareTensor(MO, RingTensor(g0, 2 * ring.f, ring, _canonical=True)),
             ShareTensor(DO, RingTensor(p1, 2 * ring.f, ring, _canonical=True)))
 
 
 def prep_grad_weight(sess, layer: int, banks, x_a: ShareTensor, x_b: ShareTensor, gy_a: ShareTensor,
-                     gy_b: ShareTensor, e: torch.Tensor | None = None) -> RingTensor:
-    """Alg. 4 weight gradient, revealed at the MO (scale 2f)."""
+                     gy_b: ShareTensor, e: torch.Tensor | None = None, mo_x_zero: bool = False,
+                     mo_gy_zero: bool = False) -> RingTensor:
+    """Alg. 4 weight gradient, revealed at the MO (scale 2f).  A cross term with
+    a zero MO share (``mo_gy_zero``: <gY>_0 (.) <X>_1 at the last layer,
+    ``mo_x_zero``: <X>_0 (.)rev <gY>_1 at the first) is zero and skipped, as is
+    the MO's local term then; the adds ride the FC GEMM epilogues."""
     x_mo, x_do = _split(x_a, x_b)
     gy_mo, gy_do = _split(gy_a, gy_b)
     ring = sess.ring
     ell = ring.ell
-    a0, a1 = online_shared_product(sess, layer, banks[GRADW], gy_mo.value.values, x_do.value.values)
-    c0, c1 = online_shared_product(sess, layer, banks[GRADWR], x_mo.value.values, gy_do.value.values)
     opd = banks[GRADW].opd
-    hat = _add(_add(a1, c1, ell), opd.apply(gy_do.value.values, x_do.value.values, ell), ell)  # DO
+    terms0, terms1 = [], []
+    if not mo_gy_zero:
+        a0, a1 = online_shared_product(sess, layer, banks[GRADW], gy_mo.value.values, x_do.value.values)
+        terms0.append(a0)
+        terms1.append(a1)
+    if not mo_x_zero:
+        c0, c1 = online_shared_product(sess, layer, banks[GRADWR], x_mo.value.values, gy_do.value.values)
+        terms0.append(c0)
+        terms1.append(c1)
+    acc1 = terms1[0] if len(terms1) == 1 else _add(*terms1, ell) if terms1 else None
+    hat = opd.apply(gy_do.value.values, x_do.value.values, ell, c=acc1)  # DO: + local term
     if e is not None:
         hat = _add(hat, e, ell)
     from .linear_protocols import MSG_GRADW
 
     sess.channel.send(DO, MSG_GRADW, hat, hat.numel() * 8)
-    out = _add(_add(_add(hat, a0, ell), c0, ell), opd.apply(gy_mo.value.values, x_mo.value.values, ell), ell)  # MO
+    out = hat
+    for t in terms0:  # MO: + its shares of the cross terms
+        out = _add(out, t, ell)
+    if not (mo_x_zero or mo_gy_zero):
+        out = opd.apply(gy_mo.value.values, x_mo.value.values, ell, c=out)  # + the MO's local term
     return RingTensor(out, 2 * ring.f, ring, _canonical=True)
