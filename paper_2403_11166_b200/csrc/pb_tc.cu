@@ -204,30 +204,132 @@ __global__ void __launch_bounds__(128, 1)
 
 // Balanced base-256 digit planes of one side, plane-major [8][rows][Kp]:
 // side 0 = the output-row operand (gemm_a), side 1 = the output-column one
-// (gemm_b); entries k >= kc (the chunk's tail up to Kp) are zero.  Four
-// consecutive contraction entries per thread: one 32-bit store per plane.
-__global__ void k_tc_digits(GemmMap d, int side, const uint64_t* __restrict__ src, int rows, int k0, int kc, int Kp,
-                            uint64_t mask, int8_t* __restrict__ out) {
-  const int q4 = Kp / 4;
-  const int64_t total = (int64_t)rows * q4;
-  const size_t plane = (size_t)rows * Kp;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int row = (int)(e / q4), kk = 4 * (int)(e - (int64_t)row * q4);
-    uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int k = kk + t;
-      uint64_t v = 0;
-      if (k < kc) v = (side == 0 ? gemm_a(d, src, row, k0 + k) : gemm_b(d, src, k0 + k, row)) & mask;
-      int8_t g[8];
-      digits8(v, g);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] |= (uint32_t)(uint8_t)g[i] << (8 * t);
+// (gemm_b); entries k >= kc (the chunk's tail up to Kp) are zero.
+// Digits: v = sum_i d_i 256^i with d_i in [-128, 127] is unique and equals
+// byte_i(v + C) - 128 for C = 0x80..80 (v < 2^59: no overflow), i.e. the int8
+// bytes of (v + C) ^ C -- two 64-bit ops per value.  A thread owns 16
+// consecutive contraction entries of one row (one 128-bit store per plane);
+// the conv gathers are specialised on the kernel size S and walk the
+// contraction index incrementally (no per-element divisions).
+template <int KIND, int S, int SIDE>
+struct Gather {
+  // per-thread state for row `row` starting at contraction index k
+  int b, c, i, j, y, x, o;
+  const uint64_t* base;
+  __device__ __forceinline__ void init(const GemmMap& d, const uint64_t* src, int row, int k) {
+    constexpr int SS = S * S;
+    base = src;
+    if (KIND == PB_CONV_FWD) {
+      if (SIDE == 0) { base = src + (size_t)row * (d.ci * SS) + k; return; }   // W[o][(c,i,j)]
+      const int hw = d.oh * d.ow;                                              // X im2col: row = (b,y,x)
+      b = row / hw; const int q = row - b * hw; y = q / d.ow; x = q - y * d.ow;
+      c = k / SS; const int r = k - c * SS; i = r / S; j = r - i * S;
+    } else if (KIND == PB_CONV_BWDX) {
+      if (SIDE == 0) { o = k / SS; const int r = k - o * SS; i = r / S; j = r - i * S; c = row; return; }
+      const int hw = d.H * d.W;                                                // dY dilated: row = (b,y,x) of dX
+      b = row / hw; const int q = row - b * hw; y = q / d.W; x = q - y * d.W;
+      o = k / SS; const int r = k - o * SS; i = r / S; j = r - i * S;
+    } else {  // GRADW, k = (b, y, x) of dY
+      const int hw = d.oh * d.ow;
+      b = k / hw; const int q = k - b * hw; y = q / d.ow; x = q - y * d.ow;
+      if (SIDE == 0) { o = row; return; }
+      c = row / SS; const int r = row - c * SS; i = r / S; j = r - i * S;     // row = (c,i,j)
     }
-    uint32_t* o = reinterpret_cast<uint32_t*>(out + (size_t)row * Kp + kk);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) o[i * (plane / 4)] = w[i];
   }
+  __device__ __forceinline__ uint64_t next(const GemmMap& d) {
+    constexpr int SS = S * S;
+    uint64_t v = 0;
+    if (KIND == PB_CONV_FWD) {
+      if (SIDE == 0) return __ldg(base++);
+      const int yy = y * d.st + i - d.p, xx = x * d.st + j - d.p;
+      if (yy >= 0 && yy < d.H && xx >= 0 && xx < d.W) v = __ldg(base + ((size_t)(b * d.ci + c) * d.H + yy) * d.W + xx);
+      if (++j == S) { j = 0; if (++i == S) { i = 0; ++c; } }
+    } else if (KIND == PB_CONV_BWDX) {
+      if (SIDE == 0) {
+        v = __ldg(base + (size_t)(o * d.ci + c) * SS + i * S + j);
+      } else {
+        const int u = y + d.p - i, w = x + d.p - j;
+        if (u >= 0 && w >= 0) {
+          const int yy = u / d.st, xx = w / d.st;
+          if (yy * d.st == u && xx * d.st == w && yy < d.oh && xx < d.ow)
+            v = __ldg(base + ((size_t)(b * d.co + o) * d.oh + yy) * d.ow + xx);
+        }
+      }
+      if (++j == S) { j = 0; if (++i == S) { i = 0; ++o; } }
+    } else {
+      if (SIDE == 0) {
+        v = __ldg(base + ((size_t)(b * d.co + o) * d.oh + y) * d.ow + x);
+      } else {
+        const int yy = y * d.st + i - d.p, xx = x * d.st + j - d.p;
+        if (yy >= 0 && yy < d.H && xx >= 0 && xx < d.W) v = __ldg(base + ((size_t)(b * d.ci + c) * d.H + yy) * d.W + xx);
+      }
+      if (++x == d.ow) { x = 0; if (++y == d.oh) { y = 0; ++b; } }
+    }
+    return v;
+  }
+};
+
+template <int KIND, int S, int SIDE>
+__global__ void __launch_bounds__(256) k_tc_digits(GemmMap d, const uint64_t* __restrict__ src, int rows, int k0,
+                                                   int kc, int Kp, uint64_t mask, int8_t* __restrict__ out) {
+  const int q16 = Kp / 16;
+  const int64_t total = (int64_t)rows * q16;
+  const size_t plane = (size_t)rows * Kp;
+  constexpr uint64_t C = 0x8080808080808080ull;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(e / q16), kk = 16 * (int)(e - (int64_t)row * q16);
+    uint64_t t[16];
+    const int nk = kc - kk < 16 ? (kc - kk > 0 ? kc - kk : 0) : 16;
+    if (KIND == 3) {  // matmul: strided or contiguous rows, no index arithmetic to save
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        t[u] = u < nk ? (SIDE == 0 ? gemm_a(d, src, row, k0 + kk + u) : gemm_b(d, src, k0 + kk + u, row)) : 0ull;
+    } else {
+      Gather<KIND, S, SIDE> g;
+      g.init(d, src, row, k0 + kk);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) t[u] = u < nk ? g.next(d) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) t[u] = ((t[u] & mask) + C) ^ C;  // the eight int8 digits, little-endian
+    uint4* o = reinterpret_cast<uint4*>(out + (size_t)row * Kp + kk);
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {  // plane p: byte p of each of the 16 values
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t h0 = (uint32_t)(t[4 * q] >> (p & 4 ? 32 : 0)), h1 = (uint32_t)(t[4 * q + 1] >> (p & 4 ? 32 : 0));
+        const uint32_t h2 = (uint32_t)(t[4 * q + 2] >> (p & 4 ? 32 : 0)), h3 = (uint32_t)(t[4 * q + 3] >> (p & 4 ? 32 : 0));
+        const uint32_t sel = (uint32_t)(p & 3);
+        const uint32_t lo = __byte_perm(h0, h1, sel | ((sel + 4) << 4));       // bytes p of v0, v1
+        const uint32_t hi = __byte_perm(h2, h3, sel | ((sel + 4) << 4));       // bytes p of v2, v3
+        w[q] = __byte_perm(lo, hi, 0x5410);
+      }
+      o[p * (plane / 16)] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+template <int SIDE>
+void launch_digits(const GemmMap& d, const uint64_t* src, int rows, int k0, int kc, int Kp, uint64_t mask, int8_t* out,
+                   cudaStream_t st) {
+  const int grid = pb_grid_1d((int64_t)rows * (Kp / 16), 256);
+#define PB_TCD(K, S) k_tc_digits<K, S, SIDE><<<grid, 256, 0, st>>>(d, src, rows, k0, kc, Kp, mask, out)
+#define PB_TCD_S(K)          \
+  switch (d.s) {             \
+    case 1: PB_TCD(K, 1); return; \
+    case 3: PB_TCD(K, 3); return; \
+    case 5: PB_TCD(K, 5); return; \
+    default: PB_TCD(3, 1); return; \
+  }
+  switch (d.kind) {  // the generic gathers (gemm_a / gemm_b) for matmuls and other kernel sizes
+    case PB_CONV_FWD: PB_TCD_S(PB_CONV_FWD);
+    case PB_CONV_BWDX: PB_TCD_S(PB_CONV_BWDX);
+    case PB_CONV_GRADW: PB_TCD_S(PB_CONV_GRADW);
+    default: PB_TCD(3, 1); return;
+  }
+#undef PB_TCD_S
+#undef PB_TCD
 }
 
 __global__ void k_tc_mask(uint64_t* v, int64_t n, uint64_t m) {
@@ -313,10 +415,13 @@ int pb_tc_ring_gemm(const GemmMap& d, const uint64_t* A, const uint64_t* Bm, int
     const int kc = (int)((K - k0) < Kc ? (K - k0) : Kc);
     const int kb = (kc + TC_BK - 1) / TC_BK;
     const int sp = (kb + kps - 1) / kps;
-    k_tc_digits<<<pb_grid_1d((int64_t)P * Kc / 4, 256), 256, 0, st>>>(d, p_side, p_side == 0 ? A : Bm, P, (int)k0, kc,
-                                                                       (int)Kc, mask, dp);
-    k_tc_digits<<<pb_grid_1d((int64_t)Q * Kc / 4, 256), 256, 0, st>>>(d, 1 - p_side, p_side == 0 ? Bm : A, Q, (int)k0,
-                                                                       kc, (int)Kc, mask, dq);
+    if (p_side == 0) {
+      launch_digits<0>(d, A, P, (int)k0, kc, (int)Kc, mask, dp, st);
+      launch_digits<1>(d, Bm, Q, (int)k0, kc, (int)Kc, mask, dq, st);
+    } else {
+      launch_digits<1>(d, Bm, P, (int)k0, kc, (int)Kc, mask, dp, st);
+      launch_digits<0>(d, A, Q, (int)k0, kc, (int)Kc, mask, dq, st);
+    }
     dim3 grid((unsigned)((P + TC_BM - 1) / TC_BM), (unsigned)((Q + TC_BN - 1) / TC_BN), (unsigned)sp);
     k_tc_ring_gemm<<<grid, 128, TC_SMEM, st>>>(tmP, tmQ, e, P, Q, kps, kb, mask, atomic, out);
   }
