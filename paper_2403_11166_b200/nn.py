@@ -727,7 +727,12 @@ class GraphStep:
         loss, _ = self._loss(labels)
         return loss
 
-    def step(self, seed: int, labels):
+    def step(self, seed: int, labels, next_batch: torch.Tensor | None = None):
+        """One private training step on the staged input; returns the DO's loss.
+        ``next_batch`` (pinned float64 host tensor): stage the NEXT step's input
+        right after this step's launches -- its H2D copy, encode and (with
+        prefetch_input) encryption then overlap this step's backward, the
+        pipelined form of ``load_batch`` for a training loop."""
         self.sess.reseed(seed, device_copy=not self.prologue)
         main = torch.cuda.current_stream()
         self._mark("start")
@@ -775,10 +780,13 @@ class GraphStep:
             self._mark("pre")
             self.g_bwd.replay()
             self._mark("bwd")
-        if self.prefetch and not self._loaded_last:  # resident input: encrypt it afresh for the next step
+        loaded_for_this = self._loaded_last
+        self._loaded_last = False
+        if next_batch is not None:
+            self.load_batch(next_batch)
+        elif self.prefetch and not loaded_for_this:  # resident input: encrypt it afresh for the next step
             self._copy_stream.wait_event(self._ev_fwd)
             self._schedule_encrypt()
-        self._loaded_last = False
         return loss
 
 

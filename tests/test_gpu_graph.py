@@ -213,3 +213,41 @@ def test_host_handoff_timeout_sets_skip():
               2_000_000_000, skip.data_ptr(), st)
     torch.cuda.synchronize()
     assert int(skip.item()) == 0 and torch.equal(dst.cpu(), src)
+
+
+def test_graph_step_pipelined_next_batch():
+    """step(..., next_batch=...) stages the next input during this step; the
+    trajectory equals loading each batch before its step (and the oracle)."""
+    import torch
+
+    from oracle import nn as ON
+    from oracle import ring as OR
+    from paper_2403_11166_b200 import bfv
+    from paper_2403_11166_b200 import nn as PN
+    from paper_2403_11166_b200.linear_protocols import Session
+    from paper_2403_11166_b200.params import BfvParams
+    from paper_2403_11166_b200.ring import RingParams, RingTensor, SeededRng, encode_fixed
+
+    ring, params = RingParams(), BfvParams()
+    kp = bfv.keygen(params, SeededRng(3, 0))
+    sizes, B = [784, 32, 10], 8
+    batches = [PN.synthetic_mnist(20 + i, B, ring) for i in range(4)]
+    pins = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x, _ in batches]
+    s1, s2 = Session(params, ring, kp, seed=1), Session(params, ring, kp, seed=1)
+    m1, m2 = PN.Model(sizes, ring, seed=4), PN.Model(sizes, ring, seed=4)
+    x0 = RingTensor(encode_fixed(batches[0][0], ring), 25, ring, _canonical=True)
+    r1 = PN.GraphStep(s1, m1, x0, prefetch_input=True)
+    r2 = PN.GraphStep(s2, m2, RingTensor(encode_fixed(batches[0][0], ring), 25, ring, _canonical=True),
+                      prefetch_input=True)
+    om = ON.Model(sizes, OR.RingParams(), seed=4)
+    r2.load_batch(pins[0])
+    for i in range(4):
+        r1.load_batch(pins[i])
+        l1 = r1.step(500 + i, batches[i][1])
+        l2 = r2.step(500 + i, batches[i][1], next_batch=pins[(i + 1) % 4])
+        xo, _ = ON.synthetic_mnist(20 + i, B, OR.RingParams())
+        l3, _, _ = ON.reference_train_step(om, xo, batches[i][1])
+        assert l1 == l2 == l3
+        for l in range(len(sizes) - 1):
+            assert np.array_equal(m1.W[l].numpy(), m2.W[l].numpy())
+            assert np.array_equal(m2.W[l].numpy(), om.W(l))
