@@ -153,10 +153,13 @@ int pb_encrypt_pk_noise(const pb_ctx* ctx, const uint32_t* pk, const uint64_t* v
                         const int8_t* u, const int8_t* e1, const int8_t* e2, uint32_t* ct,
                         void* stream);
 /* Symmetric-key encryption by the key owner: c1 = a (uniform, NTT domain),
- * c0 = NTT(e + Delta m) - a*s.  sk_ntt [L][N]. */
-int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint64_t* vals,
+ * c0 = NTT(e + Delta m) - a*s.  sk_ntt [L][N]; sk_shoup (nullable): its
+ * Shoup companions (pb_shoup_rows), which make a*s three multiplies. */
+int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint32_t* sk_shoup, const uint64_t* vals,
                   const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int64_t P,
                   uint64_t seed, const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct, void* stream);
+/* Shoup companions floor(x 2^32 / q_l) of n_rows NTT-domain rows (row r on limb r % L). */
+int pb_shoup_rows(const pb_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n_rows, void* stream);
 /* Caller-supplied a ([P][L][N], NTT domain, device order) and e (int8 [P][N]). */
 int pb_encrypt_sk_noise(const pb_ctx* ctx, const uint32_t* sk_ntt, const uint64_t* vals,
                         const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int64_t P,

@@ -60,7 +60,8 @@ SIGNATURES = {
     "pb_unpack": [P, P, P, I32, I32, I64, P, P],
     "pb_encrypt_pk": [P, P, P, P, P, I32, I64, U64, P, U64, P, P],
     "pb_encrypt_pk_noise": [P, P, P, P, P, I32, I64, P, P, P, P, P],
-    "pb_encrypt_sk": [P, P, P, P, P, I32, I64, U64, P, U64, P, P],
+    "pb_encrypt_sk": [P, P, P, P, P, P, I32, I64, U64, P, U64, P, P],
+    "pb_shoup_rows": [P, P, P, I64, P],
     "pb_encrypt_sk_zero": [P, P, I64, U64, P, U64, P, P, P],
     "pb_encrypt_sk_add": [P, P, P, P, I32, I64, P, P, P],
     "pb_encrypt_sk_noise": [P, P, P, P, P, I32, I64, P, P, P, P],

@@ -60,6 +60,13 @@ class KeyPair:
     sk_coeff: np.ndarray  # int64 [N] ternary (host copy for diagnostics)
     sk_ntt: torch.Tensor  # int32 [L, N]
     pk: torch.Tensor  # int32 [2, L, N]
+    sk_sh: torch.Tensor | None = None  # int32 [L, N]: Shoup companions of sk_ntt (symmetric encryption)
+
+    def __post_init__(self):
+        if self.sk_sh is None:
+            self.sk_sh = torch.empty_like(self.sk_ntt)
+            _lib.call("pb_shoup_rows", _ctx(self.params), _dev.ptr(self.sk_ntt), _dev.ptr(self.sk_sh),
+                      self.sk_ntt.shape[0], _dev.stream())
 
 
 def _ctx(params: BfvParams):
@@ -162,9 +169,11 @@ def encrypt(kp: KeyPair, m: torch.Tensor, rng=None, *, pack=None, mode: str = "p
     else:  # SPEC:139-147's encrypt(pk, m) has no rng: fresh OS entropy per call (randomized encryption)
         seed, sptr = int.from_bytes(os.urandom(8), "little"), None
         nonce = int.from_bytes(os.urandom(4), "little") if nonce is None else nonce
-    fn = "pb_encrypt_pk" if mode == "pk" else "pb_encrypt_sk"
-    key = _dev.ptr(kp.pk) if mode == "pk" else _dev.ptr(kp.sk_ntt)
-    _lib.call(fn, h, key, _dev.ptr(m), pp, ps, Z, P, seed, sptr, nonce, _dev.ptr(ct), st)
+    if mode == "pk":
+        _lib.call("pb_encrypt_pk", h, _dev.ptr(kp.pk), _dev.ptr(m), pp, ps, Z, P, seed, sptr, nonce, _dev.ptr(ct), st)
+    else:
+        _lib.call("pb_encrypt_sk", h, _dev.ptr(kp.sk_ntt), _dev.ptr(kp.sk_sh), _dev.ptr(m), pp, ps, Z, P, seed, sptr,
+                  nonce, _dev.ptr(ct), st)
     return Ciphertext(ct, params)
 
 

@@ -247,8 +247,8 @@ __global__ void __launch_bounds__(256) k_enc_noise(int logN, int64_t nP, uint64_
 // CTA loops over R consecutive rows in polynomial-major order.
 template <int LOGN>
 __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
-    k_encrypt_sk(PbDev P, const uint32_t* sk, PbPack src, int64_t nP, const uint32_t* a_in, const int8_t* e,
-                 uint64_t seed_arg, const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct) {
+    k_encrypt_sk(PbDev P, const uint32_t* sk, const uint32_t* sk_sh, PbPack src, int64_t nP, const uint32_t* a_in,
+                 const int8_t* e, uint64_t seed_arg, const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct) {
   using Nt = pb::Ntt<LOGN>;
   const uint64_t seed = dev_key(seed_arg, seed_dev);
   constexpr int N = Nt::N;
@@ -275,15 +275,18 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
   const int8_t* ep = e + p * N;
   uint32_t b[32];
   load_source<Nt>(b, sm, src, p, tid, [&](uint64_t v) { return delta_m(P, l, v); });
+  // + e with |e| <= 20 as e + q: Delta m + e + q < 3q stays inside the NTT's lazy input range [0, 4q)
 #pragma unroll
-  for (int c = 0; c < 32; ++c) b[c] = addmod(lift_small(ep[Nt::j1(tid, c)], q), b[c], q);
+  for (int c = 0; c < 32; ++c) b[c] += (uint32_t)((int)q + ep[Nt::j1(tid, c)]);
   Nt::forward(b, sm, P.tw_fwd + (size_t)l * N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q);
   // c1 = a, c0 = NTT(e + Delta m) - a*s, one 128-bit device-order vector at a
   // time (keeps a and s out of the register file: 32 live residues, not 96)
   const uint4* s4 = reinterpret_cast<const uint4*>(sk + (size_t)l * N) + tid;
+  const uint4* h4 = sk_sh ? reinterpret_cast<const uint4*>(sk_sh + (size_t)l * N) + tid : nullptr;
   const uint4* a4 = a_in ? reinterpret_cast<const uint4*>(a_in + (p * L + l) * N) + tid : nullptr;
   uint4* c0 = reinterpret_cast<uint4*>(ct + ((p * 2 + 0) * L + l) * N) + tid;
   uint4* c1 = reinterpret_cast<uint4*>(ct + ((p * 2 + 1) * L + l) * N) + tid;
+  const uint32_t q2 = 2 * q;
 #pragma unroll
   for (int v = 0; v < 8; ++v) {
     uint32_t a[4];
@@ -296,8 +299,19 @@ __global__ void __launch_bounds__(1 << (LOGN - 5), NTT_MINB(LOGN))
     const uint4 sv = __ldg(s4 + v * Nt::T);
     const uint32_t sk_[4] = {sv.x, sv.y, sv.z, sv.w};
     uint32_t o[4];
+    if (h4) {  // Shoup with the key's companion row: c0 = b - a s over lazy ranges, one canonicalisation
+      const uint4 hv = __ldg(h4 + v * Nt::T);
+      const uint32_t sh_[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) o[k] = submod(pb::canon4(b[4 * v + k], q), mulmod_lt(a[k], sk_[k], q, mu), q);
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t bb = min(b[4 * v + k], b[4 * v + k] - q2);           // [0, 2q)
+        const uint32_t t = mul_shoup_lazy(a[k], sk_[k], sh_[k], q);          // [0, 2q)
+        o[k] = pb::canon4(bb - t + q2, q);                                    // (0, 4q) -> [0, q)
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k] = submod(pb::canon4(b[4 * v + k], q), mulmod_lt(a[k], sk_[k], q, mu), q);
+    }
     c0[v * Nt::T] = make_uint4(o[0], o[1], o[2], o[3]);
     c1[v * Nt::T] = make_uint4(a[0], a[1], a[2], a[3]);
   }
@@ -700,13 +714,14 @@ void launch_encrypt_pk(const PbDev& P, const uint32_t* pk, PbPack src, int64_t n
 }
 
 template <int LOGN>
-void launch_encrypt_sk(const PbDev& P, const uint32_t* sk, PbPack src, int64_t nP, const uint32_t* a_in, const int8_t* e,
-                       uint64_t seed, const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct, cudaStream_t st) {
+void launch_encrypt_sk(const PbDev& P, const uint32_t* sk, const uint32_t* sk_sh, PbPack src, int64_t nP,
+                       const uint32_t* a_in, const int8_t* e, uint64_t seed, const uint64_t* seed_dev, uint64_t nonce,
+                       uint32_t* ct, cudaStream_t st) {
   using Nt = pb::Ntt<LOGN>;
   const int64_t grid = pb_row_grid(nP * P.L);
   const size_t smem = Nt::SMEM_WORDS * 4;
   set_smem(k_encrypt_sk<LOGN>, smem);
-  k_encrypt_sk<LOGN><<<(unsigned)grid, Nt::T, smem, st>>>(P, sk, src, nP, a_in, e, seed, seed_dev, nonce, ct);
+  k_encrypt_sk<LOGN><<<(unsigned)grid, Nt::T, smem, st>>>(P, sk, sk_sh, src, nP, a_in, e, seed, seed_dev, nonce, ct);
 }
 
 template <int LOGN>
@@ -859,15 +874,15 @@ extern "C" int pb_encrypt_sk_noise(const pb_ctx* ctx, const uint32_t* sk, const 
   if (!sk || !e || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
   if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
   PB_PACK_OR_RETURN(src, vals, pack_pos, pack_src, Z);
-  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, src, nP, a, e, 0ull, (const uint64_t*)nullptr, 0ull, ct,
-                   pb_stream_of(stream));
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, (const uint32_t*)nullptr, src, nP, a, e, 0ull,
+                   (const uint64_t*)nullptr, 0ull, ct, pb_stream_of(stream));
   PB_CHECK_LAUNCH();
   return PB_OK;
 }
 
-extern "C" int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk, const uint64_t* vals, const int32_t* pack_pos,
-                             const int32_t* pack_src, int32_t Z, int64_t nP, uint64_t seed, const uint64_t* seed_dev,
-                             uint64_t nonce, uint32_t* ct, void* stream) {
+extern "C" int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk, const uint32_t* sk_shoup, const uint64_t* vals,
+                             const int32_t* pack_pos, const int32_t* pack_src, int32_t Z, int64_t nP, uint64_t seed,
+                             const uint64_t* seed_dev, uint64_t nonce, uint32_t* ct, void* stream) {
   if (int s = need_big_n(ctx)) return s;
   if (nP <= 0) return PB_OK;
   if (!sk || !ct) return pb_set_error(PB_ERR_ARG, "null argument");
@@ -880,7 +895,7 @@ extern "C" int pb_encrypt_sk(const pb_ctx* ctx, const uint32_t* sk, const uint64
     return pb_set_error(PB_ERR_CUDA, "encryption noise scratch allocation failed");
   const int64_t thr = (nP * 11) << (ctx->dev.logN - 5);
   k_enc_noise<<<pb_row_grid((thr + 255) / 256), 256, 0, st>>>(ctx->dev.logN, nP, seed, seed_dev, nonce, e);
-  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, src, nP, (const uint32_t*)nullptr,
+  PB_DISPATCH_LOGN(ctx->dev.logN, launch_encrypt_sk, ctx->dev, sk, sk_shoup, src, nP, (const uint32_t*)nullptr,
                    (const int8_t*)e, seed, seed_dev, nonce, ct, st);
   cudaFreeAsync(e, st);
   PB_CHECK_LAUNCH();
@@ -969,6 +984,26 @@ extern "C" int pb_ctpt_mac_mask(const pb_ctx* ctx, const uint32_t* ct_in, const 
   if (nP > max_grid_polys(ctx)) return pb_set_error(PB_ERR_SHAPE, "too many polynomials in one call");
   PB_DISPATCH_LOGN(ctx->dev.logN, launch_mac, ctx->dev, ct_in, pt, pt_shoup, terms, K, nP, out_pos, out_dst, U,
                    mask_vals, filler, filler_seed, seed_dev, ct_out, pb_stream_of(stream));
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+// Shoup companions of NTT-domain rows: out[r][j] = floor(in[r][j] 2^32 / q_l),
+// row r on limb r % L (the secret key's companion row for pb_encrypt_sk).
+namespace {
+__global__ void k_shoup_rows(PbDev P, const uint32_t* in, uint32_t* out, int64_t n_rows) {
+  const int64_t total = n_rows * P.N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int l = (int)((e / P.N) % P.L);
+    out[e] = shoup_of(in[e], P.q[l], P.inv_q32[l]);
+  }
+}
+}  // namespace
+
+extern "C" int pb_shoup_rows(const pb_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n_rows, void* stream) {
+  if (!ctx || !in || !out) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (n_rows <= 0) return PB_OK;
+  k_shoup_rows<<<pb_grid_1d(n_rows * ctx->dev.N, 256), 256, 0, pb_stream_of(stream)>>>(ctx->dev, in, out, n_rows);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }

@@ -341,7 +341,7 @@ class Session:
         if is_ct:
             enc_rng = self.rng(layer, op, P_ENC) if rng is None else rng
             base = enc_rng.reserve((plan.n_in + plan.n_pt) * self.world)
-            _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(src), *_pk(pack), n,
+            _lib.call("pb_encrypt_sk", h, _dev.ptr(self.kp.sk_ntt), _dev.ptr(self.kp.sk_sh), _dev.ptr(src), *_pk(pack), n,
                       *enc_rng.dev_args(), base + off, _dev.ptr(buf), _dev.stream())
             self._count("pb_encrypt_sk", n * (2 * L * N * 4 + 8 * N), ntt_rows=n * L)
         else:

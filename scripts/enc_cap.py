@@ -26,7 +26,7 @@ def main():
 
             def f():
                 _lib.call("pb_set_launch_cap", cap)
-                _lib.call("pb_encrypt_sk", h, _dev.ptr(kp.sk_ntt), _dev.ptr(m), None, None, 0, nP, 1234, None, 7,
+                _lib.call("pb_encrypt_sk", h, _dev.ptr(kp.sk_ntt), _dev.ptr(kp.sk_sh), _dev.ptr(m), None, None, 0, nP, 1234, None, 7,
                           _dev.ptr(ct), _dev.stream())
                 _lib.call("pb_set_launch_cap", 0)
 

@@ -68,7 +68,7 @@ def main():
         scratch = _dev.empty_u32(sh.n_out, L, sh.U)
         mask = _dev.u64_to_device(np.zeros(g[1] * g[2], dtype=np.uint64))
         fns = {
-            "encrypt_sk": lambda: _lib.call("pb_encrypt_sk", h, _dev.ptr(kp.sk_ntt), _dev.ptr(vals), *_pk(sh.in_pack),
+            "encrypt_sk": lambda: _lib.call("pb_encrypt_sk", h, _dev.ptr(kp.sk_ntt), _dev.ptr(kp.sk_sh), _dev.ptr(vals), *_pk(sh.in_pack),
                                             sh.n_in, 5, None, 0, _dev.ptr(ct), _dev.stream()),
             "encrypt_add": lambda: _lib.call("pb_encrypt_sk_add", h, _dev.ptr(vals), *_pk(sh.in_pack), sh.n_in,
                                              _dev.ptr(ebuf), _dev.ptr(ct), _dev.stream()),

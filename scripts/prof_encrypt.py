@@ -21,7 +21,7 @@ sh = _Shard(plan, 0, 1)
 vals = _dev.u64_to_device(np.random.default_rng(0).integers(0, 1 << 59, size=784 * 64, dtype=np.uint64))
 ct = _dev.empty_u32(sh.n_in, 2, p.L, p.N)
 for i in range(2):
-    _lib.call("pb_encrypt_sk", h, _dev.ptr(kp.sk_ntt), _dev.ptr(vals), *_pk(sh.in_pack), sh.n_in, 5 + i, None, 0,
+    _lib.call("pb_encrypt_sk", h, _dev.ptr(kp.sk_ntt), _dev.ptr(kp.sk_sh), _dev.ptr(vals), *_pk(sh.in_pack), sh.n_in, 5 + i, None, 0,
               _dev.ptr(ct), _dev.stream())
 torch.cuda.synchronize()
 print("ok", sh.n_in)
