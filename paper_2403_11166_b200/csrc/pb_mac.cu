@@ -296,16 +296,18 @@ __global__ void __launch_bounds__(CT + 32, MINB)
     }
 #pragma unroll
     for (int c = 0; c < NS; ++c) bytes += on[c] ? (uint32_t)C::SLOT : 0u;
+    const uint32_t sm0 = smem_addr(pipe_sm), full0 = smem_addr(full), empty0 = smem_addr(empty);
     for (int k = 0; k < nI; ++k) {
       const int s = k % STAGES;
-      if (k >= STAGES) mbar_wait(&empty[s], (uint32_t)((k / STAGES - 1) & 1));
-      mbar_expect_tx(&full[s], bytes);
-      uint8_t* st = pipe_sm + (size_t)s * nslots * C::SLOT;
+      const uint32_t fb = full0 + 8u * s;
+      if (k >= STAGES) mbar_wait_a(empty0 + 8u * s, (uint32_t)((k / STAGES - 1) & 1));
+      mbar_expect_tx_a(fb, bytes);
+      const uint32_t st = sm0 + (uint32_t)(s * nslots * C::SLOT);
 #pragma unroll
       for (int c = 0; c < NS; ++c) {
         // slots [2TB ct | TO pt] of term A advance by ct_k / pt_k, term B [2TO ct | TB pt] likewise
         const size_t stride = (c < 2 * TB || (c >= C::SLOTS_A && c < C::SLOTS_A + 2 * TO)) ? ct_k : pt_k;
-        if (on[c]) bulk_g2s(st + dsto[c], base[c] + (size_t)k * stride, C::SLOT, &full[s]);
+        if (on[c]) bulk_g2s_a(st + dsto[c], base[c] + (size_t)k * stride, C::SLOT, fb);
       }
     }
     return;
@@ -331,9 +333,10 @@ __global__ void __launch_bounds__(CT + 32, MINB)
   const int chunk = (ctA && ctB) ? MAC_FOLD2 : MAC_FOLD1;  // k-steps between folds
   const uint32_t r32 = reduce64(1ull << 32, q, mu);            // 2^32 mod q
   int since = 0;
+  const uint32_t full0 = smem_addr(full), empty0 = smem_addr(empty);
   for (int k = 0; k < nI; ++k) {
     const int s = k % STAGES;
-    mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
+    mbar_wait_a(full0 + 8u * s, (uint32_t)((k / STAGES) & 1));
     const VT* st = reinterpret_cast<const VT*>(pipe_sm + (size_t)s * nslots * C::SLOT) + tid;
     if (ctA) {
       VT w[TO];
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(CT + 32, MINB)
       }
     }
     __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // this warp is done reading stage s
+    if ((tid & 31) == 0) mbar_arrive_a(empty0 + 8u * s);  // this warp is done reading stage s
     if (++since == chunk && k + 1 < nI) {
       since = 0;
 #pragma unroll

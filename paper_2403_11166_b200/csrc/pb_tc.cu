@@ -250,7 +250,7 @@ struct Gather {
       } else {
         const int u = y + d.p - i, w = x + d.p - j;
         if (u >= 0 && w >= 0) {
-          const int yy = u / d.st, xx = w / d.st;
+          const int yy = d.st == 1 ? u : u / d.st, xx = d.st == 1 ? w : w / d.st;  // stride 1: no division
           if (yy * d.st == u && xx * d.st == w && yy < d.oh && xx < d.ow)
             v = __ldg(base + ((size_t)(b * d.co + o) * d.oh + yy) * d.ow + xx);
         }
@@ -308,6 +308,177 @@ __global__ void __launch_bounds__(256) k_tc_digits(GemmMap d, const uint64_t* __
       o[p * (plane / 16)] = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
+}
+
+// ------------------------------------------------ fused implicit GEMM ---
+// The conv operators without digit planes in HBM: eight producer warps gather
+// each stage's u64 operand tiles straight from the activations / weights
+// (the conv pad / stride / dilation index walks of Gather), turn them into
+// balanced digits and store them, byte-transposed, into the SWIZZLE_64B
+// K-major layout the UMMA descriptors read (16-byte chunk c of row r at
+// r * 64 + ((c ^ ((r >> 1) & 3)) << 4) within each 512-byte atom); a
+// generic -> async proxy fence precedes each stage's mbarrier arrival.  The
+// MMA warp and the TMEM accumulators are the plane kernel's; eight of the
+// producer warps share the epilogue (warp w: TMEM lanes 32 (w % 4), columns
+// 32 (w / 4)).
+constexpr int TCF_PROD_WARPS = 8;
+constexpr int TCF_THREADS = (TCF_PROD_WARPS + 1) * 32;
+
+// 16 gathered u64 -> the 16-byte chunk of each of the 8 digit planes
+__device__ __forceinline__ void digit_chunk(uint64_t (&t)[16], uint4 (&o)[8]) {
+  constexpr uint64_t C = 0x8080808080808080ull;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) t[u] = (t[u] + C) ^ C;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int sh = p & 4 ? 32 : 0;
+      const uint32_t sel = (uint32_t)(p & 3);
+      const uint32_t lo = __byte_perm((uint32_t)(t[4 * q] >> sh), (uint32_t)(t[4 * q + 1] >> sh), sel | ((sel + 4) << 4));
+      const uint32_t hi =
+          __byte_perm((uint32_t)(t[4 * q + 2] >> sh), (uint32_t)(t[4 * q + 3] >> sh), sel | ((sel + 4) << 4));
+      w[q] = __byte_perm(lo, hi, 0x5410);
+    }
+    o[p] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// Fill `nrow_tile` rows x 64 contraction entries of one side's stage tile
+// (8 planes of nrow_tile x 64 bytes at `tile`), rows row0.. (< nrows valid),
+// contraction k0.. (< K valid); producer thread pt of TCF_PROD_WARPS * 32.
+template <int KIND, int S, int SIDE>
+__device__ __forceinline__ void fill_tile(uint8_t* tile, int nrow_tile, const GemmMap& d, const uint64_t* src,
+                                          int row0, int nrows, int64_t k0, int64_t K, uint64_t mask, int pt) {
+  constexpr int NT = TCF_PROD_WARPS * 32;
+  const int chunks = nrow_tile * 4;  // 16-value chunks per stage tile
+  for (int c = pt; c < chunks; c += NT) {
+    const int r = c % nrow_tile, c16 = c / nrow_tile;  // consecutive threads: consecutive rows (coalesced gathers)
+    const int row = row0 + r;
+    const int64_t k = k0 + 16 * c16;
+    uint64_t t[16];
+    const int nk = (row < nrows) ? (int)(K - k < 16 ? (K - k > 0 ? K - k : 0) : 16) : 0;
+    if (nk > 0) {
+      Gather<KIND, S, SIDE> g;
+      g.init(d, src, row, (int)k);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) t[u] = u < nk ? (g.next(d) & mask) : 0ull;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) t[u] = 0ull;
+    }
+    uint4 o[8];
+    digit_chunk(t, o);
+    const uint32_t off = (uint32_t)r * 64u + ((uint32_t)(c16 ^ ((r >> 1) & 3)) << 4);
+#pragma unroll
+    for (int p = 0; p < 8; ++p) *reinterpret_cast<uint4*>(tile + (size_t)p * nrow_tile * 64 + off) = o[p];
+  }
+}
+
+template <int KIND, int S, int PSIDE>
+__global__ void __launch_bounds__(TCF_THREADS, 1)
+    k_tc_conv_fused(GemmMap d, const uint64_t* __restrict__ srcP, const uint64_t* __restrict__ srcQ, TcEpi e, int P,
+                    int Q, int64_t K, int kb_per_split, int kb_total, uint64_t mask, int atomic,
+                    uint64_t* __restrict__ out) {
+  extern __shared__ uint8_t tc_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE);
+  uint64_t* empty = full + TC_STAGES;
+  uint64_t* done = empty + TC_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p0 = blockIdx.x * TC_BM, q0 = blockIdx.y * TC_BN;
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int nkb = min(kb_total, kb0 + kb_per_split) - kb0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&full[s], TCF_PROD_WARPS);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    mbar_init_fence();
+  }
+  if (warp == TCF_PROD_WARPS) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr int QSIDE = 1 - PSIDE;
+  if (warp < TCF_PROD_WARPS) {  // ---- producers
+    const int pt = threadIdx.x;
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % TC_STAGES;
+      const uint32_t ph = (uint32_t)(i / TC_STAGES) & 1u;
+      if (i >= TC_STAGES) mbar_wait(&empty[s], ph ^ 1u);
+      uint8_t* st = smem + s * TC_STAGE;
+      const int64_t k0 = (int64_t)(kb0 + i) * TC_BK;
+      fill_tile<KIND, S, PSIDE>(st, TC_BM, d, srcP, p0, P, k0, K, mask, pt);
+      fill_tile<KIND, S, QSIDE>(st + TC_A_STAGE, TC_BN, d, srcQ, q0, Q, k0, K, mask, pt);
+      fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core's async proxy
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+    }
+  } else if (lane == 0) {  // ---- MMA issuer
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % TC_STAGES;
+      const uint32_t ph = (uint32_t)(i / TC_STAGES) & 1u;
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      const uint32_t a0 = smem_addr(smem + s * TC_STAGE), b0 = a0 + TC_A_STAGE;
+#pragma unroll
+      for (int kk = 0; kk < TC_BK / 32; ++kk) {
+#pragma unroll
+        for (int dd = 0; dd < 8; ++dd) {
+          const uint64_t da = tc_desc(a0 + dd * TC_A_PLANE + kk * 32);
+#pragma unroll
+          for (int ee = 0; ee < 8 - dd; ++ee) {
+            const uint64_t db = tc_desc(b0 + ee * TC_B_PLANE + kk * 32);
+            tc_mma(tmem + (dd + ee) * TC_BN, da, db, (i > 0 || kk > 0 || dd > 0) ? 1u : 0u);
+          }
+        }
+      }
+      tc_commit(&empty[s]);
+    }
+    tc_commit(done);
+  }
+  __syncwarp();
+  // ---- epilogue: warps 0..7, TMEM lanes 32 (w % 4), column half w / 4
+  if (warp < 8) {
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int p = p0 + (warp & 3) * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      const int col = (warp >> 2) * 32 + c * 16;
+      uint32_t v[8][16];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) tmem_ld16(tl + s * TC_BN + col, v[s]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (p < P) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int q = q0 + col + j;
+          if (q >= Q) break;
+          uint64_t acc = 0;
+#pragma unroll
+          for (int s = 0; s < 8; ++s) acc += (uint64_t)(int64_t)(int32_t)v[s][j] << (8 * s);
+          const size_t o = e.swap ? gemm_out(e.d, q, p) : gemm_out(e.d, p, q);
+          if (atomic) atomicAdd(reinterpret_cast<unsigned long long*>(out + o), (unsigned long long)acc);
+          else out[o] = acc & mask;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == TCF_PROD_WARPS)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
 template <int SIDE>
@@ -369,6 +540,51 @@ bool plane_map(CUtensorMap* tm, const int8_t* base, int rows, int Kp, int box_ro
 // tensor cores.  Contractions are processed in chunks whose digit planes stay
 // under ~512 MB; within a chunk the K blocks split over gridDim.z so that the
 // grid covers the GPU, partial sums meeting in u64 atomics.
+template <int KIND, int S, int PSIDE>
+int launch_conv_fused(const GemmMap& d, const uint64_t* A, const uint64_t* Bm, int n, int64_t K, int m, uint64_t mask,
+                      uint64_t* out, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_tc_conv_fused<KIND, S, PSIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) !=
+        cudaSuccess)
+      return pb_set_error(PB_ERR_CUDA, "fused tcgen05 conv: shared-memory opt-in failed");
+    attr = true;
+  }
+  const int swap = PSIDE;  // P = the output-column operand exactly when the sides are swapped
+  const int P = swap ? m : n, Q = swap ? n : m;
+  const int tiles = ((P + TC_BM - 1) / TC_BM) * ((Q + TC_BN - 1) / TC_BN);
+  const int kb = (int)((K + TC_BK - 1) / TC_BK);
+  int kps = kb;
+  while (kps > 1 && (kps * TC_BK > TC_KMAX || (int64_t)tiles * ((kb + kps - 1) / kps) < 148)) kps = (kps + 1) / 2;
+  while (kps * TC_BK > TC_KMAX) kps = (kps + 1) / 2;
+  const int splits = (kb + kps - 1) / kps;
+  const int atomic = splits > 1;
+  const TcEpi e{d, swap};
+  if (atomic) cudaMemsetAsync(out, 0, (size_t)n * m * sizeof(uint64_t), st);
+  dim3 grid((unsigned)((P + TC_BM - 1) / TC_BM), (unsigned)((Q + TC_BN - 1) / TC_BN), (unsigned)splits);
+  k_tc_conv_fused<KIND, S, PSIDE><<<grid, TCF_THREADS, TC_SMEM, st>>>(d, PSIDE ? Bm : A, PSIDE ? A : Bm, e, P, Q, K,
+                                                                      kps, kb, mask, atomic, out);
+  if (atomic) {
+    const int64_t no = (int64_t)n * m;
+    k_tc_mask<<<pb_grid_1d(no, 256), 256, 0, st>>>(out, no, mask);
+  }
+  return cudaPeekAtLastError() == cudaSuccess ? PB_OK : pb_set_error(PB_ERR_CUDA, "fused tcgen05 conv launch failed");
+}
+
+template <int KIND>
+int conv_fused(const GemmMap& d, const uint64_t* A, const uint64_t* Bm, int n, int64_t K, int m, uint64_t mask,
+               uint64_t* out, cudaStream_t st) {
+  const bool swap = n < m;
+#define PB_TCF(S) return swap ? launch_conv_fused<KIND, S, 1>(d, A, Bm, n, K, m, mask, out, st) \
+                              : launch_conv_fused<KIND, S, 0>(d, A, Bm, n, K, m, mask, out, st)
+  switch (d.s) {
+    case 1: PB_TCF(1);
+    case 3: PB_TCF(3);
+    default: PB_TCF(5);
+  }
+#undef PB_TCF
+}
+
 int pb_tc_ring_gemm(const GemmMap& d, const uint64_t* A, const uint64_t* Bm, int n, int64_t K, int m, int ell,
                     uint64_t* out, cudaStream_t st) {
   static bool attr = false;
@@ -380,8 +596,20 @@ int pb_tc_ring_gemm(const GemmMap& d, const uint64_t* A, const uint64_t* Bm, int
     pb_keep_pool();
     attr = true;
   }
-  if (!encode_fn()) return pb_set_error(PB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const uint64_t mask = ell >= 64 ? ~0ull : ((1ull << ell) - 1);
+  // conv operators with the kernel sizes the models use, up to 2^29 MACs: the
+  // fused implicit GEMM (digits built in shared memory by the producer warps,
+  // no planes in HBM); above, the gathers of eight producer warps cannot keep
+  // the tensor core fed and the plane kernels win (CIFAR conv2 0.18 vs 0.19 ms,
+  // conv1 0.10 vs 0.08 ms; profiles/r02_ring_gemm_backends*.jsonl)
+  if (d.kind <= PB_CONV_GRADW && (d.s == 1 || d.s == 3 || d.s == 5) && (double)n * m * (double)K < 536870912.0) {
+    switch (d.kind) {
+      case PB_CONV_FWD: return conv_fused<PB_CONV_FWD>(d, A, Bm, n, K, m, mask, out, st);
+      case PB_CONV_BWDX: return conv_fused<PB_CONV_BWDX>(d, A, Bm, n, K, m, mask, out, st);
+      default: return conv_fused<PB_CONV_GRADW>(d, A, Bm, n, K, m, mask, out, st);
+    }
+  }
+  if (!encode_fn()) return pb_set_error(PB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const int swap = n < m;  // the longer output side takes the 128-row UMMA M dimension
   const int P = swap ? m : n, Q = swap ? n : m;
   const int p_side = swap ? 1 : 0;
