@@ -64,7 +64,8 @@ LAN_BPS = 384e6  # PAPER:777 LAN, for the census' wire-time estimate
 
 # CUPTI kernel name -> the C-ABI entry point that launches it
 KERNEL_ENTRY = {
-    "k_enc_noise": "pb_encrypt_sk", "k_encrypt_sk": "pb_encrypt_sk", "k_encode_plain_mont": "pb_encode_plain_mont",
+    "k_enc_noise": "pb_encrypt_sk", "k_encrypt_sk": "pb_encrypt_sk", "k_encrypt_pre": "pb_encrypt_sk",
+    "k_encrypt_add": "pb_encrypt_sk", "k_encode_plain_mont": "pb_encode_plain_mont",
     "k_mask_ntt": "pb_mask_ntt", "k_mac_ws": "pb_ctpt_mac_tiled", "k_mac_eager": "pb_ctpt_mac_tiled",
     "k_mask_mac": "pb_mask_mac", "k_nl": "pb_nl_op", "k_dealer": "pb_dealer_op_out",
     "k_decrypt_share_cluster": "pb_decrypt_to_share", "k_decrypt_inv": "pb_decrypt_to_share",

@@ -604,7 +604,12 @@ extern "C" int pb_ctpt_mac_tiled(const pb_ctx* ctx, const uint32_t* ctA, const u
     // (profiles/r01_mac_ws_sweep.txt).  The MLP's small two-term grad-W keeps
     // 2x2: 1x2 is 4% faster alone but its extra CTAs crowd the concurrent
     // input-gradient chain (step A/B).
-    if (ctA && ctB && (int64_t)nB * nO * nI >= 1024)
+    // One batch block (nB = 1): 1x1, no idle half tile (MLP fwd2 4.0 -> 3.2 us,
+    // grad-W2 5.4 -> 4.0 us).  The MLP step A/B (3 x 30 steps): +0.8 % with
+    // these two rules (the 512 threshold was 1024 in round 1).
+    if (nB == 1)
+      launch_ws<1, 1, 4, 4, 4>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
+    else if (ctA && ctB && (int64_t)nB * nO * nI >= 512)
       launch_ws<1, 2, 4, 4, 4>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
     else
       launch_ws<2, 2, 4, 4, 4>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);

@@ -56,6 +56,7 @@ _MASK_PREFETCH = True  # draw all MO masks of a phase up front on a fork
 _GRADW_FLIP = False    # Alg. 2 HE matmul transposed: measured 1.5 % slower
 _BG_CAP = 148          # CTA cap of background operand preparation (0: none)
 _FUSE_MIN_ROWS = 4 * 148  # output rows (ciphertexts x limbs) from which nI <= 2 evaluations fuse mask + MAC
+_PREDRAW = True        # inside a phase: the DO's message-independent encryption half at phase start
 
 
 def _stream_like(cur: torch.cuda.Stream) -> torch.cuda.Stream:
@@ -247,6 +248,11 @@ class Session:
         self._mask_streams = {}
         self._pending_join = []
         self._fork_pools = {}
+        # encryption pre-draw (begin_phase): the phase-start event, the stream the
+        # message-independent halves run on, and their persistent (ct, e) buffers
+        self._t0 = None
+        self._predraw_stream = None
+        self._predraw_bufs = {}
 
     def rng(self, layer: int, op: int, purpose: int) -> SeededRng:
         g = SeededRng(self.seed, stream_id(layer, op, purpose))
@@ -439,11 +445,59 @@ class Session:
 
     def join_side(self):
         """Join the mask-prefetch forks into the current stream (a CUDA-graph
-        capture needs every fork joined before it ends)."""
+        capture needs every fork joined before it ends); ends the phase's
+        encryption pre-draw."""
         cur = torch.cuda.current_stream()
         for st in self._pending_join:
             cur.wait_stream(st)
         self._pending_join.clear()
+        self._t0 = None
+
+    def begin_phase(self):
+        """Mark the start of a forward / backward phase on the current stream.
+        Until join_side(), each DO encryption he_eval makes on its critical
+        path is split (bfv.encrypt_zero / encrypt_add, SPEC:139-147): the
+        message-independent half -- the uniform a, c1 = a, c0 = -a s and the
+        noise e -- runs on a pre-draw stream that only waits for this point,
+        and only c0 += NTT(e + Delta m) waits for the message.  The
+        ciphertext is a fresh encryption under the same key stream; the
+        protocol's outputs (decrypted shares) are unchanged."""
+        if not _PREDRAW or _SERIAL:
+            return
+        ev = torch.cuda.Event()
+        ev.record()
+        self._t0 = ev
+
+    def _encrypt_split(self, layer, op, plan, role, src, side):
+        """Enc(src) of one ct operand as a pre-drawn half (persistent buffers,
+        pre-draw stream, ordered after the phase start only) and the
+        message-dependent half on ``side``; returns the ciphertext buffer."""
+        pack, n, _, off = self._operand_layout(plan, role)
+        h, L, N = self.ctx.handle, self.p.L, self.p.N
+        key = (layer, op, role)
+        ent = self._predraw_bufs.get(key)
+        if ent is None or ent[0].shape[0] != n:
+            # persistent: written at the start of the NEXT phase too, so never
+            # handed back to the caching allocator
+            ent = self._predraw_bufs[key] = (_dev.empty_u32(n, 2, L, N),
+                                             torch.empty(n, N, dtype=torch.int8, device=_dev.device()))
+        ct, e = ent
+        enc_rng = self.rng(layer, op, P_ENC)
+        base = enc_rng.reserve((plan.n_in + plan.n_pt) * self.world)
+        if self._predraw_stream is None:
+            self._predraw_stream = torch.cuda.Stream()
+        ps = self._predraw_stream
+        ps.wait_event(self._t0)
+        with torch.cuda.stream(ps):
+            _lib.call("pb_encrypt_sk_zero", h, _dev.ptr(self.kp.sk_ntt), n, *enc_rng.dev_args(), base + off,
+                      _dev.ptr(ct), _dev.ptr(e), _dev.stream())
+            ev = torch.cuda.Event()
+            ev.record()
+        side.wait_event(ev)
+        with torch.cuda.stream(side):
+            _lib.call("pb_encrypt_sk_add", h, _dev.ptr(src), *_pk(pack), n, _dev.ptr(e), _dev.ptr(ct), _dev.stream())
+        self._count("pb_encrypt_sk", n * (2 * L * N * 4 + 8 * N), ntt_rows=n * L)
+        return ct
 
     def mask(self, layer: int, op: int, shape) -> torch.Tensor:
         """The MO's uniform mask of protocol (layer, op): prefetched or drawn now."""
@@ -517,6 +571,8 @@ class Session:
                     buf, ev = pre
                     if ev is not None:
                         side.wait_event(ev)
+                elif is_ct and self._t0 is not None:
+                    buf = self._encrypt_split(layer, op, plan, role, src, side)
                 else:
                     buf = _dev.empty_u32(n, 2, L, N) if is_ct else _dev.empty_u32(n, L, N)
                     with torch.cuda.stream(side):

@@ -264,6 +264,7 @@ def forward_phase(sess: Session, model: Model, x: RingTensor, prep=None):
     if prep is None:  # every layer's MO mask depends only on the seed: draw them all up front
         B = x.shape[1] if len(model.in_shape) == 1 else x.shape[0]
         sess.prefetch_masks(_mask_specs(model, B, (OP_FWD,)))
+        sess.begin_phase()
     _forward_layers(sess, model, prep, cur, acts, ds, ys, seg)
     sess.join_side()
     # the MO sends its share of the logits; the DO reconstructs them
@@ -315,6 +316,8 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
                 prepare_backward(sess, model, state, prep, layers=early_layers, clear=False)
             if pre_layers:
                 prepare_backward(sess, model, state, prep, layers=pre_layers, clear=False, background=True)
+    if prep is None:
+        sess.begin_phase()  # the encryption pre-draws run beside the host handoff
     if on_start is not None:
         on_start()
     gy_do = ShareTensor(DO, RingTensor(g_do, f, ring, _canonical=True))
