@@ -599,18 +599,17 @@ extern "C" int pb_ctpt_mac_tiled(const pb_ctx* ctx, const uint32_t* ctA, const u
     // Warp-specialised TMA-pipelined lazy MAC (B200, graph-timed): FC 784x128 fwd
     // 52.7 -> 39.3 us, its grad-W 51.1 -> 45.7 us, conv-like K=16 646 -> 587 us vs
     // a single-role pipelined kernel (round 1, removed).
-    // Tiles: 2x2, except large two-term evaluations (Alg. 2 cross terms, twice
-    // the staged operands per k-step): 1x2, CIFAR conv grad-W 1148 -> 1106 us
-    // (profiles/r01_mac_ws_sweep.txt).  The MLP's small two-term grad-W keeps
-    // 2x2: 1x2 is 4% faster alone but its extra CTAs crowd the concurrent
-    // input-gradient chain (step A/B).
-    // One batch block (nB = 1): 1x1, no idle half tile (MLP fwd2 4.0 -> 3.2 us,
-    // grad-W2 5.4 -> 4.0 us).  The MLP step A/B (3 x 30 steps): +0.8 % with
-    // these two rules (the 512 threshold was 1024 in round 1).
+    // Tiles 2x2 (single-role kernels and 1x2 / 2x4 / 4x4 / grouped tiles
+    // measured slower, profiles/r02_mac_tiles.jsonl); one batch block (nB = 1):
+    // 1x1, no idle half tile (MLP fwd2 4.0 -> 3.2 us, grad-W2 5.4 -> 4.0 us).
+    // Two cross terms (Alg. 2) stage twice the operands per k-step: a 2-deep
+    // ring (48 KB) keeps 4 CTAs per SM where 4 stages (96 KB) fit only 2 --
+    // conv-like K=16 two-term 1236 -> 802 us, MLP grad-W0 79 -> 63 us (round 1
+    // used 1x2 tiles at 4 stages for these).
     if (nB == 1)
       launch_ws<1, 1, 4, 4, 4>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
-    else if (ctA && ctB && (int64_t)nB * nO * nI >= 512)
-      launch_ws<1, 2, 4, 4, 4>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
+    else if (ctA && ctB)
+      launch_ws<2, 2, 4, 2, 4>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
     else
       launch_ws<2, 2, 4, 4, 4>(ctx->dev, ctA, ptA_mont, ctB, ptB_mont, nB, nO, nI, ct_out, st);
   }
