@@ -57,6 +57,8 @@ _GRADW_FLIP = False    # Alg. 2 HE matmul transposed: measured 1.5 % slower
 _BG_CAP = 148          # CTA cap of background operand preparation (0: none)
 _FUSE_MIN_ROWS = 4 * 148  # output rows (ciphertexts x limbs) from which nI <= 2 evaluations fuse mask + MAC
 _PREDRAW = True        # inside a phase: the DO's message-independent encryption half at phase start
+_PREDRAW_MAX_ROWS = 4 * 148  # ... for encryptions of at most one wave of rows (latency-bound; the CIFAR
+                             # CNN's large ones stay fused: its step measured 9.09 ms fused, 9.22 split)
 
 
 def _stream_like(cur: torch.cuda.Stream) -> torch.cuda.Stream:
@@ -571,7 +573,7 @@ class Session:
                     buf, ev = pre
                     if ev is not None:
                         side.wait_event(ev)
-                elif is_ct and self._t0 is not None:
+                elif is_ct and self._t0 is not None and n * L <= _PREDRAW_MAX_ROWS:
                     buf = self._encrypt_split(layer, op, plan, role, src, side)
                 else:
                     buf = _dev.empty_u32(n, 2, L, N) if is_ct else _dev.empty_u32(n, L, N)
