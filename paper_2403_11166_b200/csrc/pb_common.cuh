@@ -243,6 +243,21 @@ __device__ __forceinline__ u32x4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_
 // primes, < 1/2 for any q); a rejected word is redrawn as a 64-bit
 // multiply-high sample from its own domain-separated call (statistical
 // distance 2^-34).  Half the Philox work of one 64-bit draw per residue.
+// The rejected words' redraws (probability < 2^-8 per quad): out of line, so
+// the callers' unrolled loops carry one Philox body per draw, not five
+// (k_encrypt_sk: 5960 -> ~2400 SASS instructions, instruction-cache stalls).
+__device__ __noinline__ uint4 uniform_quad_redraw(uint64_t seed, uint64_t pp, uint32_t c0, uint32_t q,
+                                                  uint32_t domain, uint4 x) {
+  uint32_t v[4] = {x.x, x.y, x.z, x.w};
+  for (int i = 0; i < 4; ++i) {
+    if (v[i] < q) continue;
+    const u32x4 s = philox4x32_10(c0, (uint32_t)pp, (uint32_t)(pp >> 32), domain ^ (0x80000000u | (uint32_t)i),
+                                  (uint32_t)seed, (uint32_t)(seed >> 32));
+    v[i] = (uint32_t)__umul64hi(((uint64_t)s.v[1] << 32) | s.v[0], q);
+  }
+  return make_uint4(v[0], v[1], v[2], v[3]);
+}
+
 __device__ __forceinline__ void uniform_quad(uint64_t seed, uint64_t pp, int l, int jq, uint32_t q, uint32_t domain,
                                              uint32_t (&x)[4]) {
   const uint32_t c0 = (uint32_t)jq | ((uint32_t)l << 24);
@@ -255,12 +270,8 @@ __device__ __forceinline__ void uniform_quad(uint64_t seed, uint64_t pp, int l, 
     bad |= x[i] >= q;
   }
   if (bad) {
-    for (int i = 0; i < 4; ++i) {
-      if (x[i] < q) continue;
-      const u32x4 s = philox4x32_10(c0, (uint32_t)pp, (uint32_t)(pp >> 32), domain ^ (0x80000000u | (uint32_t)i),
-                                    (uint32_t)seed, (uint32_t)(seed >> 32));
-      x[i] = (uint32_t)__umul64hi(((uint64_t)s.v[1] << 32) | s.v[0], q);
-    }
+    const uint4 f = uniform_quad_redraw(seed, pp, c0, q, domain, make_uint4(x[0], x[1], x[2], x[3]));
+    x[0] = f.x; x[1] = f.y; x[2] = f.z; x[3] = f.w;
   }
 }
 

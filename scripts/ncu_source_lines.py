@@ -1,11 +1,12 @@
 """Per-CUDA-source-line executed warp instructions of one kernel in an ncu report
-(--page source, cuda,sass): python scripts/ncu_source_lines.py rep.ncu-rep <kernel regex> [top]."""
+(--page source, cuda,sass): python scripts/ncu_source_lines.py rep.ncu-rep <kernel regex> [top] [column],
+column e.g. "Warp Stall Sampling (All Samples)" instead of "Instructions Executed"."""
 import csv, collections, sys, subprocess
 rep, kern = sys.argv[1], sys.argv[2]
 out = subprocess.run(["ncu","-i",rep,"--page","source","--csv","--kernel-name","regex:"+kern,"--print-source","cuda,sass"],capture_output=True,text=True).stdout
 rows=list(csv.reader(out.splitlines()))
 hdr=[r for r in rows if r and r[0]=='Line No'][0]
-i_ex=hdr.index("Instructions Executed")
+i_ex=hdr.index(sys.argv[4] if len(sys.argv)>4 else "Instructions Executed")
 res=collections.Counter(); src={}
 f=None
 for r in rows:
