@@ -246,7 +246,7 @@ __device__ __forceinline__ u32x4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_
 // The rejected words' redraws (probability < 2^-8 per quad): out of line, so
 // the callers' unrolled loops carry one Philox body per draw, not five
 // (k_encrypt_sk: 5960 -> ~2400 SASS instructions, instruction-cache stalls).
-__device__ __noinline__ uint4 uniform_quad_redraw(uint64_t seed, uint64_t pp, uint32_t c0, uint32_t q,
+static __device__ __noinline__ uint4 uniform_quad_redraw(uint64_t seed, uint64_t pp, uint32_t c0, uint32_t q,
                                                   uint32_t domain, uint4 x) {
   uint32_t v[4] = {x.x, x.y, x.z, x.w};
   for (int i = 0; i < 4; ++i) {
