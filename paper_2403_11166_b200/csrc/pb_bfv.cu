@@ -441,9 +441,11 @@ __device__ __forceinline__ int inverse_for_slots(uint32_t (&a)[32], uint32_t* sm
 // --------------------------------------------------------------- decrypt ---
 // mode 0: write x = INTT(c0 + c1 s) for all coefficients to out32 [P][L][N].
 // mode 1: write only the useful slots out_pos[p][u] to out32 [P][L][U].
-template <int LOGN>
+// (MODE a template parameter: one inverse-NTT body per kernel in the
+// instruction stream, not both.)
+template <int LOGN, int MODE>
 __global__ void __launch_bounds__(1 << (LOGN - 5))
-    k_decrypt_inv(PbDev P, const uint32_t* sk, const uint32_t* ct, int64_t nP, int mode, const int32_t* out_pos,
+    k_decrypt_inv(PbDev P, const uint32_t* sk, const uint32_t* ct, int64_t nP, const int32_t* out_pos,
                   int U, uint32_t* out32) {
   using Nt = pb::Ntt<LOGN>;
   constexpr int N = Nt::N;
@@ -462,7 +464,7 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
   Nt::gld3(ct + ((p * 2 + 0) * L + l) * N, b, tid);
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = addmod(a[c], b[c], q);
-  if (mode == 0) {
+  if constexpr (MODE == 0) {
     const uint32_t ni = P.ninv[l], nis = P.ninv_sh[l];
     Nt::inverse_scaled(a, sm, P.tw_inv + (size_t)l * N, P.tw3_inv + (size_t)l * P.tw3_stride, tid, q, ni, nis,
                        P.w0n[l], P.w0n_sh[l]);
@@ -759,8 +761,13 @@ void launch_decrypt_inv(const PbDev& P, const uint32_t* sk, const uint32_t* ct, 
                         const int32_t* out_pos, int U, uint32_t* out32, cudaStream_t st) {
   using Nt = pb::Ntt<LOGN>;
   const size_t smem = Nt::SMEM_WORDS * 4;
-  set_smem(k_decrypt_inv<LOGN>, smem);
-  k_decrypt_inv<LOGN><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, sk, ct, nP, mode, out_pos, U, out32);
+  if (mode == 0) {
+    set_smem(k_decrypt_inv<LOGN, 0>, smem);
+    k_decrypt_inv<LOGN, 0><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, sk, ct, nP, out_pos, U, out32);
+  } else {
+    set_smem(k_decrypt_inv<LOGN, 1>, smem);
+    k_decrypt_inv<LOGN, 1><<<(unsigned)(nP * P.L), Nt::T, smem, st>>>(P, sk, ct, nP, out_pos, U, out32);
+  }
 }
 
 template <int LOGN>
