@@ -255,6 +255,7 @@ class Session:
         self._t0 = None
         self._predraw_stream = None
         self._predraw_bufs = {}
+        self._predraw_used = set()  # persistent pre-draw buffers claimed in the current phase
 
     def rng(self, layer: int, op: int, purpose: int) -> SeededRng:
         g = SeededRng(self.seed, stream_id(layer, op, purpose))
@@ -454,6 +455,7 @@ class Session:
             cur.wait_stream(st)
         self._pending_join.clear()
         self._t0 = None
+        self._predraw_used.clear()
 
     def begin_phase(self):
         """Mark the start of a forward / backward phase on the current stream.
@@ -469,6 +471,14 @@ class Session:
         ev = torch.cuda.Event()
         ev.record()
         self._t0 = ev
+        self._predraw_used.clear()
+
+    def _claim(self, key) -> bool:
+        """A persistent pre-draw buffer serves one protocol call per phase."""
+        if key in self._predraw_used:
+            return False
+        self._predraw_used.add(key)
+        return True
 
     def _encrypt_split(self, layer, op, plan, role, src, side):
         """Enc(src) of one ct operand as a pre-drawn half (persistent buffers,
@@ -573,7 +583,7 @@ class Session:
                     buf, ev = pre
                     if ev is not None:
                         side.wait_event(ev)
-                elif is_ct and self._t0 is not None and n * L <= _PREDRAW_MAX_ROWS:
+                elif is_ct and self._t0 is not None and n * L <= _PREDRAW_MAX_ROWS and self._claim((layer, op, role)):
                     buf = self._encrypt_split(layer, op, plan, role, src, side)
                 else:
                     buf = _dev.empty_u32(n, 2, L, N) if is_ct else _dev.empty_u32(n, L, N)
