@@ -190,3 +190,58 @@ def test_mask_mac_fused_equals_two_step(nB, nO, nI, terms):
               mask.data_ptr(), 1, 99, None, one.data_ptr(), st)
     torch.cuda.synchronize()
     assert torch.equal(one, two)
+
+
+@pytest.mark.parametrize("nB,nO,nI,terms", [
+    (1, 3, 4, "A"), (1, 3, 4, "AB"),        # one batch block: 1x1 tiles
+    (3, 5, 13, "A"),                        # 2x2, 4-deep ring, a fold after 12 k-steps, ragged tile edges
+    (3, 5, 7, "AB"), (2, 2, 3, "AB"),       # two cross terms: 2x2, 2-deep ring, a fold after 6
+    (2, 3, 16, "B"),                        # the second term alone
+    (4, 2, 1, "A"), (3, 3, 2, "AB"),        # streaming shapes (eager kernel)
+])
+def test_ctpt_mac_tiled_vs_modular_sum(nB, nO, nI, terms):
+    """pb_ctpt_mac_tiled against the definition (K:89-95 pw_mul_acc over k):
+    c0 = c0_in + sum_k ct0 * pt * 2^-32, c1 = sum_k ct1 * pt * 2^-32 (pt in
+    Montgomery form), plus the second cross term, mod each q -- for every
+    tile / ring-depth / fold configuration the dispatcher picks."""
+    import torch
+
+    from paper_2403_11166_b200 import _lib
+    from paper_2403_11166_b200.params import BfvParams, context
+
+    p = BfvParams()
+    h = context(p).handle
+    L, N = p.L, p.N
+    rng = np.random.default_rng(nB * 1000 + nO * 100 + nI * 10 + len(terms))
+    qs = np.array(p.moduli, dtype=np.uint64)
+
+    def rnd(*lead):  # residues < q_l along the limb axis (second to last)
+        a = rng.integers(0, 1 << 62, size=(*lead, L, N), dtype=np.uint64)
+        return a % qs[:, None]
+
+    ctA = rnd(nB * nI, 2) if "A" in terms else None
+    ptA = rnd(nO * nI) if "A" in terms else None
+    ctB = rnd(nO * nI, 2) if "B" in terms else None
+    ptB = rnd(nB * nI) if "B" in terms else None
+    out0 = rnd(nB * nO, 2)
+    rinv = np.array([pow(1 << 32, -1, int(q)) for q in p.moduli], dtype=np.uint64)[:, None]
+    want = np.zeros((nB * nO, 2, L, N), dtype=np.uint64)
+    for b in range(nB):
+        for o in range(nO):
+            acc = np.zeros((2, L, N), dtype=np.uint64)
+            for k in range(nI):
+                if ctA is not None:
+                    w = ptA[o * nI + k] * rinv % qs[:, None]
+                    acc = (acc + ctA[b * nI + k] * w % qs[:, None]) % qs[:, None]
+                if ctB is not None:
+                    w = ptB[b * nI + k] * rinv % qs[:, None]
+                    acc = (acc + ctB[o * nI + k] * w % qs[:, None]) % qs[:, None]
+            want[b * nO + o, 0] = (acc[0] + out0[b * nO + o, 0]) % qs[:, None]
+            want[b * nO + o, 1] = acc[1]
+    dev = lambda a: None if a is None else torch.from_numpy(a.astype(np.int32)).cuda()  # noqa: E731
+    tA, pA, tB, pB, out = dev(ctA), dev(ptA), dev(ctB), dev(ptB), dev(out0)
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    _lib.call("pb_ctpt_mac_tiled", h, ptr(tA), ptr(pA), ptr(tB), ptr(pB), nB, nO, nI, out.data_ptr(),
+              torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().astype(np.uint64), want)
