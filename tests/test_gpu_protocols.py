@@ -67,6 +67,35 @@ def test_linear_forward_shares_bit_exact(env, n_i, n_o, B, zero):
     assert np.array_equal(rec, (OK.matmul_wrap(W, x) + b[:, None]) & RING.mask)
 
 
+def test_linear_forward_with_encryption_predraw_bit_exact(env):
+    """Inside a phase (Session.begin_phase) the DO's encryption is split: the
+    message-independent half pre-drawn on its own stream, c0 += NTT(e + Delta
+    m) on the critical path.  The ciphertexts are fresh encryptions; the
+    decrypted shares stay bit-identical to the oracle's."""
+    import torch
+
+    from paper_2403_11166_b200 import linear_protocols as LP
+    from paper_2403_11166_b200.ring import RingTensor
+
+    pr, sess = env["pr"], env["sess"]
+    n_i, n_o, B = 128, 128, 64
+    W = OR.encode_fixed(np.random.default_rng(11).uniform(-0.1, 0.1, size=(n_o, n_i)), RING)
+    b = OR.encode_fixed(np.random.default_rng(12).uniform(-0.1, 0.1, size=n_o), RING, 50)
+    x, x_mo, x_do = _rand_shares(13, (n_i, B))
+    o_mo, o_do = OPR.linear_forward(env["octx"], 1, W, b, x_mo, x_do)
+    sess._predraw_bufs.clear()
+    sess.begin_phase()
+    try:
+        y_mo, y_do = LP.linear_forward(sess, 1, RingTensor(W, 25, pr), RingTensor(b, 50, pr),
+                                       *_shares(pr, x_mo, x_do, 25))
+    finally:
+        sess.join_side()
+    torch.cuda.synchronize()
+    assert (1, LP.OP_FWD, "A_ct") in sess._predraw_bufs  # the split path ran
+    assert np.array_equal(y_do.value.numpy(), o_do)
+    assert np.array_equal(y_mo.value.numpy(), o_mo)
+
+
 def test_backward_input_and_grad_weight_bit_exact(env):
     from paper_2403_11166_b200 import linear_protocols as LP
     from paper_2403_11166_b200.ring import RingTensor
