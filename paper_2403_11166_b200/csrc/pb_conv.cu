@@ -341,15 +341,16 @@ int pb_tc_matmul(const uint64_t* a, const uint64_t* b, int n, int k, int m, int 
                  cudaStream_t st);
 
 // Backend choice is a function of the shape alone (no environment switch, no
-// fallback): ring GEMMs of >= 2^26 u64 MACs run on the tcgen05 int8 tensor
-// cores (pb_tc.cu), conv weight gradients (skinny outputs, long K: the
-// CUDA-core tiles need split-K atomics) from 2^24; smaller ones on the u64
-// CUDA-core kernels, whose single launch beats the tensor path's digit-plane
-// passes there (profiles/r02_ring_gemm_backends.jsonl).  pb_ring_conv_ex /
-// pb_ring_matmul_ex take the backend explicitly (the parity tests run every
-// backend on every shape).
+// fallback): ring GEMMs of >= 2^26 u64 MACs and convolutions of >= 2^24
+// run on the tcgen05 int8 tensor cores (pb_tc.cu; the fused implicit-GEMM
+// conv has no plane pass, so it wins down to CIFAR conv4's 2^24: 27 vs
+// 29-33 us), conv weight gradients (skinny outputs, long K: the CUDA-core
+// tiles need split-K atomics) from 2^22 (conv5 32 vs 57 us); smaller ones on
+// the u64 CUDA-core kernels (profiles/r02_ring_gemm_backends.jsonl).
+// pb_ring_conv_ex / pb_ring_matmul_ex take the backend explicitly (the
+// parity tests run every backend on every shape).
 static int auto_backend(int kind, int64_t macs) {
-  const int64_t min_macs = kind == PB_CONV_GRADW ? (1ll << 24) : (1ll << 26);
+  const int64_t min_macs = kind == PB_CONV_GRADW ? (1ll << 22) : kind >= 0 ? (1ll << 24) : (1ll << 26);
   return macs >= min_macs ? PB_BACKEND_TENSOR : PB_BACKEND_CUDA_CORE;
 }
 
