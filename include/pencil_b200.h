@@ -407,6 +407,20 @@ int pb_set_launch_cap(int32_t max_ctas);
 /* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream). */
 int pb_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
 
+/* Step prologue for a replayed graph: *dev_word = *host_word (pinned host
+ * memory read by the kernel; host_word NULL: skipped) and a D2D copy of
+ * `bytes` (multiple of 16, 16-byte aligned) from src to dst, one launch. */
+int pb_step_prologue(const uint64_t* host_word, uint64_t* dev_word, const void* src, void* dst, int64_t bytes,
+                     void* stream);
+
+/* Device -> host publication at the end of a replayed graph: one CTA copies
+ * n u64 from src (device) into pinned host memory dst_host with system-scope
+ * stores, then increments *seq_dev and writes it to the pinned word
+ * flag_host (system-scope release).  The host polls flag_host instead of a
+ * D2H copy + event (the logits the DO's loss needs). */
+int pb_host_publish(const uint64_t* src, uint64_t* dst_host, int64_t n, uint32_t* seq_dev, uint32_t* flag_host,
+                    void* stream);
+
 /* Host -> device handoff inside a CUDA graph launched ahead of the host:
  * one CTA waits until the pinned host word flag_host[0] equals *seq_dev + 1
  * (system-scope acquire), stores that into *seq_dev, acks it into
@@ -420,11 +434,6 @@ int pb_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
  * they were, so an aborted step never applies a stale gradient.
  * Replaces the loss-gradient H2D copy + graph launch between the DO's host
  * loss and the backward pass. */
-/* Step prologue for a replayed graph: *dev_word = *host_word (pinned host
- * memory read by the kernel; host_word NULL: skipped) and a D2D copy of
- * `bytes` (multiple of 16, 16-byte aligned) from src to dst, one launch. */
-int pb_step_prologue(const uint64_t* host_word, uint64_t* dev_word, const void* src, void* dst, int64_t bytes,
-                     void* stream);
 int pb_host_handoff(uint32_t* flag_host, uint32_t* seq_dev, const uint64_t* src_host, uint64_t* dst,
                     int64_t n, int64_t timeout_ns, uint32_t* skip_dev, void* stream);
 

@@ -92,6 +92,7 @@ SIGNATURES = {
     "pb_set_launch_cap": [I32],
     "pb_copy_async": [P, P, I64, P],
     "pb_host_handoff": [P, P, P, P, I64, I64, P, P],
+    "pb_host_publish": [P, P, I64, P, P, P],
     "pb_step_prologue": [P, P, P, P, I64, P],
     "pb_wire_frame_bytes": [P, I32, P],
     "pb_mod_switch_drop": [P, P, P, I64, P, P, P],

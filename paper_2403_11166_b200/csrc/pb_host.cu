@@ -162,6 +162,29 @@ __global__ void __launch_bounds__(1024) k_host_handoff(uint32_t* flag, uint32_t*
 }
 }  // namespace
 
+namespace {
+__global__ void __launch_bounds__(1024) k_host_publish(const uint64_t* src, uint64_t* dst_host, int64_t n,
+                                                      uint32_t* seq, uint32_t* flag) {
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(dst_host + i), "l"(src[i]) : "memory");
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t s = *seq + 1;
+    *seq = s;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(s) : "memory");
+  }
+}
+}  // namespace
+
+extern "C" int pb_host_publish(const uint64_t* src, uint64_t* dst_host, int64_t n, uint32_t* seq_dev,
+                               uint32_t* flag_host, void* stream) {
+  if (!seq_dev || !flag_host || n < 0 || (n && (!src || !dst_host))) return PB_ERR_ARG;
+  const int threads = (int)(n >= 1024 ? 1024 : n <= 32 ? 32 : ((n + 31) / 32) * 32);
+  k_host_publish<<<1, threads, 0, (cudaStream_t)stream>>>(src, dst_host, n, seq_dev, flag_host);
+  return cudaPeekAtLastError() == cudaSuccess ? PB_OK : PB_ERR_CUDA;
+}
+
 extern "C" int pb_host_handoff(uint32_t* flag_host, uint32_t* seq_dev, const uint64_t* src_host, uint64_t* dst,
                                int64_t n, int64_t timeout_ns, uint32_t* skip_dev, void* stream) {
   if (!flag_host || !seq_dev || n < 0 || (n && (!src_host || !dst)) || timeout_ns < 0) return PB_ERR_ARG;

@@ -211,6 +211,11 @@ class SoftmaxCE:
     def __call__(self, labels, logits=None):
         """(loss, g) with g = encode_f((softmax - onehot) / D) mod 2^ell in self.g
         (D = denom: the global batch under data parallelism; else B)."""
+        self.grad(labels, logits)
+        return self.value(), self.g
+
+    def grad(self, labels, logits=None):
+        """The gradient half: g written into self.g (the backward can go)."""
         if logits is None:
             alog = self.alog
         else:
@@ -222,8 +227,12 @@ class SoftmaxCE:
         np.exp(self.z, out=self.z)
         _lib.check(self._post(self.az, self.C, self.B, self.alab, r.ell, r.f, self.denom, self.ap, self.ag),
                    "pb_host_softmax_post")
+        return self.g
+
+    def value(self):
+        """The loss of the last grad() call (mean -log p of the labelled class)."""
         np.log(self.p, out=self.p)
-        return -self._mean(self.ap, self.B), self.g
+        return -self._mean(self.ap, self.B)
 
 
 _SMCE = {}
@@ -502,7 +511,6 @@ def private_train_step(sess: Session, model: Model, x: RingTensor, labels, lr=1e
 # Step-scheduling constants (round-1 A/B measurements):
 _LATE_PREP = True    # prepare layer 0's backward operands inside the backward graph
 _PREFETCH_BG = True  # prefetched input encryption grid-capped (background)
-_SPIN_WAIT = True    # busy-poll the logits event instead of a blocking sync
 _BX_FIRST = True     # enqueue the input-gradient protocol before the grad-W chain
 _PROLOGUE = True     # step seed + prefetched input copied by one prologue kernel
 # The one run-time switch: PB_HANDOFF=0 replaces the device-side loss handoff
@@ -546,6 +554,12 @@ class GraphStep:
         dev = x.values.device
         self.g_do = torch.zeros(n_cls, B, dtype=torch.int64, device=dev)
         self.logits_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
+        # the forward graph publishes the logits into logits_host and then bumps
+        # this pinned word (pb_host_publish); the host polls it
+        self._pub_flag = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self._pub_np = self._pub_flag.numpy().view(np.uint32)
+        self._pub_seq = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._pub_count = 0
         self.g_host = torch.empty(n_cls, B, dtype=torch.int64).pin_memory()
         self._loss = SoftmaxCE(model.ring, n_cls, B, denom=model.grad_denom(B), logits=self.logits_host.numpy().view(np.uint64),
                                g_out=self.g_host.numpy().view(np.uint64))
@@ -592,6 +606,9 @@ class GraphStep:
                           self._x_next.data_ptr() if self.prefetch else None, x.values.data_ptr(), nbytes,
                           torch.cuda.current_stream().cuda_stream)
             self.state, self.logits = forward_phase(sess, model, x, prep)
+            _lib.call("pb_host_publish", self.logits.values.data_ptr(), self.logits_host.data_ptr(),
+                      self.logits_host.numel(), self._pub_seq.data_ptr(), self._pub_flag.data_ptr(),
+                      torch.cuda.current_stream().cuda_stream)
         # the operands the backward consumes first (layers >= 1) are prepared beside
         # the host's loss step; layer 0's (consumed last) inside the backward graph,
         # beside its latency-bound first layers, so it does not wait for them
@@ -629,7 +646,6 @@ class GraphStep:
         self._pre_stream = torch.cuda.Stream()
         self._ev_fwd = torch.cuda.Event()
         self._ev_ready = torch.cuda.Event()
-        self._ev_logits = torch.cuda.Event()
         self._ev_pre = torch.cuda.Event()
         self._loaded_last = False
         torch.cuda.synchronize()
@@ -713,13 +729,15 @@ class GraphStep:
             self.timing.append((label, ev))
 
     def _wait_logits(self):
-        if _SPIN_WAIT:  # busy-poll: a blocking sync can sleep past the copy's completion
-            while not self._ev_logits.query():
-                pass
-        else:
-            self._ev_logits.synchronize()
+        """Until the forward graph has published this step's logits (polling
+        the pinned sequence word: no D2H copy, event or API call between the
+        forward's last kernel and the DO's loss)."""
+        want = self._pub_count & 0xFFFFFFFF
+        while int(self._pub_np[0]) != want:
+            pass
 
-    def _host_loss(self, labels):
+    def _host_grad(self, labels):
+        """The DO's loss gradient into g_host (raises on an out-of-range batch)."""
         if self._flag_pending:
             self._flag_pending = False
             if int(self._flag_host[0]):
@@ -727,8 +745,11 @@ class GraphStep:
 
                 limit = float(1 << (self.model.ring.ell - 1)) / float(1 << self.model.ring.f)
                 raise EncodeRangeError(f"|x| must stay below {limit}")
-        loss, _ = self._loss(labels)
-        return loss
+        self._loss.grad(labels)
+
+    def _host_loss(self, labels):
+        self._host_grad(labels)
+        return self._loss.value()
 
     def step(self, seed: int, labels, next_batch: torch.Tensor | None = None):
         """One private training step on the staged input; returns the DO's loss.
@@ -753,8 +774,7 @@ class GraphStep:
             with torch.cuda.stream(self._pre_stream):  # backward operands, beside the host's loss
                 self.g_pre.replay()
                 self._ev_pre.record()
-        self.logits_host.copy_(self.logits.values, non_blocking=True)
-        self._ev_logits.record(main)
+        self._pub_count += 1  # this replay's publication
         if self.handoff:  # the backward goes now; its chain waits on the device for the release below
             self.g_bwd.replay()
             self._mark("bwd")
@@ -764,7 +784,7 @@ class GraphStep:
                 self._wait_logits()
                 if self._hseq > 1 and int(self._hflag_np[1]) != self._hseq - 1:
                     raise RuntimeError("backward graph: the previous step's loss handoff timed out")
-                loss = self._host_loss(labels)  # g written into g_host
+                self._host_grad(labels)  # g written into g_host
                 abort = 0
             finally:
                 # release the backward even on error, so the GPU never waits for the
@@ -774,6 +794,7 @@ class GraphStep:
                 self._hflag_np[0] = self._hseq & 0xFFFFFFFF
                 if abort:  # after the skipped SGDs: later (eager) updates apply again
                     self.model.skip.zero_()
+            loss = self._loss.value()  # the loss value after the release (off the GPU's path)
         else:
             self._wait_logits()
             loss = self._host_loss(labels)
