@@ -167,7 +167,8 @@ __global__ void __launch_bounds__(1024) k_host_publish(const uint64_t* src, uint
                                                       uint32_t* seq, uint32_t* flag) {
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
     asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(dst_host + i), "l"(src[i]) : "memory");
-  __threadfence_system();
+  // the CTA barrier orders every thread's stores before thread 0's release,
+  // which is cumulative: one system-scope fence instead of one per thread
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t s = *seq + 1;

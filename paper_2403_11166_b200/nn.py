@@ -317,18 +317,23 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
     L = model.n_layers
     seg = model.segments()
     acts, ds, ys = state
+    # the handoff (a one-CTA wait for the host's loss) is enqueued first so it
+    # holds an SM before the preparation work below fills them; that work and
+    # the encryption pre-draws fork from the point before it
+    if prep is None:
+        sess.begin_phase()  # the encryption pre-draws run beside the host handoff
+    ev0 = torch.cuda.Event()
+    ev0.record()
+    if on_start is not None:
+        on_start()
     if early_layers or pre_layers:
-        cur, side = torch.cuda.current_stream(), sess.prep_stream()
-        side.wait_stream(cur)
+        side = sess.prep_stream()
+        side.wait_event(ev0)
         with torch.cuda.stream(side):
             if early_layers:
                 prepare_backward(sess, model, state, prep, layers=early_layers, clear=False)
             if pre_layers:
                 prepare_backward(sess, model, state, prep, layers=pre_layers, clear=False, background=True)
-    if prep is None:
-        sess.begin_phase()  # the encryption pre-draws run beside the host handoff
-    if on_start is not None:
-        on_start()
     gy_do = ShareTensor(DO, RingTensor(g_do, f, ring, _canonical=True))
     gy_mo = ShareTensor(MO, RingTensor(torch.zeros_like(g_do), f, ring, _canonical=True))
     gws, gbs = [None] * L, [None] * L
