@@ -66,10 +66,66 @@ __device__ __forceinline__ uint32_t triple_bits(const uint64_t (&tw)[4], int t) 
   return (uint32_t)(v & 31u);
 }
 
+// The comparison tree for a compile-time leaf count: every node's shares in
+// its own registers, every triple's bit offset a constant (the runtime-q
+// version below spends most of its ALU work on variable shifts and loop
+// control; k_nl is ALU-bound).  Level CNT -> (CNT + 1) / 2, pairs (2i, 2i+1)
+// combined in place into node i with triples T + 2i, T + 2i + 1.
+template <int CNT, int T>
+struct CmpTree {
+  __device__ __forceinline__ static void run(uint32_t (&L0)[16], uint32_t (&L1)[16], uint32_t (&E0)[16],
+                                             uint32_t (&E1)[16], const uint64_t (&tw)[4]) {
+#pragma unroll
+    for (int i = 0; i < CNT / 2; ++i) {
+      uint32_t a0, a1, b0, b1;
+      and_gate(E0[2 * i + 1], E1[2 * i + 1], L0[2 * i], L1[2 * i], triple_bits(tw, T + 2 * i), a0, a1);
+      and_gate(E0[2 * i + 1], E1[2 * i + 1], E0[2 * i], E1[2 * i], triple_bits(tw, T + 2 * i + 1), b0, b1);
+      L0[i] = L0[2 * i + 1] ^ a0;
+      L1[i] = L1[2 * i + 1] ^ a1;
+      E0[i] = b0;
+      E1[i] = b1;
+    }
+    if constexpr (CNT & 1) {
+      L0[CNT / 2] = L0[CNT - 1];
+      L1[CNT / 2] = L1[CNT - 1];
+      E0[CNT / 2] = E0[CNT - 1];
+      E1[CNT / 2] = E1[CNT - 1];
+    }
+    CmpTree<(CNT + 1) / 2, T + 2 * (CNT / 2)>::run(L0, L1, E0, E1, tw);
+  }
+};
+template <int T>
+struct CmpTree<1, T> {
+  __device__ __forceinline__ static void run(uint32_t (&)[16], uint32_t (&)[16], uint32_t (&)[16], uint32_t (&)[16],
+                                             const uint64_t (&)[4]) {}
+};
+
+template <int Q>
+__device__ __forceinline__ void cmp_lt_q(uint64_t a, uint64_t b, uint32_t lt0m, uint32_t eq0m,
+                                         const uint64_t (&tw)[4], uint32_t& c0, uint32_t& c1) {
+  uint32_t L0[16], L1[16], E0[16], E1[16];
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {  // leaf OTs: P1 (choice b_j) learns P0's table entry
+    const uint32_t aj = (uint32_t)(a >> (4 * j)) & 15u, bj = (uint32_t)(b >> (4 * j)) & 15u;
+    L0[j] = (lt0m >> j) & 1u;
+    E0[j] = (eq0m >> j) & 1u;
+    L1[j] = L0[j] ^ (uint32_t)(aj < bj);
+    E1[j] = E0[j] ^ (uint32_t)(aj == bj);
+  }
+  CmpTree<Q, 0>::run(L0, L1, E0, E1, tw);
+  c0 = L0[0];
+  c1 = L1[0];
+}
+
 // XOR shares (c0 at P0, c1 at P1) of 1{a < b} over nbits <= 64 bits.
 // lt0 / eq0: P0's random leaf masks (bit j = block j); tw: triple words.
 __device__ __forceinline__ void cmp_lt(uint64_t a, uint64_t b, int nbits, uint32_t lt0m, uint32_t eq0m,
                                        const uint64_t (&tw)[4], uint32_t& c0, uint32_t& c1) {
+  switch ((nbits + 3) >> 2) {  // the ring's comparisons: 58 / 59 bits (DReLU, wrap) and f = 25 (low carry)
+    case 15: cmp_lt_q<15>(a, b, lt0m, eq0m, tw, c0, c1); return;
+    case 7: cmp_lt_q<7>(a, b, lt0m, eq0m, tw, c0, c1); return;
+    default: break;
+  }
   const int q = (nbits + 3) >> 2;
   uint32_t L0 = 0, L1 = 0, E0 = 0, E1 = 0;  // node j's shares at bit j
   for (int j = 0; j < q; ++j) {  // leaf OTs: P1 (choice b_j) learns P0's table entry
