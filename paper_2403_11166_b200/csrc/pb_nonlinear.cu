@@ -27,23 +27,34 @@
 
 namespace {
 
-// An element's random words, generated block-wise: raw draws base .. base+n-1
-// of the numpy Philox4x64 stream come from ceil-covering 4-word counter
-// blocks, each computed once (not once per word as philox_np_raw would).
-constexpr int W_MAX = 16;
+// An element's W random words: raw draws base .. base+W-1 of the numpy
+// Philox4x64 stream, from the 4-word counter blocks covering them (each
+// computed once, not once per word as philox_np_raw would), placed by the
+// element's phase base mod 4 with selects -- compile-time indices only, so
+// the words stay in registers.
+template <int W>
 struct Rng {
-  uint64_t v[W_MAX];
+  uint64_t v[W];
   __device__ __forceinline__ uint64_t w(int k) const { return v[k]; }
-  __device__ __forceinline__ void fill(uint64_t seed, uint64_t stream, uint64_t base, int n) {
-    const uint64_t b0 = base >> 2, b1 = (base + n - 1) >> 2;
-    for (uint64_t blk = b0; blk <= b1; ++blk) {
-      const u64x4 o = philox4x64_10(blk + 1, 0, 0, 0, seed, stream);  // numpy pre-increments the counter
+  __device__ __forceinline__ void fill(uint64_t seed, uint64_t stream, uint64_t base) {
+    constexpr int NB = (W + 3) / 4 + 1;
+    const uint64_t b0 = base >> 2;
+    const int ph = (int)(base & 3);
+    const int nb = (ph + W + 3) >> 2;  // blocks this element needs (NB - 1 or NB)
+    uint64_t t[4 * NB];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t k = (int64_t)(blk * 4 + j) - (int64_t)base;
-        if (k >= 0 && k < n) v[k] = o.v[j];
+    for (int b = 0; b < NB; ++b) {
+      if (b < nb) {
+        const u64x4 o = philox4x64_10(b0 + b + 1, 0, 0, 0, seed, stream);  // numpy pre-increments the counter
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t[4 * b + j] = o.v[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t[4 * b + j] = 0ull;
       }
     }
+#pragma unroll
+    for (int k = 0; k < W; ++k) v[k] = ph == 0 ? t[k] : ph == 1 ? t[k + 1] : ph == 2 ? t[k + 2] : t[k + 3];
   }
 };
 
@@ -119,58 +130,24 @@ __device__ __forceinline__ void cmp_lt_q(uint64_t a, uint64_t b, uint32_t lt0m, 
 
 // XOR shares (c0 at P0, c1 at P1) of 1{a < b} over nbits <= 64 bits.
 // lt0 / eq0: P0's random leaf masks (bit j = block j); tw: triple words.
+// Every leaf count is a compile-time instance (pb_nl_op: nbits <= 61).
 __device__ __forceinline__ void cmp_lt(uint64_t a, uint64_t b, int nbits, uint32_t lt0m, uint32_t eq0m,
                                        const uint64_t (&tw)[4], uint32_t& c0, uint32_t& c1) {
-  switch ((nbits + 3) >> 2) {  // the ring's comparisons: 58 / 59 bits (DReLU, wrap) and f = 25 (low carry)
-    case 15: cmp_lt_q<15>(a, b, lt0m, eq0m, tw, c0, c1); return;
-    case 7: cmp_lt_q<7>(a, b, lt0m, eq0m, tw, c0, c1); return;
-    default: break;
+#define PB_CMPQ(Q) \
+  case Q: cmp_lt_q<Q>(a, b, lt0m, eq0m, tw, c0, c1); return;
+  switch ((nbits + 3) >> 2) {
+    PB_CMPQ(1) PB_CMPQ(2) PB_CMPQ(3) PB_CMPQ(4) PB_CMPQ(5) PB_CMPQ(6) PB_CMPQ(7) PB_CMPQ(8)
+    PB_CMPQ(9) PB_CMPQ(10) PB_CMPQ(11) PB_CMPQ(12) PB_CMPQ(13) PB_CMPQ(14) PB_CMPQ(15) PB_CMPQ(16)
+    default: c0 = c1 = 0u; return;
   }
-  const int q = (nbits + 3) >> 2;
-  uint32_t L0 = 0, L1 = 0, E0 = 0, E1 = 0;  // node j's shares at bit j
-  for (int j = 0; j < q; ++j) {  // leaf OTs: P1 (choice b_j) learns P0's table entry
-    const uint32_t aj = (uint32_t)(a >> (4 * j)) & 15u, bj = (uint32_t)(b >> (4 * j)) & 15u;
-    const uint32_t l0 = (lt0m >> j) & 1u, e0 = (eq0m >> j) & 1u;
-    const uint32_t lt_table = (0xFFFEu << aj) & 0xFFFFu;  // bit k: 1{a_j < k}
-    const uint32_t eq_table = 1u << aj;                   // bit k: 1{a_j == k}
-    L0 |= l0 << j;
-    E0 |= e0 << j;
-    L1 |= (l0 ^ ((lt_table >> bj) & 1u)) << j;
-    E1 |= (e0 ^ ((eq_table >> bj) & 1u)) << j;
-  }
-  int cnt = q, t = 0;
-  while (cnt > 1) {  // combine (lo = 2i, hi = 2i + 1) pairs; an odd last node passes through
-    uint32_t nL0 = 0, nL1 = 0, nE0 = 0, nE1 = 0;
-    int nc = 0;
-    for (int i = 0; i + 1 < cnt; i += 2, ++nc) {
-      const uint32_t ll0 = (L0 >> i) & 1u, ll1 = (L1 >> i) & 1u, el0 = (E0 >> i) & 1u, el1 = (E1 >> i) & 1u;
-      const uint32_t lh0 = (L0 >> (i + 1)) & 1u, lh1 = (L1 >> (i + 1)) & 1u;
-      const uint32_t eh0 = (E0 >> (i + 1)) & 1u, eh1 = (E1 >> (i + 1)) & 1u;
-      uint32_t a0, a1, b0, b1;
-      and_gate(eh0, eh1, ll0, ll1, triple_bits(tw, t++), a0, a1);  // eq_hi & lt_lo
-      and_gate(eh0, eh1, el0, el1, triple_bits(tw, t++), b0, b1);  // eq_hi & eq_lo
-      nL0 |= (lh0 ^ a0) << nc;
-      nL1 |= (lh1 ^ a1) << nc;
-      nE0 |= b0 << nc;
-      nE1 |= b1 << nc;
-    }
-    if (cnt & 1) {
-      nL0 |= ((L0 >> (cnt - 1)) & 1u) << nc;
-      nL1 |= ((L1 >> (cnt - 1)) & 1u) << nc;
-      nE0 |= ((E0 >> (cnt - 1)) & 1u) << nc;
-      nE1 |= ((E1 >> (cnt - 1)) & 1u) << nc;
-      ++nc;
-    }
-    L0 = nL0, L1 = nL1, E0 = nE0, E1 = nE1, cnt = nc;
-  }
-  c0 = L0 & 1u;
-  c1 = L1 & 1u;
+#undef PB_CMPQ
 }
 
 __device__ __forceinline__ uint64_t lmask(int ell) { return ell >= 64 ? ~0ull : ((1ull << ell) - 1); }
 
 // DReLU (4 words: leaf masks, 3 triple words): XOR shares of 1{x >= 0}.
-__device__ __forceinline__ void drelu(uint64_t x0, uint64_t x1, int ell, const Rng& r, int off, uint32_t& d0,
+template <class R>
+__device__ __forceinline__ void drelu(uint64_t x0, uint64_t x1, int ell, const R& r, int off, uint32_t& d0,
                                       uint32_t& d1) {
   const int h = ell - 1;
   const uint64_t hm = (1ull << h) - 1;
@@ -183,18 +160,20 @@ __device__ __forceinline__ void drelu(uint64_t x0, uint64_t x1, int ell, const R
 }
 
 // MUX (2 words: r0, r1): arithmetic shares of d * x from XOR-shared d.
-__device__ __forceinline__ void mux(uint32_t d0, uint32_t d1, uint64_t x0, uint64_t x1, uint64_t m, const Rng& r,
+template <class R>
+__device__ __forceinline__ void mux(uint32_t d0, uint32_t d1, uint64_t x0, uint64_t x1, uint64_t m, const R& r,
                                     int off, uint64_t& z0, uint64_t& z1) {
   const uint64_t r0 = r.w(off) & m, r1 = r.w(off + 1) & m;
-  const uint64_t m0[2] = {(uint64_t)(0 - r0) + (d0 ? x0 : 0ull), (uint64_t)(0 - r0) + (d0 ? 0ull : x0)};  // P0 sends
-  const uint64_t m1[2] = {(uint64_t)(0 - r1) + (d1 ? x1 : 0ull), (uint64_t)(0 - r1) + (d1 ? 0ull : x1)};  // P1 sends
-  const uint64_t y1 = m0[d1], y0 = m1[d0];  // 1-of-2 OTs: P1 chooses with d1, P0 with d0
+  const uint64_t m00 = (uint64_t)(0 - r0) + (d0 ? x0 : 0ull), m01 = (uint64_t)(0 - r0) + (d0 ? 0ull : x0);  // P0 sends
+  const uint64_t m10 = (uint64_t)(0 - r1) + (d1 ? x1 : 0ull), m11 = (uint64_t)(0 - r1) + (d1 ? 0ull : x1);  // P1 sends
+  const uint64_t y1 = d1 ? m01 : m00, y0 = d0 ? m11 : m10;  // 1-of-2 OTs: P1 chooses with d1, P0 with d0
   z0 = (r0 + y0) & m;
   z1 = (r1 + y1) & m;
 }
 
 // Faithful arithmetic shift by k (9 words: leaves, 3 + 1 triple words, 2 x 2 MUX words).
-__device__ __forceinline__ void trunc(uint64_t x0, uint64_t x1, int ell, int k, const Rng& r, int off, uint64_t& y0,
+template <class R>
+__device__ __forceinline__ void trunc(uint64_t x0, uint64_t x1, int ell, int k, const R& r, int off, uint64_t& y0,
                                       uint64_t& y1) {
   const uint64_t m = lmask(ell), km = (1ull << k) - 1;
   const uint64_t xb = (x0 + (1ull << (ell - 1))) & m;  // P0's biased share: signed -> unsigned order
@@ -215,43 +194,51 @@ __device__ __forceinline__ void trunc(uint64_t x0, uint64_t x1, int ell, int k, 
 constexpr int W_DRELU = 4, W_MUX = 2, W_TRUNC = 9;
 
 // op: 0 DReLU (d out), 1 MUX (d in), 2 TRUNC, 3 RELU + TRUNC (d out), 4 TRUNC + MUX (d in)
-__global__ void __launch_bounds__(256) k_nl(int op, const uint64_t* __restrict__ x0, const uint64_t* __restrict__ x1,
+template <int OP>
+struct NlWords;
+template <> struct NlWords<0> { static constexpr int W = W_DRELU; };
+template <> struct NlWords<1> { static constexpr int W = W_MUX; };
+template <> struct NlWords<2> { static constexpr int W = W_TRUNC; };
+template <> struct NlWords<3> { static constexpr int W = W_DRELU + W_MUX + W_TRUNC; };
+template <> struct NlWords<4> { static constexpr int W = W_TRUNC + W_MUX; };
+
+template <int OP>
+__global__ void __launch_bounds__(256) k_nl(const uint64_t* __restrict__ x0, const uint64_t* __restrict__ x1,
                                             int64_t n, int ell, int k, const uint8_t* __restrict__ d_in,
                                             uint8_t* __restrict__ d_out, uint64_t seed_arg, const uint64_t* seed_dev,
-                                            uint64_t stream_id, uint64_t raw_offset, int words,
+                                            uint64_t stream_id, uint64_t raw_offset,
                                             uint64_t* __restrict__ y0, uint64_t* __restrict__ y1) {
+  constexpr int W = NlWords<OP>::W;
   const uint64_t seed = np_seed(seed_arg, seed_dev);
   const uint64_t m = lmask(ell);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    Rng r;
-    r.fill(seed, stream_id, raw_offset + (uint64_t)i * words, words);
+    Rng<W> r;
+    r.fill(seed, stream_id, raw_offset + (uint64_t)i * W);
     const uint64_t a = x0[i] & m, b = x1[i] & m;
     uint32_t d0 = 0, d1 = 0;
     uint64_t z0 = a, z1 = b;
-    if (op == 1 || op == 4) {
+    if constexpr (OP == 1 || OP == 4) {
       d0 = d_in[i] & 1u;
       d1 = (d_in[i] >> 1) & 1u;
     }
-    switch (op) {
-      case 0: drelu(a, b, ell, r, 0, d0, d1); break;
-      case 1: mux(d0, d1, a, b, m, r, 0, z0, z1); break;
-      case 2: trunc(a, b, ell, k, r, 0, z0, z1); break;
-      case 3: {
-        drelu(a, b, ell, r, 0, d0, d1);
-        uint64_t u0, u1;
-        mux(d0, d1, a, b, m, r, W_DRELU, u0, u1);
-        trunc(u0, u1, ell, k, r, W_DRELU + W_MUX, z0, z1);
-        break;
-      }
-      default: {
-        uint64_t u0, u1;
-        trunc(a, b, ell, k, r, 0, u0, u1);
-        mux(d0, d1, u0, u1, m, r, W_TRUNC, z0, z1);
-        break;
-      }
+    if constexpr (OP == 0) {
+      drelu(a, b, ell, r, 0, d0, d1);
+    } else if constexpr (OP == 1) {
+      mux(d0, d1, a, b, m, r, 0, z0, z1);
+    } else if constexpr (OP == 2) {
+      trunc(a, b, ell, k, r, 0, z0, z1);
+    } else if constexpr (OP == 3) {
+      drelu(a, b, ell, r, 0, d0, d1);
+      uint64_t u0, u1;
+      mux(d0, d1, a, b, m, r, W_DRELU, u0, u1);
+      trunc(u0, u1, ell, k, r, W_DRELU + W_MUX, z0, z1);
+    } else {
+      uint64_t u0, u1;
+      trunc(a, b, ell, k, r, 0, u0, u1);
+      mux(d0, d1, u0, u1, m, r, W_TRUNC, z0, z1);
     }
-    if (op == 0 || op == 3) d_out[i] = (uint8_t)(d0 | (d1 << 1));
-    if (op != 0) {
+    if constexpr (OP == 0 || OP == 3) d_out[i] = (uint8_t)(d0 | (d1 << 1));
+    if constexpr (OP != 0) {
       y0[i] = z0;
       y1[i] = z1;
     }
@@ -286,8 +273,17 @@ extern "C" int pb_nl_op(int op, const uint64_t* x0, const uint64_t* x1, int64_t 
   if ((op == PB_NL_MUX || op == PB_NL_TRUNC_MUX) && !d_in) return pb_set_error(PB_ERR_ARG, "MUX needs d shares");
   if ((op == PB_NL_DRELU || op == PB_NL_RELU_TRUNC) && !d_out) return pb_set_error(PB_ERR_ARG, "null d_out");
   if (op != PB_NL_DRELU && (!y0 || !y1)) return pb_set_error(PB_ERR_ARG, "null output");
-  k_nl<<<pb_grid_1d(n, 256), 256, 0, pb_stream_of(stream)>>>(op, x0, x1, n, ell, k, d_in, d_out, seed, seed_dev,
-                                                             stream_id, raw_offset, words, y0, y1);
+  cudaStream_t st = pb_stream_of(stream);
+#define PB_NL(OP) k_nl<OP><<<pb_grid_1d(n, 256), 256, 0, st>>>(x0, x1, n, ell, k, d_in, d_out, seed, seed_dev, \
+                                                              stream_id, raw_offset, y0, y1)
+  switch (op) {
+    case 0: PB_NL(0); break;
+    case 1: PB_NL(1); break;
+    case 2: PB_NL(2); break;
+    case 3: PB_NL(3); break;
+    default: PB_NL(4); break;
+  }
+#undef PB_NL
   PB_CHECK_LAUNCH();
   return PB_OK;
 }
