@@ -448,7 +448,9 @@ def run_ours(args, rank, world):
     del runner
     torch.cuda.empty_cache()
     if not args.no_configs:
-        line["configs"] = {"c4": bench_c4(args, rank, world), "c5": bench_c5(args),
+        line["configs"] = {"c1": bench_c1(args) if world == 1 else None,
+                           "c3": bench_c4(args, rank, world, "mnist_cnn2"),
+                           "c4": bench_c4(args, rank, world), "c5": bench_c5(args),
                            "c2_ot_nonlinear": bench_c4(args, rank, world, "mnist_mlp", "ot"),
                            "c4_ot_nonlinear": bench_c4(args, rank, world, "cifar_cnn", "ot"),
                            "c2_prep_online": bench_c4(args, rank, world, "mnist_mlp", prep_m=8),
@@ -467,6 +469,7 @@ def run_ours(args, rank, world):
                 "value": 4 / dt4, "unit": "samples/s", "cores": cores4, "kind": "port",
                 "sample": "1 oracle private CIFAR-CNN step at B=4 (bounded sample of configs[3]; B=64 takes minutes)"}
             line["configs"]["c5"]["cpu"] = cpu_c5()
+            line["configs"]["c1"]["cpu"] = cpu_c1()
     else:
         line["cpu_baseline"] = None
     print(json.dumps(line), flush=True)
@@ -525,11 +528,120 @@ def bench_c4(args, rank, world, name="cifar_cnn", nonlinear="dealer", prep_m=0):
     del runner
     torch.cuda.empty_cache()
     wl = {"cifar_cnn": "configs[3]: CIFAR-10 CNN (5 conv + FC, PAPER Fig. 7) private training step",
-          "mnist_mlp": "configs[1]: MNIST MLP 784-128-128-10 private training step"}[name]
+          "mnist_mlp": "configs[1]: MNIST MLP 784-128-128-10 private training step",
+          "mnist_cnn2": "configs[2]: MNIST CNN (2 x conv5x5 + FC) private training step",
+          "mnist_cnn": "configs[2] (PAPER Fig. 6 variant): MNIST CNN (conv5x5 + 2 FC) private training step"}[name]
     extra = {"mode": f"prep (Pencil+, m={prep_m})", "offline_bank_build_s": bank_s} if prep_m else {"mode": "fullhe"}
     return {"workload": wl, "nonlinear": nonlinear, **extra, "batch_per_gpu": BATCH, "value": world * BATCH / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
             "steps": steps, "kernels_ms_per_step": {k: round(v, 4) for k, v in
                                                     sorted(agg.items(), key=lambda kv: -kv[1])[:10]}}
+
+
+def _fc_round_parts(B):
+    """configs[0] operands: W (128x784), b, two-sided shares of x (784xB) and gy (128xB)."""
+    rng = np.random.default_rng(1)
+    W = rng.uniform(-0.03, 0.03, (128, 784))
+    b = rng.uniform(-0.03, 0.03, 128)
+    x = rng.uniform(-1, 1, (784, B))
+    gy = rng.normal(0, 0.01, (128, B))
+    return W, b, x, gy
+
+
+def bench_c1(args):
+    """configs[0]: one FC layer 784->128 private round -- linear_forward,
+    reveal_grad_bias, grad_weight (Alg. 2) and linear_backward_input on
+    two-sided shares, B=64 -- replayed from one CUDA graph, with the oracle's
+    same round on the host cores beside it."""
+    import torch
+
+    from paper_2403_11166_b200 import bfv
+    from paper_2403_11166_b200 import linear_protocols as LP
+    from paper_2403_11166_b200.linear_protocols import Session
+    from paper_2403_11166_b200.params import BfvParams
+    from paper_2403_11166_b200.ring import DO, MO, RingParams, RingTensor, SeededRng, ShareTensor, encode_fixed
+
+    ring, params = RingParams(), BfvParams()
+    sess = Session(params, ring, bfv.keygen(params, SeededRng(SEED, 0)), seed=SEED)
+    Wf, bf, xf, gf = _fc_round_parts(BATCH)
+
+    def enc(a, sc=25):
+        return RingTensor(encode_fixed(a, ring, sc), sc, ring, _canonical=True)
+
+    W, b = enc(Wf), enc(bf, 50)
+    x, gy = encode_fixed(xf, ring), encode_fixed(gf, ring)
+    xm = SeededRng(5, 1).uniform_ring(x.shape, ring)
+    gm = SeededRng(5, 2).uniform_ring(gy.shape, ring)
+    m = (1 << ring.ell) - 1
+    xs = (ShareTensor(MO, RingTensor(xm, 25, ring, _canonical=True)),
+          ShareTensor(DO, RingTensor((x - xm) & m, 25, ring, _canonical=True)))
+    gs = (ShareTensor(MO, RingTensor(gm, 25, ring, _canonical=True)),
+          ShareTensor(DO, RingTensor((gy - gm) & m, 25, ring, _canonical=True)))
+
+    def rnd(i):
+        sess.reseed(SEED + 50 + i)
+        LP.linear_forward(sess, 1, W, b, *xs)
+        LP.reveal_grad_bias(sess, 1, *gs)
+        LP.grad_weight(sess, 1, *xs, *gs)
+        LP.linear_backward_input(sess, 1, W, *gs)
+        sess.join_side()
+
+    sess.enable_graph_mode()
+    for i in range(3):
+        rnd(100 + i)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        rnd(200)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.int64, device="cuda")
+    for i in range(3):
+        g.replay()
+    steps = max(3, min(args.steps, 20))
+
+    def replay(i):
+        sess.reseed(SEED + 300 + i)
+        g.replay()
+
+    torch.cuda.synchronize()
+    ms = _time_steps(replay, steps, flush) / steps
+    del g, flush
+    torch.cuda.empty_cache()
+    return {"workload": "configs[0]: one FC layer 784->128 private round (forward, bias reveal, Alg. 2 weight "
+                        "gradient, input gradient) on two-sided shares, B=64", "batch": BATCH,
+            "value": BATCH / (ms / 1e3), "unit": "samples/s", "ms_per_round": ms, "steps": steps,
+            "timing": "one CUDA graph per round, L2 flushed between rounds"}
+
+
+def cpu_c1():
+    """The oracle's configs[0] round on the host cores (one round after one warm-up)."""
+    from oracle import bfv as OB
+    from oracle import kernels as OK
+    from oracle import protocols as OPR
+    from oracle import ring as OR
+    from oracle.params import make_params
+
+    OK.set_threads(os.cpu_count() or 1)
+    R = OR.RingParams()
+    p = make_params(8192, 7)
+    ar = OB.Arith(p)
+    ctx = OPR.Ctx(p, R, OB.keygen(p, OR.SeededRng(SEED, 0), ar), seed=SEED, ar=ar)
+    Wf, bf, xf, gf = _fc_round_parts(BATCH)
+    W, b = OR.encode_fixed(Wf, R), OR.encode_fixed(bf, R, 50)
+    x, gy = OR.encode_fixed(xf, R), OR.encode_fixed(gf, R)
+    xm, gm = OR.SeededRng(5, 1).uniform_ring(x.shape, R), OR.SeededRng(5, 2).uniform_ring(gy.shape, R)
+    xd, gd = (x - xm) & R.mask, (gy - gm) & R.mask
+
+    def rnd():
+        OPR.linear_forward(ctx, 1, W, b, xm, xd)
+        OPR.reveal_grad_bias(ctx, 1, gm, gd)
+        OPR.grad_weight(ctx, 1, xm, xd, gm, gd)
+        OPR.linear_backward_input(ctx, 1, W, gm, gd)
+
+    rnd()
+    t0 = time.perf_counter()
+    rnd()
+    dt = time.perf_counter() - t0
+    return {"value": BATCH / dt, "unit": "samples/s", "s_per_round": dt, "cores": OK.get_threads(), "kind": "port",
+            "sample": "1 oracle round of configs[0] after 1 warm-up round"}
 
 
 def bench_c5(args):
