@@ -349,7 +349,12 @@ int pb_tc_matmul(const uint64_t* a, const uint64_t* b, int n, int k, int m, int 
 // the u64 CUDA-core kernels (profiles/r02_ring_gemm_backends.jsonl).
 // pb_ring_conv_ex / pb_ring_matmul_ex take the backend explicitly (the
 // parity tests run every backend on every shape).
-static int auto_backend(int kind, int64_t macs) {
+// Skinny convolutions (an output side < 32: the MNIST CNNs' 1- and 5-channel
+// layers) go to the tensor cores at any size: the CUDA-core 64 x 64 tiles
+// leave 92 % of their rows idle there (mnist conv2 fwd / bwdx / grad-W 67 /
+// 74 / 71 us vs 38 / 46 / 41 us).
+static int auto_backend(int kind, int64_t macs, int64_t skinny_side = 1 << 30) {
+  if (kind >= 0 && skinny_side < 32) return PB_BACKEND_TENSOR;
   const int64_t min_macs = kind == PB_CONV_GRADW ? (1ll << 22) : kind >= 0 ? (1ll << 24) : (1ll << 26);
   return macs >= min_macs ? PB_BACKEND_TENSOR : PB_BACKEND_CUDA_CORE;
 }
@@ -376,7 +381,12 @@ extern "C" int pb_ring_conv_ex(int kind, const uint64_t* a, const uint64_t* b, i
   if (big >= (1ll << 31) || (int64_t)c_o * c_i * s * s >= (1ll << 31))
     return pb_set_error(PB_ERR_GEOMETRY, "conv tensor too large for 32-bit indexing");
   if (backend < PB_BACKEND_AUTO || backend > PB_BACKEND_TENSOR) return pb_set_error(PB_ERR_ARG, "bad backend");
-  if (backend == PB_BACKEND_AUTO) backend = auto_backend(kind, (int64_t)B * c_o * c_i * s * s * oh * ow);
+  if (backend == PB_BACKEND_AUTO) {
+    const int64_t side_m = kind == PB_CONV_BWDX ? c_i : c_o;
+    const int64_t side_n = kind == PB_CONV_FWD ? (int64_t)B * oh * ow
+                         : kind == PB_CONV_BWDX ? (int64_t)B * H * W : (int64_t)c_i * s * s;
+    backend = auto_backend(kind, (int64_t)B * c_o * c_i * s * s * oh * ow, side_m < side_n ? side_m : side_n);
+  }
   if (backend == PB_BACKEND_TENSOR) return pb_tc_conv(kind, a, b, B, c_i, c_o, H, W, s, pad, stride, oh, ow, ell, out, st);
   switch (s) {  // tiled implicit GEMM for the kernel sizes the models use
     case 1: conv_gemm_launch<1>(kind, d, a, b, m, out, st); PB_CHECK_LAUNCH(); return PB_OK;

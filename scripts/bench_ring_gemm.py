@@ -19,6 +19,8 @@ CONVS = {  # name: B, c_i, c_o, H, W, s, pad, stride (oracle/nn.py MODELS["cifar
     "cifar_conv1": (64, 3, 64, 32, 32, 5, 2, 1), "cifar_conv2": (64, 64, 64, 16, 16, 5, 2, 1),
     "cifar_conv3": (64, 64, 64, 8, 8, 3, 1, 1), "cifar_conv4": (64, 64, 64, 8, 8, 1, 0, 1),
     "cifar_conv5": (64, 64, 16, 8, 8, 1, 0, 1),
+    # MNIST CNNs (configs[2]): few channels -- skinny GEMMs
+    "mnist_conv1": (64, 1, 5, 28, 28, 5, 2, 2), "mnist_conv2": (64, 5, 5, 14, 14, 5, 2, 1),
 }
 MATMULS = {"mm_1024x1600x512": (1024, 1600, 512), "mm_4096x4096x4096": (4096, 4096, 4096),
            "mm_128x784x64": (128, 784, 64)}
@@ -41,7 +43,10 @@ def timeit(fn, reps=5):
 def main():
     rng = np.random.default_rng(0)
     st = D.stream()
+    only = sys.argv[1] if len(sys.argv) > 1 else ""
     for name, (B, ci, co, H, W, s, p, stv) in CONVS.items():
+        if only and not name.startswith(only):
+            continue
         oh = (H + 2 * p - s) // stv + 1
         x = D.u64_to_device(rng.integers(0, 1 << 59, size=(B, ci, H, W), dtype=np.uint64))
         w = D.u64_to_device(rng.integers(0, 1 << 59, size=(co, ci, s, s), dtype=np.uint64))
@@ -57,6 +62,8 @@ def main():
                                   "tensor"][be], "ms": ms, "u64_macs": macs, "macs_per_s": macs / ms * 1e3}),
                       flush=True)
     for name, (n, k, m) in MATMULS.items():
+        if only:
+            continue
         a = D.u64_to_device(rng.integers(0, 1 << 59, size=(n, k), dtype=np.uint64))
         b = D.u64_to_device(rng.integers(0, 1 << 59, size=(k, m), dtype=np.uint64))
         out = D.empty_u64(n, m)
