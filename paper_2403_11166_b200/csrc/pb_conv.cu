@@ -16,6 +16,7 @@
 // B*oh*ow terms per output: one CTA per (o, c) pair keeps the S*S
 // accumulators in registers and reduces them through shared memory.
 #include "pb_common.cuh"
+#include "pb_gemm_maps.cuh"
 
 #include <stdlib.h>
 
@@ -305,6 +306,71 @@ __global__ void __launch_bounds__(256) k_gemm(typename G::Dims d, const uint64_t
   }
 }
 
+// Skinny GEMMs (M <= 16 rows: the few-channel convolutions of the MNIST CNNs,
+// 1x1 convolutions into 16 channels): one thread per output column holding
+// all MM row accumulators, the A chunk (MM x 32, zero-padded rows) staged in
+// shared memory and broadcast, one B gather per (k, column) feeding MM MACs
+// -- instead of a 64 x 64 tile whose rows sit >= 75 % idle.  Split-K over
+// gridDim.z with u64 atomics as k_gemm.
+__global__ void k_mask_inplace(uint64_t* v, int64_t n, uint64_t m);
+constexpr int SK_T = 128, SK_KT = 32;
+template <int KIND, int S, int MM>
+__global__ void __launch_bounds__(SK_T) k_gemm_skinny(GemmMap gm, ConvDims d, const uint64_t* __restrict__ A,
+                                                      const uint64_t* __restrict__ Bm, int64_t k_per_split,
+                                                      uint64_t m, uint64_t* __restrict__ out) {
+  using G = ConvGemm<S, KIND>;
+  __shared__ uint64_t As[MM][SK_KT];
+  int M, N, K;
+  G::mnk(d, M, N, K);
+  const int n = blockIdx.x * SK_T + threadIdx.x;
+  const int kb = (int)(blockIdx.z * k_per_split), ke = min(K, kb + (int)k_per_split);
+  uint64_t acc[MM];
+#pragma unroll
+  for (int i = 0; i < MM; ++i) acc[i] = 0;
+  Gather<KIND, S, 1> g;  // this column's operand, walked along k without divisions
+  if (n < N) g.init(gm, Bm, n, kb);
+  for (int k0 = kb; k0 < ke; k0 += SK_KT) {
+    for (int e = threadIdx.x; e < MM * SK_KT; e += SK_T) {
+      const int i = e / SK_KT, kk = e - i * SK_KT;
+      As[i][kk] = (i < M && k0 + kk < ke) ? G::a_at(d, A, i, k0 + kk) : 0ull;
+    }
+    __syncthreads();
+    if (n < N) {
+      const int kc = min(SK_KT, ke - k0);
+#pragma unroll 4
+      for (int kk = 0; kk < kc; ++kk) {
+        const uint64_t b = g.next(gm);
+#pragma unroll
+        for (int i = 0; i < MM; ++i) acc[i] += As[i][kk] * b;
+      }
+    }
+    __syncthreads();
+  }
+  if (n >= N) return;
+#pragma unroll
+  for (int i = 0; i < MM; ++i) {
+    if (i >= M) break;
+    const size_t o = G::out_at(d, i, n);
+    if (gridDim.z == 1) out[o] = acc[i] & m;
+    else atomicAdd(reinterpret_cast<unsigned long long*>(out + o), (unsigned long long)acc[i]);
+  }
+}
+
+template <int KIND, int S>
+void launch_skinny(const ConvDims& d, const uint64_t* A, const uint64_t* Bm, int64_t M, int64_t N, int64_t K,
+                   uint64_t m, uint64_t* out, cudaStream_t st) {
+  const GemmMap gm{KIND, d.B, d.ci, d.co, d.H, d.W, S, d.p, d.st, d.oh, d.ow, 0, 0, 0, 0, 0};
+  const int64_t tiles = (N + SK_T - 1) / SK_T;
+  int splits = 1;
+  while (tiles * splits < 2 * 148 * 4 && K / (splits * 2) >= 16) splits *= 2;
+  const int64_t kps = ((K + splits - 1) / splits + SK_KT - 1) / SK_KT * SK_KT;
+  const dim3 grid((unsigned)tiles, 1, (unsigned)splits);
+  if (splits > 1) cudaMemsetAsync(out, 0, (size_t)(M * N) * sizeof(uint64_t), st);
+  if (M <= 8) k_gemm_skinny<KIND, S, 8><<<grid, SK_T, 0, st>>>(gm, d, A, Bm, kps, m, out);
+  else k_gemm_skinny<KIND, S, 16><<<grid, SK_T, 0, st>>>(gm, d, A, Bm, kps, m, out);
+  if (splits > 1) k_mask_inplace<<<pb_grid_1d(M * N, 256), 256, 0, st>>>(out, M * N, m);
+}
+
 __global__ void k_mask_inplace(uint64_t* v, int64_t n, uint64_t m) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     v[i] &= m;
@@ -317,6 +383,12 @@ int conv_gemm_launch(int kind, const ConvDims& d, const uint64_t* a, const uint6
   if (kind == PB_CONV_FWD) { M = d.co; N = (int64_t)d.B * d.oh * d.ow; K = (int64_t)d.ci * S * S; }
   else if (kind == PB_CONV_BWDX) { M = d.ci; N = (int64_t)d.B * d.H * d.W; K = (int64_t)d.co * S * S; }
   else { M = d.co; N = (int64_t)d.ci * S * S; K = (int64_t)d.B * d.oh * d.ow; }
+  if (M <= 16) {  // few output channels (or input channels for the input gradient)
+    if (kind == PB_CONV_FWD) launch_skinny<PB_CONV_FWD, S>(d, b, a, M, N, K, m, out, st);
+    else if (kind == PB_CONV_BWDX) launch_skinny<PB_CONV_BWDX, S>(d, b, a, M, N, K, m, out, st);
+    else launch_skinny<PB_CONV_GRADW, S>(d, b, a, M, N, K, m, out, st);
+    return 0;
+  }
   const int64_t tiles = ((M + 63) / 64) * ((N + 63) / 64);
   // split K until ~2 waves of 3 resident CTAs per SM are filled (GRADW has a tiny
   // M x N and K = B*oh*ow; the forward / input-gradient GEMMs of a 64-channel
@@ -349,12 +421,14 @@ int pb_tc_matmul(const uint64_t* a, const uint64_t* b, int n, int k, int m, int 
 // the u64 CUDA-core kernels (profiles/r02_ring_gemm_backends.jsonl).
 // pb_ring_conv_ex / pb_ring_matmul_ex take the backend explicitly (the
 // parity tests run every backend on every shape).
-// Skinny convolutions (an output side < 32: the MNIST CNNs' 1- and 5-channel
-// layers) go to the tensor cores at any size: the CUDA-core 64 x 64 tiles
-// leave 92 % of their rows idle there (mnist conv2 fwd / bwdx / grad-W 67 /
-// 74 / 71 us vs 38 / 46 / 41 us).
-static int auto_backend(int kind, int64_t macs, int64_t skinny_side = 1 << 30) {
-  if (kind >= 0 && skinny_side < 32) return PB_BACKEND_TENSOR;
+// Convolutions with <= 16 output rows (M: output channels, input channels for
+// the input gradient -- the MNIST CNNs' 1- and 5-channel layers, 1x1 convs
+// into 16 channels) run on the CUDA-core skinny kernel (k_gemm_skinny) at any
+// size; other skinny ones (an output side < 32) on the tensor cores, where
+// the 64 x 64 CUDA-core tiles would leave most rows idle.
+static int auto_backend(int kind, int64_t macs, int64_t side_m = 1 << 30, int64_t side_n = 1 << 30) {
+  if (kind >= 0 && side_m <= 16) return PB_BACKEND_CUDA_CORE;
+  if (kind >= 0 && (side_m < 32 || side_n < 32)) return PB_BACKEND_TENSOR;
   const int64_t min_macs = kind == PB_CONV_GRADW ? (1ll << 22) : kind >= 0 ? (1ll << 24) : (1ll << 26);
   return macs >= min_macs ? PB_BACKEND_TENSOR : PB_BACKEND_CUDA_CORE;
 }
@@ -385,7 +459,7 @@ extern "C" int pb_ring_conv_ex(int kind, const uint64_t* a, const uint64_t* b, i
     const int64_t side_m = kind == PB_CONV_BWDX ? c_i : c_o;
     const int64_t side_n = kind == PB_CONV_FWD ? (int64_t)B * oh * ow
                          : kind == PB_CONV_BWDX ? (int64_t)B * H * W : (int64_t)c_i * s * s;
-    backend = auto_backend(kind, (int64_t)B * c_o * c_i * s * s * oh * ow, side_m < side_n ? side_m : side_n);
+    backend = auto_backend(kind, (int64_t)B * c_o * c_i * s * s * oh * ow, side_m, side_n);
   }
   if (backend == PB_BACKEND_TENSOR) return pb_tc_conv(kind, a, b, B, c_i, c_o, H, W, s, pad, stride, oh, ow, ell, out, st);
   switch (s) {  // tiled implicit GEMM for the kernel sizes the models use

@@ -83,3 +83,66 @@ __device__ __forceinline__ void digits8(uint64_t v, int8_t (&d)[8]) {
     d[i] = (int8_t)(x - (carry << 8));
   }
 }
+
+// Incremental conv gathers of one GEMM operand row (pb_tc.cu digit planes and
+// fused producers, pb_conv.cu skinny kernel): side 0 = the output-row operand
+// (gemm_a), side 1 = the output-column one (gemm_b); specialised on the
+// kernel size S, the contraction index walked without per-element divisions.
+template <int KIND, int S, int SIDE>
+struct Gather {
+  // per-thread state for row `row` starting at contraction index k
+  int b, c, i, j, y, x, o;
+  const uint64_t* base;
+  __device__ __forceinline__ void init(const GemmMap& d, const uint64_t* src, int row, int k) {
+    constexpr int SS = S * S;
+    base = src;
+    if (KIND == PB_CONV_FWD) {
+      if (SIDE == 0) { base = src + (size_t)row * (d.ci * SS) + k; return; }   // W[o][(c,i,j)]
+      const int hw = d.oh * d.ow;                                              // X im2col: row = (b,y,x)
+      b = row / hw; const int q = row - b * hw; y = q / d.ow; x = q - y * d.ow;
+      c = k / SS; const int r = k - c * SS; i = r / S; j = r - i * S;
+    } else if (KIND == PB_CONV_BWDX) {
+      if (SIDE == 0) { o = k / SS; const int r = k - o * SS; i = r / S; j = r - i * S; c = row; return; }
+      const int hw = d.H * d.W;                                                // dY dilated: row = (b,y,x) of dX
+      b = row / hw; const int q = row - b * hw; y = q / d.W; x = q - y * d.W;
+      o = k / SS; const int r = k - o * SS; i = r / S; j = r - i * S;
+    } else {  // GRADW, k = (b, y, x) of dY
+      const int hw = d.oh * d.ow;
+      b = k / hw; const int q = k - b * hw; y = q / d.ow; x = q - y * d.ow;
+      if (SIDE == 0) { o = row; return; }
+      c = row / SS; const int r = row - c * SS; i = r / S; j = r - i * S;     // row = (c,i,j)
+    }
+  }
+  __device__ __forceinline__ uint64_t next(const GemmMap& d) {
+    constexpr int SS = S * S;
+    uint64_t v = 0;
+    if (KIND == PB_CONV_FWD) {
+      if (SIDE == 0) return __ldg(base++);
+      const int yy = y * d.st + i - d.p, xx = x * d.st + j - d.p;
+      if (yy >= 0 && yy < d.H && xx >= 0 && xx < d.W) v = __ldg(base + ((size_t)(b * d.ci + c) * d.H + yy) * d.W + xx);
+      if (++j == S) { j = 0; if (++i == S) { i = 0; ++c; } }
+    } else if (KIND == PB_CONV_BWDX) {
+      if (SIDE == 0) {
+        v = __ldg(base + (size_t)(o * d.ci + c) * SS + i * S + j);
+      } else {
+        const int u = y + d.p - i, w = x + d.p - j;
+        if (u >= 0 && w >= 0) {
+          const int yy = d.st == 1 ? u : u / d.st, xx = d.st == 1 ? w : w / d.st;  // stride 1: no division
+          if (yy * d.st == u && xx * d.st == w && yy < d.oh && xx < d.ow)
+            v = __ldg(base + ((size_t)(b * d.co + o) * d.oh + yy) * d.ow + xx);
+        }
+      }
+      if (++j == S) { j = 0; if (++i == S) { i = 0; ++o; } }
+    } else {
+      if (SIDE == 0) {
+        v = __ldg(base + ((size_t)(b * d.co + o) * d.oh + y) * d.ow + x);
+      } else {
+        const int yy = y * d.st + i - d.p, xx = x * d.st + j - d.p;
+        if (yy >= 0 && yy < d.H && xx >= 0 && xx < d.W) v = __ldg(base + ((size_t)(b * d.ci + c) * d.H + yy) * d.W + xx);
+      }
+      if (++x == d.ow) { x = 0; if (++y == d.oh) { y = 0; ++b; } }
+    }
+    return v;
+  }
+};
+
