@@ -1,3 +1,4 @@
+"""ncu driver: the tiled ct x pt MAC (k_mac_ws) at the conv-like shape B_ct=64, O_pt=13, K=16, twice."""
 import os, sys
 sys.path.insert(0, '/root/repo')
 import torch
