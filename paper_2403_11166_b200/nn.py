@@ -685,6 +685,7 @@ class GraphStep:
             self._stage = torch.empty(tuple(self.x.values.shape), dtype=torch.float64, device=dev)
             self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
             self._flag_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+            self._flag_np = self._flag_host.numpy()  # read on the host's critical path: no torch indexing
             self._ev_loaded, self._ev_free = torch.cuda.Event(), None
         if self.prefetch:
             from .ring import encode_fixed_into
@@ -745,7 +746,7 @@ class GraphStep:
         """The DO's loss gradient into g_host (raises on an out-of-range batch)."""
         if self._flag_pending:
             self._flag_pending = False
-            if int(self._flag_host[0]):
+            if int(self._flag_np[0]):
                 from .errors import EncodeRangeError
 
                 limit = float(1 << (self.model.ring.ell - 1)) / float(1 << self.model.ring.f)
