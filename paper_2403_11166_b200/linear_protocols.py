@@ -768,7 +768,9 @@ def grad_w_flipped(mo_x_zero: bool, mo_gy_zero: bool) -> bool:
     plaintexts), the forward-only X side (prepared beside the loss) grows to 64.
     Measured on the MLP step: 1.5 % slower (the larger host-gap preparation
     delays the backward; profiles/r01_ab_gradw_flip.txt), so off by default;
-    one-term layers never flip (the first layer's X side would grow 80 -> 208)."""
+    one-term layers never flip (the first layer's X side would grow 80 -> 208;
+    re-measured in round 2: the gradient's critical-path encode shrinks 1120 ->
+    448 rows but the larger background preparation makes the step 4 % slower)."""
     return _GRADW_FLIP and not (mo_x_zero or mo_gy_zero)
 
 
