@@ -2,7 +2,8 @@
 reference algorithms (K:206-218 matmul_wrap, K:260-278 conv2d_wrap with the
 SPEC:284 pad / stride lowerings, oracle/convops.py), mod 2^59:
 
-* PB_BACKEND_CUDA_CORE -- u64 IMAD tiles (pb_conv.cu, pb_ring.cu);
+* PB_BACKEND_CUDA_CORE -- u64 IMAD tiles (pb_conv.cu, pb_ring.cu; convolutions
+  with <= 16 output rows on the skinny column kernel);
 * PB_BACKEND_TENSOR   -- tcgen05 kind::i8 on balanced base-256 digit planes
   with the eight partial products in TMEM (pb_tc.cu);
 * PB_BACKEND_AUTO     -- what pb_ring_matmul / pb_ring_conv pick.
@@ -89,6 +90,8 @@ CONV_SHAPES = [  # B, c_i, c_o, H, W, s, pad, stride
     (64, 64, 64, 8, 8, 3, 1, 1),     # CIFAR conv3
     (64, 64, 16, 8, 8, 1, 0, 1),     # CIFAR conv5 (1x1)
     (8, 1, 5, 28, 28, 5, 2, 2),      # MNIST conv (stride 2)
+    (64, 5, 5, 14, 14, 5, 2, 1),     # MNIST conv2 at B = 64: the skinny kernel (<= 8 rows), split-K grad-W
+    (5, 12, 11, 10, 10, 3, 1, 1),    # 9..16 rows (skinny kernel, 16-row accumulators), odd tails
     (3, 5, 7, 9, 9, 3, 1, 2),        # odd tails, stride 2 (square: K conv2d_wrap kernels are s x s)
 ]
 
