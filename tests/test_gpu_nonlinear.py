@@ -60,6 +60,35 @@ def test_nl_ops_bit_exact_vs_oracle(kind, k):
         assert np.array_equal(dout.cpu().numpy(), want[2])
 
 
+@pytest.mark.parametrize("ell,k", [(40, 7), (62, 13), (21, 9), (8, 3)])
+def test_nl_relu_trunc_other_widths_bit_exact(ell, k):
+    """Ring widths / shifts beyond the engine's ell = 59, f = 25: the
+    comparison tree's other compile-time leaf counts (ceil(bits / 4) = 1..16)."""
+    import torch
+
+    from paper_2403_11166_b200 import _dev, _lib
+
+    n, off, seed, stream = 3001, 5, 91, 2_000_321
+    m = np.uint64((1 << ell) - 1)
+    rng = np.random.default_rng(ell * 100 + k)
+    x0 = rng.integers(0, 1 << ell, size=n, dtype=np.uint64)
+    x1 = rng.integers(0, 1 << ell, size=n, dtype=np.uint64)
+    x1[:4] = [0, 1, m, m - x0[3]]
+    for kind in ("relu_trunc", "trunc", "drelu"):
+        want = NL.nl_op(kind, x0, x1, ell, k=k, seed=seed, stream=stream, offset=off)
+        y0, y1 = _dev.empty_u64(n), _dev.empty_u64(n)
+        dout = torch.empty(n, dtype=torch.uint8, device="cuda")
+        dx0, dx1 = _dev.u64_to_device(x0), _dev.u64_to_device(x1)  # referenced until the kernel ran
+        _lib.call("pb_nl_op", KINDS[kind], _dev.ptr(dx0), _dev.ptr(dx1), n, ell,
+                  k, None, _dev.ptr(dout), seed, None, stream, off, _dev.ptr(y0), _dev.ptr(y1), _dev.stream())
+        torch.cuda.synchronize()
+        if want[0] is not None:
+            assert np.array_equal(_dev.to_numpy_u64(y0), want[0]), kind
+            assert np.array_equal(_dev.to_numpy_u64(y1), want[1]), kind
+        if want[2] is not None:
+            assert np.array_equal(dout.cpu().numpy(), want[2]), kind
+
+
 @pytest.mark.parametrize("arch,B", [([784, 32, 10], 8), (((2, 8, 8), [("conv", 2, 3, 3, 1, 1), ("pool",),
                                                                    ("conv", 3, 4, 3, 1, 2), ("flatten",),
                                                                    ("fc", 16, 6), ("fc", 6, 10)]), 3)])
