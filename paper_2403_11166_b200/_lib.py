@@ -125,6 +125,9 @@ POOL_SUM, POOL_REPLICATE = range(2)
 _lib = None
 
 
+ABI_VERSION = 2  # include/pencil_b200.h PB_ABI_VERSION
+
+
 def load(build_if_missing: bool = True):
     """Load (building first if needed) the in-tree CUDA library."""
     global _lib
@@ -137,6 +140,11 @@ def load(build_if_missing: bool = True):
     if not os.path.exists(LIB_PATH):
         raise DeviceError(f"CUDA engine library missing: {LIB_PATH} (run __graft_entry__.build())")
     lib = ctypes.CDLL(LIB_PATH)
+    lib.pb_abi_version.restype = ctypes.c_int
+    got = lib.pb_abi_version()
+    if got != ABI_VERSION:  # a stale library would mis-bind the changed signatures
+        raise DeviceError(f"{LIB_PATH}: C ABI version {got}, this package binds {ABI_VERSION} "
+                          "(rebuild: __graft_entry__.build())")
     for name, args in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = args

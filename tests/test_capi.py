@@ -37,7 +37,7 @@ def test_library_is_sm100a_native():
 
 def test_abi_version_and_error_channel():
     lib = _lib.load()
-    assert lib.pb_abi_version() == 1
+    assert lib.pb_abi_version() == _lib.ABI_VERSION == 2
     # argument validation runs host-side, before any device work
     st = lib.pb_ring_binary(99, None, None, None, 0, 1, 59, None)
     assert st == 8
