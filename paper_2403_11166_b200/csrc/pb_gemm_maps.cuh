@@ -90,27 +90,38 @@ __device__ __forceinline__ void digits8(uint64_t v, int8_t (&d)[8]) {
 // kernel size S, the contraction index walked without per-element divisions.
 template <int KIND, int S, int SIDE>
 struct Gather {
-  // per-thread state for row `row` starting at contraction index k
-  int b, c, i, j, y, x, o;
-  const uint64_t* base;
+  // per-thread state for row `row` starting at contraction index k: the kernel
+  // / output indices and a pointer to the current (image, channel) plane, so
+  // each element costs an add, two unsigned bound checks and a 32-bit offset
+  int c, i, j, y, x, o;
+  int y0, x0;             // FWD: y st - p, x st - p;  GRADW side 1: i - p + y st, j - p + x st (walking)
+  const uint64_t* base;   // the current plane (side 1) / row (side 0)
   __device__ __forceinline__ void init(const GemmMap& d, const uint64_t* src, int row, int k) {
     constexpr int SS = S * S;
     base = src;
     if (KIND == PB_CONV_FWD) {
       if (SIDE == 0) { base = src + (size_t)row * (d.ci * SS) + k; return; }   // W[o][(c,i,j)]
       const int hw = d.oh * d.ow;                                              // X im2col: row = (b,y,x)
-      b = row / hw; const int q = row - b * hw; y = q / d.ow; x = q - y * d.ow;
+      const int b = row / hw, q = row - b * hw;
+      y = q / d.ow; x = q - y * d.ow;
       c = k / SS; const int r = k - c * SS; i = r / S; j = r - i * S;
+      y0 = y * d.st - d.p; x0 = x * d.st - d.p;
+      base = src + (size_t)(b * d.ci + c) * d.H * d.W;
     } else if (KIND == PB_CONV_BWDX) {
       if (SIDE == 0) { o = k / SS; const int r = k - o * SS; i = r / S; j = r - i * S; c = row; return; }
       const int hw = d.H * d.W;                                                // dY dilated: row = (b,y,x) of dX
-      b = row / hw; const int q = row - b * hw; y = q / d.W; x = q - y * d.W;
+      const int b = row / hw, q = row - b * hw;
+      y = q / d.W; x = q - y * d.W;
       o = k / SS; const int r = k - o * SS; i = r / S; j = r - i * S;
+      base = src + (size_t)(b * d.co + o) * d.oh * d.ow;
     } else {  // GRADW, k = (b, y, x) of dY
       const int hw = d.oh * d.ow;
-      b = k / hw; const int q = k - b * hw; y = q / d.ow; x = q - y * d.ow;
-      if (SIDE == 0) { o = row; return; }
+      const int b = k / hw, q = k - b * hw;
+      y = q / d.ow; x = q - y * d.ow;
+      if (SIDE == 0) { o = row; base = src + ((size_t)(b * d.co + o) * d.oh + y) * d.ow + x; return; }
       c = row / SS; const int r = row - c * SS; i = r / S; j = r - i * S;     // row = (c,i,j)
+      y0 = y * d.st + i - d.p; x0 = x * d.st + j - d.p;
+      base = src + (size_t)(b * d.ci + c) * d.H * d.W;
     }
   }
   __device__ __forceinline__ uint64_t next(const GemmMap& d) {
@@ -118,29 +129,34 @@ struct Gather {
     uint64_t v = 0;
     if (KIND == PB_CONV_FWD) {
       if (SIDE == 0) return __ldg(base++);
-      const int yy = y * d.st + i - d.p, xx = x * d.st + j - d.p;
-      if (yy >= 0 && yy < d.H && xx >= 0 && xx < d.W) v = __ldg(base + ((size_t)(b * d.ci + c) * d.H + yy) * d.W + xx);
-      if (++j == S) { j = 0; if (++i == S) { i = 0; ++c; } }
+      const int yy = y0 + i, xx = x0 + j;
+      if ((unsigned)yy < (unsigned)d.H && (unsigned)xx < (unsigned)d.W) v = __ldg(base + yy * d.W + xx);
+      if (++j == S) { j = 0; if (++i == S) { i = 0; base += (size_t)d.H * d.W; } }
     } else if (KIND == PB_CONV_BWDX) {
       if (SIDE == 0) {
         v = __ldg(base + (size_t)(o * d.ci + c) * SS + i * S + j);
       } else {
         const int u = y + d.p - i, w = x + d.p - j;
-        if (u >= 0 && w >= 0) {
-          const int yy = d.st == 1 ? u : u / d.st, xx = d.st == 1 ? w : w / d.st;  // stride 1: no division
-          if (yy * d.st == u && xx * d.st == w && yy < d.oh && xx < d.ow)
-            v = __ldg(base + ((size_t)(b * d.co + o) * d.oh + yy) * d.ow + xx);
+        if (d.st == 1) {  // stride 1: no division
+          if ((unsigned)u < (unsigned)d.oh && (unsigned)w < (unsigned)d.ow) v = __ldg(base + u * d.ow + w);
+        } else if (u >= 0 && w >= 0) {
+          const int yy = u / d.st, xx = w / d.st;
+          if (yy * d.st == u && xx * d.st == w && yy < d.oh && xx < d.ow) v = __ldg(base + yy * d.ow + xx);
         }
       }
-      if (++j == S) { j = 0; if (++i == S) { i = 0; ++o; } }
+      if (++j == S) { j = 0; if (++i == S) { i = 0; ++o; if (SIDE == 1) base += (size_t)d.oh * d.ow; } }
     } else {
       if (SIDE == 0) {
-        v = __ldg(base + ((size_t)(b * d.co + o) * d.oh + y) * d.ow + x);
-      } else {
-        const int yy = y * d.st + i - d.p, xx = x * d.st + j - d.p;
-        if (yy >= 0 && yy < d.H && xx >= 0 && xx < d.W) v = __ldg(base + ((size_t)(b * d.ci + c) * d.H + yy) * d.W + xx);
+        v = __ldg(base++);  // dY[b][o][y][x], walking (x, y) then jumping to the next image's plane o
+        if (++x == d.ow) { x = 0; if (++y == d.oh) { y = 0; base += (size_t)(d.co - 1) * d.oh * d.ow; } }
+        return v;
       }
-      if (++x == d.ow) { x = 0; if (++y == d.oh) { y = 0; ++b; } }
+      if ((unsigned)y0 < (unsigned)d.H && (unsigned)x0 < (unsigned)d.W) v = __ldg(base + y0 * d.W + x0);
+      x0 += d.st;
+      if (++x == d.ow) {
+        x = 0; x0 = j - d.p; y0 += d.st;
+        if (++y == d.oh) { y = 0; y0 = i - d.p; base += (size_t)d.ci * d.H * d.W; }
+      }
     }
     return v;
   }

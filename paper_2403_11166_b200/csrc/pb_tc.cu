@@ -219,7 +219,8 @@ __global__ void __launch_bounds__(256) k_tc_digits(GemmMap d, const uint64_t* __
   const size_t plane = (size_t)rows * Kp;
   constexpr uint64_t C = 0x8080808080808080ull;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int row = (int)(e / q16), kk = 16 * (int)(e - (int64_t)row * q16);
+    const int row = total < (1ll << 32) ? (int)((uint32_t)e / (uint32_t)q16) : (int)(e / q16);
+    const int kk = 16 * (int)(e - (int64_t)row * q16);
     uint64_t t[16];
     const int nk = kc - kk < 16 ? (kc - kk > 0 ? kc - kk : 0) : 16;
     if (KIND == 3) {  // matmul: strided or contiguous rows, no index arithmetic to save
@@ -229,8 +230,13 @@ __global__ void __launch_bounds__(256) k_tc_digits(GemmMap d, const uint64_t* __
     } else {
       Gather<KIND, S, SIDE> g;
       g.init(d, src, row, k0 + kk);
+      if (nk == 16) {  // whole chunks: no per-element tail predicate
 #pragma unroll
-      for (int u = 0; u < 16; ++u) t[u] = u < nk ? g.next(d) : 0ull;
+        for (int u = 0; u < 16; ++u) t[u] = g.next(d);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) t[u] = u < nk ? g.next(d) : 0ull;
+      }
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) t[u] = ((t[u] & mask) + C) ^ C;  // the eight int8 digits, little-endian
