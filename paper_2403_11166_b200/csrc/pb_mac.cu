@@ -231,16 +231,21 @@ struct PipeCfg {
 // never wait for the issuing thread at a CTA barrier (ncu on the round-1
 // single-role kernel: 26%
 // of stall samples were the per-k __syncthreads behind thread 0's issue work).
-template <int TB, int TO, int V, int STAGES, int MINB = 1, int CT = MAC_THREADS>
+// TERMS: 1 = cross term A only, 2 = B only (compile-time: the consumer loop
+// carries no per-k term branches and the slot layout is constant; single-term
+// evaluations 6-8 % faster); 0 = both, taken at run time -- the compile-time
+// two-term body spills at the 96-register budget (and measured 6-10 % slower).
+template <int TB, int TO, int V, int STAGES, int MINB = 1, int CT = MAC_THREADS, int TERMS = 3>
 __global__ void __launch_bounds__(CT + 32, MINB)
     k_mac_ws(PbDev P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB, int nB,
              int nO, int nI, uint32_t* ct_out) {
   using C = PipeCfg<TB, TO, V, CT>;
   using VT = typename Vec<V>::T;
+  const bool HA = TERMS ? (TERMS & 1) != 0 : ctA != nullptr, HB = TERMS ? (TERMS & 2) != 0 : ctB != nullptr;
   extern __shared__ __align__(128) uint8_t pipe_sm[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
-  const int CA = 0, PA = 2 * TB, CB = ctA ? C::SLOTS_A : 0, PB = CB + 2 * TO;
-  const int nslots = (ctA ? C::SLOTS_A : 0) + (ctB ? C::SLOTS_B : 0);
+  const int CA = 0, PA = 2 * TB, CB = HA ? C::SLOTS_A : 0, PB = CB + 2 * TO;
+  const int nslots = (HA ? C::SLOTS_A : 0) + (HB ? C::SLOTS_B : 0);
   const int N = P.N, L = P.L;
   const int slices = N / (V * CT);
   const int tilesO = (nO + TO - 1) / TO;
@@ -278,21 +283,21 @@ __global__ void __launch_bounds__(CT + 32, MINB)
       const uint8_t* a = reinterpret_cast<const uint8_t*>(ctA) + bi * ct_k + off;
       base[2 * i] = a, base[2 * i + 1] = a + (size_t)L * rowb;
       dsto[2 * i] = (CA + 2 * i) * C::SLOT, dsto[2 * i + 1] = (CA + 2 * i + 1) * C::SLOT;
-      on[2 * i] = on[2 * i + 1] = ctA && okb[i];
+      on[2 * i] = on[2 * i + 1] = HA && okb[i];
       base[C::SLOTS_A + 2 * TO + i] = reinterpret_cast<const uint8_t*>(ptB) + bi * pt_k + off;
       dsto[C::SLOTS_A + 2 * TO + i] = (PB + i) * C::SLOT;
-      on[C::SLOTS_A + 2 * TO + i] = ctB && okb[i];
+      on[C::SLOTS_A + 2 * TO + i] = HB && okb[i];
     }
 #pragma unroll
     for (int o = 0; o < TO; ++o) {
       const size_t oi = (size_t)(to * TO + o) * nI;
       base[2 * TB + o] = reinterpret_cast<const uint8_t*>(ptA) + oi * pt_k + off;
       dsto[2 * TB + o] = (PA + o) * C::SLOT;
-      on[2 * TB + o] = ctA && oko[o];
+      on[2 * TB + o] = HA && oko[o];
       const uint8_t* b = reinterpret_cast<const uint8_t*>(ctB) + oi * ct_k + off;
       base[C::SLOTS_A + 2 * o] = b, base[C::SLOTS_A + 2 * o + 1] = b + (size_t)L * rowb;
       dsto[C::SLOTS_A + 2 * o] = (CB + 2 * o) * C::SLOT, dsto[C::SLOTS_A + 2 * o + 1] = (CB + 2 * o + 1) * C::SLOT;
-      on[C::SLOTS_A + 2 * o] = on[C::SLOTS_A + 2 * o + 1] = ctB && oko[o];
+      on[C::SLOTS_A + 2 * o] = on[C::SLOTS_A + 2 * o + 1] = HB && oko[o];
     }
 #pragma unroll
     for (int c = 0; c < NS; ++c) bytes += on[c] ? (uint32_t)C::SLOT : 0u;
@@ -330,15 +335,17 @@ __global__ void __launch_bounds__(CT + 32, MINB)
     for (int e = 0; e < V; ++e) a[e] += (uint64_t)Vec<V>::get(x, e) * Vec<V>::get(w, e);
   };
   constexpr int SV = C::SLOT / (4 * V);
-  const int chunk = (ctA && ctB) ? MAC_FOLD2 : MAC_FOLD1;  // k-steps between folds
+  const int chunk = (HA && HB) ? MAC_FOLD2 : MAC_FOLD1;  // k-steps between folds
   const uint32_t r32 = reduce64(1ull << 32, q, mu);            // 2^32 mod q
   int since = 0;
   const uint32_t full0 = smem_addr(full), empty0 = smem_addr(empty);
+  const VT* st0 = reinterpret_cast<const VT*>(pipe_sm) + tid;
+  int s = 0;
+  uint32_t ph = 0;
   for (int k = 0; k < nI; ++k) {
-    const int s = k % STAGES;
-    mbar_wait_a(full0 + 8u * s, (uint32_t)((k / STAGES) & 1));
-    const VT* st = reinterpret_cast<const VT*>(pipe_sm + (size_t)s * nslots * C::SLOT) + tid;
-    if (ctA) {
+    mbar_wait_a(full0 + 8u * s, ph);
+    const VT* st = st0 + s * (nslots * SV);
+    if (HA) {
       VT w[TO];
 #pragma unroll
       for (int o = 0; o < TO; ++o) w[o] = st[(PA + o) * SV];
@@ -349,7 +356,7 @@ __global__ void __launch_bounds__(CT + 32, MINB)
         for (int o = 0; o < TO; ++o) { mac(acc[i][o][0], x0, w[o]); mac(acc[i][o][1], x1, w[o]); }
       }
     }
-    if (ctB) {
+    if (HB) {
       VT u[TB];
 #pragma unroll
       for (int i = 0; i < TB; ++i) u[i] = st[(PB + i) * SV];
@@ -362,6 +369,10 @@ __global__ void __launch_bounds__(CT + 32, MINB)
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive_a(empty0 + 8u * s);  // this warp is done reading stage s
+    if (++s == STAGES) {
+      s = 0;
+      ph ^= 1u;
+    }
     if (++since == chunk && k + 1 < nI) {
       since = 0;
 #pragma unroll
@@ -400,19 +411,27 @@ __global__ void __launch_bounds__(CT + 32, MINB)
     }
 }
 
-template <int TB, int TO, int V, int STAGES, int MINB = 1, int CT = MAC_THREADS>
-void launch_ws(const PbDev& P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB,
-               int nB, int nO, int nI, uint32_t* out, cudaStream_t st) {
+template <int TB, int TO, int V, int STAGES, int MINB, int CT, int TERMS>
+void launch_ws_t(const PbDev& P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB,
+                 int nB, int nO, int nI, uint32_t* out, cudaStream_t st) {
   using C = PipeCfg<TB, TO, V, CT>;
   const size_t smem = (size_t)STAGES * ((ctA ? C::SLOTS_A : 0) + (ctB ? C::SLOTS_B : 0)) * C::SLOT;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_mac_ws<TB, TO, V, STAGES, MINB, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((size_t)STAGES * (C::SLOTS_A + C::SLOTS_B) * C::SLOT));
+    cudaFuncSetAttribute(k_mac_ws<TB, TO, V, STAGES, MINB, CT, TERMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     attr = true;
   }
   dim3 grid((unsigned)(((nB + TB - 1) / TB) * ((nO + TO - 1) / TO)), (unsigned)(P.L * (P.N / (V * CT))));
-  k_mac_ws<TB, TO, V, STAGES, MINB, CT><<<grid, CT + 32, smem, st>>>(P, ctA, ptA, ctB, ptB, nB, nO, nI, out);
+  k_mac_ws<TB, TO, V, STAGES, MINB, CT, TERMS><<<grid, CT + 32, smem, st>>>(P, ctA, ptA, ctB, ptB, nB, nO, nI, out);
+}
+
+template <int TB, int TO, int V, int STAGES, int MINB = 1, int CT = MAC_THREADS>
+void launch_ws(const PbDev& P, const uint32_t* ctA, const uint32_t* ptA, const uint32_t* ctB, const uint32_t* ptB,
+               int nB, int nO, int nI, uint32_t* out, cudaStream_t st) {
+  if (ctA && ctB) launch_ws_t<TB, TO, V, STAGES, MINB, CT, 0>(P, ctA, ptA, ctB, ptB, nB, nO, nI, out, st);
+  else if (ctA) launch_ws_t<TB, TO, V, STAGES, MINB, CT, 1>(P, ctA, ptA, ctB, ptB, nB, nO, nI, out, st);
+  else launch_ws_t<TB, TO, V, STAGES, MINB, CT, 2>(P, ctA, ptA, ctB, ptB, nB, nO, nI, out, st);
 }
 
 // Eager variant (Montgomery multiply + reduce per term, u32 accumulators,
