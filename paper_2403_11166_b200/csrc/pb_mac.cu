@@ -340,52 +340,55 @@ __global__ void __launch_bounds__(CT + 32, MINB)
   int since = 0;
   const uint32_t full0 = smem_addr(full), empty0 = smem_addr(empty);
   const VT* st0 = reinterpret_cast<const VT*>(pipe_sm) + tid;
-  int s = 0;
+  const bool lane0 = (tid & 31) == 0;
   uint32_t ph = 0;
-  for (int k = 0; k < nI; ++k) {
-    mbar_wait_a(full0 + 8u * s, ph);
-    const VT* st = st0 + s * (nslots * SV);
-    if (HA) {
-      VT w[TO];
+  // the stage ring unrolled: stage s is a compile-time offset from one base
+  // (no per-k address arithmetic or shared-window re-derivation)
+  for (int k0 = 0; k0 < nI; k0 += STAGES, ph ^= 1u) {
 #pragma unroll
-      for (int o = 0; o < TO; ++o) w[o] = st[(PA + o) * SV];
+    for (int s = 0; s < STAGES; ++s) {
+      const int k = k0 + s;
+      if (k >= nI) break;
+      mbar_wait_a(full0 + 8u * s, ph);
+      const VT* st = st0 + s * (nslots * SV);
+      if (HA) {
+        VT w[TO];
 #pragma unroll
-      for (int i = 0; i < TB; ++i) {
-        const VT x0 = st[(CA + 2 * i) * SV], x1 = st[(CA + 2 * i + 1) * SV];
+        for (int o = 0; o < TO; ++o) w[o] = st[(PA + o) * SV];
 #pragma unroll
-        for (int o = 0; o < TO; ++o) { mac(acc[i][o][0], x0, w[o]); mac(acc[i][o][1], x1, w[o]); }
+        for (int i = 0; i < TB; ++i) {
+          const VT x0 = st[(CA + 2 * i) * SV], x1 = st[(CA + 2 * i + 1) * SV];
+#pragma unroll
+          for (int o = 0; o < TO; ++o) { mac(acc[i][o][0], x0, w[o]); mac(acc[i][o][1], x1, w[o]); }
+        }
       }
-    }
-    if (HB) {
-      VT u[TB];
+      if (HB) {
+        VT u[TB];
 #pragma unroll
-      for (int i = 0; i < TB; ++i) u[i] = st[(PB + i) * SV];
+        for (int i = 0; i < TB; ++i) u[i] = st[(PB + i) * SV];
 #pragma unroll
-      for (int o = 0; o < TO; ++o) {
-        const VT y0 = st[(CB + 2 * o) * SV], y1 = st[(CB + 2 * o + 1) * SV];
+        for (int o = 0; o < TO; ++o) {
+          const VT y0 = st[(CB + 2 * o) * SV], y1 = st[(CB + 2 * o + 1) * SV];
 #pragma unroll
-        for (int i = 0; i < TB; ++i) { mac(acc[i][o][0], y0, u[i]); mac(acc[i][o][1], y1, u[i]); }
+          for (int i = 0; i < TB; ++i) { mac(acc[i][o][0], y0, u[i]); mac(acc[i][o][1], y1, u[i]); }
+        }
       }
-    }
-    __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive_a(empty0 + 8u * s);  // this warp is done reading stage s
-    if (++s == STAGES) {
-      s = 0;
-      ph ^= 1u;
-    }
-    if (++since == chunk && k + 1 < nI) {
-      since = 0;
+      __syncwarp();
+      if (lane0) mbar_arrive_a(empty0 + 8u * s);  // this warp is done reading stage s
+      if (++since == chunk && k + 1 < nI) {
+        since = 0;
 #pragma unroll
-      for (int i = 0; i < TB; ++i)
+        for (int i = 0; i < TB; ++i)
 #pragma unroll
-        for (int o = 0; o < TO; ++o)
+          for (int o = 0; o < TO; ++o)
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
+            for (int c = 0; c < 2; ++c)
 #pragma unroll
-            for (int e = 0; e < V; ++e) {
-              const uint64_t a = acc[i][o][c][e];
-              acc[i][o][c][e] = (uint64_t)(uint32_t)(a >> 32) * r32 + (uint32_t)a;
-            }
+              for (int e = 0; e < V; ++e) {
+                const uint64_t a = acc[i][o][c][e];
+                acc[i][o][c][e] = (uint64_t)(uint32_t)(a >> 32) * r32 + (uint32_t)a;
+              }
+      }
     }
   }
   auto fin = [&](uint64_t a) { return csub(mont_lazy(reduce64(a, q, mu), 1u, q, qn), q); };
