@@ -48,12 +48,16 @@ __global__ void __launch_bounds__(1 << (LOGN - 5))
     const uint64_t mu = P.mu[l];
     const uint32_t tm = P.tmod[l];
     uint32_t a[32];
-    const int bits =  // OR of the occupied indices: structurally trivial NTT stages are skipped
-        pbk::load_source<Nt>(a, sm, src, p, tid, [&](uint64_t v) { return lift_centered(v, ell, q, mu, tm); });
-    Nt::forward(a, sm, P.tw_fwd + (size_t)l * Nt::N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q, bits);
+    // x 2^32 (Montgomery form) applied to the source values before the NTT
+    // (linear): once per occupied slot of a packed source instead of once per
+    // output coefficient
     const uint32_t r2 = P.r2[l], r2s = P.r2_sh[l];
+    const int bits =  // OR of the occupied indices: structurally trivial NTT stages are skipped
+        pbk::load_source<Nt>(a, sm, src, p, tid,
+                             [&](uint64_t v) { return mul_shoup(lift_centered(v, ell, q, mu, tm), r2, r2s, q); });
+    Nt::forward(a, sm, P.tw_fwd + (size_t)l * Nt::N, P.tw3_fwd + (size_t)l * P.tw3_stride, tid, q, bits);
 #pragma unroll
-    for (int c = 0; c < 32; ++c) a[c] = mul_shoup(pb::canon4(a[c], q), r2, r2s, q);
+    for (int c = 0; c < 32; ++c) a[c] = pb::canon4(a[c], q);
     Nt::gst3(pt + (p * L + l) * Nt::N, a, tid);
   }
 }
