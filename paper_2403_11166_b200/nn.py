@@ -117,6 +117,19 @@ class Model:
         # step-abort word (GraphStep's loss handoff): nonzero -> the SGD kernels are no-ops
         self.skip = torch.zeros(1, dtype=torch.int32, device=dev)
         self.dp_group, self.dp_world = None, 1
+        self._zeros = {}
+
+    def zero_share(self, like: torch.Tensor) -> torch.Tensor:
+        """A cached all-zero ring tensor shaped like ``like``: the MO's
+        structurally zero shares (the network input, the loss gradient).  Read
+        only -- every protocol writes fresh outputs -- so one buffer serves all
+        steps, and a graph captured after it exists carries no fill kernel on
+        its critical path."""
+        key = (tuple(like.shape), like.dtype, like.device)
+        z = self._zeros.get(key)
+        if z is None:
+            z = self._zeros[key] = torch.zeros_like(like)
+        return z
 
     def set_data_parallel(self, group, world: int):
         """Data-parallel private training over ``world`` ranks of ``group``
@@ -268,7 +281,7 @@ def forward_phase(sess: Session, model: Model, x: RingTensor, prep=None):
     HE-free online protocol (SPEC mode "prep")."""
     ring, f = model.ring, model.ring.f
     seg = model.segments()
-    cur = (ShareTensor(MO, RingTensor(torch.zeros_like(x.values), f, ring, _canonical=True)), ShareTensor(DO, x))
+    cur = (ShareTensor(MO, RingTensor(model.zero_share(x.values), f, ring, _canonical=True)), ShareTensor(DO, x))
     acts, ds, ys = [], [], []
     if prep is None:  # every layer's MO mask depends only on the seed: draw them all up front
         B = x.shape[1] if len(model.in_shape) == 1 else x.shape[0]
@@ -335,7 +348,7 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
             if pre_layers:
                 prepare_backward(sess, model, state, prep, layers=pre_layers, clear=False, background=True)
     gy_do = ShareTensor(DO, RingTensor(g_do, f, ring, _canonical=True))
-    gy_mo = ShareTensor(MO, RingTensor(torch.zeros_like(g_do), f, ring, _canonical=True))
+    gy_mo = ShareTensor(MO, RingTensor(model.zero_share(g_do), f, ring, _canonical=True))
     gws, gbs = [None] * L, [None] * L
     # The weight-gradient protocols (bias reveal + Alg.2) of layer l and the
     # input-gradient chain to layer l-1 are independent given grad Y_l: Alg.2
@@ -596,6 +609,9 @@ class GraphStep:
             self.g_enc = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.g_enc):
                 self._prefetch_encrypt()  # leaves the prepared entry the forward capture consumes
+        model.zero_share(x.values)  # the zero shares exist before capture: no fill kernels in the graphs
+        model.zero_share(self.g_do)
+        torch.cuda.synchronize()
         self.g_fwd = torch.cuda.CUDAGraph()
         self.g_pre = torch.cuda.CUDAGraph()
         self.g_bwd = torch.cuda.CUDAGraph()
