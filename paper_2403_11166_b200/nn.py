@@ -180,12 +180,15 @@ class Model:
         if check:
             self.check_range()
 
-    def sgd_layer(self, l: int, gw: RingTensor, gb: RingTensor, lr=1e-2, momentum=0.8):
-        """SGD with momentum for layer l's (W, b) on the current stream (no host sync)."""
+    def sgd_layer(self, l: int, gw: RingTensor | None, gb: RingTensor | None, lr=1e-2, momentum=0.8):
+        """SGD with momentum for layer l's W and / or b (None: skipped) on the
+        current stream (no host sync)."""
         ring = self.ring
         st = _dev.stream()
         for w, v, g, ring_t, scale in ((self.w[l], self.vw[l], gw, self.W[l], ring.f),
                                        (self.b[l], self.vb[l], gb, self.B[l], 2 * ring.f)):
+            if g is None:
+                continue
             _lib.call("pb_sgd_momentum", _dev.ptr(w), _dev.ptr(v), _dev.ptr(g.values), w.numel(), g.scale,
                       float(lr), float(momentum), ring.ell, scale, _dev.ptr(ring_t.values), _dev.ptr(self._flag),
                       _dev.ptr(self.skip), st)
@@ -370,18 +373,20 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
             wshape = (e[2], e[1]) if e[0] == "fc" else (e[2], e[1], e[3], e[3])
             eb = dp_noise(sess, l, OP_GRAD_B, (e[2],), f)
             ew = dp_noise(sess, l, OP_GRAD_W, wshape, 2 * f)
+            gbs[l] = (reveal_grad_bias if e[0] == "fc" else reveal_grad_bias_conv)(sess, l, gy_mo, gy_do, e=eb)
+            model.reduce_grads(gbs[l])  # data parallel: sum over ranks before the update
+            # b_l is not read again this step: its update goes now, beside the
+            # weight-gradient protocol instead of behind it
+            model.sgd_layer(l, None, gbs[l], lr, momentum)
             if prep is not None:
-                gbs[l] = (reveal_grad_bias if e[0] == "fc" else reveal_grad_bias_conv)(sess, l, gy_mo, gy_do, e=eb)
                 gw = PP.prep_grad_weight(sess, l, prep.banks[l], *acts[l], gy_mo, gy_do, e=ew, mo_x_zero=(l == 0),
                                          mo_gy_zero=last)
             elif e[0] == "fc":
-                gbs[l] = reveal_grad_bias(sess, l, gy_mo, gy_do, e=eb)
                 gw = grad_weight(sess, l, *acts[l], gy_mo, gy_do, e=ew, mo_x_zero=(l == 0), mo_gy_zero=last)
             else:
-                gbs[l] = reveal_grad_bias_conv(sess, l, gy_mo, gy_do, e=eb)
                 gw = conv_grad_weight(sess, l, *acts[l], gy_mo, gy_do, e[3], e[4], e[5], e=ew, mo_x_zero=(l == 0),
                                       mo_gy_zero=last)
-            model.reduce_grads(gw, gbs[l])  # data parallel: sum over ranks at 2f, before the shift
+            model.reduce_grads(gw)  # at 2f, before the shift
             gws[l] = arith_shift(gw, f)
         keep.append((gy_mo, gy_do))
         if trace is not None:
@@ -392,7 +397,7 @@ def backward_phase(sess: Session, model: Model, state, g_do: torch.Tensor, lr=1e
         # the last use of W_l (this layer's input-gradient protocol) are enqueued
         gstream.wait_stream(main)
         with torch.cuda.stream(gstream):
-            model.sgd_layer(l, gws[l], gbs[l], lr, momentum)
+            model.sgd_layer(l, gws[l], None, lr, momentum)
         if l > 0:
             if any(model.layers[k][0] == "pool" for k in seg[l - 1]):
                 t_mo, t_do = truncate(sess, l, *ga, f, backward=True)
