@@ -211,6 +211,23 @@ __global__ void __launch_bounds__(128, 1)
 // consecutive contraction entries of one row (one 128-bit store per plane);
 // the conv gathers are specialised on the kernel size S and walk the
 // contraction index incrementally (no per-element divisions).
+// 4 planes (bytes 4h .. 4h+3) of 16 values t[], word q of plane 4h + k =
+// byte 4h + k of t[4q .. 4q+3]: a 4 x 4 byte transpose per group of four
+// values in 8 byte permutes (two interleave levels).
+__device__ __forceinline__ void byte_planes(const uint64_t (&t)[16], int h, uint32_t (&w)[4][4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t a = (uint32_t)(t[4 * q] >> (32 * h)), b = (uint32_t)(t[4 * q + 1] >> (32 * h));
+    const uint32_t c = (uint32_t)(t[4 * q + 2] >> (32 * h)), d = (uint32_t)(t[4 * q + 3] >> (32 * h));
+    const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);  // a0 b0 a1 b1 | a2 b2 a3 b3
+    const uint32_t t2 = __byte_perm(c, d, 0x5140), t3 = __byte_perm(c, d, 0x7362);
+    w[0][q] = __byte_perm(t0, t2, 0x5410);
+    w[1][q] = __byte_perm(t0, t2, 0x7632);
+    w[2][q] = __byte_perm(t1, t3, 0x5410);
+    w[3][q] = __byte_perm(t1, t3, 0x7632);
+  }
+}
+
 template <int KIND, int S, int SIDE>
 __global__ void __launch_bounds__(256) k_tc_digits(GemmMap d, const uint64_t* __restrict__ src, int rows, int k0,
                                                    int kc, int Kp, uint64_t mask, int8_t* __restrict__ out) {
@@ -242,18 +259,11 @@ __global__ void __launch_bounds__(256) k_tc_digits(GemmMap d, const uint64_t* __
     for (int u = 0; u < 16; ++u) t[u] = ((t[u] & mask) + C) ^ C;  // the eight int8 digits, little-endian
     uint4* o = reinterpret_cast<uint4*>(out + (size_t)row * Kp + kk);
 #pragma unroll
-    for (int p = 0; p < 8; ++p) {  // plane p: byte p of each of the 16 values
-      uint32_t w[4];
+    for (int h = 0; h < 2; ++h) {  // planes 4h .. 4h+3: bytes 4h .. 4h+3 of each of the 16 values
+      uint32_t w[4][4];
+      byte_planes(t, h, w);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t h0 = (uint32_t)(t[4 * q] >> (p & 4 ? 32 : 0)), h1 = (uint32_t)(t[4 * q + 1] >> (p & 4 ? 32 : 0));
-        const uint32_t h2 = (uint32_t)(t[4 * q + 2] >> (p & 4 ? 32 : 0)), h3 = (uint32_t)(t[4 * q + 3] >> (p & 4 ? 32 : 0));
-        const uint32_t sel = (uint32_t)(p & 3);
-        const uint32_t lo = __byte_perm(h0, h1, sel | ((sel + 4) << 4));       // bytes p of v0, v1
-        const uint32_t hi = __byte_perm(h2, h3, sel | ((sel + 4) << 4));       // bytes p of v2, v3
-        w[q] = __byte_perm(lo, hi, 0x5410);
-      }
-      o[p * (plane / 16)] = make_uint4(w[0], w[1], w[2], w[3]);
+      for (int k = 0; k < 4; ++k) o[(4 * h + k) * (plane / 16)] = make_uint4(w[k][0], w[k][1], w[k][2], w[k][3]);
     }
   }
 }
@@ -278,18 +288,11 @@ __device__ __forceinline__ void digit_chunk(uint64_t (&t)[16], uint4 (&o)[8]) {
 #pragma unroll
   for (int u = 0; u < 16; ++u) t[u] = (t[u] + C) ^ C;
 #pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    uint32_t w[4];
+  for (int h = 0; h < 2; ++h) {
+    uint32_t w[4][4];
+    byte_planes(t, h, w);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int sh = p & 4 ? 32 : 0;
-      const uint32_t sel = (uint32_t)(p & 3);
-      const uint32_t lo = __byte_perm((uint32_t)(t[4 * q] >> sh), (uint32_t)(t[4 * q + 1] >> sh), sel | ((sel + 4) << 4));
-      const uint32_t hi =
-          __byte_perm((uint32_t)(t[4 * q + 2] >> sh), (uint32_t)(t[4 * q + 3] >> sh), sel | ((sel + 4) << 4));
-      w[q] = __byte_perm(lo, hi, 0x5410);
-    }
-    o[p] = make_uint4(w[0], w[1], w[2], w[3]);
+    for (int k = 0; k < 4; ++k) o[4 * h + k] = make_uint4(w[k][0], w[k][1], w[k][2], w[k][3]);
   }
 }
 
