@@ -760,8 +760,16 @@ class GraphStep:
         the pinned sequence word: no D2H copy, event or API call between the
         forward's last kernel and the DO's loss)."""
         want = self._pub_count & 0xFFFFFFFF
-        while int(self._pub_np[0]) != want:
-            pass
+        pub = self._pub_np
+        spins = 0
+        while int(pub[0]) != want:
+            spins += 1
+            if spins & 0xFFFF == 0:  # now and then: a faulted or finished-but-silent forward
+                # query() raises on a device fault; a completed forward must have published
+                if self._ev_fwd.query() and int(pub[0]) != want:
+                    from .errors import DeviceError
+
+                    raise DeviceError("forward graph completed without publishing the logits")
 
     def _host_grad(self, labels):
         """The DO's loss gradient into g_host (raises on an out-of-range batch)."""
