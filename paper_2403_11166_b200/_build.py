@@ -39,8 +39,18 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def _manifest() -> str:
+    return os.path.join(PKG, "build", "sources.txt")
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
+        return True
+    try:  # a source added or removed since the last link
+        with open(_manifest()) as f:
+            if f.read().split() != [os.path.basename(x) for x in sources()]:
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "pencil_b200.h")]
@@ -74,6 +84,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}{r.stderr}")
     os.replace(tmp, LIB)
+    with open(_manifest(), "w") as f:
+        f.write("\n".join(os.path.basename(x) for x in sources()) + "\n")
     return LIB
 
 
