@@ -54,7 +54,7 @@ FRAME_HEADER = 12  # {u16 type, u16 flags, u64 len}
 _SERIAL = False        # True: every protocol fork on the calling stream (debugging)
 _MASK_PREFETCH = True  # draw all MO masks of a phase up front on a fork
 _GRADW_FLIP = False    # Alg. 2 HE matmul transposed: measured 1.5 % slower
-_BG_CAP = 2 * 148      # CTA cap of background operand preparation (0: none); 148 / 296 / 444 within noise (r02)
+_BG_CAP = 2 * 148      # CTA cap of background operand preparation (0: none); 74-444 within noise, 37 slower (r02_ab_bg_cap)
 _FUSE_MIN_ROWS = 4 * 148  # output rows (ciphertexts x limbs) from which nI <= 2 evaluations fuse mask + MAC
 _PREDRAW = True        # inside a phase: the DO's message-independent encryption half at phase start
 _PREDRAW_MAX_ROWS = 4 * 148  # ... for encryptions of at most one wave of rows (latency-bound; the CIFAR
