@@ -233,12 +233,13 @@ def run_reference(args, rank, world):
     dt, cores = cpu_model_steps("mnist_mlp", BATCH, steps_run, warm - 1)
     v = BATCH / dt
     sample = (f"{steps_run} oracle private training step(s) of the MNIST MLP 784-128-128-10, B={BATCH}, N=8192, "
-              f"L=7, after {warm} in-process warm-up steps (oracle = reference kernels restated in C/OpenMP + numpy)")
+              f"L=7, after {warm} in-process warm-up steps (oracle = reference kernels restated in C/OpenMP + numpy)"
+              + (f"; rank 0 of {world} alone, one host process" if world > 1 else ""))
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
         "steps": steps_run, "warmup": warm, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak" if world > 1 else "n/a", "vs_baseline": None, "dtype": "u32-rns/u64-ring",
-        "data": "synthetic", "config": _config(1), "nonlinear": NONLINEAR,
+        "data": "synthetic", "config": _config(world), "nonlinear": NONLINEAR,  # the GPU arm's config
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -734,7 +735,8 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        if args.impl == "ours":  # the reference arm is host-only (gloo): no device needed
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
     if args.impl == "reference":
         run_reference(args, rank, world)
