@@ -285,6 +285,10 @@ int pb_scatter_u64(uint64_t* out, const uint64_t* src, const int64_t* dst, int64
 /* Row reduction: out[i] = sum_j a[i][j] mod 2^ell  (reveal_grad_bias). */
 int pb_ring_rowsum(const uint64_t* a, int64_t rows, int64_t cols, int32_t ell, uint64_t* out,
                    void* stream);
+/* Channel reduction of an NCHW tensor a (B, C, HW): out[c] = sum_{b,i}
+ * a[b][c][i] mod 2^ell (reveal_grad_bias for Conv2d). */
+int pb_ring_chansum(const uint64_t* a, int32_t B, int32_t C, int64_t HW, int32_t ell, uint64_t* out,
+                    void* stream);
 /* K:221-238 im2col_wrap, K:241-257 col2im_wrap, K:260-278 conv2d_wrap. */
 int pb_im2col(const uint64_t* x, int32_t B, int32_t C, int32_t H, int32_t W, int32_t s,
               int32_t stride, uint64_t* out, void* stream);

@@ -99,6 +99,7 @@ SIGNATURES = {
     "pb_wire_serialize": [P, P, I64, I32, I32, P, P],
     "pb_wire_deserialize": [P, P, I64, I32, I32, P, P, P],
     "pb_ring_rowsum": [P, I64, I64, I32, P, P],
+    "pb_ring_chansum": [P, I32, I32, I64, I32, P, P],
     "pb_im2col": [P, I32, I32, I32, I32, I32, I32, P, P],
     "pb_col2im": [P, I32, I32, I32, I32, I32, I32, P, P],
     "pb_conv2d": [P, P, I32, I32, I32, I32, I32, I32, I32, P, P],

@@ -8,6 +8,8 @@
 
 #include "pb_common.cuh"
 
+#include <algorithm>
+
 namespace {
 
 __device__ __forceinline__ uint64_t ring_mask(int ell) { return ell >= 64 ? ~0ull : ((1ull << ell) - 1); }
@@ -227,6 +229,58 @@ __global__ void k_rowsum(const uint64_t* a, int64_t rows, int64_t cols, uint64_t
   if (threadIdx.x == 0) out[r] = red[0] & mask;
 }
 
+// Per-channel sums of a (B, C, HW) tensor, out[c] = sum_{b,i} a[b][c][i] mod
+// 2^ell (the conv bias gradient), straight from the NCHW layout:
+// CTA (s, c) adds a contiguous chunk of channel c's flattened (b, i) range
+// into part[c][s] (u64 sums wrap mod 2^64: any split is exact), then one warp
+// per channel adds its S partials and masks.  Replaces a permute copy and a
+// one-CTA-per-channel reduction (C = 64 CTAs: 35 us per call on CIFAR conv1).
+__device__ __forceinline__ uint64_t block_sum_u64(uint64_t acc) {
+  __shared__ uint64_t red[32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0ull;
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(256) k_chansum_part(const uint64_t* __restrict__ a, int C, uint32_t HW,
+                                                      uint32_t total, uint32_t chunk, uint64_t* __restrict__ part) {
+  const int c = blockIdx.y;
+  const uint32_t j0 = blockIdx.x * chunk, j1 = min(total, j0 + chunk);
+  uint64_t acc = 0;
+  if (HW >= blockDim.x) {  // (b, i) of the first element once, then walked (at most one wrap per step)
+    uint32_t b = (j0 + threadIdx.x) / HW, i = j0 + threadIdx.x - b * HW;
+    for (uint32_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+      acc += __ldg(a + ((uint64_t)b * C + c) * HW + i);
+      i += blockDim.x;
+      if (i >= HW) { i -= HW; ++b; }
+    }
+  } else {
+    for (uint32_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+      const uint32_t b = j / HW;
+      acc += __ldg(a + ((uint64_t)b * C + c) * HW + (j - b * HW));
+    }
+  }
+  acc = block_sum_u64(acc);
+  if (threadIdx.x == 0) part[(uint64_t)c * gridDim.x + blockIdx.x] = acc;
+}
+
+__global__ void k_chansum_fin(const uint64_t* __restrict__ part, int C, int S, uint64_t mask, uint64_t* out) {
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (c >= C) return;
+  uint64_t acc = 0;
+  for (int s = lane; s < S; s += 32) acc += part[(int64_t)c * S + s];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) out[c] = acc & mask;
+}
+
 // K:221-238 im2col (gather form: one thread per output element).
 __global__ void k_im2col(const uint64_t* x, int B, int C, int H, int W, int s, int stride, uint64_t* out) {
   const int oh = (H - s) / stride + 1, ow = (W - s) / stride + 1;
@@ -425,6 +479,32 @@ extern "C" int pb_ring_rowsum(const uint64_t* a, int64_t rows, int64_t cols, int
   if (rows <= 0) return PB_OK;
   const uint64_t mask = (ell >= 64 || ell <= 0) ? ~0ull : ((1ull << ell) - 1);
   k_rowsum<<<(unsigned)rows, 256, 0, pb_stream_of(stream)>>>(a, rows, cols, mask, out);
+  PB_CHECK_LAUNCH();
+  return PB_OK;
+}
+
+extern "C" int pb_ring_chansum(const uint64_t* a, int32_t B, int32_t C, int64_t HW, int32_t ell, uint64_t* out,
+                               void* stream) {
+  if (B < 0 || C < 0 || HW < 0) return pb_set_error(PB_ERR_SHAPE, "negative extent");
+  if (C == 0) return PB_OK;
+  if (!out || (!a && (int64_t)B * HW > 0)) return pb_set_error(PB_ERR_ARG, "null argument");
+  if (C > 65535 || (int64_t)B * HW > 0x7fffffffLL) return pb_set_error(PB_ERR_SHAPE, "tensor too large");
+  const uint64_t mask = (ell >= 64 || ell <= 0) ? ~0ull : ((1ull << ell) - 1);
+  cudaStream_t st = pb_stream_of(stream);
+  const uint32_t total = (uint32_t)((int64_t)B * HW);
+  // splits: about four CTAs per SM over all channels, at least 2048 elements each
+  int S = (int)std::max<int64_t>(1, std::min<int64_t>((4 * 148 + C - 1) / C, (total + 2047) / 2048));
+  const uint32_t chunk = (total + S - 1) / S;
+  if (total) S = (int)((total + chunk - 1) / chunk);
+  uint64_t* part = nullptr;
+  if (cudaMallocAsync((void**)&part, (size_t)C * S * sizeof(uint64_t), st) != cudaSuccess)
+    return pb_set_error(PB_ERR_CUDA, "channel-sum scratch allocation failed");
+  if (total)
+    k_chansum_part<<<dim3((unsigned)S, (unsigned)C), 256, 0, st>>>(a, C, (uint32_t)HW, total, chunk, part);
+  else
+    cudaMemsetAsync(part, 0, (size_t)C * S * sizeof(uint64_t), st);
+  k_chansum_fin<<<(unsigned)((C + 7) / 8), 256, 0, st>>>(part, C, S, mask, out);
+  cudaFreeAsync(part, st);
   PB_CHECK_LAUNCH();
   return PB_OK;
 }

@@ -487,6 +487,23 @@ bool plane_map(CUtensorMap* tm, const int8_t* base, int rows, int Kp, int box_ro
 
 }  // namespace
 
+// K blocks per CTA for `tiles` output tiles over `kb` K blocks: one CTA per SM
+// (192 KB of shared memory), so the launch takes ceil(tiles * splits / 148)
+// waves of about kps + 2 block-times each (2: the TMEM epilogue and its
+// atomics).  Minimise that instead of doubling the splits until the grid
+// covers the GPU, which left a 12-CTA second wave at 160 CTAs.
+static int pick_kps(int tiles, int kb) {
+  const int kmax = TC_KMAX / TC_BK;
+  int best = kb < kmax ? kb : kmax;
+  int64_t best_cost = INT64_MAX;
+  for (int kps = best; kps >= 1; --kps) {
+    const int64_t splits = (kb + kps - 1) / kps;
+    const int64_t cost = (((int64_t)tiles * splits + 147) / 148) * (kps + 2);
+    if (cost < best_cost) best_cost = cost, best = kps;  // ties keep the fewer splits
+  }
+  return best;
+}
+
 // out (n x m, through d's output map) = A (n x K) . B (K x m) mod 2^ell on the
 // tensor cores.  Contractions are processed in chunks whose digit planes stay
 // under ~512 MB; within a chunk the K blocks split over gridDim.z so that the
@@ -505,9 +522,7 @@ int launch_conv_fused(const GemmMap& d, const uint64_t* A, const uint64_t* Bm, i
   const int P = swap ? m : n, Q = swap ? n : m;
   const int tiles = ((P + TC_BM - 1) / TC_BM) * ((Q + TC_BN - 1) / TC_BN);
   const int kb = (int)((K + TC_BK - 1) / TC_BK);
-  int kps = kb;
-  while (kps > 1 && (kps * TC_BK > TC_KMAX || (int64_t)tiles * ((kb + kps - 1) / kps) < 148)) kps = (kps + 1) / 2;
-  while (kps * TC_BK > TC_KMAX) kps = (kps + 1) / 2;
+  const int kps = pick_kps(tiles, kb);
   const int splits = (kb + kps - 1) / kps;
   const int atomic = splits > 1;
   const TcEpi e{d, swap};
@@ -572,9 +587,7 @@ int pb_tc_ring_gemm(const GemmMap& d, const uint64_t* A, const uint64_t* Bm, int
   const int nchunks = (int)((K + Kc - 1) / Kc);
   const int tiles = ((P + TC_BM - 1) / TC_BM) * ((Q + TC_BN - 1) / TC_BN);
   const int kb_chunk = (int)(Kc / TC_BK);
-  int kps = kb_chunk;  // K blocks per CTA
-  while (kps > 1 && (kps * TC_BK > TC_KMAX || (int64_t)tiles * ((kb_chunk + kps - 1) / kps) < 148)) kps = (kps + 1) / 2;
-  while (kps * TC_BK > TC_KMAX) kps = (kps + 1) / 2;
+  const int kps = pick_kps(tiles, kb_chunk);  // K blocks per CTA
   const int splits = (kb_chunk + kps - 1) / kps;
   const int atomic = nchunks > 1 || splits > 1;
   int8_t *dp = nullptr, *dq = nullptr;

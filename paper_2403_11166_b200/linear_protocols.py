@@ -956,10 +956,9 @@ def reveal_grad_bias_conv(sess: Session, layer: int, gy_a: ShareTensor, gy_b: Sh
     ring = sess.ring
     B, c, h, w = gy_do.shape
 
-    def chan_sum(v):
-        t = v.reshape(B, c, h * w).permute(1, 0, 2).contiguous()  # local data movement
+    def chan_sum(v):  # straight from NCHW (no permute copy)
         out = _dev.empty_u64(c)
-        _lib.call("pb_ring_rowsum", _dev.ptr(t), c, B * h * w, ring.ell, _dev.ptr(out), _dev.stream())
+        _lib.call("pb_ring_chansum", _dev.ptr(v.contiguous()), B, c, h * w, ring.ell, _dev.ptr(out), _dev.stream())
         return out
 
     sd = chan_sum(gy_do.value.values)

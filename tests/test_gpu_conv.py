@@ -82,6 +82,23 @@ def test_pool_kernels_bit_exact():
     assert np.array_equal(_np(_pool_local(_lib.POOL_REPLICATE, _dev(x), (12, 16), 59)), CO.pool_replicate(x))
 
 
+@pytest.mark.parametrize("shape", [(64, 64, 32, 32), (64, 128, 8, 8), (3, 5, 7, 9), (1, 1, 1, 1), (2, 3, 1, 1),
+                                   (5, 2, 16, 16), (0, 4, 3, 3), (7, 1, 300, 1)])
+def test_chansum_bit_exact(shape):
+    """pb_ring_chansum (conv bias gradient) vs the numpy sum over
+    (b, h, w) mod 2^59, straight from NCHW -- every split of the range."""
+    from paper_2403_11166_b200 import _dev as D
+    from paper_2403_11166_b200 import _lib
+
+    B, c, h, w = shape
+    x = np.random.default_rng(B * 7 + c).integers(0, 1 << 64, size=shape, dtype=np.uint64)
+    want = x.reshape(B, c, h * w).transpose(1, 0, 2).reshape(c, -1).sum(axis=1, dtype=np.uint64) & RING.mask
+    out = D.empty_u64(c)
+    xd = _dev(x)
+    _lib.call("pb_ring_chansum", D.ptr(xd), B, c, h * w, 59, D.ptr(out), D.stream())
+    assert np.array_equal(_np(out), want)
+
+
 def _shares(pr, mo, do, scale):
     from paper_2403_11166_b200.ring import DO, MO, RingTensor, ShareTensor
 
