@@ -37,7 +37,7 @@ extern "C" {
 
 /* 2: round 2 -- pb_encrypt_sk takes the key's Shoup row, pb_host_softmax_post a
  * denominator; new pb_mask_mac, pb_nl_op / pb_nl_words, pb_scatter_u64,
- * pb_prep_scalars, pb_shoup_rows, pb_host_publish, pb_*_ex backends. */
+ * pb_prep_scalars, pb_shoup_rows, pb_host_publish, pb_ring_chansum, pb_*_ex backends. */
 #define PB_ABI_VERSION 2
 #define PB_MAX_LIMBS 8
 
