@@ -342,36 +342,49 @@ __global__ void k_conv2d(const uint64_t* x, const uint64_t* w, int B, int Ci, in
 
 // Dealer-assisted non-linear step: reconstruct, apply, reshare with the
 // numpy-identical uniform_ring stream (so oracle and device shares agree).
+// One thread per numpy Philox block (4 raw draws): the reshare words of four
+// consecutive elements from one Philox4x64-10 evaluation (one per element
+// recomputed the block 4x -- the kernel was RNG-bound, 60 us on 4M elements).
 __global__ void k_dealer(int op, const uint64_t* in_mo, const uint64_t* in_do, uint64_t* mo, uint64_t* dov, int64_t n,
                          int k, const uint8_t* d_in, uint8_t* d_out, uint64_t seed_arg, const uint64_t* seed_dev,
                          uint64_t stream_id, uint64_t off, int ell) {
   const uint64_t seed = np_seed(seed_arg, seed_dev);
   const uint64_t m = ring_mask(ell);
   const int shift = 64 - ell;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t x = (in_mo[i] + in_do[i]) & m;
-    uint64_t y;
-    switch (op) {
-      case PB_DEALER_RELU: {
-        const bool pos = to_signed(x, ell) >= 0;
-        if (d_out) d_out[i] = pos ? 1 : 0;
-        y = pos ? x : 0ull;
-        break;
+  const uint64_t first_blk = off >> 2;
+  const int64_t nblk = (int64_t)(((off + n + 3) >> 2) - first_blk);
+  for (int64_t bi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; bi < nblk; bi += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t blk = first_blk + bi;
+    const u64x4 rv = philox4x64_10(blk + 1, 0, 0, 0, seed, stream_id);  // numpy pre-increments the counter
+#pragma unroll
+    for (int lane = 0; lane < 4; ++lane) {
+      const uint64_t raw = blk * 4 + lane;
+      if (raw < off || raw >= off + (uint64_t)n) continue;
+      const int64_t i = (int64_t)(raw - off);
+      const uint64_t x = (in_mo[i] + in_do[i]) & m;
+      uint64_t y;
+      switch (op) {
+        case PB_DEALER_RELU: {
+          const bool pos = to_signed(x, ell) >= 0;
+          if (d_out) d_out[i] = pos ? 1 : 0;
+          y = pos ? x : 0ull;
+          break;
+        }
+        case PB_DEALER_TRUNC: y = (uint64_t)(to_signed(x, ell) >> k) & m; break;
+        case PB_DEALER_SELECT: y = d_in[i] ? x : 0ull; break;
+        case PB_DEALER_RELU_TRUNC: {  // trunc_k(relu(x)): the relu reshare is never observed
+          const bool pos = to_signed(x, ell) >= 0;
+          if (d_out) d_out[i] = pos ? 1 : 0;
+          y = pos ? ((uint64_t)(to_signed(x, ell) >> k) & m) : 0ull;
+          break;
+        }
+        case PB_DEALER_TRUNC_SELECT: y = d_in[i] ? ((uint64_t)(to_signed(x, ell) >> k) & m) : 0ull; break;
+        default: y = x; break;
       }
-      case PB_DEALER_TRUNC: y = (uint64_t)(to_signed(x, ell) >> k) & m; break;
-      case PB_DEALER_SELECT: y = d_in[i] ? x : 0ull; break;
-      case PB_DEALER_RELU_TRUNC: {  // trunc_k(relu(x)): the relu reshare is never observed
-        const bool pos = to_signed(x, ell) >= 0;
-        if (d_out) d_out[i] = pos ? 1 : 0;
-        y = pos ? ((uint64_t)(to_signed(x, ell) >> k) & m) : 0ull;
-        break;
-      }
-      case PB_DEALER_TRUNC_SELECT: y = d_in[i] ? ((uint64_t)(to_signed(x, ell) >> k) & m) : 0ull; break;
-      default: y = x; break;
+      const uint64_t r = rv.v[lane] >> shift;
+      mo[i] = r;
+      dov[i] = (y - r) & m;
     }
-    const uint64_t r = philox_np_raw(seed, stream_id, off + (uint64_t)i) >> shift;
-    mo[i] = r;
-    dov[i] = (y - r) & m;
   }
 }
 
@@ -560,7 +573,7 @@ extern "C" int pb_dealer_op_out(int op, const uint64_t* in_mo, const uint64_t* i
     return pb_set_error(PB_ERR_ARG, "select needs d_in");
   if (ell < 2 || ell > 63 || k < 0 || k >= ell) return pb_set_error(PB_ERR_ARG, "bad ell / shift");
   if (n <= 0) return PB_OK;
-  k_dealer<<<RING_GRID(n)>>>(op, in_mo, in_do, mo, do_, n, k, d_in, d_out, seed, seed_dev, stream_id, raw_offset,
+  k_dealer<<<RING_GRID((n + 3) / 4 + 1)>>>(op, in_mo, in_do, mo, do_, n, k, d_in, d_out, seed, seed_dev, stream_id, raw_offset,
                              ell);
   PB_CHECK_LAUNCH();
   return PB_OK;
