@@ -120,6 +120,30 @@ __global__ void k_ring_lincomb(int sub, uint64_t* out, const uint64_t* base, con
   }
   __syncthreads();
   const int mm = ma * mb;
+  // two consecutive elements per thread with 16-byte loads when every mask
+  // row is 16-byte aligned (n even), eight rows in flight per batch
+  const int64_t np = (n & 1) ? 0 : n >> 1;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < np; x += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2* T2 = reinterpret_cast<const ulonglong2*>(T) + x;
+    uint64_t acc0 = 0, acc1 = 0;
+    int t = 0;
+    for (; t + 8 <= mm; t += 8) {
+      ulonglong2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(T2 + (int64_t)(t + u) * np);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc0 += coef[t + u] * v[u].x, acc1 += coef[t + u] * v[u].y;
+    }
+    for (; t < mm; ++t) {
+      const ulonglong2 v = __ldg(T2 + (int64_t)t * np);
+      acc0 += coef[t] * v.x, acc1 += coef[t] * v.y;
+    }
+    ulonglong2 b0 = make_ulonglong2(0ull, 0ull);
+    if (base) b0 = reinterpret_cast<const ulonglong2*>(base)[x];
+    reinterpret_cast<ulonglong2*>(out)[x] =
+        make_ulonglong2((sub ? b0.x - acc0 : b0.x + acc0) & mask, (sub ? b0.y - acc1 : b0.y + acc1) & mask);
+  }
+  if (np) return;
   for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
     uint64_t acc = 0;
     for (int t = 0; t < mm; ++t) acc += coef[t] * __ldg(T + (int64_t)t * n + x);
