@@ -147,6 +147,20 @@ __global__ void k_pool2(int op, const uint64_t* __restrict__ in, int64_t bc, int
   // op 0: in (bc, H, W) -> out (bc, H/2, W/2) window sums; op 1: in (bc, H/2, W/2) -> out (bc, H, W)
   const int h2 = H / 2, w2 = W / 2;
   const int64_t total = op == 0 ? bc * h2 * w2 : bc * H * W;
+  if (total < (1ll << 31)) {  // 32-bit index arithmetic (64-bit division dominated the kernel)
+    const uint32_t t32 = (uint32_t)total, hw2 = (uint32_t)(h2 * w2), hw = (uint32_t)(H * W);
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < t32; e += gridDim.x * blockDim.x) {
+      if (op == 0) {
+        const uint32_t q = e / hw2, r = e - q * hw2, y = r / (uint32_t)w2, x = r - y * (uint32_t)w2;
+        const uint64_t* ip = in + (uint64_t)q * hw + (2 * y) * (uint32_t)W + 2 * x;
+        out[e] = (ip[0] + ip[1] + ip[W] + ip[W + 1]) & m;
+      } else {
+        const uint32_t q = e / hw, r = e - q * hw, y = r / (uint32_t)W, x = r - y * (uint32_t)W;
+        out[e] = in[(uint64_t)q * hw2 + (y / 2) * (uint32_t)w2 + x / 2] & m;
+      }
+    }
+    return;
+  }
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     if (op == 0) {
       const int x = (int)(e % w2), y = (int)((e / w2) % h2);

@@ -377,15 +377,29 @@ __global__ void k_dealer(int op, const uint64_t* in_mo, const uint64_t* in_do, u
   const int shift = 64 - ell;
   const uint64_t first_blk = off >> 2;
   const int64_t nblk = (int64_t)(((off + n + 3) >> 2) - first_blk);
+  const bool al = (((uintptr_t)in_mo | (uintptr_t)in_do | (uintptr_t)mo | (uintptr_t)dov) & 15) == 0;
   for (int64_t bi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; bi < nblk; bi += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t blk = first_blk + bi;
     const u64x4 rv = philox4x64_10(blk + 1, 0, 0, 0, seed, stream_id);  // numpy pre-increments the counter
+    // the block's four elements as two 16-byte vectors when they are all in
+    // range and 16-byte aligned (off even), else element by element
+    const int64_t i0 = (int64_t)(blk * 4) - (int64_t)off;
+    const bool vec = al && !(off & 1) && i0 >= 0 && i0 + 4 <= n;
+    uint64_t xs[4];
+    if (vec) {
+      const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(in_mo + i0),
+                       a1 = *reinterpret_cast<const ulonglong2*>(in_mo + i0 + 2),
+                       b0 = *reinterpret_cast<const ulonglong2*>(in_do + i0),
+                       b1 = *reinterpret_cast<const ulonglong2*>(in_do + i0 + 2);
+      xs[0] = (a0.x + b0.x) & m, xs[1] = (a0.y + b0.y) & m, xs[2] = (a1.x + b1.x) & m, xs[3] = (a1.y + b1.y) & m;
+    }
+    uint64_t ro[4], rd[4];
 #pragma unroll
     for (int lane = 0; lane < 4; ++lane) {
       const uint64_t raw = blk * 4 + lane;
-      if (raw < off || raw >= off + (uint64_t)n) continue;
+      if (!vec && (raw < off || raw >= off + (uint64_t)n)) continue;
       const int64_t i = (int64_t)(raw - off);
-      const uint64_t x = (in_mo[i] + in_do[i]) & m;
+      const uint64_t x = vec ? xs[lane] : (in_mo[i] + in_do[i]) & m;
       uint64_t y;
       switch (op) {
         case PB_DEALER_RELU: {
@@ -406,8 +420,14 @@ __global__ void k_dealer(int op, const uint64_t* in_mo, const uint64_t* in_do, u
         default: y = x; break;
       }
       const uint64_t r = rv.v[lane] >> shift;
-      mo[i] = r;
-      dov[i] = (y - r) & m;
+      ro[lane] = r, rd[lane] = (y - r) & m;
+      if (!vec) mo[i] = r, dov[i] = rd[lane];
+    }
+    if (vec) {
+      *reinterpret_cast<ulonglong2*>(mo + i0) = make_ulonglong2(ro[0], ro[1]);
+      *reinterpret_cast<ulonglong2*>(mo + i0 + 2) = make_ulonglong2(ro[2], ro[3]);
+      *reinterpret_cast<ulonglong2*>(dov + i0) = make_ulonglong2(rd[0], rd[1]);
+      *reinterpret_cast<ulonglong2*>(dov + i0 + 2) = make_ulonglong2(rd[2], rd[3]);
     }
   }
 }
