@@ -524,6 +524,16 @@ __global__ void k_decode_gather(PbDev P, const uint32_t* x, int64_t nP, int U, c
                                 const int64_t* out_dst, uint64_t* share) {
   const int L = P.L;
   const int64_t total = nP * U;
+  if (total < (1ll << 31)) {  // 32-bit slot arithmetic (a 64-bit division per slot was a large share of the kernel)
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < (uint32_t)total; e += gridDim.x * blockDim.x) {
+      if (out_pos[e] < 0) continue;
+      const uint32_t p = e / (uint32_t)U, u = e - p * (uint32_t)U;
+      uint32_t d[PB_MAXL];
+      garner_dev(P, x + (uint64_t)p * L * U + u, U, d);
+      share[out_dst[e]] = scale_round_dev(P, d);
+    }
+    return;
+  }
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     if (out_pos[e] < 0) continue;
     const int64_t p = e / U;
