@@ -499,7 +499,7 @@ __device__ __forceinline__ void garner_dev(const PbDev& P, const uint32_t* x, in
       uint32_t acc = 0;
 #pragma unroll
       for (int k = 0; k < PB_MAXL; ++k)
-        if (k < i) acc = addmod(acc, mulmod(d[k], P.pmod[i][k], qi, mu), qi);
+        if (k < i) acc = addmod(acc, mul_shoup(d[k], P.pmod[i][k], P.pmod_sh[i][k], qi), qi);
       const uint32_t xv = reduce64(x[i * xs], qi, mu);
       d[i] = mul_shoup(submod(xv, acc, qi), P.pinv[i], P.pinv_sh[i], qi);
     }

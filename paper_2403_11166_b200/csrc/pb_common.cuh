@@ -28,6 +28,7 @@ struct PbDev {
   uint32_t tmod[PB_MAXL];                      // t mod q_i (centered lift)
   uint32_t pinv[PB_MAXL], pinv_sh[PB_MAXL];    // Garner (q_0..q_{i-1})^-1 mod q_i
   uint32_t pmod[PB_MAXL][PB_MAXL];             // pmod[i][k] = (q_0..q_{k-1}) mod q_i
+  uint32_t pmod_sh[PB_MAXL][PB_MAXL];          // their Shoup companions (Garner's inner products)
   uint64_t sc_int[PB_MAXL];                    // floor(t P_{i-1} / Q) mod 2^64
   double sc_frac[PB_MAXL];                     // frac(t P_{i-1} / Q)
   const uint2* tw_fwd;                         // [L][N] {psi^brv(i), shoup}

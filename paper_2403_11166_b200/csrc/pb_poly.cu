@@ -113,6 +113,7 @@ extern "C" int pb_ctx_create(const pb_params* p, pb_ctx** out) {
     uint64_t prod = 1;
     for (int k = 0; k < PB_MAX_LIMBS; ++k) {
       d.pmod[i][k] = (uint32_t)prod;
+      d.pmod_sh[i][k] = h_shoup(d.pmod[i][k], q);
       if (k < L) prod = h_mulmod(prod, p->q[k] % q, q);
     }
     d.sc_int[i] = p->scale_int[i];
@@ -580,7 +581,7 @@ __device__ __forceinline__ void garner(const PbDev& P, const uint32_t* x, int64_
       uint32_t acc = 0;
 #pragma unroll
       for (int k = 0; k < PB_MAXL; ++k)
-        if (k < i) acc = addmod(acc, mulmod(d[k], P.pmod[i][k], qi, mu), qi);
+        if (k < i) acc = addmod(acc, mul_shoup(d[k], P.pmod[i][k], P.pmod_sh[i][k], qi), qi);
       const uint32_t xv = reduce64(x[i * xs], qi, mu);
       d[i] = mul_shoup(submod(xv, acc, qi), P.pinv[i], P.pinv_sh[i], qi);
     }
