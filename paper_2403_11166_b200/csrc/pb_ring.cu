@@ -121,8 +121,9 @@ __global__ void k_ring_lincomb(int sub, uint64_t* out, const uint64_t* base, con
   __syncthreads();
   const int mm = ma * mb;
   // two consecutive elements per thread with 16-byte loads when every mask
-  // row is 16-byte aligned (n even), eight rows in flight per batch
-  const int64_t np = (n & 1) ? 0 : n >> 1;
+  // row is 16-byte aligned (n even, aligned bases), eight rows in flight per batch
+  const bool al = (((uintptr_t)T | (uintptr_t)out | (uintptr_t)base) & 15) == 0;
+  const int64_t np = ((n & 1) || !al) ? 0 : n >> 1;
   for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < np; x += (int64_t)gridDim.x * blockDim.x) {
     const ulonglong2* T2 = reinterpret_cast<const ulonglong2*>(T) + x;
     uint64_t acc0 = 0, acc1 = 0;

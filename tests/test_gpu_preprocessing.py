@@ -89,3 +89,32 @@ def test_prep_step_matches_reference_engine(env, name, B, m):
     census = sess.channel.census
     assert not any(t in census for t in (0x10, 0x11, 0x20, 0x21, 0x40, 0x41)), census  # no ciphertext frames online
     assert 0x42 in census and 0x43 in census
+
+
+@pytest.mark.parametrize("n,ma,mb,shift,sub", [(4096, 8, 8, 0, 1), (4097, 8, 8, 0, 0), (1000, 3, 5, 1, 1),
+                                                (2, 8, 1, 0, 0), (513, 1, 1, 1, 0), (64, 16, 16, 0, 1)])
+def test_ring_lincomb_bit_exact(n, ma, mb, shift, sub):
+    """pb_ring_lincomb (Alg. 3 steps 7-10 mask combination) vs numpy, including
+    odd lengths and 8-byte-offset views (the scalar path) beside the 16-byte path."""
+    import torch
+
+    from paper_2403_11166_b200 import _dev as D
+    from paper_2403_11166_b200 import _lib
+
+    rng = np.random.default_rng(n + ma * 31 + mb)
+    T = rng.integers(0, 1 << 64, size=(ma * mb, n), dtype=np.uint64)
+    a = rng.integers(0, 1 << 59, size=ma, dtype=np.uint64)
+    b = rng.integers(0, 1 << 59, size=mb, dtype=np.uint64)
+    base = rng.integers(0, 1 << 59, size=n, dtype=np.uint64)
+    coef = (a[:, None] * b[None, :]).reshape(-1)
+    acc = (coef[:, None] * T).sum(axis=0, dtype=np.uint64)
+    want = ((base - acc) if sub else (base + acc)) & RING.mask
+    td = D.u64_to_device(T)
+    bd = torch.cat([torch.zeros(shift, dtype=torch.int64, device="cuda"), D.u64_to_device(base)])[shift:]
+    out_buf = torch.zeros(n + shift, dtype=torch.int64, device="cuda")
+    out = out_buf[shift:]
+    ad, bv = D.u64_to_device(a), D.u64_to_device(b)  # kept alive until the kernel has run
+    _lib.call("pb_ring_lincomb", sub, D.ptr(out), D.ptr(bd), D.ptr(ad), ma, D.ptr(bv), mb, D.ptr(td), n, 59,
+              D.stream())
+    torch.cuda.synchronize()
+    assert np.array_equal(D.to_numpy_u64(out), want)
