@@ -567,7 +567,9 @@ int pb_tc_ring_gemm(const GemmMap& d, const uint64_t* A, const uint64_t* Bm, int
   // fused implicit GEMM (digits built in shared memory by the producer warps,
   // no planes in HBM); above, the gathers of eight producer warps cannot keep
   // the tensor core fed and the plane kernels win (CIFAR conv2 0.18 vs 0.19 ms,
-  // conv1 0.10 vs 0.08 ms; profiles/r02_ring_gemm_backends*.jsonl)
+  // conv1 0.10 vs 0.08 ms; profiles/r02_ring_gemm_backends*.jsonl; re-measured
+  // with pick_kps: conv2 fwd / dX / dW planes 0.15 / 0.15 / 0.19 ms, fused
+  // 0.16 / 0.23 / 0.21, CIFAR step 8.2 vs 8.4 ms)
   if (d.kind <= PB_CONV_GRADW && (d.s == 1 || d.s == 3 || d.s == 5) && (double)n * m * (double)K < 536870912.0) {
     switch (d.kind) {
       case PB_CONV_FWD: return conv_fused<PB_CONV_FWD>(d, A, Bm, n, K, m, mask, out, st);
